@@ -1,0 +1,160 @@
+/*
+ * knnm.h -- C-ABI of libknnm.so, the B200 (sm_100a) engine for the
+ * cross-subset NN-Descent local join behind S-Merge / J-Merge
+ * ("On the Merge of k-NN Graph", arXiv 1908.00814).
+ *
+ * The reference (`knnmerge`, pkg/src/knnmerge/) has no FFI: its operator
+ * layer is a set of numba functions on flat numpy arrays, called as
+ * `_k.<name>(...)` from construct.py / merge.py.  Each entry point below
+ * names the reference call(s) it replaces (file:line, relative to
+ * pkg/src/knnmerge/).  Python binds this header with ctypes
+ * (paper_1908_00814_b200/_lib.py); INTEGRATION.md shows the binding.
+ *
+ * Conventions
+ *   - Plain host pointers and sizes only; the library owns all device
+ *     memory and copies host<->device itself (stream-ordered on the
+ *     context's private CUDA stream).
+ *   - Array layout is the reference's (_kernels.py:1-15): ids int32 (n,k)
+ *     padded -1, dists float64 (n,k) padded +inf, flags uint8 (n,k),
+ *     sizes int32 (n).  Row r of the engine state is local id r, i.e. the
+ *     r-th entry of the ascending union of member ids.
+ *   - Every function returns KNNM_OK (0) or a negative error code; the
+ *     message is available from knnm_last_error() (thread-local).  Input
+ *     validation that the reference performs in Python (ValueError) stays
+ *     in the Python host layer; these calls return KNNM_ERR_ARG for
+ *     contract breaches they can detect.
+ *   - A context is not re-entrant; one context per device per thread.
+ *   - Arithmetic: distances are bit-identical to the reference's
+ *     dense_dist (fp64 accumulation of fp32 inputs, sequential, no FMA),
+ *     and list updates replay the reference's sequential per-row insertion
+ *     order, so results are bit-exact with the reference.
+ */
+#ifndef KNNM_H
+#define KNNM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KNNM_OK 0
+#define KNNM_ERR_CUDA -1   /* CUDA runtime / launch failure            */
+#define KNNM_ERR_ARG -2    /* invalid argument                          */
+#define KNNM_ERR_STATE -3  /* call out of order (e.g. round before begin) */
+#define KNNM_ERR_NOMEM -4  /* device allocation failed                  */
+#define KNNM_ERR_LIMIT -5  /* input exceeds a supported bound            */
+
+/* Metric tags (_kernels.py:24-27; core.py:28-51 Metric). */
+#define KNNM_L1 0
+#define KNNM_L2 1
+#define KNNM_COSINE 2
+
+/* Pair-admissibility modes (_kernels.py:29-31). */
+#define KNNM_MODE_ALL 0
+#define KNNM_MODE_CROSS 1
+#define KNNM_MODE_CROSS_OR_S2 2
+
+typedef struct knnm_ctx knnm_ctx;
+
+/* Per-context counters and timings (cumulative since create / reset). */
+typedef struct knnm_stats {
+    double join_ms;        /* local-join kernel time (CUDA events)        */
+    double reverse_ms;     /* reverse CSR build                           */
+    double assemble_ms;    /* neighbourhood assembly (+pair counting)     */
+    double update_ms;      /* candidate bucketing + sequential insertion  */
+    double other_ms;       /* init, phi, export, merge-rear               */
+    int64_t join_launches; /* local-join kernel launches                  */
+    int64_t pairs;         /* admissible pairs evaluated (= distance evals) */
+    int64_t init_evals;    /* init-path distance evaluations              */
+    int64_t members;       /* sum over active hoods of |M_u| (members in >=1 pair) */
+    int64_t candidates;    /* directed updates surviving the prefilter     */
+    int64_t accepted;      /* accepted list insertions                    */
+    int64_t rounds;        /* rounds run                                  */
+    int64_t exact_evals;   /* pairs re-evaluated in fp64 after fp32 screen */
+} knnm_stats;
+
+const char *knnm_last_error(void);
+int knnm_version(void);
+
+/* Create / destroy an engine bound to CUDA device `device`. */
+int knnm_create(int device, knnm_ctx **out);
+int knnm_destroy(knnm_ctx *ctx);
+
+/* Upload the dense dataset (Dataset.vectors, core.py:96-104): float32
+ * (n_all, d) row-major host array; metric = KNNM_L1/L2/COSINE.  The device
+ * copy is kept across merges (tree merges and H-Merge reuse it). */
+int knnm_set_dataset(knnm_ctx *ctx, const float *vectors, int64_t n_all,
+                     int32_t d, int32_t metric);
+
+/* Begin a merge or build over `n` local rows.  Replaces
+ * `Dataset.take(union_gids)` (core.py:148-166; merge.py:217-219, 297-301),
+ * the label setup (merge.py:222-223, 304-305) and the list allocation
+ * (merge.py:227-230, 308-311).  union_gids: ascending int64 (n) global ids;
+ * labels: int8 (n); k = list capacity. Lists start empty. */
+int knnm_begin(knnm_ctx *ctx, const int64_t *union_gids, int64_t n,
+               const int8_t *labels, int32_t k);
+
+/* Load one input subgraph.  Replaces split (graph.py:202-229) +
+ * _localize_rows (merge.py:129-143) + the rear-list assembly
+ * (merge.py:249-256 / 333-335).  rows: int32 (m) local rows of the graph's
+ * members; g_ids int32 (m, gk) GLOBAL neighbour ids, g_dists float64 (m,gk),
+ * g_sizes int32 (m).  Entries [0,k1) become the list head (flags old);
+ * entries [k1,size) are kept as the rear list for knnm_export. */
+int knnm_load_graph(knnm_ctx *ctx, const int32_t *rows, int64_t m,
+                    const int32_t *g_ids, const double *g_dists,
+                    const int32_t *g_sizes, int32_t gk, int32_t k1);
+
+/* Directed inserts in the given order.  Replaces _eval_pairs +
+ * apply_updates_directed (construct.py:86-108; _kernels.py:208-214) as used
+ * by _append_random (merge.py:166-176), the raw-row init (merge.py:318-325)
+ * and the random init of nn_descent (construct.py:255-259).  rows/nids:
+ * int32 (m) local ids.  *accepted receives the accepted count.
+ * If capture is on, the m distances are kept for knnm_capture_fetch. */
+int knnm_insert_directed(knnm_ctx *ctx, const int32_t *rows,
+                         const int32_t *nids, int64_t m, int64_t *accepted);
+
+/* One local-join round.  Replaces one iteration of _descent_rounds
+ * (construct.py:136-164): reverse_csr, assemble_neighborhoods (rev_cap),
+ * flag clear, count_pairs/fill_pairs, pair_dists_dense and
+ * apply_updates_grouped (_kernels.py:262-437, 113-119, 217-254).
+ * *pairs = admissible pairs (RoundStats.pairs), *accepted = accepted
+ * inserts (RoundStats.updates). */
+int knnm_round(knnm_ctx *ctx, int32_t mode, int32_t rev_cap,
+               uint64_t round_seed, int64_t *pairs, int64_t *accepted);
+
+/* phi over the current lists (construct.py:79-83), with numpy's pairwise
+ * summation order, so the value is bit-identical to the reference. */
+int knnm_phi(knnm_ctx *ctx, double *out);
+
+/* Export the lists in global id space (construct.py:212-223), merging the
+ * loaded rear lists back in when merge_rear != 0 (graph.py:259-280,
+ * _kernels.py:529-563).  Outputs: ids int32 (n,k), dists float64 (n,k),
+ * sizes int32 (n); flags are all False, as in the reference. */
+int knnm_export(knnm_ctx *ctx, int32_t merge_rear, int32_t *out_ids,
+                double *out_dists, int32_t *out_sizes);
+
+/* Download the raw local-id state (for per-iteration parity checks). */
+int knnm_get_state(knnm_ctx *ctx, int32_t *ids, double *dists,
+                   uint8_t *flags, int32_t *sizes);
+
+/* Capture mode for the reference's on_pair hook (construct.py:102-108):
+ * when on, every distance evaluation of the next insert_directed / round
+ * call is recorded in reference order (local ids pa, pb and value pd). */
+int knnm_set_capture(knnm_ctx *ctx, int32_t on);
+int knnm_capture_count(knnm_ctx *ctx, int64_t *count);
+int knnm_capture_fetch(knnm_ctx *ctx, int32_t *pa, int32_t *pb, double *pd,
+                       int64_t count);
+
+/* Timing / counters. profiling=1 records CUDA events around every phase. */
+int knnm_set_profiling(knnm_ctx *ctx, int32_t on);
+int knnm_get_stats(knnm_ctx *ctx, knnm_stats *out);
+int knnm_reset_stats(knnm_ctx *ctx);
+
+/* Block until all work on the context stream is done. */
+int knnm_sync(knnm_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KNNM_H */

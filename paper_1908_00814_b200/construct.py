@@ -1,0 +1,194 @@
+"""Round engine and NN-Descent build on the B200 engine.
+
+Host mirror of the reference's construct.py (pkg/src/knnmerge/construct.py).
+The per-round work of ``_descent_rounds`` (construct.py:111-179) runs in one
+``knnm_round`` call on the device; only the PCG64 round-seed draw, the
+distance counter, the report and the convergence test stay on the host,
+exactly where the reference keeps them.
+"""
+
+from __future__ import annotations
+
+import logging
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .core import Dataset, DistanceCounter, Metric, sample_distinct
+from .engine import get_engine
+from .graph import KnnGraph
+
+logger = logging.getLogger(__name__)
+
+MODE_ALL = 0          # _kernels.py:29
+MODE_CROSS = 1        # _kernels.py:30
+MODE_CROSS_OR_S2 = 2  # _kernels.py:31
+
+
+@dataclass
+class DescentParams:
+    """Knobs for NN-Descent style iteration (construct.py:31-50)."""
+
+    k: int
+    max_iters: int = 50
+    min_update_fraction: float = 0.001
+
+    def __post_init__(self) -> None:
+        if self.k < 2:
+            raise ValueError("k must be >= 2")
+        if not 0.0 <= self.min_update_fraction < 1.0:
+            raise ValueError("min_update_fraction must be in [0, 1)")
+        if self.max_iters < 1:
+            raise ValueError("max_iters must be >= 1")
+
+
+@dataclass
+class RoundStats:
+    iteration: int
+    pairs: int
+    updates: int
+    phi: float
+    distance_count: int
+
+
+@dataclass
+class BuildReport:
+    """Per-round trace of a build or merge run (construct.py:62-76)."""
+
+    phi_initial: float = 0.0
+    rounds: list = field(default_factory=list)
+    converged: bool = False
+
+    @property
+    def iterations(self) -> int:
+        return len(self.rounds)
+
+    @property
+    def final_phi(self) -> float:
+        return self.rounds[-1].phi if self.rounds else self.phi_initial
+
+
+def _emit_captured(engine, on_pair, gids) -> None:
+    """Replay the captured evaluations through the on_pair hook in reference
+    order (construct.py:102-108)."""
+    if on_pair is None:
+        return
+    pa, pb, pd = engine.fetch_captured()
+    ga = gids[pa]
+    gb = gids[pb]
+    for a, b, d in zip(ga.tolist(), gb.tolist(), pd.tolist()):
+        on_pair(int(a), int(b), float(d))
+
+
+def _insert_directed(engine, rows, nids, counter, on_pair, gids) -> int:
+    """_eval_pairs + apply_updates_directed (construct.py:86-108,
+    _kernels.py:208-214) in one device call."""
+    m = int(np.asarray(rows).shape[0])
+    if m == 0:
+        return 0
+    acc = engine.insert_directed(rows, nids)
+    counter.add(m)
+    _emit_captured(engine, on_pair, gids)
+    return acc
+
+
+def _descent_rounds(engine, n: int, mode: int, k: int, params, rng, counter, on_pair, gids,
+                    report: BuildReport | None, rev_cap: int | None = None) -> None:
+    """construct.py:111-179 on the device engine (state already loaded)."""
+    threshold = params.min_update_fraction * n * k
+    rev_cap = k if rev_cap is None else int(rev_cap)
+    for it in range(1, params.max_iters + 1):
+        round_seed = int(rng.integers(0, 2**63 - 1))
+        pairs, accepted = engine.round(mode, rev_cap, round_seed)
+        if pairs > 0:
+            counter.add(pairs)
+        _emit_captured(engine, on_pair, gids)
+        cur_phi = engine.phi()
+        logger.info("iter=%d pairs=%d updates=%d phi=%.6f dists=%d",
+                    it, pairs, accepted, cur_phi, counter.count)
+        if report is not None:
+            report.rounds.append(RoundStats(it, pairs, accepted, cur_phi, counter.count))
+        if accepted <= threshold:
+            if report is not None:
+                report.converged = True
+            return
+    if report is not None:
+        report.converged = False
+
+
+def _resolve_members(dataset: Dataset, member_ids) -> np.ndarray:
+    if member_ids is None:
+        return np.arange(dataset.n, dtype=np.int64)
+    gids = np.unique(np.asarray(member_ids, dtype=np.int64))
+    if gids.size and (gids[0] < 0 or gids[-1] >= dataset.n):
+        raise ValueError("member ids outside the dataset")
+    return gids
+
+
+def _random_lists(rng, n: int, k: int) -> np.ndarray:
+    """n rows of k distinct local ids, self excluded (construct.py:192-209;
+    the same PCG64 calls, so the same draws as the reference)."""
+    if 4 * k * k >= n:
+        out = np.empty((n, k), dtype=np.int64)
+        for u in range(n):
+            out[u] = sample_distinct(rng, n, k, exclude=u)
+        return out
+    cand = rng.integers(0, n - 1, size=(n, k))
+    cand += cand >= np.arange(n)[:, None]
+    while True:
+        srt = np.sort(cand, axis=1)
+        bad = (np.diff(srt, axis=1) == 0).any(axis=1)
+        if not bad.any():
+            return cand
+        rows = np.nonzero(bad)[0]
+        redraw = rng.integers(0, n - 1, size=(rows.size, k))
+        redraw += redraw >= rows[:, None]
+        cand[rows] = redraw
+
+
+def _graph_from(gids, k, metric, ids, dists, sizes) -> KnnGraph:
+    g = KnnGraph(gids, k, metric)
+    g.ids = ids
+    g.dists = dists
+    g.sizes = sizes
+    return g
+
+
+def _capture(engine, on_pair) -> None:
+    engine.set_capture(on_pair is not None)
+
+
+def nn_descent(dataset: Dataset, metric: Metric, params: DescentParams, seed: int,
+               member_ids=None, counter: DistanceCounter | None = None, on_pair=None,
+               return_report: bool = False, device: int | None = None):
+    """NN-Descent from a random initial graph (construct.py:226-270)."""
+    metric = Metric(metric)
+    metric.check_kind(dataset.kind)
+    gids = _resolve_members(dataset, member_ids)
+    n = gids.shape[0]
+    k = params.k
+    if n < 2:
+        raise ValueError("need at least 2 members")
+    if k >= n:
+        raise ValueError(f"k={k} must be below the member count {n}")
+    if counter is None:
+        counter = DistanceCounter()
+    rng = np.random.default_rng(seed)
+    eng = get_engine(device)
+    eng.set_dataset(dataset.vectors, int(metric))
+    eng.begin(gids, np.zeros(n, dtype=np.int8), k)
+    _capture(eng, on_pair)
+    try:
+        cand = _random_lists(rng, n, k)
+        rows = np.repeat(np.arange(n, dtype=np.int32), k)
+        nids = cand.ravel().astype(np.int32)
+        _insert_directed(eng, rows, nids, counter, on_pair, gids)
+        report = BuildReport(phi_initial=eng.phi())
+        _descent_rounds(eng, n, MODE_ALL, k, params, rng, counter, on_pair, gids, report)
+        ids, dists, sizes = eng.export(merge_rear=False)
+    finally:
+        eng.set_capture(False)
+    graph = _graph_from(gids, k, metric, ids, dists, sizes)
+    if return_report:
+        return graph, report
+    return graph

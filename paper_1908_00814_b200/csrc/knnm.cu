@@ -1,0 +1,912 @@
+// knnm.cu -- libknnm.so: context, memory plan and the C-ABI (include/knnm.h)
+// for the B200 S-Merge / J-Merge round engine.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <functional>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/knnm.h"
+#include "knnm_kernels.cuh"
+
+using namespace knnm;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return code;
+}
+
+#define CK(x)                                                                             \
+    do {                                                                                  \
+        cudaError_t e_ = (x);                                                             \
+        if (e_ != cudaSuccess)                                                            \
+            return fail(e_ == cudaErrorMemoryAllocation ? KNNM_ERR_NOMEM : KNNM_ERR_CUDA, \
+                        "%s:%d %s: %s", __FILE__, __LINE__, #x, cudaGetErrorString(e_));  \
+    } while (0)
+#define CKL() CK(cudaGetLastError())
+#define TRY(...)                \
+    do {                        \
+        int r_ = (__VA_ARGS__); \
+        if (r_ != KNNM_OK) return r_; \
+    } while (0)
+
+struct DBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+    template <typename T>
+    T *as() const { return reinterpret_cast<T *>(p); }
+};
+
+int ensure(DBuf &b, size_t bytes) {
+    if (bytes == 0) bytes = 16;
+    if (b.bytes >= bytes) return KNNM_OK;
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+    CK(cudaMalloc(&b.p, bytes));
+    b.bytes = bytes;
+    return KNNM_OK;
+}
+
+void release(DBuf &b) {
+    if (b.p) cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+}
+
+int bits_for(uint64_t maxval) {  // bits to represent values in [0, maxval]
+    int b = 1;
+    while (b < 64 && (maxval >> b) != 0) b++;
+    return b;
+}
+
+enum Phase { PH_JOIN = 0, PH_REVERSE, PH_ASSEMBLE, PH_UPDATE, PH_OTHER, PH_NUM };
+
+struct PhiTree {
+    int64_t N = -1;
+    std::vector<int64_t> leaf_lo;
+    std::vector<int32_t> leaf_len;
+    std::vector<int32_t> left, right, level_start;
+};
+
+}  // namespace
+
+struct knnm_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t st = nullptr;
+    // dataset
+    DBuf vec;
+    int64_t n_all = 0;
+    int d = 0, dp = 0, metric = 1;
+    bool have_data = false;
+    // current merge
+    DBuf sub, ugid, labels;
+    const float *subp = nullptr;
+    int64_t n = 0;
+    int k = 0;
+    bool begun = false;
+    DBuf ids, dists, flags, sizes;
+    DBuf tail_ids, tail_d, tail_s;
+    int tk = 0;
+    bool have_tail = false;
+    // round scratch
+    DBuf indeg, roff, rev, heavy, giant, gscratch32, nbh, nlen, hpairs, poff, worst0, active;
+    DBuf tcnt, toff, candA, candB, heavy_rows, gscratch64;
+    DBuf scan_tmp[4], scan_off[4];
+    DBuf counters;
+    unsigned long long cap = 0;  // candidate record capacity
+    size_t cand_budget_bytes = (size_t)16 << 30;
+    // staging
+    DBuf stage[4];
+    unsigned long long *hcnt = nullptr;  // pinned mirror of counters
+    // outputs
+    DBuf out_ids, out_d, out_s;
+    // phi
+    PhiTree phi;
+    DBuf phi_leaf_lo, phi_leaf_len, phi_left, phi_right, phi_level, phi_leaves, phi_inner;
+    // capture
+    bool capture = false;
+    std::vector<int32_t> cap_pa, cap_pb;
+    std::vector<double> cap_pd;
+    // profiling
+    bool profiling = false;
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::vector<cudaEvent_t> ev_pool;
+    double phase_ms[PH_NUM] = {0, 0, 0, 0, 0};
+    knnm_stats stats{};
+};
+
+namespace {
+
+int ev_get(knnm_ctx *c, cudaEvent_t *e) {
+    if (!c->ev_pool.empty()) {
+        *e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return KNNM_OK;
+    }
+    CK(cudaEventCreate(e));
+    return KNNM_OK;
+}
+
+struct PhaseTimer {
+    knnm_ctx *c;
+    int ph;
+    cudaEvent_t a = nullptr, b = nullptr;
+    PhaseTimer(knnm_ctx *c_, int ph_) : c(c_), ph(ph_) {
+        if (c->profiling && ev_get(c, &a) == KNNM_OK) cudaEventRecord(a, c->st);
+    }
+    ~PhaseTimer() {
+        if (a && ev_get(c, &b) == KNNM_OK) {
+            cudaEventRecord(b, c->st);
+            c->pending.push_back({ph, {a, b}});
+        }
+    }
+};
+
+int resolve_timers(knnm_ctx *c) {
+    for (auto &p : c->pending) {
+        float ms = 0;
+        CK(cudaEventSynchronize(p.second.second));
+        CK(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+        c->phase_ms[p.first] += ms;
+        c->ev_pool.push_back(p.second.first);
+        c->ev_pool.push_back(p.second.second);
+    }
+    c->pending.clear();
+    return KNNM_OK;
+}
+
+int grid_for(knnm_ctx *c, int64_t work, int threads, int per_sm = 8) {
+    int64_t g = (work + threads - 1) / threads;
+    int64_t cap = (int64_t)c->sms * per_sm;
+    if (g > cap) g = cap;
+    if (g < 1) g = 1;
+    return (int)g;
+}
+
+int sync_counters(knnm_ctx *c) {
+    CK(cudaMemcpyAsync(c->hcnt, c->counters.p, sizeof(unsigned long long) * C_NUM,
+                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return KNNM_OK;
+}
+
+// Exclusive scan of n values into out[0..n] (out[n] = total).  Tile sums
+// recurse through preallocated per-level buffers (no allocation per call
+// once warmed up).
+template <typename TI, typename TO>
+int scan(knnm_ctx *c, const TI *in, TO *out, int64_t n, int level = 0) {
+    int64_t ntiles = (n + SCAN_TILE - 1) / SCAN_TILE;
+    if (ntiles < 1) ntiles = 1;
+    if (level >= 4) return fail(KNNM_ERR_LIMIT, "scan too deep");
+    TRY(ensure(c->scan_tmp[level], sizeof(TO) * (size_t)(ntiles + 1)));
+    TRY(ensure(c->scan_off[level], sizeof(TO) * (size_t)(ntiles + 1)));
+    TO *tiles = c->scan_tmp[level].as<TO>();
+    TO *toffs = c->scan_off[level].as<TO>();
+    k_scan_tiles<TI, TO><<<(unsigned)ntiles, SCAN_THREADS, 0, c->st>>>(in, out, n, tiles);
+    CKL();
+    if (ntiles == 1) {
+        CK(cudaMemcpyAsync(out + n, tiles, sizeof(TO), cudaMemcpyDeviceToDevice, c->st));
+        return KNNM_OK;
+    }
+    TRY((scan<TO, TO>(c, tiles, toffs, ntiles, level + 1)));
+    k_scan_add<TO><<<(unsigned)((n + 255) / 256), 256, 0, c->st>>>(out, n, toffs);
+    CKL();
+    k_scan_total<TO><<<1, 1, 0, c->st>>>(out, n, toffs, ntiles);
+    CKL();
+    return KNNM_OK;
+}
+
+// Bucketing + sequential per-row application of the C_CAND candidate
+// records currently in candA.  key_max = largest key value used.
+int run_updates(knnm_ctx *c, uint64_t key_max) {
+    int keybits = bits_for(key_max);
+    int ib = 64 - keybits;
+    if (ib < 15) return fail(KNNM_ERR_LIMIT, "reference-order keys need %d bits", keybits);
+    int64_t n = c->n;
+    TRY(scan<uint32_t, uint32_t>(c, c->tcnt.as<uint32_t>(), c->toff.as<uint32_t>(), n));
+    unsigned long long *cnt = c->counters.as<unsigned long long>();
+    // scatter (count read on device through a pinned-free path: copy scalar first)
+    CK(cudaMemcpyAsync(c->hcnt, c->counters.p, sizeof(unsigned long long) * C_NUM,
+                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    unsigned long long ncand = c->hcnt[C_CAND];
+    if (c->hcnt[C_OVERFLOW]) return fail(KNNM_ERR_LIMIT, "candidate buffer overflow");
+    c->stats.candidates += (int64_t)ncand;
+    if (ncand == 0) return KNNM_OK;
+    k_scatter<<<grid_for(c, (int64_t)ncand, 256), 256, 0, c->st>>>(
+        c->candA.as<CandA>(), ncand, c->toff.as<uint32_t>(), c->tcnt.as<uint32_t>(),
+        c->candB.as<CandB>());
+    CKL();
+    CK(cudaMemsetAsync(cnt + C_HEAVY_APPLY, 0, sizeof(unsigned long long) * 2, c->st));
+    int E = (c->k + 31) / 32;
+    int blocks = grid_for(c, n * 32, APPLY_WARPS * 32, 16);
+    size_t hsm = sizeof(uint64_t) * BLOCK_SORT_MAX;
+    if (E == 1) {
+        k_apply<1><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
+            n, c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(), ib, c->ids.as<int32_t>(),
+            c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
+            c->heavy_rows.as<int32_t>(), cnt);
+        CKL();
+        k_apply_heavy<1><<<c->sms, 256, hsm, c->st>>>(
+            c->heavy_rows.as<int32_t>(), c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(), ib,
+            c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
+            c->sizes.as<int32_t>(), cnt, nullptr, BLOCK_SORT_MAX, c->giant.as<int32_t>());
+        CKL();
+    } else {
+        k_apply<2><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
+            n, c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(), ib, c->ids.as<int32_t>(),
+            c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
+            c->heavy_rows.as<int32_t>(), cnt);
+        CKL();
+        k_apply_heavy<2><<<c->sms, 256, hsm, c->st>>>(
+            c->heavy_rows.as<int32_t>(), c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(), ib,
+            c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
+            c->sizes.as<int32_t>(), cnt, nullptr, BLOCK_SORT_MAX, c->giant.as<int32_t>());
+        CKL();
+    }
+    TRY(sync_counters(c));
+    if (c->hcnt[C_GIANT_APPLY]) {
+        unsigned long long maxc = c->hcnt[C_MAXC];
+        if (bits_for(maxc) > ib) return fail(KNNM_ERR_LIMIT, "row with %llu candidates", maxc);
+        TRY(ensure(c->gscratch64, sizeof(uint64_t) * next_pow2((uint32_t)maxc)));
+        if (E == 1)
+            k_apply_heavy<1><<<1, 1024, 0, c->st>>>(
+                c->heavy_rows.as<int32_t>(), c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(),
+                ib, c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
+                c->sizes.as<int32_t>(), cnt, c->gscratch64.as<uint64_t>(), BLOCK_SORT_MAX,
+                c->giant.as<int32_t>());
+        else
+            k_apply_heavy<2><<<1, 1024, 0, c->st>>>(
+                c->heavy_rows.as<int32_t>(), c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(),
+                ib, c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
+                c->sizes.as<int32_t>(), cnt, c->gscratch64.as<uint64_t>(), BLOCK_SORT_MAX,
+                c->giant.as<int32_t>());
+        CKL();
+    }
+    return KNNM_OK;
+}
+
+int ensure_candidates(knnm_ctx *c, unsigned long long want) {
+    unsigned long long per = sizeof(CandA) + sizeof(CandB);
+    unsigned long long maxrec = c->cand_budget_bytes / per;
+    if (want > maxrec) want = maxrec;
+    if (want < (1ull << 16)) want = 1ull << 16;
+    if (c->cap >= want) return KNNM_OK;
+    TRY(ensure(c->candA, sizeof(CandA) * want));
+    TRY(ensure(c->candB, sizeof(CandB) * want));
+    c->cap = want;
+    return KNNM_OK;
+}
+
+void build_phi_tree(PhiTree &t, int64_t N) {
+    t.N = N;
+    t.leaf_lo.clear();
+    t.leaf_len.clear();
+    struct Node { int32_t l, r, h; };
+    std::vector<Node> nodes;
+    struct Res { int32_t ref, h; };
+    // iterative-safe recursion (depth ~ log2(N/64))
+    std::function<Res(int64_t, int64_t)> rec = [&](int64_t lo, int64_t n) -> Res {
+        if (n <= 128) {
+            t.leaf_lo.push_back(lo);
+            t.leaf_len.push_back((int32_t)n);
+            return Res{-(int32_t)t.leaf_lo.size(), 0};
+        }
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        Res a = rec(lo, n2);
+        Res b = rec(lo + n2, n - n2);
+        int32_t h = std::max(a.h, b.h) + 1;
+        nodes.push_back(Node{a.ref, b.ref, h});
+        return Res{(int32_t)nodes.size() - 1, h};
+    };
+    rec(0, N);
+    int32_t H = 0;
+    for (auto &nd : nodes) H = std::max(H, nd.h);
+    std::vector<int32_t> order(nodes.size());
+    for (size_t i = 0; i < nodes.size(); i++) order[i] = (int32_t)i;
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int32_t a, int32_t b) { return nodes[a].h < nodes[b].h; });
+    std::vector<int32_t> pos(nodes.size());
+    for (size_t i = 0; i < order.size(); i++) pos[order[i]] = (int32_t)i;
+    t.left.resize(nodes.size());
+    t.right.resize(nodes.size());
+    for (size_t i = 0; i < order.size(); i++) {
+        const Node &nd = nodes[order[i]];
+        t.left[i] = nd.l >= 0 ? pos[nd.l] : nd.l;
+        t.right[i] = nd.r >= 0 ? pos[nd.r] : nd.r;
+    }
+    t.level_start.assign(H + 1, 0);
+    // level h (1..H) occupies [level_start[h-1], level_start[h])
+    std::vector<int32_t> cnt(H + 1, 0);
+    for (auto &nd : nodes) cnt[nd.h]++;
+    t.level_start[0] = 0;
+    for (int h = 1; h <= H; h++) t.level_start[h] = t.level_start[h - 1] + cnt[h];
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *knnm_last_error(void) { return g_err.c_str(); }
+int knnm_version(void) { return 1; }
+
+int knnm_create(int device, knnm_ctx **out) {
+    if (!out) return fail(KNNM_ERR_ARG, "null out");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(KNNM_ERR_ARG, "device %d of %d", device, ndev);
+    CK(cudaSetDevice(device));
+    knnm_ctx *c = new knnm_ctx();
+    c->device = device;
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    c->sms = prop.multiProcessorCount;
+    CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
+    CK(cudaHostAlloc((void **)&c->hcnt, sizeof(unsigned long long) * C_NUM, cudaHostAllocDefault));
+    TRY(ensure(c->counters, sizeof(unsigned long long) * C_NUM));
+    CK(cudaMemset(c->counters.p, 0, sizeof(unsigned long long) * C_NUM));
+    CK(cudaFuncSetAttribute(k_rev_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(2 * sizeof(uint32_t) * BLOCK_SORT_MAX)));
+    CK(cudaFuncSetAttribute(k_apply_heavy<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(uint64_t) * BLOCK_SORT_MAX)));
+    CK(cudaFuncSetAttribute(k_apply_heavy<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)(sizeof(uint64_t) * BLOCK_SORT_MAX)));
+    for (auto f : {k_join_exact<0>, k_join_exact<1>, k_join_exact<2>})
+        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    *out = c;
+    return KNNM_OK;
+}
+
+int knnm_destroy(knnm_ctx *c) {
+    if (!c) return KNNM_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->st);
+    DBuf *all[] = {&c->vec, &c->sub, &c->ugid, &c->labels, &c->ids, &c->dists, &c->flags,
+                   &c->sizes, &c->tail_ids, &c->tail_d, &c->tail_s, &c->indeg, &c->roff,
+                   &c->rev, &c->heavy, &c->giant, &c->gscratch32, &c->nbh, &c->nlen, &c->hpairs,
+                   &c->poff, &c->worst0, &c->active, &c->tcnt, &c->toff, &c->candA, &c->candB,
+                   &c->heavy_rows, &c->gscratch64, &c->counters, &c->out_ids, &c->out_d,
+                   &c->out_s, &c->phi_leaf_lo, &c->phi_leaf_len, &c->phi_left, &c->phi_right,
+                   &c->phi_level, &c->phi_leaves, &c->phi_inner};
+    for (DBuf *b : all) release(*b);
+    for (auto &b : c->scan_tmp) release(b);
+    for (auto &b : c->scan_off) release(b);
+    for (auto &b : c->stage) release(b);
+    for (auto &p : c->pending) {
+        cudaEventDestroy(p.second.first);
+        cudaEventDestroy(p.second.second);
+    }
+    for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->hcnt) cudaFreeHost(c->hcnt);
+    cudaStreamDestroy(c->st);
+    delete c;
+    return KNNM_OK;
+}
+
+int knnm_set_dataset(knnm_ctx *c, const float *vectors, int64_t n_all, int32_t d, int32_t metric) {
+    if (!c || (!vectors && n_all > 0)) return fail(KNNM_ERR_ARG, "null argument");
+    if (n_all < 1 || d < 1) return fail(KNNM_ERR_ARG, "empty dataset");
+    if (metric < 0 || metric > 2) return fail(KNNM_ERR_ARG, "metric tag %d not dense", metric);
+    CK(cudaSetDevice(c->device));
+    PhaseTimer pt(c, PH_OTHER);
+    int dp = (d + 3) & ~3;
+    TRY(ensure(c->vec, sizeof(float) * (size_t)n_all * dp));
+    if (dp == d) {
+        CK(cudaMemcpyAsync(c->vec.p, vectors, sizeof(float) * (size_t)n_all * d,
+                           cudaMemcpyHostToDevice, c->st));
+    } else {
+        TRY(ensure(c->stage[0], sizeof(float) * (size_t)n_all * d));
+        CK(cudaMemcpyAsync(c->stage[0].p, vectors, sizeof(float) * (size_t)n_all * d,
+                           cudaMemcpyHostToDevice, c->st));
+        k_pad_rows<<<grid_for(c, n_all * dp, 256), 256, 0, c->st>>>(
+            c->stage[0].as<float>(), d, dp, n_all, c->vec.as<float>());
+        CKL();
+    }
+    c->n_all = n_all;
+    c->d = d;
+    c->dp = dp;
+    c->metric = metric;
+    c->have_data = true;
+    c->begun = false;
+    return KNNM_OK;
+}
+
+int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *labels, int32_t k) {
+    if (!c || !union_gids || !labels) return fail(KNNM_ERR_ARG, "null argument");
+    if (!c->have_data) return fail(KNNM_ERR_STATE, "knnm_set_dataset first");
+    if (n < 1) return fail(KNNM_ERR_ARG, "empty union");
+    if (k < 1 || k > 64) return fail(KNNM_ERR_LIMIT, "k=%d outside [1, 64]", k);
+    if ((uint64_t)n * (uint64_t)k >= (1ull << 31)) return fail(KNNM_ERR_LIMIT, "n*k too large");
+    if (union_gids[0] < 0 || union_gids[n - 1] >= c->n_all)
+        return fail(KNNM_ERR_ARG, "union ids outside the dataset");
+    CK(cudaSetDevice(c->device));
+    PhaseTimer pt(c, PH_OTHER);
+    c->n = n;
+    c->k = k;
+    TRY(ensure(c->ugid, sizeof(int64_t) * n));
+    CK(cudaMemcpyAsync(c->ugid.p, union_gids, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->st));
+    bool identity = (n == c->n_all && union_gids[0] == 0 && union_gids[n - 1] == n - 1);
+    if (identity) {
+        c->subp = c->vec.as<float>();
+    } else {
+        TRY(ensure(c->sub, sizeof(float) * (size_t)n * c->dp));
+        k_gather_rows<<<grid_for(c, n * (c->dp / 4), 256), 256, 0, c->st>>>(
+            c->vec.as<float>(), c->dp, c->ugid.as<int64_t>(), n, c->sub.as<float>());
+        CKL();
+        c->subp = c->sub.as<float>();
+    }
+    TRY(ensure(c->labels, n));
+    CK(cudaMemcpyAsync(c->labels.p, labels, n, cudaMemcpyHostToDevice, c->st));
+    size_t nk = (size_t)n * k;
+    TRY(ensure(c->ids, sizeof(int32_t) * nk));
+    TRY(ensure(c->dists, sizeof(double) * nk));
+    TRY(ensure(c->flags, nk));
+    TRY(ensure(c->sizes, sizeof(int32_t) * n));
+    k_init_lists<<<grid_for(c, (int64_t)nk, 256), 256, 0, c->st>>>(
+        n, k, c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
+        c->sizes.as<int32_t>());
+    CKL();
+    // per-round scratch sized for this union
+    int W = 2 * k;
+    TRY(ensure(c->indeg, sizeof(uint32_t) * (n + 1)));
+    TRY(ensure(c->roff, sizeof(uint32_t) * (n + 1)));
+    TRY(ensure(c->rev, sizeof(uint32_t) * nk));
+    TRY(ensure(c->heavy, sizeof(int32_t) * n));
+    TRY(ensure(c->giant, sizeof(int32_t) * n));
+    TRY(ensure(c->nbh, sizeof(uint32_t) * (size_t)n * W));
+    TRY(ensure(c->nlen, sizeof(int32_t) * n));
+    TRY(ensure(c->hpairs, sizeof(uint32_t) * (n + 1)));
+    TRY(ensure(c->poff, sizeof(uint64_t) * (n + 1)));
+    TRY(ensure(c->worst0, sizeof(double) * n));
+    TRY(ensure(c->active, sizeof(int32_t) * n));
+    TRY(ensure(c->tcnt, sizeof(uint32_t) * (n + 1)));
+    TRY(ensure(c->toff, sizeof(uint32_t) * (n + 1)));
+    TRY(ensure(c->heavy_rows, sizeof(int32_t) * n));
+    CK(cudaMemsetAsync(c->tcnt.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+    CK(cudaMemsetAsync(c->indeg.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+    c->tk = 0;
+    c->have_tail = false;
+    c->begun = true;
+    return KNNM_OK;
+}
+
+int knnm_load_graph(knnm_ctx *c, const int32_t *rows, int64_t m, const int32_t *g_ids,
+                    const double *g_dists, const int32_t *g_sizes, int32_t gk, int32_t k1) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    if (m == 0) return KNNM_OK;
+    if (!rows || !g_sizes || (gk > 0 && (!g_ids || !g_dists))) return fail(KNNM_ERR_ARG, "null argument");
+    if (k1 < 0 || k1 > c->k || gk < k1) return fail(KNNM_ERR_ARG, "bad k1=%d (gk=%d k=%d)", k1, gk, c->k);
+    CK(cudaSetDevice(c->device));
+    PhaseTimer pt(c, PH_OTHER);
+    int tk = c->k - k1;
+    if (tk > 0) {
+        if (c->have_tail && c->tk != tk) return fail(KNNM_ERR_ARG, "inconsistent k1 across graphs");
+        if (!c->have_tail) {
+            size_t nt = (size_t)c->n * tk;
+            TRY(ensure(c->tail_ids, sizeof(int32_t) * nt));
+            TRY(ensure(c->tail_d, sizeof(double) * nt));
+            TRY(ensure(c->tail_s, sizeof(int32_t) * c->n));
+            k_init_lists<<<grid_for(c, (int64_t)nt, 256), 256, 0, c->st>>>(
+                c->n, tk, c->tail_ids.as<int32_t>(), c->tail_d.as<double>(), nullptr,
+                c->tail_s.as<int32_t>());
+            CKL();
+            c->tk = tk;
+            c->have_tail = true;
+        }
+    }
+    size_t mg = (size_t)m * (gk > 0 ? gk : 1);
+    TRY(ensure(c->stage[0], sizeof(int32_t) * m));
+    TRY(ensure(c->stage[1], sizeof(int32_t) * mg));
+    TRY(ensure(c->stage[2], sizeof(double) * mg));
+    TRY(ensure(c->stage[3], sizeof(int32_t) * m));
+    CK(cudaMemcpyAsync(c->stage[0].p, rows, sizeof(int32_t) * m, cudaMemcpyHostToDevice, c->st));
+    if (gk > 0) {
+        CK(cudaMemcpyAsync(c->stage[1].p, g_ids, sizeof(int32_t) * m * gk, cudaMemcpyHostToDevice, c->st));
+        CK(cudaMemcpyAsync(c->stage[2].p, g_dists, sizeof(double) * m * gk, cudaMemcpyHostToDevice, c->st));
+    }
+    CK(cudaMemcpyAsync(c->stage[3].p, g_sizes, sizeof(int32_t) * m, cudaMemcpyHostToDevice, c->st));
+    if (gk > 0) {
+        k_load_graph<<<grid_for(c, m * gk, 256), 256, 0, c->st>>>(
+            c->stage[0].as<int32_t>(), m, c->stage[1].as<int32_t>(), c->stage[2].as<double>(),
+            c->stage[3].as<int32_t>(), gk, k1, c->k, c->ugid.as<int64_t>(), c->n,
+            c->ids.as<int32_t>(), c->dists.as<double>(), c->sizes.as<int32_t>(),
+            tk > 0 ? c->tail_ids.as<int32_t>() : nullptr, tk > 0 ? c->tail_d.as<double>() : nullptr,
+            tk > 0 ? c->tail_s.as<int32_t>() : nullptr, tk);
+        CKL();
+    }
+    CK(cudaStreamSynchronize(c->st));  // staging buffers are reused by the next call
+    return KNNM_OK;
+}
+
+int knnm_insert_directed(knnm_ctx *c, const int32_t *rows, const int32_t *nids, int64_t m,
+                         int64_t *accepted) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    if (accepted) *accepted = 0;
+    if (m == 0) return KNNM_OK;
+    if (!rows || !nids) return fail(KNNM_ERR_ARG, "null argument");
+    CK(cudaSetDevice(c->device));
+    TRY(ensure_candidates(c, (unsigned long long)m));
+    TRY(ensure(c->stage[0], sizeof(int32_t) * m));
+    TRY(ensure(c->stage[1], sizeof(int32_t) * m));
+    CK(cudaMemcpyAsync(c->stage[0].p, rows, sizeof(int32_t) * m, cudaMemcpyHostToDevice, c->st));
+    CK(cudaMemcpyAsync(c->stage[1].p, nids, sizeof(int32_t) * m, cudaMemcpyHostToDevice, c->st));
+    double *capd = nullptr;
+    if (c->capture) {
+        TRY(ensure(c->stage[2], sizeof(double) * m));
+        capd = c->stage[2].as<double>();
+    }
+    unsigned long long *cnt = c->counters.as<unsigned long long>();
+    int64_t acc_total = 0;
+    for (int64_t c0 = 0; c0 < m; c0 += (int64_t)c->cap) {
+        int64_t cm = std::min<int64_t>((int64_t)c->cap, m - c0);
+        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
+        {
+            PhaseTimer pt(c, PH_OTHER);
+            k_directed_emit<<<(unsigned)((cm + 255) / 256), 256, 0, c->st>>>(
+                c->stage[0].as<int32_t>() + c0, c->stage[1].as<int32_t>() + c0, cm, c0, c->subp,
+                c->dp, c->d, c->metric, c->sizes.as<int32_t>(), c->dists.as<double>(), c->k,
+                c->candA.as<CandA>(), c->tcnt.as<uint32_t>(), cnt, capd ? capd + c0 : nullptr);
+            CKL();
+        }
+        {
+            PhaseTimer pt(c, PH_UPDATE);
+            TRY(run_updates(c, (uint64_t)(c0 + cm)));
+        }
+        TRY(sync_counters(c));
+        acc_total += (int64_t)c->hcnt[C_ACCEPTED];
+    }
+    c->stats.init_evals += m;
+    c->stats.accepted += acc_total;
+    if (c->capture) {
+        size_t o = c->cap_pa.size();
+        c->cap_pa.resize(o + m);
+        c->cap_pb.resize(o + m);
+        c->cap_pd.resize(o + m);
+        memcpy(c->cap_pa.data() + o, rows, sizeof(int32_t) * m);
+        memcpy(c->cap_pb.data() + o, nids, sizeof(int32_t) * m);
+        CK(cudaMemcpyAsync(c->cap_pd.data() + o, capd, sizeof(double) * m, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+    }
+    TRY(resolve_timers(c));
+    if (accepted) *accepted = acc_total;
+    return KNNM_OK;
+}
+
+int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, int64_t *pairs,
+               int64_t *accepted) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    if (mode < 0 || mode > 2) return fail(KNNM_ERR_ARG, "mode %d", mode);
+    if (rev_cap < 0 || rev_cap > c->k) return fail(KNNM_ERR_ARG, "rev_cap %d", rev_cap);
+    CK(cudaSetDevice(c->device));
+    int64_t n = c->n;
+    int k = c->k;
+    int W = k + rev_cap;
+    unsigned long long *cnt = c->counters.as<unsigned long long>();
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
+    {
+        PhaseTimer pt(c, PH_REVERSE);
+        CK(cudaMemsetAsync(c->indeg.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+        k_rev_count<<<grid_for(c, n * k, 256), 256, 0, c->st>>>(
+            c->ids.as<int32_t>(), c->sizes.as<int32_t>(), n, k, c->indeg.as<uint32_t>());
+        CKL();
+        TRY(scan<uint32_t, uint32_t>(c, c->indeg.as<uint32_t>(), c->roff.as<uint32_t>(), n));
+        k_rev_fill<<<grid_for(c, n * k, 256), 256, 0, c->st>>>(
+            c->ids.as<int32_t>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), n, k,
+            c->roff.as<uint32_t>(), c->indeg.as<uint32_t>(), c->rev.as<uint32_t>());
+        CKL();
+        k_find_heavy<<<grid_for(c, n, 256), 256, 0, c->st>>>(
+            c->roff.as<uint32_t>(), n, std::max(rev_cap, WARP_REV_MAX), c->heavy.as<int32_t>(), cnt);
+        CKL();
+        k_rev_heavy<<<c->sms * 2, 256, 2 * sizeof(uint32_t) * BLOCK_SORT_MAX, c->st>>>(
+            c->heavy.as<int32_t>(), cnt, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(), rev_cap,
+            round_seed, nullptr, BLOCK_SORT_MAX);
+        CKL();
+        TRY(sync_counters(c));
+        unsigned long long maxdeg = c->hcnt[C_MAXDEG];
+        if (c->hcnt[C_HEAVY_REV] && next_pow2((uint32_t)maxdeg) > (uint32_t)BLOCK_SORT_MAX) {
+            TRY(ensure(c->gscratch32, 2 * sizeof(uint32_t) * next_pow2((uint32_t)maxdeg)));
+            k_rev_heavy<<<1, 1024, 0, c->st>>>(c->heavy.as<int32_t>(), cnt, c->roff.as<uint32_t>(),
+                                               c->rev.as<uint32_t>(), rev_cap, round_seed,
+                                               c->gscratch32.as<uint32_t>(), BLOCK_SORT_MAX);
+            CKL();
+        }
+    }
+    {
+        PhaseTimer pt(c, PH_ASSEMBLE);
+        k_assemble<<<grid_for(c, n * 32, ASM_WARPS * 32, 16), ASM_WARPS * 32, 0, c->st>>>(
+            c->ids.as<int32_t>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
+            c->dists.as<double>(), n, k, rev_cap, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(),
+            round_seed, c->labels.as<int8_t>(), mode, W, c->nbh.as<uint32_t>(),
+            c->nlen.as<int32_t>(), c->hpairs.as<uint32_t>(), c->worst0.as<double>(),
+            c->active.as<int32_t>(), cnt);
+        CKL();
+        TRY(scan<uint32_t, uint64_t>(c, c->hpairs.as<uint32_t>(), c->poff.as<uint64_t>(), n));
+    }
+    uint64_t P = 0;
+    CK(cudaMemcpyAsync(&c->hcnt[C_NUM - 1], c->poff.as<uint64_t>() + n, sizeof(uint64_t),
+                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(c->hcnt, c->counters.p, sizeof(unsigned long long) * (C_NUM - 1),
+                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    P = c->hcnt[C_NUM - 1];
+    unsigned long long nactive = c->hcnt[C_ACTIVE];
+    c->stats.members += (int64_t)c->hcnt[C_MEMBERS];
+    c->stats.pairs += (int64_t)P;
+    c->stats.rounds += 1;
+
+    if (c->capture && P > 0) {
+        DBuf pa, pb, pd;
+        TRY(ensure(pa, sizeof(int32_t) * P));
+        TRY(ensure(pb, sizeof(int32_t) * P));
+        TRY(ensure(pd, sizeof(double) * P));
+        k_capture_pairs<<<(unsigned)((n + 127) / 128), 128, 0, c->st>>>(
+            c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), 0, n, W, c->labels.as<int8_t>(), mode,
+            c->poff.as<uint64_t>(), c->subp, c->dp, c->d, c->metric, pa.as<int32_t>(),
+            pb.as<int32_t>(), pd.as<double>());
+        CKL();
+        size_t o = c->cap_pa.size();
+        c->cap_pa.resize(o + P);
+        c->cap_pb.resize(o + P);
+        c->cap_pd.resize(o + P);
+        CK(cudaMemcpyAsync(c->cap_pa.data() + o, pa.p, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(c->cap_pb.data() + o, pb.p, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(c->cap_pd.data() + o, pd.p, sizeof(double) * P, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        release(pa);
+        release(pb);
+        release(pd);
+    }
+
+    int64_t acc_total = 0;
+    if (P > 0) {
+        TRY(ensure_candidates(c, 2 * P));
+        uint64_t key_max = ((uint64_t)n * W) * W;
+        size_t smem = sizeof(float) * (size_t)W * c->dp;
+        if (smem > 200 * 1024) return fail(KNNM_ERR_LIMIT, "neighbourhood of %d x %d floats exceeds shared memory", W, c->dp);
+        auto launch_join = [&](const int32_t *act, unsigned nblocks) -> int {
+            PhaseTimer pt(c, PH_JOIN);
+            if (c->metric == 1)
+                k_join_exact<1><<<nblocks, JOIN_THREADS, smem, c->st>>>(
+                    act, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,
+                    c->subp, c->dp, c->d, c->worst0.as<double>(), c->candA.as<CandA>(), c->cap,
+                    c->tcnt.as<uint32_t>(), cnt);
+            else if (c->metric == 2)
+                k_join_exact<2><<<nblocks, JOIN_THREADS, smem, c->st>>>(
+                    act, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,
+                    c->subp, c->dp, c->d, c->worst0.as<double>(), c->candA.as<CandA>(), c->cap,
+                    c->tcnt.as<uint32_t>(), cnt);
+            else
+                k_join_exact<0><<<nblocks, JOIN_THREADS, smem, c->st>>>(
+                    act, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,
+                    c->subp, c->dp, c->d, c->worst0.as<double>(), c->candA.as<CandA>(), c->cap,
+                    c->tcnt.as<uint32_t>(), cnt);
+            CKL();
+            c->stats.join_launches += 1;
+            return KNNM_OK;
+        };
+        if (2 * P <= c->cap) {
+            TRY(launch_join(c->active.as<int32_t>(), (unsigned)nactive));
+            {
+                PhaseTimer pt(c, PH_UPDATE);
+                TRY(run_updates(c, key_max));
+            }
+            TRY(sync_counters(c));
+            acc_total = (int64_t)c->hcnt[C_ACCEPTED];
+        } else {
+            // Chunk hoods by index so each chunk's worst case fits; chunks run
+            // in ascending hood order, preserving the reference's per-row order.
+            std::vector<uint64_t> hpoff(n + 1);
+            CK(cudaMemcpyAsync(hpoff.data(), c->poff.p, sizeof(uint64_t) * (n + 1),
+                               cudaMemcpyDeviceToHost, c->st));
+            CK(cudaStreamSynchronize(c->st));
+            // the compacted list is not ordered; build per-chunk lists on host
+            std::vector<uint32_t> hh(n);
+            CK(cudaMemcpy(hh.data(), c->hpairs.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
+            uint64_t budget = c->cap / 2;
+            int64_t lo = 0;
+            while (lo < n) {
+                int64_t hi = lo;
+                std::vector<int32_t> lst;
+                while (hi < n && (hpoff[hi + 1] - hpoff[lo] <= budget || hi == lo)) {
+                    if (hh[hi]) lst.push_back((int32_t)hi);
+                    hi++;
+                }
+                if (!lst.empty()) {
+                    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
+                    CK(cudaMemcpyAsync(c->active.p, lst.data(), sizeof(int32_t) * lst.size(),
+                                       cudaMemcpyHostToDevice, c->st));
+                    TRY(launch_join(c->active.as<int32_t>(), (unsigned)lst.size()));
+                    {
+                        PhaseTimer pt(c, PH_UPDATE);
+                        TRY(run_updates(c, key_max));
+                    }
+                    TRY(sync_counters(c));
+                    acc_total += (int64_t)c->hcnt[C_ACCEPTED];
+                }
+                lo = hi;
+            }
+        }
+    }
+    c->stats.accepted += acc_total;
+    TRY(resolve_timers(c));
+    if (pairs) *pairs = (int64_t)P;
+    if (accepted) *accepted = acc_total;
+    return KNNM_OK;
+}
+
+int knnm_phi(knnm_ctx *c, double *out) {
+    if (!c || !out) return fail(KNNM_ERR_ARG, "null argument");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    CK(cudaSetDevice(c->device));
+    int64_t N = c->n * c->k;
+    if (N == 0) {
+        *out = 0.0;
+        return KNNM_OK;
+    }
+    PhaseTimer pt(c, PH_OTHER);
+    if (c->phi.N != N) {
+        build_phi_tree(c->phi, N);
+        size_t nl = c->phi.leaf_lo.size(), ni = c->phi.left.size();
+        TRY(ensure(c->phi_leaf_lo, sizeof(int64_t) * nl));
+        TRY(ensure(c->phi_leaf_len, sizeof(int32_t) * nl));
+        TRY(ensure(c->phi_leaves, sizeof(double) * nl));
+        TRY(ensure(c->phi_left, sizeof(int32_t) * (ni + 1)));
+        TRY(ensure(c->phi_right, sizeof(int32_t) * (ni + 1)));
+        TRY(ensure(c->phi_inner, sizeof(double) * (ni + 1)));
+        TRY(ensure(c->phi_level, sizeof(int32_t) * c->phi.level_start.size()));
+        CK(cudaMemcpy(c->phi_leaf_lo.p, c->phi.leaf_lo.data(), sizeof(int64_t) * nl, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c->phi_leaf_len.p, c->phi.leaf_len.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice));
+        if (ni) {
+            CK(cudaMemcpy(c->phi_left.p, c->phi.left.data(), sizeof(int32_t) * ni, cudaMemcpyHostToDevice));
+            CK(cudaMemcpy(c->phi_right.p, c->phi.right.data(), sizeof(int32_t) * ni, cudaMemcpyHostToDevice));
+        }
+        CK(cudaMemcpy(c->phi_level.p, c->phi.level_start.data(),
+                      sizeof(int32_t) * c->phi.level_start.size(), cudaMemcpyHostToDevice));
+    }
+    int64_t nl = (int64_t)c->phi.leaf_lo.size();
+    int64_t ni = (int64_t)c->phi.left.size();
+    k_phi_leaves<<<(unsigned)((nl + 127) / 128), 128, 0, c->st>>>(
+        c->dists.as<double>(), c->sizes.as<int32_t>(), c->k, c->phi_leaf_lo.as<int64_t>(),
+        c->phi_leaf_len.as<int32_t>(), nl, c->phi_leaves.as<double>());
+    CKL();
+    if (ni > 0) {
+        k_phi_tree<<<1, 1024, 0, c->st>>>(c->phi_left.as<int32_t>(), c->phi_right.as<int32_t>(),
+                                          c->phi_level.as<int32_t>(),
+                                          (int)c->phi.level_start.size() - 1,
+                                          c->phi_leaves.as<double>(), c->phi_inner.as<double>());
+        CKL();
+        CK(cudaMemcpyAsync(out, c->phi_inner.as<double>() + (ni - 1), sizeof(double),
+                           cudaMemcpyDeviceToHost, c->st));
+    } else {
+        CK(cudaMemcpyAsync(out, c->phi_leaves.p, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+    }
+    CK(cudaStreamSynchronize(c->st));
+    return KNNM_OK;
+}
+
+int knnm_export(knnm_ctx *c, int32_t merge_rear, int32_t *out_ids, double *out_dists,
+                int32_t *out_sizes) {
+    if (!c || !out_ids || !out_dists || !out_sizes) return fail(KNNM_ERR_ARG, "null argument");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    CK(cudaSetDevice(c->device));
+    PhaseTimer pt(c, PH_OTHER);
+    int64_t n = c->n, nk = c->n * c->k;
+    TRY(ensure(c->out_ids, sizeof(int32_t) * nk));
+    k_export<<<grid_for(c, nk, 256), 256, 0, c->st>>>(c->ids.as<int32_t>(), c->ugid.as<int64_t>(),
+                                                       nk, c->out_ids.as<int32_t>());
+    CKL();
+    if (merge_rear && c->have_tail && c->tk > 0) {
+        TRY(ensure(c->out_d, sizeof(double) * nk));
+        TRY(ensure(c->out_s, sizeof(int32_t) * n));
+        TRY(ensure(c->stage[0], sizeof(int32_t) * nk));
+        k_merge_rear<<<(unsigned)((n + 127) / 128), 128, 0, c->st>>>(
+            c->out_ids.as<int32_t>(), c->dists.as<double>(), c->sizes.as<int32_t>(),
+            c->tail_ids.as<int32_t>(), c->tail_d.as<double>(), c->tail_s.as<int32_t>(), n, c->k,
+            c->tk, c->stage[0].as<int32_t>(), c->out_d.as<double>(), c->out_s.as<int32_t>());
+        CKL();
+        CK(cudaMemcpyAsync(out_ids, c->stage[0].p, sizeof(int32_t) * nk, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(out_dists, c->out_d.p, sizeof(double) * nk, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(out_sizes, c->out_s.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->st));
+    } else {
+        CK(cudaMemcpyAsync(out_ids, c->out_ids.p, sizeof(int32_t) * nk, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(out_dists, c->dists.p, sizeof(double) * nk, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaMemcpyAsync(out_sizes, c->sizes.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->st));
+    }
+    CK(cudaStreamSynchronize(c->st));
+    return KNNM_OK;
+}
+
+int knnm_get_state(knnm_ctx *c, int32_t *ids, double *dists, uint8_t *flags, int32_t *sizes) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    CK(cudaSetDevice(c->device));
+    size_t nk = (size_t)c->n * c->k;
+    if (ids) CK(cudaMemcpyAsync(ids, c->ids.p, sizeof(int32_t) * nk, cudaMemcpyDeviceToHost, c->st));
+    if (dists) CK(cudaMemcpyAsync(dists, c->dists.p, sizeof(double) * nk, cudaMemcpyDeviceToHost, c->st));
+    if (flags) CK(cudaMemcpyAsync(flags, c->flags.p, nk, cudaMemcpyDeviceToHost, c->st));
+    if (sizes) CK(cudaMemcpyAsync(sizes, c->sizes.p, sizeof(int32_t) * c->n, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    return KNNM_OK;
+}
+
+int knnm_set_capture(knnm_ctx *c, int32_t on) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    c->capture = on != 0;
+    c->cap_pa.clear();
+    c->cap_pb.clear();
+    c->cap_pd.clear();
+    return KNNM_OK;
+}
+
+int knnm_capture_count(knnm_ctx *c, int64_t *count) {
+    if (!c || !count) return fail(KNNM_ERR_ARG, "null argument");
+    *count = (int64_t)c->cap_pa.size();
+    return KNNM_OK;
+}
+
+int knnm_capture_fetch(knnm_ctx *c, int32_t *pa, int32_t *pb, double *pd, int64_t count) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (count != (int64_t)c->cap_pa.size()) return fail(KNNM_ERR_ARG, "count mismatch");
+    if (count) {
+        memcpy(pa, c->cap_pa.data(), sizeof(int32_t) * count);
+        memcpy(pb, c->cap_pb.data(), sizeof(int32_t) * count);
+        memcpy(pd, c->cap_pd.data(), sizeof(double) * count);
+    }
+    c->cap_pa.clear();
+    c->cap_pb.clear();
+    c->cap_pd.clear();
+    return KNNM_OK;
+}
+
+int knnm_set_profiling(knnm_ctx *c, int32_t on) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    c->profiling = on != 0;
+    return KNNM_OK;
+}
+
+int knnm_get_stats(knnm_ctx *c, knnm_stats *out) {
+    if (!c || !out) return fail(KNNM_ERR_ARG, "null argument");
+    TRY(resolve_timers(c));
+    *out = c->stats;
+    out->join_ms = c->phase_ms[PH_JOIN];
+    out->reverse_ms = c->phase_ms[PH_REVERSE];
+    out->assemble_ms = c->phase_ms[PH_ASSEMBLE];
+    out->update_ms = c->phase_ms[PH_UPDATE];
+    out->other_ms = c->phase_ms[PH_OTHER];
+    return KNNM_OK;
+}
+
+int knnm_reset_stats(knnm_ctx *c) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    TRY(resolve_timers(c));
+    c->stats = knnm_stats{};
+    for (double &v : c->phase_ms) v = 0;
+    return KNNM_OK;
+}
+
+int knnm_sync(knnm_ctx *c) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    CK(cudaStreamSynchronize(c->st));
+    return KNNM_OK;
+}
+
+}  // extern "C"

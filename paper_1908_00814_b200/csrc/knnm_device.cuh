@@ -1,0 +1,265 @@
+// knnm_device.cuh -- device helpers shared by the knnm kernels (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define FULL_MASK 0xffffffffu
+
+namespace knnm {
+
+constexpr uint64_t U64_GAMMA = 0x9E3779B97F4A7C15ULL;  // _kernels.py:33
+constexpr uint64_t U64_MIX1 = 0xBF58476D1CE4E5B9ULL;   // _kernels.py:34
+constexpr uint64_t U64_MIX2 = 0x94D049BB133111EBULL;   // _kernels.py:35
+
+// Indices into the per-context device counter block.
+enum Counter {
+    C_CAND = 0,       // candidate records emitted (directed updates)
+    C_ACCEPTED = 1,   // accepted insertions
+    C_ACTIVE = 2,     // active hoods (>= 1 admissible pair)
+    C_HEAVY_REV = 3,  // vertices whose reverse segment needs block selection
+    C_MAXDEG = 4,     // max reverse degree among heavy vertices
+    C_MEMBERS = 5,    // sum |M_u| over hoods
+    C_HEAVY_APPLY = 6,// rows with more candidates than the warp path holds
+    C_GIANT_APPLY = 7,// rows with more candidates than the block smem path holds
+    C_OVERFLOW = 8,   // candidate buffer overflow (must stay 0)
+    C_EXACT = 9,      // pairs re-evaluated in fp64 after the fp32 screen
+    C_MAXC = 10,      // max candidates on a giant row
+    C_NUM = 16
+};
+
+// splitmix64 output for a state that was already advanced (_kernels.py:306-313).
+__device__ __forceinline__ uint64_t mix64(uint64_t z) {
+    z = (z ^ (z >> 30)) * U64_MIX1;
+    z = (z ^ (z >> 27)) * U64_MIX2;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+__host__ __device__ __forceinline__ uint32_t next_pow2(uint32_t x) {
+    uint32_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+// ---------------------------------------------------------------------------
+// Exact metric (_kernels.py:43-80): fp64 accumulation of fp32 inputs, strictly
+// sequential, no contraction (explicit _rn intrinsics are never fused).
+// ---------------------------------------------------------------------------
+template <int TAG>
+__device__ __forceinline__ double exact_dist(const float *__restrict__ a,
+                                             const float *__restrict__ b, int d) {
+    if (TAG == 1) {
+        double acc = 0.0;
+        for (int t = 0; t < d; t++) {
+            double df = __dsub_rn((double)a[t], (double)b[t]);
+            acc = __dadd_rn(acc, __dmul_rn(df, df));
+        }
+        return acc;
+    } else if (TAG == 0) {
+        double acc = 0.0;
+        for (int t = 0; t < d; t++) acc = __dadd_rn(acc, fabs(__dsub_rn((double)a[t], (double)b[t])));
+        return acc;
+    } else {
+        double dot = 0.0, na = 0.0, nb = 0.0;
+        for (int t = 0; t < d; t++) {
+            double x = (double)a[t], y = (double)b[t];
+            dot = __dadd_rn(dot, __dmul_rn(x, y));
+            na = __dadd_rn(na, __dmul_rn(x, x));
+            nb = __dadd_rn(nb, __dmul_rn(y, y));
+        }
+        if (na == 0.0 || nb == 0.0) return (na == nb) ? 0.0 : 1.0;
+        if (dot > 0.0 && __dmul_rn(dot, dot) >= __dmul_rn(na, nb)) return 0.0;
+        double r = __dsub_rn(1.0, __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(na), __dsqrt_rn(nb))));
+        return r < 0.0 ? 0.0 : r;
+    }
+}
+
+__device__ __forceinline__ double exact_dist_tag(int tag, const float *a, const float *b, int d) {
+    if (tag == 1) return exact_dist<1>(a, b, d);
+    if (tag == 2) return exact_dist<2>(a, b, d);
+    return exact_dist<0>(a, b, d);
+}
+
+// ---------------------------------------------------------------------------
+// Bitonic sorts over shared (or global) arrays of power-of-two length.
+// Group = one warp (sync = __syncwarp) or one block (sync = __syncthreads).
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ void bitonic_warp(T *a, uint32_t P2, unsigned lane) {
+    for (uint32_t k2 = 2; k2 <= P2; k2 <<= 1) {
+        for (uint32_t j = k2 >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = lane; i < P2; i += 32) {
+                uint32_t ixj = i ^ j;
+                if (ixj > i) {
+                    T x = a[i], y = a[ixj];
+                    bool asc = (i & k2) == 0;
+                    if ((x > y) == asc) { a[i] = y; a[ixj] = x; }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void bitonic_block(T *a, uint32_t P2) {
+    for (uint32_t k2 = 2; k2 <= P2; k2 <<= 1) {
+        for (uint32_t j = k2 >> 1; j > 0; j >>= 1) {
+            for (uint32_t i = threadIdx.x; i < P2; i += blockDim.x) {
+                uint32_t ixj = i ^ j;
+                if (ixj > i) {
+                    T x = a[i], y = a[ixj];
+                    bool asc = (i & k2) == 0;
+                    if ((x > y) == asc) { a[i] = y; a[ixj] = x; }
+                }
+            }
+            __syncthreads();
+        }
+    }
+}
+
+// Register bitonic sort of one u64 per lane (ascending by lane).
+__device__ __forceinline__ uint64_t bitonic_reg32(uint64_t v, unsigned lane) {
+#pragma unroll
+    for (int k2 = 2; k2 <= 32; k2 <<= 1) {
+#pragma unroll
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+            uint64_t o = __shfl_xor_sync(FULL_MASK, v, j);
+            bool up = (lane & k2) == 0;
+            bool lower = (lane & j) == 0;
+            uint64_t mn = v < o ? v : o, mx = v < o ? o : v;
+            v = (lower == up) ? mn : mx;
+        }
+    }
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// One row of the k-NN state held by a warp: entry t = e*32 + lane.
+// warp_insert() is _insert (_kernels.py:159-192) executed cooperatively.
+// ---------------------------------------------------------------------------
+template <int E>
+struct WarpRow {
+    int id[E];
+    double d[E];
+    int fl[E];
+    int sz;
+    double worst;  // dists[k-1] when sz == k
+};
+
+template <int E>
+__device__ __forceinline__ void row_load(WarpRow<E> &s, const int32_t *ids, const double *dists,
+                                         const uint8_t *flags, const int32_t *sizes, int64_t r,
+                                         int k, unsigned lane) {
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        int t = e * 32 + lane;
+        if (t < k) {
+            s.id[e] = ids[r * k + t];
+            s.d[e] = dists[r * k + t];
+            s.fl[e] = flags[r * k + t];
+        } else {
+            s.id[e] = -1;
+            s.d[e] = __longlong_as_double(0x7ff0000000000000LL);
+            s.fl[e] = 0;
+        }
+    }
+    s.sz = sizes[r];
+    s.worst = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; e++)
+        if (e == ((k - 1) >> 5)) s.worst = __shfl_sync(FULL_MASK, s.d[e], (k - 1) & 31);
+}
+
+template <int E>
+__device__ __forceinline__ void row_store(const WarpRow<E> &s, int32_t *ids, double *dists,
+                                          uint8_t *flags, int32_t *sizes, int64_t r, int k,
+                                          unsigned lane) {
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        int t = e * 32 + lane;
+        if (t < k) {
+            ids[r * k + t] = s.id[e];
+            dists[r * k + t] = s.d[e];
+            flags[r * k + t] = (uint8_t)s.fl[e];
+        }
+    }
+    if (lane == 0) sizes[r] = s.sz;
+}
+
+// Returns 1 (warp-uniform) when the candidate is accepted.
+template <int E>
+__device__ __forceinline__ int warp_insert(WarpRow<E> &s, int k, int src, double nd, unsigned lane) {
+    if (s.sz == k && nd >= s.worst) return 0;
+    bool dup = false;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        int t = e * 32 + lane;
+        dup |= (t < s.sz && s.id[e] == src);
+    }
+    if (__any_sync(FULL_MASK, dup)) return 0;
+    int pos = s.sz;
+#pragma unroll
+    for (int e = E - 1; e >= 0; e--) {
+        int t = e * 32 + lane;
+        bool before = t < s.sz && (nd < s.d[e] || (nd == s.d[e] && src < s.id[e]));
+        unsigned b = __ballot_sync(FULL_MASK, before);
+        if (b) pos = e * 32 + __ffs(b) - 1;
+    }
+    int last;
+    if (s.sz == k) {
+        last = k - 1;
+    } else {
+        last = s.sz;
+        s.sz += 1;
+    }
+#pragma unroll
+    for (int e = E - 1; e >= 0; e--) {
+        int up_id = __shfl_up_sync(FULL_MASK, s.id[e], 1);
+        double up_d = __shfl_up_sync(FULL_MASK, s.d[e], 1);
+        int up_f = __shfl_up_sync(FULL_MASK, s.fl[e], 1);
+        if (e > 0) {
+            int pid = __shfl_sync(FULL_MASK, s.id[e > 0 ? e - 1 : 0], 31);
+            double pd = __shfl_sync(FULL_MASK, s.d[e > 0 ? e - 1 : 0], 31);
+            int pf = __shfl_sync(FULL_MASK, s.fl[e > 0 ? e - 1 : 0], 31);
+            if (lane == 0) { up_id = pid; up_d = pd; up_f = pf; }
+        }
+        int t = e * 32 + lane;
+        if (t > pos && t <= last) { s.id[e] = up_id; s.d[e] = up_d; s.fl[e] = up_f; }
+        if (t == pos) { s.id[e] = src; s.d[e] = nd; s.fl[e] = 1; }
+    }
+    if (s.sz == k) {
+#pragma unroll
+        for (int e = 0; e < E; e++)
+            if (e == ((k - 1) >> 5)) s.worst = __shfl_sync(FULL_MASK, s.d[e], (k - 1) & 31);
+    }
+    return 1;
+}
+
+// Apply up to 32 in-order candidates held one per lane (lanes [0, cnt)).
+// Candidates that cannot pass the "full and nd >= worst" test are skipped
+// without changing the outcome (worst is non-increasing once a row is full).
+template <int E>
+__device__ __forceinline__ int warp_apply_chunk(WarpRow<E> &s, int k, int src_l, double d_l,
+                                                int cnt, unsigned lane) {
+    int acc = 0;
+    int i = -1;
+    while (true) {
+        bool live = (int)lane > i && (int)lane < cnt && (s.sz < k || d_l < s.worst);
+        unsigned m = __ballot_sync(FULL_MASK, live);
+        if (!m) break;
+        i = __ffs(m) - 1;
+        int src = __shfl_sync(FULL_MASK, src_l, i);
+        double nd = __shfl_sync(FULL_MASK, d_l, i);
+        acc += warp_insert<E>(s, k, src, nd, lane);
+    }
+    return acc;
+}
+
+}  // namespace knnm

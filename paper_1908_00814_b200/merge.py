@@ -1,0 +1,234 @@
+"""Symmetric (S-Merge) and joint (J-Merge) k-NN graph merges on B200.
+
+Drop-in mirror of the reference's merge.py (pkg/src/knnmerge/merge.py):
+``s_merge`` / ``j_merge`` keep their signatures, argument meaning, input
+validation (ValueError messages included), PCG64 draw sequence, return
+types and output layout.  The data path -- union gather, split/localise,
+random cross appends, every local-join round, export and rear merge --
+runs in libknnm.so on the GPU and is bit-identical to the reference.
+"""
+
+from __future__ import annotations
+
+import logging
+from dataclasses import dataclass
+
+import numpy as np
+
+from .construct import (
+    MODE_CROSS,
+    MODE_CROSS_OR_S2,
+    BuildReport,
+    DescentParams,
+    _capture,
+    _descent_rounds,
+    _graph_from,
+    _insert_directed,
+)
+from .core import DistanceCounter, Metric, sample_distinct
+from .engine import get_engine
+from .graph import KnnGraph, phi as graph_phi
+
+logger = logging.getLogger(__name__)
+
+
+@dataclass
+class MergeParams:
+    """Merge knobs (merge.py:40-71): k, kept fraction r (k1 = round(r*k)),
+    round limit and stop fraction, seed."""
+
+    k: int
+    r: float = 0.5
+    max_iters: int = 50
+    min_update_fraction: float = 0.001
+    seed: int = 0
+
+    def __post_init__(self) -> None:
+        if self.k < 2:
+            raise ValueError("k must be >= 2")
+        if not 0.0 <= self.r <= 1.0:
+            raise ValueError("r must be in [0, 1]")
+
+    @property
+    def k1(self) -> int:
+        return int(round(self.r * self.k))
+
+    def descent_params(self) -> DescentParams:
+        return DescentParams(k=self.k, max_iters=self.max_iters,
+                             min_update_fraction=self.min_update_fraction)
+
+
+def _lookup_local(union_gids: np.ndarray, gids: np.ndarray) -> np.ndarray:
+    return np.searchsorted(union_gids, gids).astype(np.int32)
+
+
+def _sample_pool_rows(rng, nrows: int, t: int, pool: np.ndarray) -> np.ndarray:
+    """(nrows, t) distinct draws per row from ``pool`` (merge.py:146-163;
+    identical PCG64 call sequence)."""
+    m = pool.shape[0]
+    if t > m:
+        raise ValueError("cannot draw more samples than the pool holds")
+    if t == m or 4 * t * t >= m:
+        out = np.empty((nrows, t), dtype=np.int64)
+        for u in range(nrows):
+            out[u] = rng.choice(m, size=t, replace=False)
+        return pool[out]
+    cand = rng.integers(0, m, size=(nrows, t))
+    while True:
+        srt = np.sort(cand, axis=1)
+        bad = (np.diff(srt, axis=1) == 0).any(axis=1)
+        if not bad.any():
+            return pool[cand]
+        rows = np.nonzero(bad)[0]
+        cand[rows] = rng.integers(0, m, size=(rows.size, t))
+
+
+def _append_random(engine, rows, pool, count, rng, counter, on_pair, gids) -> None:
+    """merge.py:166-176: append ``count`` random pool members to each row,
+    flagged new, with exact distances (device)."""
+    if count <= 0 or rows.size == 0 or pool.size == 0:
+        return
+    picks = _sample_pool_rows(rng, rows.size, count, pool)
+    tgt = np.repeat(rows.astype(np.int32), count)
+    nids = picks.ravel().astype(np.int32)
+    _insert_directed(engine, tgt, nids, counter, on_pair, gids)
+
+
+def _check_merge_inputs(dataset, g: KnnGraph, other_ids: np.ndarray, params: MergeParams,
+                        other_graph: KnnGraph | None) -> None:
+    """merge.py:179-192, same checks and messages."""
+    if np.intersect1d(g.member_ids, other_ids).size:
+        raise ValueError("subsets must be disjoint")
+    if g.k != params.k:
+        raise ValueError(f"graph capacity {g.k} does not match params.k={params.k}")
+    if other_graph is not None:
+        if other_graph.metric != g.metric:
+            raise ValueError("graphs must share a metric")
+        if other_graph.k != params.k:
+            raise ValueError("graphs must share capacity k")
+    Metric(g.metric).check_kind(dataset.kind)
+    if other_ids.size and (other_ids.min() < 0 or other_ids.max() >= dataset.n):
+        raise ValueError("ids outside the dataset")
+
+
+def s_merge(dataset, g: KnnGraph, h: KnnGraph, params: MergeParams,
+            counter: DistanceCounter | None = None, on_pair=None, return_report: bool = False,
+            device: int | None = None):
+    """Symmetric merge of two built k-NN graphs over disjoint subsets
+    (merge.py:195-260; Alg. 1 of the paper)."""
+    _check_merge_inputs(dataset, g, h.member_ids, params, h)
+    if counter is None:
+        counter = DistanceCounter()
+    rng = np.random.default_rng(params.seed)
+    metric = Metric(g.metric)
+    k = params.k
+    k1 = params.k1
+
+    union_gids = np.union1d(g.member_ids, h.member_ids)
+    n = union_gids.shape[0]
+    rows_g = _lookup_local(union_gids, g.member_ids)
+    rows_h = _lookup_local(union_gids, h.member_ids)
+    labels = np.zeros(n, dtype=np.int8)
+    labels[rows_h] = 1
+
+    eng = get_engine(device)
+    eng.set_dataset(dataset.vectors, int(metric))
+    eng.begin(union_gids, labels, k)
+    _capture(eng, on_pair)
+    try:
+        eng.load_graph(rows_g, g, k1)
+        eng.load_graph(rows_h, h, k1)
+        fill = k - k1
+        _append_random(eng, rows_g, rows_h.astype(np.int64), min(fill, rows_h.size), rng,
+                       counter, on_pair, union_gids)
+        _append_random(eng, rows_h, rows_g.astype(np.int64), min(fill, rows_g.size), rng,
+                       counter, on_pair, union_gids)
+        report = BuildReport(phi_initial=eng.phi())
+        _descent_rounds(eng, n, MODE_CROSS, k, params.descent_params(), rng, counter, on_pair,
+                        union_gids, report)
+        ids, dists, sizes = eng.export(merge_rear=k - k1 > 0)
+    finally:
+        eng.set_capture(False)
+    u = _graph_from(union_gids, k, metric, ids, dists, sizes)
+    if return_report:
+        return u, report
+    return u
+
+
+def j_merge(dataset, g: KnnGraph, raw_ids, params: MergeParams,
+            counter: DistanceCounter | None = None, on_pair=None, return_report: bool = False,
+            device: int | None = None):
+    """Joint merge of a raw id set into a built k-NN graph
+    (merge.py:263-338; Alg. 2 of the paper)."""
+    raw = np.unique(np.asarray(raw_ids, dtype=np.int64))
+    _check_merge_inputs(dataset, g, raw, params, None)
+    if counter is None:
+        counter = DistanceCounter()
+    metric = Metric(g.metric)
+    k = params.k
+    k1 = params.k1
+    eng = get_engine(device)
+    if raw.size == 0:
+        # trivial split / merge-sort round trip (merge.py:283-291)
+        eng.set_dataset(dataset.vectors, int(metric))
+        eng.begin(g.member_ids, np.zeros(g.n, dtype=np.int8), k)
+        eng.load_graph(np.arange(g.n, dtype=np.int32), g, k1)
+        ids, dists, sizes = eng.export(merge_rear=k - k1 > 0)
+        out = _graph_from(g.member_ids.copy(), k, metric, ids, dists, sizes)
+        if return_report:
+            return out, BuildReport(phi_initial=graph_phi(out))
+        return out
+    rng = np.random.default_rng(params.seed)
+    union_gids = np.union1d(g.member_ids, raw)
+    n = union_gids.shape[0]
+    if k >= n:
+        raise ValueError(f"k={k} must be below the union size {n}")
+    rows_g = _lookup_local(union_gids, g.member_ids)
+    rows_raw = _lookup_local(union_gids, raw)
+    labels = np.zeros(n, dtype=np.int8)
+    labels[rows_raw] = 1
+
+    eng.set_dataset(dataset.vectors, int(metric))
+    eng.begin(union_gids, labels, k)
+    _capture(eng, on_pair)
+    try:
+        eng.load_graph(rows_g, g, k1)
+        _append_random(eng, rows_g, rows_raw.astype(np.int64), min(k - k1, rows_raw.size), rng,
+                       counter, on_pair, union_gids)
+        # raw lists start from k random draws over the whole union (merge.py:318-325)
+        init = np.empty((rows_raw.size, k), dtype=np.int64)
+        for t, row in enumerate(rows_raw):
+            init[t] = sample_distinct(rng, n, k, exclude=int(row))
+        tgt = np.repeat(rows_raw.astype(np.int32), k)
+        _insert_directed(eng, tgt, init.ravel().astype(np.int32), counter, on_pair, union_gids)
+        report = BuildReport(phi_initial=eng.phi())
+        _descent_rounds(eng, n, MODE_CROSS_OR_S2, k, params.descent_params(), rng, counter,
+                        on_pair, union_gids, report)
+        ids, dists, sizes = eng.export(merge_rear=k - k1 > 0)
+    finally:
+        eng.set_capture(False)
+    u = _graph_from(union_gids, k, metric, ids, dists, sizes)
+    if return_report:
+        return u, report
+    return u
+
+
+def merge_rear(u: KnnGraph, tail: KnnGraph, device: int | None = None) -> KnnGraph:
+    """Per-vertex sorted merge of u's lists with rear lists, truncated to k
+    (graph.py:259-280, _kernels.py:529-563), on the device."""
+    if not np.all(np.isin(tail.member_ids, u.member_ids)):
+        raise ValueError("tail vertices must be members of the merged graph")
+    if tail.k > u.k:
+        raise ValueError("rear lists wider than the merged capacity are not supported")
+    eng = get_engine(device)
+    # the engine needs a dataset that covers the member ids; rear merging
+    # never reads vectors, so a one-column placeholder is enough
+    need = int(u.member_ids[-1]) + 1 if u.n else 1
+    if eng._vectors is None or eng._vectors.shape[0] < need:
+        eng.set_dataset(np.zeros((need, 1), dtype=np.float32), int(u.metric))
+    eng.begin(u.member_ids, np.zeros(u.n, dtype=np.int8), u.k)
+    eng.load_graph(np.arange(u.n, dtype=np.int32), u, u.k)
+    if tail.k > 0:
+        eng.load_graph(_lookup_local(u.member_ids, tail.member_ids), tail, 0)
+    ids, dists, sizes = eng.export(merge_rear=tail.k > 0)
+    return _graph_from(u.member_ids.copy(), u.k, u.metric, ids, dists, sizes)

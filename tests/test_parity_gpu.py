@@ -1,0 +1,111 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle.
+
+Bit-exact on ids, dists, sizes, the distance counter and every per-round
+report field (pairs, updates, phi), because the oracle restates the
+reference arithmetic exactly and the device path replays the reference's
+per-row insertion order.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import split_ids
+
+pytestmark = pytest.mark.gpu
+
+
+def _km():
+    import paper_1908_00814_b200 as km
+
+    return km
+
+
+def _same_graph(a, b):
+    assert np.array_equal(np.asarray(a.member_ids), np.asarray(b.member_ids))
+    assert np.array_equal(a.sizes, b.sizes)
+    assert np.array_equal(a.ids, b.ids)
+    assert np.array_equal(a.dists, b.dists)
+
+
+def _same_report(rep, orep):
+    assert rep.phi_initial == orep.phi_initial
+    got = [(r.iteration, r.pairs, r.updates, r.phi, r.distance_count) for r in rep.rounds]
+    want = [(r.iteration, r.pairs, r.updates, r.phi, r.distance_count) for r in orep.rounds]
+    assert got == want
+    assert rep.converged == orep.converged
+
+
+CASES = [
+    # n, d, k, metric, data kind
+    (600, 4, 8, 1, "uniform"),
+    (3000, 16, 10, 1, "uniform"),
+    (2000, 12, 12, 2, "uniform"),
+    (4000, 32, 20, 1, "uniform"),
+    (3000, 8, 40, 1, "uniform"),
+    (6000, 128, 20, 1, "intgmm"),
+    (3000, 100, 40, 2, "sphere"),
+    (2000, 960, 20, 1, "unitgmm"),
+    (1500, 5, 6, 0, "uniform"),
+]
+
+
+def _data(km, n, d, kind, seed):
+    if kind == "uniform":
+        return km.generate_uniform(n, d, seed=seed)
+    if kind == "intgmm":
+        return km.generate_int_gmm(n, d, n_centres=50, seed=seed)
+    if kind == "unitgmm":
+        return km.generate_unit_gmm(n, d, n_centres=20, seed=seed)
+    return km.generate_sphere_gmm(n, d, n_centres=40, seed=seed)
+
+
+@pytest.mark.parametrize("n,d,k,metric,kind", CASES)
+def test_nn_descent_matches_oracle(oracle, n, d, k, metric, kind):
+    km = _km()
+    ds = _data(km, n, d, kind, seed=n + d)
+    s1, _ = split_ids(n, seed=1)
+    g, rep = km.nn_descent(ds, metric, km.DescentParams(k=k), 1, member_ids=s1,
+                           return_report=True)
+    og, orep, ocount = oracle.nn_descent(ds.vectors, metric, k, 1, member_ids=s1)
+    _same_graph(g, og)
+    _same_report(rep, orep)
+
+
+@pytest.mark.parametrize("n,d,k,metric,kind", CASES)
+def test_s_merge_matches_oracle(oracle, n, d, k, metric, kind):
+    km = _km()
+    ds = _data(km, n, d, kind, seed=n + d)
+    s1, s2 = split_ids(n, seed=2)
+    g, _, _ = oracle.nn_descent(ds.vectors, metric, k, 1, member_ids=s1)
+    h, _, _ = oracle.nn_descent(ds.vectors, metric, k, 2, member_ids=s2)
+    gg = _to_graph(km, g)
+    hh = _to_graph(km, h)
+    c = km.DistanceCounter()
+    u, rep = km.s_merge(ds, gg, hh, km.MergeParams(k=k, seed=3), counter=c, return_report=True)
+    ou, orep, ocount = oracle.s_merge(ds.vectors, g, h, k, seed=3)
+    _same_graph(u, ou)
+    _same_report(rep, orep)
+    assert c.count == ocount
+
+
+@pytest.mark.parametrize("n,d,k,metric,kind", CASES)
+def test_j_merge_matches_oracle(oracle, n, d, k, metric, kind):
+    km = _km()
+    ds = _data(km, n, d, kind, seed=n + d)
+    s1, s2 = split_ids(n, seed=4)
+    g, _, _ = oracle.nn_descent(ds.vectors, metric, k, 1, member_ids=s1)
+    c = km.DistanceCounter()
+    u, rep = km.j_merge(ds, _to_graph(km, g), s2, km.MergeParams(k=k, seed=5), counter=c,
+                        return_report=True)
+    ou, orep, ocount = oracle.j_merge(ds.vectors, g, s2, k, seed=5)
+    _same_graph(u, ou)
+    _same_report(rep, orep)
+    assert c.count == ocount
+
+
+def _to_graph(km, og):
+    g = km.KnnGraph(og.member_ids, og.k, og.metric)
+    g.ids = og.ids.copy()
+    g.dists = og.dists.copy()
+    g.sizes = og.sizes.copy()
+    return g
