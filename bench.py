@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""bench.py -- S-Merge throughput on B200 at BASELINE.json config 2.
+
+Workload (BASELINE.json configs[1]): symmetric merge of two k=20
+subgraphs of 500,000 points each; d=128 fp32 from a 1,000-component
+Gaussian mixture (centres U[0,255], sigma 20) clipped to [0,255] and
+rounded; L2.  Synthetic, seeded data stands in for SIFT1M.
+The subgraphs are built first (untimed) with this package's NN-Descent,
+which is bit-identical to the reference's.
+
+One step = one full ``s_merge`` call (split, random cross appends, every
+local-join round to convergence, export, rear merge).
+
+  value  distance evaluations/s with the dataset and both subgraphs already
+         resident in HBM and the result left in HBM (CUDA events on the
+         engine stream).
+  e2e    the same metric through the public API with host numpy inputs:
+         dataset upload, graph upload, result download inside the region.
+
+``--impl reference`` times the CPU oracle (oracle/, a C/OpenMP restatement
+of the reference's numba kernels; the Python reference cannot travel to the
+GPU box) on a bounded sample of the same workload with all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CFG = dict(n=1_000_000, d=128, k=20, r=0.5, n_centres=1000, sigma=20.0, data_seed=7,
+           split_seed=1, g_seed=1, h_seed=2, merge_seed=3)
+CPU_SAMPLE_N = 100_000  # 2 x 50k points of the same distribution
+METRIC = "distance_evals_per_s"
+UNIT = "evals/s"
+
+
+def split_ids(n, seed):
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(n)
+    h = n // 2
+    return np.sort(perm[:h]), np.sort(perm[h:])
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) == 6:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def make_inputs(km, n):
+    ds = km.generate_int_gmm(n, CFG["d"], n_centres=CFG["n_centres"], sigma=CFG["sigma"],
+                             seed=CFG["data_seed"])
+    s1, s2 = split_ids(n, CFG["split_seed"])
+    return ds, s1, s2
+
+
+def recall_sample(ds, graph, device, nq=1000, seed=0):
+    """recall@10 of `graph` on nq sampled nodes against exact brute force
+    (fp32 GEMM on the GPU is exact here: integer data, sums < 2^24)."""
+    import torch
+
+    rng = np.random.default_rng(seed)
+    q = np.sort(rng.choice(ds.n, size=min(nq, ds.n), replace=False))
+    X = torch.from_numpy(ds.vectors).to(f"cuda:{device}")
+    Q = X[torch.from_numpy(q).to(X.device)]
+    d = (Q * Q).sum(1, keepdim=True) + (X * X).sum(1)[None, :] - 2.0 * Q @ X.T
+    d[torch.arange(len(q)), torch.from_numpy(q).to(X.device)] = float("inf")
+    truth = torch.topk(d, 10, largest=False).indices.cpu().numpy()
+    rows = np.searchsorted(np.asarray(graph.member_ids), q)
+    got = np.asarray(graph.ids)[rows, :10]
+    hits = sum(len(set(t.tolist()) & set(g.tolist())) for t, g in zip(truth, got))
+    del X, Q, d
+    return hits / (len(q) * 10)
+
+
+def cpu_baseline(n_sample=CPU_SAMPLE_N):
+    """Oracle S-Merge on a bounded sample (2 x n/2 points, same distribution)."""
+    from oracle import oracle as O
+    import paper_1908_00814_b200.core as core
+
+    O.build()
+    ds = core.generate_int_gmm(n_sample, CFG["d"], n_centres=CFG["n_centres"],
+                               sigma=CFG["sigma"], seed=CFG["data_seed"])
+    s1, s2 = split_ids(n_sample, CFG["split_seed"])
+    g, _, _ = O.nn_descent(ds.vectors, 1, CFG["k"], CFG["g_seed"], member_ids=s1)
+    h, _, _ = O.nn_descent(ds.vectors, 1, CFG["k"], CFG["h_seed"], member_ids=s2)
+    t0 = time.perf_counter()
+    u, rep, count = O.s_merge(ds.vectors, g, h, CFG["k"], r=CFG["r"], seed=CFG["merge_seed"])
+    dt = time.perf_counter() - t0
+    return dict(value=count / dt, seconds=dt, evals=count, rounds=len(rep.rounds),
+                cores=os.cpu_count(), kind="port",
+                sample=f"s_merge of 2x{n_sample // 2} points, config-2 distribution, k=20; "
+                       "subgraphs built by the oracle's nn_descent (untimed)")
+
+
+def run_reference(args):
+    world, rank, _ = dist_setup()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    import paper_1908_00814_b200.core as core
+
+    O.build()
+    n = int(CPU_SAMPLE_N * args.scale) if args.scale < 1 else CPU_SAMPLE_N
+    ds = core.generate_int_gmm(n, CFG["d"], n_centres=CFG["n_centres"], sigma=CFG["sigma"],
+                               seed=CFG["data_seed"])
+    s1, s2 = split_ids(n, CFG["split_seed"])
+    g, _, _ = O.nn_descent(ds.vectors, 1, CFG["k"], CFG["g_seed"], member_ids=s1)
+    h, _, _ = O.nn_descent(ds.vectors, 1, CFG["k"], CFG["h_seed"], member_ids=s2)
+    for _ in range(args.warmup):
+        O.s_merge(ds.vectors, g, h, CFG["k"], r=CFG["r"], seed=CFG["merge_seed"])
+    t0 = time.perf_counter()
+    evals = 0
+    for _ in range(args.steps):
+        _, rep, count = O.s_merge(ds.vectors, g, h, CFG["k"], r=CFG["r"], seed=CFG["merge_seed"])
+        evals += count
+    dt = time.perf_counter() - t0
+    v = evals / dt
+    sample = (f"s_merge of 2x{n // 2} points (config-2 distribution, k=20) per step; "
+              "oracle C/OpenMP restatement of the reference kernels")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "config2_smerge_2x500k_d128_k20",
+                                            "sample_points": n, "parallelism": "host threads"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args):
+    import torch
+
+    world, rank, local = dist_setup()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1908_00814_b200 as km
+    from paper_1908_00814_b200.engine import get_engine
+
+    n = int(CFG["n"] * args.scale)
+    k = CFG["k"]
+    t_setup = time.perf_counter()
+    ds, s1, s2 = make_inputs(km, n)
+    eng = get_engine(local)
+    # subgraphs (untimed), kept resident in HBM as device tensors for `value`
+    g_dev = km.nn_descent(ds, km.Metric.L2, km.DescentParams(k=k), CFG["g_seed"], member_ids=s1,
+                          device=local, out_device=True)
+    h_dev = km.nn_descent(ds, km.Metric.L2, km.DescentParams(k=k), CFG["h_seed"], member_ids=s2,
+                          device=local, out_device=True)
+
+    def to_host(gr):
+        out = km.KnnGraph(gr.member_ids, gr.k, gr.metric)
+        out.ids = gr.ids.cpu().numpy()
+        out.dists = gr.dists.cpu().numpy()
+        out.sizes = gr.sizes.cpu().numpy()
+        return out
+
+    g_host, h_host = to_host(g_dev), to_host(h_dev)
+    setup_s = time.perf_counter() - t_setup
+    params = km.MergeParams(k=k, r=CFG["r"], seed=CFG["merge_seed"])
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    def step_device():
+        c = km.DistanceCounter()
+        u = km.s_merge(ds, g_dev, h_dev, params, counter=c, device=local, out_device=True)
+        return c.count, u
+
+    def step_e2e():
+        eng._vectors = None  # force the dataset upload inside the timed region
+        c = km.DistanceCounter()
+        u = km.s_merge(ds, g_host, h_host, params, counter=c, device=local)
+        return c.count, u
+
+    for _ in range(args.warmup):
+        step_device()
+    barrier()
+    eng.reset_stats()
+    eng.set_profiling(True)
+    evals = 0
+    with ClockSampler(local) as clk:
+        eng.mark(0)
+        for _ in range(args.steps):
+            cnt, u_dev = step_device()
+            evals += cnt
+        eng.mark(1)
+        dev_ms = eng.elapsed_ms(0, 1)
+    barrier()
+    st = eng.stats()
+    eng.set_profiling(False)
+    ms_max = dev_ms
+    if world > 1:
+        t = torch.tensor([dev_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms_max = float(t.item())
+    value = world * evals / (ms_max / 1e3)
+
+    # e2e through the public API with host buffers
+    step_e2e()  # warm
+    barrier()
+    eng.reset_stats()
+    e_evals = 0
+    eng.mark(2)
+    for _ in range(args.steps):
+        cnt, u_host = step_e2e()
+        e_evals += cnt
+    eng.mark(3)
+    e_ms = eng.elapsed_ms(2, 3)
+    est = eng.stats()
+    if world > 1:
+        t = torch.tensor([e_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e_ms = float(t.item())
+    e2e = world * e_evals / (e_ms / 1e3)
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
+        return
+
+    # roofline of the dominant kernel (local join): algorithmic bytes / time
+    hbm_peak, peak_kind = peaks()
+    join_s = st["join_ms"] / 1e3
+    join_bytes = 4.0 * CFG["d"] * st["members"] + 24.0 * st["candidates"]
+    achieved = join_bytes / join_s / 1e9 if join_s > 0 else 0.0
+    rec = recall_sample(ds, u_host, local) if not args.no_recall else None
+    cpu = None if args.no_cpu else cpu_baseline()
+    steps = args.steps
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "config2_smerge_2x500k_d128_k20", "n": n, "d": CFG["d"], "k": k,
+                   "r": CFG["r"], "metric": "l2", "rho": 1.0,
+                   "parallelism": f"replicas{world}" if world > 1 else "single",
+                   "l2_note": "inputs (512 MB vectors + lists) exceed the 126 MB L2"},
+        "merge_seconds": ms_max / steps / 1e3,
+        "evals_per_step": evals // steps,
+        "recall_at_10": rec,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None, "peak_kind": peak_kind,
+                     "kernel": "k_join_exact",
+                     "bytes_model": "4*d*sum|M_u| + 24*candidates",
+                     "join_ms_per_step": st["join_ms"] / steps,
+                     "join_share": st["join_ms"] / max(ms_max, 1e-9)},
+        "stats_per_step": {key: st[key] / steps for key in ("candidates", "exact_evals", "members", "accepted", "join_redos", "rounds")},
+        "phases_ms_per_step": {key: st[key] / steps for key in
+                               ("join_ms", "reverse_ms", "assemble_ms", "update_ms", "other_ms")},
+        "e2e": {"value": e2e, "unit": UNIT, "ms_per_step": e_ms / steps,
+                "h2d_bytes_per_step": est["h2d_bytes"] // steps,
+                "d2h_bytes_per_step": est["d2h_bytes"] // steps},
+        "gpu_launches": st["launches"],
+        "clocks": clk.summary(),
+        "setup_seconds": setup_s,
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--scale", type=float, default=1.0, help="fraction of the config size")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    ap.add_argument("--no-recall", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -72,6 +72,10 @@ typedef struct knnm_stats {
     int64_t accepted;      /* accepted list insertions                    */
     int64_t rounds;        /* rounds run                                  */
     int64_t exact_evals;   /* pairs re-evaluated in fp64 after fp32 screen */
+    int64_t launches;      /* kernels launched by this context            */
+    int64_t h2d_bytes;     /* host -> device bytes copied                 */
+    int64_t join_redos;    /* optimistic single-shot joins redone in chunks */
+    int64_t d2h_bytes;     /* device -> host bytes copied                 */
 } knnm_stats;
 
 const char *knnm_last_error(void);
@@ -105,6 +109,12 @@ int knnm_load_graph(knnm_ctx *ctx, const int32_t *rows, int64_t m,
                     const int32_t *g_ids, const double *g_dists,
                     const int32_t *g_sizes, int32_t gk, int32_t k1);
 
+/* As knnm_load_graph, but g_ids / g_dists / g_sizes are device pointers
+ * (graph already resident in HBM, e.g. a torch CUDA tensor). */
+int knnm_load_graph_dev(knnm_ctx *ctx, const int32_t *rows, int64_t m,
+                        const int32_t *g_ids, const double *g_dists,
+                        const int32_t *g_sizes, int32_t gk, int32_t k1);
+
 /* Directed inserts in the given order.  Replaces _eval_pairs +
  * apply_updates_directed (construct.py:86-108; _kernels.py:208-214) as used
  * by _append_random (merge.py:166-176), the raw-row init (merge.py:318-325)
@@ -113,6 +123,26 @@ int knnm_load_graph(knnm_ctx *ctx, const int32_t *rows, int64_t m,
  * If capture is on, the m distances are kept for knnm_capture_fetch. */
 int knnm_insert_directed(knnm_ctx *ctx, const int32_t *rows,
                          const int32_t *nids, int64_t m, int64_t *accepted);
+
+/* knnm_insert_directed with rows[i] repeated `count` times (the
+ * np.repeat(rows, count) target layout of merge.py:173); nids has
+ * mrows*count entries.  The repeat is expanded on the device. */
+int knnm_insert_rows(knnm_ctx *ctx, const int32_t *rows, int64_t mrows,
+                     int32_t count, const int32_t *nids, int64_t *accepted);
+
+/* Random cross-subset append (merge.py:146-176, _sample_pool_rows +
+ * _append_random).  The host makes the PCG64 draws in the reference's order;
+ * the device holds the (nrows, t) draw matrix and reports rows containing a
+ * repeated value (ascending, as np.nonzero does), the host redraws exactly
+ * those rows, and finally the device maps the draws through `pool` (local
+ * ids of the other side) and inserts them into `rows` (targets repeat t
+ * times, apply_updates_directed order).  bad must hold nrows entries. */
+int knnm_draws_load(knnm_ctx *ctx, const int64_t *cand, int64_t nrows,
+                    int32_t t, int64_t *bad, int64_t *nbad);
+int knnm_draws_replace(knnm_ctx *ctx, const int64_t *rows, int64_t nrows,
+                       const int64_t *vals, int64_t *bad, int64_t *nbad);
+int knnm_draws_insert(knnm_ctx *ctx, const int32_t *rows, const int32_t *pool,
+                      int64_t npool, int64_t *accepted);
 
 /* One local-join round.  Replaces one iteration of _descent_rounds
  * (construct.py:136-164): reverse_csr, assemble_neighborhoods (rev_cap),
@@ -134,6 +164,10 @@ int knnm_phi(knnm_ctx *ctx, double *out);
 int knnm_export(knnm_ctx *ctx, int32_t merge_rear, int32_t *out_ids,
                 double *out_dists, int32_t *out_sizes);
 
+/* As knnm_export, but the outputs are device pointers (result stays in HBM). */
+int knnm_export_dev(knnm_ctx *ctx, int32_t merge_rear, int32_t *out_ids,
+                    double *out_dists, int32_t *out_sizes);
+
 /* Download the raw local-id state (for per-iteration parity checks). */
 int knnm_get_state(knnm_ctx *ctx, int32_t *ids, double *dists,
                    uint8_t *flags, int32_t *sizes);
@@ -146,10 +180,26 @@ int knnm_capture_count(knnm_ctx *ctx, int64_t *count);
 int knnm_capture_fetch(knnm_ctx *ctx, int32_t *pa, int32_t *pb, double *pd,
                        int64_t count);
 
+/* Local-join kernel choice: -1 auto (tiled when the hood fits shared
+ * memory), 0 = exact route (fp64 on every pair), 1 = tiled route (fp32
+ * SIMT screen, exact by certificate or by fp64 re-evaluation).  Both give
+ * bit-identical results; the switch exists for tests and measurement. */
+int knnm_set_join_variant(knnm_ctx *ctx, int32_t variant);
+
+/* Dataset facts: cert = 1 when fp32 arithmetic is provably exact for the
+ * uploaded dataset and metric (integer entries, d*range^2 < 2^24 for L2);
+ * dp = padded row length in floats. */
+int knnm_get_info(knnm_ctx *ctx, int32_t *cert, int32_t *dp);
+
 /* Timing / counters. profiling=1 records CUDA events around every phase. */
 int knnm_set_profiling(knnm_ctx *ctx, int32_t on);
 int knnm_get_stats(knnm_ctx *ctx, knnm_stats *out);
 int knnm_reset_stats(knnm_ctx *ctx);
+
+/* Stream-ordered timing: record event `slot` (0..7) on the context stream;
+ * knnm_elapsed waits for slot b and returns the device time b - a in ms. */
+int knnm_mark(knnm_ctx *ctx, int32_t slot);
+int knnm_elapsed(knnm_ctx *ctx, int32_t a, int32_t b, double *ms);
 
 /* Block until all work on the context stream is done. */
 int knnm_sync(knnm_ctx *ctx);

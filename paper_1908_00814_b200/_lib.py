@@ -48,6 +48,10 @@ class KnnmStats(ctypes.Structure):
         ("accepted", I64),
         ("rounds", I64),
         ("exact_evals", I64),
+        ("launches", I64),
+        ("h2d_bytes", I64),
+        ("join_redos", I64),
+        ("d2h_bytes", I64),
     ]
 
     def as_dict(self) -> dict:
@@ -62,17 +66,27 @@ SIGNATURES = {
     "knnm_set_dataset": (ctypes.c_int, [P, P, I64, I32, I32]),
     "knnm_begin": (ctypes.c_int, [P, P, I64, P, I32]),
     "knnm_load_graph": (ctypes.c_int, [P, P, I64, P, P, P, I32, I32]),
+    "knnm_load_graph_dev": (ctypes.c_int, [P, P, I64, P, P, P, I32, I32]),
     "knnm_insert_directed": (ctypes.c_int, [P, P, P, I64, PI64]),
+    "knnm_insert_rows": (ctypes.c_int, [P, P, I64, I32, P, PI64]),
+    "knnm_draws_load": (ctypes.c_int, [P, P, I64, I32, P, PI64]),
+    "knnm_draws_replace": (ctypes.c_int, [P, P, I64, P, P, PI64]),
+    "knnm_draws_insert": (ctypes.c_int, [P, P, P, I64, PI64]),
     "knnm_round": (ctypes.c_int, [P, I32, I32, U64, PI64, PI64]),
     "knnm_phi": (ctypes.c_int, [P, PDBL]),
     "knnm_export": (ctypes.c_int, [P, I32, P, P, P]),
+    "knnm_export_dev": (ctypes.c_int, [P, I32, P, P, P]),
     "knnm_get_state": (ctypes.c_int, [P, P, P, P, P]),
     "knnm_set_capture": (ctypes.c_int, [P, I32]),
     "knnm_capture_count": (ctypes.c_int, [P, PI64]),
     "knnm_capture_fetch": (ctypes.c_int, [P, P, P, P, I64]),
+    "knnm_set_join_variant": (ctypes.c_int, [P, I32]),
+    "knnm_get_info": (ctypes.c_int, [P, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
     "knnm_set_profiling": (ctypes.c_int, [P, I32]),
     "knnm_get_stats": (ctypes.c_int, [P, ctypes.POINTER(KnnmStats)]),
     "knnm_reset_stats": (ctypes.c_int, [P]),
+    "knnm_mark": (ctypes.c_int, [P, I32]),
+    "knnm_elapsed": (ctypes.c_int, [P, I32, I32, PDBL]),
     "knnm_sync": (ctypes.c_int, [P]),
 }
 

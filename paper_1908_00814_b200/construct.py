@@ -92,6 +92,17 @@ def _insert_directed(engine, rows, nids, counter, on_pair, gids) -> int:
     return acc
 
 
+def _insert_rows(engine, rows, count, nids, counter, on_pair, gids) -> int:
+    """Directed inserts with targets np.repeat(rows, count) (merge.py:173)."""
+    m = int(np.asarray(nids).shape[0])
+    if m == 0:
+        return 0
+    acc = engine.insert_rows(rows, count, nids)
+    counter.add(m)
+    _emit_captured(engine, on_pair, gids)
+    return acc
+
+
 def _descent_rounds(engine, n: int, mode: int, k: int, params, rng, counter, on_pair, gids,
                     report: BuildReport | None, rev_cap: int | None = None) -> None:
     """construct.py:111-179 on the device engine (state already loaded)."""
@@ -160,7 +171,8 @@ def _capture(engine, on_pair) -> None:
 
 def nn_descent(dataset: Dataset, metric: Metric, params: DescentParams, seed: int,
                member_ids=None, counter: DistanceCounter | None = None, on_pair=None,
-               return_report: bool = False, device: int | None = None):
+               return_report: bool = False, device: int | None = None,
+               out_device: bool = False):
     """NN-Descent from a random initial graph (construct.py:226-270)."""
     metric = Metric(metric)
     metric.check_kind(dataset.kind)
@@ -180,12 +192,11 @@ def nn_descent(dataset: Dataset, metric: Metric, params: DescentParams, seed: in
     _capture(eng, on_pair)
     try:
         cand = _random_lists(rng, n, k)
-        rows = np.repeat(np.arange(n, dtype=np.int32), k)
-        nids = cand.ravel().astype(np.int32)
-        _insert_directed(eng, rows, nids, counter, on_pair, gids)
+        _insert_rows(eng, np.arange(n, dtype=np.int32), k, cand.ravel().astype(np.int32),
+                     counter, on_pair, gids)
         report = BuildReport(phi_initial=eng.phi())
         _descent_rounds(eng, n, MODE_ALL, k, params, rng, counter, on_pair, gids, report)
-        ids, dists, sizes = eng.export(merge_rear=False)
+        ids, dists, sizes = eng.export(merge_rear=False, on_device=out_device)
     finally:
         eng.set_capture(False)
     graph = _graph_from(gids, k, metric, ids, dists, sizes)

@@ -36,7 +36,11 @@ int fail(int code, const char *fmt, ...) {
             return fail(e_ == cudaErrorMemoryAllocation ? KNNM_ERR_NOMEM : KNNM_ERR_CUDA, \
                         "%s:%d %s: %s", __FILE__, __LINE__, #x, cudaGetErrorString(e_));  \
     } while (0)
-#define CKL() CK(cudaGetLastError())
+#define CKL()                     \
+    do {                          \
+        CK(cudaGetLastError());   \
+        c->stats.launches += 1;   \
+    } while (0)
 #define TRY(...)                \
     do {                        \
         int r_ = (__VA_ARGS__); \
@@ -93,6 +97,8 @@ struct knnm_ctx {
     int64_t n_all = 0;
     int d = 0, dp = 0, metric = 1;
     bool have_data = false;
+    bool cert = false;  // fp32 arithmetic is exact for this dataset + metric
+    int join_variant = -1;  // -1 auto, 0 exact (fp64 every pair), 1 tiled
     // current merge
     DBuf sub, ugid, labels;
     const float *subp = nullptr;
@@ -106,10 +112,13 @@ struct knnm_ctx {
     // round scratch
     DBuf indeg, roff, rev, heavy, giant, gscratch32, nbh, nlen, hpairs, poff, worst0, active;
     DBuf tcnt, toff, candA, candB, heavy_rows, gscratch64;
+    DBuf draws, draw_rows, draw_bad, pool;  // random-append draw matrix (device)
+    int64_t draw_n = 0;
+    int draw_t = 0;
     DBuf scan_tmp[4], scan_off[4];
     DBuf counters;
     unsigned long long cap = 0;  // candidate record capacity
-    size_t cand_budget_bytes = (size_t)16 << 30;
+    size_t cand_budget_bytes = (size_t)40 << 30;
     // staging
     DBuf stage[4];
     unsigned long long *hcnt = nullptr;  // pinned mirror of counters
@@ -128,6 +137,7 @@ struct knnm_ctx {
     std::vector<cudaEvent_t> ev_pool;
     double phase_ms[PH_NUM] = {0, 0, 0, 0, 0};
     knnm_stats stats{};
+    cudaEvent_t marks[8] = {};
 };
 
 namespace {
@@ -178,9 +188,22 @@ int grid_for(knnm_ctx *c, int64_t work, int threads, int per_sm = 8) {
     return (int)g;
 }
 
+int h2d(knnm_ctx *c, void *dst, const void *src, size_t bytes) {
+    if (bytes == 0) return KNNM_OK;
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->st));
+    c->stats.h2d_bytes += (int64_t)bytes;
+    return KNNM_OK;
+}
+
+int d2h(knnm_ctx *c, void *dst, const void *src, size_t bytes) {
+    if (bytes == 0) return KNNM_OK;
+    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->st));
+    c->stats.d2h_bytes += (int64_t)bytes;
+    return KNNM_OK;
+}
+
 int sync_counters(knnm_ctx *c) {
-    CK(cudaMemcpyAsync(c->hcnt, c->counters.p, sizeof(unsigned long long) * C_NUM,
-                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(c->hcnt, c->counters.p, sizeof(unsigned long long) * C_NUM, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     return KNNM_OK;
 }
@@ -221,10 +244,10 @@ int run_updates(knnm_ctx *c, uint64_t key_max) {
     TRY(scan<uint32_t, uint32_t>(c, c->tcnt.as<uint32_t>(), c->toff.as<uint32_t>(), n));
     unsigned long long *cnt = c->counters.as<unsigned long long>();
     // scatter (count read on device through a pinned-free path: copy scalar first)
-    CK(cudaMemcpyAsync(c->hcnt, c->counters.p, sizeof(unsigned long long) * C_NUM,
-                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(c->hcnt, c->counters.p, sizeof(unsigned long long) * C_NUM, cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     unsigned long long ncand = c->hcnt[C_CAND];
+    c->stats.exact_evals += (int64_t)c->hcnt[C_EXACT];
     if (c->hcnt[C_OVERFLOW]) return fail(KNNM_ERR_LIMIT, "candidate buffer overflow");
     c->stats.candidates += (int64_t)ncand;
     if (ncand == 0) return KNNM_OK;
@@ -233,37 +256,43 @@ int run_updates(knnm_ctx *c, uint64_t key_max) {
         c->candB.as<CandB>());
     CKL();
     CK(cudaMemsetAsync(cnt + C_HEAVY_APPLY, 0, sizeof(unsigned long long) * 2, c->st));
+    CK(cudaMemsetAsync(cnt + C_MAXC, 0, sizeof(unsigned long long), c->st));
     int E = (c->k + 31) / 32;
     int blocks = grid_for(c, n * 32, APPLY_WARPS * 32, 16);
-    size_t hsm = sizeof(uint64_t) * BLOCK_SORT_MAX;
-    if (E == 1) {
+    if (E == 1)
         k_apply<1><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
             n, c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(), ib, c->ids.as<int32_t>(),
             c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
             c->heavy_rows.as<int32_t>(), cnt);
-        CKL();
-        k_apply_heavy<1><<<c->sms, 256, hsm, c->st>>>(
-            c->heavy_rows.as<int32_t>(), c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(), ib,
-            c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
-            c->sizes.as<int32_t>(), cnt, nullptr, BLOCK_SORT_MAX, c->giant.as<int32_t>());
-        CKL();
-    } else {
+    else
         k_apply<2><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
             n, c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(), ib, c->ids.as<int32_t>(),
             c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
             c->heavy_rows.as<int32_t>(), cnt);
-        CKL();
-        k_apply_heavy<2><<<c->sms, 256, hsm, c->st>>>(
+    CKL();
+    TRY(sync_counters(c));
+    unsigned long long nheavy = c->hcnt[C_HEAVY_APPLY];
+    if (nheavy == 0) return KNNM_OK;
+    unsigned long long maxc = c->hcnt[C_MAXC];
+    if (bits_for(maxc) > ib) return fail(KNNM_ERR_LIMIT, "row with %llu candidates", maxc);
+    uint32_t p2 = next_pow2((uint32_t)maxc);
+    uint32_t smem_elems = std::min<uint32_t>(p2, (uint32_t)BLOCK_SORT_MAX);
+    size_t hsm = sizeof(uint64_t) * smem_elems;
+    int per_sm = std::max(1, (int)((200u * 1024u) / std::max<size_t>(hsm, 1)));
+    int hgrid = (int)std::min<unsigned long long>(nheavy, (unsigned long long)c->sms * per_sm);
+    if (E == 1)
+        k_apply_heavy<1><<<hgrid, 256, hsm, c->st>>>(
             c->heavy_rows.as<int32_t>(), c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(), ib,
             c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
-            c->sizes.as<int32_t>(), cnt, nullptr, BLOCK_SORT_MAX, c->giant.as<int32_t>());
-        CKL();
-    }
-    TRY(sync_counters(c));
-    if (c->hcnt[C_GIANT_APPLY]) {
-        unsigned long long maxc = c->hcnt[C_MAXC];
-        if (bits_for(maxc) > ib) return fail(KNNM_ERR_LIMIT, "row with %llu candidates", maxc);
-        TRY(ensure(c->gscratch64, sizeof(uint64_t) * next_pow2((uint32_t)maxc)));
+            c->sizes.as<int32_t>(), cnt, nullptr, (int)smem_elems, c->giant.as<int32_t>());
+    else
+        k_apply_heavy<2><<<hgrid, 256, hsm, c->st>>>(
+            c->heavy_rows.as<int32_t>(), c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(), ib,
+            c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
+            c->sizes.as<int32_t>(), cnt, nullptr, (int)smem_elems, c->giant.as<int32_t>());
+    CKL();
+    if (p2 > (uint32_t)BLOCK_SORT_MAX) {
+        TRY(ensure(c->gscratch64, sizeof(uint64_t) * p2));
         if (E == 1)
             k_apply_heavy<1><<<1, 1024, 0, c->st>>>(
                 c->heavy_rows.as<int32_t>(), c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(),
@@ -369,6 +398,9 @@ int knnm_create(int device, knnm_ctx **out) {
                             (int)(sizeof(uint64_t) * BLOCK_SORT_MAX)));
     for (auto f : {k_join_exact<0>, k_join_exact<1>, k_join_exact<2>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (auto f : {k_join_tiled<0, false>, k_join_tiled<1, false>, k_join_tiled<2, false>,
+                   k_join_tiled<0, true>, k_join_tiled<1, true>})
+        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     *out = c;
     return KNNM_OK;
 }
@@ -381,7 +413,8 @@ int knnm_destroy(knnm_ctx *c) {
                    &c->sizes, &c->tail_ids, &c->tail_d, &c->tail_s, &c->indeg, &c->roff,
                    &c->rev, &c->heavy, &c->giant, &c->gscratch32, &c->nbh, &c->nlen, &c->hpairs,
                    &c->poff, &c->worst0, &c->active, &c->tcnt, &c->toff, &c->candA, &c->candB,
-                   &c->heavy_rows, &c->gscratch64, &c->counters, &c->out_ids, &c->out_d,
+                   &c->heavy_rows, &c->gscratch64, &c->counters, &c->draws, &c->draw_rows,
+                   &c->draw_bad, &c->pool, &c->out_ids, &c->out_d,
                    &c->out_s, &c->phi_leaf_lo, &c->phi_leaf_len, &c->phi_left, &c->phi_right,
                    &c->phi_level, &c->phi_leaves, &c->phi_inner};
     for (DBuf *b : all) release(*b);
@@ -393,6 +426,8 @@ int knnm_destroy(knnm_ctx *c) {
         cudaEventDestroy(p.second.second);
     }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    for (auto e : c->marks)
+        if (e) cudaEventDestroy(e);
     if (c->hcnt) cudaFreeHost(c->hcnt);
     cudaStreamDestroy(c->st);
     delete c;
@@ -408,12 +443,10 @@ int knnm_set_dataset(knnm_ctx *c, const float *vectors, int64_t n_all, int32_t d
     int dp = (d + 3) & ~3;
     TRY(ensure(c->vec, sizeof(float) * (size_t)n_all * dp));
     if (dp == d) {
-        CK(cudaMemcpyAsync(c->vec.p, vectors, sizeof(float) * (size_t)n_all * d,
-                           cudaMemcpyHostToDevice, c->st));
+        TRY(h2d(c, c->vec.p, vectors, sizeof(float) * (size_t)n_all * d));
     } else {
         TRY(ensure(c->stage[0], sizeof(float) * (size_t)n_all * d));
-        CK(cudaMemcpyAsync(c->stage[0].p, vectors, sizeof(float) * (size_t)n_all * d,
-                           cudaMemcpyHostToDevice, c->st));
+        TRY(h2d(c, c->stage[0].p, vectors, sizeof(float) * (size_t)n_all * d));
         k_pad_rows<<<grid_for(c, n_all * dp, 256), 256, 0, c->st>>>(
             c->stage[0].as<float>(), d, dp, n_all, c->vec.as<float>());
         CKL();
@@ -423,6 +456,31 @@ int knnm_set_dataset(knnm_ctx *c, const float *vectors, int64_t n_all, int32_t d
     c->dp = dp;
     c->metric = metric;
     c->have_data = true;
+    // exactness certificate: integer entries and d * range^2 < 2^24 (L2) or
+    // d * range < 2^24 (L1) make every fp32 partial sum an exact integer
+    {
+        unsigned long long *cnt = c->counters.as<unsigned long long>();
+        unsigned long long init[3] = {0ull, 0ull, 0xffffffffull};
+        CK(cudaMemcpyAsync(cnt + C_NUM - 3, init, sizeof(init), cudaMemcpyHostToDevice, c->st));
+        k_data_stats<<<grid_for(c, n_all * dp, 256), 256, 0, c->st>>>(c->vec.as<float>(),
+                                                                      n_all * dp, cnt + C_NUM - 3);
+        CKL();
+        TRY(sync_counters(c));
+        auto unkey = [](unsigned long long k) {
+            uint32_t kk = (uint32_t)k;
+            uint32_t b = (kk & 0x80000000u) ? (kk & 0x7fffffffu) : ~kk;
+            float f;
+            memcpy(&f, &b, 4);
+            return (double)f;
+        };
+        double mx = unkey(c->hcnt[C_NUM - 2]), mn = unkey(c->hcnt[C_NUM - 1]);
+        bool ints = c->hcnt[C_NUM - 3] == 0;
+        double range = mx - mn;
+        c->cert = false;
+        if (ints && metric == KNNM_L2) c->cert = (double)d * range * range < 16777216.0;
+        if (ints && metric == KNNM_L1) c->cert = (double)d * range < 16777216.0;
+        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
+    }
     c->begun = false;
     return KNNM_OK;
 }
@@ -440,7 +498,7 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     c->n = n;
     c->k = k;
     TRY(ensure(c->ugid, sizeof(int64_t) * n));
-    CK(cudaMemcpyAsync(c->ugid.p, union_gids, sizeof(int64_t) * n, cudaMemcpyHostToDevice, c->st));
+    TRY(h2d(c, c->ugid.p, union_gids, sizeof(int64_t) * n));
     bool identity = (n == c->n_all && union_gids[0] == 0 && union_gids[n - 1] == n - 1);
     if (identity) {
         c->subp = c->vec.as<float>();
@@ -452,7 +510,7 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
         c->subp = c->sub.as<float>();
     }
     TRY(ensure(c->labels, n));
-    CK(cudaMemcpyAsync(c->labels.p, labels, n, cudaMemcpyHostToDevice, c->st));
+    TRY(h2d(c, c->labels.p, labels, n));
     size_t nk = (size_t)n * k;
     TRY(ensure(c->ids, sizeof(int32_t) * nk));
     TRY(ensure(c->dists, sizeof(double) * nk));
@@ -486,8 +544,9 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     return KNNM_OK;
 }
 
-int knnm_load_graph(knnm_ctx *c, const int32_t *rows, int64_t m, const int32_t *g_ids,
-                    const double *g_dists, const int32_t *g_sizes, int32_t gk, int32_t k1) {
+static int load_impl(knnm_ctx *c, const int32_t *rows, int64_t m, const int32_t *g_ids,
+                     const double *g_dists, const int32_t *g_sizes, int32_t gk, int32_t k1,
+                     bool on_device) {
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     if (m == 0) return KNNM_OK;
@@ -511,21 +570,27 @@ int knnm_load_graph(knnm_ctx *c, const int32_t *rows, int64_t m, const int32_t *
             c->have_tail = true;
         }
     }
-    size_t mg = (size_t)m * (gk > 0 ? gk : 1);
+    const int32_t *gi = g_ids, *gs = g_sizes;
+    const double *gd = g_dists;
     TRY(ensure(c->stage[0], sizeof(int32_t) * m));
-    TRY(ensure(c->stage[1], sizeof(int32_t) * mg));
-    TRY(ensure(c->stage[2], sizeof(double) * mg));
-    TRY(ensure(c->stage[3], sizeof(int32_t) * m));
-    CK(cudaMemcpyAsync(c->stage[0].p, rows, sizeof(int32_t) * m, cudaMemcpyHostToDevice, c->st));
-    if (gk > 0) {
-        CK(cudaMemcpyAsync(c->stage[1].p, g_ids, sizeof(int32_t) * m * gk, cudaMemcpyHostToDevice, c->st));
-        CK(cudaMemcpyAsync(c->stage[2].p, g_dists, sizeof(double) * m * gk, cudaMemcpyHostToDevice, c->st));
+    TRY(h2d(c, c->stage[0].p, rows, sizeof(int32_t) * m));
+    if (!on_device) {
+        size_t mg = (size_t)m * (gk > 0 ? gk : 1);
+        TRY(ensure(c->stage[1], sizeof(int32_t) * mg));
+        TRY(ensure(c->stage[2], sizeof(double) * mg));
+        TRY(ensure(c->stage[3], sizeof(int32_t) * m));
+        if (gk > 0) {
+            TRY(h2d(c, c->stage[1].p, g_ids, sizeof(int32_t) * m * gk));
+            TRY(h2d(c, c->stage[2].p, g_dists, sizeof(double) * m * gk));
+        }
+        TRY(h2d(c, c->stage[3].p, g_sizes, sizeof(int32_t) * m));
+        gi = c->stage[1].as<int32_t>();
+        gd = c->stage[2].as<double>();
+        gs = c->stage[3].as<int32_t>();
     }
-    CK(cudaMemcpyAsync(c->stage[3].p, g_sizes, sizeof(int32_t) * m, cudaMemcpyHostToDevice, c->st));
     if (gk > 0) {
         k_load_graph<<<grid_for(c, m * gk, 256), 256, 0, c->st>>>(
-            c->stage[0].as<int32_t>(), m, c->stage[1].as<int32_t>(), c->stage[2].as<double>(),
-            c->stage[3].as<int32_t>(), gk, k1, c->k, c->ugid.as<int64_t>(), c->n,
+            c->stage[0].as<int32_t>(), m, gi, gd, gs, gk, k1, c->k, c->ugid.as<int64_t>(), c->n,
             c->ids.as<int32_t>(), c->dists.as<double>(), c->sizes.as<int32_t>(),
             tk > 0 ? c->tail_ids.as<int32_t>() : nullptr, tk > 0 ? c->tail_d.as<double>() : nullptr,
             tk > 0 ? c->tail_s.as<int32_t>() : nullptr, tk);
@@ -535,19 +600,37 @@ int knnm_load_graph(knnm_ctx *c, const int32_t *rows, int64_t m, const int32_t *
     return KNNM_OK;
 }
 
-int knnm_insert_directed(knnm_ctx *c, const int32_t *rows, const int32_t *nids, int64_t m,
-                         int64_t *accepted) {
+int knnm_load_graph(knnm_ctx *c, const int32_t *rows, int64_t m, const int32_t *g_ids,
+                    const double *g_dists, const int32_t *g_sizes, int32_t gk, int32_t k1) {
+    return load_impl(c, rows, m, g_ids, g_dists, g_sizes, gk, k1, false);
+}
+
+int knnm_load_graph_dev(knnm_ctx *c, const int32_t *rows, int64_t m, const int32_t *g_ids,
+                        const double *g_dists, const int32_t *g_sizes, int32_t gk, int32_t k1) {
+    return load_impl(c, rows, m, g_ids, g_dists, g_sizes, gk, k1, true);
+}
+
+static int insert_impl(knnm_ctx *c, const int32_t *rows, int64_t mrows, int32_t count,
+                       const int32_t *nids, int64_t m, int64_t *accepted, bool nids_on_device) {
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     if (accepted) *accepted = 0;
     if (m == 0) return KNNM_OK;
-    if (!rows || !nids) return fail(KNNM_ERR_ARG, "null argument");
+    if (!rows || (!nids && !nids_on_device)) return fail(KNNM_ERR_ARG, "null argument");
     CK(cudaSetDevice(c->device));
     TRY(ensure_candidates(c, (unsigned long long)m));
     TRY(ensure(c->stage[0], sizeof(int32_t) * m));
     TRY(ensure(c->stage[1], sizeof(int32_t) * m));
-    CK(cudaMemcpyAsync(c->stage[0].p, rows, sizeof(int32_t) * m, cudaMemcpyHostToDevice, c->st));
-    CK(cudaMemcpyAsync(c->stage[1].p, nids, sizeof(int32_t) * m, cudaMemcpyHostToDevice, c->st));
+    if (count > 0) {
+        TRY(ensure(c->stage[3], sizeof(int32_t) * mrows));
+        TRY(h2d(c, c->stage[3].p, rows, sizeof(int32_t) * mrows));
+        k_repeat_rows<<<grid_for(c, m, 256), 256, 0, c->st>>>(c->stage[3].as<int32_t>(), count, m,
+                                                             c->stage[0].as<int32_t>());
+        CKL();
+    } else {
+        TRY(h2d(c, c->stage[0].p, rows, sizeof(int32_t) * m));
+    }
+    if (!nids_on_device) TRY(h2d(c, c->stage[1].p, nids, sizeof(int32_t) * m));
     double *capd = nullptr;
     if (c->capture) {
         TRY(ensure(c->stage[2], sizeof(double) * m));
@@ -580,14 +663,112 @@ int knnm_insert_directed(knnm_ctx *c, const int32_t *rows, const int32_t *nids, 
         c->cap_pa.resize(o + m);
         c->cap_pb.resize(o + m);
         c->cap_pd.resize(o + m);
-        memcpy(c->cap_pa.data() + o, rows, sizeof(int32_t) * m);
-        memcpy(c->cap_pb.data() + o, nids, sizeof(int32_t) * m);
-        CK(cudaMemcpyAsync(c->cap_pd.data() + o, capd, sizeof(double) * m, cudaMemcpyDeviceToHost, c->st));
+        if (count > 0) {
+            for (int64_t i = 0; i < m; i++) c->cap_pa[o + i] = rows[i / count];
+        } else {
+            memcpy(c->cap_pa.data() + o, rows, sizeof(int32_t) * m);
+        }
+        if (nids_on_device)
+            TRY(d2h(c, c->cap_pb.data() + o, c->stage[1].p, sizeof(int32_t) * m));
+        else
+            memcpy(c->cap_pb.data() + o, nids, sizeof(int32_t) * m);
+        TRY(d2h(c, c->cap_pd.data() + o, capd, sizeof(double) * m));
         CK(cudaStreamSynchronize(c->st));
     }
     TRY(resolve_timers(c));
     if (accepted) *accepted = acc_total;
     return KNNM_OK;
+}
+
+int knnm_insert_directed(knnm_ctx *c, const int32_t *rows, const int32_t *nids, int64_t m,
+                         int64_t *accepted) {
+    return insert_impl(c, rows, m, 0, nids, m, accepted, false);
+}
+
+int knnm_insert_rows(knnm_ctx *c, const int32_t *rows, int64_t mrows, int32_t count,
+                     const int32_t *nids, int64_t *accepted) {
+    if (count < 0) return fail(KNNM_ERR_ARG, "negative count");
+    if (count == 0 || mrows == 0) {
+        if (accepted) *accepted = 0;
+        return KNNM_OK;
+    }
+    return insert_impl(c, rows, mrows, count, nids, mrows * (int64_t)count, accepted, false);
+}
+
+static int insert_impl(knnm_ctx *c, const int32_t *rows, int64_t mrows, int32_t count,
+                       const int32_t *nids, int64_t m, int64_t *accepted, bool nids_on_device);
+
+static int dup_check(knnm_ctx *c, const int64_t *rows_dev, int64_t nchk, int64_t *bad_out,
+                     int64_t *nbad) {
+    unsigned long long *cnt = c->counters.as<unsigned long long>();
+    CK(cudaMemsetAsync(cnt + C_CAND, 0, sizeof(unsigned long long), c->st));
+    int64_t work = rows_dev ? nchk : c->draw_n;
+    k_dup_rows<<<grid_for(c, work, 256), 256, 0, c->st>>>(c->draws.as<int64_t>(), c->draw_n,
+                                                           c->draw_t, rows_dev, nchk,
+                                                           c->draw_bad.as<int64_t>(), cnt);
+    CKL();
+    TRY(sync_counters(c));
+    int64_t nb = (int64_t)c->hcnt[C_CAND];
+    if (nb > 0) {
+        CK(cudaMemcpyAsync(bad_out, c->draw_bad.p, sizeof(int64_t) * nb, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        std::sort(bad_out, bad_out + nb);  // np.nonzero order: ascending rows
+    }
+    *nbad = nb;
+    return KNNM_OK;
+}
+
+int knnm_draws_load(knnm_ctx *c, const int64_t *cand, int64_t nrows, int32_t t, int64_t *bad,
+                    int64_t *nbad) {
+    if (!c || !cand || !bad || !nbad || nrows < 0 || t < 1) return fail(KNNM_ERR_ARG, "bad argument");
+    CK(cudaSetDevice(c->device));
+    PhaseTimer pt(c, PH_OTHER);
+    size_t m = (size_t)nrows * t;
+    TRY(ensure(c->draws, sizeof(int64_t) * m));
+    TRY(ensure(c->draw_bad, sizeof(int64_t) * (nrows + 1)));
+    TRY(ensure(c->draw_rows, sizeof(int64_t) * (nrows + 1)));
+    TRY(h2d(c, c->draws.p, cand, sizeof(int64_t) * m));
+    c->draw_n = nrows;
+    c->draw_t = t;
+    return dup_check(c, nullptr, 0, bad, nbad);
+}
+
+int knnm_draws_replace(knnm_ctx *c, const int64_t *rows, int64_t nrows, const int64_t *vals,
+                       int64_t *bad, int64_t *nbad) {
+    if (!c || !rows || !vals || !bad || !nbad) return fail(KNNM_ERR_ARG, "bad argument");
+    if (nrows > c->draw_n) return fail(KNNM_ERR_ARG, "too many rows");
+    CK(cudaSetDevice(c->device));
+    PhaseTimer pt(c, PH_OTHER);
+    if (nrows == 0) {
+        *nbad = 0;
+        return KNNM_OK;
+    }
+    TRY(ensure(c->stage[2], sizeof(int64_t) * (size_t)nrows * c->draw_t));
+    TRY(h2d(c, c->draw_rows.p, rows, sizeof(int64_t) * nrows));
+    TRY(h2d(c, c->stage[2].p, vals, sizeof(int64_t) * (size_t)nrows * c->draw_t));
+    k_put_rows<<<grid_for(c, nrows * c->draw_t, 256), 256, 0, c->st>>>(
+        c->draws.as<int64_t>(), c->draw_t, c->draw_rows.as<int64_t>(), nrows, c->stage[2].as<int64_t>());
+    CKL();
+    return dup_check(c, c->draw_rows.as<int64_t>(), nrows, bad, nbad);
+}
+
+int knnm_draws_insert(knnm_ctx *c, const int32_t *rows, const int32_t *pool, int64_t npool,
+                      int64_t *accepted) {
+    if (!c || !rows || !pool) return fail(KNNM_ERR_ARG, "bad argument");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    CK(cudaSetDevice(c->device));
+    int64_t m = c->draw_n * c->draw_t;
+    if (m == 0) {
+        if (accepted) *accepted = 0;
+        return KNNM_OK;
+    }
+    TRY(ensure(c->pool, sizeof(int32_t) * npool));
+    TRY(h2d(c, c->pool.p, pool, sizeof(int32_t) * npool));
+    TRY(ensure(c->stage[1], sizeof(int32_t) * m));
+    k_pool_map<<<grid_for(c, m, 256), 256, 0, c->st>>>(c->draws.as<int64_t>(), m, c->pool.as<int32_t>(),
+                                                         c->stage[1].as<int32_t>());
+    CKL();
+    return insert_impl(c, rows, c->draw_n, c->draw_t, nullptr, m, accepted, true);
 }
 
 int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, int64_t *pairs,
@@ -642,10 +823,8 @@ int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, 
         TRY(scan<uint32_t, uint64_t>(c, c->hpairs.as<uint32_t>(), c->poff.as<uint64_t>(), n));
     }
     uint64_t P = 0;
-    CK(cudaMemcpyAsync(&c->hcnt[C_NUM - 1], c->poff.as<uint64_t>() + n, sizeof(uint64_t),
-                       cudaMemcpyDeviceToHost, c->st));
-    CK(cudaMemcpyAsync(c->hcnt, c->counters.p, sizeof(unsigned long long) * (C_NUM - 1),
-                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(&c->hcnt[C_NUM - 1], c->poff.as<uint64_t>() + n, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
+    CK(cudaMemcpyAsync(c->hcnt, c->counters.p, sizeof(unsigned long long) * (C_NUM - 1), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     P = c->hcnt[C_NUM - 1];
     unsigned long long nactive = c->hcnt[C_ACTIVE];
@@ -667,9 +846,9 @@ int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, 
         c->cap_pa.resize(o + P);
         c->cap_pb.resize(o + P);
         c->cap_pd.resize(o + P);
-        CK(cudaMemcpyAsync(c->cap_pa.data() + o, pa.p, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaMemcpyAsync(c->cap_pb.data() + o, pb.p, sizeof(int32_t) * P, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaMemcpyAsync(c->cap_pd.data() + o, pd.p, sizeof(double) * P, cudaMemcpyDeviceToHost, c->st));
+        TRY(d2h(c, c->cap_pa.data() + o, pa.p, sizeof(int32_t) * P));
+        TRY(d2h(c, c->cap_pb.data() + o, pb.p, sizeof(int32_t) * P));
+        TRY(d2h(c, c->cap_pd.data() + o, pd.p, sizeof(double) * P));
         CK(cudaStreamSynchronize(c->st));
         release(pa);
         release(pb);
@@ -681,9 +860,42 @@ int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, 
         TRY(ensure_candidates(c, 2 * P));
         uint64_t key_max = ((uint64_t)n * W) * W;
         size_t smem = sizeof(float) * (size_t)W * c->dp;
+        size_t smem_tiled = sizeof(float) * (size_t)W * (c->dp + 4);
         if (smem > 200 * 1024) return fail(KNNM_ERR_LIMIT, "neighbourhood of %d x %d floats exceeds shared memory", W, c->dp);
+        const bool tiled = c->join_variant == 1 || (c->join_variant < 0 && smem_tiled <= 96 * 1024);
+        const double mrel = 1.0 + (double)(c->d + 8) * ldexp(1.0, -23);
+        const double mabs = (double)(4 * c->d + 64) * ldexp(1.0, -24);
         auto launch_join = [&](const int32_t *act, unsigned nblocks) -> int {
             PhaseTimer pt(c, PH_JOIN);
+            if (tiled) {
+                const void *fn;
+                if (c->metric == 1) fn = c->cert ? (const void *)k_join_tiled<1, true> : (const void *)k_join_tiled<1, false>;
+                else if (c->metric == 2) fn = (const void *)k_join_tiled<2, false>;
+                else fn = c->cert ? (const void *)k_join_tiled<0, true> : (const void *)k_join_tiled<0, false>;
+                int per_sm = 1;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TJ_THREADS, smem_tiled));
+                unsigned grid = (unsigned)std::min<int64_t>((int64_t)nblocks, (int64_t)c->sms * std::max(per_sm, 1));
+                if (grid == 0) grid = 1;
+                int na = (int)nblocks;
+#define KNNM_TJ_ARGS                                                                          \
+    act, na, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,  \
+        c->subp, c->dp, c->d, c->worst0.as<double>(), c->candA.as<CandA>(), c->cap,          \
+        c->tcnt.as<uint32_t>(), cnt, mrel, mabs
+                if (c->metric == 1 && c->cert)
+                    k_join_tiled<1, true><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+                else if (c->metric == 1)
+                    k_join_tiled<1, false><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+                else if (c->metric == 2)
+                    k_join_tiled<2, false><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+                else if (c->cert)
+                    k_join_tiled<0, true><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+                else
+                    k_join_tiled<0, false><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+#undef KNNM_TJ_ARGS
+                CKL();
+                c->stats.join_launches += 1;
+                return KNNM_OK;
+            }
             if (c->metric == 1)
                 k_join_exact<1><<<nblocks, JOIN_THREADS, smem, c->st>>>(
                     act, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,
@@ -703,20 +915,32 @@ int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, 
             c->stats.join_launches += 1;
             return KNNM_OK;
         };
-        if (2 * P <= c->cap) {
+        bool done = false;
+        {
+            // Single shot over all active hoods.  Guaranteed to fit when
+            // 2P <= cap; otherwise optimistic (the exact prefilter keeps far
+            // fewer than 2P candidates) with a chunked redo on overflow --
+            // the lists are untouched until the apply phase, so a redo is safe.
             TRY(launch_join(c->active.as<int32_t>(), (unsigned)nactive));
-            {
-                PhaseTimer pt(c, PH_UPDATE);
-                TRY(run_updates(c, key_max));
-            }
             TRY(sync_counters(c));
-            acc_total = (int64_t)c->hcnt[C_ACCEPTED];
-        } else {
+            if (c->hcnt[C_CAND] <= c->cap) {
+                {
+                    PhaseTimer pt(c, PH_UPDATE);
+                    TRY(run_updates(c, key_max));
+                }
+                TRY(sync_counters(c));
+                acc_total = (int64_t)c->hcnt[C_ACCEPTED];
+                done = true;
+            } else {
+                c->stats.join_redos += 1;
+                CK(cudaMemsetAsync(c->tcnt.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+            }
+        }
+        if (!done) {
             // Chunk hoods by index so each chunk's worst case fits; chunks run
             // in ascending hood order, preserving the reference's per-row order.
             std::vector<uint64_t> hpoff(n + 1);
-            CK(cudaMemcpyAsync(hpoff.data(), c->poff.p, sizeof(uint64_t) * (n + 1),
-                               cudaMemcpyDeviceToHost, c->st));
+            TRY(d2h(c, hpoff.data(), c->poff.p, sizeof(uint64_t) * (n + 1)));
             CK(cudaStreamSynchronize(c->st));
             // the compacted list is not ordered; build per-chunk lists on host
             std::vector<uint32_t> hh(n);
@@ -794,17 +1018,16 @@ int knnm_phi(knnm_ctx *c, double *out) {
                                           (int)c->phi.level_start.size() - 1,
                                           c->phi_leaves.as<double>(), c->phi_inner.as<double>());
         CKL();
-        CK(cudaMemcpyAsync(out, c->phi_inner.as<double>() + (ni - 1), sizeof(double),
-                           cudaMemcpyDeviceToHost, c->st));
+        TRY(d2h(c, out, c->phi_inner.as<double>() + (ni - 1), sizeof(double)));
     } else {
-        CK(cudaMemcpyAsync(out, c->phi_leaves.p, sizeof(double), cudaMemcpyDeviceToHost, c->st));
+        TRY(d2h(c, out, c->phi_leaves.p, sizeof(double)));
     }
     CK(cudaStreamSynchronize(c->st));
     return KNNM_OK;
 }
 
-int knnm_export(knnm_ctx *c, int32_t merge_rear, int32_t *out_ids, double *out_dists,
-                int32_t *out_sizes) {
+static int export_impl(knnm_ctx *c, int32_t merge_rear, int32_t *out_ids, double *out_dists,
+                       int32_t *out_sizes, bool on_device) {
     if (!c || !out_ids || !out_dists || !out_sizes) return fail(KNNM_ERR_ARG, "null argument");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     CK(cudaSetDevice(c->device));
@@ -814,6 +1037,7 @@ int knnm_export(knnm_ctx *c, int32_t merge_rear, int32_t *out_ids, double *out_d
     k_export<<<grid_for(c, nk, 256), 256, 0, c->st>>>(c->ids.as<int32_t>(), c->ugid.as<int64_t>(),
                                                        nk, c->out_ids.as<int32_t>());
     CKL();
+    const void *src_i = c->out_ids.p, *src_d = c->dists.p, *src_s = c->sizes.p;
     if (merge_rear && c->have_tail && c->tk > 0) {
         TRY(ensure(c->out_d, sizeof(double) * nk));
         TRY(ensure(c->out_s, sizeof(int32_t) * n));
@@ -823,16 +1047,31 @@ int knnm_export(knnm_ctx *c, int32_t merge_rear, int32_t *out_ids, double *out_d
             c->tail_ids.as<int32_t>(), c->tail_d.as<double>(), c->tail_s.as<int32_t>(), n, c->k,
             c->tk, c->stage[0].as<int32_t>(), c->out_d.as<double>(), c->out_s.as<int32_t>());
         CKL();
-        CK(cudaMemcpyAsync(out_ids, c->stage[0].p, sizeof(int32_t) * nk, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaMemcpyAsync(out_dists, c->out_d.p, sizeof(double) * nk, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaMemcpyAsync(out_sizes, c->out_s.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->st));
+        src_i = c->stage[0].p;
+        src_d = c->out_d.p;
+        src_s = c->out_s.p;
+    }
+    if (on_device) {
+        CK(cudaMemcpyAsync(out_ids, src_i, sizeof(int32_t) * nk, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaMemcpyAsync(out_dists, src_d, sizeof(double) * nk, cudaMemcpyDeviceToDevice, c->st));
+        CK(cudaMemcpyAsync(out_sizes, src_s, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, c->st));
     } else {
-        CK(cudaMemcpyAsync(out_ids, c->out_ids.p, sizeof(int32_t) * nk, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaMemcpyAsync(out_dists, c->dists.p, sizeof(double) * nk, cudaMemcpyDeviceToHost, c->st));
-        CK(cudaMemcpyAsync(out_sizes, c->sizes.p, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->st));
+        TRY(d2h(c, out_ids, src_i, sizeof(int32_t) * nk));
+        TRY(d2h(c, out_dists, src_d, sizeof(double) * nk));
+        TRY(d2h(c, out_sizes, src_s, sizeof(int32_t) * n));
     }
     CK(cudaStreamSynchronize(c->st));
     return KNNM_OK;
+}
+
+int knnm_export(knnm_ctx *c, int32_t merge_rear, int32_t *out_ids, double *out_dists,
+                int32_t *out_sizes) {
+    return export_impl(c, merge_rear, out_ids, out_dists, out_sizes, false);
+}
+
+int knnm_export_dev(knnm_ctx *c, int32_t merge_rear, int32_t *out_ids, double *out_dists,
+                    int32_t *out_sizes) {
+    return export_impl(c, merge_rear, out_ids, out_dists, out_sizes, true);
 }
 
 int knnm_get_state(knnm_ctx *c, int32_t *ids, double *dists, uint8_t *flags, int32_t *sizes) {
@@ -840,10 +1079,10 @@ int knnm_get_state(knnm_ctx *c, int32_t *ids, double *dists, uint8_t *flags, int
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     CK(cudaSetDevice(c->device));
     size_t nk = (size_t)c->n * c->k;
-    if (ids) CK(cudaMemcpyAsync(ids, c->ids.p, sizeof(int32_t) * nk, cudaMemcpyDeviceToHost, c->st));
-    if (dists) CK(cudaMemcpyAsync(dists, c->dists.p, sizeof(double) * nk, cudaMemcpyDeviceToHost, c->st));
-    if (flags) CK(cudaMemcpyAsync(flags, c->flags.p, nk, cudaMemcpyDeviceToHost, c->st));
-    if (sizes) CK(cudaMemcpyAsync(sizes, c->sizes.p, sizeof(int32_t) * c->n, cudaMemcpyDeviceToHost, c->st));
+    if (ids) TRY(d2h(c, ids, c->ids.p, sizeof(int32_t) * nk));
+    if (dists) TRY(d2h(c, dists, c->dists.p, sizeof(double) * nk));
+    if (flags) TRY(d2h(c, flags, c->flags.p, nk));
+    if (sizes) TRY(d2h(c, sizes, c->sizes.p, sizeof(int32_t) * c->n));
     CK(cudaStreamSynchronize(c->st));
     return KNNM_OK;
 }
@@ -877,6 +1116,19 @@ int knnm_capture_fetch(knnm_ctx *c, int32_t *pa, int32_t *pb, double *pd, int64_
     return KNNM_OK;
 }
 
+int knnm_set_join_variant(knnm_ctx *c, int32_t variant) {
+    if (!c || variant < -1 || variant > 1) return fail(KNNM_ERR_ARG, "variant %d", variant);
+    c->join_variant = variant;
+    return KNNM_OK;
+}
+
+int knnm_get_info(knnm_ctx *c, int32_t *cert, int32_t *dp) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (cert) *cert = c->cert ? 1 : 0;
+    if (dp) *dp = c->dp;
+    return KNNM_OK;
+}
+
 int knnm_set_profiling(knnm_ctx *c, int32_t on) {
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
     c->profiling = on != 0;
@@ -900,6 +1152,24 @@ int knnm_reset_stats(knnm_ctx *c) {
     TRY(resolve_timers(c));
     c->stats = knnm_stats{};
     for (double &v : c->phase_ms) v = 0;
+    return KNNM_OK;
+}
+
+int knnm_mark(knnm_ctx *c, int32_t slot) {
+    if (!c || slot < 0 || slot >= 8) return fail(KNNM_ERR_ARG, "bad slot");
+    CK(cudaSetDevice(c->device));
+    if (!c->marks[slot]) CK(cudaEventCreate(&c->marks[slot]));
+    CK(cudaEventRecord(c->marks[slot], c->st));
+    return KNNM_OK;
+}
+
+int knnm_elapsed(knnm_ctx *c, int32_t a, int32_t b, double *ms) {
+    if (!c || !ms || a < 0 || a >= 8 || b < 0 || b >= 8 || !c->marks[a] || !c->marks[b])
+        return fail(KNNM_ERR_ARG, "bad slots");
+    float f = 0;
+    CK(cudaEventSynchronize(c->marks[b]));
+    CK(cudaEventElapsedTime(&f, c->marks[a], c->marks[b]));
+    *ms = f;
     return KNNM_OK;
 }
 

@@ -9,7 +9,7 @@ namespace knnm {
 
 constexpr int WARP_REV_MAX = 256;      // reverse segments a warp sorts itself
 constexpr int BLOCK_SORT_MAX = 16384;  // elements a block sorts in shared memory
-constexpr int APPLY_WARP_MAX = 256;    // candidates per row handled by one warp
+constexpr int APPLY_WARP_MAX = 1024;   // candidates per row handled by one warp
 constexpr int MAX_W = 128;             // k + rev_cap upper bound
 
 struct CandA {  // emitted directed update (unsorted)
@@ -159,6 +159,51 @@ __global__ void k_load_graph(const int32_t *__restrict__ rows, int64_t m, const 
             if (tk > 0) tail_s[r] = sz > k1 ? sz - k1 : 0;
         }
     }
+}
+
+__global__ void k_repeat_rows(const int32_t *__restrict__ rows, int count, int64_t m,
+                              int32_t *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = rows[i / count];
+}
+
+// Random-append candidate matrix (merge.py:146-163): flag rows of an
+// (nrows, t) int64 draw matrix that contain a repeated value.  Only rows in
+// `rows` (or all rows when rows == nullptr) are checked.
+__global__ void k_dup_rows(const int64_t *__restrict__ cand, int64_t nrows, int t,
+                           const int64_t *__restrict__ rows, int64_t nchk, int64_t *bad,
+                           unsigned long long *counters) {
+    int64_t total = rows ? nchk : nrows;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = rows ? rows[i] : i;
+        const int64_t *row = cand + r * t;
+        bool dup = false;
+        for (int a = 1; a < t && !dup; a++) {
+            int64_t x = row[a];
+            for (int b = 0; b < a; b++)
+                if (row[b] == x) { dup = true; break; }
+        }
+        if (dup) bad[atomicAdd(&counters[C_CAND], 1ull)] = r;
+    }
+}
+
+// Replace rows of the draw matrix with redrawn values.
+__global__ void k_put_rows(int64_t *cand, int t, const int64_t *__restrict__ rows, int64_t nbad,
+                           const int64_t *__restrict__ vals) {
+    int64_t total = nbad * t;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x)
+        cand[rows[i / t] * t + i % t] = vals[i];
+}
+
+// nids = pool[cand] as int32 local ids.
+__global__ void k_pool_map(const int64_t *__restrict__ cand, int64_t m, const int32_t *__restrict__ pool,
+                           int32_t *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = pool[cand[i]];
 }
 
 // ---------------------------------------------------------------------------
@@ -501,6 +546,340 @@ k_join_exact(const int32_t *__restrict__ active, const uint32_t *__restrict__ nb
     }
 }
 
+// ---------------------------------------------------------------------------
+// Local join, tiled route (the product kernel).  One CTA per active hood
+// (grid-stride).  Member vectors are staged into shared memory by TMA bulk
+// copies (cp.async.bulk, one per member row, completion on an mbarrier).
+// Members are re-ordered into classes (label, new-first) so the admissible
+// region is a union of dense blocks:
+//     CROSS        A x B                    (A = label 0, B = label 1)
+//     CROSS_OR_S2  A x B  +  B x B (upper)
+//     ALL          M x M (upper)
+// Each thread owns 2x2 register tiles of the block (fp32 SIMT FMA, 128-bit
+// shared loads, broadcast-friendly lane layout).  Tiles that hold only
+// old x old pairs are skipped.
+//   CERT  : the dataset carries an exactness certificate (integer values,
+//           d * range^2 < 2^24): every fp32 partial sum is an exact integer,
+//           so the fp32 value IS the reference's fp64 value.
+//   !CERT : the fp32 value screens with a rigorous error margin; pairs that
+//           may pass are re-evaluated with the exact fp64 metric from the
+//           staged vectors.
+// Emission as in k_join_exact: reference-order key (u, p, q), exact-safe
+// prefilter against the round-start worst of each target.
+// ---------------------------------------------------------------------------
+constexpr int TJ_WARPS = 2;
+constexpr int TJ_THREADS = TJ_WARPS * 32;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void fence_proxy_async() {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+template <int TAG, bool CERT>
+__global__ void __launch_bounds__(TJ_THREADS)
+k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
+             const int32_t *__restrict__ nlen, int W, const int8_t *__restrict__ labels, int mode,
+             const float *__restrict__ sub, int dp, int d, const double *__restrict__ worst0,
+             CandA *A, unsigned long long cap, uint32_t *tcnt, unsigned long long *counters,
+             double mrel, double mabs) {
+    extern __shared__ __align__(128) float4 sv4[];
+    __shared__ int s_id[MAX_W];
+    __shared__ int s_pos[MAX_W];
+    __shared__ int s_new[MAX_W];
+    __shared__ double s_w[MAX_W];
+    __shared__ float s_nrm[MAX_W];
+    __shared__ int s_cls[4];
+    __shared__ __align__(8) uint64_t s_bar;
+    const float *sv = reinterpret_cast<const float *>(sv4);
+    const int tid = threadIdx.x;
+    const unsigned lane = lane_id();
+    const int warp = tid >> 5;
+    const int q4 = dp >> 2;
+    const int qs = q4 + 1;  // padded row stride in float4
+    if (tid == 0) mbar_init(&s_bar, 1);
+    __syncthreads();
+    uint32_t phase = 0;
+    unsigned long long n_exact = 0;
+
+    for (int hi = blockIdx.x; hi < nactive; hi += gridDim.x) {
+        const int64_t u = active[hi];
+        const int w = nlen[u];
+        // ---- classify members: class = (label != 0) * 2 + (!new) ----------
+        if (tid < 32) {
+            int cnts[4] = {0, 0, 0, 0};
+            int base_cls[4];
+            // first pass: class counts
+            for (int b = 0; b < w; b += 32) {
+                int j = b + lane;
+                int cls = 4;
+                if (j < w) {
+                    uint32_t e = nbh[u * W + j];
+                    int lab = mode == 0 ? 0 : (labels[e >> 1] != 0);
+                    cls = lab * 2 + ((e & 1) ? 0 : 1);
+                }
+#pragma unroll
+                for (int c = 0; c < 4; c++) cnts[c] += __popc(__ballot_sync(FULL_MASK, cls == c));
+            }
+            base_cls[0] = 0;
+            base_cls[1] = cnts[0];
+            base_cls[2] = cnts[0] + cnts[1];
+            base_cls[3] = base_cls[2] + cnts[2];
+            int fill[4] = {0, 0, 0, 0};
+            for (int b = 0; b < w; b += 32) {
+                int j = b + lane;
+                int cls = 4;
+                uint32_t e = 0;
+                if (j < w) {
+                    e = nbh[u * W + j];
+                    int lab = mode == 0 ? 0 : (labels[e >> 1] != 0);
+                    cls = lab * 2 + ((e & 1) ? 0 : 1);
+                }
+#pragma unroll
+                for (int c = 0; c < 4; c++) {
+                    unsigned m = __ballot_sync(FULL_MASK, cls == c);
+                    if (cls == c) {
+                        int slot = base_cls[c] + fill[c] + __popc(m & lanemask_lt());
+                        int id = (int)(e >> 1);
+                        s_id[slot] = id;
+                        s_pos[slot] = j;
+                        s_new[slot] = (int)(e & 1);
+                        s_w[slot] = worst0[id];
+                    }
+                    fill[c] += __popc(m);
+                }
+            }
+            if (lane < 4) s_cls[lane] = cnts[lane];
+        }
+        __syncthreads();
+        // ---- stage the member rows with TMA bulk copies ---------------------
+        // smem row stride = dp + 4 floats: consecutive rows start 16 B apart
+        // modulo 128 B, so 8 distinct rows per wavefront are conflict-free.
+        if (tid == 0) {
+            fence_proxy_async();
+            const uint32_t row_bytes = (uint32_t)dp * 4u;
+            mbar_expect_tx(&s_bar, row_bytes * (uint32_t)w);
+            for (int sl = 0; sl < w; sl++)
+                bulk_g2s(sv4 + (size_t)sl * qs, sub + (int64_t)s_id[sl] * dp, row_bytes, &s_bar);
+        }
+        mbar_wait(&s_bar, phase);
+        phase ^= 1u;
+        if (TAG == 2) {
+            // fp32 norms for the cosine screen
+            for (int sl = warp; sl < w; sl += TJ_WARPS) {
+                float acc = 0.f;
+                for (int c = lane; c < q4; c += 32) {
+                    float4 a = sv4[(size_t)sl * qs + c];
+                    acc = fmaf(a.x, a.x, acc);
+                    acc = fmaf(a.y, a.y, acc);
+                    acc = fmaf(a.z, a.z, acc);
+                    acc = fmaf(a.w, a.w, acc);
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, o);
+                if (lane == 0) s_nrm[sl] = acc;
+            }
+            __syncthreads();
+        }
+        // ---- blocks ----------------------------------------------------------
+        const int nAn = s_cls[0], nAo = s_cls[1], nBn = s_cls[2];
+        const int nA = nAn + nAo;
+        // block 0 and (CROSS_OR_S2 only) block 1; plain scalars, no local arrays
+        const int b0r0 = 0, b0r1 = mode == 0 ? w : nA, b0c0 = mode == 0 ? 0 : nA, b0c1 = w;
+        const int b0rn = nAn, b0cn = mode == 0 ? nAn : nBn, b0tri = mode == 0;
+        const int b1r0 = nA, b1r1 = w, b1c0 = nA, b1c1 = w, b1rn = nBn, b1cn = nBn;
+        const int nblk = mode == 2 ? 2 : 1;
+        const int nrt0 = (b0r1 - b0r0 + 1) >> 1, nct0 = (b0c1 - b0c0 + 1) >> 1;
+        const int nrt1 = (b1r1 - b1r0 + 1) >> 1, nct1 = (b1c1 - b1c0 + 1) >> 1;
+        const int pc0 = (nct0 + 7) >> 3, np0 = ((nrt0 + 3) >> 2) * pc0;
+        const int pc1 = (nct1 + 7) >> 3, np1 = nblk == 2 ? ((nrt1 + 3) >> 2) * pc1 : 0;
+        // each warp takes 4 x 8 patches of 2 x 2 tiles (8 rows x 16 cols)
+        for (int pid = warp; pid < np0 + np1; pid += TJ_WARPS) {
+            const bool second = pid >= np0;
+            const int lp = second ? pid - np0 : pid;
+            const int pcs = second ? pc1 : pc0;
+            const int pr = lp / pcs, pcc = lp - pr * pcs;
+            const int rt = pr * 4 + (int)(lane >> 3), ct = pcc * 8 + (int)(lane & 7);
+            const int r0 = second ? b1r0 : b0r0, r1 = second ? b1r1 : b0r1;
+            const int c0 = second ? b1c0 : b0c0, c1 = second ? b1c1 : b0c1;
+            const int rn = second ? b1rn : b0rn, cn = second ? b1cn : b0cn;
+            const bool tri = second ? true : (bool)b0tri;
+            const int i0 = r0 + 2 * rt, j0 = c0 + 2 * ct;
+            bool live = i0 < r1 && j0 < c1;
+            if (live && tri && rt > ct) live = false;             // below diagonal
+            if (live && 2 * rt >= rn && 2 * ct >= cn) live = false;  // old x old
+            const bool vi1 = i0 + 1 < r1, vj1 = j0 + 1 < c1;
+            float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+            if (live) {
+                const float4 *a0p = sv4 + (size_t)i0 * qs;
+                const float4 *a1p = sv4 + (size_t)(vi1 ? i0 + 1 : i0) * qs;
+                const float4 *b0p = sv4 + (size_t)j0 * qs;
+                const float4 *b1p = sv4 + (size_t)(vj1 ? j0 + 1 : j0) * qs;
+#pragma unroll 4
+                for (int c = 0; c < q4; c++) {
+                    float4 a0 = a0p[c], a1 = a1p[c], b0 = b0p[c], b1 = b1p[c];
+                    if (TAG == 1) {
+#define KNNM_L2_ACC(ACC, X, Y)                         \
+    {                                                  \
+        float t_;                                      \
+        t_ = X.x - Y.x; ACC = fmaf(t_, t_, ACC);       \
+        t_ = X.y - Y.y; ACC = fmaf(t_, t_, ACC);       \
+        t_ = X.z - Y.z; ACC = fmaf(t_, t_, ACC);       \
+        t_ = X.w - Y.w; ACC = fmaf(t_, t_, ACC);       \
+    }
+                        KNNM_L2_ACC(acc[0][0], a0, b0);
+                        KNNM_L2_ACC(acc[0][1], a0, b1);
+                        KNNM_L2_ACC(acc[1][0], a1, b0);
+                        KNNM_L2_ACC(acc[1][1], a1, b1);
+#undef KNNM_L2_ACC
+                    } else if (TAG == 0) {
+#define KNNM_L1_ACC(ACC, X, Y)                                                          \
+    {                                                                                   \
+        ACC += fabsf(X.x - Y.x); ACC += fabsf(X.y - Y.y);                               \
+        ACC += fabsf(X.z - Y.z); ACC += fabsf(X.w - Y.w);                               \
+    }
+                        KNNM_L1_ACC(acc[0][0], a0, b0);
+                        KNNM_L1_ACC(acc[0][1], a0, b1);
+                        KNNM_L1_ACC(acc[1][0], a1, b0);
+                        KNNM_L1_ACC(acc[1][1], a1, b1);
+#undef KNNM_L1_ACC
+                    } else {
+#define KNNM_DOT_ACC(ACC, X, Y)                                                          \
+    {                                                                                    \
+        ACC = fmaf(X.x, Y.x, ACC); ACC = fmaf(X.y, Y.y, ACC);                            \
+        ACC = fmaf(X.z, Y.z, ACC); ACC = fmaf(X.w, Y.w, ACC);                            \
+    }
+                        KNNM_DOT_ACC(acc[0][0], a0, b0);
+                        KNNM_DOT_ACC(acc[0][1], a0, b1);
+                        KNNM_DOT_ACC(acc[1][0], a1, b0);
+                        KNNM_DOT_ACC(acc[1][1], a1, b1);
+#undef KNNM_DOT_ACC
+                    }
+                }
+            }
+            // ---- finalize the 4 pairs of the tile --------------------------
+#pragma unroll
+            for (int s = 0; s < 4; s++) {
+                const int ii = i0 + (s >> 1), jj = j0 + (s & 1);
+                bool ok = live && ii < r1 && jj < c1;
+                if (ok && tri) ok = ii < jj;
+                if (ok) ok = s_new[ii] || s_new[jj];
+                double dd = 0.0;
+                bool e1 = false, e2 = false;
+                if (ok) {
+                    const double wi = s_w[ii], wj = s_w[jj];
+                    const double wmax = wi > wj ? wi : wj;
+                    float f = acc[s >> 1][s & 1];
+                    if (CERT) {
+                        dd = (double)f;
+                    } else {
+                        bool maybe;
+                        if (TAG == 2) {
+                            float na = s_nrm[ii], nb = s_nrm[jj];
+                            if (na == 0.f || nb == 0.f) {
+                                maybe = true;
+                            } else {
+                                float cs = 1.0f - f / (sqrtf(na) * sqrtf(nb));
+                                maybe = (double)cs <= wmax + mabs;
+                            }
+                        } else {
+                            maybe = (double)f <= wmax * mrel;
+                        }
+                        if (maybe) {
+                            dd = exact_dist<TAG>(sv + (size_t)ii * qs * 4, sv + (size_t)jj * qs * 4, d);
+                            n_exact++;
+                        } else {
+                            dd = __longlong_as_double(0x7ff0000000000000LL);
+                        }
+                    }
+                    e1 = dd < wi;  // id[ii] <- id[jj]
+                    e2 = dd < wj;  // id[jj] <- id[ii]
+                }
+                unsigned m1 = __ballot_sync(FULL_MASK, e1), m2 = __ballot_sync(FULL_MASK, e2);
+                int tot = __popc(m1) + __popc(m2);
+                if (tot) {
+                    unsigned long long bb = 0;
+                    if (lane == 0) bb = atomicAdd(&counters[C_CAND], (unsigned long long)tot);
+                    bb = __shfl_sync(FULL_MASK, bb, 0);
+                    if (e1 || e2) {
+                        const int pi = s_pos[ii], pj = s_pos[jj];
+                        const int p = pi < pj ? pi : pj, q = pi < pj ? pj : pi;
+                        const uint64_t key = ((uint64_t)u * W + p) * W + q;
+                        const int idi = s_id[ii], idj = s_id[jj];
+                        if (e1) {
+                            unsigned long long pos = bb + __popc(m1 & lanemask_lt());
+                            if (pos < cap) {
+                                A[pos] = CandA{key, dd, idj, idi};
+                                atomicAdd(&tcnt[idi], 1u);
+                            }
+                        }
+                        if (e2) {
+                            unsigned long long pos = bb + __popc(m1) + __popc(m2 & lanemask_lt());
+                            if (pos < cap) {
+                                A[pos] = CandA{key, dd, idi, idj};
+                                atomicAdd(&tcnt[idj], 1u);
+                            }
+                        }
+                    }
+                }
+            }
+        }
+        __syncthreads();  // smem reused by the next hood
+    }
+    if (!CERT) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) n_exact += __shfl_xor_sync(FULL_MASK, n_exact, o);
+        if (lane == 0 && n_exact) atomicAdd(&counters[C_EXACT], n_exact);
+    }
+}
+
+// Dataset exactness certificate: integer-valued entries and their range.
+__global__ void k_data_stats(const float *__restrict__ v, int64_t total, unsigned long long *out) {
+    // out[0] = count of non-integer / non-finite entries, out[1] = max as
+    // ordered bits, out[2] = min as ordered bits (float -> sortable u32)
+    unsigned long long bad = 0;
+    unsigned int mx = 0, mn = 0xffffffffu;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float x = v[i];
+        if (!(fabsf(x) < 16777216.0f) || rintf(x) != x) bad++;
+        unsigned int b = __float_as_uint(x);
+        unsigned int key = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+        mx = key > mx ? key : mx;
+        mn = key < mn ? key : mn;
+    }
+    if (bad) atomicAdd(&out[0], bad);
+    atomicMax(&out[1], (unsigned long long)mx);
+    atomicMin(&out[2], (unsigned long long)mn);
+}
+
 // on_pair capture: every admissible pair of every hood in (u, p, q) order.
 __global__ void k_capture_pairs(const uint32_t *__restrict__ nbh, const int32_t *__restrict__ nlen,
                                 int64_t lo, int64_t hi, int W, const int8_t *__restrict__ labels,
@@ -544,7 +923,36 @@ __global__ void k_scatter(const CandA *__restrict__ A, unsigned long long count,
 // row loop, _kernels.py:248-254, each step _insert _kernels.py:159-192).
 // One warp per row; the row's candidates are sorted by reference key first.
 // ---------------------------------------------------------------------------
-constexpr int APPLY_WARPS = 8;
+constexpr int APPLY_WARPS = 4;
+
+// Sort a row's c <= 32*NE candidates in registers by reference key, then
+// apply them in order, 32 at a time.
+template <int E, int NE>
+__device__ __forceinline__ int apply_sorted_reg(WarpRow<E> &s, int k, const CandB *__restrict__ Bp,
+                                                int c, int ib, uint64_t mask, unsigned lane) {
+    uint64_t v[NE];
+#pragma unroll
+    for (int e = 0; e < NE; e++) {
+        int j = e * 32 + (int)lane;
+        v[e] = j < c ? ((Bp[j].key << ib) | (uint64_t)j) : ~0ull;
+    }
+    warp_sort_reg<NE>(v, lane);
+    int a = 0;
+#pragma unroll
+    for (int e = 0; e < NE; e++) {
+        const int base = e * 32;
+        if (base >= c) break;
+        int src = 0;
+        double dd = 0.0;
+        if (base + (int)lane < c) {
+            const CandB &cb = Bp[(uint32_t)(v[e] & mask)];
+            src = cb.src;
+            dd = cb.d;
+        }
+        a += warp_apply_chunk<E>(s, k, src, dd, c - base < 32 ? c - base : 32, lane);
+    }
+    return a;
+}
 
 template <int E>
 __global__ void __launch_bounds__(APPLY_WARPS * 32)
@@ -561,24 +969,24 @@ k_apply(int64_t n, int k, const uint32_t *__restrict__ toff, const CandB *__rest
         int c = (int)(toff[r + 1] - lo);
         if (c == 0) continue;
         if (c > APPLY_WARP_MAX) {
-            if (lane == 0) heavy[atomicAdd(&counters[C_HEAVY_APPLY], 1ull)] = (int32_t)r;
+            if (lane == 0) {
+                heavy[atomicAdd(&counters[C_HEAVY_APPLY], 1ull)] = (int32_t)r;
+                atomicMax(&counters[C_MAXC], (unsigned long long)c);
+            }
             continue;
         }
         WarpRow<E> s;
         row_load<E>(s, ids, dists, flags, sizes, r, k, lane);
-        uint64_t mask = (1ull << ib) - 1ull;
+        const uint64_t mask = (1ull << ib) - 1ull;
         int a = 0;
         if (c <= 32) {
-            uint64_t v = (int)lane < c ? ((B[lo + lane].key << ib) | lane) : ~0ull;
-            v = bitonic_reg32(v, lane);
-            int src = 0;
-            double dd = 0.0;
-            if ((int)lane < c) {
-                const CandB &cb = B[lo + (uint32_t)(v & mask)];
-                src = cb.src;
-                dd = cb.d;
-            }
-            a += warp_apply_chunk<E>(s, k, src, dd, c, lane);
+            a += apply_sorted_reg<E, 1>(s, k, B + lo, c, ib, mask, lane);
+        } else if (c <= 64) {
+            a += apply_sorted_reg<E, 2>(s, k, B + lo, c, ib, mask, lane);
+        } else if (c <= 128) {
+            a += apply_sorted_reg<E, 4>(s, k, B + lo, c, ib, mask, lane);
+        } else if (c <= 256) {
+            a += apply_sorted_reg<E, 8>(s, k, B + lo, c, ib, mask, lane);
         } else {
             uint32_t P2 = next_pow2((uint32_t)c);
             for (uint32_t j = lane; j < P2; j += 32)
@@ -621,13 +1029,7 @@ __global__ void k_apply_heavy(const int32_t *__restrict__ heavy, int64_t k_, con
         uint32_t c = toff[r + 1] - lo;
         uint32_t P2 = next_pow2(c);
         bool in_smem = P2 <= (uint32_t)smem_max;
-        if (gscratch == nullptr && !in_smem) {
-            if (threadIdx.x == 0) {
-                giant[atomicAdd(&counters[C_GIANT_APPLY], 1ull)] = (int32_t)r;
-                atomicMax(&counters[C_MAXC], (unsigned long long)c);
-            }
-            continue;
-        }
+        if (gscratch == nullptr && !in_smem) continue;  // giant rows: second pass
         if (gscratch != nullptr && in_smem) continue;
         uint64_t *srt = in_smem ? hsrt : gscratch;
         uint64_t mask = (1ull << ib) - 1ull;

@@ -65,6 +65,18 @@ class Engine:
 
     def load_graph(self, rows: np.ndarray, graph, k1: int) -> None:
         rows = np.ascontiguousarray(rows, dtype=np.int32)
+        if _is_cuda_tensor(graph.ids):
+            # graph already resident in HBM (torch CUDA tensors): no host copy
+            gi, gd, gs = graph.ids, graph.dists, graph.sizes
+            for t, dt in ((gi, "int32"), (gd, "float64"), (gs, "int32")):
+                if not (_is_cuda_tensor(t) and t.is_contiguous() and str(t.dtype).endswith(dt)):
+                    raise ValueError("device graph arrays must be contiguous CUDA tensors "
+                                     "(ids int32, dists float64, sizes int32)")
+            check(self._lib.knnm_load_graph_dev(
+                self._h, ptr(rows), rows.shape[0], ctypes.c_void_p(gi.data_ptr()),
+                ctypes.c_void_p(gd.data_ptr()), ctypes.c_void_p(gs.data_ptr()), int(graph.k),
+                int(k1)), "knnm_load_graph_dev")
+            return
         gi = np.ascontiguousarray(graph.ids, dtype=np.int32)
         gd = np.ascontiguousarray(graph.dists, dtype=np.float64)
         gs = np.ascontiguousarray(graph.sizes, dtype=np.int32)
@@ -79,6 +91,46 @@ class Engine:
                                              ctypes.byref(acc)), "knnm_insert_directed")
         return int(acc.value)
 
+    def insert_rows(self, rows: np.ndarray, count: int, nids: np.ndarray) -> int:
+        """Directed inserts with targets np.repeat(rows, count), expanded on device."""
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        nids = np.ascontiguousarray(nids, dtype=np.int32)
+        if nids.shape[0] != rows.shape[0] * int(count):
+            raise ValueError("nids must hold len(rows) * count entries")
+        acc = ctypes.c_int64()
+        check(self._lib.knnm_insert_rows(self._h, ptr(rows), rows.shape[0], int(count), ptr(nids),
+                                         ctypes.byref(acc)), "knnm_insert_rows")
+        return int(acc.value)
+
+    # -- random-append draw matrix (merge.py:146-163) ------------------------
+    def _bad(self, n):
+        return np.empty(max(int(n), 1), dtype=np.int64)
+
+    def draws_load(self, cand: np.ndarray) -> np.ndarray:
+        cand = np.ascontiguousarray(cand, dtype=np.int64)
+        bad = self._bad(cand.shape[0])
+        nb = ctypes.c_int64()
+        check(self._lib.knnm_draws_load(self._h, ptr(cand), cand.shape[0], cand.shape[1],
+                                        ptr(bad), ctypes.byref(nb)), "knnm_draws_load")
+        return bad[: nb.value].copy()
+
+    def draws_replace(self, rows: np.ndarray, vals: np.ndarray) -> np.ndarray:
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        vals = np.ascontiguousarray(vals, dtype=np.int64)
+        bad = self._bad(rows.shape[0])
+        nb = ctypes.c_int64()
+        check(self._lib.knnm_draws_replace(self._h, ptr(rows), rows.shape[0], ptr(vals), ptr(bad),
+                                           ctypes.byref(nb)), "knnm_draws_replace")
+        return bad[: nb.value].copy()
+
+    def draws_insert(self, rows: np.ndarray, pool: np.ndarray) -> int:
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        pool = np.ascontiguousarray(pool, dtype=np.int32)
+        acc = ctypes.c_int64()
+        check(self._lib.knnm_draws_insert(self._h, ptr(rows), ptr(pool), pool.shape[0],
+                                          ctypes.byref(acc)), "knnm_draws_insert")
+        return int(acc.value)
+
     def round(self, mode: int, rev_cap: int, seed: int):
         pairs = ctypes.c_int64()
         acc = ctypes.c_int64()
@@ -91,7 +143,19 @@ class Engine:
         check(self._lib.knnm_phi(self._h, ctypes.byref(out)), "knnm_phi")
         return float(out.value)
 
-    def export(self, merge_rear: bool):
+    def export(self, merge_rear: bool, on_device: bool = False):
+        if on_device:
+            import torch
+
+            dev = torch.device("cuda", self.device)
+            ids = torch.empty((self.n, self.k), dtype=torch.int32, device=dev)
+            dists = torch.empty((self.n, self.k), dtype=torch.float64, device=dev)
+            sizes = torch.empty(self.n, dtype=torch.int32, device=dev)
+            check(self._lib.knnm_export_dev(self._h, int(bool(merge_rear)),
+                                            ctypes.c_void_p(ids.data_ptr()),
+                                            ctypes.c_void_p(dists.data_ptr()),
+                                            ctypes.c_void_p(sizes.data_ptr())), "knnm_export_dev")
+            return ids, dists, sizes
         ids = np.empty((self.n, self.k), dtype=np.int32)
         dists = np.empty((self.n, self.k), dtype=np.float64)
         sizes = np.empty(self.n, dtype=np.int32)
@@ -123,6 +187,16 @@ class Engine:
               "knnm_capture_fetch")
         return pa, pb, pd
 
+    def set_join_variant(self, variant: int) -> None:
+        """-1 auto, 0 exact fp64 route, 1 tiled fp32-screen route."""
+        check(self._lib.knnm_set_join_variant(self._h, int(variant)), "knnm_set_join_variant")
+
+    def info(self) -> dict:
+        cert = ctypes.c_int32()
+        dp = ctypes.c_int32()
+        check(self._lib.knnm_get_info(self._h, ctypes.byref(cert), ctypes.byref(dp)), "knnm_get_info")
+        return {"cert": bool(cert.value), "dp": int(dp.value)}
+
     # -- instrumentation ---------------------------------------------------
     def set_profiling(self, on: bool) -> None:
         check(self._lib.knnm_set_profiling(self._h, int(bool(on))), "knnm_set_profiling")
@@ -135,8 +209,20 @@ class Engine:
     def reset_stats(self) -> None:
         check(self._lib.knnm_reset_stats(self._h), "knnm_reset_stats")
 
+    def mark(self, slot: int) -> None:
+        check(self._lib.knnm_mark(self._h, int(slot)), "knnm_mark")
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        out = ctypes.c_double()
+        check(self._lib.knnm_elapsed(self._h, int(a), int(b), ctypes.byref(out)), "knnm_elapsed")
+        return float(out.value)
+
     def sync(self) -> None:
         check(self._lib.knnm_sync(self._h), "knnm_sync")
+
+
+def _is_cuda_tensor(x) -> bool:
+    return hasattr(x, "data_ptr") and getattr(x, "is_cuda", False)
 
 
 _engines: dict[int, Engine] = {}

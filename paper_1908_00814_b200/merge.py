@@ -23,7 +23,9 @@ from .construct import (
     _capture,
     _descent_rounds,
     _graph_from,
+    _emit_captured,
     _insert_directed,
+    _insert_rows,
 )
 from .core import DistanceCounter, Metric, sample_distinct
 from .engine import get_engine
@@ -62,6 +64,29 @@ def _lookup_local(union_gids: np.ndarray, gids: np.ndarray) -> np.ndarray:
     return np.searchsorted(union_gids, gids).astype(np.int32)
 
 
+def _ascending(a: np.ndarray) -> bool:
+    return a.size < 2 or bool(np.all(a[1:] > a[:-1]))
+
+
+def _overlaps(a: np.ndarray, b: np.ndarray) -> bool:
+    """np.intersect1d(a, b).size > 0 for ascending unique arrays, in
+    O(|b| log |a|) instead of a full sort."""
+    if a.size == 0 or b.size == 0:
+        return False
+    if not (_ascending(a) and _ascending(b)):
+        return bool(np.intersect1d(a, b).size)
+    idx = np.minimum(np.searchsorted(a, b), a.size - 1)
+    return bool(np.any(a[idx] == b))
+
+
+def _union(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """np.union1d for disjoint ascending arrays: a linear two-run merge
+    (timsort detects the runs), same result as the reference's union1d."""
+    if _ascending(a) and _ascending(b):
+        return np.sort(np.concatenate((a, b)), kind="stable")
+    return np.union1d(a, b)
+
+
 def _sample_pool_rows(rng, nrows: int, t: int, pool: np.ndarray) -> np.ndarray:
     """(nrows, t) distinct draws per row from ``pool`` (merge.py:146-163;
     identical PCG64 call sequence)."""
@@ -85,19 +110,37 @@ def _sample_pool_rows(rng, nrows: int, t: int, pool: np.ndarray) -> np.ndarray:
 
 def _append_random(engine, rows, pool, count, rng, counter, on_pair, gids) -> None:
     """merge.py:166-176: append ``count`` random pool members to each row,
-    flagged new, with exact distances (device)."""
+    flagged new, with exact distances (device).
+
+    The PCG64 draws stay on the host and are made in exactly the reference's
+    order (merge.py:156-163); the duplicate-row test, the pool mapping and
+    the inserts run on the device.  Only rows redrawn in the previous pass
+    can become (or stay) bad, so re-checking just those rows finds the same
+    set np.nonzero(bad) does in the reference loop."""
     if count <= 0 or rows.size == 0 or pool.size == 0:
         return
-    picks = _sample_pool_rows(rng, rows.size, count, pool)
-    tgt = np.repeat(rows.astype(np.int32), count)
-    nids = picks.ravel().astype(np.int32)
-    _insert_directed(engine, tgt, nids, counter, on_pair, gids)
+    m = pool.shape[0]
+    t = int(count)
+    if t > m:
+        raise ValueError("cannot draw more samples than the pool holds")
+    if t == m or 4 * t * t >= m:
+        picks = _sample_pool_rows(rng, rows.size, count, pool)
+        _insert_rows(engine, rows.astype(np.int32), count, picks.ravel().astype(np.int32),
+                     counter, on_pair, gids)
+        return
+    cand = rng.integers(0, m, size=(rows.size, t))
+    bad = engine.draws_load(cand)
+    while bad.size:
+        bad = engine.draws_replace(bad, rng.integers(0, m, size=(bad.size, t)))
+    engine.draws_insert(rows.astype(np.int32), pool.astype(np.int32))
+    counter.add(rows.size * t)
+    _emit_captured(engine, on_pair, gids)
 
 
 def _check_merge_inputs(dataset, g: KnnGraph, other_ids: np.ndarray, params: MergeParams,
                         other_graph: KnnGraph | None) -> None:
     """merge.py:179-192, same checks and messages."""
-    if np.intersect1d(g.member_ids, other_ids).size:
+    if _overlaps(np.asarray(g.member_ids), np.asarray(other_ids)):
         raise ValueError("subsets must be disjoint")
     if g.k != params.k:
         raise ValueError(f"graph capacity {g.k} does not match params.k={params.k}")
@@ -113,7 +156,7 @@ def _check_merge_inputs(dataset, g: KnnGraph, other_ids: np.ndarray, params: Mer
 
 def s_merge(dataset, g: KnnGraph, h: KnnGraph, params: MergeParams,
             counter: DistanceCounter | None = None, on_pair=None, return_report: bool = False,
-            device: int | None = None):
+            device: int | None = None, out_device: bool = False):
     """Symmetric merge of two built k-NN graphs over disjoint subsets
     (merge.py:195-260; Alg. 1 of the paper)."""
     _check_merge_inputs(dataset, g, h.member_ids, params, h)
@@ -124,7 +167,7 @@ def s_merge(dataset, g: KnnGraph, h: KnnGraph, params: MergeParams,
     k = params.k
     k1 = params.k1
 
-    union_gids = np.union1d(g.member_ids, h.member_ids)
+    union_gids = _union(np.asarray(g.member_ids), np.asarray(h.member_ids))
     n = union_gids.shape[0]
     rows_g = _lookup_local(union_gids, g.member_ids)
     rows_h = _lookup_local(union_gids, h.member_ids)
@@ -146,7 +189,7 @@ def s_merge(dataset, g: KnnGraph, h: KnnGraph, params: MergeParams,
         report = BuildReport(phi_initial=eng.phi())
         _descent_rounds(eng, n, MODE_CROSS, k, params.descent_params(), rng, counter, on_pair,
                         union_gids, report)
-        ids, dists, sizes = eng.export(merge_rear=k - k1 > 0)
+        ids, dists, sizes = eng.export(merge_rear=k - k1 > 0, on_device=out_device)
     finally:
         eng.set_capture(False)
     u = _graph_from(union_gids, k, metric, ids, dists, sizes)
@@ -157,7 +200,7 @@ def s_merge(dataset, g: KnnGraph, h: KnnGraph, params: MergeParams,
 
 def j_merge(dataset, g: KnnGraph, raw_ids, params: MergeParams,
             counter: DistanceCounter | None = None, on_pair=None, return_report: bool = False,
-            device: int | None = None):
+            device: int | None = None, out_device: bool = False):
     """Joint merge of a raw id set into a built k-NN graph
     (merge.py:263-338; Alg. 2 of the paper)."""
     raw = np.unique(np.asarray(raw_ids, dtype=np.int64))
@@ -179,7 +222,7 @@ def j_merge(dataset, g: KnnGraph, raw_ids, params: MergeParams,
             return out, BuildReport(phi_initial=graph_phi(out))
         return out
     rng = np.random.default_rng(params.seed)
-    union_gids = np.union1d(g.member_ids, raw)
+    union_gids = _union(np.asarray(g.member_ids), raw)
     n = union_gids.shape[0]
     if k >= n:
         raise ValueError(f"k={k} must be below the union size {n}")
@@ -199,12 +242,12 @@ def j_merge(dataset, g: KnnGraph, raw_ids, params: MergeParams,
         init = np.empty((rows_raw.size, k), dtype=np.int64)
         for t, row in enumerate(rows_raw):
             init[t] = sample_distinct(rng, n, k, exclude=int(row))
-        tgt = np.repeat(rows_raw.astype(np.int32), k)
-        _insert_directed(eng, tgt, init.ravel().astype(np.int32), counter, on_pair, union_gids)
+        _insert_rows(eng, rows_raw.astype(np.int32), k, init.ravel().astype(np.int32), counter,
+                     on_pair, union_gids)
         report = BuildReport(phi_initial=eng.phi())
         _descent_rounds(eng, n, MODE_CROSS_OR_S2, k, params.descent_params(), rng, counter,
                         on_pair, union_gids, report)
-        ids, dists, sizes = eng.export(merge_rear=k - k1 > 0)
+        ids, dists, sizes = eng.export(merge_rear=k - k1 > 0, on_device=out_device)
     finally:
         eng.set_capture(False)
     u = _graph_from(union_gids, k, metric, ids, dists, sizes)

@@ -109,3 +109,40 @@ def _to_graph(km, og):
     g.dists = og.dists.copy()
     g.sizes = og.sizes.copy()
     return g
+
+
+@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("n,d,k,metric,kind", [CASES[1], CASES[5], CASES[6], CASES[8]])
+def test_join_variants_agree(oracle, variant, n, d, k, metric, kind):
+    """Both local-join routes (fp64-every-pair / fp32-screen tiled) are
+    bit-identical to the oracle."""
+    km = _km()
+    from paper_1908_00814_b200.engine import get_engine
+
+    eng = get_engine()
+    ds = _data(km, n, d, kind, seed=n + d + 1)
+    s1, s2 = split_ids(n, seed=7)
+    g, _, _ = oracle.nn_descent(ds.vectors, metric, k, 1, member_ids=s1)
+    h, _, _ = oracle.nn_descent(ds.vectors, metric, k, 2, member_ids=s2)
+    eng.set_join_variant(variant)
+    try:
+        u, rep = km.s_merge(ds, _to_graph(km, g), _to_graph(km, h), km.MergeParams(k=k, seed=9),
+                            return_report=True)
+    finally:
+        eng.set_join_variant(-1)
+    ou, orep, _ = oracle.s_merge(ds.vectors, g, h, k, seed=9)
+    _same_graph(u, ou)
+    _same_report(rep, orep)
+
+
+def test_certificate_detection():
+    km = _km()
+    from paper_1908_00814_b200.engine import get_engine
+
+    eng = get_engine()
+    eng.set_dataset(km.generate_int_gmm(1000, 128, n_centres=10, seed=1).vectors, 1)
+    assert eng.info()["cert"]
+    eng.set_dataset(km.generate_uniform(1000, 16, seed=1).vectors, 1)
+    assert not eng.info()["cert"]
+    eng.set_dataset(km.generate_int_gmm(1000, 128, n_centres=10, seed=1).vectors, 2)
+    assert not eng.info()["cert"]  # cosine is never certified
