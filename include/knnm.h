@@ -180,15 +180,17 @@ int knnm_capture_count(knnm_ctx *ctx, int64_t *count);
 int knnm_capture_fetch(knnm_ctx *ctx, int32_t *pa, int32_t *pb, double *pd,
                        int64_t count);
 
-/* Local-join kernel choice: -1 auto (tiled when the hood fits shared
- * memory), 0 = exact route (fp64 on every pair), 1 = tiled route (fp32
- * SIMT screen, exact by certificate or by fp64 re-evaluation).  Both give
+/* Local-join kernel choice: -1 auto, 0 = exact route (fp64 on every pair),
+ * 1 = tiled route (fp32 SIMT screen, exact by certificate or by fp64
+ * re-evaluation), 2 = tensor-core route (fp16 mma.sync Gram blocks; only for
+ * datasets with the dot-form certificate, otherwise auto).  All routes give
  * bit-identical results; the switch exists for tests and measurement. */
 int knnm_set_join_variant(knnm_ctx *ctx, int32_t variant);
 
-/* Dataset facts: cert = 1 when fp32 arithmetic is provably exact for the
- * uploaded dataset and metric (integer entries, d*range^2 < 2^24 for L2);
- * dp = padded row length in floats. */
+/* Dataset facts: cert bit 0 = fp32 difference-form arithmetic is provably
+ * exact (integer entries, d*range^2 < 2^24 for L2); bit 1 = fp16 rows with
+ * fp32 dot products are exact (integer entries, |v| <= 2048,
+ * 2*d*max|v|^2 < 2^24); dp = padded row length in floats. */
 int knnm_get_info(knnm_ctx *ctx, int32_t *cert, int32_t *dp);
 
 /* Timing / counters. profiling=1 records CUDA events around every phase. */

@@ -158,11 +158,9 @@ def _random_lists(rng, n: int, k: int) -> np.ndarray:
 
 
 def _graph_from(gids, k, metric, ids, dists, sizes) -> KnnGraph:
-    g = KnnGraph(gids, k, metric)
-    g.ids = ids
-    g.dists = dists
-    g.sizes = sizes
-    return g
+    """Wrap exported arrays without allocating placeholder lists; flags are
+    all False like the reference's _export_graph (construct.py:212-223)."""
+    return KnnGraph.from_arrays(gids, k, metric, ids, dists, sizes)
 
 
 def _capture(engine, on_pair) -> None:

@@ -1,6 +1,8 @@
 // knnm.cu -- libknnm.so: context, memory plan and the C-ABI (include/knnm.h)
 // for the B200 S-Merge / J-Merge round engine.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <cmath>
 
 #include <algorithm>
 #include <cstdarg>
@@ -98,7 +100,12 @@ struct knnm_ctx {
     int d = 0, dp = 0, metric = 1;
     bool have_data = false;
     bool cert = false;  // fp32 arithmetic is exact for this dataset + metric
-    int join_variant = -1;  // -1 auto, 0 exact (fp64 every pair), 1 tiled
+    bool cert_dot = false;  // fp16 rows + fp32 dot products are exact (L2)
+    int dph = 0;            // fp16 row length (multiple of 16)
+    DBuf vec16, norms, sub16, subnorms;
+    const __half *sub16p = nullptr;
+    const float *subnormp = nullptr;
+    int join_variant = -1;  // -1 auto, 0 exact (fp64 every pair), 1 tiled, 2 tensor core
     // current merge
     DBuf sub, ugid, labels;
     const float *subp = nullptr;
@@ -111,7 +118,8 @@ struct knnm_ctx {
     bool have_tail = false;
     // round scratch
     DBuf indeg, roff, rev, heavy, giant, gscratch32, nbh, nlen, hpairs, poff, worst0, active;
-    DBuf tcnt, toff, candA, candB, heavy_rows, gscratch64;
+    DBuf bound, boff, mcount, moff, mcur, memb, start, Bd, Bs;
+    uint64_t memb_cap = 0, start_cap = 0;
     DBuf draws, draw_rows, draw_bad, pool;  // random-append draw matrix (device)
     int64_t draw_n = 0;
     int draw_t = 0;
@@ -234,91 +242,56 @@ int scan(knnm_ctx *c, const TI *in, TO *out, int64_t n, int level = 0) {
     return KNNM_OK;
 }
 
-// Bucketing + sequential per-row application of the C_CAND candidate
-// records currently in candA.  key_max = largest key value used.
-int run_updates(knnm_ctx *c, uint64_t key_max) {
-    int keybits = bits_for(key_max);
-    int ib = 64 - keybits;
-    if (ib < 15) return fail(KNNM_ERR_LIMIT, "reference-order keys need %d bits", keybits);
-    int64_t n = c->n;
-    TRY(scan<uint32_t, uint32_t>(c, c->tcnt.as<uint32_t>(), c->toff.as<uint32_t>(), n));
-    unsigned long long *cnt = c->counters.as<unsigned long long>();
-    // scatter (count read on device through a pinned-free path: copy scalar first)
-    CK(cudaMemcpyAsync(c->hcnt, c->counters.p, sizeof(unsigned long long) * C_NUM, cudaMemcpyDeviceToHost, c->st));
-    CK(cudaStreamSynchronize(c->st));
-    unsigned long long ncand = c->hcnt[C_CAND];
-    c->stats.exact_evals += (int64_t)c->hcnt[C_EXACT];
-    if (c->hcnt[C_OVERFLOW]) return fail(KNNM_ERR_LIMIT, "candidate buffer overflow");
-    c->stats.candidates += (int64_t)ncand;
-    if (ncand == 0) return KNNM_OK;
-    k_scatter<<<grid_for(c, (int64_t)ncand, 256), 256, 0, c->st>>>(
-        c->candA.as<CandA>(), ncand, c->toff.as<uint32_t>(), c->tcnt.as<uint32_t>(),
-        c->candB.as<CandB>());
-    CKL();
-    CK(cudaMemsetAsync(cnt + C_HEAVY_APPLY, 0, sizeof(unsigned long long) * 2, c->st));
-    CK(cudaMemsetAsync(cnt + C_MAXC, 0, sizeof(unsigned long long), c->st));
-    int E = (c->k + 31) / 32;
-    int blocks = grid_for(c, n * 32, APPLY_WARPS * 32, 16);
-    if (E == 1)
-        k_apply<1><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
-            n, c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(), ib, c->ids.as<int32_t>(),
-            c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
-            c->heavy_rows.as<int32_t>(), cnt);
-    else
-        k_apply<2><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
-            n, c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(), ib, c->ids.as<int32_t>(),
-            c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
-            c->heavy_rows.as<int32_t>(), cnt);
-    CKL();
-    TRY(sync_counters(c));
-    unsigned long long nheavy = c->hcnt[C_HEAVY_APPLY];
-    if (nheavy == 0) return KNNM_OK;
-    unsigned long long maxc = c->hcnt[C_MAXC];
-    if (bits_for(maxc) > ib) return fail(KNNM_ERR_LIMIT, "row with %llu candidates", maxc);
-    uint32_t p2 = next_pow2((uint32_t)maxc);
-    uint32_t smem_elems = std::min<uint32_t>(p2, (uint32_t)BLOCK_SORT_MAX);
-    size_t hsm = sizeof(uint64_t) * smem_elems;
-    int per_sm = std::max(1, (int)((200u * 1024u) / std::max<size_t>(hsm, 1)));
-    int hgrid = (int)std::min<unsigned long long>(nheavy, (unsigned long long)c->sms * per_sm);
-    if (E == 1)
-        k_apply_heavy<1><<<hgrid, 256, hsm, c->st>>>(
-            c->heavy_rows.as<int32_t>(), c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(), ib,
-            c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
-            c->sizes.as<int32_t>(), cnt, nullptr, (int)smem_elems, c->giant.as<int32_t>());
-    else
-        k_apply_heavy<2><<<hgrid, 256, hsm, c->st>>>(
-            c->heavy_rows.as<int32_t>(), c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(), ib,
-            c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
-            c->sizes.as<int32_t>(), cnt, nullptr, (int)smem_elems, c->giant.as<int32_t>());
-    CKL();
-    if (p2 > (uint32_t)BLOCK_SORT_MAX) {
-        TRY(ensure(c->gscratch64, sizeof(uint64_t) * p2));
-        if (E == 1)
-            k_apply_heavy<1><<<1, 1024, 0, c->st>>>(
-                c->heavy_rows.as<int32_t>(), c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(),
-                ib, c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
-                c->sizes.as<int32_t>(), cnt, c->gscratch64.as<uint64_t>(), BLOCK_SORT_MAX,
-                c->giant.as<int32_t>());
-        else
-            k_apply_heavy<2><<<1, 1024, 0, c->st>>>(
-                c->heavy_rows.as<int32_t>(), c->k, c->toff.as<uint32_t>(), c->candB.as<CandB>(),
-                ib, c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
-                c->sizes.as<int32_t>(), cnt, c->gscratch64.as<uint64_t>(), BLOCK_SORT_MAX,
-                c->giant.as<int32_t>());
-        CKL();
+uint64_t bucket_budget(knnm_ctx *c) { return c->cand_budget_bytes / (sizeof(double) + sizeof(int32_t)); }
+
+int ensure_slots(knnm_ctx *c, uint64_t slots) {
+    TRY(ensure(c->Bd, sizeof(double) * slots));
+    TRY(ensure(c->Bs, sizeof(int32_t) * slots));
+    return KNNM_OK;
+}
+
+int ensure_memb(knnm_ctx *c, uint64_t recs, uint64_t starts) {
+    if (recs > c->memb_cap) {
+        TRY(ensure(c->memb, sizeof(MembRec) * recs));
+        c->memb_cap = recs;
+    }
+    if (starts > c->start_cap) {
+        TRY(ensure(c->start, sizeof(uint32_t) * starts));
+        c->start_cap = starts;
     }
     return KNNM_OK;
 }
 
-int ensure_candidates(knnm_ctx *c, unsigned long long want) {
-    unsigned long long per = sizeof(CandA) + sizeof(CandB);
-    unsigned long long maxrec = c->cand_budget_bytes / per;
-    if (want > maxrec) want = maxrec;
-    if (want < (1ull << 16)) want = 1ull << 16;
-    if (c->cap >= want) return KNNM_OK;
-    TRY(ensure(c->candA, sizeof(CandA) * want));
-    TRY(ensure(c->candB, sizeof(CandB) * want));
-    c->cap = want;
+// Membership ranking: moff = scan(mcount); bucket memberships by row (fill
+// kernel launched by the caller between the two halves); then k_seg_rank.
+int rank_memberships(knnm_ctx *c) {
+    k_seg_rank<<<grid_for(c, c->n * 32, SEG_WARPS * 32, 16), SEG_WARPS * 32, 0, c->st>>>(
+        c->n, c->moff.as<uint32_t>(), c->memb.as<MembRec>(), c->start.as<uint32_t>());
+    CKL();
+    return KNNM_OK;
+}
+
+// Sequential per-row application of the slot buckets (row r: slots
+// [boff[r], boff[r+1]), already in the reference's order).
+int run_updates(knnm_ctx *c) {
+    int64_t n = c->n;
+    unsigned long long *cnt = c->counters.as<unsigned long long>();
+    CK(cudaMemsetAsync(cnt + C_CAND, 0, sizeof(unsigned long long) * 2, c->st));
+    const int E = (c->k + 31) / 32;
+    const int blocks = grid_for(c, n * 32, APPLY_WARPS * 32, 16);
+    if (E == 1)
+        k_apply_stream<1><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
+            n, c->k, c->boff.as<uint64_t>(), c->Bd.as<double>(), c->Bs.as<int32_t>(),
+            c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
+            c->sizes.as<int32_t>(), cnt);
+    else
+        k_apply_stream<2><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
+            n, c->k, c->boff.as<uint64_t>(), c->Bd.as<double>(), c->Bs.as<int32_t>(),
+            c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
+            c->sizes.as<int32_t>(), cnt);
+    CKL();
+    TRY(sync_counters(c));
+    c->stats.candidates += (int64_t)c->hcnt[C_CAND];
     return KNNM_OK;
 }
 
@@ -392,12 +365,9 @@ int knnm_create(int device, knnm_ctx **out) {
     CK(cudaMemset(c->counters.p, 0, sizeof(unsigned long long) * C_NUM));
     CK(cudaFuncSetAttribute(k_rev_heavy, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)(2 * sizeof(uint32_t) * BLOCK_SORT_MAX)));
-    CK(cudaFuncSetAttribute(k_apply_heavy<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(sizeof(uint64_t) * BLOCK_SORT_MAX)));
-    CK(cudaFuncSetAttribute(k_apply_heavy<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)(sizeof(uint64_t) * BLOCK_SORT_MAX)));
     for (auto f : {k_join_exact<0>, k_join_exact<1>, k_join_exact<2>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_join_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (auto f : {k_join_tiled<0, false>, k_join_tiled<1, false>, k_join_tiled<2, false>,
                    k_join_tiled<0, true>, k_join_tiled<1, true>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -412,9 +382,9 @@ int knnm_destroy(knnm_ctx *c) {
     DBuf *all[] = {&c->vec, &c->sub, &c->ugid, &c->labels, &c->ids, &c->dists, &c->flags,
                    &c->sizes, &c->tail_ids, &c->tail_d, &c->tail_s, &c->indeg, &c->roff,
                    &c->rev, &c->heavy, &c->giant, &c->gscratch32, &c->nbh, &c->nlen, &c->hpairs,
-                   &c->poff, &c->worst0, &c->active, &c->tcnt, &c->toff, &c->candA, &c->candB,
-                   &c->heavy_rows, &c->gscratch64, &c->counters, &c->draws, &c->draw_rows,
-                   &c->draw_bad, &c->pool, &c->out_ids, &c->out_d,
+                   &c->poff, &c->worst0, &c->active, &c->bound, &c->boff, &c->mcount, &c->moff, &c->mcur, &c->memb, &c->start, &c->Bd, &c->Bs,
+                   &c->counters, &c->draws, &c->draw_rows,
+                   &c->draw_bad, &c->pool, &c->vec16, &c->norms, &c->sub16, &c->subnorms, &c->out_ids, &c->out_d,
                    &c->out_s, &c->phi_leaf_lo, &c->phi_leaf_len, &c->phi_left, &c->phi_right,
                    &c->phi_level, &c->phi_leaves, &c->phi_inner};
     for (DBuf *b : all) release(*b);
@@ -479,7 +449,18 @@ int knnm_set_dataset(knnm_ctx *c, const float *vectors, int64_t n_all, int32_t d
         c->cert = false;
         if (ints && metric == KNNM_L2) c->cert = (double)d * range * range < 16777216.0;
         if (ints && metric == KNNM_L1) c->cert = (double)d * range < 16777216.0;
+        const double maxabs = std::max(std::fabs(mx), std::fabs(mn));
+        c->cert_dot = ints && metric == KNNM_L2 && maxabs <= 2048.0 &&
+                      2.0 * (double)d * maxabs * maxabs < 16777216.0;
         CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
+        if (c->cert_dot) {
+            c->dph = (d + 15) & ~15;
+            TRY(ensure(c->vec16, sizeof(__half) * (size_t)n_all * c->dph));
+            TRY(ensure(c->norms, sizeof(float) * (size_t)n_all));
+            k_to_half<<<grid_for(c, n_all * 32, 256, 16), 256, 0, c->st>>>(
+                c->vec.as<float>(), dp, n_all, c->dph, c->vec16.as<__half>(), c->norms.as<float>());
+            CKL();
+        }
     }
     c->begun = false;
     return KNNM_OK;
@@ -500,6 +481,22 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     TRY(ensure(c->ugid, sizeof(int64_t) * n));
     TRY(h2d(c, c->ugid.p, union_gids, sizeof(int64_t) * n));
     bool identity = (n == c->n_all && union_gids[0] == 0 && union_gids[n - 1] == n - 1);
+    c->sub16p = c->vec16.as<__half>();
+    c->subnormp = c->norms.as<float>();
+    if (c->cert_dot && !identity) {
+        TRY(ensure(c->sub16, sizeof(__half) * (size_t)n * c->dph));
+        TRY(ensure(c->subnorms, sizeof(float) * (size_t)n));
+        k_gather_rows<<<grid_for(c, n * (c->dph / 8), 256), 256, 0, c->st>>>(
+            reinterpret_cast<const float *>(c->vec16.p), c->dph / 2, c->ugid.as<int64_t>(), n,
+            c->sub16.as<float>());
+        CKL();
+        k_gather_norms<<<grid_for(c, n, 256), 256, 0, c->st>>>(c->norms.as<float>(),
+                                                                c->ugid.as<int64_t>(), n,
+                                                                c->subnorms.as<float>());
+        CKL();
+        c->sub16p = c->sub16.as<__half>();
+        c->subnormp = c->subnorms.as<float>();
+    }
     if (identity) {
         c->subp = c->vec.as<float>();
     } else {
@@ -533,10 +530,11 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     TRY(ensure(c->poff, sizeof(uint64_t) * (n + 1)));
     TRY(ensure(c->worst0, sizeof(double) * n));
     TRY(ensure(c->active, sizeof(int32_t) * n));
-    TRY(ensure(c->tcnt, sizeof(uint32_t) * (n + 1)));
-    TRY(ensure(c->toff, sizeof(uint32_t) * (n + 1)));
-    TRY(ensure(c->heavy_rows, sizeof(int32_t) * n));
-    CK(cudaMemsetAsync(c->tcnt.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+    TRY(ensure(c->bound, sizeof(uint32_t) * (n + 1)));
+    TRY(ensure(c->boff, sizeof(uint64_t) * (n + 1)));
+    TRY(ensure(c->mcount, sizeof(uint32_t) * (n + 1)));
+    TRY(ensure(c->moff, sizeof(uint32_t) * (n + 1)));
+    TRY(ensure(c->mcur, sizeof(uint32_t) * (n + 1)));
     CK(cudaMemsetAsync(c->indeg.p, 0, sizeof(uint32_t) * (n + 1), c->st));
     c->tk = 0;
     c->have_tail = false;
@@ -618,7 +616,6 @@ static int insert_impl(knnm_ctx *c, const int32_t *rows, int64_t mrows, int32_t 
     if (m == 0) return KNNM_OK;
     if (!rows || (!nids && !nids_on_device)) return fail(KNNM_ERR_ARG, "null argument");
     CK(cudaSetDevice(c->device));
-    TRY(ensure_candidates(c, (unsigned long long)m));
     TRY(ensure(c->stage[0], sizeof(int32_t) * m));
     TRY(ensure(c->stage[1], sizeof(int32_t) * m));
     if (count > 0) {
@@ -638,22 +635,40 @@ static int insert_impl(knnm_ctx *c, const int32_t *rows, int64_t mrows, int32_t 
     }
     unsigned long long *cnt = c->counters.as<unsigned long long>();
     int64_t acc_total = 0;
-    for (int64_t c0 = 0; c0 < m; c0 += (int64_t)c->cap) {
-        int64_t cm = std::min<int64_t>((int64_t)c->cap, m - c0);
+    const int64_t chunk = (int64_t)std::max<uint64_t>(bucket_budget(c), 1u << 20);
+    for (int64_t c0 = 0; c0 < m; c0 += chunk) {
+        const int64_t cm = std::min<int64_t>(chunk, m - c0);
+        const int32_t *rows_d = c->stage[0].as<int32_t>() + c0;
         CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
         {
             PhaseTimer pt(c, PH_OTHER);
-            k_directed_emit<<<(unsigned)((cm + 255) / 256), 256, 0, c->st>>>(
-                c->stage[0].as<int32_t>() + c0, c->stage[1].as<int32_t>() + c0, cm, c0, c->subp,
-                c->dp, c->d, c->metric, c->sizes.as<int32_t>(), c->dists.as<double>(), c->k,
-                c->candA.as<CandA>(), c->tcnt.as<uint32_t>(), cnt, capd ? capd + c0 : nullptr);
+            // ordinal memberships of weight 1: slot = rank of the entry
+            // among the entries of its row (apply_updates_directed order)
+            CK(cudaMemsetAsync(c->mcount.p, 0, sizeof(uint32_t) * (c->n + 1), c->st));
+            CK(cudaMemsetAsync(c->mcur.p, 0, sizeof(uint32_t) * (c->n + 1), c->st));
+            k_directed_memb<false><<<grid_for(c, cm, 256), 256, 0, c->st>>>(
+                rows_d, cm, c->mcount.as<uint32_t>(), nullptr, nullptr, nullptr);
+            CKL();
+            TRY(scan<uint32_t, uint32_t>(c, c->mcount.as<uint32_t>(), c->moff.as<uint32_t>(), c->n));
+            TRY(scan<uint32_t, uint64_t>(c, c->mcount.as<uint32_t>(), c->boff.as<uint64_t>(), c->n));
+            TRY(ensure_memb(c, (uint64_t)cm, (uint64_t)cm));
+            TRY(ensure_slots(c, (uint64_t)cm));
+            k_directed_memb<true><<<grid_for(c, cm, 256), 256, 0, c->st>>>(
+                rows_d, cm, nullptr, c->moff.as<uint32_t>(), c->mcur.as<uint32_t>(),
+                c->memb.as<MembRec>());
+            CKL();
+            TRY(rank_memberships(c));
+            k_directed_emit<<<grid_for(c, cm, 256, 32), 256, 0, c->st>>>(
+                rows_d, c->stage[1].as<int32_t>() + c0, cm, c->subp, c->dp, c->d, c->metric,
+                c->sizes.as<int32_t>(), c->dists.as<double>(), c->k, c->boff.as<uint64_t>(),
+                c->start.as<uint32_t>(), c->Bd.as<double>(), c->Bs.as<int32_t>(),
+                capd ? capd + c0 : nullptr);
             CKL();
         }
         {
             PhaseTimer pt(c, PH_UPDATE);
-            TRY(run_updates(c, (uint64_t)(c0 + cm)));
+            TRY(run_updates(c));
         }
-        TRY(sync_counters(c));
         acc_total += (int64_t)c->hcnt[C_ACCEPTED];
     }
     c->stats.init_evals += m;
@@ -857,114 +872,135 @@ int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, 
 
     int64_t acc_total = 0;
     if (P > 0) {
-        TRY(ensure_candidates(c, 2 * P));
-        uint64_t key_max = ((uint64_t)n * W) * W;
+        const uint64_t key_max = ((uint64_t)n * W) * W;
         size_t smem = sizeof(float) * (size_t)W * c->dp;
         size_t smem_tiled = sizeof(float) * (size_t)W * (c->dp + 4);
         if (smem > 200 * 1024) return fail(KNNM_ERR_LIMIT, "neighbourhood of %d x %d floats exceeds shared memory", W, c->dp);
-        const bool tiled = c->join_variant == 1 || (c->join_variant < 0 && smem_tiled <= 96 * 1024);
+        const int Wp = W + 16;
+        const size_t mj_per_warp = mj_meta_bytes(Wp) + (size_t)Wp * (c->dph * 2 + 16);
+        const size_t smem_mma = MJ_WARPS * mj_per_warp;
+        const bool use_mma = c->cert_dot && smem_mma <= 200 * 1024 &&
+                             (c->join_variant == 2 || c->join_variant < 0);
+        const bool tiled = !use_mma && (c->join_variant == 1 || (c->join_variant < 0 && smem_tiled <= 96 * 1024));
         const double mrel = 1.0 + (double)(c->d + 8) * ldexp(1.0, -23);
         const double mabs = (double)(4 * c->d + 64) * ldexp(1.0, -24);
-        auto launch_join = [&](const int32_t *act, unsigned nblocks) -> int {
-            PhaseTimer pt(c, PH_JOIN);
-            if (tiled) {
-                const void *fn;
-                if (c->metric == 1) fn = c->cert ? (const void *)k_join_tiled<1, true> : (const void *)k_join_tiled<1, false>;
-                else if (c->metric == 2) fn = (const void *)k_join_tiled<2, false>;
-                else fn = c->cert ? (const void *)k_join_tiled<0, true> : (const void *)k_join_tiled<0, false>;
-                int per_sm = 1;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TJ_THREADS, smem_tiled));
-                unsigned grid = (unsigned)std::min<int64_t>((int64_t)nblocks, (int64_t)c->sms * std::max(per_sm, 1));
-                if (grid == 0) grid = 1;
-                int na = (int)nblocks;
+        // One pass per hood chunk: bounds -> bucket offsets -> join -> apply.
+        auto run_chunk = [&](const int32_t *act, int64_t nact, uint64_t pairs2) -> int {
+            CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
+            {
+                PhaseTimer pt(c, PH_JOIN);
+                // reference-order slot layout (see MembRec in knnm_kernels.cuh)
+                CK(cudaMemsetAsync(c->bound.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+                CK(cudaMemsetAsync(c->mcount.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+                CK(cudaMemsetAsync(c->mcur.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+                const int hgrid = grid_for(c, nact * 32, 256, 16);
+                k_hood_memb<false><<<hgrid, 256, 0, c->st>>>(
+                    act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
+                    c->labels.as<int8_t>(), mode, c->bound.as<uint32_t>(), c->mcount.as<uint32_t>(),
+                    nullptr, nullptr, nullptr);
+                CKL();
+                TRY(scan<uint32_t, uint64_t>(c, c->bound.as<uint32_t>(), c->boff.as<uint64_t>(), n));
+                TRY(scan<uint32_t, uint32_t>(c, c->mcount.as<uint32_t>(), c->moff.as<uint32_t>(), n));
+                TRY(ensure_memb(c, (uint64_t)n * W, (uint64_t)n * W));
+                TRY(ensure_slots(c, pairs2));
+                k_hood_memb<true><<<hgrid, 256, 0, c->st>>>(
+                    act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
+                    c->labels.as<int8_t>(), mode, nullptr, nullptr, c->moff.as<uint32_t>(),
+                    c->mcur.as<uint32_t>(), c->memb.as<MembRec>());
+                CKL();
+                TRY(rank_memberships(c));
+                const uint64_t *boff = c->boff.as<uint64_t>();
+                const uint32_t *stt = c->start.as<uint32_t>();
+                double *Bd = c->Bd.as<double>();
+                int32_t *Bs = c->Bs.as<int32_t>();
+                if (use_mma) {
+                    int per_sm = 1;
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_join_mma, MJ_WARPS * 32,
+                                                                     smem_mma));
+                    unsigned grid = (unsigned)std::min<int64_t>((nact + MJ_WARPS - 1) / MJ_WARPS,
+                                                                (int64_t)c->sms * std::max(per_sm, 1));
+                    if (grid == 0) grid = 1;
+                    k_join_mma<<<grid, MJ_WARPS * 32, smem_mma, c->st>>>(
+                        act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
+                        c->labels.as<int8_t>(), mode, c->sub16p, c->dph, c->subnormp,
+                        c->worst0.as<double>(), boff, stt, Bd, Bs);
+                } else if (tiled) {
+                    const void *fn;
+                    if (c->metric == 1) fn = c->cert ? (const void *)k_join_tiled<1, true> : (const void *)k_join_tiled<1, false>;
+                    else if (c->metric == 2) fn = (const void *)k_join_tiled<2, false>;
+                    else fn = c->cert ? (const void *)k_join_tiled<0, true> : (const void *)k_join_tiled<0, false>;
+                    int per_sm = 1;
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TJ_THREADS, smem_tiled));
+                    unsigned grid = (unsigned)std::min<int64_t>(nact, (int64_t)c->sms * std::max(per_sm, 1));
+                    if (grid == 0) grid = 1;
+                    int na = (int)nact;
 #define KNNM_TJ_ARGS                                                                          \
     act, na, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,  \
-        c->subp, c->dp, c->d, c->worst0.as<double>(), c->candA.as<CandA>(), c->cap,          \
-        c->tcnt.as<uint32_t>(), cnt, mrel, mabs
-                if (c->metric == 1 && c->cert)
-                    k_join_tiled<1, true><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
-                else if (c->metric == 1)
-                    k_join_tiled<1, false><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
-                else if (c->metric == 2)
-                    k_join_tiled<2, false><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
-                else if (c->cert)
-                    k_join_tiled<0, true><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
-                else
-                    k_join_tiled<0, false><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+        c->subp, c->dp, c->d, c->worst0.as<double>(), boff, stt, Bd, Bs, cnt, mrel, mabs
+                    if (c->metric == 1 && c->cert)
+                        k_join_tiled<1, true><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+                    else if (c->metric == 1)
+                        k_join_tiled<1, false><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+                    else if (c->metric == 2)
+                        k_join_tiled<2, false><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+                    else if (c->cert)
+                        k_join_tiled<0, true><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+                    else
+                        k_join_tiled<0, false><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
 #undef KNNM_TJ_ARGS
+                } else {
+#define KNNM_JE_ARGS                                                                          \
+    act, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,       \
+        c->subp, c->dp, c->d, c->worst0.as<double>(), boff, stt, Bd, Bs
+                    if (c->metric == 1)
+                        k_join_exact<1><<<(unsigned)nact, JOIN_THREADS, smem, c->st>>>(KNNM_JE_ARGS);
+                    else if (c->metric == 2)
+                        k_join_exact<2><<<(unsigned)nact, JOIN_THREADS, smem, c->st>>>(KNNM_JE_ARGS);
+                    else
+                        k_join_exact<0><<<(unsigned)nact, JOIN_THREADS, smem, c->st>>>(KNNM_JE_ARGS);
+#undef KNNM_JE_ARGS
+                }
                 CKL();
                 c->stats.join_launches += 1;
-                return KNNM_OK;
             }
-            if (c->metric == 1)
-                k_join_exact<1><<<nblocks, JOIN_THREADS, smem, c->st>>>(
-                    act, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,
-                    c->subp, c->dp, c->d, c->worst0.as<double>(), c->candA.as<CandA>(), c->cap,
-                    c->tcnt.as<uint32_t>(), cnt);
-            else if (c->metric == 2)
-                k_join_exact<2><<<nblocks, JOIN_THREADS, smem, c->st>>>(
-                    act, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,
-                    c->subp, c->dp, c->d, c->worst0.as<double>(), c->candA.as<CandA>(), c->cap,
-                    c->tcnt.as<uint32_t>(), cnt);
-            else
-                k_join_exact<0><<<nblocks, JOIN_THREADS, smem, c->st>>>(
-                    act, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,
-                    c->subp, c->dp, c->d, c->worst0.as<double>(), c->candA.as<CandA>(), c->cap,
-                    c->tcnt.as<uint32_t>(), cnt);
-            CKL();
-            c->stats.join_launches += 1;
+            {
+                PhaseTimer pt(c, PH_UPDATE);
+                TRY(run_updates(c));
+            }
+            c->stats.exact_evals += (int64_t)c->hcnt[C_EXACT];
+            acc_total += (int64_t)c->hcnt[C_ACCEPTED];
             return KNNM_OK;
         };
-        bool done = false;
-        {
-            // Single shot over all active hoods.  Guaranteed to fit when
-            // 2P <= cap; otherwise optimistic (the exact prefilter keeps far
-            // fewer than 2P candidates) with a chunked redo on overflow --
-            // the lists are untouched until the apply phase, so a redo is safe.
-            TRY(launch_join(c->active.as<int32_t>(), (unsigned)nactive));
-            TRY(sync_counters(c));
-            if (c->hcnt[C_CAND] <= c->cap) {
-                {
-                    PhaseTimer pt(c, PH_UPDATE);
-                    TRY(run_updates(c, key_max));
-                }
-                TRY(sync_counters(c));
-                acc_total = (int64_t)c->hcnt[C_ACCEPTED];
-                done = true;
-            } else {
-                c->stats.join_redos += 1;
-                CK(cudaMemsetAsync(c->tcnt.p, 0, sizeof(uint32_t) * (n + 1), c->st));
-            }
-        }
-        if (!done) {
-            // Chunk hoods by index so each chunk's worst case fits; chunks run
-            // in ascending hood order, preserving the reference's per-row order.
+        const uint64_t budget = bucket_budget(c);
+        if (2 * P <= budget) {
+            TRY(run_chunk(c->active.as<int32_t>(), (int64_t)nactive, 2 * P));
+        } else {
+            // Chunk hoods by index so each chunk's buckets fit; chunks run in
+            // ascending hood order, which preserves the reference's per-row
+            // order (keys are (u, p, q)).
             std::vector<uint64_t> hpoff(n + 1);
-            TRY(d2h(c, hpoff.data(), c->poff.p, sizeof(uint64_t) * (n + 1)));
-            CK(cudaStreamSynchronize(c->st));
-            // the compacted list is not ordered; build per-chunk lists on host
             std::vector<uint32_t> hh(n);
-            CK(cudaMemcpy(hh.data(), c->hpairs.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost));
-            uint64_t budget = c->cap / 2;
+            CK(cudaMemcpyAsync(hpoff.data(), c->poff.p, sizeof(uint64_t) * (n + 1),
+                               cudaMemcpyDeviceToHost, c->st));
+            CK(cudaMemcpyAsync(hh.data(), c->hpairs.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost,
+                               c->st));
+            CK(cudaStreamSynchronize(c->st));
+            c->stats.join_redos += 1;
             int64_t lo = 0;
+            std::vector<int32_t> lst;
             while (lo < n) {
                 int64_t hi = lo;
-                std::vector<int32_t> lst;
-                while (hi < n && (hpoff[hi + 1] - hpoff[lo] <= budget || hi == lo)) {
+                lst.clear();
+                while (hi < n && (2 * (hpoff[hi + 1] - hpoff[lo]) <= budget || hi == lo)) {
                     if (hh[hi]) lst.push_back((int32_t)hi);
                     hi++;
                 }
                 if (!lst.empty()) {
-                    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
                     CK(cudaMemcpyAsync(c->active.p, lst.data(), sizeof(int32_t) * lst.size(),
                                        cudaMemcpyHostToDevice, c->st));
-                    TRY(launch_join(c->active.as<int32_t>(), (unsigned)lst.size()));
-                    {
-                        PhaseTimer pt(c, PH_UPDATE);
-                        TRY(run_updates(c, key_max));
-                    }
-                    TRY(sync_counters(c));
-                    acc_total += (int64_t)c->hcnt[C_ACCEPTED];
+                    TRY(run_chunk(c->active.as<int32_t>(), (int64_t)lst.size(),
+                                  2 * (hpoff[hi] - hpoff[lo])));
+                    CK(cudaStreamSynchronize(c->st));  // lst is reused
                 }
                 lo = hi;
             }
@@ -1117,14 +1153,14 @@ int knnm_capture_fetch(knnm_ctx *c, int32_t *pa, int32_t *pb, double *pd, int64_
 }
 
 int knnm_set_join_variant(knnm_ctx *c, int32_t variant) {
-    if (!c || variant < -1 || variant > 1) return fail(KNNM_ERR_ARG, "variant %d", variant);
+    if (!c || variant < -1 || variant > 2) return fail(KNNM_ERR_ARG, "variant %d", variant);
     c->join_variant = variant;
     return KNNM_OK;
 }
 
 int knnm_get_info(knnm_ctx *c, int32_t *cert, int32_t *dp) {
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
-    if (cert) *cert = c->cert ? 1 : 0;
+    if (cert) *cert = (c->cert ? 1 : 0) | (c->cert_dot ? 2 : 0);
     if (dp) *dp = c->dp;
     return KNNM_OK;
 }

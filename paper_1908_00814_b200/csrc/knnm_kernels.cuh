@@ -3,27 +3,72 @@
 // Each kernel cites the reference numba kernel (pkg/src/knnmerge/_kernels.py)
 // whose result it reproduces bit-for-bit.  Design notes live in DESIGN.md.
 #pragma once
+#include <cuda_fp16.h>
+
 #include "knnm_device.cuh"
 
 namespace knnm {
 
 constexpr int WARP_REV_MAX = 256;      // reverse segments a warp sorts itself
 constexpr int BLOCK_SORT_MAX = 16384;  // elements a block sorts in shared memory
-constexpr int APPLY_WARP_MAX = 1024;   // candidates per row handled by one warp
 constexpr int MAX_W = 128;             // k + rev_cap upper bound
+constexpr int SEG_SMEM = 256;          // membership segments ranked in shared memory
 
-struct CandA {  // emitted directed update (unsorted)
-    uint64_t key;  // reference order: (u*W + p)*W + q, or the init ordinal
-    double d;
-    int32_t src;
-    int32_t tgt;
+// Reference-order slots.  Row r's update bucket has one slot per admissible
+// (hood, partner) pair it takes part in, laid out in the reference's
+// sequential order: hoods ascending, then partner position ascending (pairs
+// (x, p) with x < p, then (p, x) with x > p, _kernels.py:424-436).  Slot
+// base of (hood u, member at position p) = boff[r] + start[u * W + p]; the
+// partner's rank within the hood comes from per-class position prefix counts.
+struct MembRec {  // one (hood, member) membership, bucketed by member row
+    uint64_t key;    // hood id (or directed-insert ordinal)
+    uint32_t weight; // slots the membership occupies (admissible partners)
+    uint32_t out;    // where its exclusive rank goes: u * W + p (or ordinal)
 };
-struct CandB {  // bucketed by target row
-    uint64_t key;
-    double d;
-    int32_t src;
-    int32_t pad;
-};
+
+// Admissible partner classes of a member, by pair mode and member class
+// (class = (label != 0) * 2 + !new; _kernels.py:391-399).  bit c set ->
+// members of class c are partners; SELF: the member's own class is in the
+// mask (it is not its own partner).
+__host__ __device__ __forceinline__ int partner_mask(int mode, int cls) {
+    if (mode == 0) return cls == 0 ? 0x3 : 0x1;
+    if (mode == 1) return cls == 0 ? 0xC : cls == 1 ? 0x4 : cls == 2 ? 0x3 : 0x1;
+    return cls == 0 ? 0xC : cls == 1 ? 0x4 : cls == 2 ? 0xF : 0x5;
+}
+__host__ __device__ __forceinline__ bool partner_self(int mode, int cls) {
+    return (mode == 0 && cls == 0) || (mode == 2 && cls == 2);
+}
+
+// P[c * (MAX_W + 1) + x] = members of class c at nbh positions < x.
+typedef uint8_t PosPrefix[4 * (MAX_W + 1)];
+
+// Rank of partner position px among the admissible partners of the member
+// (class ct, position pt) -- the slot offset inside the membership's range.
+__device__ __forceinline__ uint32_t pair_rank(const uint8_t *__restrict__ P, int mode, int ct, int pt,
+                                              int px) {
+    const int mk = partner_mask(mode, ct);
+    uint32_t r = 0;
+#pragma unroll
+    for (int c = 0; c < 4; c++)
+        if (mk & (1 << c)) r += P[c * (MAX_W + 1) + px];
+    if (partner_self(mode, ct) && pt < px) r -= 1;
+    return r;
+}
+
+// Warp-cooperative: fill P from the per-position classes clsv[b] of lanes
+// (position b * 32 + lane; class 4 = no member).
+__device__ __forceinline__ void build_pos_prefix(uint8_t *P, const int (&clsv)[4], unsigned lane) {
+    int base[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            const unsigned mk = __ballot_sync(FULL_MASK, clsv[b] == c);
+            P[c * (MAX_W + 1) + b * 32 + lane] = (uint8_t)(base[c] + __popc(mk & lanemask_lt()));
+            base[c] += __popc(mk);
+        }
+    }
+}
 
 // ---------------------------------------------------------------------------
 // Scan: exclusive prefix sum, out has n+1 entries (out[n] = total).
@@ -87,6 +132,13 @@ __global__ void k_scan_total(TO *__restrict__ out, int64_t n, const TO *__restri
 // ---------------------------------------------------------------------------
 // State setup
 // ---------------------------------------------------------------------------
+__global__ void k_gather_norms(const float *__restrict__ src, const int64_t *__restrict__ gids,
+                               int64_t n, float *__restrict__ dst) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[gids[i]];
+}
+
 __global__ void k_gather_rows(const float *__restrict__ src, int dp, const int64_t *__restrict__ gids,
                               int64_t n, float *__restrict__ dst) {
     int64_t q = dp / 4;
@@ -211,32 +263,20 @@ __global__ void k_pool_map(const int64_t *__restrict__ cand, int64_t m, const in
 // (_eval_pairs -> pair_dists_dense, then apply_updates_directed order).
 // ---------------------------------------------------------------------------
 __global__ void k_directed_emit(const int32_t *__restrict__ rows, const int32_t *__restrict__ nids,
-                                int64_t m, int64_t key0, const float *__restrict__ sub, int dp,
-                                int d, int tag, const int32_t *__restrict__ sizes,
-                                const double *__restrict__ dists, int k, CandA *A, uint32_t *tcnt,
-                                unsigned long long *counters, double *cap_d) {
-    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    bool valid = i < m;
-    bool emit = false;
-    int32_t r = 0, s = 0;
-    double dd = 0.0;
-    if (valid) {
-        r = rows[i];
-        s = nids[i];
-        dd = exact_dist_tag(tag, sub + (int64_t)r * dp, sub + (int64_t)s * dp, d);
+                                int64_t m, const float *__restrict__ sub, int dp, int d, int tag,
+                                const int32_t *__restrict__ sizes, const double *__restrict__ dists,
+                                int k, const uint64_t *__restrict__ boff,
+                                const uint32_t *__restrict__ start, double *__restrict__ Bd,
+                                int32_t *__restrict__ Bs, double *cap_d) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = rows[i], s = nids[i];
+        const double dd = exact_dist_tag(tag, sub + (int64_t)r * dp, sub + (int64_t)s * dp, d);
         if (cap_d) cap_d[i] = dd;
-        // exact-safe prefilter: the row is untouched until the apply phase
-        emit = !(sizes[r] == k && dd >= dists[(int64_t)r * k + k - 1]);
-    }
-    unsigned lane = lane_id();
-    unsigned mk = __ballot_sync(FULL_MASK, emit);
-    unsigned long long base = 0;
-    if (lane == 0 && mk) base = atomicAdd(&counters[C_CAND], (unsigned long long)__popc(mk));
-    base = __shfl_sync(FULL_MASK, base, 0);
-    if (emit) {
-        unsigned long long pos = base + __popc(mk & lanemask_lt());
-        A[pos] = CandA{(uint64_t)(key0 + i), dd, s, r};
-        atomicAdd(&tcnt[r], 1u);
+        const uint64_t slot = boff[r] + start[i];
+        Bd[slot] = dd;
+        // the source id is only ever read for a candidate that can pass
+        if (!(sizes[r] == k && dd >= dists[(int64_t)r * k + k - 1])) Bs[slot] = s;
     }
 }
 
@@ -485,64 +525,57 @@ __global__ void __launch_bounds__(JOIN_THREADS)
 k_join_exact(const int32_t *__restrict__ active, const uint32_t *__restrict__ nbh,
              const int32_t *__restrict__ nlen, int W, const int8_t *__restrict__ labels, int mode,
              const float *__restrict__ sub, int dp, int d, const double *__restrict__ worst0,
-             CandA *A, unsigned long long cap, uint32_t *tcnt, unsigned long long *counters) {
+             const uint64_t *__restrict__ boff, const uint32_t *__restrict__ start,
+             double *__restrict__ Bd, int32_t *__restrict__ Bs) {
     extern __shared__ float4 sv4[];
     __shared__ int s_id[MAX_W];
     __shared__ int s_new[MAX_W];
-    __shared__ int s_lab[MAX_W];
+    __shared__ int s_cls[MAX_W];
     __shared__ double s_w[MAX_W];
+    __shared__ uint64_t s_st[MAX_W];
+    __shared__ PosPrefix s_P;
     const float *sv = reinterpret_cast<const float *>(sv4);
-    int64_t u = active[blockIdx.x];
-    int w = nlen[u];
-    for (int i = threadIdx.x; i < w; i += blockDim.x) {
-        uint32_t e = nbh[u * W + i];
-        int id = (int)(e >> 1);
-        s_id[i] = id;
-        s_new[i] = e & 1;
-        s_lab[i] = labels[id];
-        s_w[i] = worst0[id];
+    const int64_t u = active[blockIdx.x];
+    const int w = nlen[u];
+    if (threadIdx.x < 32) {
+        const unsigned lane = lane_id();
+        int clsv[4];
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const int j = b * 32 + (int)lane;
+            clsv[b] = 4;
+            if (j < w) {
+                const uint32_t e = nbh[u * W + j];
+                const int id = (int)(e >> 1);
+                const int lab = mode == 0 ? 0 : (labels[id] != 0);
+                clsv[b] = lab * 2 + ((e & 1) ? 0 : 1);
+                s_id[j] = id;
+                s_new[j] = e & 1;
+                s_cls[j] = clsv[b];
+                s_w[j] = worst0[id];
+                s_st[j] = boff[id] + start[u * W + j];
+            }
+        }
+        build_pos_prefix(s_P, clsv, lane);
     }
     __syncthreads();
-    int q4 = dp >> 2;
+    const int q4 = dp >> 2;
     for (int i = threadIdx.x; i < w * q4; i += blockDim.x) {
-        int r = i / q4, c = i - r * q4;
+        const int r = i / q4, c = i - r * q4;
         sv4[i] = __ldg(reinterpret_cast<const float4 *>(sub + (int64_t)s_id[r] * dp) + c);
     }
     __syncthreads();
-    unsigned lane = lane_id();
-    int total = w * w;
-    for (int base = 0; base < total; base += blockDim.x) {
-        int L = base + threadIdx.x;
-        int p = L / w, q = L - (L / w) * w;
-        bool ok = L < total && q > p && admissible(s_new[p], s_new[q], s_lab[p], s_lab[q], mode);
-        double dd = 0.0;
-        if (ok) dd = exact_dist<TAG>(sv + p * dp, sv + q * dp, d);
-        bool e1 = ok && dd < s_w[p];  // id[p] <- id[q]
-        bool e2 = ok && dd < s_w[q];  // id[q] <- id[p]
-        unsigned m1 = __ballot_sync(FULL_MASK, e1), m2 = __ballot_sync(FULL_MASK, e2);
-        int tot = __popc(m1) + __popc(m2);
-        unsigned long long b0 = 0;
-        if (lane == 0 && tot) b0 = atomicAdd(&counters[C_CAND], (unsigned long long)tot);
-        b0 = __shfl_sync(FULL_MASK, b0, 0);
-        uint64_t key = ((uint64_t)u * W + p) * W + q;
-        if (e1) {
-            unsigned long long pos = b0 + __popc(m1 & lanemask_lt());
-            if (pos < cap) {
-                A[pos] = CandA{key, dd, s_id[q], s_id[p]};
-                atomicAdd(&tcnt[s_id[p]], 1u);
-            } else {
-                atomicAdd(&counters[C_OVERFLOW], 1ull);
-            }
-        }
-        if (e2) {
-            unsigned long long pos = b0 + __popc(m1) + __popc(m2 & lanemask_lt());
-            if (pos < cap) {
-                A[pos] = CandA{key, dd, s_id[p], s_id[q]};
-                atomicAdd(&tcnt[s_id[q]], 1u);
-            } else {
-                atomicAdd(&counters[C_OVERFLOW], 1ull);
-            }
-        }
+    const int total = w * w;
+    for (int L = threadIdx.x; L < total; L += blockDim.x) {
+        const int p = L / w, q = L - (L / w) * w;
+        if (q <= p || !admissible(s_new[p], s_new[q], s_cls[p] >> 1, s_cls[q] >> 1, mode)) continue;
+        const double dd = exact_dist<TAG>(sv + p * dp, sv + q * dp, d);
+        const uint64_t spq = s_st[p] + pair_rank(s_P, mode, s_cls[p], p, q);
+        const uint64_t sqp = s_st[q] + pair_rank(s_P, mode, s_cls[q], q, p);
+        Bd[spq] = dd;
+        Bd[sqp] = dd;
+        if (dd < s_w[p]) Bs[spq] = s_id[q];
+        if (dd < s_w[q]) Bs[sqp] = s_id[p];
     }
 }
 
@@ -608,7 +641,8 @@ __global__ void __launch_bounds__(TJ_THREADS)
 k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
              const int32_t *__restrict__ nlen, int W, const int8_t *__restrict__ labels, int mode,
              const float *__restrict__ sub, int dp, int d, const double *__restrict__ worst0,
-             CandA *A, unsigned long long cap, uint32_t *tcnt, unsigned long long *counters,
+             const uint64_t *__restrict__ boff, const uint32_t *__restrict__ start,
+             double *__restrict__ Bd, int32_t *__restrict__ Bs, unsigned long long *counters,
              double mrel, double mabs) {
     extern __shared__ __align__(128) float4 sv4[];
     __shared__ int s_id[MAX_W];
@@ -616,6 +650,9 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
     __shared__ int s_new[MAX_W];
     __shared__ double s_w[MAX_W];
     __shared__ float s_nrm[MAX_W];
+    __shared__ uint64_t s_st[MAX_W];
+    __shared__ int s_sc[MAX_W];
+    __shared__ PosPrefix s_P;
     __shared__ int s_cls[4];
     __shared__ __align__(8) uint64_t s_bar;
     const float *sv = reinterpret_cast<const float *>(sv4);
@@ -634,60 +671,65 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
         const int w = nlen[u];
         // ---- classify members: class = (label != 0) * 2 + (!new) ----------
         if (tid < 32) {
+            uint32_t ev[4];
+            int clsv[4];
             int cnts[4] = {0, 0, 0, 0};
-            int base_cls[4];
-            // first pass: class counts
-            for (int b = 0; b < w; b += 32) {
-                int j = b + lane;
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                const int j = b * 32 + (int)lane;
+                ev[b] = j < w ? nbh[u * W + j] : 0u;
+            }
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                const int j = b * 32 + (int)lane;
                 int cls = 4;
                 if (j < w) {
-                    uint32_t e = nbh[u * W + j];
-                    int lab = mode == 0 ? 0 : (labels[e >> 1] != 0);
-                    cls = lab * 2 + ((e & 1) ? 0 : 1);
+                    const int lab = mode == 0 ? 0 : (labels[ev[b] >> 1] != 0);
+                    cls = lab * 2 + ((ev[b] & 1) ? 0 : 1);
                 }
+                clsv[b] = cls;
 #pragma unroll
                 for (int c = 0; c < 4; c++) cnts[c] += __popc(__ballot_sync(FULL_MASK, cls == c));
             }
-            base_cls[0] = 0;
-            base_cls[1] = cnts[0];
-            base_cls[2] = cnts[0] + cnts[1];
-            base_cls[3] = base_cls[2] + cnts[2];
+            const int base_cls[4] = {0, cnts[0], cnts[0] + cnts[1], cnts[0] + cnts[1] + cnts[2]};
             int fill[4] = {0, 0, 0, 0};
-            for (int b = 0; b < w; b += 32) {
-                int j = b + lane;
-                int cls = 4;
-                uint32_t e = 0;
-                if (j < w) {
-                    e = nbh[u * W + j];
-                    int lab = mode == 0 ? 0 : (labels[e >> 1] != 0);
-                    cls = lab * 2 + ((e & 1) ? 0 : 1);
-                }
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                const int j = b * 32 + (int)lane;
 #pragma unroll
                 for (int c = 0; c < 4; c++) {
-                    unsigned m = __ballot_sync(FULL_MASK, cls == c);
-                    if (cls == c) {
-                        int slot = base_cls[c] + fill[c] + __popc(m & lanemask_lt());
-                        int id = (int)(e >> 1);
+                    const unsigned m = __ballot_sync(FULL_MASK, clsv[b] == c);
+                    if (clsv[b] == c) {
+                        const int slot = base_cls[c] + fill[c] + __popc(m & lanemask_lt());
+                        const int id = (int)(ev[b] >> 1);
                         s_id[slot] = id;
                         s_pos[slot] = j;
-                        s_new[slot] = (int)(e & 1);
+                        s_new[slot] = (int)(ev[b] & 1);
+                        s_sc[slot] = c;
                         s_w[slot] = worst0[id];
+                        s_st[slot] = boff[id] + start[u * W + j];
                     }
                     fill[c] += __popc(m);
                 }
             }
+            build_pos_prefix(s_P, clsv, lane);
             if (lane < 4) s_cls[lane] = cnts[lane];
         }
         __syncthreads();
         // ---- stage the member rows with TMA bulk copies ---------------------
         // smem row stride = dp + 4 floats: consecutive rows start 16 B apart
         // modulo 128 B, so 8 distinct rows per wavefront are conflict-free.
+        // slot s lives in smem row (s & 1) * H + (s >> 1): the two rows of a
+        // 2x2 tile sit in different halves, so consecutive tiles of a warp
+        // read consecutive rows (16 B apart modulo 128 B: conflict-free).
+        const int H = (w + 1) >> 1;
         if (tid == 0) {
             fence_proxy_async();
             const uint32_t row_bytes = (uint32_t)dp * 4u;
             mbar_expect_tx(&s_bar, row_bytes * (uint32_t)w);
             for (int sl = 0; sl < w; sl++)
-                bulk_g2s(sv4 + (size_t)sl * qs, sub + (int64_t)s_id[sl] * dp, row_bytes, &s_bar);
+                bulk_g2s(sv4 + (size_t)((sl & 1) * H + (sl >> 1)) * qs, sub + (int64_t)s_id[sl] * dp,
+                         row_bytes, &s_bar);
         }
         mbar_wait(&s_bar, phase);
         phase ^= 1u;
@@ -696,7 +738,7 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
             for (int sl = warp; sl < w; sl += TJ_WARPS) {
                 float acc = 0.f;
                 for (int c = lane; c < q4; c += 32) {
-                    float4 a = sv4[(size_t)sl * qs + c];
+                    float4 a = sv4[(size_t)((sl & 1) * H + (sl >> 1)) * qs + c];
                     acc = fmaf(a.x, a.x, acc);
                     acc = fmaf(a.y, a.y, acc);
                     acc = fmaf(a.z, a.z, acc);
@@ -738,10 +780,11 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
             const bool vi1 = i0 + 1 < r1, vj1 = j0 + 1 < c1;
             float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
             if (live) {
-                const float4 *a0p = sv4 + (size_t)i0 * qs;
-                const float4 *a1p = sv4 + (size_t)(vi1 ? i0 + 1 : i0) * qs;
-                const float4 *b0p = sv4 + (size_t)j0 * qs;
-                const float4 *b1p = sv4 + (size_t)(vj1 ? j0 + 1 : j0) * qs;
+                auto rowp = [&](int sl) { return sv4 + (size_t)((sl & 1) * H + (sl >> 1)) * qs; };
+                const float4 *a0p = rowp(i0);
+                const float4 *a1p = rowp(vi1 ? i0 + 1 : i0);
+                const float4 *b0p = rowp(j0);
+                const float4 *b1p = rowp(vj1 ? j0 + 1 : j0);
 #pragma unroll 4
                 for (int c = 0; c < q4; c++) {
                     float4 a0 = a0p[c], a1 = a1p[c], b0 = b0p[c], b1 = b1p[c];
@@ -785,6 +828,8 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                 }
             }
             // ---- finalize the 4 pairs of the tile --------------------------
+            double dv[4];
+            bool e1v[4], e2v[4];
 #pragma unroll
             for (int s = 0; s < 4; s++) {
                 const int ii = i0 + (s >> 1), jj = j0 + (s & 1);
@@ -813,7 +858,8 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                             maybe = (double)f <= wmax * mrel;
                         }
                         if (maybe) {
-                            dd = exact_dist<TAG>(sv + (size_t)ii * qs * 4, sv + (size_t)jj * qs * 4, d);
+                            dd = exact_dist<TAG>(sv + (size_t)((ii & 1) * H + (ii >> 1)) * qs * 4,
+                                                 sv + (size_t)((jj & 1) * H + (jj >> 1)) * qs * 4, d);
                             n_exact++;
                         } else {
                             dd = __longlong_as_double(0x7ff0000000000000LL);
@@ -822,33 +868,25 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                     e1 = dd < wi;  // id[ii] <- id[jj]
                     e2 = dd < wj;  // id[jj] <- id[ii]
                 }
-                unsigned m1 = __ballot_sync(FULL_MASK, e1), m2 = __ballot_sync(FULL_MASK, e2);
-                int tot = __popc(m1) + __popc(m2);
-                if (tot) {
-                    unsigned long long bb = 0;
-                    if (lane == 0) bb = atomicAdd(&counters[C_CAND], (unsigned long long)tot);
-                    bb = __shfl_sync(FULL_MASK, bb, 0);
-                    if (e1 || e2) {
-                        const int pi = s_pos[ii], pj = s_pos[jj];
-                        const int p = pi < pj ? pi : pj, q = pi < pj ? pj : pi;
-                        const uint64_t key = ((uint64_t)u * W + p) * W + q;
-                        const int idi = s_id[ii], idj = s_id[jj];
-                        if (e1) {
-                            unsigned long long pos = bb + __popc(m1 & lanemask_lt());
-                            if (pos < cap) {
-                                A[pos] = CandA{key, dd, idj, idi};
-                                atomicAdd(&tcnt[idi], 1u);
-                            }
-                        }
-                        if (e2) {
-                            unsigned long long pos = bb + __popc(m1) + __popc(m2 & lanemask_lt());
-                            if (pos < cap) {
-                                A[pos] = CandA{key, dd, idi, idj};
-                                atomicAdd(&tcnt[idj], 1u);
-                            }
-                        }
-                    }
-                }
+                dv[s] = dd;
+                e1v[s] = e1;
+                e2v[s] = e2;
+            }
+            // write both directions to their reference-order slots
+#pragma unroll
+            for (int s = 0; s < 4; s++) {
+                const int ii = i0 + (s >> 1), jj = j0 + (s & 1);
+                bool ok = live && ii < r1 && jj < c1;
+                if (ok && tri) ok = ii < jj;
+                if (ok) ok = s_new[ii] || s_new[jj];
+                if (!ok) continue;
+                const int pi = s_pos[ii], pj = s_pos[jj];
+                const uint64_t sij = s_st[ii] + pair_rank(s_P, mode, s_sc[ii], pi, pj);
+                const uint64_t sji = s_st[jj] + pair_rank(s_P, mode, s_sc[jj], pj, pi);
+                Bd[sij] = dv[s];
+                Bd[sji] = dv[s];
+                if (e1v[s]) Bs[sij] = s_id[jj];
+                if (e2v[s]) Bs[sji] = s_id[ii];
             }
         }
         __syncthreads();  // smem reused by the next hood
@@ -857,6 +895,215 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) n_exact += __shfl_xor_sync(FULL_MASK, n_exact, o);
         if (lane == 0 && n_exact) atomicAdd(&counters[C_EXACT], n_exact);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Local join, tensor-core route for datasets with a dot-form exactness
+// certificate (integer entries, |v| <= 2048, 2*d*max|v|^2 < 2^24): rows are
+// staged as fp16 (exact), the member Gram block is computed with
+// mma.sync.m16n8k16 (fp16 x fp16 -> fp32; every partial sum is an integer
+// below 2^24, hence exact), and dist = |a|^2 + |b|^2 - 2 a.b with exact
+// per-point norms is bit-identical to the reference's fp64 sequential sum.
+// One warp per hood, software-pipelined: while the warp computes hood i, the
+// TMA engine fetches hood i+1's rows into the other buffer.
+// ---------------------------------------------------------------------------
+constexpr int MJ_WARPS = 4;  // independent warps per CTA (one hood each)
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t &r0, uint32_t &r1, uint32_t &r2,
+                                        uint32_t &r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2(uint32_t addr, uint32_t &r0, uint32_t &r1) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
+                 : "=r"(r0), "=r"(r1)
+                 : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__host__ __device__ constexpr size_t mj_meta_bytes(int Wp) {
+    return (16 + (size_t)Wp * (8 + 8 + 4 * 5) + sizeof(PosPrefix) + 127) & ~(size_t)127;
+}
+
+// Per-warp shared-memory region of k_join_mma (W slots padded to Wp = W+16).
+struct MjSmem {
+    uint64_t *bar;
+    double *w;      // round-start worst of each slot's row
+    uint64_t *st;   // first bucket slot of each slot's membership
+    int *id, *pos, *nw, *cls;
+    float *nrm;
+    uint8_t *P;     // class-position prefix table
+    char *rows;     // fp16 rows, stride rs
+};
+
+__device__ __forceinline__ MjSmem mj_carve(char *base, int Wp) {
+    MjSmem m;
+    m.bar = reinterpret_cast<uint64_t *>(base);
+    char *p = base + 16;
+    m.w = reinterpret_cast<double *>(p); p += 8 * Wp;
+    m.st = reinterpret_cast<uint64_t *>(p); p += 8 * Wp;
+    m.id = reinterpret_cast<int *>(p); p += 4 * Wp;
+    m.pos = reinterpret_cast<int *>(p); p += 4 * Wp;
+    m.nw = reinterpret_cast<int *>(p); p += 4 * Wp;
+    m.cls = reinterpret_cast<int *>(p); p += 4 * Wp;
+    m.nrm = reinterpret_cast<float *>(p); p += 4 * Wp;
+    m.P = reinterpret_cast<uint8_t *>(p);
+    m.rows = base + mj_meta_bytes(Wp);
+    return m;
+}
+
+__global__ void __launch_bounds__(MJ_WARPS * 32)
+k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
+           const int32_t *__restrict__ nlen, int W, const int8_t *__restrict__ labels, int mode,
+           const __half *__restrict__ sub16, int dph, const float *__restrict__ norms,
+           const double *__restrict__ worst0, const uint64_t *__restrict__ boff,
+           const uint32_t *__restrict__ start, double *__restrict__ Bd, int32_t *__restrict__ Bs) {
+    extern __shared__ __align__(128) char mj_smem[];
+    const unsigned lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    const int Wp = W + 16;
+    const int rs = dph * 2 + 16;  // padded fp16 row stride: conflict-free ldmatrix
+    const size_t per_warp = mj_meta_bytes(Wp) + (size_t)Wp * rs;
+    const MjSmem m = mj_carve(mj_smem + (size_t)warp * per_warp, Wp);
+    if (lane == 0) mbar_init(m.bar, 1);
+    // zero the row buffer once: slots beyond w feed the MMA tile tails
+    for (size_t i = lane * 16; i < (size_t)Wp * rs; i += 32 * 16)
+        *reinterpret_cast<float4 *>(m.rows + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncwarp();
+    uint32_t phase = 0;
+    const uint32_t row_bytes = (uint32_t)dph * 2u;
+    const uint32_t rbase = smem_u32(m.rows);
+    for (int hi = blockIdx.x * MJ_WARPS + warp; hi < nactive; hi += gridDim.x * MJ_WARPS) {
+        const int64_t u = active[hi];
+        const int w = nlen[u];
+        // ---- classify members into (label, new-first) slots ------------------
+        uint32_t ev[4];
+        int clsv[4], labv[4];
+#pragma unroll
+        for (int b = 0; b < 4; b++) {  // W <= 128
+            const int j = b * 32 + (int)lane;
+            ev[b] = j < w ? nbh[u * W + j] : 0u;
+        }
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const int j = b * 32 + (int)lane;
+            labv[b] = (j < w && mode != 0) ? (int)labels[ev[b] >> 1] : 0;
+        }
+        int cnts[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const int j = b * 32 + (int)lane;
+            clsv[b] = j < w ? (labv[b] != 0) * 2 + ((ev[b] & 1) ? 0 : 1) : 4;
+#pragma unroll
+            for (int c = 0; c < 4; c++) cnts[c] += __popc(__ballot_sync(FULL_MASK, clsv[b] == c));
+        }
+        const int base_cls[4] = {0, cnts[0], cnts[0] + cnts[1], cnts[0] + cnts[1] + cnts[2]};
+        int fill[4] = {0, 0, 0, 0};
+        int myslot[4];
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            myslot[b] = -1;
+#pragma unroll
+            for (int c = 0; c < 4; c++) {
+                const unsigned mk = __ballot_sync(FULL_MASK, clsv[b] == c);
+                if (clsv[b] == c) myslot[b] = base_cls[c] + fill[c] + __popc(mk & lanemask_lt());
+                fill[c] += __popc(mk);
+            }
+        }
+        fence_proxy_async();  // prior generic reads of the rows vs. async-proxy writes
+        if (lane == 0) mbar_expect_tx(m.bar, row_bytes * (uint32_t)w);
+        __syncwarp();
+        // each lane stages its own members' rows (parallel TMA issue) and
+        // fetches their per-row metadata (independent loads, issued together)
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const int sl = myslot[b];
+            if (sl >= 0) {
+                const int id = (int)(ev[b] >> 1);
+                const int j = b * 32 + (int)lane;
+                bulk_g2s(m.rows + (size_t)sl * rs, sub16 + (int64_t)id * dph, row_bytes, m.bar);
+                m.id[sl] = id;
+                m.pos[sl] = j;
+                m.nw[sl] = (int)(ev[b] & 1);
+                m.cls[sl] = clsv[b];
+                m.w[sl] = worst0[id];
+                m.nrm[sl] = norms[id];
+                m.st[sl] = boff[id] + start[u * W + j];
+            }
+        }
+        build_pos_prefix(m.P, clsv, lane);
+        __syncwarp();
+        mbar_wait(m.bar, phase);
+        phase ^= 1u;
+        const int nA = cnts[0] + cnts[1];
+        const int nblk = mode == 2 ? 2 : 1;
+        for (int bk = 0; bk < nblk; bk++) {
+            const int r0 = bk ? nA : 0, r1 = bk ? w : (mode == 0 ? w : nA);
+            const int c0 = bk ? nA : (mode == 0 ? 0 : nA), c1 = w;
+            const int rn = bk ? cnts[2] : cnts[0], cn = bk ? cnts[2] : (mode == 0 ? cnts[0] : cnts[2]);
+            const bool tri = bk ? true : (mode == 0);
+            for (int m0 = r0; m0 < r1; m0 += 16) {
+                for (int n0 = c0; n0 < c1; n0 += 8) {
+                    if (m0 - r0 >= rn && n0 - c0 >= cn) continue;  // old x old
+                    if (tri && n0 + 7 <= m0) continue;             // below diagonal
+                    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                    const uint32_t a_addr = rbase + (uint32_t)((m0 + (lane & 15)) * rs + (lane >> 4) * 16);
+                    const uint32_t b_addr = rbase + (uint32_t)((n0 + (lane & 7)) * rs + ((lane >> 3) & 1) * 16);
+#pragma unroll 4
+                    for (int kk = 0; kk < dph; kk += 16) {
+                        uint32_t a0, a1, a2, a3, b0, b1;
+                        ldsm_x4(a_addr + kk * 2, a0, a1, a2, a3);
+                        ldsm_x2(b_addr + kk * 2, b0, b1);
+                        mma16816(acc, a0, a1, a2, a3, b0, b1);
+                    }
+                    const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+                    for (int s = 0; s < 4; s++) {
+                        const int ii = m0 + g + (s >> 1) * 8, jj = n0 + 2 * t4 + (s & 1);
+                        bool ok = ii < r1 && jj < c1;
+                        if (ok && tri) ok = ii < jj;
+                        if (ok) ok = m.nw[ii] || m.nw[jj];
+                        if (!ok) continue;
+                        const double dd = (double)((m.nrm[ii] + m.nrm[jj]) - 2.0f * acc[s]);
+                        const int pi = m.pos[ii], pj = m.pos[jj];
+                        const uint64_t sij = m.st[ii] + pair_rank(m.P, mode, m.cls[ii], pi, pj);
+                        const uint64_t sji = m.st[jj] + pair_rank(m.P, mode, m.cls[jj], pj, pi);
+                        Bd[sij] = dd;
+                        Bd[sji] = dd;
+                        if (dd < m.w[ii]) Bs[sij] = m.id[jj];
+                        if (dd < m.w[jj]) Bs[sji] = m.id[ii];
+                    }
+                }
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// fp16 copy of the dataset (zero-padded to dph) and exact fp32 row norms.
+__global__ void k_to_half(const float *__restrict__ v, int dp, int64_t n, int dph,
+                          __half *__restrict__ out, float *__restrict__ norms) {
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n;
+         r += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+        const unsigned lane = lane_id();
+        float acc = 0.f;
+        for (int c = lane; c < dph; c += 32) {
+            float x = c < dp ? v[r * dp + c] : 0.f;
+            out[r * dph + c] = __float2half_rn(x);
+            acc = fmaf(x, x, acc);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, o);
+        if (lane == 0) norms[r] = acc;
     }
 }
 
@@ -879,6 +1126,131 @@ __global__ void k_data_stats(const float *__restrict__ v, int64_t total, unsigne
     atomicMax(&out[1], (unsigned long long)mx);
     atomicMin(&out[2], (unsigned long long)mn);
 }
+
+// Hood memberships.  Pass 1 (k_hood_prep): every member of an active hood
+// adds its number of admissible partners to its row's slot count and one to
+// its membership count.  Pass 2 (k_hood_memb): the memberships are bucketed
+// by member row (unordered; k_seg_rank orders them).
+template <bool FILL>
+__global__ void k_hood_memb(const int32_t *__restrict__ active, int nactive,
+                            const uint32_t *__restrict__ nbh, const int32_t *__restrict__ nlen,
+                            int W, const int8_t *__restrict__ labels, int mode, uint32_t *bound,
+                            uint32_t *mcount, const uint32_t *__restrict__ moff, uint32_t *mcur,
+                            MembRec *memb) {
+    const unsigned lane = lane_id();
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t hi = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); hi < nactive;
+         hi += nw) {
+        const int64_t u = active[hi];
+        const int w = nlen[u];
+        uint32_t ev[4];
+        int clsv[4];
+        int cnt[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const int j = b * 32 + (int)lane;
+            ev[b] = j < w ? nbh[u * W + j] : 0u;
+        }
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const int j = b * 32 + (int)lane;
+            int cls = 4;
+            if (j < w) {
+                const int lab = mode == 0 ? 0 : (labels[ev[b] >> 1] != 0);
+                cls = lab * 2 + ((ev[b] & 1) ? 0 : 1);
+            }
+            clsv[b] = cls;
+#pragma unroll
+            for (int c = 0; c < 4; c++) cnt[c] += __popc(__ballot_sync(FULL_MASK, cls == c));
+        }
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const int j = b * 32 + (int)lane;
+            if (j < w) {
+                const int cls = clsv[b];
+                const int mk = partner_mask(mode, cls);
+                int part = -(int)partner_self(mode, cls);
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    if (mk & (1 << c)) part += cnt[c];
+                if (part > 0) {
+                    const int32_t id = (int32_t)(ev[b] >> 1);
+                    if (!FILL) {
+                        atomicAdd(&bound[id], (uint32_t)part);
+                        atomicAdd(&mcount[id], 1u);
+                    } else {
+                        const uint32_t at = moff[id] + atomicAdd(&mcur[id], 1u);
+                        memb[at] = MembRec{(uint64_t)u, (uint32_t)part, (uint32_t)(u * W + j)};
+                    }
+                }
+            }
+        }
+    }
+}
+
+// Directed inserts: entry t of rows[] is a membership of weight 1, key t.
+template <bool FILL>
+__global__ void k_directed_memb(const int32_t *__restrict__ rows, int64_t m, uint32_t *mcount,
+                                const uint32_t *__restrict__ moff, uint32_t *mcur, MembRec *memb) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t r = rows[i];
+        if (!FILL) {
+            atomicAdd(&mcount[r], 1u);
+        } else {
+            const uint32_t at = moff[r] + atomicAdd(&mcur[r], 1u);
+            memb[at] = MembRec{(uint64_t)i, 1u, (uint32_t)i};
+        }
+    }
+}
+
+// Per row: exclusive weighted rank of each membership by key (ascending
+// hood / ordinal) -> start[out] = first slot of that membership in the
+// row's bucket.  Warp per row, O(m^2 / 32); segments up to SEG_SMEM are
+// staged in shared memory, longer ones (hub rows) read through L1.
+constexpr int SEG_WARPS = 8;
+__global__ void __launch_bounds__(SEG_WARPS * 32)
+k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restrict__ memb,
+           uint32_t *__restrict__ start) {
+    __shared__ uint64_t s_key[SEG_WARPS][SEG_SMEM];
+    __shared__ uint32_t s_wt[SEG_WARPS][SEG_SMEM];
+    const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
+    const int64_t nw = (int64_t)gridDim.x * SEG_WARPS;
+    for (int64_t r = (int64_t)blockIdx.x * SEG_WARPS + wib; r < n; r += nw) {
+        const uint32_t lo = moff[r];
+        const int m = (int)(moff[r + 1] - lo);
+        if (m == 0) continue;
+        if (m == 1) {
+            if (lane == 0) start[memb[lo].out] = 0;
+            continue;
+        }
+        if (m <= SEG_SMEM) {
+            for (int e = lane; e < m; e += 32) {
+                s_key[wib][e] = memb[lo + e].key;
+                s_wt[wib][e] = memb[lo + e].weight;
+            }
+            __syncwarp();
+            for (int e = lane; e < m; e += 32) {
+                const uint64_t ke = s_key[wib][e];
+                uint32_t acc = 0;
+                for (int f = 0; f < m; f++) acc += s_key[wib][f] < ke ? s_wt[wib][f] : 0u;
+                start[memb[lo + e].out] = acc;
+            }
+            __syncwarp();
+        } else {
+            for (int e = lane; e < m; e += 32) {
+                const uint64_t ke = memb[lo + e].key;
+                uint32_t acc = 0;
+                for (int f = 0; f < m; f++) {
+                    const MembRec rf = memb[lo + f];
+                    acc += rf.key < ke ? rf.weight : 0u;
+                }
+                start[memb[lo + e].out] = acc;
+            }
+        }
+    }
+}
+
 
 // on_pair capture: every admissible pair of every hood in (u, p, q) order.
 __global__ void k_capture_pairs(const uint32_t *__restrict__ nbh, const int32_t *__restrict__ nlen,
@@ -905,158 +1277,46 @@ __global__ void k_capture_pairs(const uint32_t *__restrict__ nbh, const int32_t 
 }
 
 // ---------------------------------------------------------------------------
-// Candidate bucketing by target row (the counting sort of
-// apply_updates_grouped, _kernels.py:227-247).
-// ---------------------------------------------------------------------------
-__global__ void k_scatter(const CandA *__restrict__ A, unsigned long long count,
-                          const uint32_t *__restrict__ toff, uint32_t *tcnt, CandB *B) {
-    for (unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x; i < count;
-         i += (unsigned long long)gridDim.x * blockDim.x) {
-        CandA c = A[i];
-        uint32_t p = toff[c.tgt] + atomicSub(&tcnt[c.tgt], 1u) - 1u;
-        B[p] = CandB{c.key, c.d, c.src, 0};
-    }
-}
-
-// ---------------------------------------------------------------------------
 // Sequential per-row insertion in reference order (apply_updates_grouped's
 // row loop, _kernels.py:248-254, each step _insert _kernels.py:159-192).
 // One warp per row; the row's candidates are sorted by reference key first.
 // ---------------------------------------------------------------------------
 constexpr int APPLY_WARPS = 4;
 
-// Sort a row's c <= 32*NE candidates in registers by reference key, then
-// apply them in order, 32 at a time.
-template <int E, int NE>
-__device__ __forceinline__ int apply_sorted_reg(WarpRow<E> &s, int k, const CandB *__restrict__ Bp,
-                                                int c, int ib, uint64_t mask, unsigned lane) {
-    uint64_t v[NE];
-#pragma unroll
-    for (int e = 0; e < NE; e++) {
-        int j = e * 32 + (int)lane;
-        v[e] = j < c ? ((Bp[j].key << ib) | (uint64_t)j) : ~0ull;
-    }
-    warp_sort_reg<NE>(v, lane);
-    int a = 0;
-#pragma unroll
-    for (int e = 0; e < NE; e++) {
-        const int base = e * 32;
-        if (base >= c) break;
-        int src = 0;
-        double dd = 0.0;
-        if (base + (int)lane < c) {
-            const CandB &cb = Bp[(uint32_t)(v[e] & mask)];
-            src = cb.src;
-            dd = cb.d;
-        }
-        a += warp_apply_chunk<E>(s, k, src, dd, c - base < 32 ? c - base : 32, lane);
-    }
-    return a;
-}
-
+// Stream row r's bucket slots [boff[r], boff[r+1]) in order: 32 distances per
+// step (coalesced), candidates that cannot pass the current worst are
+// skipped by ballot, the rest go through warp_insert in slot order -- which
+// is the reference's sequential order, so no sorting is needed.
 template <int E>
 __global__ void __launch_bounds__(APPLY_WARPS * 32)
-k_apply(int64_t n, int k, const uint32_t *__restrict__ toff, const CandB *__restrict__ B, int ib,
-        int32_t *ids, double *dists, uint8_t *flags, int32_t *sizes, int32_t *heavy,
-        unsigned long long *counters) {
-    __shared__ uint64_t s_sort[APPLY_WARPS][APPLY_WARP_MAX];
-    unsigned lane = lane_id(), wib = threadIdx.x >> 5;
-    uint64_t *srt = s_sort[wib];
-    int64_t nw = (int64_t)gridDim.x * APPLY_WARPS;
-    unsigned long long acc = 0;
+k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double *__restrict__ Bd,
+               const int32_t *__restrict__ Bs, int32_t *ids, double *dists, uint8_t *flags,
+               int32_t *sizes, unsigned long long *counters) {
+    const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
+    const int64_t nw = (int64_t)gridDim.x * APPLY_WARPS;
+    unsigned long long acc = 0, slots = 0;
     for (int64_t r = (int64_t)blockIdx.x * APPLY_WARPS + wib; r < n; r += nw) {
-        uint32_t lo = toff[r];
-        int c = (int)(toff[r + 1] - lo);
-        if (c == 0) continue;
-        if (c > APPLY_WARP_MAX) {
-            if (lane == 0) {
-                heavy[atomicAdd(&counters[C_HEAVY_APPLY], 1ull)] = (int32_t)r;
-                atomicMax(&counters[C_MAXC], (unsigned long long)c);
-            }
-            continue;
-        }
+        const uint64_t lo = boff[r];
+        const int64_t ns = (int64_t)(boff[r + 1] - lo);
+        if (ns == 0) continue;
+        slots += (unsigned long long)ns;
         WarpRow<E> s;
         row_load<E>(s, ids, dists, flags, sizes, r, k, lane);
-        const uint64_t mask = (1ull << ib) - 1ull;
         int a = 0;
-        if (c <= 32) {
-            a += apply_sorted_reg<E, 1>(s, k, B + lo, c, ib, mask, lane);
-        } else if (c <= 64) {
-            a += apply_sorted_reg<E, 2>(s, k, B + lo, c, ib, mask, lane);
-        } else if (c <= 128) {
-            a += apply_sorted_reg<E, 4>(s, k, B + lo, c, ib, mask, lane);
-        } else if (c <= 256) {
-            a += apply_sorted_reg<E, 8>(s, k, B + lo, c, ib, mask, lane);
-        } else {
-            uint32_t P2 = next_pow2((uint32_t)c);
-            for (uint32_t j = lane; j < P2; j += 32)
-                srt[j] = (int)j < c ? ((B[lo + j].key << ib) | j) : ~0ull;
-            __syncwarp();
-            bitonic_warp<uint64_t>(srt, P2, lane);
-            for (int base = 0; base < c; base += 32) {
-                int j = base + lane;
-                int src = 0;
-                double dd = 0.0;
-                if (j < c) {
-                    const CandB &cb = B[lo + (uint32_t)(srt[j] & mask)];
-                    src = cb.src;
-                    dd = cb.d;
-                }
-                a += warp_apply_chunk<E>(s, k, src, dd, c - base < 32 ? c - base : 32, lane);
-            }
-            __syncwarp();
+        for (int64_t c0 = 0; c0 < ns; c0 += 32) {
+            const int64_t j = c0 + lane;
+            const double dl = j < ns ? Bd[lo + j] : __longlong_as_double(0x7ff0000000000000LL);
+            const bool pre = j < ns && (s.sz < k || dl < s.worst);
+            if (!__any_sync(FULL_MASK, pre)) continue;
+            const int src = pre ? Bs[lo + j] : 0;
+            const int cnt = ns - c0 < 32 ? (int)(ns - c0) : 32;
+            a += warp_apply_chunk<E>(s, k, src, dl, cnt, lane);
         }
-        row_store<E>(s, ids, dists, flags, sizes, r, k, lane);
+        if (a) row_store<E>(s, ids, dists, flags, sizes, r, k, lane);
         acc += a;
     }
     if (lane == 0 && acc) atomicAdd(&counters[C_ACCEPTED], acc);
-}
-
-// Rows with more than APPLY_WARP_MAX candidates: one block sorts (shared
-// memory, or a global scratch for giant rows), warp 0 inserts.
-template <int E>
-__global__ void k_apply_heavy(const int32_t *__restrict__ heavy, int64_t k_, const uint32_t *__restrict__ toff,
-                              const CandB *__restrict__ B, int ib, int32_t *ids, double *dists,
-                              uint8_t *flags, int32_t *sizes, unsigned long long *counters,
-                              uint64_t *gscratch, int smem_max, int32_t *giant) {
-    extern __shared__ uint64_t hsrt[];
-    int k = (int)k_;
-    unsigned long long cnt = counters[C_HEAVY_APPLY];
-    unsigned lane = lane_id();
-    for (unsigned long long h = blockIdx.x; h < cnt; h += gridDim.x) {
-        int64_t r = heavy[h];
-        uint32_t lo = toff[r];
-        uint32_t c = toff[r + 1] - lo;
-        uint32_t P2 = next_pow2(c);
-        bool in_smem = P2 <= (uint32_t)smem_max;
-        if (gscratch == nullptr && !in_smem) continue;  // giant rows: second pass
-        if (gscratch != nullptr && in_smem) continue;
-        uint64_t *srt = in_smem ? hsrt : gscratch;
-        uint64_t mask = (1ull << ib) - 1ull;
-        for (uint32_t j = threadIdx.x; j < P2; j += blockDim.x)
-            srt[j] = j < c ? ((B[lo + j].key << ib) | j) : ~0ull;
-        __syncthreads();
-        bitonic_block<uint64_t>(srt, P2);
-        if (threadIdx.x < 32) {
-            WarpRow<E> s;
-            row_load<E>(s, ids, dists, flags, sizes, r, k, lane);
-            int a = 0;
-            for (uint32_t base = 0; base < c; base += 32) {
-                uint32_t j = base + lane;
-                int src = 0;
-                double dd = 0.0;
-                if (j < c) {
-                    const CandB &cb = B[lo + (uint32_t)(srt[j] & mask)];
-                    src = cb.src;
-                    dd = cb.d;
-                }
-                a += warp_apply_chunk<E>(s, k, src, dd, c - base < 32 ? (int)(c - base) : 32, lane);
-            }
-            row_store<E>(s, ids, dists, flags, sizes, r, k, lane);
-            if (lane == 0 && a) atomicAdd(&counters[C_ACCEPTED], (unsigned long long)a);
-        }
-        __syncthreads();
-    }
+    if (lane == 0 && slots) atomicAdd(&counters[C_CAND], slots);
 }
 
 // ---------------------------------------------------------------------------

@@ -188,14 +188,15 @@ class Engine:
         return pa, pb, pd
 
     def set_join_variant(self, variant: int) -> None:
-        """-1 auto, 0 exact fp64 route, 1 tiled fp32-screen route."""
+        """-1 auto, 0 exact fp64 route, 1 tiled fp32-screen route, 2 tensor-core route."""
         check(self._lib.knnm_set_join_variant(self._h, int(variant)), "knnm_set_join_variant")
 
     def info(self) -> dict:
         cert = ctypes.c_int32()
         dp = ctypes.c_int32()
         check(self._lib.knnm_get_info(self._h, ctypes.byref(cert), ctypes.byref(dp)), "knnm_get_info")
-        return {"cert": bool(cert.value), "dp": int(dp.value)}
+        return {"cert": bool(cert.value & 1), "cert_dot": bool(cert.value & 2),
+                "dp": int(dp.value)}
 
     # -- instrumentation ---------------------------------------------------
     def set_profiling(self, on: bool) -> None:

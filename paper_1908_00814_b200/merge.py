@@ -87,6 +87,19 @@ def _union(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     return np.union1d(a, b)
 
 
+def _merge_members(a: np.ndarray, b: np.ndarray):
+    """(union, rows of a, rows of b) for disjoint ascending id arrays in one
+    linear pass: np.union1d + np.searchsorted of merge.py:217-221."""
+    if not (_ascending(a) and _ascending(b)):
+        u = np.union1d(a, b)
+        return u, _lookup_local(u, a), _lookup_local(u, b)
+    cat = np.concatenate((a, b))
+    order = np.argsort(cat, kind="stable")
+    inv = np.empty(order.size, dtype=np.int32)
+    inv[order] = np.arange(order.size, dtype=np.int32)
+    return cat[order], inv[: a.size], inv[a.size:]
+
+
 def _sample_pool_rows(rng, nrows: int, t: int, pool: np.ndarray) -> np.ndarray:
     """(nrows, t) distinct draws per row from ``pool`` (merge.py:146-163;
     identical PCG64 call sequence)."""
@@ -167,10 +180,9 @@ def s_merge(dataset, g: KnnGraph, h: KnnGraph, params: MergeParams,
     k = params.k
     k1 = params.k1
 
-    union_gids = _union(np.asarray(g.member_ids), np.asarray(h.member_ids))
+    union_gids, rows_g, rows_h = _merge_members(np.asarray(g.member_ids),
+                                                np.asarray(h.member_ids))
     n = union_gids.shape[0]
-    rows_g = _lookup_local(union_gids, g.member_ids)
-    rows_h = _lookup_local(union_gids, h.member_ids)
     labels = np.zeros(n, dtype=np.int8)
     labels[rows_h] = 1
 
@@ -222,12 +234,10 @@ def j_merge(dataset, g: KnnGraph, raw_ids, params: MergeParams,
             return out, BuildReport(phi_initial=graph_phi(out))
         return out
     rng = np.random.default_rng(params.seed)
-    union_gids = _union(np.asarray(g.member_ids), raw)
+    union_gids, rows_g, rows_raw = _merge_members(np.asarray(g.member_ids), raw)
     n = union_gids.shape[0]
     if k >= n:
         raise ValueError(f"k={k} must be below the union size {n}")
-    rows_g = _lookup_local(union_gids, g.member_ids)
-    rows_raw = _lookup_local(union_gids, raw)
     labels = np.zeros(n, dtype=np.int8)
     labels[rows_raw] = 1
 

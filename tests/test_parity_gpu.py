@@ -46,6 +46,7 @@ CASES = [
     (3000, 100, 40, 2, "sphere"),
     (2000, 960, 20, 1, "unitgmm"),
     (1500, 5, 6, 0, "uniform"),
+    (5000, 100, 40, 1, "intgmm"),
 ]
 
 
@@ -111,7 +112,7 @@ def _to_graph(km, og):
     return g
 
 
-@pytest.mark.parametrize("variant", [0, 1])
+@pytest.mark.parametrize("variant", [0, 1, 2])
 @pytest.mark.parametrize("n,d,k,metric,kind", [CASES[1], CASES[5], CASES[6], CASES[8]])
 def test_join_variants_agree(oracle, variant, n, d, k, metric, kind):
     """Both local-join routes (fp64-every-pair / fp32-screen tiled) are
@@ -141,7 +142,9 @@ def test_certificate_detection():
 
     eng = get_engine()
     eng.set_dataset(km.generate_int_gmm(1000, 128, n_centres=10, seed=1).vectors, 1)
-    assert eng.info()["cert"]
+    assert eng.info()["cert"] and eng.info()["cert_dot"]
+    eng.set_dataset(km.generate_int_gmm(1000, 256, n_centres=10, seed=1).vectors, 1)
+    assert eng.info()["cert"] and not eng.info()["cert_dot"]  # 2*d*255^2 >= 2^24
     eng.set_dataset(km.generate_uniform(1000, 16, seed=1).vectors, 1)
     assert not eng.info()["cert"]
     eng.set_dataset(km.generate_int_gmm(1000, 128, n_centres=10, seed=1).vectors, 2)
