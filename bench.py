@@ -254,12 +254,14 @@ def run_b200(args):
     eng.set_profiling(True)
     evals = 0
     with ClockSampler(local) as clk:
+        torch.cuda.profiler.start()  # ncu --profile-from-start off sees the timed region only
         eng.mark(0)
         for _ in range(args.steps):
             cnt, u_dev = step_device()
             evals += cnt
         eng.mark(1)
         dev_ms = eng.elapsed_ms(0, 1)
+        torch.cuda.profiler.stop()
     barrier()
     st = eng.stats()
     eng.set_profiling(False)

@@ -20,6 +20,10 @@ from .graph import KnnGraph
 
 logger = logging.getLogger(__name__)
 
+# Debug hook: when set to a callable, it is called as ROUND_HOOK(engine)
+# after every round (tests use it for per-iteration state parity).
+ROUND_HOOK = None
+
 MODE_ALL = 0          # _kernels.py:29
 MODE_CROSS = 1        # _kernels.py:30
 MODE_CROSS_OR_S2 = 2  # _kernels.py:31
@@ -114,6 +118,8 @@ def _descent_rounds(engine, n: int, mode: int, k: int, params, rng, counter, on_
         if pairs > 0:
             counter.add(pairs)
         _emit_captured(engine, on_pair, gids)
+        if ROUND_HOOK is not None:
+            ROUND_HOOK(engine)
         cur_phi = engine.phi()
         logger.info("iter=%d pairs=%d updates=%d phi=%.6f dists=%d",
                     it, pairs, accepted, cur_phi, counter.count)

@@ -1,0 +1,98 @@
+"""Host-side logic of the drop-in package (no GPU needed)."""
+
+import numpy as np
+import pytest
+
+import paper_1908_00814_b200 as km
+from paper_1908_00814_b200 import merge as M
+
+
+def test_merge_params_validation():
+    with pytest.raises(ValueError, match="r must be"):
+        km.MergeParams(k=8, r=1.5)
+    with pytest.raises(ValueError, match="k must be"):
+        km.MergeParams(k=1)
+    assert km.MergeParams(k=20, r=0.5).k1 == 10
+    assert km.MergeParams(k=10, r=0.25).k1 == 2  # banker's rounding like the reference
+    assert km.MergeParams(k=4, r=0.3).k1 == 1
+
+
+@pytest.mark.parametrize("seed", range(5))
+def test_merge_members_matches_union1d(seed):
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(1000 + seed * 17)
+    a, b = np.sort(perm[:400]), np.sort(perm[400:])
+    u, ra, rb = M._merge_members(a, b)
+    assert np.array_equal(u, np.union1d(a, b))
+    assert np.array_equal(ra, np.searchsorted(u, a))
+    assert np.array_equal(rb, np.searchsorted(u, b))
+    assert not M._overlaps(a, b)
+    assert M._overlaps(a, np.sort(np.concatenate((b[:3], a[:1]))))
+
+
+def test_check_merge_inputs_messages():
+    ds = km.generate_uniform(50, 3, seed=1)
+    g = km.KnnGraph(np.arange(25), 4, km.Metric.L2)
+    h = km.KnnGraph(np.arange(20, 50), 4, km.Metric.L2)
+    with pytest.raises(ValueError, match="disjoint"):
+        M._check_merge_inputs(ds, g, h.member_ids, km.MergeParams(k=4), h)
+    h2 = km.KnnGraph(np.arange(25, 50), 4, km.Metric.L2)
+    with pytest.raises(ValueError, match="params.k"):
+        M._check_merge_inputs(ds, g, h2.member_ids, km.MergeParams(k=6), h2)
+    with pytest.raises(ValueError, match="outside"):
+        M._check_merge_inputs(ds, g, np.array([60]), km.MergeParams(k=4), None)
+
+
+def test_split_and_validate(oracle):
+    vec = km.generate_uniform(300, 4, seed=3).vectors
+    og = oracle.brute_force_graph(vec, 1, 8)
+    g = km.KnnGraph.from_arrays(og.member_ids, 8, km.Metric.L2, og.ids, og.dists, og.sizes)
+    g.validate()
+    parts = km.split(g, 3)
+    assert parts.head.k == 3 and parts.tail.k == 5
+    assert np.array_equal(np.concatenate([parts.head.ids, parts.tail.ids], axis=1), g.ids)
+    parts.head.validate()
+
+
+def test_scalar_distance_bit_identical_to_oracle(oracle):
+    rng = np.random.default_rng(0)
+    c = km.DistanceCounter()
+    for metric in (0, 1, 2):
+        for _ in range(50):
+            a = rng.standard_normal(37).astype(np.float32)
+            b = rng.standard_normal(37).astype(np.float32)
+            assert km.distance(metric, a, b, c) == oracle.dense_dist(a, b, metric)
+    assert c.count == 150
+    z = np.zeros(4, dtype=np.float32)
+    assert km.distance(km.Metric.COSINE, z, z, c) == 0.0
+    assert km.distance(km.Metric.COSINE, z, np.ones(4, np.float32), c) == 1.0
+    assert km.distance(km.Metric.L2, np.array([0, 0], np.float32), np.array([3, 4], np.float32), c) == 25.0
+
+
+def test_update_nn_spec():
+    nl = km.NeighborList(3, owner=0)
+    assert km.update_nn(nl, 5, 2.0)
+    assert km.update_nn(nl, 4, 2.0)  # tie: smaller id first
+    assert nl.ids() == [4, 5]
+    assert not km.update_nn(nl, 5, 1.0)  # duplicate id
+    assert km.update_nn(nl, 7, 3.0)
+    assert not km.update_nn(nl, 8, 3.0)  # full and not strictly closer
+    assert km.update_nn(nl, 9, 0.5)
+    assert nl.ids() == [9, 4, 5]
+
+
+def test_recall_helpers():
+    truth = [[1, 2, 3], [4, 5, 6]]
+    assert km.recall_at_k([[1, 2, 9], [6, 5, 4]], truth, 3) == 5 / 6
+    assert km.recall_at_k_arrays(np.array([[1, 2, 9], [6, 5, 4]]), np.array(truth), 3) == 5 / 6
+    assert km.scanning_rate(45, 10) == 1.0
+
+
+def test_generators_shapes_and_certificates():
+    ds = km.generate_int_gmm(500, 128, n_centres=10, seed=1)
+    assert ds.vectors.dtype == np.float32 and np.all(ds.vectors == np.rint(ds.vectors))
+    assert ds.vectors.min() >= 0 and ds.vectors.max() <= 255
+    s = km.generate_sphere_gmm(200, 100, n_centres=5, seed=1)
+    assert np.allclose(np.linalg.norm(s.vectors, axis=1), 1.0, atol=1e-5)
+    u = km.generate_unit_gmm(100, 960, n_centres=5, seed=1)
+    assert u.vectors.min() >= 0 and u.vectors.max() <= 1
