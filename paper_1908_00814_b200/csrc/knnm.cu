@@ -247,6 +247,8 @@ uint64_t bucket_budget(knnm_ctx *c) { return c->cand_budget_bytes / (sizeof(doub
 int ensure_slots(knnm_ctx *c, uint64_t slots) {
     TRY(ensure(c->Bd, sizeof(double) * slots));
     TRY(ensure(c->Bs, sizeof(int32_t) * slots));
+    // NaN fill: a slot the join does not write cannot pass (see k_apply_stream)
+    CK(cudaMemsetAsync(c->Bd.p, 0xff, sizeof(double) * slots, c->st));
     return KNNM_OK;
 }
 
@@ -660,7 +662,7 @@ static int insert_impl(knnm_ctx *c, const int32_t *rows, int64_t mrows, int32_t 
             TRY(rank_memberships(c));
             k_directed_emit<<<grid_for(c, cm, 256, 32), 256, 0, c->st>>>(
                 rows_d, c->stage[1].as<int32_t>() + c0, cm, c->subp, c->dp, c->d, c->metric,
-                c->sizes.as<int32_t>(), c->dists.as<double>(), c->k, c->boff.as<uint64_t>(),
+                (int)(c->cert && c->metric != KNNM_COSINE), c->sizes.as<int32_t>(), c->dists.as<double>(), c->k, c->boff.as<uint64_t>(),
                 c->start.as<uint32_t>(), c->Bd.as<double>(), c->Bs.as<int32_t>(),
                 capd ? capd + c0 : nullptr);
             CKL();

@@ -285,7 +285,9 @@ __device__ __forceinline__ int warp_apply_chunk(WarpRow<E> &s, int k, int src_l,
     int acc = 0;
     int i = -1;
     while (true) {
-        bool live = (int)lane > i && (int)lane < cnt && (s.sz < k || d_l < s.worst);
+        // d_l = +inf marks an empty slot (real distances are finite)
+        bool live = (int)lane > i && (int)lane < cnt && d_l < __longlong_as_double(0x7ff0000000000000LL) &&
+                    (s.sz < k || d_l < s.worst);
         unsigned m = __ballot_sync(FULL_MASK, live);
         if (!m) break;
         i = __ffs(m) - 1;

@@ -39,33 +39,41 @@ __host__ __device__ __forceinline__ bool partner_self(int mode, int cls) {
     return (mode == 0 && cls == 0) || (mode == 2 && cls == 2);
 }
 
-// P[c * (MAX_W + 1) + x] = members of class c at nbh positions < x.
+// Q[ct * (MAX_W + 1) + x] = admissible partners of a class-ct member at nbh
+// positions < x, i.e. sum over the classes c in partner_mask(mode, ct) of the
+// class-c members before position x.
 typedef uint8_t PosPrefix[4 * (MAX_W + 1)];
 
 // Rank of partner position px among the admissible partners of the member
 // (class ct, position pt) -- the slot offset inside the membership's range.
-__device__ __forceinline__ uint32_t pair_rank(const uint8_t *__restrict__ P, int mode, int ct, int pt,
+__device__ __forceinline__ uint32_t pair_rank(const uint8_t *__restrict__ Q, int mode, int ct, int pt,
                                               int px) {
-    const int mk = partner_mask(mode, ct);
-    uint32_t r = 0;
-#pragma unroll
-    for (int c = 0; c < 4; c++)
-        if (mk & (1 << c)) r += P[c * (MAX_W + 1) + px];
-    if (partner_self(mode, ct) && pt < px) r -= 1;
-    return r;
+    return (uint32_t)Q[ct * (MAX_W + 1) + px] - (uint32_t)(partner_self(mode, ct) && pt < px);
 }
 
-// Warp-cooperative: fill P from the per-position classes clsv[b] of lanes
+// Warp-cooperative: fill Q from the per-position classes clsv[b] of lanes
 // (position b * 32 + lane; class 4 = no member).
-__device__ __forceinline__ void build_pos_prefix(uint8_t *P, const int (&clsv)[4], unsigned lane) {
+__device__ __forceinline__ void build_pos_prefix(uint8_t *Q, const int (&clsv)[4], int mode,
+                                                 unsigned lane) {
     int base[4] = {0, 0, 0, 0};
+    int mk[4];
+#pragma unroll
+    for (int c = 0; c < 4; c++) mk[c] = partner_mask(mode, c);
 #pragma unroll
     for (int b = 0; b < 4; b++) {
+        int before[4];
 #pragma unroll
         for (int c = 0; c < 4; c++) {
-            const unsigned mk = __ballot_sync(FULL_MASK, clsv[b] == c);
-            P[c * (MAX_W + 1) + b * 32 + lane] = (uint8_t)(base[c] + __popc(mk & lanemask_lt()));
-            base[c] += __popc(mk);
+            const unsigned m = __ballot_sync(FULL_MASK, clsv[b] == c);
+            before[c] = base[c] + __popc(m & lanemask_lt());
+            base[c] += __popc(m);
+        }
+#pragma unroll
+        for (int ct = 0; ct < 4; ct++) {
+            int q = 0;
+#pragma unroll
+            for (int c = 0; c < 4; c++) q += (mk[ct] >> c & 1) ? before[c] : 0;
+            Q[ct * (MAX_W + 1) + b * 32 + lane] = (uint8_t)q;
         }
     }
 }
@@ -262,8 +270,27 @@ __global__ void k_pool_map(const int64_t *__restrict__ cand, int64_t m, const in
 // Directed init inserts: distances + candidate emission
 // (_eval_pairs -> pair_dists_dense, then apply_updates_directed order).
 // ---------------------------------------------------------------------------
+// Certified data (integer entries, d * range^2 < 2^24): every fp32 partial
+// sum is an exact integer, so any summation order gives the reference's value.
+__device__ __forceinline__ double cert_dist(const float *__restrict__ a, const float *__restrict__ b,
+                                            int dp, int tag) {
+    const float4 *a4 = reinterpret_cast<const float4 *>(a);
+    const float4 *b4 = reinterpret_cast<const float4 *>(b);
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    for (int c = 0; c < (dp >> 2); c++) {
+        const float4 x = __ldg(a4 + c), y = __ldg(b4 + c);
+        const float t0 = x.x - y.x, t1 = x.y - y.y, t2 = x.z - y.z, t3 = x.w - y.w;
+        if (tag == 1) {
+            s0 = fmaf(t0, t0, s0); s1 = fmaf(t1, t1, s1); s2 = fmaf(t2, t2, s2); s3 = fmaf(t3, t3, s3);
+        } else {
+            s0 += fabsf(t0); s1 += fabsf(t1); s2 += fabsf(t2); s3 += fabsf(t3);
+        }
+    }
+    return (double)((s0 + s1) + (s2 + s3));
+}
+
 __global__ void k_directed_emit(const int32_t *__restrict__ rows, const int32_t *__restrict__ nids,
-                                int64_t m, const float *__restrict__ sub, int dp, int d, int tag,
+                                int64_t m, const float *__restrict__ sub, int dp, int d, int tag, int cert,
                                 const int32_t *__restrict__ sizes, const double *__restrict__ dists,
                                 int k, const uint64_t *__restrict__ boff,
                                 const uint32_t *__restrict__ start, double *__restrict__ Bd,
@@ -271,12 +298,15 @@ __global__ void k_directed_emit(const int32_t *__restrict__ rows, const int32_t 
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t r = rows[i], s = nids[i];
-        const double dd = exact_dist_tag(tag, sub + (int64_t)r * dp, sub + (int64_t)s * dp, d);
+        const double dd = cert ? cert_dist(sub + (int64_t)r * dp, sub + (int64_t)s * dp, dp, tag)
+                               : exact_dist_tag(tag, sub + (int64_t)r * dp, sub + (int64_t)s * dp, d);
         if (cap_d) cap_d[i] = dd;
         const uint64_t slot = boff[r] + start[i];
-        Bd[slot] = dd;
-        // the source id is only ever read for a candidate that can pass
-        if (!(sizes[r] == k && dd >= dists[(int64_t)r * k + k - 1])) Bs[slot] = s;
+        // slots are pre-filled with NaN; only updates that can pass are written
+        if (!(sizes[r] == k && dd >= dists[(int64_t)r * k + k - 1])) {
+            Bd[slot] = dd;
+            Bs[slot] = s;
+        }
     }
 }
 
@@ -556,7 +586,7 @@ k_join_exact(const int32_t *__restrict__ active, const uint32_t *__restrict__ nb
                 s_st[j] = boff[id] + start[u * W + j];
             }
         }
-        build_pos_prefix(s_P, clsv, lane);
+        build_pos_prefix(s_P, clsv, mode, lane);
     }
     __syncthreads();
     const int q4 = dp >> 2;
@@ -572,10 +602,10 @@ k_join_exact(const int32_t *__restrict__ active, const uint32_t *__restrict__ nb
         const double dd = exact_dist<TAG>(sv + p * dp, sv + q * dp, d);
         const uint64_t spq = s_st[p] + pair_rank(s_P, mode, s_cls[p], p, q);
         const uint64_t sqp = s_st[q] + pair_rank(s_P, mode, s_cls[q], q, p);
-        Bd[spq] = dd;
-        Bd[sqp] = dd;
-        if (dd < s_w[p]) Bs[spq] = s_id[q];
-        if (dd < s_w[q]) Bs[sqp] = s_id[p];
+        // slots are pre-filled with NaN ("cannot pass"); only updates that
+        // can still be accepted (d < round-start worst) are written
+        if (dd < s_w[p]) { Bd[spq] = dd; Bs[spq] = s_id[q]; }
+        if (dd < s_w[q]) { Bd[sqp] = dd; Bs[sqp] = s_id[p]; }
     }
 }
 
@@ -712,7 +742,7 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                     fill[c] += __popc(m);
                 }
             }
-            build_pos_prefix(s_P, clsv, lane);
+            build_pos_prefix(s_P, clsv, mode, lane);
             if (lane < 4) s_cls[lane] = cnts[lane];
         }
         __syncthreads();
@@ -883,10 +913,8 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                 const int pi = s_pos[ii], pj = s_pos[jj];
                 const uint64_t sij = s_st[ii] + pair_rank(s_P, mode, s_sc[ii], pi, pj);
                 const uint64_t sji = s_st[jj] + pair_rank(s_P, mode, s_sc[jj], pj, pi);
-                Bd[sij] = dv[s];
-                Bd[sji] = dv[s];
-                if (e1v[s]) Bs[sij] = s_id[jj];
-                if (e2v[s]) Bs[sji] = s_id[ii];
+                if (e1v[s]) { Bd[sij] = dv[s]; Bs[sij] = s_id[jj]; }
+                if (e2v[s]) { Bd[sji] = dv[s]; Bs[sji] = s_id[ii]; }
             }
         }
         __syncthreads();  // smem reused by the next hood
@@ -1040,7 +1068,7 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                 m.st[sl] = boff[id] + start[u * W + j];
             }
         }
-        build_pos_prefix(m.P, clsv, lane);
+        build_pos_prefix(m.P, clsv, mode, lane);
         __syncwarp();
         mbar_wait(m.bar, phase);
         phase ^= 1u;
@@ -1074,13 +1102,19 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                         if (ok) ok = m.nw[ii] || m.nw[jj];
                         if (!ok) continue;
                         const double dd = (double)((m.nrm[ii] + m.nrm[jj]) - 2.0f * acc[s]);
+                        const bool e1 = dd < m.w[ii], e2 = dd < m.w[jj];
+                        if (!(e1 || e2)) continue;
                         const int pi = m.pos[ii], pj = m.pos[jj];
-                        const uint64_t sij = m.st[ii] + pair_rank(m.P, mode, m.cls[ii], pi, pj);
-                        const uint64_t sji = m.st[jj] + pair_rank(m.P, mode, m.cls[jj], pj, pi);
-                        Bd[sij] = dd;
-                        Bd[sji] = dd;
-                        if (dd < m.w[ii]) Bs[sij] = m.id[jj];
-                        if (dd < m.w[jj]) Bs[sji] = m.id[ii];
+                        if (e1) {
+                            const uint64_t sij = m.st[ii] + pair_rank(m.P, mode, m.cls[ii], pi, pj);
+                            Bd[sij] = dd;
+                            Bs[sij] = m.id[jj];
+                        }
+                        if (e2) {
+                            const uint64_t sji = m.st[jj] + pair_rank(m.P, mode, m.cls[jj], pj, pi);
+                            Bd[sji] = dd;
+                            Bs[sji] = m.id[ii];
+                        }
                     }
                 }
             }
@@ -1305,8 +1339,11 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
         int a = 0;
         for (int64_t c0 = 0; c0 < ns; c0 += 32) {
             const int64_t j = c0 + lane;
-            const double dl = j < ns ? Bd[lo + j] : __longlong_as_double(0x7ff0000000000000LL);
-            const bool pre = j < ns && (s.sz < k || dl < s.worst);
+            double dl = j < ns ? Bd[lo + j] : __longlong_as_double(0x7ff0000000000000LL);
+            if (dl != dl) dl = __longlong_as_double(0x7ff0000000000000LL);  // unwritten slot
+            // an unwritten slot belongs to a row that was full at round start
+            // and a distance >= its worst: it can never pass
+            const bool pre = j < ns && (dl < s.worst || (s.sz < k && dl < __longlong_as_double(0x7ff0000000000000LL)));
             if (!__any_sync(FULL_MASK, pre)) continue;
             const int src = pre ? Bs[lo + j] : 0;
             const int cnt = ns - c0 < 32 ? (int)(ns - c0) : 32;
