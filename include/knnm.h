@@ -153,6 +153,28 @@ int knnm_draws_insert(knnm_ctx *ctx, const int32_t *rows, const int32_t *pool,
 int knnm_round(knnm_ctx *ctx, int32_t mode, int32_t rev_cap,
                uint64_t round_seed, int64_t *pairs, int64_t *accepted);
 
+/* Id-sharded rounds.  The context owns local rows [lo, hi);
+ * list arrays stay replicated between rounds (the host all-gathers owned row
+ * blocks after each round, see paper_1908_00814_b200/distributed.py).
+ * knnm_round_local runs the reverse step into owned rows, the hoods of owned
+ * vertices and the local join over them, leaving reference-order update
+ * slots for EVERY target row: cnt (u32, n) slots per target, boff (u64, n+1)
+ * their offsets, Bd (f64) / Bs (int32) the slots -- rows of rank q are the
+ * contiguous slot range [boff[lo_q], boff[hi_q]).  knnm_round_apply applies
+ * owned rows from nsrc received blocks in source-rank order (= hood order =
+ * the reference's order): recv_cnt (nsrc, hi-lo) u32 device array,
+ * recv_base host array of nsrc element offsets of each block in recv_Bd /
+ * recv_Bs (device).  knnm_local_views / knnm_state_views expose device
+ * pointers for the collectives. */
+int knnm_set_shard(knnm_ctx *ctx, int64_t lo, int64_t hi);
+int knnm_round_local(knnm_ctx *ctx, int32_t mode, int32_t rev_cap,
+                     uint64_t round_seed, int64_t *pairs_local);
+int knnm_local_views(knnm_ctx *ctx, void **cnt, void **boff, void **Bd, void **Bs);
+int knnm_round_apply(knnm_ctx *ctx, int32_t nsrc, const uint32_t *recv_cnt,
+                     const uint64_t *recv_base, const double *recv_Bd,
+                     const int32_t *recv_Bs, int64_t *accepted);
+int knnm_state_views(knnm_ctx *ctx, void **ids, void **dists, void **flags, void **sizes);
+
 /* phi over the current lists (construct.py:79-83), with numpy's pairwise
  * summation order, so the value is bit-identical to the reference. */
 int knnm_phi(knnm_ctx *ctx, double *out);

@@ -73,6 +73,11 @@ SIGNATURES = {
     "knnm_draws_replace": (ctypes.c_int, [P, P, I64, P, P, PI64]),
     "knnm_draws_insert": (ctypes.c_int, [P, P, P, I64, PI64]),
     "knnm_round": (ctypes.c_int, [P, I32, I32, U64, PI64, PI64]),
+    "knnm_set_shard": (ctypes.c_int, [P, I64, I64]),
+    "knnm_round_local": (ctypes.c_int, [P, I32, I32, U64, PI64]),
+    "knnm_local_views": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]),
+    "knnm_round_apply": (ctypes.c_int, [P, I32, P, P, P, P, PI64]),
+    "knnm_state_views": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]),
     "knnm_phi": (ctypes.c_int, [P, PDBL]),
     "knnm_export": (ctypes.c_int, [P, I32, P, P, P]),
     "knnm_export_dev": (ctypes.c_int, [P, I32, P, P, P]),

@@ -116,6 +116,7 @@ struct knnm_ctx {
     DBuf tail_ids, tail_d, tail_s;
     int tk = 0;
     bool have_tail = false;
+    int64_t shard_lo = 0, shard_hi = -1;  // owned rows (sharded rounds); -1 = n
     // round scratch
     DBuf indeg, roff, rev, heavy, giant, gscratch32, nbh, nlen, hpairs, poff, worst0, active;
     DBuf bound, boff, mcount, moff, mcur, memb, start, Bd, Bs;
@@ -243,6 +244,12 @@ int scan(knnm_ctx *c, const TI *in, TO *out, int64_t n, int level = 0) {
 }
 
 uint64_t bucket_budget(knnm_ctx *c) { return c->cand_budget_bytes / (sizeof(double) + sizeof(int32_t)); }
+
+int ensure_slots_noinit(knnm_ctx *c, uint64_t slots) {
+    TRY(ensure(c->Bd, sizeof(double) * slots));
+    TRY(ensure(c->Bs, sizeof(int32_t) * slots));
+    return KNNM_OK;
+}
 
 int ensure_slots(knnm_ctx *c, uint64_t slots) {
     TRY(ensure(c->Bd, sizeof(double) * slots));
@@ -540,6 +547,8 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     CK(cudaMemsetAsync(c->indeg.p, 0, sizeof(uint32_t) * (n + 1), c->st));
     c->tk = 0;
     c->have_tail = false;
+    c->shard_lo = 0;
+    c->shard_hi = -1;
     c->begun = true;
     return KNNM_OK;
 }
@@ -788,8 +797,8 @@ int knnm_draws_insert(knnm_ctx *c, const int32_t *rows, const int32_t *pool, int
     return insert_impl(c, rows, c->draw_n, c->draw_t, nullptr, m, accepted, true);
 }
 
-int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, int64_t *pairs,
-               int64_t *accepted) {
+static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed,
+                      int64_t *pairs, int64_t *accepted, bool local_only) {
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     if (mode < 0 || mode > 2) return fail(KNNM_ERR_ARG, "mode %d", mode);
@@ -798,21 +807,24 @@ int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, 
     int64_t n = c->n;
     int k = c->k;
     int W = k + rev_cap;
+    // owned rows: all of them, or the shard set by knnm_set_shard
+    const int64_t lo = local_only ? c->shard_lo : 0;
+    const int64_t hi = local_only ? (c->shard_hi < 0 ? n : c->shard_hi) : n;
     unsigned long long *cnt = c->counters.as<unsigned long long>();
     CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
     {
         PhaseTimer pt(c, PH_REVERSE);
         CK(cudaMemsetAsync(c->indeg.p, 0, sizeof(uint32_t) * (n + 1), c->st));
         k_rev_count<<<grid_for(c, n * k, 256), 256, 0, c->st>>>(
-            c->ids.as<int32_t>(), c->sizes.as<int32_t>(), n, k, c->indeg.as<uint32_t>());
+            c->ids.as<int32_t>(), c->sizes.as<int32_t>(), n, k, c->indeg.as<uint32_t>(), lo, hi);
         CKL();
         TRY(scan<uint32_t, uint32_t>(c, c->indeg.as<uint32_t>(), c->roff.as<uint32_t>(), n));
         k_rev_fill<<<grid_for(c, n * k, 256), 256, 0, c->st>>>(
             c->ids.as<int32_t>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), n, k,
-            c->roff.as<uint32_t>(), c->indeg.as<uint32_t>(), c->rev.as<uint32_t>());
+            c->roff.as<uint32_t>(), c->indeg.as<uint32_t>(), c->rev.as<uint32_t>(), lo, hi);
         CKL();
-        k_find_heavy<<<grid_for(c, n, 256), 256, 0, c->st>>>(
-            c->roff.as<uint32_t>(), n, std::max(rev_cap, WARP_REV_MAX), c->heavy.as<int32_t>(), cnt);
+        k_find_heavy<<<grid_for(c, hi - lo, 256), 256, 0, c->st>>>(
+            c->roff.as<uint32_t>(), lo, hi, std::max(rev_cap, WARP_REV_MAX), c->heavy.as<int32_t>(), cnt);
         CKL();
         k_rev_heavy<<<c->sms * 2, 256, 2 * sizeof(uint32_t) * BLOCK_SORT_MAX, c->st>>>(
             c->heavy.as<int32_t>(), cnt, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(), rev_cap,
@@ -830,12 +842,21 @@ int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, 
     }
     {
         PhaseTimer pt(c, PH_ASSEMBLE);
-        k_assemble<<<grid_for(c, n * 32, ASM_WARPS * 32, 16), ASM_WARPS * 32, 0, c->st>>>(
+        if (local_only) {
+            // the join needs the round-start worst of every row (lists are
+            // replicated); hoods outside the shard contribute no pairs
+            k_worst0_all<<<grid_for(c, n, 256), 256, 0, c->st>>>(c->sizes.as<int32_t>(),
+                                                                 c->dists.as<double>(), n, k,
+                                                                 c->worst0.as<double>());
+            CKL();
+            CK(cudaMemsetAsync(c->hpairs.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+        }
+        k_assemble<<<grid_for(c, (hi - lo) * 32, ASM_WARPS * 32, 16), ASM_WARPS * 32, 0, c->st>>>(
             c->ids.as<int32_t>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
-            c->dists.as<double>(), n, k, rev_cap, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(),
+            c->dists.as<double>(), hi, k, rev_cap, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(),
             round_seed, c->labels.as<int8_t>(), mode, W, c->nbh.as<uint32_t>(),
             c->nlen.as<int32_t>(), c->hpairs.as<uint32_t>(), c->worst0.as<double>(),
-            c->active.as<int32_t>(), cnt);
+            c->active.as<int32_t>(), cnt, lo);
         CKL();
         TRY(scan<uint32_t, uint64_t>(c, c->hpairs.as<uint32_t>(), c->poff.as<uint64_t>(), n));
     }
@@ -965,6 +986,11 @@ int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, 
                 CKL();
                 c->stats.join_launches += 1;
             }
+            if (local_only) {  // slots stay for the exchange (knnm_local_views)
+                TRY(sync_counters(c));
+                c->stats.exact_evals += (int64_t)c->hcnt[C_EXACT];
+                return KNNM_OK;
+            }
             {
                 PhaseTimer pt(c, PH_UPDATE);
                 TRY(run_updates(c));
@@ -974,6 +1000,8 @@ int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, 
             return KNNM_OK;
         };
         const uint64_t budget = bucket_budget(c);
+        if (local_only && 2 * P > budget)
+            return fail(KNNM_ERR_LIMIT, "sharded round needs %llu slots > budget", (unsigned long long)(2 * P));
         if (2 * P <= budget) {
             TRY(run_chunk(c->active.as<int32_t>(), (int64_t)nactive, 2 * P));
         } else {
@@ -1012,6 +1040,91 @@ int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, 
     TRY(resolve_timers(c));
     if (pairs) *pairs = (int64_t)P;
     if (accepted) *accepted = acc_total;
+    return KNNM_OK;
+}
+
+int knnm_round(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed, int64_t *pairs,
+               int64_t *accepted) {
+    return round_impl(c, mode, rev_cap, round_seed, pairs, accepted, false);
+}
+
+int knnm_set_shard(knnm_ctx *c, int64_t lo, int64_t hi) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    if (lo < 0 || hi < lo || hi > c->n) return fail(KNNM_ERR_ARG, "bad shard [%lld, %lld)", (long long)lo, (long long)hi);
+    c->shard_lo = lo;
+    c->shard_hi = hi;
+    return KNNM_OK;
+}
+
+int knnm_round_local(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed,
+                     int64_t *pairs_local) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    if (c->capture) return fail(KNNM_ERR_STATE, "on_pair capture is not supported in sharded rounds");
+    // an empty round leaves empty slot views
+    CK(cudaSetDevice(c->device));
+    CK(cudaMemsetAsync(c->bound.p, 0, sizeof(uint32_t) * (c->n + 1), c->st));
+    CK(cudaMemsetAsync(c->boff.p, 0, sizeof(uint64_t) * (c->n + 1), c->st));
+    return round_impl(c, mode, rev_cap, round_seed, pairs_local, nullptr, true);
+}
+
+int knnm_local_views(knnm_ctx *c, void **cnt, void **boff, void **Bd, void **Bs) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    TRY(ensure_slots_noinit(c, 1));
+    if (cnt) *cnt = c->bound.p;
+    if (boff) *boff = c->boff.p;
+    if (Bd) *Bd = c->Bd.p;
+    if (Bs) *Bs = c->Bs.p;
+    return KNNM_OK;
+}
+
+int knnm_round_apply(knnm_ctx *c, int32_t nsrc, const uint32_t *recv_cnt, const uint64_t *recv_base,
+                     const double *recv_Bd, const int32_t *recv_Bs, int64_t *accepted) {
+    if (!c || nsrc < 1 || !recv_cnt || !recv_base) return fail(KNNM_ERR_ARG, "bad argument");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    CK(cudaSetDevice(c->device));
+    const int64_t lo = c->shard_lo, hi = c->shard_hi < 0 ? c->n : c->shard_hi, no = hi - lo;
+    unsigned long long *cnt = c->counters.as<unsigned long long>();
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
+    if (accepted) *accepted = 0;
+    if (no == 0) return KNNM_OK;
+    PhaseTimer pt(c, PH_UPDATE);
+    TRY(ensure(c->stage[2], sizeof(uint64_t) * (size_t)nsrc * (no + 1)));
+    uint64_t *off = c->stage[2].as<uint64_t>();
+    for (int s = 0; s < nsrc; s++) {
+        TRY(scan<uint32_t, uint64_t>(c, recv_cnt + (size_t)s * no, off + (size_t)s * (no + 1), no));
+        if (recv_base[s]) {
+            k_add_base<<<grid_for(c, no + 1, 256), 256, 0, c->st>>>(off + (size_t)s * (no + 1), no + 1,
+                                                                   recv_base[s]);
+            CKL();
+        }
+    }
+    const int E = (c->k + 31) / 32;
+    const int blocks = grid_for(c, no * 32, APPLY_WARPS * 32, 16);
+    if (E == 1)
+        k_apply_stream_multi<1><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
+            lo, no, c->k, nsrc, off, recv_cnt, recv_Bd, recv_Bs, c->ids.as<int32_t>(),
+            c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), cnt);
+    else
+        k_apply_stream_multi<2><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
+            lo, no, c->k, nsrc, off, recv_cnt, recv_Bd, recv_Bs, c->ids.as<int32_t>(),
+            c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), cnt);
+    CKL();
+    TRY(sync_counters(c));
+    c->stats.accepted += (int64_t)c->hcnt[C_ACCEPTED];
+    if (accepted) *accepted = (int64_t)c->hcnt[C_ACCEPTED];
+    return KNNM_OK;
+}
+
+int knnm_state_views(knnm_ctx *c, void **ids, void **dists, void **flags, void **sizes) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    if (ids) *ids = c->ids.p;
+    if (dists) *dists = c->dists.p;
+    if (flags) *flags = c->flags.p;
+    if (sizes) *sizes = c->sizes.p;
     return KNNM_OK;
 }
 

@@ -316,25 +316,29 @@ __global__ void k_directed_emit(const int32_t *__restrict__ rows, const int32_t 
 // (Fisher-Yates subsampling) by sorting on the source id in the assemble step.
 // ---------------------------------------------------------------------------
 __global__ void k_rev_count(const int32_t *__restrict__ ids, const int32_t *__restrict__ sizes,
-                            int64_t n, int k, uint32_t *indeg) {
-    int64_t total = n * k;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t r = i / k;
-        int t = (int)(i % k);
-        if (t < sizes[r]) atomicAdd(&indeg[ids[i]], 1u);
-    }
-}
-
-__global__ void k_rev_fill(const int32_t *__restrict__ ids, const uint8_t *__restrict__ flags,
-                           const int32_t *__restrict__ sizes, int64_t n, int k,
-                           const uint32_t *__restrict__ roff, uint32_t *indeg, uint32_t *rev) {
+                            int64_t n, int k, uint32_t *indeg, int64_t tlo, int64_t thi) {
     int64_t total = n * k;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t r = i / k;
         int t = (int)(i % k);
         if (t < sizes[r]) {
+            const int32_t j = ids[i];
+            if (j >= tlo && j < thi) atomicAdd(&indeg[j], 1u);
+        }
+    }
+}
+
+__global__ void k_rev_fill(const int32_t *__restrict__ ids, const uint8_t *__restrict__ flags,
+                           const int32_t *__restrict__ sizes, int64_t n, int k,
+                           const uint32_t *__restrict__ roff, uint32_t *indeg, uint32_t *rev,
+                           int64_t tlo, int64_t thi) {
+    int64_t total = n * k;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t r = i / k;
+        int t = (int)(i % k);
+        if (t < sizes[r] && ids[i] >= tlo && ids[i] < thi) {
             int32_t j = ids[i];
             uint32_t p = roff[j] + atomicSub(&indeg[j], 1u) - 1u;
             rev[p] = ((uint32_t)r << 1) | (uint32_t)flags[i];
@@ -342,9 +346,9 @@ __global__ void k_rev_fill(const int32_t *__restrict__ ids, const uint8_t *__res
     }
 }
 
-__global__ void k_find_heavy(const uint32_t *__restrict__ roff, int64_t n, int limit,
+__global__ void k_find_heavy(const uint32_t *__restrict__ roff, int64_t lo, int64_t n, int limit,
                              int32_t *heavy, unsigned long long *counters) {
-    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+    for (int64_t u = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
          u += (int64_t)gridDim.x * blockDim.x) {
         uint32_t deg = roff[u + 1] - roff[u];
         if (deg > (uint32_t)limit) {
@@ -438,7 +442,8 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
            const double *__restrict__ dists, int64_t n, int k, int rev_cap,
            const uint32_t *__restrict__ roff, const uint32_t *__restrict__ rev, uint64_t seed,
            const int8_t *__restrict__ labels, int mode, int W, uint32_t *nbh, int32_t *nlen,
-           uint32_t *hpairs, double *worst0, int32_t *active, unsigned long long *counters) {
+           uint32_t *hpairs, double *worst0, int32_t *active, unsigned long long *counters,
+           int64_t lo) {
     __shared__ uint32_t s_seg[ASM_WARPS][WARP_REV_MAX];
     __shared__ uint32_t s_idx[ASM_WARPS][WARP_REV_MAX];
     __shared__ uint32_t s_R[ASM_WARPS][MAX_W];
@@ -447,7 +452,7 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
     uint32_t *seg = s_seg[wib], *idx = s_idx[wib], *R = s_R[wib], *buf = s_buf[wib];
     int64_t nw = (int64_t)gridDim.x * ASM_WARPS;
     unsigned long long members = 0;
-    for (int64_t u = (int64_t)blockIdx.x * ASM_WARPS + wib; u < n; u += nw) {
+    for (int64_t u = lo + (int64_t)blockIdx.x * ASM_WARPS + wib; u < n; u += nw) {
         int sz = sizes[u];
         for (int t = lane; t < sz; t += 32)
             buf[t] = ((uint32_t)ids[u * k + t] << 1) | (uint32_t)flags[u * k + t];
@@ -1354,6 +1359,63 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
     }
     if (lane == 0 && acc) atomicAdd(&counters[C_ACCEPTED], acc);
     if (lane == 0 && slots) atomicAdd(&counters[C_CAND], slots);
+}
+
+// Round-start worst of every row (sharded rounds: the join needs the
+// snapshot of rows owned by other ranks; lists are replicated).
+__global__ void k_worst0_all(const int32_t *__restrict__ sizes, const double *__restrict__ dists,
+                             int64_t n, int k, double *worst0) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x)
+        worst0[r] = sizes[r] == k ? dists[r * k + k - 1] : __longlong_as_double(0x7ff0000000000000LL);
+}
+
+// Sharded rounds: row r (owned, r in [lo, lo+no)) receives one slot block per
+// source rank; blocks are processed in source order, which is hood order,
+// which is the reference's order.  off[s * (no+1) + i] = element offset of
+// row lo+i's segment in the receive buffers.
+template <int E>
+__global__ void __launch_bounds__(APPLY_WARPS * 32)
+k_apply_stream_multi(int64_t lo, int64_t no, int k, int nsrc, const uint64_t *__restrict__ off,
+                     const uint32_t *__restrict__ cnt, const double *__restrict__ Bd,
+                     const int32_t *__restrict__ Bs, int32_t *ids, double *dists, uint8_t *flags,
+                     int32_t *sizes, unsigned long long *counters) {
+    const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
+    const int64_t nw = (int64_t)gridDim.x * APPLY_WARPS;
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    unsigned long long acc = 0;
+    for (int64_t i = (int64_t)blockIdx.x * APPLY_WARPS + wib; i < no; i += nw) {
+        const int64_t r = lo + i;
+        bool any = false;
+        for (int s = 0; s < nsrc && !any; s++) any = cnt[(int64_t)s * no + i] != 0;
+        if (!any) continue;
+        WarpRow<E> st;
+        row_load<E>(st, ids, dists, flags, sizes, r, k, lane);
+        int a = 0;
+        for (int s = 0; s < nsrc; s++) {
+            const uint64_t base = off[(int64_t)s * (no + 1) + i];
+            const int64_t ns = cnt[(int64_t)s * no + i];
+            for (int64_t c0 = 0; c0 < ns; c0 += 32) {
+                const int64_t j = c0 + lane;
+                double dl = j < ns ? Bd[base + j] : inf;
+                if (dl != dl) dl = inf;
+                const bool pre = j < ns && (dl < st.worst || (st.sz < k && dl < inf));
+                if (!__any_sync(FULL_MASK, pre)) continue;
+                const int src = pre ? Bs[base + j] : 0;
+                const int c = ns - c0 < 32 ? (int)(ns - c0) : 32;
+                a += warp_apply_chunk<E>(st, k, src, dl, c, lane);
+            }
+        }
+        if (a) row_store<E>(st, ids, dists, flags, sizes, r, k, lane);
+        acc += a;
+    }
+    if (lane == 0 && acc) atomicAdd(&counters[C_ACCEPTED], acc);
+}
+
+__global__ void k_add_base(uint64_t *off, int64_t m, uint64_t base) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x)
+        off[i] += base;
 }
 
 // ---------------------------------------------------------------------------

@@ -1,0 +1,62 @@
+"""Sharded (multi-rank) merges on one GPU: P virtual ranks in one process
+(LoopbackComm), each with its own engine context, run the full id-sharded
+protocol -- per-rank reverse/hoods/join, all-to-all of reference-order slot
+blocks, per-owner apply, all-gather -- and must be bit-identical to the
+single-GPU merge (and so to the reference)."""
+
+import numpy as np
+import pytest
+
+from conftest import split_ids
+
+pytestmark = pytest.mark.gpu
+
+
+def _engines(world):
+    from paper_1908_00814_b200.engine import Engine
+
+    return {r: Engine(0) for r in range(world)}
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+@pytest.mark.parametrize("kind", ["intgmm", "uniform"])
+def test_sharded_s_merge_bit_identical(oracle, world, kind):
+    import paper_1908_00814_b200 as km
+    from paper_1908_00814_b200 import distributed as D
+
+    n = 3000
+    ds = (km.generate_int_gmm(n, 128, n_centres=30, seed=3) if kind == "intgmm"
+          else km.generate_uniform(n, 16, seed=3))
+    s1, s2 = split_ids(n, seed=2)
+    g = km.nn_descent(ds, km.Metric.L2, km.DescentParams(k=12), 1, member_ids=s1)
+    h = km.nn_descent(ds, km.Metric.L2, km.DescentParams(k=12), 2, member_ids=s2)
+    mp = km.MergeParams(k=12, seed=5)
+    c1 = km.DistanceCounter()
+    want, rep_w = km.s_merge(ds, g, h, mp, counter=c1, return_report=True)
+    c2 = km.DistanceCounter()
+    got, rep_g = D.s_merge_sharded(ds, g, h, mp, D.LoopbackComm(world), _engines(world),
+                                   counter=c2, return_report=True)
+    assert np.array_equal(got.ids, want.ids)
+    assert np.array_equal(got.dists, want.dists)
+    assert np.array_equal(got.sizes, want.sizes)
+    assert c1.count == c2.count
+    assert [(r.pairs, r.updates, r.phi) for r in rep_g.rounds] == \
+        [(r.pairs, r.updates, r.phi) for r in rep_w.rounds]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_j_merge_bit_identical(oracle, world):
+    import paper_1908_00814_b200 as km
+    from paper_1908_00814_b200 import distributed as D
+
+    ds = km.generate_sphere_gmm(2500, 100, n_centres=20, seed=4)
+    s1, s2 = split_ids(2500, seed=8)
+    g = km.nn_descent(ds, km.Metric.COSINE, km.DescentParams(k=16), 1, member_ids=s1)
+    mp = km.MergeParams(k=16, seed=7)
+    want, rep_w = km.j_merge(ds, g, s2, mp, return_report=True)
+    got, rep_g = D.j_merge_sharded(ds, g, s2, mp, D.LoopbackComm(world), _engines(world),
+                                   return_report=True)
+    assert np.array_equal(got.ids, want.ids)
+    assert np.array_equal(got.dists, want.dists)
+    assert [(r.pairs, r.updates, r.phi) for r in rep_g.rounds] == \
+        [(r.pairs, r.updates, r.phi) for r in rep_w.rounds]
