@@ -144,6 +144,22 @@ int knnm_draws_replace(knnm_ctx *ctx, const int64_t *rows, int64_t nrows,
 int knnm_draws_insert(knnm_ctx *ctx, const int32_t *rows, const int32_t *pool,
                       int64_t npool, int64_t *accepted);
 
+/* Device-side draws for knnm_draws_*: a bit-exact restatement of numpy's
+ * PCG64 + Generator.integers(0, m, size=(nrows, t)) (pcg64.h,
+ * distributions.c buffered_bounded_lemire_uint32).  pcg = {state_hi,
+ * state_lo, inc_hi, inc_lo} of rng.bit_generator.state; has_uint32 /
+ * uinteger its half-buffer.  *consumed = raw 32-bit values used, so the
+ * caller can advance its generator to the identical state.  gen fills the
+ * whole matrix; regen redraws the listed rows (ascending, row-major, as
+ * `cand[rows] = rng.integers(0, m, size=(len(rows), t))`).  Both return the
+ * rows that contain a repeated value, as knnm_draws_load does. */
+int knnm_draws_gen(knnm_ctx *ctx, const uint64_t *pcg, int32_t has_uint32,
+                   uint32_t uinteger, uint64_t m, int64_t nrows, int32_t t,
+                   int64_t *consumed, int64_t *bad, int64_t *nbad);
+int knnm_draws_regen(knnm_ctx *ctx, const uint64_t *pcg, int32_t has_uint32,
+                     uint32_t uinteger, uint64_t m, const int64_t *rows,
+                     int64_t nrows, int64_t *consumed, int64_t *bad, int64_t *nbad);
+
 /* One local-join round.  Replaces one iteration of _descent_rounds
  * (construct.py:136-164): reverse_csr, assemble_neighborhoods (rev_cap),
  * flag clear, count_pairs/fill_pairs, pair_dists_dense and
@@ -208,6 +224,11 @@ int knnm_capture_fetch(knnm_ctx *ctx, int32_t *pa, int32_t *pb, double *pd,
  * datasets with the dot-form certificate, otherwise auto).  All routes give
  * bit-identical results; the switch exists for tests and measurement. */
 int knnm_set_join_variant(knnm_ctx *ctx, int32_t variant);
+
+/* Hood processing order (performance only; results are independent of it):
+ * iters > 0 rounds of min-label propagation over the lists build a
+ * locality order once per merge; 0 processes hoods in id order. */
+int knnm_set_locality(knnm_ctx *ctx, int32_t iters);
 
 /* Dataset facts: cert bit 0 = fp32 difference-form arithmetic is provably
  * exact (integer entries, d*range^2 < 2^24 for L2); bit 1 = fp16 rows with

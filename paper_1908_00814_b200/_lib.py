@@ -72,6 +72,8 @@ SIGNATURES = {
     "knnm_draws_load": (ctypes.c_int, [P, P, I64, I32, P, PI64]),
     "knnm_draws_replace": (ctypes.c_int, [P, P, I64, P, P, PI64]),
     "knnm_draws_insert": (ctypes.c_int, [P, P, P, I64, PI64]),
+    "knnm_draws_gen": (ctypes.c_int, [P, P, I32, ctypes.c_uint32, U64, I64, I32, PI64, P, PI64]),
+    "knnm_draws_regen": (ctypes.c_int, [P, P, I32, ctypes.c_uint32, U64, P, I64, PI64, P, PI64]),
     "knnm_round": (ctypes.c_int, [P, I32, I32, U64, PI64, PI64]),
     "knnm_set_shard": (ctypes.c_int, [P, I64, I64]),
     "knnm_round_local": (ctypes.c_int, [P, I32, I32, U64, PI64]),
@@ -86,6 +88,7 @@ SIGNATURES = {
     "knnm_capture_count": (ctypes.c_int, [P, PI64]),
     "knnm_capture_fetch": (ctypes.c_int, [P, P, P, P, I64]),
     "knnm_set_join_variant": (ctypes.c_int, [P, I32]),
+    "knnm_set_locality": (ctypes.c_int, [P, I32]),
     "knnm_get_info": (ctypes.c_int, [P, ctypes.POINTER(I32), ctypes.POINTER(I32)]),
     "knnm_set_profiling": (ctypes.c_int, [P, I32]),
     "knnm_get_stats": (ctypes.c_int, [P, ctypes.POINTER(KnnmStats)]),

@@ -120,8 +120,11 @@ struct knnm_ctx {
     // round scratch
     DBuf indeg, roff, rev, heavy, giant, gscratch32, nbh, nlen, hpairs, poff, worst0, active;
     DBuf bound, boff, mcount, moff, mcur, memb, start, Bd, Bs;
+    DBuf order, lab0, lab1;       // locality order of hoods (per merge)
+    bool have_order = false;
+    int locality_iters = 8;
     uint64_t memb_cap = 0, start_cap = 0;
-    DBuf draws, draw_rows, draw_bad, pool;  // random-append draw matrix (device)
+    DBuf draws, draw_rows, draw_bad, pool, scan_pos;  // random-append draw matrix (device)
     int64_t draw_n = 0;
     int draw_t = 0;
     DBuf scan_tmp[4], scan_off[4];
@@ -304,6 +307,34 @@ int run_updates(knnm_ctx *c) {
     return KNNM_OK;
 }
 
+// Locality order of the hoods for this merge (see k_label_prop).
+int build_locality_order(knnm_ctx *c) {
+    const int64_t n = c->n;
+    TRY(ensure(c->order, sizeof(int32_t) * n));
+    TRY(ensure(c->lab0, sizeof(int32_t) * (n + 1)));
+    TRY(ensure(c->lab1, sizeof(int32_t) * (n + 1)));
+    int32_t *a = c->lab0.as<int32_t>(), *b = c->lab1.as<int32_t>();
+    k_iota<<<grid_for(c, n, 256), 256, 0, c->st>>>(a, n);
+    CKL();
+    for (int it = 0; it < c->locality_iters; it++) {
+        k_label_prop<<<grid_for(c, n, 256), 256, 0, c->st>>>(c->ids.as<int32_t>(), c->flags.as<uint8_t>(),
+                                                            c->sizes.as<int32_t>(), n, c->k, a, b);
+        CKL();
+        std::swap(a, b);
+    }
+    // counting sort by label (labels are row ids in [0, n))
+    CK(cudaMemsetAsync(c->mcount.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+    CK(cudaMemsetAsync(c->mcur.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+    k_label_hist<<<grid_for(c, n, 256), 256, 0, c->st>>>(a, n, c->mcount.as<uint32_t>());
+    CKL();
+    TRY(scan<uint32_t, uint32_t>(c, c->mcount.as<uint32_t>(), c->moff.as<uint32_t>(), n));
+    k_label_scatter<<<grid_for(c, n, 256), 256, 0, c->st>>>(a, n, c->moff.as<uint32_t>(),
+                                                           c->mcur.as<uint32_t>(), c->order.as<int32_t>());
+    CKL();
+    c->have_order = true;
+    return KNNM_OK;
+}
+
 void build_phi_tree(PhiTree &t, int64_t N) {
     t.N = N;
     t.leaf_lo.clear();
@@ -391,9 +422,9 @@ int knnm_destroy(knnm_ctx *c) {
     DBuf *all[] = {&c->vec, &c->sub, &c->ugid, &c->labels, &c->ids, &c->dists, &c->flags,
                    &c->sizes, &c->tail_ids, &c->tail_d, &c->tail_s, &c->indeg, &c->roff,
                    &c->rev, &c->heavy, &c->giant, &c->gscratch32, &c->nbh, &c->nlen, &c->hpairs,
-                   &c->poff, &c->worst0, &c->active, &c->bound, &c->boff, &c->mcount, &c->moff, &c->mcur, &c->memb, &c->start, &c->Bd, &c->Bs,
+                   &c->poff, &c->worst0, &c->active, &c->order, &c->lab0, &c->lab1, &c->bound, &c->boff, &c->mcount, &c->moff, &c->mcur, &c->memb, &c->start, &c->Bd, &c->Bs,
                    &c->counters, &c->draws, &c->draw_rows,
-                   &c->draw_bad, &c->pool, &c->vec16, &c->norms, &c->sub16, &c->subnorms, &c->out_ids, &c->out_d,
+                   &c->draw_bad, &c->pool, &c->scan_pos, &c->vec16, &c->norms, &c->sub16, &c->subnorms, &c->out_ids, &c->out_d,
                    &c->out_s, &c->phi_leaf_lo, &c->phi_leaf_len, &c->phi_left, &c->phi_right,
                    &c->phi_level, &c->phi_leaves, &c->phi_inner};
     for (DBuf *b : all) release(*b);
@@ -549,6 +580,7 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     c->have_tail = false;
     c->shard_lo = 0;
     c->shard_hi = -1;
+    c->have_order = false;
     c->begun = true;
     return KNNM_OK;
 }
@@ -744,6 +776,80 @@ static int dup_check(knnm_ctx *c, const int64_t *rows_dev, int64_t nchk, int64_t
     return KNNM_OK;
 }
 
+// Generate N = (#rows) * t numpy-identical draws on the device (see
+// k_pcg_raw).  rows == nullptr: fill the whole draw matrix; else overwrite
+// the listed rows (device array).  *consumed = raw u32 values used.
+static int pcg_fill(knnm_ctx *c, const uint64_t *st, int has0, uint32_t uint0, uint64_t m,
+                    int64_t N, const int64_t *rows_dev, int64_t *consumed) {
+    if (m == 0 || m > 0xFFFFFFFFull) return fail(KNNM_ERR_LIMIT, "draw range %llu", (unsigned long long)m);
+    if (N == 0) {
+        *consumed = 0;
+        return KNNM_OK;
+    }
+    int64_t R = N + N / 512 + 256;
+    for (int attempt = 0; attempt < 8; attempt++) {
+        TRY(ensure(c->stage[2], sizeof(uint32_t) * 2 * (size_t)(R + 1)));
+        TRY(ensure(c->scan_pos, sizeof(uint64_t) * (size_t)(R + 1)));
+        uint32_t *val = c->stage[2].as<uint32_t>(), *acc = val + (R + 1);
+        const int per = 16;
+        const int64_t nout = (R + 1) / 2 + 1;
+        k_pcg_raw<<<grid_for(c, (nout + per - 1) / per, 256, 8), 256, 0, c->st>>>(
+            st[0], st[1], st[2], st[3], has0, uint0, m, R, per, val, acc);
+        CKL();
+        TRY(scan<uint32_t, uint64_t>(c, acc, c->scan_pos.as<uint64_t>(), R));
+        uint64_t total = 0;
+        CK(cudaMemcpyAsync(&total, c->scan_pos.as<uint64_t>() + R, sizeof(uint64_t), cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        if ((int64_t)total < N) {  // more Lemire rejections than the slack
+            R = R * 2;
+            continue;
+        }
+        unsigned long long *cnt = c->counters.as<unsigned long long>();
+        k_pcg_compact<<<grid_for(c, R, 256), 256, 0, c->st>>>(val, acc, c->scan_pos.as<uint64_t>(), R, N,
+                                                           c->draws.as<int64_t>(), rows_dev, c->draw_t,
+                                                           cnt + C_MAXC);
+        CKL();
+        TRY(sync_counters(c));
+        *consumed = (int64_t)c->hcnt[C_MAXC] + 1;
+        return KNNM_OK;
+    }
+    return fail(KNNM_ERR_LIMIT, "could not generate %lld draws", (long long)N);
+}
+
+int knnm_draws_gen(knnm_ctx *c, const uint64_t *pcg, int32_t has_uint32, uint32_t uinteger,
+                   uint64_t m, int64_t nrows, int32_t t, int64_t *consumed, int64_t *bad,
+                   int64_t *nbad) {
+    if (!c || !pcg || !consumed || !bad || !nbad || nrows < 0 || t < 1) return fail(KNNM_ERR_ARG, "bad argument");
+    CK(cudaSetDevice(c->device));
+    PhaseTimer pt(c, PH_OTHER);
+    const size_t mm = (size_t)nrows * t;
+    TRY(ensure(c->draws, sizeof(int64_t) * (mm + 1)));
+    TRY(ensure(c->draw_bad, sizeof(int64_t) * (nrows + 1)));
+    TRY(ensure(c->draw_rows, sizeof(int64_t) * (nrows + 1)));
+    c->draw_n = nrows;
+    c->draw_t = t;
+    TRY(pcg_fill(c, pcg, has_uint32, uinteger, m, (int64_t)mm, nullptr, consumed));
+    return dup_check(c, nullptr, 0, bad, nbad);
+}
+
+int knnm_draws_regen(knnm_ctx *c, const uint64_t *pcg, int32_t has_uint32, uint32_t uinteger,
+                     uint64_t m, const int64_t *rows, int64_t nrows, int64_t *consumed, int64_t *bad,
+                     int64_t *nbad) {
+    if (!c || !pcg || !rows || !consumed || !bad || !nbad) return fail(KNNM_ERR_ARG, "bad argument");
+    if (nrows > c->draw_n) return fail(KNNM_ERR_ARG, "too many rows");
+    CK(cudaSetDevice(c->device));
+    PhaseTimer pt(c, PH_OTHER);
+    if (nrows == 0) {
+        *consumed = 0;
+        *nbad = 0;
+        return KNNM_OK;
+    }
+    TRY(h2d(c, c->draw_rows.p, rows, sizeof(int64_t) * nrows));
+    TRY(pcg_fill(c, pcg, has_uint32, uinteger, m, nrows * (int64_t)c->draw_t, c->draw_rows.as<int64_t>(),
+                 consumed));
+    return dup_check(c, c->draw_rows.as<int64_t>(), nrows, bad, nbad);
+}
+
 int knnm_draws_load(knnm_ctx *c, const int64_t *cand, int64_t nrows, int32_t t, int64_t *bad,
                     int64_t *nbad) {
     if (!c || !cand || !bad || !nbad || nrows < 0 || t < 1) return fail(KNNM_ERR_ARG, "bad argument");
@@ -840,6 +946,10 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
             CKL();
         }
     }
+    if (!local_only && !c->have_order && c->locality_iters > 0) {
+        PhaseTimer pt(c, PH_ASSEMBLE);
+        TRY(build_locality_order(c));
+    }
     {
         PhaseTimer pt(c, PH_ASSEMBLE);
         if (local_only) {
@@ -851,12 +961,15 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
             CKL();
             CK(cudaMemsetAsync(c->hpairs.p, 0, sizeof(uint32_t) * (n + 1), c->st));
         }
+        CK(cudaMemsetAsync(c->bound.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+        CK(cudaMemsetAsync(c->mcount.p, 0, sizeof(uint32_t) * (n + 1), c->st));
         k_assemble<<<grid_for(c, (hi - lo) * 32, ASM_WARPS * 32, 16), ASM_WARPS * 32, 0, c->st>>>(
             c->ids.as<int32_t>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
             c->dists.as<double>(), hi, k, rev_cap, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(),
             round_seed, c->labels.as<int8_t>(), mode, W, c->nbh.as<uint32_t>(),
             c->nlen.as<int32_t>(), c->hpairs.as<uint32_t>(), c->worst0.as<double>(),
-            c->active.as<int32_t>(), cnt, lo);
+            c->active.as<int32_t>(), cnt, lo, c->bound.as<uint32_t>(), c->mcount.as<uint32_t>(),
+            (!local_only && c->have_order) ? c->order.as<int32_t>() : nullptr);
         CKL();
         TRY(scan<uint32_t, uint64_t>(c, c->hpairs.as<uint32_t>(), c->poff.as<uint64_t>(), n));
     }
@@ -908,20 +1021,23 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         const double mrel = 1.0 + (double)(c->d + 8) * ldexp(1.0, -23);
         const double mabs = (double)(4 * c->d + 64) * ldexp(1.0, -24);
         // One pass per hood chunk: bounds -> bucket offsets -> join -> apply.
-        auto run_chunk = [&](const int32_t *act, int64_t nact, uint64_t pairs2) -> int {
+        auto run_chunk = [&](const int32_t *act, int64_t nact, uint64_t pairs2, bool counted) -> int {
             CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
             {
                 PhaseTimer pt(c, PH_JOIN);
-                // reference-order slot layout (see MembRec in knnm_kernels.cuh)
-                CK(cudaMemsetAsync(c->bound.p, 0, sizeof(uint32_t) * (n + 1), c->st));
-                CK(cudaMemsetAsync(c->mcount.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+                // reference-order slot layout (see MembRec in knnm_kernels.cuh);
+                // k_assemble already counted every active hood's memberships
                 CK(cudaMemsetAsync(c->mcur.p, 0, sizeof(uint32_t) * (n + 1), c->st));
                 const int hgrid = grid_for(c, nact * 32, 256, 16);
-                k_hood_memb<false><<<hgrid, 256, 0, c->st>>>(
-                    act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
-                    c->labels.as<int8_t>(), mode, c->bound.as<uint32_t>(), c->mcount.as<uint32_t>(),
-                    nullptr, nullptr, nullptr);
-                CKL();
+                if (!counted) {
+                    CK(cudaMemsetAsync(c->bound.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+                    CK(cudaMemsetAsync(c->mcount.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+                    k_hood_memb<false><<<hgrid, 256, 0, c->st>>>(
+                        act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
+                        c->labels.as<int8_t>(), mode, c->bound.as<uint32_t>(),
+                        c->mcount.as<uint32_t>(), nullptr, nullptr, nullptr);
+                    CKL();
+                }
                 TRY(scan<uint32_t, uint64_t>(c, c->bound.as<uint32_t>(), c->boff.as<uint64_t>(), n));
                 TRY(scan<uint32_t, uint32_t>(c, c->mcount.as<uint32_t>(), c->moff.as<uint32_t>(), n));
                 TRY(ensure_memb(c, (uint64_t)n * W, (uint64_t)n * W));
@@ -1003,7 +1119,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         if (local_only && 2 * P > budget)
             return fail(KNNM_ERR_LIMIT, "sharded round needs %llu slots > budget", (unsigned long long)(2 * P));
         if (2 * P <= budget) {
-            TRY(run_chunk(c->active.as<int32_t>(), (int64_t)nactive, 2 * P));
+            TRY(run_chunk(c->active.as<int32_t>(), (int64_t)nactive, 2 * P, true));
         } else {
             // Chunk hoods by index so each chunk's buckets fit; chunks run in
             // ascending hood order, which preserves the reference's per-row
@@ -1029,7 +1145,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                     CK(cudaMemcpyAsync(c->active.p, lst.data(), sizeof(int32_t) * lst.size(),
                                        cudaMemcpyHostToDevice, c->st));
                     TRY(run_chunk(c->active.as<int32_t>(), (int64_t)lst.size(),
-                                  2 * (hpoff[hi] - hpoff[lo])));
+                                  2 * (hpoff[hi] - hpoff[lo]), false));
                     CK(cudaStreamSynchronize(c->st));  // lst is reused
                 }
                 lo = hi;
@@ -1264,6 +1380,13 @@ int knnm_capture_fetch(knnm_ctx *c, int32_t *pa, int32_t *pb, double *pd, int64_
     c->cap_pa.clear();
     c->cap_pb.clear();
     c->cap_pd.clear();
+    return KNNM_OK;
+}
+
+int knnm_set_locality(knnm_ctx *c, int32_t iters) {
+    if (!c || iters < 0) return fail(KNNM_ERR_ARG, "bad argument");
+    c->locality_iters = iters;
+    c->have_order = false;
     return KNNM_OK;
 }
 

@@ -228,6 +228,99 @@ __global__ void k_repeat_rows(const int32_t *__restrict__ rows, int count, int64
         out[i] = rows[i / count];
 }
 
+// ---------------------------------------------------------------------------
+// numpy PCG64 (XSL-RR 128/64) + Generator.integers(0, m) on the device.
+// A bit-exact restatement of numpy/random/src/pcg64/pcg64.h (step, output,
+// next_uint32 with the has_uint32 half-buffer) and of
+// buffered_bounded_lemire_uint32 (distributions.c) -- the draws of
+// merge.py:156-163 (rng.integers(0, m, size=(nrows, t))).  The raw 32-bit
+// stream is produced in parallel by LCG jump-ahead; Lemire rejections are
+// removed by a scan, so draw j is the j-th accepted raw value, exactly as
+// numpy's sequential loop consumes them.  The host advances numpy's
+// generator state by the consumed raw count afterwards.
+// ---------------------------------------------------------------------------
+typedef unsigned __int128 u128;
+
+__host__ __device__ __forceinline__ u128 pcg_mult() {
+    return ((u128)0x2360ED051FC65DA4ULL << 64) | (u128)0x4385DF649FCCF645ULL;
+}
+
+__device__ __forceinline__ uint64_t pcg_out(u128 st) {
+    const uint64_t x = (uint64_t)(st >> 64) ^ (uint64_t)st;
+    const unsigned r = (unsigned)(st >> 122);
+    return (x >> r) | (x << ((64u - r) & 63u));
+}
+
+// state after `delta` LCG steps (pcg_advance_lcg_128)
+__device__ __forceinline__ u128 pcg_advance(u128 st, u128 inc, uint64_t delta) {
+    u128 acc_mult = 1, acc_plus = 0, cur_mult = pcg_mult(), cur_plus = inc;
+    while (delta > 0) {
+        if (delta & 1) {
+            acc_mult *= cur_mult;
+            acc_plus = acc_plus * cur_mult + cur_plus;
+        }
+        cur_plus = (cur_mult + 1) * cur_plus;
+        cur_mult *= cur_mult;
+        delta >>= 1;
+    }
+    return acc_mult * st + acc_plus;
+}
+
+// Raw u32 stream r = 0..R-1 -> (value, accepted).  With a buffered half
+// (has0), raw 0 is uint0 and raw r >= 1 comes from output (r-1)/2; else raw
+// r comes from output r/2 (low half first).  Each thread covers `per`
+// consecutive outputs.
+__global__ void k_pcg_raw(uint64_t st_hi, uint64_t st_lo, uint64_t inc_hi, uint64_t inc_lo, int has0,
+                          uint32_t uint0, uint64_t m, int64_t R, int per, uint32_t *val,
+                          uint32_t *acc) {
+    const u128 st0 = ((u128)st_hi << 64) | st_lo, inc = ((u128)inc_hi << 64) | inc_lo;
+    const uint32_t thr = (uint32_t)((0xFFFFFFFFull - (m - 1)) % m);
+    const int64_t nout = (R - (has0 ? 1 : 0) + 1) / 2;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t * per < nout;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t o0 = t * per;
+        u128 st = pcg_advance(st0, inc, (uint64_t)o0);
+        for (int q = 0; q < per && o0 + q < nout; q++) {
+            st = st * pcg_mult() + inc;
+            const uint64_t v = pcg_out(st);
+            const int64_t rbase = (has0 ? 1 : 0) + 2 * (o0 + q);
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+                const int64_t r = rbase + h;
+                if (r < R) {
+                    const uint32_t x = h ? (uint32_t)(v >> 32) : (uint32_t)v;
+                    const uint64_t mm = (uint64_t)x * m;
+                    val[r] = (uint32_t)(mm >> 32);
+                    acc[r] = ((uint32_t)mm >= thr) ? 1u : 0u;
+                }
+            }
+        }
+    }
+    if (has0 && blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint64_t mm = (uint64_t)uint0 * m;
+        val[0] = (uint32_t)(mm >> 32);
+        acc[0] = ((uint32_t)mm >= thr) ? 1u : 0u;
+    }
+}
+
+// Compact accepted raw values into draws[0..N) (row-major into the listed
+// rows of the draw matrix when rows != nullptr); record the raw index of
+// the N-th accepted value.
+__global__ void k_pcg_compact(const uint32_t *__restrict__ val, const uint32_t *__restrict__ acc,
+                              const uint64_t *__restrict__ pos, int64_t R, int64_t N,
+                              int64_t *draws, const int64_t *__restrict__ rows, int t,
+                              unsigned long long *last) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < R;
+         r += (int64_t)gridDim.x * blockDim.x) {
+        if (!acc[r]) continue;
+        const uint64_t j = pos[r];
+        if (j >= (uint64_t)N) continue;
+        const int64_t dst = rows ? rows[j / t] * t + (int64_t)(j % t) : (int64_t)j;
+        draws[dst] = (int64_t)val[r];
+        if (j == (uint64_t)N - 1) *last = (unsigned long long)r;
+    }
+}
+
 // Random-append candidate matrix (merge.py:146-163): flag rows of an
 // (nrows, t) int64 draw matrix that contain a repeated value.  Only rows in
 // `rows` (or all rows when rows == nullptr) are checked.
@@ -414,6 +507,52 @@ __global__ void k_rev_heavy(const int32_t *__restrict__ heavy, const unsigned lo
 }
 
 // ---------------------------------------------------------------------------
+// Locality order of hoods (performance only: results do not depend on the
+// order hoods are processed in, since updates land in reference-order slots).
+// Min-label propagation over the forward lists groups vertices by graph
+// region; a counting sort by label gives the assembly (and join) order, so
+// concurrently processed hoods share members and the gathers hit L2.
+// ---------------------------------------------------------------------------
+// Only "old" entries (the input subgraphs' lists) carry labels: the random
+// cross appends are new-flagged and would turn the graph into an expander.
+__global__ void k_label_prop(const int32_t *__restrict__ ids, const uint8_t *__restrict__ flags,
+                             const int32_t *__restrict__ sizes, int64_t n, int k,
+                             const int32_t *__restrict__ lin, int32_t *lout) {
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        int32_t m = lin[u];
+        const int sz = sizes[u];
+        for (int t = 0; t < sz; t++) {
+            if (flags[u * k + t]) continue;
+            const int32_t v = lin[ids[u * k + t]];
+            m = v < m ? v : m;
+        }
+        lout[u] = m;
+    }
+}
+
+__global__ void k_iota(int32_t *a, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        a[i] = (int32_t)i;
+}
+
+__global__ void k_label_hist(const int32_t *__restrict__ lab, int64_t n, uint32_t *hist) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&hist[lab[i]], 1u);
+}
+
+__global__ void k_label_scatter(const int32_t *__restrict__ lab, int64_t n,
+                                const uint32_t *__restrict__ off, uint32_t *cur, int32_t *order) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t l = lab[i];
+        order[off[l] + atomicAdd(&cur[l], 1u)] = (int32_t)i;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Neighbourhood assembly (_kernels.py:316-383) + flag clear
 // (construct.py:142) + pair counting (_kernels.py:402-417, closed form) +
 // round-start worst snapshot for the exact prefilter.  One warp per vertex.
@@ -443,7 +582,7 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
            const uint32_t *__restrict__ roff, const uint32_t *__restrict__ rev, uint64_t seed,
            const int8_t *__restrict__ labels, int mode, int W, uint32_t *nbh, int32_t *nlen,
            uint32_t *hpairs, double *worst0, int32_t *active, unsigned long long *counters,
-           int64_t lo) {
+           int64_t lo, uint32_t *bound, uint32_t *mcount, const int32_t *__restrict__ order) {
     __shared__ uint32_t s_seg[ASM_WARPS][WARP_REV_MAX];
     __shared__ uint32_t s_idx[ASM_WARPS][WARP_REV_MAX];
     __shared__ uint32_t s_R[ASM_WARPS][MAX_W];
@@ -452,7 +591,8 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
     uint32_t *seg = s_seg[wib], *idx = s_idx[wib], *R = s_R[wib], *buf = s_buf[wib];
     int64_t nw = (int64_t)gridDim.x * ASM_WARPS;
     unsigned long long members = 0;
-    for (int64_t u = lo + (int64_t)blockIdx.x * ASM_WARPS + wib; u < n; u += nw) {
+    for (int64_t uu = lo + (int64_t)blockIdx.x * ASM_WARPS + wib; uu < n; uu += nw) {
+        const int64_t u = order ? (int64_t)order[uu] : uu;
         int sz = sizes[u];
         for (int t = lane; t < sz; t += 32)
             buf[t] = ((uint32_t)ids[u * k + t] << 1) | (uint32_t)flags[u * k + t];
@@ -511,8 +651,10 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
             unsigned em = __ballot_sync(FULL_MASK, end);
             int lab = 0;
             if (end) {
-                nbh[u * W + w + __popc(em & lanemask_lt())] = v;
-                lab = labels[v >> 1];
+                lab = labels[v >> 1] != 0;
+                // hood entry: id << 2 | label << 1 | new (the label rides along
+                // so the join needs no dependent labels[] load)
+                nbh[u * W + w + __popc(em & lanemask_lt())] = ((v >> 1) << 2) | ((uint32_t)lab << 1) | (v & 1);
             }
             bool nw_ = end && (v & 1);
             an += __popc(__ballot_sync(FULL_MASK, end && lab == 0 && nw_));
@@ -521,9 +663,9 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
             bo += __popc(__ballot_sync(FULL_MASK, end && lab != 0 && !nw_));
             w += __popc(em);
         }
+        const uint64_t pc = pairs_closed_form(mode, an, ao, bn, bo);
         if (lane == 0) {
             nlen[u] = w;
-            uint64_t pc = pairs_closed_form(mode, an, ao, bn, bo);
             hpairs[u] = (uint32_t)pc;
             if (pc > 0) {
                 unsigned long long p = atomicAdd(&counters[C_ACTIVE], 1ull);
@@ -532,6 +674,24 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
             }
         }
         __syncwarp();
+        if (bound != nullptr && pc > 0) {
+            // membership counting for the reference-order slot layout (the
+            // first pass of k_hood_memb, fused): admissible partners per member
+            const int cnt4[4] = {an, ao, bn, bo};
+            for (int j = lane; j < w; j += 32) {
+                const uint32_t e = nbh[u * W + j];
+                const int cls = (mode == 0 ? 0 : (int)((e >> 1) & 1)) * 2 + ((e & 1) ? 0 : 1);
+                const int mk = partner_mask(mode, cls);
+                int part = -(int)partner_self(mode, cls);
+#pragma unroll
+                for (int c = 0; c < 4; c++)
+                    if (mk & (1 << c)) part += cnt4[c];
+                if (part > 0) {
+                    atomicAdd(&bound[e >> 2], (uint32_t)part);
+                    atomicAdd(&mcount[e >> 2], 1u);
+                }
+            }
+        }
     }
     if (lane == 0 && members) atomicAdd(&counters[C_MEMBERS], members);
 }
@@ -581,8 +741,8 @@ k_join_exact(const int32_t *__restrict__ active, const uint32_t *__restrict__ nb
             clsv[b] = 4;
             if (j < w) {
                 const uint32_t e = nbh[u * W + j];
-                const int id = (int)(e >> 1);
-                const int lab = mode == 0 ? 0 : (labels[id] != 0);
+                const int id = (int)(e >> 2);
+                const int lab = mode == 0 ? 0 : (int)((e >> 1) & 1);
                 clsv[b] = lab * 2 + ((e & 1) ? 0 : 1);
                 s_id[j] = id;
                 s_new[j] = e & 1;
@@ -719,7 +879,7 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                 const int j = b * 32 + (int)lane;
                 int cls = 4;
                 if (j < w) {
-                    const int lab = mode == 0 ? 0 : (labels[ev[b] >> 1] != 0);
+                    const int lab = mode == 0 ? 0 : (int)((ev[b] >> 1) & 1);
                     cls = lab * 2 + ((ev[b] & 1) ? 0 : 1);
                 }
                 clsv[b] = cls;
@@ -736,7 +896,7 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                     const unsigned m = __ballot_sync(FULL_MASK, clsv[b] == c);
                     if (clsv[b] == c) {
                         const int slot = base_cls[c] + fill[c] + __popc(m & lanemask_lt());
-                        const int id = (int)(ev[b] >> 1);
+                        const int id = (int)(ev[b] >> 2);
                         s_id[slot] = id;
                         s_pos[slot] = j;
                         s_new[slot] = (int)(ev[b] & 1);
@@ -1015,21 +1175,29 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
     uint32_t phase = 0;
     const uint32_t row_bytes = (uint32_t)dph * 2u;
     const uint32_t rbase = smem_u32(m.rows);
-    for (int hi = blockIdx.x * MJ_WARPS + warp; hi < nactive; hi += gridDim.x * MJ_WARPS) {
-        const int64_t u = active[hi];
-        const int w = nlen[u];
-        // ---- classify members into (label, new-first) slots ------------------
-        uint32_t ev[4];
-        int clsv[4], labv[4];
+    // software prefetch: the next hood's id/length/entries are loaded while
+    // the current hood's rows are in flight (TMA) and its Gram block computes
+    const int stride = gridDim.x * MJ_WARPS;
+    int hi = blockIdx.x * MJ_WARPS + warp;
+    int64_t u_cur = hi < nactive ? active[hi] : 0;
+    int w_cur = hi < nactive ? nlen[u_cur] : 0;
+    uint32_t ev[4];
 #pragma unroll
-        for (int b = 0; b < 4; b++) {  // W <= 128
-            const int j = b * 32 + (int)lane;
-            ev[b] = j < w ? nbh[u * W + j] : 0u;
-        }
+    for (int b = 0; b < 4; b++) {
+        const int j = b * 32 + (int)lane;
+        ev[b] = j < w_cur ? nbh[u_cur * W + j] : 0u;
+    }
+    int64_t u_nxt = hi + stride < nactive ? active[hi + stride] : 0;
+    for (; hi < nactive; hi += stride) {
+        const int64_t u = u_cur;
+        const int w = w_cur;
+        const int w_nxt = hi + stride < nactive ? nlen[u_nxt] : 0;
+        // ---- classify members into (label, new-first) slots ------------------
+        int clsv[4], labv[4];
 #pragma unroll
         for (int b = 0; b < 4; b++) {
             const int j = b * 32 + (int)lane;
-            labv[b] = (j < w && mode != 0) ? (int)labels[ev[b] >> 1] : 0;
+            labv[b] = (j < w && mode != 0) ? (int)((ev[b] >> 1) & 1) : 0;
         }
         int cnts[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -1061,7 +1229,7 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
         for (int b = 0; b < 4; b++) {
             const int sl = myslot[b];
             if (sl >= 0) {
-                const int id = (int)(ev[b] >> 1);
+                const int id = (int)(ev[b] >> 2);
                 const int j = b * 32 + (int)lane;
                 bulk_g2s(m.rows + (size_t)sl * rs, sub16 + (int64_t)id * dph, row_bytes, m.bar);
                 m.id[sl] = id;
@@ -1074,6 +1242,13 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
             }
         }
         build_pos_prefix(m.P, clsv, mode, lane);
+        uint32_t ev_nxt[4];
+#pragma unroll
+        for (int b = 0; b < 4; b++) {
+            const int j = b * 32 + (int)lane;
+            ev_nxt[b] = j < w_nxt ? nbh[u_nxt * W + j] : 0u;
+        }
+        const int64_t u_nn = hi + 2 * stride < nactive ? active[hi + 2 * stride] : 0;
         __syncwarp();
         mbar_wait(m.bar, phase);
         phase ^= 1u;
@@ -1125,6 +1300,11 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
             }
         }
         __syncwarp();
+        u_cur = u_nxt;
+        w_cur = w_nxt;
+#pragma unroll
+        for (int b = 0; b < 4; b++) ev[b] = ev_nxt[b];
+        u_nxt = u_nn;
     }
 }
 
@@ -1195,7 +1375,7 @@ __global__ void k_hood_memb(const int32_t *__restrict__ active, int nactive,
             const int j = b * 32 + (int)lane;
             int cls = 4;
             if (j < w) {
-                const int lab = mode == 0 ? 0 : (labels[ev[b] >> 1] != 0);
+                const int lab = mode == 0 ? 0 : (int)((ev[b] >> 1) & 1);
                 cls = lab * 2 + ((ev[b] & 1) ? 0 : 1);
             }
             clsv[b] = cls;
@@ -1213,7 +1393,7 @@ __global__ void k_hood_memb(const int32_t *__restrict__ active, int nactive,
                 for (int c = 0; c < 4; c++)
                     if (mk & (1 << c)) part += cnt[c];
                 if (part > 0) {
-                    const int32_t id = (int32_t)(ev[b] >> 1);
+                    const int32_t id = (int32_t)(ev[b] >> 2);
                     if (!FILL) {
                         atomicAdd(&bound[id], (uint32_t)part);
                         atomicAdd(&mcount[id], 1u);
@@ -1304,7 +1484,7 @@ __global__ void k_capture_pairs(const uint32_t *__restrict__ nbh, const int32_t 
         uint32_t ep = nbh[u * W + p];
         for (int q = p + 1; q < w; q++) {
             uint32_t eq = nbh[u * W + q];
-            int ip = ep >> 1, iq = eq >> 1;
+            int ip = ep >> 2, iq = eq >> 2;
             if (admissible(ep & 1, eq & 1, labels[ip], labels[iq], mode)) {
                 pa[pos] = ip;
                 pb[pos] = iq;

@@ -271,15 +271,14 @@ def _append_random_all(engines, rows, pool, count, rng, counter):
         for e in engines:
             e.insert_rows(rows.astype(np.int32), count, picks)
     else:
-        cand = rng.integers(0, m, size=(rows.size, t))
-        bad = engines[0].draws_load(cand)
-        while bad.size:
-            vals = rng.integers(0, m, size=(bad.size, t))
-            cand[bad] = vals
-            bad = engines[0].draws_replace(bad, vals)
-        engines[0].draws_insert(rows.astype(np.int32), pool.astype(np.int32))
-        for e in engines[1:]:
-            e.draws_load(cand)
+        # every local engine replays the same PCG64 stream on the device
+        st0 = rng.bit_generator.state
+        for i, e in enumerate(engines):
+            if i:
+                rng.bit_generator.state = st0
+            bad = e.draws_gen(rng, m, rows.size, t)
+            while bad.size:
+                bad = e.draws_regen(rng, m, bad)
             e.draws_insert(rows.astype(np.int32), pool.astype(np.int32))
     counter.add(rows.size * t)
 

@@ -123,6 +123,32 @@ class Engine:
                                            ctypes.byref(nb)), "knnm_draws_replace")
         return bad[: nb.value].copy()
 
+    def draws_gen(self, rng, m: int, nrows: int, t: int) -> np.ndarray:
+        """rng.integers(0, m, size=(nrows, t)) generated on the device (same
+        values, same resulting generator state); returns the bad rows."""
+        st, arr, has, uint = _pcg_split(rng)
+        bad = self._bad(nrows)
+        nb = ctypes.c_int64()
+        used = ctypes.c_int64()
+        check(self._lib.knnm_draws_gen(self._h, ptr(arr), int(has), ctypes.c_uint32(uint), int(m),
+                                       int(nrows), int(t), ctypes.byref(used), ptr(bad),
+                                       ctypes.byref(nb)), "knnm_draws_gen")
+        _pcg_consume(rng, st, int(used.value))
+        return bad[: nb.value].copy()
+
+    def draws_regen(self, rng, m: int, rows: np.ndarray) -> np.ndarray:
+        """cand[rows] = rng.integers(0, m, size=(len(rows), t)) on the device."""
+        rows = np.ascontiguousarray(rows, dtype=np.int64)
+        st, arr, has, uint = _pcg_split(rng)
+        bad = self._bad(rows.shape[0])
+        nb = ctypes.c_int64()
+        used = ctypes.c_int64()
+        check(self._lib.knnm_draws_regen(self._h, ptr(arr), int(has), ctypes.c_uint32(uint), int(m),
+                                         ptr(rows), rows.shape[0], ctypes.byref(used), ptr(bad),
+                                         ctypes.byref(nb)), "knnm_draws_regen")
+        _pcg_consume(rng, st, int(used.value))
+        return bad[: nb.value].copy()
+
     def draws_insert(self, rows: np.ndarray, pool: np.ndarray) -> int:
         rows = np.ascontiguousarray(rows, dtype=np.int32)
         pool = np.ascontiguousarray(pool, dtype=np.int32)
@@ -191,6 +217,10 @@ class Engine:
         """-1 auto, 0 exact fp64 route, 1 tiled fp32-screen route, 2 tensor-core route."""
         check(self._lib.knnm_set_join_variant(self._h, int(variant)), "knnm_set_join_variant")
 
+    def set_locality(self, iters: int) -> None:
+        """Label-propagation rounds for the hood locality order (0 = id order)."""
+        check(self._lib.knnm_set_locality(self._h, int(iters)), "knnm_set_locality")
+
     def info(self) -> dict:
         cert = ctypes.c_int32()
         dp = ctypes.c_int32()
@@ -220,6 +250,61 @@ class Engine:
 
     def sync(self) -> None:
         check(self._lib.knnm_sync(self._h), "knnm_sync")
+
+
+# --- numpy PCG64 state hand-off (numpy/random/src/pcg64/pcg64.h) ----------
+_M64 = (1 << 64) - 1
+_M128 = (1 << 128) - 1
+_PCG_MULT = 0x2360ED051FC65DA44385DF649FCCF645
+
+
+def _pcg_split(rng):
+    st = rng.bit_generator.state
+    if st.get("bit_generator") != "PCG64":
+        raise ValueError("device draws need a PCG64 generator (np.random.default_rng)")
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    arr = np.array([s >> 64, s & _M64, inc >> 64, inc & _M64], dtype=np.uint64)
+    return st, arr, st["has_uint32"], st["uinteger"]
+
+
+def _pcg_advance(s, inc, delta):
+    """pcg_advance_lcg_128: the LCG state after `delta` steps."""
+    acc_mult, acc_plus, cur_mult, cur_plus = 1, 0, _PCG_MULT, inc
+    while delta > 0:
+        if delta & 1:
+            acc_mult = (acc_mult * cur_mult) & _M128
+            acc_plus = (acc_plus * cur_mult + cur_plus) & _M128
+        cur_plus = ((cur_mult + 1) * cur_plus) & _M128
+        cur_mult = (cur_mult * cur_mult) & _M128
+        delta >>= 1
+    return (acc_mult * s + acc_plus) & _M128
+
+
+def _pcg_out(s):
+    x = ((s >> 64) ^ s) & _M64
+    r = s >> 122
+    return ((x >> r) | (x << ((64 - r) & 63))) & _M64
+
+
+def _pcg_consume(rng, st, used):
+    """Advance rng exactly as `used` next_uint32 calls would."""
+    s, inc = st["state"]["state"], st["state"]["inc"]
+    has, uint = st["has_uint32"], st["uinteger"]
+    if used <= 0:
+        return
+    if has:
+        used -= 1
+        has = 0
+    outs = (used + 1) // 2
+    if outs:
+        s = _pcg_advance(s, inc, outs)
+        uint = _pcg_out(s) >> 32
+        has = used % 2
+    new = dict(st)
+    new["state"] = {"state": s, "inc": inc}
+    new["has_uint32"] = has
+    new["uinteger"] = uint
+    rng.bit_generator.state = new
 
 
 def _is_cuda_tensor(x) -> bool:

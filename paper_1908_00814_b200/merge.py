@@ -141,10 +141,12 @@ def _append_random(engine, rows, pool, count, rng, counter, on_pair, gids) -> No
         _insert_rows(engine, rows.astype(np.int32), count, picks.ravel().astype(np.int32),
                      counter, on_pair, gids)
         return
-    cand = rng.integers(0, m, size=(rows.size, t))
-    bad = engine.draws_load(cand)
+    # rng.integers(0, m, size=(rows.size, t)) and the redraw loop, generated
+    # on the device with numpy's exact PCG64 stream (the host generator is
+    # advanced to the identical state)
+    bad = engine.draws_gen(rng, m, rows.size, t)
     while bad.size:
-        bad = engine.draws_replace(bad, rng.integers(0, m, size=(bad.size, t)))
+        bad = engine.draws_regen(rng, m, bad)
     engine.draws_insert(rows.astype(np.int32), pool.astype(np.int32))
     counter.add(rows.size * t)
     _emit_captured(engine, on_pair, gids)

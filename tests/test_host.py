@@ -96,3 +96,19 @@ def test_generators_shapes_and_certificates():
     assert np.allclose(np.linalg.norm(s.vectors, axis=1), 1.0, atol=1e-5)
     u = km.generate_unit_gmm(100, 960, n_centres=5, seed=1)
     assert u.vectors.min() >= 0 and u.vectors.max() <= 1
+
+
+def test_pcg_state_handoff_matches_numpy():
+    """_pcg_consume advances numpy's PCG64 exactly as next_uint32 calls do."""
+    from paper_1908_00814_b200.engine import _pcg_consume
+
+    for seed in range(6):
+        a = np.random.default_rng(seed)
+        a.integers(0, 5, size=seed)  # vary the half-buffer
+        b = np.random.default_rng(seed)
+        b.integers(0, 5, size=seed)
+        st = b.bit_generator.state
+        n = 17 + seed
+        a.integers(0, 2**32 - 1, size=n, dtype=np.uint64)  # one next_uint32 per draw (no rejection at 2^32-1)
+        _pcg_consume(b, st, n)
+        assert a.bit_generator.state == b.bit_generator.state
