@@ -143,8 +143,8 @@ __device__ __forceinline__ uint64_t bitonic_reg32(uint64_t v, unsigned lane) {
 // Register bitonic sort of NE keys per lane; element index i = e * 32 + lane,
 // ascending in i afterwards.  Cross-lane stages use shuffles, in-lane stages
 // plain register swaps (no shared memory, no barriers).
-template <int NE>
-__device__ __forceinline__ void warp_sort_reg(uint64_t (&v)[NE], unsigned lane) {
+template <int NE, typename T = uint64_t>
+__device__ __forceinline__ void warp_sort_reg(T (&v)[NE], unsigned lane) {
 #pragma unroll
     for (int k2 = 2; k2 <= 32 * NE; k2 <<= 1) {
 #pragma unroll
@@ -156,17 +156,17 @@ __device__ __forceinline__ void warp_sort_reg(uint64_t (&v)[NE], unsigned lane) 
                     if ((e & je) == 0) {
                         const int f = e | je;
                         const bool asc = (((e * 32 + (int)lane) & k2) == 0);
-                        uint64_t x = v[e], y = v[f];
+                        T x = v[e], y = v[f];
                         if ((x > y) == asc) { v[e] = y; v[f] = x; }
                     }
                 }
             } else {
 #pragma unroll
                 for (int e = 0; e < NE; e++) {
-                    uint64_t o = __shfl_xor_sync(FULL_MASK, v[e], j);
+                    T o = __shfl_xor_sync(FULL_MASK, v[e], j);
                     const bool asc = (((e * 32 + (int)lane) & k2) == 0);
                     const bool lower = (lane & j) == 0;
-                    uint64_t mn = v[e] < o ? v[e] : o, mx = v[e] < o ? o : v[e];
+                    T mn = v[e] < o ? v[e] : o, mx = v[e] < o ? o : v[e];
                     v[e] = (lower == asc) ? mn : mx;
                 }
             }

@@ -560,6 +560,30 @@ __global__ void k_label_scatter(const int32_t *__restrict__ lab, int64_t n,
 // ---------------------------------------------------------------------------
 constexpr int ASM_WARPS = 8;
 
+// Sort a[0..m) (u32, m <= 32 * NE) with a register bitonic sort and write it
+// back (padding slots become 0xffffffff).
+template <int NE>
+__device__ __forceinline__ void warp_sort_smem_u32(uint32_t *a, int m, unsigned lane) {
+    uint32_t v[NE];
+#pragma unroll
+    for (int e = 0; e < NE; e++) {
+        const int j = e * 32 + (int)lane;
+        v[e] = j < m ? a[j] : 0xffffffffu;
+    }
+    warp_sort_reg<NE, uint32_t>(v, lane);
+#pragma unroll
+    for (int e = 0; e < NE; e++) a[e * 32 + lane] = v[e];
+    __syncwarp();
+}
+
+__device__ __forceinline__ void warp_sort_any_u32(uint32_t *a, int m, unsigned lane) {
+    __syncwarp();
+    if (m <= 32) warp_sort_smem_u32<1>(a, m, lane);
+    else if (m <= 64) warp_sort_smem_u32<2>(a, m, lane);
+    else if (m <= 128) warp_sort_smem_u32<4>(a, m, lane);
+    else warp_sort_smem_u32<8>(a, m, lane);
+}
+
 __device__ __forceinline__ uint64_t pairs_closed_form(int mode, int an, int ao, int bn, int bo) {
     uint64_t a = an + ao, b = bn + bo, w = a + b, wo = ao + bo;
     if (mode == 0) return w * (w - 1) / 2 - wo * (wo - (wo ? 1 : 0)) / 2;
@@ -605,9 +629,8 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
             for (uint32_t j = lane; j < deg; j += 32) buf[m + j] = rev[lo + j];
             m += deg;
         } else if (deg <= (uint32_t)WARP_REV_MAX) {
-            uint32_t P2 = next_pow2(deg);
-            for (uint32_t j = lane; j < P2; j += 32) {
-                seg[j] = j < deg ? rev[lo + j] : 0xffffffffu;
+            for (uint32_t j = lane; j < deg; j += 32) {
+                seg[j] = rev[lo + j];
                 idx[j] = j;
             }
             uint64_t st0 = seed ^ ((uint64_t)(u + 1) * U64_GAMMA);
@@ -615,8 +638,7 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
                 uint64_t z = mix64(st0 + (uint64_t)(t + 2) * U64_GAMMA);
                 R[t] = (uint32_t)t + (uint32_t)(z % (uint64_t)(deg - (uint32_t)t));
             }
-            __syncwarp();
-            bitonic_warp<uint32_t>(seg, P2, lane);
+            warp_sort_any_u32(seg, (int)deg, lane);
             if (lane == 0) {
                 for (int t = 0; t < rev_cap; t++) {
                     uint32_t r = R[t];
@@ -632,11 +654,7 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
             for (int t = lane; t < rev_cap; t += 32) buf[m + t] = rev[lo + t];  // pre-selected
             m += rev_cap;
         }
-        __syncwarp();
-        uint32_t P2u = next_pow2((uint32_t)(m > 1 ? m : 1));
-        for (uint32_t j = m + lane; j < P2u; j += 32) buf[j] = 0xffffffffu;
-        __syncwarp();
-        bitonic_warp<uint32_t>(buf, P2u, lane);
+        warp_sort_any_u32(buf, m, lane);  // m <= k + rev_cap <= MAX_W
         // compact runs of equal ids; the last element of a run carries OR(flags)
         int w = 0;
         int an = 0, ao = 0, bn = 0, bo = 0;
@@ -1519,16 +1537,20 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
         const int64_t ns = (int64_t)(boff[r + 1] - lo);
         if (ns == 0) continue;
         slots += (unsigned long long)ns;
+        const double inf = __longlong_as_double(0x7ff0000000000000LL);
+        // the next 32 slot distances are loaded while this chunk is applied
+        double dnext = (int64_t)lane < ns ? Bd[lo + lane] : inf;
         WarpRow<E> s;
         row_load<E>(s, ids, dists, flags, sizes, r, k, lane);
         int a = 0;
         for (int64_t c0 = 0; c0 < ns; c0 += 32) {
             const int64_t j = c0 + lane;
-            double dl = j < ns ? Bd[lo + j] : __longlong_as_double(0x7ff0000000000000LL);
-            if (dl != dl) dl = __longlong_as_double(0x7ff0000000000000LL);  // unwritten slot
+            double dl = dnext;
+            dnext = j + 32 < ns ? Bd[lo + j + 32] : inf;
+            if (dl != dl) dl = inf;  // unwritten slot
             // an unwritten slot belongs to a row that was full at round start
             // and a distance >= its worst: it can never pass
-            const bool pre = j < ns && (dl < s.worst || (s.sz < k && dl < __longlong_as_double(0x7ff0000000000000LL)));
+            const bool pre = j < ns && (dl < s.worst || (s.sz < k && dl < inf));
             if (!__any_sync(FULL_MASK, pre)) continue;
             const int src = pre ? Bs[lo + j] : 0;
             const int cnt = ns - c0 < 32 ? (int)(ns - c0) : 32;

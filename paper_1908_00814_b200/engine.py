@@ -28,6 +28,7 @@ class Engine:
         self._lib = lib
         self._vectors = None  # host array currently resident on the device
         self._metric = None
+        self.pinned_outputs = False  # export into page-locked host buffers
         self.n = 0
         self.k = 0
 
@@ -182,9 +183,9 @@ class Engine:
                                             ctypes.c_void_p(dists.data_ptr()),
                                             ctypes.c_void_p(sizes.data_ptr())), "knnm_export_dev")
             return ids, dists, sizes
-        ids = np.empty((self.n, self.k), dtype=np.int32)
-        dists = np.empty((self.n, self.k), dtype=np.float64)
-        sizes = np.empty(self.n, dtype=np.int32)
+        ids = _host_empty((self.n, self.k), np.int32, self.pinned_outputs)
+        dists = _host_empty((self.n, self.k), np.float64, self.pinned_outputs)
+        sizes = _host_empty((self.n,), np.int32, self.pinned_outputs)
         check(self._lib.knnm_export(self._h, int(bool(merge_rear)), ptr(ids), ptr(dists),
                                     ptr(sizes)), "knnm_export")
         return ids, dists, sizes
@@ -305,6 +306,25 @@ def _pcg_consume(rng, st, used):
     new["has_uint32"] = has
     new["uinteger"] = uint
     rng.bit_generator.state = new
+
+
+def _host_empty(shape, dtype, pinned: bool) -> np.ndarray:
+    if not pinned:
+        return np.empty(shape, dtype=dtype)
+    import torch
+
+    tdt = {np.int32: torch.int32, np.float64: torch.float64}[dtype]
+    return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+
+
+def pinned_copy(a: np.ndarray) -> np.ndarray:
+    """A page-locked copy of a host array (DMA at full PCIe speed)."""
+    import torch
+
+    t = torch.empty(a.shape, dtype=torch.from_numpy(np.empty(0, dtype=a.dtype)).dtype, pin_memory=True)
+    out = t.numpy()
+    out[...] = a
+    return out
 
 
 def _is_cuda_tensor(x) -> bool:

@@ -87,17 +87,23 @@ def _union(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     return np.union1d(a, b)
 
 
-def _merge_members(a: np.ndarray, b: np.ndarray):
+def _merge_members(a: np.ndarray, b: np.ndarray, with_overlap: bool = False):
     """(union, rows of a, rows of b) for disjoint ascending id arrays in one
-    linear pass: np.union1d + np.searchsorted of merge.py:217-221."""
+    linear pass: np.union1d + np.searchsorted of merge.py:217-221.  With
+    with_overlap, also whether a and b share an id (merge.py:181)."""
     if not (_ascending(a) and _ascending(b)):
         u = np.union1d(a, b)
-        return u, _lookup_local(u, a), _lookup_local(u, b)
+        out = (u, _lookup_local(u, a), _lookup_local(u, b))
+        return out + (bool(np.intersect1d(a, b).size),) if with_overlap else out
     cat = np.concatenate((a, b))
     order = np.argsort(cat, kind="stable")
+    srt = cat[order]
     inv = np.empty(order.size, dtype=np.int32)
     inv[order] = np.arange(order.size, dtype=np.int32)
-    return cat[order], inv[: a.size], inv[a.size:]
+    out = (srt, inv[: a.size], inv[a.size:])
+    if with_overlap:
+        return out + (bool(srt.size > 1 and np.any(srt[1:] == srt[:-1])),)
+    return out
 
 
 def _sample_pool_rows(rng, nrows: int, t: int, pool: np.ndarray) -> np.ndarray:
@@ -153,9 +159,11 @@ def _append_random(engine, rows, pool, count, rng, counter, on_pair, gids) -> No
 
 
 def _check_merge_inputs(dataset, g: KnnGraph, other_ids: np.ndarray, params: MergeParams,
-                        other_graph: KnnGraph | None) -> None:
+                        other_graph: KnnGraph | None, overlap: bool | None = None) -> None:
     """merge.py:179-192, same checks and messages."""
-    if _overlaps(np.asarray(g.member_ids), np.asarray(other_ids)):
+    if overlap is None:
+        overlap = _overlaps(np.asarray(g.member_ids), np.asarray(other_ids))
+    if overlap:
         raise ValueError("subsets must be disjoint")
     if g.k != params.k:
         raise ValueError(f"graph capacity {g.k} does not match params.k={params.k}")
@@ -174,16 +182,15 @@ def s_merge(dataset, g: KnnGraph, h: KnnGraph, params: MergeParams,
             device: int | None = None, out_device: bool = False):
     """Symmetric merge of two built k-NN graphs over disjoint subsets
     (merge.py:195-260; Alg. 1 of the paper)."""
-    _check_merge_inputs(dataset, g, h.member_ids, params, h)
+    union_gids, rows_g, rows_h, overlap = _merge_members(
+        np.asarray(g.member_ids), np.asarray(h.member_ids), with_overlap=True)
+    _check_merge_inputs(dataset, g, h.member_ids, params, h, overlap=overlap)
     if counter is None:
         counter = DistanceCounter()
     rng = np.random.default_rng(params.seed)
     metric = Metric(g.metric)
     k = params.k
     k1 = params.k1
-
-    union_gids, rows_g, rows_h = _merge_members(np.asarray(g.member_ids),
-                                                np.asarray(h.member_ids))
     n = union_gids.shape[0]
     labels = np.zeros(n, dtype=np.int8)
     labels[rows_h] = 1
