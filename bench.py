@@ -323,11 +323,22 @@ def run_b200(args):
             torch.distributed.destroy_process_group()
         return
 
-    # roofline of the dominant kernel (local join): algorithmic bytes / time
+    # roofline of the dominant kernel (the local join, timed alone with CUDA
+    # events on the engine stream): algorithmic bytes per launch / time.
+    # bytes = gathered member rows (sum |M_u| x row bytes: fp16 rows on the
+    # tensor-core route) + hood entries (4 B x members) + written update
+    # slots (8 B dist + 4 B source per prefilter survivor)
     hbm_peak, peak_kind = peaks()
-    join_s = st["join_ms"] / 1e3
-    join_bytes = 4.0 * CFG["d"] * st["members"] + 24.0 * st["candidates"]
-    achieved = join_bytes / join_s / 1e9 if join_s > 0 else 0.0
+    jk_s = st["join_kernel_ms"] / 1e3
+    row_b = st["join_row_bytes"] or 4 * CFG["d"]
+    join_bytes = (row_b + 4.0) * st["members"] + 12.0 * st["written_slots"]
+    achieved = join_bytes / jk_s / 1e9 if jk_s > 0 else 0.0
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_join_traffic.json")) as f:
+            traffic = json.load(f)
+    except Exception:
+        pass
     u_host = None if args.no_recall else to_host(u_dev)
     rec = recall_sample(ds, u_host, local) if not args.no_recall else None
     eng.set_dataset(ds.vectors, 1)
@@ -345,14 +356,15 @@ def run_b200(args):
         "evals_per_step": evals // steps,
         "recall_at_10": rec,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None, "peak_kind": peak_kind,
-                     "kernel": "k_join_exact",
-                     "bytes_model": "4*d*sum|M_u| + 24*candidates",
-                     "join_ms_per_step": st["join_ms"] / steps,
-                     "join_share": st["join_ms"] / max(ms_max, 1e-9)},
-        "stats_per_step": {key: st[key] / steps for key in ("candidates", "exact_evals", "members", "accepted", "join_redos", "rounds")},
+                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
+                     "kernel": "k_join_mma" if st["join_row_bytes"] == 2 * 128 else "k_join_tiled",
+                     "bytes_model": "(row_bytes + 4) * sum|M_u| + 12 * written_slots",
+                     "bytes_per_step": join_bytes / steps,
+                     "kernel_ms_per_step": st["join_kernel_ms"] / steps,
+                     "kernel_share_of_step": st["join_kernel_ms"] / max(ms_max, 1e-9)},
+        "stats_per_step": {key: st[key] / steps for key in ("candidates", "written_slots", "exact_evals", "members", "accepted", "join_redos", "rounds")},
         "phases_ms_per_step": {key: st[key] / steps for key in
-                               ("join_ms", "reverse_ms", "assemble_ms", "update_ms", "other_ms")},
+                               ("join_ms", "join_kernel_ms", "reverse_ms", "assemble_ms", "update_ms", "other_ms")},
         "e2e": {"value": e2e, "unit": UNIT, "ms_per_step": e_ms / steps,
                 "h2d_bytes_per_step": est["h2d_bytes"] // steps,
                 "d2h_bytes_per_step": est["d2h_bytes"] // steps},

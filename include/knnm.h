@@ -76,6 +76,9 @@ typedef struct knnm_stats {
     int64_t h2d_bytes;     /* host -> device bytes copied                 */
     int64_t join_redos;    /* optimistic single-shot joins redone in chunks */
     int64_t d2h_bytes;     /* device -> host bytes copied                 */
+    double join_kernel_ms; /* local-join kernel alone (roofline denominator) */
+    int64_t written_slots; /* update slots the join wrote (prefilter survivors) */
+    int64_t join_row_bytes; /* bytes per gathered member row in the join   */
 } knnm_stats;
 
 const char *knnm_last_error(void);

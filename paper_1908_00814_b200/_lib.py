@@ -52,6 +52,9 @@ class KnnmStats(ctypes.Structure):
         ("h2d_bytes", I64),
         ("join_redos", I64),
         ("d2h_bytes", I64),
+        ("join_kernel_ms", ctypes.c_double),
+        ("written_slots", I64),
+        ("join_row_bytes", I64),
     ]
 
     def as_dict(self) -> dict:

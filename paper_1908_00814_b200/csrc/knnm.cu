@@ -79,7 +79,7 @@ int bits_for(uint64_t maxval) {  // bits to represent values in [0, maxval]
     return b;
 }
 
-enum Phase { PH_JOIN = 0, PH_REVERSE, PH_ASSEMBLE, PH_UPDATE, PH_OTHER, PH_NUM };
+enum Phase { PH_JOIN = 0, PH_REVERSE, PH_ASSEMBLE, PH_UPDATE, PH_OTHER, PH_JOINK, PH_NUM };
 
 struct PhiTree {
     int64_t N = -1;
@@ -147,7 +147,7 @@ struct knnm_ctx {
     bool profiling = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> ev_pool;
-    double phase_ms[PH_NUM] = {0, 0, 0, 0, 0};
+    double phase_ms[PH_NUM] = {0, 0, 0, 0, 0, 0};
     knnm_stats stats{};
     cudaEvent_t marks[8] = {};
 };
@@ -289,6 +289,7 @@ int run_updates(knnm_ctx *c) {
     int64_t n = c->n;
     unsigned long long *cnt = c->counters.as<unsigned long long>();
     CK(cudaMemsetAsync(cnt + C_CAND, 0, sizeof(unsigned long long) * 2, c->st));
+    CK(cudaMemsetAsync(cnt + C_WRITTEN, 0, sizeof(unsigned long long), c->st));
     const int E = (c->k + 31) / 32;
     const int blocks = grid_for(c, n * 32, APPLY_WARPS * 32, 16);
     if (E == 1)
@@ -304,6 +305,7 @@ int run_updates(knnm_ctx *c) {
     CKL();
     TRY(sync_counters(c));
     c->stats.candidates += (int64_t)c->hcnt[C_CAND];
+    c->stats.written_slots += (int64_t)c->hcnt[C_WRITTEN];
     return KNNM_OK;
 }
 
@@ -1015,6 +1017,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         const int Wp = W + 16;
         const size_t mj_per_warp = mj_meta_bytes(Wp) + (size_t)Wp * (c->dph * 2 + 16);
         const size_t smem_mma = MJ_WARPS * mj_per_warp;
+        c->stats.join_row_bytes = c->cert_dot ? 2 * c->dph : 4 * c->dp;
         const bool use_mma = c->cert_dot && smem_mma <= 200 * 1024 &&
                              (c->join_variant == 2 || c->join_variant < 0);
         const bool tiled = !use_mma && (c->join_variant == 1 || (c->join_variant < 0 && smem_tiled <= 96 * 1024));
@@ -1052,6 +1055,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                 const uint32_t *stt = c->start.as<uint32_t>();
                 double *Bd = c->Bd.as<double>();
                 int32_t *Bs = c->Bs.as<int32_t>();
+                PhaseTimer ptk(c, PH_JOINK);  // the local-join kernel alone (roofline)
                 if (use_mma) {
                     int per_sm = 1;
                     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_join_mma, MJ_WARPS * 32,
@@ -1418,6 +1422,7 @@ int knnm_get_stats(knnm_ctx *c, knnm_stats *out) {
     out->assemble_ms = c->phase_ms[PH_ASSEMBLE];
     out->update_ms = c->phase_ms[PH_UPDATE];
     out->other_ms = c->phase_ms[PH_OTHER];
+    out->join_kernel_ms = c->phase_ms[PH_JOINK];
     return KNNM_OK;
 }
 

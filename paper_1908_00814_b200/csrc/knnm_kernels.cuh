@@ -1531,7 +1531,7 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
                int32_t *sizes, unsigned long long *counters) {
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * APPLY_WARPS;
-    unsigned long long acc = 0, slots = 0;
+    unsigned long long acc = 0, slots = 0, written = 0;
     for (int64_t r = (int64_t)blockIdx.x * APPLY_WARPS + wib; r < n; r += nw) {
         const uint64_t lo = boff[r];
         const int64_t ns = (int64_t)(boff[r + 1] - lo);
@@ -1548,6 +1548,7 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
             double dl = dnext;
             dnext = j + 32 < ns ? Bd[lo + j + 32] : inf;
             if (dl != dl) dl = inf;  // unwritten slot
+            else if (j < ns) written++;
             // an unwritten slot belongs to a row that was full at round start
             // and a distance >= its worst: it can never pass
             const bool pre = j < ns && (dl < s.worst || (s.sz < k && dl < inf));
@@ -1561,6 +1562,9 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
     }
     if (lane == 0 && acc) atomicAdd(&counters[C_ACCEPTED], acc);
     if (lane == 0 && slots) atomicAdd(&counters[C_CAND], slots);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) written += __shfl_xor_sync(FULL_MASK, written, o);
+    if (lane == 0 && written) atomicAdd(&counters[C_WRITTEN], written);
 }
 
 // Round-start worst of every row (sharded rounds: the join needs the
