@@ -233,10 +233,15 @@ int knnm_set_join_variant(knnm_ctx *ctx, int32_t variant);
  * locality order once per merge; 0 processes hoods in id order. */
 int knnm_set_locality(knnm_ctx *ctx, int32_t iters);
 
+/* on = 0 disables the u8 tensor-core route (integer data in [0, 255]) so the
+ * fp16 route is used instead; takes effect at the next knnm_set_dataset. */
+int knnm_set_u8(knnm_ctx *ctx, int32_t on);
+
 /* Dataset facts: cert bit 0 = fp32 difference-form arithmetic is provably
  * exact (integer entries, d*range^2 < 2^24 for L2); bit 1 = fp16 rows with
  * fp32 dot products are exact (integer entries, |v| <= 2048,
- * 2*d*max|v|^2 < 2^24); dp = padded row length in floats. */
+ * 2*d*max|v|^2 < 2^24); bit 2 = entries are integers in [0, 255] (u8
+ * rows, s32 integer MMA); dp = padded row length in floats. */
 int knnm_get_info(knnm_ctx *ctx, int32_t *cert, int32_t *dp);
 
 /* Timing / counters. profiling=1 records CUDA events around every phase. */

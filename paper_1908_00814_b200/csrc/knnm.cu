@@ -101,11 +101,14 @@ struct knnm_ctx {
     bool have_data = false;
     bool cert = false;  // fp32 arithmetic is exact for this dataset + metric
     bool cert_dot = false;  // fp16 rows + fp32 dot products are exact (L2)
+    bool cert_u8 = false;   // entries are integers in [0, 255]: u8 rows, s32 MMA
     int dph = 0;            // fp16 row length (multiple of 16)
+    int rowb = 0;           // staged bytes per row for the tensor-core join
     DBuf vec16, norms, sub16, subnorms;
-    const __half *sub16p = nullptr;
+    const uint8_t *sub16p = nullptr;
     const float *subnormp = nullptr;
     int join_variant = -1;  // -1 auto, 0 exact (fp64 every pair), 1 tiled, 2 tensor core
+    bool u8_enabled = true;
     // current merge
     DBuf sub, ugid, labels;
     const float *subp = nullptr;
@@ -409,7 +412,8 @@ int knnm_create(int device, knnm_ctx **out) {
                             (int)(2 * sizeof(uint32_t) * BLOCK_SORT_MAX)));
     for (auto f : {k_join_exact<0>, k_join_exact<1>, k_join_exact<2>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(k_join_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_join_mma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_join_mma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (auto f : {k_join_tiled<0, false>, k_join_tiled<1, false>, k_join_tiled<2, false>,
                    k_join_tiled<0, true>, k_join_tiled<1, true>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -495,8 +499,18 @@ int knnm_set_dataset(knnm_ctx *c, const float *vectors, int64_t n_all, int32_t d
         c->cert_dot = ints && metric == KNNM_L2 && maxabs <= 2048.0 &&
                       2.0 * (double)d * maxabs * maxabs < 16777216.0;
         CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
-        if (c->cert_dot) {
+        c->cert_u8 = c->cert_dot && mn >= 0.0 && mx <= 255.0 && c->u8_enabled;
+        if (c->cert_u8) {
+            c->dph = (d + 31) & ~31;  // u8 elements per row
+            c->rowb = c->dph;
+            TRY(ensure(c->vec16, (size_t)n_all * c->rowb));
+            TRY(ensure(c->norms, sizeof(float) * (size_t)n_all));
+            k_to_u8<<<grid_for(c, n_all * 32, 256, 16), 256, 0, c->st>>>(
+                c->vec.as<float>(), dp, n_all, c->dph, c->vec16.as<uint8_t>(), c->norms.as<float>());
+            CKL();
+        } else if (c->cert_dot) {
             c->dph = (d + 15) & ~15;
+            c->rowb = 2 * c->dph;
             TRY(ensure(c->vec16, sizeof(__half) * (size_t)n_all * c->dph));
             TRY(ensure(c->norms, sizeof(float) * (size_t)n_all));
             k_to_half<<<grid_for(c, n_all * 32, 256, 16), 256, 0, c->st>>>(
@@ -523,20 +537,20 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     TRY(ensure(c->ugid, sizeof(int64_t) * n));
     TRY(h2d(c, c->ugid.p, union_gids, sizeof(int64_t) * n));
     bool identity = (n == c->n_all && union_gids[0] == 0 && union_gids[n - 1] == n - 1);
-    c->sub16p = c->vec16.as<__half>();
+    c->sub16p = c->vec16.as<uint8_t>();
     c->subnormp = c->norms.as<float>();
     if (c->cert_dot && !identity) {
-        TRY(ensure(c->sub16, sizeof(__half) * (size_t)n * c->dph));
+        TRY(ensure(c->sub16, (size_t)n * c->rowb));
         TRY(ensure(c->subnorms, sizeof(float) * (size_t)n));
-        k_gather_rows<<<grid_for(c, n * (c->dph / 8), 256), 256, 0, c->st>>>(
-            reinterpret_cast<const float *>(c->vec16.p), c->dph / 2, c->ugid.as<int64_t>(), n,
+        k_gather_rows<<<grid_for(c, n * (c->rowb / 16), 256), 256, 0, c->st>>>(
+            reinterpret_cast<const float *>(c->vec16.p), c->rowb / 4, c->ugid.as<int64_t>(), n,
             c->sub16.as<float>());
         CKL();
         k_gather_norms<<<grid_for(c, n, 256), 256, 0, c->st>>>(c->norms.as<float>(),
                                                                 c->ugid.as<int64_t>(), n,
                                                                 c->subnorms.as<float>());
         CKL();
-        c->sub16p = c->sub16.as<__half>();
+        c->sub16p = c->sub16.as<uint8_t>();
         c->subnormp = c->subnorms.as<float>();
     }
     if (identity) {
@@ -1015,9 +1029,9 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         size_t smem_tiled = sizeof(float) * (size_t)W * (c->dp + 4);
         if (smem > 200 * 1024) return fail(KNNM_ERR_LIMIT, "neighbourhood of %d x %d floats exceeds shared memory", W, c->dp);
         const int Wp = W + 16;
-        const size_t mj_per_warp = mj_meta_bytes(Wp) + (size_t)Wp * (c->dph * 2 + 16);
+        const size_t mj_per_warp = mj_meta_bytes(Wp) + (size_t)Wp * (c->rowb + 16);
         const size_t smem_mma = MJ_WARPS * mj_per_warp;
-        c->stats.join_row_bytes = c->cert_dot ? 2 * c->dph : 4 * c->dp;
+        c->stats.join_row_bytes = c->cert_dot ? c->rowb : 4 * c->dp;
         const bool use_mma = c->cert_dot && smem_mma <= 200 * 1024 &&
                              (c->join_variant == 2 || c->join_variant < 0);
         const bool tiled = !use_mma && (c->join_variant == 1 || (c->join_variant < 0 && smem_tiled <= 96 * 1024));
@@ -1058,15 +1072,21 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                 PhaseTimer ptk(c, PH_JOINK);  // the local-join kernel alone (roofline)
                 if (use_mma) {
                     int per_sm = 1;
-                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_join_mma, MJ_WARPS * 32,
-                                                                     smem_mma));
+                    const void *fn = c->cert_u8 ? (const void *)k_join_mma<true> : (const void *)k_join_mma<false>;
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, MJ_WARPS * 32, smem_mma));
                     unsigned grid = (unsigned)std::min<int64_t>((nact + MJ_WARPS - 1) / MJ_WARPS,
                                                                 (int64_t)c->sms * std::max(per_sm, 1));
                     if (grid == 0) grid = 1;
-                    k_join_mma<<<grid, MJ_WARPS * 32, smem_mma, c->st>>>(
-                        act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
-                        c->labels.as<int8_t>(), mode, c->sub16p, c->dph, c->subnormp,
-                        c->worst0.as<double>(), boff, stt, Bd, Bs);
+                    if (c->cert_u8)
+                        k_join_mma<true><<<grid, MJ_WARPS * 32, smem_mma, c->st>>>(
+                            act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
+                            c->labels.as<int8_t>(), mode, c->sub16p, c->rowb, c->subnormp,
+                            c->worst0.as<double>(), boff, stt, Bd, Bs);
+                    else
+                        k_join_mma<false><<<grid, MJ_WARPS * 32, smem_mma, c->st>>>(
+                            act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
+                            c->labels.as<int8_t>(), mode, c->sub16p, c->rowb, c->subnormp,
+                            c->worst0.as<double>(), boff, stt, Bd, Bs);
                 } else if (tiled) {
                     const void *fn;
                     if (c->metric == 1) fn = c->cert ? (const void *)k_join_tiled<1, true> : (const void *)k_join_tiled<1, false>;
@@ -1394,6 +1414,12 @@ int knnm_set_locality(knnm_ctx *c, int32_t iters) {
     return KNNM_OK;
 }
 
+int knnm_set_u8(knnm_ctx *c, int32_t on) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    c->u8_enabled = on != 0;
+    return KNNM_OK;
+}
+
 int knnm_set_join_variant(knnm_ctx *c, int32_t variant) {
     if (!c || variant < -1 || variant > 2) return fail(KNNM_ERR_ARG, "variant %d", variant);
     c->join_variant = variant;
@@ -1402,7 +1428,7 @@ int knnm_set_join_variant(knnm_ctx *c, int32_t variant) {
 
 int knnm_get_info(knnm_ctx *c, int32_t *cert, int32_t *dp) {
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
-    if (cert) *cert = (c->cert ? 1 : 0) | (c->cert_dot ? 2 : 0);
+    if (cert) *cert = (c->cert ? 1 : 0) | (c->cert_dot ? 2 : 0) | (c->cert_u8 ? 4 : 0);
     if (dp) *dp = c->dp;
     return KNNM_OK;
 }

@@ -1145,6 +1145,15 @@ __host__ __device__ constexpr size_t mj_meta_bytes(int Wp) {
     return (16 + (size_t)Wp * (8 + 8 + 4 * 5) + sizeof(PosPrefix) + 127) & ~(size_t)127;
 }
 
+__device__ __forceinline__ void mma16832_u8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                            uint32_t a3, uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.u8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(c[0]), "+r"(c[1]), "+r"(c[2]), "+r"(c[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
 // Per-warp shared-memory region of k_join_mma (W slots padded to Wp = W+16).
 struct MjSmem {
     uint64_t *bar;
@@ -1172,17 +1181,22 @@ __device__ __forceinline__ MjSmem mj_carve(char *base, int Wp) {
     return m;
 }
 
+// U8 = true: rows are u8 (integer data in [0, 255]); the Gram block uses
+// mma.m16n8k32 u8 x u8 -> s32, exact integer arithmetic; norms are integers.
+// U8 = false: fp16 rows, m16n8k16 fp16 -> fp32 (exact under the dot-form
+// certificate).  `rowb` = staged bytes per row (multiple of 32).
+template <bool U8>
 __global__ void __launch_bounds__(MJ_WARPS * 32)
 k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
            const int32_t *__restrict__ nlen, int W, const int8_t *__restrict__ labels, int mode,
-           const __half *__restrict__ sub16, int dph, const float *__restrict__ norms,
+           const uint8_t *__restrict__ sub16, int rowb, const float *__restrict__ norms,
            const double *__restrict__ worst0, const uint64_t *__restrict__ boff,
            const uint32_t *__restrict__ start, double *__restrict__ Bd, int32_t *__restrict__ Bs) {
     extern __shared__ __align__(128) char mj_smem[];
     const unsigned lane = lane_id();
     const int warp = threadIdx.x >> 5;
     const int Wp = W + 16;
-    const int rs = dph * 2 + 16;  // padded fp16 row stride: conflict-free ldmatrix
+    const int rs = rowb + 16;  // padded row stride: conflict-free ldmatrix
     const size_t per_warp = mj_meta_bytes(Wp) + (size_t)Wp * rs;
     const MjSmem m = mj_carve(mj_smem + (size_t)warp * per_warp, Wp);
     if (lane == 0) mbar_init(m.bar, 1);
@@ -1191,7 +1205,7 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
         *reinterpret_cast<float4 *>(m.rows + i) = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncwarp();
     uint32_t phase = 0;
-    const uint32_t row_bytes = (uint32_t)dph * 2u;
+    const uint32_t row_bytes = (uint32_t)rowb;
     const uint32_t rbase = smem_u32(m.rows);
     // software prefetch: the next hood's id/length/entries are loaded while
     // the current hood's rows are in flight (TMA) and its Gram block computes
@@ -1249,7 +1263,7 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
             if (sl >= 0) {
                 const int id = (int)(ev[b] >> 2);
                 const int j = b * 32 + (int)lane;
-                bulk_g2s(m.rows + (size_t)sl * rs, sub16 + (int64_t)id * dph, row_bytes, m.bar);
+                bulk_g2s(m.rows + (size_t)sl * rs, sub16 + (int64_t)id * rowb, row_bytes, m.bar);
                 m.id[sl] = id;
                 m.pos[sl] = j;
                 m.nw[sl] = (int)(ev[b] & 1);
@@ -1282,14 +1296,20 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                     if (m0 - r0 >= rn && n0 - c0 >= cn) continue;  // old x old
                     if (tri && n0 + 7 <= m0) continue;             // below diagonal
                     float acc[4] = {0.f, 0.f, 0.f, 0.f};
+                    int iacc[4] = {0, 0, 0, 0};
                     const uint32_t a_addr = rbase + (uint32_t)((m0 + (lane & 15)) * rs + (lane >> 4) * 16);
                     const uint32_t b_addr = rbase + (uint32_t)((n0 + (lane & 7)) * rs + ((lane >> 3) & 1) * 16);
+                    // 32 bytes of K per step: 16 fp16 or 32 u8 elements; the
+                    // ldmatrix byte layout is the same for both
 #pragma unroll 4
-                    for (int kk = 0; kk < dph; kk += 16) {
+                    for (int kb = 0; kb < rowb; kb += 32) {
                         uint32_t a0, a1, a2, a3, b0, b1;
-                        ldsm_x4(a_addr + kk * 2, a0, a1, a2, a3);
-                        ldsm_x2(b_addr + kk * 2, b0, b1);
-                        mma16816(acc, a0, a1, a2, a3, b0, b1);
+                        ldsm_x4(a_addr + kb, a0, a1, a2, a3);
+                        ldsm_x2(b_addr + kb, b0, b1);
+                        if (U8)
+                            mma16832_u8(iacc, a0, a1, a2, a3, b0, b1);
+                        else
+                            mma16816(acc, a0, a1, a2, a3, b0, b1);
                     }
                     const int g = lane >> 2, t4 = lane & 3;
 #pragma unroll
@@ -1299,7 +1319,9 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                         if (ok && tri) ok = ii < jj;
                         if (ok) ok = m.nw[ii] || m.nw[jj];
                         if (!ok) continue;
-                        const double dd = (double)((m.nrm[ii] + m.nrm[jj]) - 2.0f * acc[s]);
+                        const double dd =
+                            U8 ? (double)((__float_as_int(m.nrm[ii]) + __float_as_int(m.nrm[jj])) - 2 * iacc[s])
+                               : (double)((m.nrm[ii] + m.nrm[jj]) - 2.0f * acc[s]);
                         const bool e1 = dd < m.w[ii], e2 = dd < m.w[jj];
                         if (!(e1 || e2)) continue;
                         const int pi = m.pos[ii], pj = m.pos[jj];
@@ -1323,6 +1345,25 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
 #pragma unroll
         for (int b = 0; b < 4; b++) ev[b] = ev_nxt[b];
         u_nxt = u_nn;
+    }
+}
+
+// u8 copy of the dataset (integers in [0, 255], zero-padded to dpu) and exact
+// integer row norms (stored as int bit patterns in the float norms array).
+__global__ void k_to_u8(const float *__restrict__ v, int dp, int64_t n, int dpu,
+                        uint8_t *__restrict__ out, float *__restrict__ norms) {
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n;
+         r += (int64_t)gridDim.x * (blockDim.x >> 5)) {
+        const unsigned lane = lane_id();
+        int acc = 0;
+        for (int c = lane; c < dpu; c += 32) {
+            const int x = c < dp ? (int)v[r * dp + c] : 0;
+            out[r * dpu + c] = (uint8_t)x;
+            acc += x * x;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, o);
+        if (lane == 0) norms[r] = __int_as_float(acc);
     }
 }
 

@@ -227,7 +227,12 @@ class Engine:
         dp = ctypes.c_int32()
         check(self._lib.knnm_get_info(self._h, ctypes.byref(cert), ctypes.byref(dp)), "knnm_get_info")
         return {"cert": bool(cert.value & 1), "cert_dot": bool(cert.value & 2),
-                "dp": int(dp.value)}
+                "cert_u8": bool(cert.value & 4), "dp": int(dp.value)}
+
+    def set_u8(self, on: bool) -> None:
+        """Enable/disable the u8 integer tensor-core route (next set_dataset)."""
+        check(self._lib.knnm_set_u8(self._h, int(bool(on))), "knnm_set_u8")
+        self._vectors = None
 
     # -- instrumentation ---------------------------------------------------
     def set_profiling(self, on: bool) -> None:

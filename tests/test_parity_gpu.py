@@ -149,3 +149,28 @@ def test_certificate_detection():
     assert not eng.info()["cert"]
     eng.set_dataset(km.generate_int_gmm(1000, 128, n_centres=10, seed=1).vectors, 2)
     assert not eng.info()["cert"]  # cosine is never certified
+
+
+@pytest.mark.parametrize("u8", [True, False])
+def test_tensor_core_routes_u8_and_fp16(oracle, u8):
+    """Integer data in [0,255]: the u8 (s32 MMA) and fp16 (f32 MMA) tensor-core
+    routes are both bit-identical to the oracle."""
+    km = _km()
+    from paper_1908_00814_b200.engine import get_engine
+
+    eng = get_engine()
+    ds = km.generate_int_gmm(5000, 128, n_centres=40, seed=21)
+    s1, s2 = split_ids(5000, seed=3)
+    g, _, _ = oracle.nn_descent(ds.vectors, 1, 20, 1, member_ids=s1)
+    h, _, _ = oracle.nn_descent(ds.vectors, 1, 20, 2, member_ids=s2)
+    eng.set_u8(u8)
+    try:
+        u, rep = km.s_merge(ds, _to_graph(km, g), _to_graph(km, h), km.MergeParams(k=20, seed=4),
+                            return_report=True)
+        info = eng.info()
+    finally:
+        eng.set_u8(True)
+    assert info["cert_dot"] and info["cert_u8"] == u8
+    ou, orep, _ = oracle.s_merge(ds.vectors, g, h, 20, seed=4)
+    _same_graph(u, ou)
+    _same_report(rep, orep)
