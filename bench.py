@@ -124,20 +124,20 @@ def make_inputs(km, n):
 
 def recall_sample(ds, graph, device, nq=1000, seed=0):
     """recall@10 of `graph` on nq sampled nodes against exact brute force
-    (fp32 GEMM on the GPU is exact here: integer data, sums < 2^24)."""
-    import torch
+    (the package's GPU brute force: exact fp64 distances, (dist, id) order,
+    self excluded -- reference brute_force_queries semantics)."""
+    import paper_1908_00814_b200 as km
+    from paper_1908_00814_b200.engine import get_engine
 
     rng = np.random.default_rng(seed)
     q = np.sort(rng.choice(ds.n, size=min(nq, ds.n), replace=False))
-    X = torch.from_numpy(ds.vectors).to(f"cuda:{device}")
-    Q = X[torch.from_numpy(q).to(X.device)]
-    d = (Q * Q).sum(1, keepdim=True) + (X * X).sum(1)[None, :] - 2.0 * Q @ X.T
-    d[torch.arange(len(q)), torch.from_numpy(q).to(X.device)] = float("inf")
-    truth = torch.topk(d, 10, largest=False).indices.cpu().numpy()
+    eng = get_engine(device)
+    eng.set_dataset(ds.vectors, int(km.Metric.L2))
+    ids, _ = eng.bf_topk(11, queries=ds.vectors[q])
+    truth = [[int(v) for v in row if v != qq][:10] for row, qq in zip(ids, q)]
     rows = np.searchsorted(np.asarray(graph.member_ids), q)
     got = np.asarray(graph.ids)[rows, :10]
-    hits = sum(len(set(t.tolist()) & set(g.tolist())) for t, g in zip(truth, got))
-    del X, Q, d
+    hits = sum(len(set(t) & set(g.tolist())) for t, g in zip(truth, got))
     return hits / (len(q) * 10)
 
 

@@ -194,6 +194,16 @@ int knnm_round_apply(knnm_ctx *ctx, int32_t nsrc, const uint32_t *recv_cnt,
                      const int32_t *recv_Bs, int64_t *accepted);
 int knnm_state_views(knnm_ctx *ctx, void **ids, void **dists, void **flags, void **sizes);
 
+/* Exact brute-force top-k (construct.py:273-348; _kernels.py:445-506):
+ * for each query -- queries[nq, d] (host) or dataset rows rows[nq] -- the k
+ * nearest candidates by (exact fp64 distance, id).  Row queries search the
+ * rows of the current union (knnm_begin; ids are local rows); vector queries
+ * search the whole dataset.  exclude_self drops the query row itself
+ * (brute_force_graph).
+ * Missing entries are -1 / +inf.  k <= 64. */
+int knnm_bf_topk(knnm_ctx *ctx, const float *queries, const int64_t *rows, int64_t nq,
+                 int32_t k, int32_t exclude_self, int32_t *out_ids, double *out_dists);
+
 /* phi over the current lists (construct.py:79-83), with numpy's pairwise
  * summation order, so the value is bit-identical to the reference. */
 int knnm_phi(knnm_ctx *ctx, double *out);

@@ -6,7 +6,14 @@ same public names and signatures for ``s_merge``, ``j_merge``,
 sm_100a CUDA kernels in ``libknnm.so`` (see include/knnm.h).
 """
 
-from .construct import BuildReport, DescentParams, RoundStats, nn_descent
+from .construct import (
+    BuildReport,
+    DescentParams,
+    RoundStats,
+    brute_force_graph,
+    brute_force_queries,
+    nn_descent,
+)
 from .core import (
     Dataset,
     DistanceCounter,
@@ -20,6 +27,7 @@ from .core import (
 )
 from .evaluate import recall_at_k, recall_at_k_arrays, scanning_rate
 from .graph import KnnGraph, Neighbor, NeighborList, SplitGraph, phi, split, update_nn
+from .hierarchy import Hierarchy, HierarchyLayer, doubling_layer_sizes, h_merge
 from .merge import MergeParams, j_merge, merge_rear, s_merge
 
 __version__ = "0.1.0"
@@ -29,14 +37,20 @@ __all__ = [
     "Dataset",
     "DescentParams",
     "DistanceCounter",
+    "Hierarchy",
+    "HierarchyLayer",
     "KnnGraph",
     "MergeParams",
     "Metric",
     "Neighbor",
     "NeighborList",
     "RoundStats",
+    "brute_force_graph",
+    "brute_force_queries",
     "SplitGraph",
     "distance",
+    "doubling_layer_sizes",
+    "h_merge",
     "generate_int_gmm",
     "generate_sphere_gmm",
     "generate_uniform",

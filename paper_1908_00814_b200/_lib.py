@@ -83,6 +83,7 @@ SIGNATURES = {
     "knnm_local_views": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]),
     "knnm_round_apply": (ctypes.c_int, [P, I32, P, P, P, P, PI64]),
     "knnm_state_views": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]),
+    "knnm_bf_topk": (ctypes.c_int, [P, P, P, I64, I32, I32, P, P]),
     "knnm_phi": (ctypes.c_int, [P, PDBL]),
     "knnm_export": (ctypes.c_int, [P, I32, P, P, P]),
     "knnm_export_dev": (ctypes.c_int, [P, I32, P, P, P]),

@@ -207,3 +207,49 @@ def nn_descent(dataset: Dataset, metric: Metric, params: DescentParams, seed: in
     if return_report:
         return graph, report
     return graph
+
+
+def brute_force_graph(dataset: Dataset, metric: Metric, k: int, member_ids=None,
+                      counter: DistanceCounter | None = None, on_pair=None,
+                      device: int | None = None) -> KnnGraph:
+    """Exact k-NN graph (construct.py:273-320) on the GPU.
+
+    The reference inserts candidates in ascending id order, which makes its
+    lists exactly the top-k by (fp64 distance, id); the device computes the
+    same exact distances and selects by (distance, id)."""
+    if on_pair is not None:
+        raise NotImplementedError("the on_pair route of brute_force_graph is not supported on the GPU")
+    metric = Metric(metric)
+    metric.check_kind(dataset.kind)
+    gids = _resolve_members(dataset, member_ids)
+    n = gids.shape[0]
+    if k >= n:
+        raise ValueError(f"k={k} must be below the member count {n}")
+    if counter is None:
+        counter = DistanceCounter()
+    eng = get_engine(device)
+    eng.set_dataset(dataset.vectors, int(metric))
+    eng.begin(gids, np.zeros(n, dtype=np.int8), k)
+    loc, dists = eng.bf_topk(k, rows=np.arange(n, dtype=np.int64), exclude_self=True)
+    counter.add(n * (n - 1) // 2)
+    ids = np.where(loc >= 0, gids.astype(np.int32)[np.maximum(loc, 0)], -1).astype(np.int32)
+    sizes = np.full(n, min(k, n - 1), dtype=np.int32)
+    return _graph_from(gids, k, metric, ids, dists, sizes)
+
+
+def brute_force_queries(dataset: Dataset, metric: Metric, queries: Dataset, k: int,
+                        counter: DistanceCounter | None = None, device: int | None = None):
+    """Exact top-k (ids int64, dists) of every query against the dataset
+    (construct.py:323-348), on the GPU."""
+    metric = Metric(metric)
+    metric.check_kind(dataset.kind)
+    metric.check_kind(queries.kind)
+    if k > dataset.n:
+        raise ValueError("k exceeds dataset size")
+    if counter is None:
+        counter = DistanceCounter()
+    eng = get_engine(device)
+    eng.set_dataset(dataset.vectors, int(metric))
+    ids, dists = eng.bf_topk(k, queries=queries.vectors)
+    counter.add(queries.n * dataset.n)
+    return ids.astype(np.int64), dists

@@ -413,6 +413,9 @@ int knnm_create(int device, knnm_ctx **out) {
     for (auto f : {k_join_exact<0>, k_join_exact<1>, k_join_exact<2>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     CK(cudaFuncSetAttribute(k_join_mma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (auto f : {k_bf_topk<0>, k_bf_topk<1>, k_bf_topk<2>})
+        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)(BF_THREADS * BF_MAXK * (sizeof(double) + sizeof(int32_t)))));
     CK(cudaFuncSetAttribute(k_join_mma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (auto f : {k_join_tiled<0, false>, k_join_tiled<1, false>, k_join_tiled<2, false>,
                    k_join_tiled<0, true>, k_join_tiled<1, true>})
@@ -1265,6 +1268,55 @@ int knnm_state_views(knnm_ctx *c, void **ids, void **dists, void **flags, void *
     if (dists) *dists = c->dists.p;
     if (flags) *flags = c->flags.p;
     if (sizes) *sizes = c->sizes.p;
+    return KNNM_OK;
+}
+
+int knnm_bf_topk(knnm_ctx *c, const float *queries, const int64_t *rows, int64_t nq, int32_t k,
+                 int32_t exclude_self, int32_t *out_ids, double *out_dists) {
+    if (!c || (!queries && !rows) || !out_ids || !out_dists) return fail(KNNM_ERR_ARG, "null argument");
+    if (!c->have_data) return fail(KNNM_ERR_STATE, "knnm_set_dataset first");
+    if (k < 1 || k > BF_MAXK) return fail(KNNM_ERR_LIMIT, "brute-force k=%d outside [1, %d]", k, BF_MAXK);
+    if (nq == 0) return KNNM_OK;
+    CK(cudaSetDevice(c->device));
+    PhaseTimer pt(c, PH_OTHER);
+    // row queries: candidates are the rows of the current union (local ids);
+    // vector queries: candidates are the whole dataset
+    if (rows && !c->begun) return fail(KNNM_ERR_STATE, "row queries need knnm_begin");
+    const float *data = rows ? c->subp : c->vec.as<float>();
+    const int64_t n = rows ? c->n : c->n_all;
+    const float *qd = nullptr;
+    const int64_t *rd = nullptr;
+    if (rows) {
+        TRY(ensure(c->stage[0], sizeof(int64_t) * nq));
+        TRY(h2d(c, c->stage[0].p, rows, sizeof(int64_t) * nq));
+        rd = c->stage[0].as<int64_t>();
+    } else {
+        TRY(ensure(c->stage[0], sizeof(float) * (size_t)nq * c->dp));
+        if (c->dp == c->d) {
+            TRY(h2d(c, c->stage[0].p, queries, sizeof(float) * (size_t)nq * c->d));
+        } else {
+            TRY(ensure(c->stage[1], sizeof(float) * (size_t)nq * c->d));
+            TRY(h2d(c, c->stage[1].p, queries, sizeof(float) * (size_t)nq * c->d));
+            k_pad_rows<<<grid_for(c, nq * c->dp, 256), 256, 0, c->st>>>(c->stage[1].as<float>(), c->d, c->dp,
+                                                                    nq, c->stage[0].as<float>());
+            CKL();
+        }
+        qd = c->stage[0].as<float>();
+    }
+    TRY(ensure(c->stage[2], (sizeof(int32_t) + sizeof(double)) * (size_t)nq * k + 8));
+    int32_t *oi = c->stage[2].as<int32_t>();
+    double *od = reinterpret_cast<double *>(c->stage[2].as<char>() + ((sizeof(int32_t) * (size_t)nq * k + 7) & ~(size_t)7));
+    const size_t smem = (size_t)BF_THREADS * k * (sizeof(double) + sizeof(int32_t));
+    const unsigned grid = (unsigned)std::min<int64_t>(nq, (int64_t)c->sms * 8);
+#define KNNM_BF_ARGS data, n, c->dp, c->d, qd, c->dp, rd, nq, k, exclude_self, oi, od
+    if (c->metric == 1) k_bf_topk<1><<<grid, BF_THREADS, smem, c->st>>>(KNNM_BF_ARGS);
+    else if (c->metric == 2) k_bf_topk<2><<<grid, BF_THREADS, smem, c->st>>>(KNNM_BF_ARGS);
+    else k_bf_topk<0><<<grid, BF_THREADS, smem, c->st>>>(KNNM_BF_ARGS);
+#undef KNNM_BF_ARGS
+    CKL();
+    TRY(d2h(c, out_ids, oi, sizeof(int32_t) * (size_t)nq * k));
+    TRY(d2h(c, out_dists, od, sizeof(double) * (size_t)nq * k));
+    CK(cudaStreamSynchronize(c->st));
     return KNNM_OK;
 }
 

@@ -1666,6 +1666,93 @@ __global__ void k_add_base(uint64_t *off, int64_t m, uint64_t base) {
 }
 
 // ---------------------------------------------------------------------------
+// Exact brute force (construct.py:273-348, _kernels.py:445-506).  The
+// reference inserts candidates in ascending id order, so its lists are the
+// top-k by (dist, id) with exact fp64 distances -- any evaluation order that
+// keeps (dist, id) order gives the same lists.  One block per query; each
+// thread keeps a sorted top-k of its strided share, then the block merges
+// with k rounds of (dist, id) arg-min.
+// ---------------------------------------------------------------------------
+constexpr int BF_THREADS = 256;
+constexpr int BF_MAXK = 64;
+
+__device__ __forceinline__ bool dist_id_less(double d1, int32_t i1, double d2, int32_t i2) {
+    return d1 < d2 || (d1 == d2 && i1 < i2);
+}
+
+template <int TAG>
+__global__ void __launch_bounds__(BF_THREADS)
+k_bf_topk(const float *__restrict__ data, int64_t n, int dp, int d, const float *__restrict__ queries,
+          int qdp, const int64_t *__restrict__ qrows, int64_t nq, int k, int exclude_self,
+          int32_t *out_ids, double *out_dists) {
+    extern __shared__ double bf_sm[];  // q (dp doubles, unused) + BF_THREADS * k candidates
+    double *cd = bf_sm;
+    int32_t *ci = reinterpret_cast<int32_t *>(bf_sm + (size_t)BF_THREADS * k);
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    for (int64_t qi = blockIdx.x; qi < nq; qi += gridDim.x) {
+        const float *q = qrows ? data + qrows[qi] * dp : queries + qi * qdp;
+        const int64_t self = (qrows && exclude_self) ? qrows[qi] : -1;
+        double td[BF_MAXK];
+        int32_t ti[BF_MAXK];
+        for (int t = 0; t < k; t++) { td[t] = inf; ti[t] = 0x7fffffff; }
+        for (int64_t i = threadIdx.x; i < n; i += BF_THREADS) {
+            if (i == self) continue;
+            const double dd = exact_dist<TAG>(q, data + i * dp, d);
+            if (!dist_id_less(dd, (int32_t)i, td[k - 1], ti[k - 1])) continue;
+            int t = k - 1;
+            while (t > 0 && dist_id_less(dd, (int32_t)i, td[t - 1], ti[t - 1])) {
+                td[t] = td[t - 1];
+                ti[t] = ti[t - 1];
+                t--;
+            }
+            td[t] = dd;
+            ti[t] = (int32_t)i;
+        }
+        for (int t = 0; t < k; t++) {
+            cd[threadIdx.x * k + t] = td[t];
+            ci[threadIdx.x * k + t] = ti[t];
+        }
+        __syncthreads();
+        // k rounds of block arg-min over the per-thread heads
+        __shared__ double s_bd[BF_THREADS / 32];
+        __shared__ int32_t s_bi[BF_THREADS / 32];
+        __shared__ int s_bt[BF_THREADS / 32];
+        __shared__ int s_win;
+        int head = 0;  // next unused entry of this thread's list
+        for (int r = 0; r < k; r++) {
+            double bd = head < k ? cd[threadIdx.x * k + head] : inf;
+            int32_t bi = head < k ? ci[threadIdx.x * k + head] : 0x7fffffff;
+            int bt = threadIdx.x;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const double od = __shfl_xor_sync(FULL_MASK, bd, o);
+                const int32_t oi = __shfl_xor_sync(FULL_MASK, bi, o);
+                const int ot = __shfl_xor_sync(FULL_MASK, bt, o);
+                if (dist_id_less(od, oi, bd, bi)) { bd = od; bi = oi; bt = ot; }
+            }
+            if ((threadIdx.x & 31) == 0) {
+                s_bd[threadIdx.x >> 5] = bd;
+                s_bi[threadIdx.x >> 5] = bi;
+                s_bt[threadIdx.x >> 5] = bt;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int w = 0;
+                for (int x = 1; x < BF_THREADS / 32; x++)
+                    if (dist_id_less(s_bd[x], s_bi[x], s_bd[w], s_bi[w])) w = x;
+                s_win = s_bt[w];
+                const bool real = s_bd[w] < inf;
+                out_ids[qi * k + r] = real ? s_bi[w] : -1;
+                out_dists[qi * k + r] = s_bd[w];
+            }
+            __syncthreads();
+            if ((int)threadIdx.x == s_win) head++;
+            __syncthreads();
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // phi (construct.py:79-83) with numpy's pairwise summation tree.
 // ---------------------------------------------------------------------------
 __global__ void k_phi_leaves(const double *__restrict__ dists, const int32_t *__restrict__ sizes, int k,

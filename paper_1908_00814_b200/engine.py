@@ -165,6 +165,24 @@ class Engine:
                                    ctypes.byref(pairs), ctypes.byref(acc)), "knnm_round")
         return int(pairs.value), int(acc.value)
 
+    def bf_topk(self, k: int, queries: np.ndarray | None = None, rows: np.ndarray | None = None,
+                exclude_self: bool = False):
+        """Exact top-k by (fp64 distance, id) against the current union (or
+        the whole dataset when no merge is active)."""
+        if (queries is None) == (rows is None):
+            raise ValueError("pass exactly one of queries / rows")
+        if queries is not None:
+            q = np.ascontiguousarray(queries, dtype=np.float32)
+            nq, qp, rp = q.shape[0], ptr(q), None
+        else:
+            r = np.ascontiguousarray(rows, dtype=np.int64)
+            nq, qp, rp = r.shape[0], None, ptr(r)
+        ids = np.empty((nq, k), dtype=np.int32)
+        dists = np.empty((nq, k), dtype=np.float64)
+        check(self._lib.knnm_bf_topk(self._h, qp, rp, nq, int(k), int(bool(exclude_self)), ptr(ids),
+                                     ptr(dists)), "knnm_bf_topk")
+        return ids, dists
+
     def phi(self) -> float:
         out = ctypes.c_double()
         check(self._lib.knnm_phi(self._h, ctypes.byref(out)), "knnm_phi")

@@ -150,5 +150,38 @@ def main():
         json.dump(out, f, indent=1)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--extra" not in sys.argv:
     main()
+
+
+def extra():
+    """H-Merge and KNNG file golden vectors (tests/golden/golden_extra.json)."""
+    import knnmerge as km
+    import knnmerge.io as kio
+    import tempfile
+
+    out = {}
+    ds = km.Dataset.from_dense(C.make_data(dict(data="uniform", n=2000, d=4, data_seed=13)), validate=False)
+    c = km.DistanceCounter()
+    graph, hier, reps = km.h_merge(ds, km.Metric.L2, km.MergeParams(k=10, seed=4), counter=c,
+                                   return_report=True)
+    out["hmerge"] = dict(out=h_graph(graph.ids, graph.dists, graph.sizes), count=c.count,
+                         layer_sizes=hier.layer_sizes,
+                         layers=[h_graph(l.graph.ids, l.graph.dists, l.graph.sizes) for l in hier.layers],
+                         reports=[[name, report_dict(r)] for name, r in reps])
+    ds2 = km.Dataset.from_dense(C.make_data(dict(data="uniform", n=300, d=5, data_seed=2)), validate=False)
+    g = km.nn_descent(ds2, km.Metric.L2, km.DescentParams(k=6), 3, member_ids=np.arange(0, 300, 2))
+    with tempfile.TemporaryDirectory() as tmp:
+        kio.save_graph(tmp + "/g.knng", g)
+        kio.save_member_ids(tmp + "/g.ids", g.member_ids)
+        import hashlib
+        out["knng"] = dict(graph=h_graph(g.ids, g.dists, g.sizes),
+                           file_sha256=hashlib.sha256(open(tmp + "/g.knng", "rb").read()).hexdigest(),
+                           ids_sha256=hashlib.sha256(open(tmp + "/g.ids", "rb").read()).hexdigest())
+    with open(os.path.join(HERE, "golden_extra.json"), "w") as f:
+        json.dump(out, f, indent=1)
+    print("extra", out["hmerge"]["layer_sizes"], out["hmerge"]["count"])
+
+
+if __name__ == "__main__" and "--extra" in sys.argv:
+    extra()
