@@ -1037,7 +1037,9 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         c->stats.join_row_bytes = c->cert_dot ? c->rowb : 4 * c->dp;
         const bool use_mma = c->cert_dot && smem_mma <= 200 * 1024 &&
                              (c->join_variant == 2 || c->join_variant < 0);
-        const bool tiled = !use_mma && (c->join_variant == 1 || (c->join_variant < 0 && smem_tiled <= 96 * 1024));
+        const bool tiled = !use_mma && (c->join_variant == 1 || (c->join_variant < 0 && smem_tiled <= 200 * 1024));
+        // long rows (large d): more warps share one staged hood
+        const int tj_threads = smem_tiled > 48 * 1024 ? TJ_WARPS_BIG * 32 : TJ_THREADS;
         const double mrel = 1.0 + (double)(c->d + 8) * ldexp(1.0, -23);
         const double mabs = (double)(4 * c->d + 64) * ldexp(1.0, -24);
         // One pass per hood chunk: bounds -> bucket offsets -> join -> apply.
@@ -1096,7 +1098,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                     else if (c->metric == 2) fn = (const void *)k_join_tiled<2, false>;
                     else fn = c->cert ? (const void *)k_join_tiled<0, true> : (const void *)k_join_tiled<0, false>;
                     int per_sm = 1;
-                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, TJ_THREADS, smem_tiled));
+                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, tj_threads, smem_tiled));
                     unsigned grid = (unsigned)std::min<int64_t>(nact, (int64_t)c->sms * std::max(per_sm, 1));
                     if (grid == 0) grid = 1;
                     int na = (int)nact;
@@ -1104,15 +1106,15 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
     act, na, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,  \
         c->subp, c->dp, c->d, c->worst0.as<double>(), boff, stt, Bd, Bs, cnt, mrel, mabs
                     if (c->metric == 1 && c->cert)
-                        k_join_tiled<1, true><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+                        k_join_tiled<1, true><<<grid, tj_threads, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
                     else if (c->metric == 1)
-                        k_join_tiled<1, false><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+                        k_join_tiled<1, false><<<grid, tj_threads, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
                     else if (c->metric == 2)
-                        k_join_tiled<2, false><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+                        k_join_tiled<2, false><<<grid, tj_threads, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
                     else if (c->cert)
-                        k_join_tiled<0, true><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+                        k_join_tiled<0, true><<<grid, tj_threads, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
                     else
-                        k_join_tiled<0, false><<<grid, TJ_THREADS, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+                        k_join_tiled<0, false><<<grid, tj_threads, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
 #undef KNNM_TJ_ARGS
                 } else {
 #define KNNM_JE_ARGS                                                                          \

@@ -81,6 +81,29 @@ __device__ __forceinline__ double exact_dist(const float *__restrict__ a,
     }
 }
 
+// Cosine with the two fp64 norms precomputed: the reference accumulates
+// na = sum x*x and nb = sum y*y in the same sequential loop as the dot
+// (_kernels.py:65-70); each depends only on its own vector, so computing them
+// once per vector gives the same bits.  Post-processing as _kernels.py:71-80.
+__device__ __forceinline__ double exact_cos_norms(const float *__restrict__ a, const float *__restrict__ b,
+                                                  int d, double na, double nb) {
+    double dot = 0.0;
+    for (int t = 0; t < d; t++) dot = __dadd_rn(dot, __dmul_rn((double)a[t], (double)b[t]));
+    if (na == 0.0 || nb == 0.0) return (na == nb) ? 0.0 : 1.0;
+    if (dot > 0.0 && __dmul_rn(dot, dot) >= __dmul_rn(na, nb)) return 0.0;
+    double r = __dsub_rn(1.0, __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(na), __dsqrt_rn(nb))));
+    return r < 0.0 ? 0.0 : r;
+}
+
+__device__ __forceinline__ double exact_sqnorm(const float *__restrict__ a, int d) {
+    double acc = 0.0;
+    for (int t = 0; t < d; t++) {
+        const double x = (double)a[t];
+        acc = __dadd_rn(acc, __dmul_rn(x, x));
+    }
+    return acc;
+}
+
 __device__ __forceinline__ double exact_dist_tag(int tag, const float *a, const float *b, int d) {
     if (tag == 1) return exact_dist<1>(a, b, d);
     if (tag == 2) return exact_dist<2>(a, b, d);

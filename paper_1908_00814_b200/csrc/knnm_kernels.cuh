@@ -813,7 +813,8 @@ k_join_exact(const int32_t *__restrict__ active, const uint32_t *__restrict__ nb
 // Emission as in k_join_exact: reference-order key (u, p, q), exact-safe
 // prefilter against the round-start worst of each target.
 // ---------------------------------------------------------------------------
-constexpr int TJ_WARPS = 2;
+constexpr int TJ_WARPS = 2;       // warps per hood for small rows
+constexpr int TJ_WARPS_BIG = 8;   // warps per hood when rows are long (large d)
 constexpr int TJ_THREADS = TJ_WARPS * 32;
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -850,7 +851,7 @@ __device__ __forceinline__ void fence_proxy_async() {
 }
 
 template <int TAG, bool CERT>
-__global__ void __launch_bounds__(TJ_THREADS)
+__global__ void __launch_bounds__(TJ_WARPS_BIG * 32)
 k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
              const int32_t *__restrict__ nlen, int W, const int8_t *__restrict__ labels, int mode,
              const float *__restrict__ sub, int dp, int d, const double *__restrict__ worst0,
@@ -863,6 +864,7 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
     __shared__ int s_new[MAX_W];
     __shared__ double s_w[MAX_W];
     __shared__ float s_nrm[MAX_W];
+    __shared__ double s_nrm64[MAX_W];
     __shared__ uint64_t s_st[MAX_W];
     __shared__ int s_sc[MAX_W];
     __shared__ PosPrefix s_P;
@@ -872,6 +874,7 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
     const int tid = threadIdx.x;
     const unsigned lane = lane_id();
     const int warp = tid >> 5;
+    const int nwarps = blockDim.x >> 5;
     const int q4 = dp >> 2;
     const int qs = q4 + 1;  // padded row stride in float4
     if (tid == 0) mbar_init(&s_bar, 1);
@@ -948,7 +951,7 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
         phase ^= 1u;
         if (TAG == 2) {
             // fp32 norms for the cosine screen
-            for (int sl = warp; sl < w; sl += TJ_WARPS) {
+            for (int sl = warp; sl < w; sl += nwarps) {
                 float acc = 0.f;
                 for (int c = lane; c < q4; c += 32) {
                     float4 a = sv4[(size_t)((sl & 1) * H + (sl >> 1)) * qs + c];
@@ -961,6 +964,10 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                 for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, o);
                 if (lane == 0) s_nrm[sl] = acc;
             }
+            // exact fp64 norms (sequential, as the reference), one per member
+            if (!CERT)
+                for (int sl = tid; sl < w; sl += blockDim.x)
+                    s_nrm64[sl] = exact_sqnorm(sv + (size_t)((sl & 1) * H + (sl >> 1)) * qs * 4, d);
             __syncthreads();
         }
         // ---- blocks ----------------------------------------------------------
@@ -976,7 +983,7 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
         const int pc0 = (nct0 + 7) >> 3, np0 = ((nrt0 + 3) >> 2) * pc0;
         const int pc1 = (nct1 + 7) >> 3, np1 = nblk == 2 ? ((nrt1 + 3) >> 2) * pc1 : 0;
         // each warp takes 4 x 8 patches of 2 x 2 tiles (8 rows x 16 cols)
-        for (int pid = warp; pid < np0 + np1; pid += TJ_WARPS) {
+        for (int pid = warp; pid < np0 + np1; pid += nwarps) {
             const bool second = pid >= np0;
             const int lp = second ? pid - np0 : pid;
             const int pcs = second ? pc1 : pc0;
@@ -1071,8 +1078,10 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                             maybe = (double)f <= wmax * mrel;
                         }
                         if (maybe) {
-                            dd = exact_dist<TAG>(sv + (size_t)((ii & 1) * H + (ii >> 1)) * qs * 4,
-                                                 sv + (size_t)((jj & 1) * H + (jj >> 1)) * qs * 4, d);
+                            const float *ra = sv + (size_t)((ii & 1) * H + (ii >> 1)) * qs * 4;
+                            const float *rb = sv + (size_t)((jj & 1) * H + (jj >> 1)) * qs * 4;
+                            dd = TAG == 2 ? exact_cos_norms(ra, rb, d, s_nrm64[ii], s_nrm64[jj])
+                                          : exact_dist<TAG>(ra, rb, d);
                             n_exact++;
                         } else {
                             dd = __longlong_as_double(0x7ff0000000000000LL);
