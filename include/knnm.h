@@ -163,6 +163,15 @@ int knnm_draws_regen(knnm_ctx *ctx, const uint64_t *pcg, int32_t has_uint32,
                      uint32_t uinteger, uint64_t m, const int64_t *rows,
                      int64_t nrows, int64_t *consumed, int64_t *bad, int64_t *nbad);
 
+/* Host-side (no context, no GPU): nrows successive
+ * sample_distinct(rng, n, k, exclude=exclude[r]) draws (core.py:222-230,
+ * numpy Generator.choice(pool, k, replace=False)) from the PCG64 state
+ * {state_hi, state_lo, inc_hi, inc_lo} + half-buffer, which are updated in
+ * place to numpy's state after the draws.  out: int64 (nrows, k). */
+int knnm_sample_distinct_rows(uint64_t *pcg, int32_t *has_uint32, uint32_t *uinteger,
+                              int64_t n, int32_t k, const int32_t *exclude,
+                              int64_t nrows, int64_t *out);
+
 /* One local-join round.  Replaces one iteration of _descent_rounds
  * (construct.py:136-164): reverse_csr, assemble_neighborhoods (rev_cap),
  * flag clear, count_pairs/fill_pairs, pair_dists_dense and

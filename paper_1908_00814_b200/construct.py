@@ -146,10 +146,9 @@ def _random_lists(rng, n: int, k: int) -> np.ndarray:
     """n rows of k distinct local ids, self excluded (construct.py:192-209;
     the same PCG64 calls, so the same draws as the reference)."""
     if 4 * k * k >= n:
-        out = np.empty((n, k), dtype=np.int64)
-        for u in range(n):
-            out[u] = sample_distinct(rng, n, k, exclude=u)
-        return out
+        from .core import sample_distinct_rows
+
+        return sample_distinct_rows(rng, n, k, np.arange(n, dtype=np.int32))
     cand = rng.integers(0, n - 1, size=(n, k))
     cand += cand >= np.arange(n)[:, None]
     while True:

@@ -173,6 +173,32 @@ def sample_distinct(rng, n: int, k: int, exclude: int = -1) -> np.ndarray:
     return out
 
 
+def sample_distinct_rows(rng, n: int, k: int, exclude: np.ndarray) -> np.ndarray:
+    """[sample_distinct(rng, n, k, exclude=e) for e in exclude] as an
+    (len(exclude), k) int64 array, computed natively (libknnm.so) with the
+    same PCG64 stream; rng ends in the identical state."""
+    import ctypes
+
+    from . import _lib
+    from .engine import _pcg_split
+
+    exclude = np.ascontiguousarray(exclude, dtype=np.int32)
+    out = np.empty((exclude.shape[0], k), dtype=np.int64)
+    st, arr, has, uint = _pcg_split(rng)
+    h = ctypes.c_int32(int(has))
+    u = ctypes.c_uint32(int(uint))
+    _lib.check(_lib.load().knnm_sample_distinct_rows(_lib.ptr(arr), ctypes.byref(h), ctypes.byref(u),
+                                                     int(n), int(k), _lib.ptr(exclude),
+                                                     exclude.shape[0], _lib.ptr(out)),
+               "knnm_sample_distinct_rows")
+    new = dict(st)
+    new["state"] = {"state": (int(arr[0]) << 64) | int(arr[1]), "inc": st["state"]["inc"]}
+    new["has_uint32"] = int(h.value)
+    new["uinteger"] = int(u.value)
+    rng.bit_generator.state = new
+    return out
+
+
 # ---------------------------------------------------------------------------
 # Synthetic stand-ins for the BASELINE.json configs (SURVEY.md §8d).  The
 # reference ships only generate_uniform; these restate the configs'

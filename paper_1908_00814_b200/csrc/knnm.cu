@@ -388,6 +388,88 @@ void build_phi_tree(PhiTree &t, int64_t N) {
 
 }  // namespace
 
+// ---------------------------------------------------------------------------
+// Host-side numpy PCG64 (pcg64.h) and Generator.choice(pop, size,
+// replace=False) (Floyd's algorithm with a linear-probing hash set, or the
+// tail shuffle for large samples, then an in-place Fisher-Yates shuffle; all
+// bounded draws via Lemire's method).  Restated natively so the per-row
+// sample_distinct loop of merge.py:318-325 runs in C++ instead of 500k Python
+// calls; tests/test_host.py pins it against numpy.
+// ---------------------------------------------------------------------------
+namespace {
+struct HostPcg {
+    unsigned __int128 s, inc;
+    int has;
+    uint32_t u;
+    static unsigned __int128 mult() {
+        return ((unsigned __int128)0x2360ED051FC65DA4ULL << 64) | 0x4385DF649FCCF645ULL;
+    }
+    uint32_t next32() {
+        if (has) {
+            has = 0;
+            return u;
+        }
+        s = s * mult() + inc;
+        const uint64_t x = (uint64_t)(s >> 64) ^ (uint64_t)s;
+        const unsigned r = (unsigned)(s >> 122);
+        const uint64_t v = (x >> r) | (x << ((64u - r) & 63u));
+        has = 1;
+        u = (uint32_t)(v >> 32);
+        return (uint32_t)v;
+    }
+    uint64_t bounded(uint64_t rng) {  // random_bounded_uint64(0, rng), rng < 2^32
+        if (rng == 0) return 0;
+        if (rng == 0xFFFFFFFFull) return next32();
+        const uint64_t excl = rng + 1;
+        uint64_t m = (uint64_t)next32() * excl;
+        uint32_t left = (uint32_t)m;
+        if (left < excl) {
+            const uint32_t thr = (uint32_t)((0xFFFFFFFFull - rng) % excl);
+            while (left < thr) {
+                m = (uint64_t)next32() * excl;
+                left = (uint32_t)m;
+            }
+        }
+        return m >> 32;
+    }
+};
+
+void host_choice(HostPcg &p, int64_t pop, int64_t size, int64_t *out, std::vector<uint64_t> &hs,
+                 std::vector<int64_t> &tmp) {
+    if (pop > 10000 && size > pop / 50) {  // tail shuffle
+        tmp.resize(pop);
+        for (int64_t i = 0; i < pop; i++) tmp[i] = i;
+        for (int64_t i = pop - 1; i >= std::max<int64_t>(pop - size, 1); i--) {
+            const int64_t j = (int64_t)p.bounded((uint64_t)i);
+            std::swap(tmp[i], tmp[j]);
+        }
+        for (int64_t t = 0; t < size; t++) out[t] = tmp[pop - size + t];
+        return;
+    }
+    uint64_t mask = (uint64_t)(1.2 * (double)size);
+    for (int sh = 1; sh < 64; sh <<= 1) mask |= mask >> sh;
+    hs.assign(mask + 1, ~0ull);
+    for (int64_t j = pop - size; j < pop; j++) {
+        const uint64_t val = p.bounded((uint64_t)j);
+        uint64_t loc = val & mask;
+        while (hs[loc] != ~0ull && hs[loc] != val) loc = (loc + 1) & mask;
+        if (hs[loc] == ~0ull) {
+            hs[loc] = val;
+            out[j - pop + size] = (int64_t)val;
+        } else {
+            loc = (uint64_t)j & mask;
+            while (hs[loc] != ~0ull) loc = (loc + 1) & mask;
+            hs[loc] = (uint64_t)j;
+            out[j - pop + size] = j;
+        }
+    }
+    for (int64_t i = size - 1; i >= 1; i--) {
+        const int64_t j = (int64_t)p.bounded((uint64_t)i);
+        std::swap(out[i], out[j]);
+    }
+}
+}  // namespace
+
 extern "C" {
 
 const char *knnm_last_error(void) { return g_err.c_str(); }
@@ -1322,6 +1404,34 @@ int knnm_bf_topk(knnm_ctx *c, const float *queries, const int64_t *rows, int64_t
     return KNNM_OK;
 }
 
+int knnm_sample_distinct_rows(uint64_t *pcg, int32_t *has_uint32, uint32_t *uinteger, int64_t n,
+                              int32_t k, const int32_t *exclude, int64_t nrows, int64_t *out) {
+    if (!pcg || !has_uint32 || !uinteger || !out || (nrows > 0 && !exclude) || k < 0)
+        return fail(KNNM_ERR_ARG, "bad argument");
+    HostPcg p;
+    p.s = ((unsigned __int128)pcg[0] << 64) | pcg[1];
+    p.inc = ((unsigned __int128)pcg[2] << 64) | pcg[3];
+    p.has = *has_uint32;
+    p.u = *uinteger;
+    std::vector<uint64_t> hs;
+    std::vector<int64_t> tmp;
+    for (int64_t r = 0; r < nrows; r++) {
+        const int64_t ex = exclude[r];
+        const int64_t pool = (ex >= 0 && ex < n) ? n - 1 : n;  // core.py:222-230
+        if (k > pool) return fail(KNNM_ERR_ARG, "not enough values to sample from");
+        if (pool > 0xFFFFFFFFll) return fail(KNNM_ERR_LIMIT, "population too large");
+        int64_t *o = out + r * k;
+        host_choice(p, pool, k, o, hs, tmp);
+        if (ex >= 0 && ex < n)
+            for (int t = 0; t < k; t++) o[t] += o[t] >= ex ? 1 : 0;
+    }
+    pcg[0] = (uint64_t)(p.s >> 64);
+    pcg[1] = (uint64_t)p.s;
+    *has_uint32 = p.has;
+    *uinteger = p.u;
+    return KNNM_OK;
+}
+
 int knnm_phi(knnm_ctx *c, double *out) {
     if (!c || !out) return fail(KNNM_ERR_ARG, "null argument");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
@@ -1358,11 +1468,23 @@ int knnm_phi(knnm_ctx *c, double *out) {
         c->phi_leaf_len.as<int32_t>(), nl, c->phi_leaves.as<double>());
     CKL();
     if (ni > 0) {
-        k_phi_tree<<<1, 1024, 0, c->st>>>(c->phi_left.as<int32_t>(), c->phi_right.as<int32_t>(),
-                                          c->phi_level.as<int32_t>(),
-                                          (int)c->phi.level_start.size() - 1,
-                                          c->phi_leaves.as<double>(), c->phi_inner.as<double>());
-        CKL();
+        // wide levels: one grid each; the narrow top of the tree in one block
+        const int nlev = (int)c->phi.level_start.size() - 1;
+        int h = 0;
+        for (; h < nlev; h++) {
+            const int lo = c->phi.level_start[h], hi = c->phi.level_start[h + 1];
+            if (hi - lo < 4096) break;
+            k_phi_level<<<(unsigned)((hi - lo + 255) / 256), 256, 0, c->st>>>(
+                c->phi_left.as<int32_t>(), c->phi_right.as<int32_t>(), lo, hi,
+                c->phi_leaves.as<double>(), c->phi_inner.as<double>());
+            CKL();
+        }
+        if (h < nlev) {
+            k_phi_tree<<<1, 1024, 0, c->st>>>(c->phi_left.as<int32_t>(), c->phi_right.as<int32_t>(),
+                                              c->phi_level.as<int32_t>() + h, nlev - h,
+                                              c->phi_leaves.as<double>(), c->phi_inner.as<double>());
+            CKL();
+        }
         TRY(d2h(c, out, c->phi_inner.as<double>() + (ni - 1), sizeof(double)));
     } else {
         TRY(d2h(c, out, c->phi_leaves.p, sizeof(double)));

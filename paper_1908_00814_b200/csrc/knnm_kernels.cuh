@@ -870,6 +870,11 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
     __shared__ PosPrefix s_P;
     __shared__ int s_cls[4];
     __shared__ __align__(8) uint64_t s_bar;
+    // screened-pair queue of the !CERT route: < nthreads left over + one wave
+    // of nwarps patches x 128 pairs
+    __shared__ uint32_t s_q[CERT ? 1 : TJ_WARPS_BIG * 32 + TJ_WARPS_BIG * 128];
+    __shared__ int s_qlen;
+    __shared__ unsigned long long s_nexact;
     const float *sv = reinterpret_cast<const float *>(sv4);
     const int tid = threadIdx.x;
     const unsigned lane = lane_id();
@@ -877,10 +882,13 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
     const int nwarps = blockDim.x >> 5;
     const int q4 = dp >> 2;
     const int qs = q4 + 1;  // padded row stride in float4
-    if (tid == 0) mbar_init(&s_bar, 1);
+    if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        s_qlen = 0;
+        s_nexact = 0;
+    }
     __syncthreads();
     uint32_t phase = 0;
-    unsigned long long n_exact = 0;
 
     for (int hi = blockIdx.x; hi < nactive; hi += gridDim.x) {
         const int64_t u = active[hi];
@@ -983,24 +991,28 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
         const int pc0 = (nct0 + 7) >> 3, np0 = ((nrt0 + 3) >> 2) * pc0;
         const int pc1 = (nct1 + 7) >> 3, np1 = nblk == 2 ? ((nrt1 + 3) >> 2) * pc1 : 0;
         // each warp takes 4 x 8 patches of 2 x 2 tiles (8 rows x 16 cols)
-        for (int pid = warp; pid < np0 + np1; pid += nwarps) {
+        auto rowp = [&](int sl) { return sv4 + (size_t)((sl & 1) * H + (sl >> 1)) * qs; };
+        // fp32 2x2 tile of patch pid; returns whether the lane's tile is live
+        auto patch = [&](int pid, int &i0, int &j0, int &r1, int &c1, bool &tri, float (&acc)[2][2]) {
             const bool second = pid >= np0;
             const int lp = second ? pid - np0 : pid;
             const int pcs = second ? pc1 : pc0;
             const int pr = lp / pcs, pcc = lp - pr * pcs;
             const int rt = pr * 4 + (int)(lane >> 3), ct = pcc * 8 + (int)(lane & 7);
-            const int r0 = second ? b1r0 : b0r0, r1 = second ? b1r1 : b0r1;
-            const int c0 = second ? b1c0 : b0c0, c1 = second ? b1c1 : b0c1;
+            const int r0 = second ? b1r0 : b0r0;
+            const int c0 = second ? b1c0 : b0c0;
+            r1 = second ? b1r1 : b0r1;
+            c1 = second ? b1c1 : b0c1;
             const int rn = second ? b1rn : b0rn, cn = second ? b1cn : b0cn;
-            const bool tri = second ? true : (bool)b0tri;
-            const int i0 = r0 + 2 * rt, j0 = c0 + 2 * ct;
+            tri = second ? true : (bool)b0tri;
+            i0 = r0 + 2 * rt;
+            j0 = c0 + 2 * ct;
             bool live = i0 < r1 && j0 < c1;
             if (live && tri && rt > ct) live = false;             // below diagonal
             if (live && 2 * rt >= rn && 2 * ct >= cn) live = false;  // old x old
             const bool vi1 = i0 + 1 < r1, vj1 = j0 + 1 < c1;
-            float acc[2][2] = {{0.f, 0.f}, {0.f, 0.f}};
+            acc[0][0] = acc[0][1] = acc[1][0] = acc[1][1] = 0.f;
             if (live) {
-                auto rowp = [&](int sl) { return sv4 + (size_t)((sl & 1) * H + (sl >> 1)) * qs; };
                 const float4 *a0p = rowp(i0);
                 const float4 *a1p = rowp(vi1 ? i0 + 1 : i0);
                 const float4 *b0p = rowp(j0);
@@ -1047,75 +1059,112 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                     }
                 }
             }
-            // ---- finalize the 4 pairs of the tile --------------------------
-            double dv[4];
-            bool e1v[4], e2v[4];
-#pragma unroll
-            for (int s = 0; s < 4; s++) {
-                const int ii = i0 + (s >> 1), jj = j0 + (s & 1);
-                bool ok = live && ii < r1 && jj < c1;
-                if (ok && tri) ok = ii < jj;
-                if (ok) ok = s_new[ii] || s_new[jj];
-                double dd = 0.0;
-                bool e1 = false, e2 = false;
-                if (ok) {
-                    const double wi = s_w[ii], wj = s_w[jj];
-                    const double wmax = wi > wj ? wi : wj;
-                    float f = acc[s >> 1][s & 1];
-                    if (CERT) {
-                        dd = (double)f;
-                    } else {
-                        bool maybe;
-                        if (TAG == 2) {
-                            float na = s_nrm[ii], nb = s_nrm[jj];
-                            if (na == 0.f || nb == 0.f) {
-                                maybe = true;
-                            } else {
-                                float cs = 1.0f - f / (sqrtf(na) * sqrtf(nb));
-                                maybe = (double)cs <= wmax + mabs;
-                            }
-                        } else {
-                            maybe = (double)f <= wmax * mrel;
-                        }
-                        if (maybe) {
-                            const float *ra = sv + (size_t)((ii & 1) * H + (ii >> 1)) * qs * 4;
-                            const float *rb = sv + (size_t)((jj & 1) * H + (jj >> 1)) * qs * 4;
-                            dd = TAG == 2 ? exact_cos_norms(ra, rb, d, s_nrm64[ii], s_nrm64[jj])
-                                          : exact_dist<TAG>(ra, rb, d);
-                            n_exact++;
-                        } else {
-                            dd = __longlong_as_double(0x7ff0000000000000LL);
-                        }
-                    }
-                    e1 = dd < wi;  // id[ii] <- id[jj]
-                    e2 = dd < wj;  // id[jj] <- id[ii]
-                }
-                dv[s] = dd;
-                e1v[s] = e1;
-                e2v[s] = e2;
-            }
-            // write both directions to their reference-order slots
-#pragma unroll
-            for (int s = 0; s < 4; s++) {
-                const int ii = i0 + (s >> 1), jj = j0 + (s & 1);
-                bool ok = live && ii < r1 && jj < c1;
-                if (ok && tri) ok = ii < jj;
-                if (ok) ok = s_new[ii] || s_new[jj];
-                if (!ok) continue;
-                const int pi = s_pos[ii], pj = s_pos[jj];
+            return live;
+        };
+        // admissible pair (ii, jj) of a tile
+        auto pair_ok = [&](bool live, int ii, int jj, int r1, int c1, bool tri) {
+            bool ok = live && ii < r1 && jj < c1;
+            if (ok && tri) ok = ii < jj;
+            if (ok) ok = s_new[ii] || s_new[jj];
+            return ok;
+        };
+        // write both directions of an evaluated pair to their reference-order slots
+        auto emit = [&](int ii, int jj, double dd) {
+            const bool e1 = dd < s_w[ii];  // id[ii] <- id[jj]
+            const bool e2 = dd < s_w[jj];  // id[jj] <- id[ii]
+            const int pi = s_pos[ii], pj = s_pos[jj];
+            if (e1) {
                 const uint64_t sij = s_st[ii] + pair_rank(s_P, mode, s_sc[ii], pi, pj);
+                Bd[sij] = dd;
+                Bs[sij] = s_id[jj];
+            }
+            if (e2) {
                 const uint64_t sji = s_st[jj] + pair_rank(s_P, mode, s_sc[jj], pj, pi);
-                if (e1v[s]) { Bd[sij] = dv[s]; Bs[sij] = s_id[jj]; }
-                if (e2v[s]) { Bd[sji] = dv[s]; Bs[sji] = s_id[ii]; }
+                Bd[sji] = dd;
+                Bs[sji] = s_id[ii];
+            }
+        };
+        const int npatch = np0 + np1;
+        if (CERT) {
+            // every fp32 value is exact: finalize in place
+            for (int pid = warp; pid < npatch; pid += nwarps) {
+                int i0, j0, r1, c1;
+                bool tri;
+                float acc[2][2];
+                const bool live = patch(pid, i0, j0, r1, c1, tri, acc);
+#pragma unroll
+                for (int s = 0; s < 4; s++) {
+                    const int ii = i0 + (s >> 1), jj = j0 + (s & 1);
+                    if (!pair_ok(live, ii, jj, r1, c1, tri)) continue;
+                    const double dd = (double)acc[s >> 1][s & 1];
+                    if (dd < s_w[ii] || dd < s_w[jj]) emit(ii, jj, dd);
+                }
+            }
+        } else {
+            // fp32 screen in synchronized waves (one patch per warp per wave);
+            // pairs that may pass go to a shared queue, drained in whole
+            // multiples of the block (one exact fp64 evaluation per thread,
+            // no divergence, no straggler warp at the hood barrier)
+            const int nthreads = blockDim.x;
+            const int nwaves = (npatch + nwarps - 1) / nwarps;
+            for (int wave = 0; wave < nwaves; wave++) {
+                const int pid = wave * nwarps + warp;
+                if (pid < npatch) {
+                    int i0, j0, r1, c1;
+                    bool tri;
+                    float acc[2][2];
+                    const bool live = patch(pid, i0, j0, r1, c1, tri, acc);
+#pragma unroll
+                    for (int s = 0; s < 4; s++) {
+                        const int ii = i0 + (s >> 1), jj = j0 + (s & 1);
+                        bool maybe = pair_ok(live, ii, jj, r1, c1, tri);
+                        if (maybe) {
+                            const double wi = s_w[ii], wj = s_w[jj];
+                            const double wmax = wi > wj ? wi : wj;
+                            const float f = acc[s >> 1][s & 1];
+                            if (TAG == 2) {
+                                const float na = s_nrm[ii], nb = s_nrm[jj];
+                                if (na != 0.f && nb != 0.f) {
+                                    const float cs = 1.0f - f / (sqrtf(na) * sqrtf(nb));
+                                    maybe = (double)cs <= wmax + mabs;
+                                }
+                            } else {
+                                maybe = (double)f <= wmax * mrel;
+                            }
+                        }
+                        const unsigned m = __ballot_sync(FULL_MASK, maybe);
+                        int base = 0;
+                        if (lane == 0 && m) base = atomicAdd(&s_qlen, __popc(m));
+                        base = __shfl_sync(FULL_MASK, base, 0);
+                        if (maybe) s_q[base + __popc(m & lanemask_lt())] = (uint32_t)(ii | (jj << 8));
+                    }
+                }
+                __syncthreads();
+                const int qlen = s_qlen;
+                const bool last = wave == nwaves - 1;
+                if (qlen >= nthreads || (last && qlen > 0)) {
+                    const int take = last ? qlen : (qlen / nthreads) * nthreads;
+                    for (int e = qlen - take + tid; e < qlen; e += nthreads) {
+                        const uint32_t code = s_q[e];
+                        const int ii = (int)(code & 0xFF), jj = (int)(code >> 8);
+                        const float *ra = reinterpret_cast<const float *>(rowp(ii));
+                        const float *rb = reinterpret_cast<const float *>(rowp(jj));
+                        const double dd = TAG == 2 ? exact_cos_norms(ra, rb, d, s_nrm64[ii], s_nrm64[jj])
+                                                   : exact_dist<TAG>(ra, rb, d);
+                        emit(ii, jj, dd);
+                    }
+                    __syncthreads();
+                    if (tid == 0) {
+                        s_qlen = qlen - take;
+                        s_nexact += (unsigned long long)take;
+                    }
+                    __syncthreads();
+                }
             }
         }
         __syncthreads();  // smem reused by the next hood
     }
-    if (!CERT) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) n_exact += __shfl_xor_sync(FULL_MASK, n_exact, o);
-        if (lane == 0 && n_exact) atomicAdd(&counters[C_EXACT], n_exact);
-    }
+    if (!CERT && tid == 0 && s_nexact) atomicAdd(&counters[C_EXACT], s_nexact);
 }
 
 // ---------------------------------------------------------------------------
@@ -1794,6 +1843,17 @@ __global__ void k_phi_leaves(const double *__restrict__ dists, const int32_t *__
         for (; i < n; i++) res = __dadd_rn(res, val(lo + i));
     }
     out[li] = res;
+}
+
+// One tree level (nodes [lo, hi) of the height-sorted node array).
+__global__ void k_phi_level(const int32_t *__restrict__ left, const int32_t *__restrict__ right,
+                            int lo, int hi, const double *__restrict__ leaves, double *inner) {
+    const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hi) return;
+    const int l = left[i], r = right[i];
+    const double a = l >= 0 ? inner[l] : leaves[-l - 1];
+    const double b = r >= 0 ? inner[r] : leaves[-r - 1];
+    inner[i] = __dadd_rn(a, b);
 }
 
 // Internal nodes sorted by height; ref >= 0 -> internal node, ref < 0 -> leaf (-ref-1).

@@ -337,9 +337,9 @@ def j_merge_sharded(dataset, g, raw_ids, params: MergeParams, comm, engines, cou
         e.load_graph(rows_g, g, k1)
     _append_random_all(local, rows_g, rows_raw.astype(np.int64), min(k - k1, rows_raw.size), rng,
                        counter)
-    init = np.empty((rows_raw.size, k), dtype=np.int64)
-    for t, row in enumerate(rows_raw):
-        init[t] = sample_distinct(rng, n, k, exclude=int(row))
+    from .core import sample_distinct_rows
+
+    init = sample_distinct_rows(rng, n, k, rows_raw)
     for e in local:
         e.insert_rows(rows_raw.astype(np.int32), k, init.ravel().astype(np.int32))
     counter.add(rows_raw.size * k)

@@ -27,7 +27,7 @@ from .construct import (
     _insert_directed,
     _insert_rows,
 )
-from .core import DistanceCounter, Metric, sample_distinct
+from .core import DistanceCounter, Metric, sample_distinct, sample_distinct_rows
 from .engine import get_engine
 from .graph import KnnGraph, phi as graph_phi
 
@@ -258,9 +258,7 @@ def j_merge(dataset, g: KnnGraph, raw_ids, params: MergeParams,
         _append_random(eng, rows_g, rows_raw.astype(np.int64), min(k - k1, rows_raw.size), rng,
                        counter, on_pair, union_gids)
         # raw lists start from k random draws over the whole union (merge.py:318-325)
-        init = np.empty((rows_raw.size, k), dtype=np.int64)
-        for t, row in enumerate(rows_raw):
-            init[t] = sample_distinct(rng, n, k, exclude=int(row))
+        init = sample_distinct_rows(rng, n, k, rows_raw)  # natively, same stream
         _insert_rows(eng, rows_raw.astype(np.int32), k, init.ravel().astype(np.int32), counter,
                      on_pair, union_gids)
         report = BuildReport(phi_initial=eng.phi())

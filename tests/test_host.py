@@ -112,3 +112,20 @@ def test_pcg_state_handoff_matches_numpy():
         a.integers(0, 2**32 - 1, size=n, dtype=np.uint64)  # one next_uint32 per draw (no rejection at 2^32-1)
         _pcg_consume(b, st, n)
         assert a.bit_generator.state == b.bit_generator.state
+
+
+@pytest.mark.parametrize("n,k", [(1_000_000, 20), (500, 10), (12000, 300), (60, 40), (20001, 800)])
+def test_native_sample_distinct_rows_matches_numpy(n, k):
+    """Native Generator.choice restatement == the reference's per-row
+    sample_distinct loop (core.py:222-230), values and final rng state."""
+    from paper_1908_00814_b200.core import sample_distinct, sample_distinct_rows
+
+    rows = np.random.default_rng(9).choice(n, size=min(n, 300), replace=False).astype(np.int32)
+    a = np.random.default_rng(n + k)
+    a.integers(0, 3, size=1)
+    b = np.random.default_rng(n + k)
+    b.integers(0, 3, size=1)
+    want = np.stack([sample_distinct(a, n, k, exclude=int(r)) for r in rows])
+    got = sample_distinct_rows(b, n, k, rows)
+    assert np.array_equal(got, want)
+    assert a.bit_generator.state == b.bit_generator.state

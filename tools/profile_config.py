@@ -1,0 +1,53 @@
+"""One warm merge of a BASELINE config (c2 / c3 / c4 stand-in) at a given
+scale, with the CUDA profiler range around a second merge only (for
+`ncu --profile-from-start off`).  Usage:
+    python tools/profile_config.py c3 [--scale 0.1]"""
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+
+
+def main():
+    import torch
+    import paper_1908_00814_b200 as km
+    from configs_bench import split
+
+    name = sys.argv[1]
+    scale = float(sys.argv[sys.argv.index("--scale") + 1]) if "--scale" in sys.argv else 0.1
+    if name == "c2":
+        n = int(1_000_000 * scale)
+        ds, metric, k, op = km.generate_int_gmm(n, 128, 1000, 20.0, seed=7), km.Metric.L2, 20, "s"
+    elif name == "c3":
+        n = int(1_000_000 * scale)
+        ds, metric, k, op = km.generate_unit_gmm(n, 960, 500, 0.05, seed=7), km.Metric.L2, 20, "j"
+    else:
+        n = int(1_200_000 * scale)
+        ds, metric, k, op = km.generate_sphere_gmm(n, 100, 2000, 0.3, seed=7), km.Metric.COSINE, 40, "s"
+    s1, s2 = split(n)
+    g = km.nn_descent(ds, metric, km.DescentParams(k=k), 1, member_ids=s1)
+    h = km.nn_descent(ds, metric, km.DescentParams(k=k), 2, member_ids=s2) if op == "s" else None
+    params = km.MergeParams(k=k, seed=3)
+
+    def once():
+        c = km.DistanceCounter()
+        t = time.perf_counter()
+        u = km.s_merge(ds, g, h, params, counter=c) if op == "s" else km.j_merge(ds, g, s2, params, counter=c)
+        return time.perf_counter() - t, c.count, u
+
+    once()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
+    dt, cnt, _ = once()
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    print(f"{name} scale {scale}: merge {dt:.3f} s evals {cnt}")
+
+
+if __name__ == "__main__":
+    main()
