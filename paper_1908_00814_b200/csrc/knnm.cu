@@ -101,6 +101,8 @@ struct knnm_ctx {
     bool have_data = false;
     bool cert = false;  // fp32 arithmetic is exact for this dataset + metric
     bool cert_dot = false;  // fp16 rows + fp32 dot products are exact (L2)
+    DBuf nrm64;             // exact fp64 squared norm of every subset row (cosine)
+    bool slots_lazy = false;  // this round's slots may hold approximations (LazyExact)
     bool cert_u8 = false;   // entries are integers in [0, 255]: u8 rows, s32 MMA
     int dph = 0;            // fp16 row length (multiple of 16)
     int rowb = 0;           // staged bytes per row for the tensor-core join
@@ -288,6 +290,26 @@ int rank_memberships(knnm_ctx *c) {
 
 // Sequential per-row application of the slot buckets (row r: slots
 // [boff[r], boff[r+1]), already in the reference's order).
+// Exact-evaluation context of the apply kernels.  Approximate slots (sign
+// bit set) are written only by the non-certified tiled join.
+bool metric_is_cos(const knnm_ctx *c) { return c->metric == KNNM_COSINE; }
+
+// Row length above which non-certified joins defer exact evaluation to the
+// apply (measured crossover: d = 100 favours the join, d = 960 the apply).
+constexpr int LAZY_MIN_D = 384;
+
+LazyExact lazy_of(knnm_ctx *c) {
+    LazyExact z;
+    z.sub = c->subp;
+    z.nrm64 = c->metric == KNNM_COSINE ? c->nrm64.as<double>() : nullptr;
+    z.dp = c->dp;
+    z.d = c->d;
+    z.tag = c->metric;
+    z.lo_rel = 1.0 - (double)(c->d + 8) * ldexp(1.0, -23);
+    z.lo_abs = (double)(4 * c->d + 64) * ldexp(1.0, -24);
+    return z;
+}
+
 int run_updates(knnm_ctx *c) {
     int64_t n = c->n;
     unsigned long long *cnt = c->counters.as<unsigned long long>();
@@ -295,16 +317,19 @@ int run_updates(knnm_ctx *c) {
     CK(cudaMemsetAsync(cnt + C_WRITTEN, 0, sizeof(unsigned long long), c->st));
     const int E = (c->k + 31) / 32;
     const int blocks = grid_for(c, n * 32, APPLY_WARPS * 32, 16);
-    if (E == 1)
-        k_apply_stream<1><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
-            n, c->k, c->boff.as<uint64_t>(), c->Bd.as<double>(), c->Bs.as<int32_t>(),
-            c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
-            c->sizes.as<int32_t>(), cnt);
-    else
-        k_apply_stream<2><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
-            n, c->k, c->boff.as<uint64_t>(), c->Bd.as<double>(), c->Bs.as<int32_t>(),
-            c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(),
-            c->sizes.as<int32_t>(), cnt);
+#define KNNM_AP_LAUNCH(EE, LZ)                                                                   \
+    k_apply_stream<EE, LZ><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(                             \
+        n, c->k, c->boff.as<uint64_t>(), c->Bd.as<double>(), c->Bs.as<int32_t>(),               \
+        c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), \
+        cnt, lazy_of(c))
+    if (E == 1) {
+        if (c->slots_lazy) KNNM_AP_LAUNCH(1, true);
+        else KNNM_AP_LAUNCH(1, false);
+    } else {
+        if (c->slots_lazy) KNNM_AP_LAUNCH(2, true);
+        else KNNM_AP_LAUNCH(2, false);
+    }
+#undef KNNM_AP_LAUNCH
     CKL();
     TRY(sync_counters(c));
     c->stats.candidates += (int64_t)c->hcnt[C_CAND];
@@ -499,8 +524,10 @@ int knnm_create(int device, knnm_ctx **out) {
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(BF_THREADS * BF_MAXK * (sizeof(double) + sizeof(int32_t)))));
     CK(cudaFuncSetAttribute(k_join_mma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    for (auto f : {k_join_tiled<0, false>, k_join_tiled<1, false>, k_join_tiled<2, false>,
-                   k_join_tiled<0, true>, k_join_tiled<1, true>})
+    for (auto f : {k_join_tiled<0, false, false>, k_join_tiled<1, false, false>,
+                   k_join_tiled<2, false, false>, k_join_tiled<0, false, true>,
+                   k_join_tiled<1, false, true>, k_join_tiled<2, false, true>,
+                   k_join_tiled<0, true, false>, k_join_tiled<1, true, false>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     *out = c;
     return KNNM_OK;
@@ -619,6 +646,7 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     PhaseTimer pt(c, PH_OTHER);
     c->n = n;
     c->k = k;
+    c->slots_lazy = false;
     TRY(ensure(c->ugid, sizeof(int64_t) * n));
     TRY(h2d(c, c->ugid.p, union_gids, sizeof(int64_t) * n));
     bool identity = (n == c->n_all && union_gids[0] == 0 && union_gids[n - 1] == n - 1);
@@ -646,6 +674,12 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
             c->vec.as<float>(), c->dp, c->ugid.as<int64_t>(), n, c->sub.as<float>());
         CKL();
         c->subp = c->sub.as<float>();
+    }
+    if (metric_is_cos(c)) {
+        TRY(ensure(c->nrm64, sizeof(double) * (size_t)n));
+        k_row_sqnorm64<<<grid_for(c, n, 128), 128, 0, c->st>>>(c->subp, c->dp, c->d, n,
+                                                               c->nrm64.as<double>());
+        CKL();
     }
     TRY(ensure(c->labels, n));
     TRY(h2d(c, c->labels.p, labels, n));
@@ -1011,6 +1045,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
     if (mode < 0 || mode > 2) return fail(KNNM_ERR_ARG, "mode %d", mode);
     if (rev_cap < 0 || rev_cap > c->k) return fail(KNNM_ERR_ARG, "rev_cap %d", rev_cap);
     CK(cudaSetDevice(c->device));
+    c->slots_lazy = false;  // set by a lazy join below
     int64_t n = c->n;
     int k = c->k;
     int W = k + rev_cap;
@@ -1122,8 +1157,9 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         const bool tiled = !use_mma && (c->join_variant == 1 || (c->join_variant < 0 && smem_tiled <= 200 * 1024));
         // long rows (large d): more warps share one staged hood
         const int tj_threads = smem_tiled > 48 * 1024 ? TJ_WARPS_BIG * 32 : TJ_THREADS;
-        const double mrel = 1.0 + (double)(c->d + 8) * ldexp(1.0, -23);
-        const double mabs = (double)(4 * c->d + 64) * ldexp(1.0, -24);
+        // lower bounds of the exact value from the fp32 one (LazyExact)
+        const double lo_rel = 1.0 - (double)(c->d + 8) * ldexp(1.0, -23);
+        const double lo_abs = (double)(4 * c->d + 64) * ldexp(1.0, -24);
         // One pass per hood chunk: bounds -> bucket offsets -> join -> apply.
         auto run_chunk = [&](const int32_t *act, int64_t nact, uint64_t pairs2, bool counted) -> int {
             CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
@@ -1175,28 +1211,44 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                             c->labels.as<int8_t>(), mode, c->sub16p, c->rowb, c->subnormp,
                             c->worst0.as<double>(), boff, stt, Bd, Bs);
                 } else if (tiled) {
+                    // non-certified rows: exact values in the join from the
+                    // staged rows for short rows; for long rows the exact
+                    // evaluation is deferred to the apply (LazyExact), which
+                    // needs it for few slots only
+                    const bool lazy = !c->cert && c->d > LAZY_MIN_D;
+                    c->slots_lazy = c->slots_lazy || lazy;
                     const void *fn;
-                    if (c->metric == 1) fn = c->cert ? (const void *)k_join_tiled<1, true> : (const void *)k_join_tiled<1, false>;
-                    else if (c->metric == 2) fn = (const void *)k_join_tiled<2, false>;
-                    else fn = c->cert ? (const void *)k_join_tiled<0, true> : (const void *)k_join_tiled<0, false>;
+                    if (c->cert) fn = c->metric == 1 ? (const void *)k_join_tiled<1, true, false>
+                                                     : (const void *)k_join_tiled<0, true, false>;
+                    else if (lazy) fn = c->metric == 1 ? (const void *)k_join_tiled<1, false, true>
+                                        : c->metric == 2 ? (const void *)k_join_tiled<2, false, true>
+                                                         : (const void *)k_join_tiled<0, false, true>;
+                    else fn = c->metric == 1 ? (const void *)k_join_tiled<1, false, false>
+                              : c->metric == 2 ? (const void *)k_join_tiled<2, false, false>
+                                               : (const void *)k_join_tiled<0, false, false>;
                     int per_sm = 1;
                     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, tj_threads, smem_tiled));
                     unsigned grid = (unsigned)std::min<int64_t>(nact, (int64_t)c->sms * std::max(per_sm, 1));
                     if (grid == 0) grid = 1;
                     int na = (int)nact;
+                    const double *nrm = c->metric == KNNM_COSINE ? c->nrm64.as<double>() : nullptr;
 #define KNNM_TJ_ARGS                                                                          \
     act, na, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,  \
-        c->subp, c->dp, c->d, c->worst0.as<double>(), boff, stt, Bd, Bs, cnt, mrel, mabs
-                    if (c->metric == 1 && c->cert)
-                        k_join_tiled<1, true><<<grid, tj_threads, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
-                    else if (c->metric == 1)
-                        k_join_tiled<1, false><<<grid, tj_threads, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
-                    else if (c->metric == 2)
-                        k_join_tiled<2, false><<<grid, tj_threads, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
-                    else if (c->cert)
-                        k_join_tiled<0, true><<<grid, tj_threads, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
-                    else
-                        k_join_tiled<0, false><<<grid, tj_threads, smem_tiled, c->st>>>(KNNM_TJ_ARGS);
+        c->subp, c->dp, c->d, c->worst0.as<double>(), boff, stt, Bd, Bs, lo_rel, lo_abs, nrm, cnt
+#define KNNM_TJ_LAUNCH(T, C, L) k_join_tiled<T, C, L><<<grid, tj_threads, smem_tiled, c->st>>>(KNNM_TJ_ARGS)
+                    if (c->cert) {
+                        if (c->metric == 1) KNNM_TJ_LAUNCH(1, true, false);
+                        else KNNM_TJ_LAUNCH(0, true, false);
+                    } else if (lazy) {
+                        if (c->metric == 1) KNNM_TJ_LAUNCH(1, false, true);
+                        else if (c->metric == 2) KNNM_TJ_LAUNCH(2, false, true);
+                        else KNNM_TJ_LAUNCH(0, false, true);
+                    } else {
+                        if (c->metric == 1) KNNM_TJ_LAUNCH(1, false, false);
+                        else if (c->metric == 2) KNNM_TJ_LAUNCH(2, false, false);
+                        else KNNM_TJ_LAUNCH(0, false, false);
+                    }
+#undef KNNM_TJ_LAUNCH
 #undef KNNM_TJ_ARGS
                 } else {
 #define KNNM_JE_ARGS                                                                          \
@@ -1330,17 +1382,22 @@ int knnm_round_apply(knnm_ctx *c, int32_t nsrc, const uint32_t *recv_cnt, const 
     }
     const int E = (c->k + 31) / 32;
     const int blocks = grid_for(c, no * 32, APPLY_WARPS * 32, 16);
-    if (E == 1)
-        k_apply_stream_multi<1><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
-            lo, no, c->k, nsrc, off, recv_cnt, recv_Bd, recv_Bs, c->ids.as<int32_t>(),
-            c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), cnt);
-    else
-        k_apply_stream_multi<2><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(
-            lo, no, c->k, nsrc, off, recv_cnt, recv_Bd, recv_Bs, c->ids.as<int32_t>(),
-            c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), cnt);
+#define KNNM_APM_LAUNCH(EE, LZ)                                                                 \
+    k_apply_stream_multi<EE, LZ><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(                      \
+        lo, no, c->k, nsrc, off, recv_cnt, recv_Bd, recv_Bs, c->ids.as<int32_t>(),             \
+        c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), cnt, lazy_of(c))
+    if (E == 1) {
+        if (c->slots_lazy) KNNM_APM_LAUNCH(1, true);
+        else KNNM_APM_LAUNCH(1, false);
+    } else {
+        if (c->slots_lazy) KNNM_APM_LAUNCH(2, true);
+        else KNNM_APM_LAUNCH(2, false);
+    }
+#undef KNNM_APM_LAUNCH
     CKL();
     TRY(sync_counters(c));
     c->stats.accepted += (int64_t)c->hcnt[C_ACCEPTED];
+    c->stats.exact_evals += (int64_t)c->hcnt[C_EXACT];
     if (accepted) *accepted = (int64_t)c->hcnt[C_ACCEPTED];
     return KNNM_OK;
 }

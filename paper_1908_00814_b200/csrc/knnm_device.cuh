@@ -104,6 +104,13 @@ __device__ __forceinline__ double exact_sqnorm(const float *__restrict__ a, int 
     return acc;
 }
 
+__device__ __forceinline__ double cos_finish(double dot, double na, double nb) {
+    if (na == 0.0 || nb == 0.0) return (na == nb) ? 0.0 : 1.0;
+    if (dot > 0.0 && __dmul_rn(dot, dot) >= __dmul_rn(na, nb)) return 0.0;
+    double r = __dsub_rn(1.0, __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(na), __dsqrt_rn(nb))));
+    return r < 0.0 ? 0.0 : r;
+}
+
 __device__ __forceinline__ double exact_dist_tag(int tag, const float *a, const float *b, int d) {
     if (tag == 1) return exact_dist<1>(a, b, d);
     if (tag == 2) return exact_dist<2>(a, b, d);
@@ -298,6 +305,157 @@ __device__ __forceinline__ int warp_insert(WarpRow<E> &s, int k, int src, double
             if (e == ((k - 1) >> 5)) s.worst = __shfl_sync(FULL_MASK, s.d[e], (k - 1) & 31);
     }
     return 1;
+}
+
+// ---------------------------------------------------------------------------
+// Lazy exact evaluation (non-certified datasets).  The tiled join stores the
+// fp32 screen value f of a pair with the sign bit set ("approximate"); the
+// apply resolves it to the reference's fp64 value only when its rigorous
+// lower bound can still beat the row's current worst.  Decisions are always
+// taken on exact values, so the outcome is the reference's.
+//   L2 / L1 : exact >= f * lo_rel    (|f / exact - 1| <= (d + 8) 2^-23)
+//   cosine  : exact >= f - lo_abs    (|f - exact| <= (4 d + 64) 2^-24)
+// ---------------------------------------------------------------------------
+struct LazyExact {
+    const float *sub;     // subset rows, dp floats each (zero padded)
+    const double *nrm64;  // exact fp64 squared norms per row (cosine only)
+    int dp, d, tag;
+    double lo_rel, lo_abs;
+};
+
+__device__ __forceinline__ bool slot_is_approx(double v) { return __double_as_longlong(v) < 0; }
+
+__device__ __forceinline__ double slot_lower(double v, const LazyExact z) {
+    const double f = -v;
+    return z.tag == 2 ? f - z.lo_abs : f * z.lo_rel;
+}
+
+// Resolve the lane's slot for row r: returns the distance to apply (+inf when
+// the slot cannot pass the row's current state).  need = approximate slot
+// whose lower bound beats the current worst: its exact value must be
+// computed (lazy_warp_eval) before the chunk is applied.
+template <int E>
+__device__ __forceinline__ double lazy_resolve(const WarpRow<E> &s, int k, bool in, double dl,
+                                               const int32_t *__restrict__ Bs, uint64_t pos,
+                                               const LazyExact z, int &src, bool &need) {
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    if (dl != dl) dl = inf;  // unwritten slot
+    const bool apx = z.sub && in && slot_is_approx(dl);
+    const double lb = apx ? slot_lower(dl, z) : dl;
+    const bool pre = in && (lb < s.worst || (s.sz < k && lb < inf));
+    src = pre ? Bs[pos] : 0;
+    need = pre && apx;
+    if (__any_sync(FULL_MASK, need)) {
+        // a candidate already in the list is rejected whatever its distance
+        // (_kernels.py insertion: worst test, then duplicate test): no exact
+        // evaluation for it
+#pragma unroll
+        for (int e = 0; e < E; e++)
+            for (int t = 0; t < 32; t++) {
+                const int id = __shfl_sync(FULL_MASK, s.id[e], t);
+                if (e * 32 + t < s.sz && id == src) need = false;
+            }
+    }
+    if (!pre || apx) return inf;  // approximate: replaced by the exact value if needed
+    return dl;
+}
+
+// Exact reference metric for every lane with need set, computed by the whole
+// warp: groups of up to LZ_G pairs; for each block of 32 dimensions lane t
+// forms the terms of dimension t0 + t for all pairs of the group (coalesced
+// loads, one row conversion shared by the group), the terms go through
+// shared memory, and lane j folds pair j's terms sequentially in index order
+// -- the reference's exact sequence of fp64 roundings (_kernels.py:43-80).
+constexpr int LZ_G = 8;
+constexpr int LZ_S = 33;  // padded term stride (conflict-free column reads)
+
+template <int TAG>
+__device__ __forceinline__ double lz_term(double x, double y) {
+    if (TAG == 1) {
+        const double t = __dsub_rn(x, y);
+        return __dmul_rn(t, t);
+    }
+    if (TAG == 0) return fabs(__dsub_rn(x, y));
+    return __dmul_rn(x, y);
+}
+
+template <int TAG>
+__device__ __noinline__ double lazy_warp_eval_t(const LazyExact z, int64_t r, bool need, int src, double dl,
+                                                double *__restrict__ sm, unsigned lane) {
+    unsigned M = __ballot_sync(FULL_MASK, need);
+    const float *ra = z.sub + r * z.dp;
+    while (M) {
+        // the group: the first (up to) LZ_G lanes of M
+        int cid[LZ_G];
+        unsigned mm = M;
+        int P = 0;
+#pragma unroll
+        for (int j = 0; j < LZ_G; j++) {
+            cid[j] = 0;
+            if (mm) {
+                const int pl = __ffs(mm) - 1;
+                mm &= mm - 1;
+                cid[j] = __shfl_sync(FULL_MASK, src, pl);
+                P = j + 1;
+            } else {
+                (void)__shfl_sync(FULL_MASK, src, 0);
+            }
+        }
+        const unsigned grp = M & ~mm;
+        M = mm;
+        double acc = 0.0;
+        // one block ahead in registers
+        float xn = lane < (unsigned)z.d ? __ldg(ra + lane) : 0.f;
+        float yn[LZ_G];
+#pragma unroll
+        for (int j = 0; j < LZ_G; j++)
+            yn[j] = (j < P && lane < (unsigned)z.d) ? __ldg(z.sub + (int64_t)cid[j] * z.dp + lane) : 0.f;
+        for (int t0 = 0; t0 < z.d; t0 += 32) {
+            const float xc = xn;
+            float yc[LZ_G];
+#pragma unroll
+            for (int j = 0; j < LZ_G; j++) yc[j] = yn[j];
+            const int tn = t0 + 32 + (int)lane;
+            if (t0 + 32 < z.d) {
+                xn = tn < z.d ? __ldg(ra + tn) : 0.f;
+#pragma unroll
+                for (int j = 0; j < LZ_G; j++)
+                    yn[j] = (j < P && tn < z.d) ? __ldg(z.sub + (int64_t)cid[j] * z.dp + tn) : 0.f;
+            }
+            const double x = (double)xc;
+#pragma unroll
+            for (int j = 0; j < LZ_G; j++)
+                if (j < P) sm[j * LZ_S + lane] = lz_term<TAG>(x, (double)yc[j]);
+            __syncwarp();
+            if ((int)lane < P) {
+                const int nb = z.d - t0 < 32 ? z.d - t0 : 32;
+                const double *col = sm + lane * LZ_S;
+                for (int i = 0; i < nb; i++) acc = __dadd_rn(acc, col[i]);
+            }
+            __syncwarp();
+        }
+        if (TAG == 2 && (int)lane < P) {
+            int my = 0;
+#pragma unroll
+            for (int j = 0; j < LZ_G; j++)
+                if (j == (int)lane) my = cid[j];
+            acc = cos_finish(acc, z.nrm64[r], z.nrm64[my]);
+        }
+        // hand pair j's value to its lane
+        const int rank = __popc(grp & lanemask_lt());
+        const double v = __shfl_sync(FULL_MASK, acc, rank < LZ_G ? rank : 0);
+        if ((grp >> lane) & 1u) dl = v;
+    }
+    return dl;
+}
+
+__device__ __forceinline__ void lazy_warp_eval(const LazyExact z, int64_t r, bool need, int src, double &dl,
+                                               double *sm, unsigned lane, unsigned long long &nexact) {
+    const unsigned m = __ballot_sync(FULL_MASK, need);
+    if (lane == 0) nexact += (unsigned long long)__popc(m);
+    if (z.tag == 1) dl = lazy_warp_eval_t<1>(z, r, need, src, dl, sm, lane);
+    else if (z.tag == 0) dl = lazy_warp_eval_t<0>(z, r, need, src, dl, sm, lane);
+    else dl = lazy_warp_eval_t<2>(z, r, need, src, dl, sm, lane);
 }
 
 // Apply up to 32 in-order candidates held one per lane (lanes [0, cnt)).

@@ -159,6 +159,14 @@ __global__ void k_gather_rows(const float *__restrict__ src, int dp, const int64
     }
 }
 
+// Exact fp64 squared norm of every row (sequential, as _kernels.py:65-70).
+__global__ void k_row_sqnorm64(const float *__restrict__ sub, int dp, int d, int64_t n,
+                               double *__restrict__ out) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < n;
+         r += (int64_t)gridDim.x * blockDim.x)
+        out[r] = exact_sqnorm(sub + r * dp, d);
+}
+
 __global__ void k_pad_rows(const float *__restrict__ src, int d, int dp, int64_t n,
                            float *__restrict__ dst) {
     int64_t total = n * dp;
@@ -807,9 +815,10 @@ k_join_exact(const int32_t *__restrict__ active, const uint32_t *__restrict__ nb
 //   CERT  : the dataset carries an exactness certificate (integer values,
 //           d * range^2 < 2^24): every fp32 partial sum is an exact integer,
 //           so the fp32 value IS the reference's fp64 value.
-//   !CERT : the fp32 value screens with a rigorous error margin; pairs that
-//           may pass are re-evaluated with the exact fp64 metric from the
-//           staged vectors.
+//   !CERT : the fp32 value is stored as an approximation (sign bit set) when
+//           its rigorous lower bound can beat the target's round-start worst;
+//           the apply evaluates the exact fp64 metric only for slots that can
+//           still pass the row's current state (LazyExact, knnm_device.cuh).
 // Emission as in k_join_exact: reference-order key (u, p, q), exact-safe
 // prefilter against the round-start worst of each target.
 // ---------------------------------------------------------------------------
@@ -850,29 +859,30 @@ __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
-template <int TAG, bool CERT>
+template <int TAG, bool CERT, bool LAZY>
 __global__ void __launch_bounds__(TJ_WARPS_BIG * 32)
 k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
              const int32_t *__restrict__ nlen, int W, const int8_t *__restrict__ labels, int mode,
              const float *__restrict__ sub, int dp, int d, const double *__restrict__ worst0,
              const uint64_t *__restrict__ boff, const uint32_t *__restrict__ start,
-             double *__restrict__ Bd, int32_t *__restrict__ Bs, unsigned long long *counters,
-             double mrel, double mabs) {
+             double *__restrict__ Bd, int32_t *__restrict__ Bs, double lo_rel, double lo_abs,
+             const double *__restrict__ nrm64, unsigned long long *counters) {
     extern __shared__ __align__(128) float4 sv4[];
     __shared__ int s_id[MAX_W];
     __shared__ int s_pos[MAX_W];
     __shared__ int s_new[MAX_W];
     __shared__ double s_w[MAX_W];
     __shared__ float s_nrm[MAX_W];
-    __shared__ double s_nrm64[MAX_W];
     __shared__ uint64_t s_st[MAX_W];
     __shared__ int s_sc[MAX_W];
     __shared__ PosPrefix s_P;
     __shared__ int s_cls[4];
     __shared__ __align__(8) uint64_t s_bar;
-    // screened-pair queue of the !CERT route: < nthreads left over + one wave
-    // of nwarps patches x 128 pairs
-    __shared__ uint32_t s_q[CERT ? 1 : TJ_WARPS_BIG * 32 + TJ_WARPS_BIG * 128];
+    // exact-in-join route (!CERT && !LAZY): screened-pair queue (< nthreads
+    // left over + one wave of nwarps patches x 128 pairs) and exact norms
+    constexpr bool QUEUE = !CERT && !LAZY;
+    __shared__ uint32_t s_q[QUEUE ? TJ_WARPS_BIG * 32 + TJ_WARPS_BIG * 128 : 1];
+    __shared__ double s_nrm64[QUEUE && TAG == 2 ? MAX_W : 1];
     __shared__ int s_qlen;
     __shared__ unsigned long long s_nexact;
     const float *sv = reinterpret_cast<const float *>(sv4);
@@ -931,6 +941,7 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                         s_new[slot] = (int)(ev[b] & 1);
                         s_sc[slot] = c;
                         s_w[slot] = worst0[id];
+                        if (QUEUE && TAG == 2) s_nrm64[slot] = nrm64[id];
                         s_st[slot] = boff[id] + start[u * W + j];
                     }
                     fill[c] += __popc(m);
@@ -972,10 +983,6 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                 for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL_MASK, acc, o);
                 if (lane == 0) s_nrm[sl] = acc;
             }
-            // exact fp64 norms (sequential, as the reference), one per member
-            if (!CERT)
-                for (int sl = tid; sl < w; sl += blockDim.x)
-                    s_nrm64[sl] = exact_sqnorm(sv + (size_t)((sl & 1) * H + (sl >> 1)) * qs * 4, d);
             __syncthreads();
         }
         // ---- blocks ----------------------------------------------------------
@@ -1068,10 +1075,11 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
             if (ok) ok = s_new[ii] || s_new[jj];
             return ok;
         };
-        // write both directions of an evaluated pair to their reference-order slots
-        auto emit = [&](int ii, int jj, double dd) {
-            const bool e1 = dd < s_w[ii];  // id[ii] <- id[jj]
-            const bool e2 = dd < s_w[jj];  // id[jj] <- id[ii]
+        // write both directions of a pair to their reference-order slots
+        // (value dd; lb = a lower bound of the exact distance, or dd itself)
+        auto emit = [&](int ii, int jj, double dd, double lb) {
+            const bool e1 = lb < s_w[ii];  // id[ii] <- id[jj]
+            const bool e2 = lb < s_w[jj];  // id[jj] <- id[ii]
             const int pi = s_pos[ii], pj = s_pos[jj];
             if (e1) {
                 const uint64_t sij = s_st[ii] + pair_rank(s_P, mode, s_sc[ii], pi, pj);
@@ -1084,27 +1092,57 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                 Bs[sji] = s_id[ii];
             }
         };
+        // approximate value v (>= 0) and a rigorous lower bound of the exact
+        // distance from the fp32 one; values outside the fp32-safe range give
+        // bound 0 / -lo_abs (always evaluated exactly)
+        auto approx = [&](int ii, int jj, float f, float &v) {
+            double lb;
+            if (TAG == 2) {
+                const float na = s_nrm[ii], nb = s_nrm[jj];
+                if (na >= 1e-30f && nb >= 1e-30f && na <= 1e30f && nb <= 1e30f) {
+                    v = fmaxf(1.0f - f / (sqrtf(na) * sqrtf(nb)), 0.0f);
+                    lb = (double)v - lo_abs;
+                } else {
+                    v = 0.0f;
+                    lb = -lo_abs;
+                }
+            } else {
+                v = (f >= 1e-30f && f <= 1e30f) ? f : 0.0f;
+                lb = (double)v * lo_rel;
+            }
+            return lb;
+        };
         const int npatch = np0 + np1;
-        if (CERT) {
-            // every fp32 value is exact: finalize in place
-            for (int pid = warp; pid < npatch; pid += nwarps) {
-                int i0, j0, r1, c1;
-                bool tri;
-                float acc[2][2];
-                const bool live = patch(pid, i0, j0, r1, c1, tri, acc);
+        if (!QUEUE) {
+        for (int pid = warp; pid < npatch; pid += nwarps) {
+            int i0, j0, r1, c1;
+            bool tri;
+            float acc[2][2];
+            const bool live = patch(pid, i0, j0, r1, c1, tri, acc);
 #pragma unroll
-                for (int s = 0; s < 4; s++) {
-                    const int ii = i0 + (s >> 1), jj = j0 + (s & 1);
-                    if (!pair_ok(live, ii, jj, r1, c1, tri)) continue;
-                    const double dd = (double)acc[s >> 1][s & 1];
-                    if (dd < s_w[ii] || dd < s_w[jj]) emit(ii, jj, dd);
+            for (int s = 0; s < 4; s++) {
+                const int ii = i0 + (s >> 1), jj = j0 + (s & 1);
+                if (!pair_ok(live, ii, jj, r1, c1, tri)) continue;
+                const float f = acc[s >> 1][s & 1];
+                if (CERT) {
+                    // every fp32 value is exact
+                    const double dd = (double)f;
+                    if (dd < s_w[ii] || dd < s_w[jj]) emit(ii, jj, dd, dd);
+                } else {
+                    // LAZY: store the approximation (sign bit set); the apply
+                    // evaluates it exactly only if it can still pass
+                    float v;
+                    const double lb = approx(ii, jj, f, v);
+                    if (lb < s_w[ii] || lb < s_w[jj]) emit(ii, jj, -(double)v, lb);
                 }
             }
+        }
         } else {
-            // fp32 screen in synchronized waves (one patch per warp per wave);
-            // pairs that may pass go to a shared queue, drained in whole
-            // multiples of the block (one exact fp64 evaluation per thread,
-            // no divergence, no straggler warp at the hood barrier)
+            // exact in the join: fp32 screen in synchronized waves (one patch
+            // per warp per wave); pairs that may pass go to a shared queue,
+            // drained in whole multiples of the block (one exact fp64
+            // evaluation per thread from the staged rows, no divergence, no
+            // straggler warp at the hood barrier)
             const int nthreads = blockDim.x;
             const int nwaves = (npatch + nwarps - 1) / nwarps;
             for (int wave = 0; wave < nwaves; wave++) {
@@ -1119,18 +1157,9 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                         const int ii = i0 + (s >> 1), jj = j0 + (s & 1);
                         bool maybe = pair_ok(live, ii, jj, r1, c1, tri);
                         if (maybe) {
-                            const double wi = s_w[ii], wj = s_w[jj];
-                            const double wmax = wi > wj ? wi : wj;
-                            const float f = acc[s >> 1][s & 1];
-                            if (TAG == 2) {
-                                const float na = s_nrm[ii], nb = s_nrm[jj];
-                                if (na != 0.f && nb != 0.f) {
-                                    const float cs = 1.0f - f / (sqrtf(na) * sqrtf(nb));
-                                    maybe = (double)cs <= wmax + mabs;
-                                }
-                            } else {
-                                maybe = (double)f <= wmax * mrel;
-                            }
+                            float v;
+                            const double lb = approx(ii, jj, acc[s >> 1][s & 1], v);
+                            maybe = lb < s_w[ii] || lb < s_w[jj];
                         }
                         const unsigned m = __ballot_sync(FULL_MASK, maybe);
                         int base = 0;
@@ -1151,7 +1180,7 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                         const float *rb = reinterpret_cast<const float *>(rowp(jj));
                         const double dd = TAG == 2 ? exact_cos_norms(ra, rb, d, s_nrm64[ii], s_nrm64[jj])
                                                    : exact_dist<TAG>(ra, rb, d);
-                        emit(ii, jj, dd);
+                        emit(ii, jj, dd, dd);
                     }
                     __syncthreads();
                     if (tid == 0) {
@@ -1164,7 +1193,7 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
         }
         __syncthreads();  // smem reused by the next hood
     }
-    if (!CERT && tid == 0 && s_nexact) atomicAdd(&counters[C_EXACT], s_nexact);
+    if (QUEUE && tid == 0 && s_nexact) atomicAdd(&counters[C_EXACT], s_nexact);
 }
 
 // ---------------------------------------------------------------------------
@@ -1623,14 +1652,15 @@ constexpr int APPLY_WARPS = 4;
 // step (coalesced), candidates that cannot pass the current worst are
 // skipped by ballot, the rest go through warp_insert in slot order -- which
 // is the reference's sequential order, so no sorting is needed.
-template <int E>
+template <int E, bool LAZY>
 __global__ void __launch_bounds__(APPLY_WARPS * 32)
 k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double *__restrict__ Bd,
                const int32_t *__restrict__ Bs, int32_t *ids, double *dists, uint8_t *flags,
-               int32_t *sizes, unsigned long long *counters) {
+               int32_t *sizes, unsigned long long *counters, LazyExact z) {
+    __shared__ double s_lz[LAZY ? APPLY_WARPS : 1][LAZY ? LZ_G * LZ_S : 1];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * APPLY_WARPS;
-    unsigned long long acc = 0, slots = 0, written = 0;
+    unsigned long long acc = 0, slots = 0, written = 0, nexact = 0;
     for (int64_t r = (int64_t)blockIdx.x * APPLY_WARPS + wib; r < n; r += nw) {
         const uint64_t lo = boff[r];
         const int64_t ns = (int64_t)(boff[r + 1] - lo);
@@ -1646,13 +1676,22 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
             const int64_t j = c0 + lane;
             double dl = dnext;
             dnext = j + 32 < ns ? Bd[lo + j + 32] : inf;
-            if (dl != dl) dl = inf;  // unwritten slot
-            else if (j < ns) written++;
-            // an unwritten slot belongs to a row that was full at round start
-            // and a distance >= its worst: it can never pass
-            const bool pre = j < ns && (dl < s.worst || (s.sz < k && dl < inf));
-            if (!__any_sync(FULL_MASK, pre)) continue;
-            const int src = pre ? Bs[lo + j] : 0;
+            // an unwritten slot (NaN) belongs to a row that was full at round
+            // start and a distance >= its worst: it can never pass
+            int src;
+            if (LAZY) {
+                if (j < ns && dl == dl) written++;
+                bool need;
+                dl = lazy_resolve<E>(s, k, j < ns, dl, Bs, lo + j, z, src, need);
+                if (__any_sync(FULL_MASK, need)) lazy_warp_eval(z, r, need, src, dl, s_lz[wib], lane, nexact);
+                if (!__any_sync(FULL_MASK, dl < inf)) continue;
+            } else {
+                if (dl != dl) dl = inf;
+                else if (j < ns) written++;
+                const bool pre = j < ns && (dl < s.worst || (s.sz < k && dl < inf));
+                if (!__any_sync(FULL_MASK, pre)) continue;
+                src = pre ? Bs[lo + j] : 0;
+            }
             const int cnt = ns - c0 < 32 ? (int)(ns - c0) : 32;
             a += warp_apply_chunk<E>(s, k, src, dl, cnt, lane);
         }
@@ -1662,8 +1701,12 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
     if (lane == 0 && acc) atomicAdd(&counters[C_ACCEPTED], acc);
     if (lane == 0 && slots) atomicAdd(&counters[C_CAND], slots);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) written += __shfl_xor_sync(FULL_MASK, written, o);
+    for (int o = 16; o > 0; o >>= 1) {
+        written += __shfl_xor_sync(FULL_MASK, written, o);
+        nexact += __shfl_xor_sync(FULL_MASK, nexact, o);
+    }
     if (lane == 0 && written) atomicAdd(&counters[C_WRITTEN], written);
+    if (lane == 0 && nexact) atomicAdd(&counters[C_EXACT], nexact);
 }
 
 // Round-start worst of every row (sharded rounds: the join needs the
@@ -1679,16 +1722,17 @@ __global__ void k_worst0_all(const int32_t *__restrict__ sizes, const double *__
 // source rank; blocks are processed in source order, which is hood order,
 // which is the reference's order.  off[s * (no+1) + i] = element offset of
 // row lo+i's segment in the receive buffers.
-template <int E>
+template <int E, bool LAZY>
 __global__ void __launch_bounds__(APPLY_WARPS * 32)
 k_apply_stream_multi(int64_t lo, int64_t no, int k, int nsrc, const uint64_t *__restrict__ off,
                      const uint32_t *__restrict__ cnt, const double *__restrict__ Bd,
                      const int32_t *__restrict__ Bs, int32_t *ids, double *dists, uint8_t *flags,
-                     int32_t *sizes, unsigned long long *counters) {
+                     int32_t *sizes, unsigned long long *counters, LazyExact z) {
+    __shared__ double s_lz[LAZY ? APPLY_WARPS : 1][LAZY ? LZ_G * LZ_S : 1];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * APPLY_WARPS;
     const double inf = __longlong_as_double(0x7ff0000000000000LL);
-    unsigned long long acc = 0;
+    unsigned long long acc = 0, nexact = 0;
     for (int64_t i = (int64_t)blockIdx.x * APPLY_WARPS + wib; i < no; i += nw) {
         const int64_t r = lo + i;
         bool any = false;
@@ -1703,10 +1747,18 @@ k_apply_stream_multi(int64_t lo, int64_t no, int k, int nsrc, const uint64_t *__
             for (int64_t c0 = 0; c0 < ns; c0 += 32) {
                 const int64_t j = c0 + lane;
                 double dl = j < ns ? Bd[base + j] : inf;
-                if (dl != dl) dl = inf;
-                const bool pre = j < ns && (dl < st.worst || (st.sz < k && dl < inf));
-                if (!__any_sync(FULL_MASK, pre)) continue;
-                const int src = pre ? Bs[base + j] : 0;
+                int src;
+                if (LAZY) {
+                    bool need;
+                    dl = lazy_resolve<E>(st, k, j < ns, dl, Bs, base + j, z, src, need);
+                    if (__any_sync(FULL_MASK, need)) lazy_warp_eval(z, r, need, src, dl, s_lz[wib], lane, nexact);
+                    if (!__any_sync(FULL_MASK, dl < inf)) continue;
+                } else {
+                    if (dl != dl) dl = inf;
+                    const bool pre = j < ns && (dl < st.worst || (st.sz < k && dl < inf));
+                    if (!__any_sync(FULL_MASK, pre)) continue;
+                    src = pre ? Bs[base + j] : 0;
+                }
                 const int c = ns - c0 < 32 ? (int)(ns - c0) : 32;
                 a += warp_apply_chunk<E>(st, k, src, dl, c, lane);
             }
@@ -1715,6 +1767,9 @@ k_apply_stream_multi(int64_t lo, int64_t no, int k, int nsrc, const uint64_t *__
         acc += a;
     }
     if (lane == 0 && acc) atomicAdd(&counters[C_ACCEPTED], acc);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nexact += __shfl_xor_sync(FULL_MASK, nexact, o);
+    if (lane == 0 && nexact) atomicAdd(&counters[C_EXACT], nexact);
 }
 
 __global__ void k_add_base(uint64_t *off, int64_t m, uint64_t base) {

@@ -47,6 +47,9 @@ CASES = [
     (2000, 960, 20, 1, "unitgmm"),
     (1500, 5, 6, 0, "uniform"),
     (5000, 100, 40, 1, "intgmm"),
+    (2500, 70, 16, 0, "uniform"),  # L1, non-certified, ragged 32-dim blocks
+    (1500, 400, 10, 2, "sphere"),  # d > 384: exact evaluation deferred to the apply
+    (1500, 420, 12, 0, "uniform"),
 ]
 
 

@@ -64,7 +64,7 @@ def run(name, scale):
     st = eng.stats()
     eng.set_profiling(False)
     print(f"{name}: n={ds.n} d={ds.d} merge {dt:.3f} s, {c.count/dt:.3e} evals/s, evals {c.count}, "
-          f"recall@10 {recall(ds, metric, u):.4f}, setup {setup:.1f} s, exact_evals {st['exact_evals']}, "
+          f"recall@10 {recall(ds, metric, u):.4f}, setup {setup:.1f} s, exact_evals {st["exact_evals"]}, accepted {st["accepted"]}, "
           f"phases ms " + " ".join(f"{k}={st[k]:.1f}" for k in ("join_ms", "join_kernel_ms", "assemble_ms",
                                                                 "update_ms", "reverse_ms", "other_ms")),
           flush=True)
