@@ -519,11 +519,12 @@ int knnm_create(int device, knnm_ctx **out) {
                             (int)(2 * sizeof(uint32_t) * BLOCK_SORT_MAX)));
     for (auto f : {k_join_exact<0>, k_join_exact<1>, k_join_exact<2>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    CK(cudaFuncSetAttribute(k_join_mma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (auto f : {k_join_mma<false, 1>, k_join_mma<false, 2>, k_join_mma<false, 4>,
+                   k_join_mma<true, 1>, k_join_mma<true, 2>, k_join_mma<true, 4>})
+        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (auto f : {k_bf_topk<0>, k_bf_topk<1>, k_bf_topk<2>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(BF_THREADS * BF_MAXK * (sizeof(double) + sizeof(int32_t)))));
-    CK(cudaFuncSetAttribute(k_join_mma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (auto f : {k_join_tiled<0, false, false>, k_join_tiled<1, false, false>,
                    k_join_tiled<2, false, false>, k_join_tiled<0, false, true>,
                    k_join_tiled<1, false, true>, k_join_tiled<2, false, true>,
@@ -1195,21 +1196,31 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                 PhaseTimer ptk(c, PH_JOINK);  // the local-join kernel alone (roofline)
                 if (use_mma) {
                     int per_sm = 1;
-                    const void *fn = c->cert_u8 ? (const void *)k_join_mma<true> : (const void *)k_join_mma<false>;
+                    // 32-entry position blocks per hood
+                    const int nb = W <= 32 ? 1 : W <= 64 ? 2 : 4;
+                    const void *fn;
+                    if (c->cert_u8) fn = nb == 1 ? (const void *)k_join_mma<true, 1>
+                                       : nb == 2 ? (const void *)k_join_mma<true, 2> : (const void *)k_join_mma<true, 4>;
+                    else fn = nb == 1 ? (const void *)k_join_mma<false, 1>
+                              : nb == 2 ? (const void *)k_join_mma<false, 2> : (const void *)k_join_mma<false, 4>;
                     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, MJ_WARPS * 32, smem_mma));
                     unsigned grid = (unsigned)std::min<int64_t>((nact + MJ_WARPS - 1) / MJ_WARPS,
                                                                 (int64_t)c->sms * std::max(per_sm, 1));
                     if (grid == 0) grid = 1;
-                    if (c->cert_u8)
-                        k_join_mma<true><<<grid, MJ_WARPS * 32, smem_mma, c->st>>>(
-                            act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
-                            c->labels.as<int8_t>(), mode, c->sub16p, c->rowb, c->subnormp,
-                            c->worst0.as<double>(), boff, stt, Bd, Bs);
-                    else
-                        k_join_mma<false><<<grid, MJ_WARPS * 32, smem_mma, c->st>>>(
-                            act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
-                            c->labels.as<int8_t>(), mode, c->sub16p, c->rowb, c->subnormp,
-                            c->worst0.as<double>(), boff, stt, Bd, Bs);
+#define KNNM_MJ_LAUNCH(U, N)                                                                      \
+    k_join_mma<U, N><<<grid, MJ_WARPS * 32, smem_mma, c->st>>>(                                  \
+        act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), \
+        mode, c->sub16p, c->rowb, c->subnormp, c->worst0.as<double>(), boff, stt, Bd, Bs)
+                    if (c->cert_u8) {
+                        if (nb == 1) KNNM_MJ_LAUNCH(true, 1);
+                        else if (nb == 2) KNNM_MJ_LAUNCH(true, 2);
+                        else KNNM_MJ_LAUNCH(true, 4);
+                    } else {
+                        if (nb == 1) KNNM_MJ_LAUNCH(false, 1);
+                        else if (nb == 2) KNNM_MJ_LAUNCH(false, 2);
+                        else KNNM_MJ_LAUNCH(false, 4);
+                    }
+#undef KNNM_MJ_LAUNCH
                 } else if (tiled) {
                     // non-certified rows: exact values in the join from the
                     // staged rows for short rows; for long rows the exact

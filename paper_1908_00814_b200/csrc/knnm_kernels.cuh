@@ -1228,8 +1228,18 @@ __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// One member of a staged hood (32 bytes: two 128-bit shared loads).
+struct __align__(16) MjRec {
+    double w;     // round-start worst of the member's row
+    uint64_t st;  // first bucket slot of the membership
+    int id;       // member row
+    float nrm;    // row norm (int bits on the u8 route)
+    int pk;       // nbh position | new << 8 | class << 9 | partner_self << 11
+    int pad;
+};
+
 __host__ __device__ constexpr size_t mj_meta_bytes(int Wp) {
-    return (16 + (size_t)Wp * (8 + 8 + 4 * 5) + sizeof(PosPrefix) + 127) & ~(size_t)127;
+    return (16 + (size_t)Wp * sizeof(MjRec) + sizeof(PosPrefix) + 127) & ~(size_t)127;
 }
 
 __device__ __forceinline__ void mma16832_u8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
@@ -1241,38 +1251,68 @@ __device__ __forceinline__ void mma16832_u8(int (&c)[4], uint32_t a0, uint32_t a
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// Per-warp shared-memory region of k_join_mma (W slots padded to Wp = W+16).
-struct MjSmem {
-    uint64_t *bar;
-    double *w;      // round-start worst of each slot's row
-    uint64_t *st;   // first bucket slot of each slot's membership
-    int *id, *pos, *nw, *cls;
-    float *nrm;
-    uint8_t *P;     // class-position prefix table
-    char *rows;     // fp16 rows, stride rs
-};
+// Warp-cooperative Q fill (build_pos_prefix) over NB position blocks.
+template <int NB>
+__device__ __forceinline__ void build_pos_prefix_nb(uint8_t *Q, const int (&clsv)[NB], int mode,
+                                                    unsigned lane) {
+    int base0 = 0, base1 = 0, base2 = 0, base3 = 0;
+    const int mk0 = partner_mask(mode, 0), mk1 = partner_mask(mode, 1);
+    const int mk2 = partner_mask(mode, 2), mk3 = partner_mask(mode, 3);
+    const unsigned lt = lanemask_lt();
+#pragma unroll
+    for (int b = 0; b < NB; b++) {
+        const unsigned m0 = __ballot_sync(FULL_MASK, clsv[b] == 0);
+        const unsigned m1 = __ballot_sync(FULL_MASK, clsv[b] == 1);
+        const unsigned m2 = __ballot_sync(FULL_MASK, clsv[b] == 2);
+        const unsigned m3 = __ballot_sync(FULL_MASK, clsv[b] == 3);
+        const int be0 = base0 + __popc(m0 & lt), be1 = base1 + __popc(m1 & lt);
+        const int be2 = base2 + __popc(m2 & lt), be3 = base3 + __popc(m3 & lt);
+        base0 += __popc(m0);
+        base1 += __popc(m1);
+        base2 += __popc(m2);
+        base3 += __popc(m3);
+        auto q = [&](int mk) {
+            return (mk & 1 ? be0 : 0) + (mk & 2 ? be1 : 0) + (mk & 4 ? be2 : 0) + (mk & 8 ? be3 : 0);
+        };
+        const int x = b * 32 + (int)lane;
+        Q[0 * (MAX_W + 1) + x] = (uint8_t)q(mk0);
+        Q[1 * (MAX_W + 1) + x] = (uint8_t)q(mk1);
+        Q[2 * (MAX_W + 1) + x] = (uint8_t)q(mk2);
+        Q[3 * (MAX_W + 1) + x] = (uint8_t)q(mk3);
+    }
+}
 
-__device__ __forceinline__ MjSmem mj_carve(char *base, int Wp) {
-    MjSmem m;
-    m.bar = reinterpret_cast<uint64_t *>(base);
-    char *p = base + 16;
-    m.w = reinterpret_cast<double *>(p); p += 8 * Wp;
-    m.st = reinterpret_cast<uint64_t *>(p); p += 8 * Wp;
-    m.id = reinterpret_cast<int *>(p); p += 4 * Wp;
-    m.pos = reinterpret_cast<int *>(p); p += 4 * Wp;
-    m.nw = reinterpret_cast<int *>(p); p += 4 * Wp;
-    m.cls = reinterpret_cast<int *>(p); p += 4 * Wp;
-    m.nrm = reinterpret_cast<float *>(p); p += 4 * Wp;
-    m.P = reinterpret_cast<uint8_t *>(p);
-    m.rows = base + mj_meta_bytes(Wp);
-    return m;
+__device__ __forceinline__ MjRec lds_rec(const MjRec *p) {
+    const float4 a = reinterpret_cast<const float4 *>(p)[0];
+    const float4 b = reinterpret_cast<const float4 *>(p)[1];
+    MjRec r;
+    r.w = __hiloint2double(__float_as_int(a.y), __float_as_int(a.x));
+    r.st = ((uint64_t)(uint32_t)__float_as_int(a.w) << 32) | (uint32_t)__float_as_int(a.z);
+    r.id = __float_as_int(b.x);
+    r.nrm = b.y;
+    r.pk = __float_as_int(b.z);
+    r.pad = 0;
+    return r;
+}
+
+// Slot of the update "member a receives partner b" (reference order, see
+// pair_rank): membership start + rank of b's position among a's partners.
+__device__ __forceinline__ uint64_t mj_slot(const uint8_t *__restrict__ Q, const MjRec &a, const MjRec &b) {
+    const int pa = a.pk & 0xFF, pb = b.pk & 0xFF, ca = (a.pk >> 9) & 3;
+    return a.st + (uint32_t)Q[ca * (MAX_W + 1) + pb] - (uint32_t)(((a.pk >> 11) & 1) && pa < pb);
 }
 
 // U8 = true: rows are u8 (integer data in [0, 255]); the Gram block uses
 // mma.m16n8k32 u8 x u8 -> s32, exact integer arithmetic; norms are integers.
 // U8 = false: fp16 rows, m16n8k16 fp16 -> fp32 (exact under the dot-form
-// certificate).  `rowb` = staged bytes per row (multiple of 32).
-template <bool U8>
+// certificate).  `rowb` = staged bytes per row (multiple of 32).  NB = 32-entry
+// blocks of a hood (W <= 32 * NB).
+//
+// One warp per hood, software-pipelined three deep: while hood i's rows are
+// in flight (TMA) and its Gram block computes, hood i+1's per-member metadata
+// gathers (worst, norm, bucket offset) and hood i+2's neighbour entries are
+// already loading into registers.
+template <bool U8, int NB>
 __global__ void __launch_bounds__(MJ_WARPS * 32)
 k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
            const int32_t *__restrict__ nlen, int W, const int8_t *__restrict__ labels, int mode,
@@ -1285,103 +1325,143 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
     const int Wp = W + 16;
     const int rs = rowb + 16;  // padded row stride: conflict-free ldmatrix
     const size_t per_warp = mj_meta_bytes(Wp) + (size_t)Wp * rs;
-    const MjSmem m = mj_carve(mj_smem + (size_t)warp * per_warp, Wp);
-    if (lane == 0) mbar_init(m.bar, 1);
+    char *base = mj_smem + (size_t)warp * per_warp;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(base);
+    MjRec *rec = reinterpret_cast<MjRec *>(base + 16);
+    uint8_t *Q = reinterpret_cast<uint8_t *>(rec + Wp);
+    char *rows = base + mj_meta_bytes(Wp);
+    if (lane == 0) mbar_init(bar, 1);
     // zero the row buffer once: slots beyond w feed the MMA tile tails
     for (size_t i = lane * 16; i < (size_t)Wp * rs; i += 32 * 16)
-        *reinterpret_cast<float4 *>(m.rows + i) = make_float4(0.f, 0.f, 0.f, 0.f);
+        *reinterpret_cast<float4 *>(rows + i) = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncwarp();
     uint32_t phase = 0;
     const uint32_t row_bytes = (uint32_t)rowb;
-    const uint32_t rbase = smem_u32(m.rows);
-    // software prefetch: the next hood's id/length/entries are loaded while
-    // the current hood's rows are in flight (TMA) and its Gram block computes
+    const uint32_t rbase = smem_u32(rows);
     const int stride = gridDim.x * MJ_WARPS;
-    int hi = blockIdx.x * MJ_WARPS + warp;
-    int64_t u_cur = hi < nactive ? active[hi] : 0;
-    int w_cur = hi < nactive ? nlen[u_cur] : 0;
-    uint32_t ev[4];
+    const unsigned lt = lanemask_lt();
+
+    // neighbour entries of hood u (all W positions; masked by length later)
+    auto load_ev = [&](bool ok, int64_t u, uint32_t (&ev)[NB]) {
 #pragma unroll
-    for (int b = 0; b < 4; b++) {
-        const int j = b * 32 + (int)lane;
-        ev[b] = j < w_cur ? nbh[u_cur * W + j] : 0u;
-    }
-    int64_t u_nxt = hi + stride < nactive ? active[hi + stride] : 0;
-    for (; hi < nactive; hi += stride) {
-        const int64_t u = u_cur;
-        const int w = w_cur;
-        const int w_nxt = hi + stride < nactive ? nlen[u_nxt] : 0;
-        // ---- classify members into (label, new-first) slots ------------------
-        int clsv[4], labv[4];
-#pragma unroll
-        for (int b = 0; b < 4; b++) {
+        for (int b = 0; b < NB; b++) {
             const int j = b * 32 + (int)lane;
-            labv[b] = (j < w && mode != 0) ? (int)((ev[b] >> 1) & 1) : 0;
+            ev[b] = (ok && j < W) ? __ldg(nbh + u * W + j) : 0u;
         }
-        int cnts[4] = {0, 0, 0, 0};
+    };
+    // per-member metadata of hood u (independent gathers, issued together)
+    auto gather = [&](int64_t u, int w, const uint32_t (&ev)[NB], double (&mw)[NB], float (&mn)[NB],
+                      uint64_t (&mb)[NB]) {
 #pragma unroll
-        for (int b = 0; b < 4; b++) {
+        for (int b = 0; b < NB; b++) {
             const int j = b * 32 + (int)lane;
-            clsv[b] = j < w ? (labv[b] != 0) * 2 + ((ev[b] & 1) ? 0 : 1) : 4;
-#pragma unroll
-            for (int c = 0; c < 4; c++) cnts[c] += __popc(__ballot_sync(FULL_MASK, clsv[b] == c));
-        }
-        const int base_cls[4] = {0, cnts[0], cnts[0] + cnts[1], cnts[0] + cnts[1] + cnts[2]};
-        int fill[4] = {0, 0, 0, 0};
-        int myslot[4];
-#pragma unroll
-        for (int b = 0; b < 4; b++) {
-            myslot[b] = -1;
-#pragma unroll
-            for (int c = 0; c < 4; c++) {
-                const unsigned mk = __ballot_sync(FULL_MASK, clsv[b] == c);
-                if (clsv[b] == c) myslot[b] = base_cls[c] + fill[c] + __popc(mk & lanemask_lt());
-                fill[c] += __popc(mk);
+            if (j < w) {
+                const int id = (int)(ev[b] >> 2);
+                mw[b] = __ldg(worst0 + id);
+                mn[b] = __ldg(norms + id);
+                mb[b] = __ldg(boff + id) + __ldg(start + u * W + j);
+            } else {
+                mw[b] = 0.0;
+                mn[b] = 0.f;
+                mb[b] = 0;
             }
+        }
+    };
+
+    int hi = blockIdx.x * MJ_WARPS + warp;
+    int64_t u0 = hi < nactive ? __ldg(active + hi) : 0;
+    int w0 = hi < nactive ? __ldg(nlen + u0) : 0;
+    uint32_t ev0[NB];
+    load_ev(hi < nactive, u0, ev0);
+    int64_t u1 = hi + stride < nactive ? __ldg(active + hi + stride) : 0;
+    int w1 = hi + stride < nactive ? __ldg(nlen + u1) : 0;
+    uint32_t ev1[NB];
+    load_ev(hi + stride < nactive, u1, ev1);
+    int64_t u2 = hi + 2 * stride < nactive ? __ldg(active + hi + 2 * stride) : 0;
+    double mw0[NB];
+    float mn0[NB];
+    uint64_t mb0[NB];
+    gather(u0, w0, ev0, mw0, mn0, mb0);
+
+    for (; hi < nactive; hi += stride) {
+        const int w = w0;
+        // ---- classify members into (label, new-first) slots ------------------
+        int clsv[NB];
+        int c0n = 0, c1n = 0, c2n = 0, c3n = 0;
+#pragma unroll
+        for (int b = 0; b < NB; b++) {
+            const int j = b * 32 + (int)lane;
+            const int lab = (j < w && mode != 0) ? (int)((ev0[b] >> 1) & 1) : 0;
+            clsv[b] = j < w ? lab * 2 + ((ev0[b] & 1) ? 0 : 1) : 4;
+            c0n += __popc(__ballot_sync(FULL_MASK, clsv[b] == 0));
+            c1n += __popc(__ballot_sync(FULL_MASK, clsv[b] == 1));
+            c2n += __popc(__ballot_sync(FULL_MASK, clsv[b] == 2));
+            c3n += __popc(__ballot_sync(FULL_MASK, clsv[b] == 3));
         }
         fence_proxy_async();  // prior generic reads of the rows vs. async-proxy writes
-        if (lane == 0) mbar_expect_tx(m.bar, row_bytes * (uint32_t)w);
+        if (lane == 0) mbar_expect_tx(bar, row_bytes * (uint32_t)w);
         __syncwarp();
-        // each lane stages its own members' rows (parallel TMA issue) and
-        // fetches their per-row metadata (independent loads, issued together)
+        {
+            int f0 = 0, f1 = c0n, f2 = c0n + c1n, f3 = c0n + c1n + c2n;  // class bases
 #pragma unroll
-        for (int b = 0; b < 4; b++) {
-            const int sl = myslot[b];
-            if (sl >= 0) {
-                const int id = (int)(ev[b] >> 2);
-                const int j = b * 32 + (int)lane;
-                bulk_g2s(m.rows + (size_t)sl * rs, sub16 + (int64_t)id * rowb, row_bytes, m.bar);
-                m.id[sl] = id;
-                m.pos[sl] = j;
-                m.nw[sl] = (int)(ev[b] & 1);
-                m.cls[sl] = clsv[b];
-                m.w[sl] = worst0[id];
-                m.nrm[sl] = norms[id];
-                m.st[sl] = boff[id] + start[u * W + j];
+            for (int b = 0; b < NB; b++) {
+                const unsigned k0 = __ballot_sync(FULL_MASK, clsv[b] == 0);
+                const unsigned k1 = __ballot_sync(FULL_MASK, clsv[b] == 1);
+                const unsigned k2 = __ballot_sync(FULL_MASK, clsv[b] == 2);
+                const unsigned k3 = __ballot_sync(FULL_MASK, clsv[b] == 3);
+                const int c = clsv[b];
+                const int sl = c == 0 ? f0 + __popc(k0 & lt)
+                             : c == 1 ? f1 + __popc(k1 & lt)
+                             : c == 2 ? f2 + __popc(k2 & lt)
+                             : c == 3 ? f3 + __popc(k3 & lt) : -1;
+                f0 += __popc(k0);
+                f1 += __popc(k1);
+                f2 += __popc(k2);
+                f3 += __popc(k3);
+                if (sl >= 0) {
+                    // each lane stages its own members' rows (parallel TMA issue)
+                    const int id = (int)(ev0[b] >> 2);
+                    const int j = b * 32 + (int)lane;
+                    bulk_g2s(rows + (size_t)sl * rs, sub16 + (int64_t)id * rowb, row_bytes, bar);
+                    const int pk = j | (int)((ev0[b] & 1) << 8) | (c << 9) | ((int)partner_self(mode, c) << 11);
+                    float4 *dst = reinterpret_cast<float4 *>(rec + sl);
+                    dst[0] = make_float4(__int_as_float(__double2loint(mw0[b])), __int_as_float(__double2hiint(mw0[b])),
+                                         __int_as_float((int)(uint32_t)mb0[b]), __int_as_float((int)(uint32_t)(mb0[b] >> 32)));
+                    dst[1] = make_float4(__int_as_float(id), mn0[b], __int_as_float(pk), 0.f);
+                }
             }
         }
-        build_pos_prefix(m.P, clsv, mode, lane);
-        uint32_t ev_nxt[4];
-#pragma unroll
-        for (int b = 0; b < 4; b++) {
-            const int j = b * 32 + (int)lane;
-            ev_nxt[b] = j < w_nxt ? nbh[u_nxt * W + j] : 0u;
-        }
-        const int64_t u_nn = hi + 2 * stride < nactive ? active[hi + 2 * stride] : 0;
+        build_pos_prefix_nb<NB>(Q, clsv, mode, lane);
+        // ---- prefetch: hood i+1 metadata, hood i+2 entries, hood i+3 id --------
+        double mw1[NB];
+        float mn1[NB];
+        uint64_t mb1[NB];
+        gather(u1, w1, ev1, mw1, mn1, mb1);
+        const bool ok2 = hi + 2 * stride < nactive;
+        const int w2 = ok2 ? __ldg(nlen + u2) : 0;
+        uint32_t ev2[NB];
+        load_ev(ok2, u2, ev2);
+        const int64_t u3 = hi + 3 * stride < nactive ? __ldg(active + hi + 3 * stride) : 0;
         __syncwarp();
-        mbar_wait(m.bar, phase);
+        mbar_wait(bar, phase);
         phase ^= 1u;
-        const int nA = cnts[0] + cnts[1];
+        // ---- Gram blocks and emission -----------------------------------------
+        const int nA = c0n + c1n;
         const int nblk = mode == 2 ? 2 : 1;
+        const int g = lane >> 2, t4 = lane & 3;
         for (int bk = 0; bk < nblk; bk++) {
             const int r0 = bk ? nA : 0, r1 = bk ? w : (mode == 0 ? w : nA);
-            const int c0 = bk ? nA : (mode == 0 ? 0 : nA), c1 = w;
-            const int rn = bk ? cnts[2] : cnts[0], cn = bk ? cnts[2] : (mode == 0 ? cnts[0] : cnts[2]);
+            const int cc0 = bk ? nA : (mode == 0 ? 0 : nA), cc1 = w;
+            const int rn = bk ? c2n : c0n, cn = bk ? c2n : (mode == 0 ? c0n : c2n);
             const bool tri = bk ? true : (mode == 0);
             for (int m0 = r0; m0 < r1; m0 += 16) {
-                for (int n0 = c0; n0 < c1; n0 += 8) {
-                    if (m0 - r0 >= rn && n0 - c0 >= cn) continue;  // old x old
-                    if (tri && n0 + 7 <= m0) continue;             // below diagonal
+                // this lane's two row members of the tile row (hoisted)
+                const int ia = m0 + g, ib = m0 + g + 8;
+                const MjRec ra = lds_rec(rec + (ia < r1 ? ia : r0));
+                const MjRec rb = lds_rec(rec + (ib < r1 ? ib : r0));
+                for (int n0 = cc0; n0 < cc1; n0 += 8) {
+                    if (m0 - r0 >= rn && n0 - cc0 >= cn) continue;  // old x old
+                    if (tri && n0 + 7 <= m0) continue;              // below diagonal
                     float acc[4] = {0.f, 0.f, 0.f, 0.f};
                     int iacc[4] = {0, 0, 0, 0};
                     const uint32_t a_addr = rbase + (uint32_t)((m0 + (lane & 15)) * rs + (lane >> 4) * 16);
@@ -1398,40 +1478,49 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                         else
                             mma16816(acc, a0, a1, a2, a3, b0, b1);
                     }
-                    const int g = lane >> 2, t4 = lane & 3;
+                    const int ja = n0 + 2 * t4, jb = ja + 1;
+                    const MjRec ca = lds_rec(rec + (ja < cc1 ? ja : cc0));
+                    const MjRec cb = lds_rec(rec + (jb < cc1 ? jb : cc0));
 #pragma unroll
                     for (int s = 0; s < 4; s++) {
-                        const int ii = m0 + g + (s >> 1) * 8, jj = n0 + 2 * t4 + (s & 1);
-                        bool ok = ii < r1 && jj < c1;
+                        const MjRec &R = (s >> 1) ? rb : ra;
+                        const MjRec &C = (s & 1) ? cb : ca;
+                        const int ii = (s >> 1) ? ib : ia, jj = (s & 1) ? jb : ja;
+                        bool ok = ii < r1 && jj < cc1;
                         if (ok && tri) ok = ii < jj;
-                        if (ok) ok = m.nw[ii] || m.nw[jj];
+                        if (ok) ok = ((R.pk | C.pk) >> 8) & 1;  // at least one new
                         if (!ok) continue;
                         const double dd =
-                            U8 ? (double)((__float_as_int(m.nrm[ii]) + __float_as_int(m.nrm[jj])) - 2 * iacc[s])
-                               : (double)((m.nrm[ii] + m.nrm[jj]) - 2.0f * acc[s]);
-                        const bool e1 = dd < m.w[ii], e2 = dd < m.w[jj];
-                        if (!(e1 || e2)) continue;
-                        const int pi = m.pos[ii], pj = m.pos[jj];
-                        if (e1) {
-                            const uint64_t sij = m.st[ii] + pair_rank(m.P, mode, m.cls[ii], pi, pj);
-                            Bd[sij] = dd;
-                            Bs[sij] = m.id[jj];
+                            U8 ? (double)((__float_as_int(R.nrm) + __float_as_int(C.nrm)) - 2 * iacc[s])
+                               : (double)((R.nrm + C.nrm) - 2.0f * acc[s]);
+                        if (dd < R.w) {  // id[ii] <- id[jj]
+                            const uint64_t sl = mj_slot(Q, R, C);
+                            Bd[sl] = dd;
+                            Bs[sl] = C.id;
                         }
-                        if (e2) {
-                            const uint64_t sji = m.st[jj] + pair_rank(m.P, mode, m.cls[jj], pj, pi);
-                            Bd[sji] = dd;
-                            Bs[sji] = m.id[ii];
+                        if (dd < C.w) {  // id[jj] <- id[ii]
+                            const uint64_t sl = mj_slot(Q, C, R);
+                            Bd[sl] = dd;
+                            Bs[sl] = R.id;
                         }
                     }
                 }
             }
         }
         __syncwarp();
-        u_cur = u_nxt;
-        w_cur = w_nxt;
+        // ---- rotate the pipeline ------------------------------------------------
+        w0 = w1;
+        u1 = u2;
+        w1 = w2;
+        u2 = u3;
 #pragma unroll
-        for (int b = 0; b < 4; b++) ev[b] = ev_nxt[b];
-        u_nxt = u_nn;
+        for (int b = 0; b < NB; b++) {
+            ev0[b] = ev1[b];
+            ev1[b] = ev2[b];
+            mw0[b] = mw1[b];
+            mn0[b] = mn1[b];
+            mb0[b] = mb1[b];
+        }
     }
 }
 
