@@ -329,6 +329,9 @@ def run_b200(args):
     # tensor-core route) + hood entries (4 B x members) + written update
     # slots (8 B dist + 4 B source per prefilter survivor)
     hbm_peak, peak_kind = peaks()
+    inf = eng.info()
+    join_kernel = ("k_join_mma<u8>" if inf["cert_u8"] else "k_join_mma<fp16>" if inf["cert_dot"]
+                   else "k_join_tiled")
     jk_s = st["join_kernel_ms"] / 1e3
     row_b = st["join_row_bytes"] or 4 * CFG["d"]
     join_bytes = (row_b + 4.0) * st["members"] + 12.0 * st["written_slots"]
@@ -357,7 +360,7 @@ def run_b200(args):
         "recall_at_10": rec,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": "k_join_mma" if st["join_row_bytes"] == 2 * 128 else "k_join_tiled",
+                     "kernel": join_kernel,
                      "bytes_model": "(row_bytes + 4) * sum|M_u| + 12 * written_slots",
                      "bytes_per_step": join_bytes / steps,
                      "kernel_ms_per_step": st["join_kernel_ms"] / steps,

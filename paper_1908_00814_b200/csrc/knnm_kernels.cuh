@@ -1313,7 +1313,7 @@ __device__ __forceinline__ uint64_t mj_slot(const uint8_t *__restrict__ Q, const
 // gathers (worst, norm, bucket offset) and hood i+2's neighbour entries are
 // already loading into registers.
 template <bool U8, int NB>
-__global__ void __launch_bounds__(MJ_WARPS * 32)
+__global__ void __launch_bounds__(MJ_WARPS * 32, 4)
 k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
            const int32_t *__restrict__ nlen, int W, const int8_t *__restrict__ labels, int mode,
            const uint8_t *__restrict__ sub16, int rowb, const float *__restrict__ norms,
@@ -1350,8 +1350,10 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
         }
     };
     // per-member metadata of hood u (independent gathers, issued together)
+    // (results are consumed one hood later: no arithmetic on them here, or
+    // the warp would wait for the loads right away)
     auto gather = [&](int64_t u, int w, const uint32_t (&ev)[NB], double (&mw)[NB], float (&mn)[NB],
-                      uint64_t (&mb)[NB]) {
+                      uint64_t (&mb)[NB], uint32_t (&ms)[NB]) {
 #pragma unroll
         for (int b = 0; b < NB; b++) {
             const int j = b * 32 + (int)lane;
@@ -1359,11 +1361,13 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                 const int id = (int)(ev[b] >> 2);
                 mw[b] = __ldg(worst0 + id);
                 mn[b] = __ldg(norms + id);
-                mb[b] = __ldg(boff + id) + __ldg(start + u * W + j);
+                mb[b] = __ldg(boff + id);
+                ms[b] = __ldg(start + u * W + j);
             } else {
                 mw[b] = 0.0;
                 mn[b] = 0.f;
                 mb[b] = 0;
+                ms[b] = 0;
             }
         }
     };
@@ -1381,7 +1385,8 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
     double mw0[NB];
     float mn0[NB];
     uint64_t mb0[NB];
-    gather(u0, w0, ev0, mw0, mn0, mb0);
+    uint32_t ms0[NB];
+    gather(u0, w0, ev0, mw0, mn0, mb0, ms0);
 
     for (; hi < nactive; hi += stride) {
         const int w = w0;
@@ -1424,9 +1429,10 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                     const int j = b * 32 + (int)lane;
                     bulk_g2s(rows + (size_t)sl * rs, sub16 + (int64_t)id * rowb, row_bytes, bar);
                     const int pk = j | (int)((ev0[b] & 1) << 8) | (c << 9) | ((int)partner_self(mode, c) << 11);
+                    const uint64_t st = mb0[b] + ms0[b];
                     float4 *dst = reinterpret_cast<float4 *>(rec + sl);
                     dst[0] = make_float4(__int_as_float(__double2loint(mw0[b])), __int_as_float(__double2hiint(mw0[b])),
-                                         __int_as_float((int)(uint32_t)mb0[b]), __int_as_float((int)(uint32_t)(mb0[b] >> 32)));
+                                         __int_as_float((int)(uint32_t)st), __int_as_float((int)(uint32_t)(st >> 32)));
                     dst[1] = make_float4(__int_as_float(id), mn0[b], __int_as_float(pk), 0.f);
                 }
             }
@@ -1436,7 +1442,8 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
         double mw1[NB];
         float mn1[NB];
         uint64_t mb1[NB];
-        gather(u1, w1, ev1, mw1, mn1, mb1);
+        uint32_t ms1[NB];
+        gather(u1, w1, ev1, mw1, mn1, mb1, ms1);
         const bool ok2 = hi + 2 * stride < nactive;
         const int w2 = ok2 ? __ldg(nlen + u2) : 0;
         uint32_t ev2[NB];
@@ -1520,6 +1527,7 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
             mw0[b] = mw1[b];
             mn0[b] = mn1[b];
             mb0[b] = mb1[b];
+            ms0[b] = ms1[b];
         }
     }
 }

@@ -95,6 +95,21 @@ def _merge_members(a: np.ndarray, b: np.ndarray, with_overlap: bool = False):
         u = np.union1d(a, b)
         out = (u, _lookup_local(u, a), _lookup_local(u, b))
         return out + (bool(np.intersect1d(a, b).size),) if with_overlap else out
+    na, nb = a.size, b.size
+    top = max(int(a[-1]) if na else -1, int(b[-1]) if nb else -1) + 1
+    if na and nb and int(min(a[0], b[0])) >= 0 and top <= 4 * (na + nb):
+        # dense id range: O(range) marker pass instead of a sort
+        mark = np.zeros(top, dtype=np.int8)
+        mark[a] = 1
+        mark[b] += 2
+        nz = mark != 0
+        pos = np.cumsum(nz, dtype=np.int32) - 1
+        out = (np.flatnonzero(nz).astype(np.result_type(a, b), copy=False), pos[a], pos[b])
+        shared = bool(np.any(mark[b] == 3))
+        if with_overlap:
+            return out + (shared,)
+        if not shared:  # (shared ids keep the sort path's behaviour below)
+            return out
     cat = np.concatenate((a, b))
     order = np.argsort(cat, kind="stable")
     srt = cat[order]
