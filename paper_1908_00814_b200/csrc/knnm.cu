@@ -281,9 +281,10 @@ int ensure_memb(knnm_ctx *c, uint64_t recs, uint64_t starts) {
 
 // Membership ranking: moff = scan(mcount); bucket memberships by row (fill
 // kernel launched by the caller between the two halves); then k_seg_rank.
-int rank_memberships(knnm_ctx *c) {
+int rank_memberships(knnm_ctx *c, bool fused = false) {
     k_seg_rank<<<grid_for(c, c->n * 32, SEG_WARPS * 32, 16), SEG_WARPS * 32, 0, c->st>>>(
-        c->n, c->moff.as<uint32_t>(), c->memb.as<MembRec>(), c->start.as<uint32_t>());
+        c->n, c->moff.as<uint32_t>(), c->memb.as<MembRec>(), c->start.as<uint32_t>(),
+        fused ? c->roff.as<uint32_t>() : nullptr, c->k + 1, c->mcount.as<uint32_t>());
     CKL();
     return KNNM_OK;
 }
@@ -1052,6 +1053,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
     int W = k + rev_cap;
     // owned rows: all of them, or the shard set by knnm_set_shard
     const int64_t lo = local_only ? c->shard_lo : 0;
+    bool fused_memb = false;  // k_assemble writes the membership records
     const int64_t hi = local_only ? (c->shard_hi < 0 ? n : c->shard_hi) : n;
     unsigned long long *cnt = c->counters.as<unsigned long long>();
     CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
@@ -1100,13 +1102,18 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         }
         CK(cudaMemsetAsync(c->bound.p, 0, sizeof(uint32_t) * (n + 1), c->st));
         CK(cudaMemsetAsync(c->mcount.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+        // membership records written by k_assemble itself (unsharded rounds):
+        // row x's segment holds indeg(x) + k + 1 records (see k_assemble)
+        fused_memb = !local_only && lo == 0 && hi == n;
+        if (fused_memb) TRY(ensure_memb(c, (uint64_t)n * (uint64_t)(2 * k + 1), (uint64_t)n * W));
         k_assemble<<<grid_for(c, (hi - lo) * 32, ASM_WARPS * 32, 16), ASM_WARPS * 32, 0, c->st>>>(
             c->ids.as<int32_t>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
             c->dists.as<double>(), hi, k, rev_cap, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(),
             round_seed, c->labels.as<int8_t>(), mode, W, c->nbh.as<uint32_t>(),
             c->nlen.as<int32_t>(), c->hpairs.as<uint32_t>(), c->worst0.as<double>(),
             c->active.as<int32_t>(), cnt, lo, c->bound.as<uint32_t>(), c->mcount.as<uint32_t>(),
-            (!local_only && c->have_order) ? c->order.as<int32_t>() : nullptr);
+            (!local_only && c->have_order) ? c->order.as<int32_t>() : nullptr,
+            fused_memb ? c->memb.as<MembRec>() : nullptr);
         CKL();
         TRY(scan<uint32_t, uint64_t>(c, c->hpairs.as<uint32_t>(), c->poff.as<uint64_t>(), n));
     }
@@ -1168,7 +1175,9 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                 PhaseTimer pt(c, PH_JOIN);
                 // reference-order slot layout (see MembRec in knnm_kernels.cuh);
                 // k_assemble already counted every active hood's memberships
-                CK(cudaMemsetAsync(c->mcur.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+                // (and, when fused, wrote their records)
+                const bool fused = counted && fused_memb;
+                if (!fused) CK(cudaMemsetAsync(c->mcur.p, 0, sizeof(uint32_t) * (n + 1), c->st));
                 const int hgrid = grid_for(c, nact * 32, 256, 16);
                 if (!counted) {
                     CK(cudaMemsetAsync(c->bound.p, 0, sizeof(uint32_t) * (n + 1), c->st));
@@ -1180,15 +1189,17 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                     CKL();
                 }
                 TRY(scan<uint32_t, uint64_t>(c, c->bound.as<uint32_t>(), c->boff.as<uint64_t>(), n));
-                TRY(scan<uint32_t, uint32_t>(c, c->mcount.as<uint32_t>(), c->moff.as<uint32_t>(), n));
-                TRY(ensure_memb(c, (uint64_t)n * W, (uint64_t)n * W));
                 TRY(ensure_slots(c, pairs2));
-                k_hood_memb<true><<<hgrid, 256, 0, c->st>>>(
-                    act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
-                    c->labels.as<int8_t>(), mode, nullptr, nullptr, c->moff.as<uint32_t>(),
-                    c->mcur.as<uint32_t>(), c->memb.as<MembRec>());
-                CKL();
-                TRY(rank_memberships(c));
+                if (!fused) {
+                    TRY(scan<uint32_t, uint32_t>(c, c->mcount.as<uint32_t>(), c->moff.as<uint32_t>(), n));
+                    TRY(ensure_memb(c, (uint64_t)n * W, (uint64_t)n * W));
+                    k_hood_memb<true><<<hgrid, 256, 0, c->st>>>(
+                        act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
+                        c->labels.as<int8_t>(), mode, nullptr, nullptr, c->moff.as<uint32_t>(),
+                        c->mcur.as<uint32_t>(), c->memb.as<MembRec>());
+                    CKL();
+                }
+                TRY(rank_memberships(c, fused));
                 const uint64_t *boff = c->boff.as<uint64_t>();
                 const uint32_t *stt = c->start.as<uint32_t>();
                 double *Bd = c->Bd.as<double>();

@@ -614,7 +614,8 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
            const uint32_t *__restrict__ roff, const uint32_t *__restrict__ rev, uint64_t seed,
            const int8_t *__restrict__ labels, int mode, int W, uint32_t *nbh, int32_t *nlen,
            uint32_t *hpairs, double *worst0, int32_t *active, unsigned long long *counters,
-           int64_t lo, uint32_t *bound, uint32_t *mcount, const int32_t *__restrict__ order) {
+           int64_t lo, uint32_t *bound, uint32_t *mcount, const int32_t *__restrict__ order,
+           MembRec *memb) {
     __shared__ uint32_t s_seg[ASM_WARPS][WARP_REV_MAX];
     __shared__ uint32_t s_idx[ASM_WARPS][WARP_REV_MAX];
     __shared__ uint32_t s_R[ASM_WARPS][MAX_W];
@@ -713,8 +714,16 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
                 for (int c = 0; c < 4; c++)
                     if (mk & (1 << c)) part += cnt4[c];
                 if (part > 0) {
-                    atomicAdd(&bound[e >> 2], (uint32_t)part);
-                    atomicAdd(&mcount[e >> 2], 1u);
+                    const uint32_t x = e >> 2;
+                    atomicAdd(&bound[x], (uint32_t)part);
+                    const uint32_t at = atomicAdd(&mcount[x], 1u);
+                    // fused membership record (unsharded, unchunked rounds):
+                    // row x lies in at most indeg(x) + k hoods (x in fwd(u)
+                    // <=> u in rev(x); x in rev(u) <=> u in fwd(x)), so its
+                    // records fit the segment at roff[x] + x * (k + 1)
+                    if (memb)
+                        memb[roff[x] + x * (uint32_t)(k + 1) + at] =
+                            MembRec{(uint64_t)u, (uint32_t)part, (uint32_t)(u * W + j)};
                 }
             }
         }
@@ -1673,17 +1682,52 @@ __global__ void k_directed_memb(const int32_t *__restrict__ rows, int64_t m, uin
 constexpr int SEG_WARPS = 8;
 __global__ void __launch_bounds__(SEG_WARPS * 32)
 k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restrict__ memb,
-           uint32_t *__restrict__ start) {
+           uint32_t *__restrict__ start, const uint32_t *__restrict__ roff, int kp1,
+           const uint32_t *__restrict__ mcount) {
     __shared__ uint64_t s_key[SEG_WARPS][SEG_SMEM];
     __shared__ uint32_t s_wt[SEG_WARPS][SEG_SMEM];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * SEG_WARPS;
-    for (int64_t r = (int64_t)blockIdx.x * SEG_WARPS + wib; r < n; r += nw) {
-        const uint32_t lo = moff[r];
-        const int m = (int)(moff[r + 1] - lo);
+    // rows with m <= 32 memberships (almost all): one membership per lane in
+    // registers, ranked by a shuffle loop; the next row's segment is loaded
+    // while the current one is ranked (the kernel is load-latency bound)
+    // (pipeline: offsets two rows ahead, records one row ahead)
+    // segment of row x: [moff[x], moff[x+1]) (compacted), or the fused
+    // fixed-capacity segment [roff[x] + x * kp1, + mcount[x]) (k_assemble)
+    auto seg = [&](int64_t x, uint32_t &a, uint32_t &b) {
+        if (roff) {
+            a = roff[x] + (uint32_t)x * (uint32_t)kp1;
+            b = a + mcount[x];
+        } else {
+            a = moff[x];
+            b = moff[x + 1];
+        }
+    };
+    int64_t r = (int64_t)blockIdx.x * SEG_WARPS + wib;
+    uint32_t lo1 = 0, hi1 = 0, lo2 = 0, hi2 = 0;
+    MembRec rec1 = MembRec{0, 0, 0};
+    if (r < n) {
+        seg(r, lo1, hi1);
+        if (lane < hi1 - lo1) rec1 = memb[lo1 + lane];
+    }
+    if (r + nw < n) seg(r + nw, lo2, hi2);
+    for (; r < n; r += nw) {
+        const uint32_t lo = lo1;
+        const int m = (int)(hi1 - lo1);
+        const MembRec rec = rec1;
+        lo1 = lo2;
+        hi1 = hi2;
+        rec1 = (r + nw < n && lane < hi1 - lo1) ? memb[lo1 + lane] : MembRec{0, 0, 0};
+        if (r + 2 * nw < n) seg(r + 2 * nw, lo2, hi2);
         if (m == 0) continue;
-        if (m == 1) {
-            if (lane == 0) start[memb[lo].out] = 0;
+        if (m <= 32) {
+            uint32_t acc = 0;
+            for (int f = 0; f < m; f++) {
+                const uint64_t kf = __shfl_sync(FULL_MASK, rec.key, f);
+                const uint32_t wf = __shfl_sync(FULL_MASK, rec.weight, f);
+                acc += kf < rec.key ? wf : 0u;
+            }
+            if ((int)lane < m) start[rec.out] = acc;
             continue;
         }
         if (m <= SEG_SMEM) {
