@@ -325,16 +325,19 @@ def run_b200(args):
 
     # roofline of the dominant kernel (the local join, timed alone with CUDA
     # events on the engine stream): algorithmic bytes per launch / time.
-    # bytes = gathered member rows (sum |M_u| x row bytes: fp16 rows on the
-    # tensor-core route) + hood entries (4 B x members) + written update
-    # slots (8 B dist + 4 B source per prefilter survivor)
+    # bytes = gathered member rows (sum |M_u| x row bytes: u8 / fp16 rows on
+    # the tensor-core route) + hood entries (4 B x members) + written update
+    # slots (one packed 8 B record on certified routes, else 8 B dist + 4 B
+    # source, per prefilter survivor)
     hbm_peak, peak_kind = peaks()
     inf = eng.info()
     join_kernel = ("k_join_mma<u8>" if inf["cert_u8"] else "k_join_mma<fp16>" if inf["cert_dot"]
                    else "k_join_tiled")
     jk_s = st["join_kernel_ms"] / 1e3
     row_b = st["join_row_bytes"] or 4 * CFG["d"]
-    join_bytes = (row_b + 4.0) * st["members"] + 12.0 * st["written_slots"]
+    # packed 8-byte slots on the certified routes, f64 + int32 otherwise
+    slot_b = 8.0 if (inf["cert"] or inf["cert_dot"]) else 12.0
+    join_bytes = (row_b + 4.0) * st["members"] + slot_b * st["written_slots"]
     achieved = join_bytes / jk_s / 1e9 if jk_s > 0 else 0.0
     traffic = None
     try:
@@ -361,7 +364,7 @@ def run_b200(args):
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
                      "kernel": join_kernel,
-                     "bytes_model": "(row_bytes + 4) * sum|M_u| + 12 * written_slots",
+                     "bytes_model": f"(row_bytes + 4) * sum|M_u| + {int(slot_b)} * written_slots",
                      "bytes_per_step": join_bytes / steps,
                      "kernel_ms_per_step": st["join_kernel_ms"] / steps,
                      "kernel_share_of_step": st["join_kernel_ms"] / max(ms_max, 1e-9)},

@@ -102,7 +102,7 @@ struct knnm_ctx {
     bool cert = false;  // fp32 arithmetic is exact for this dataset + metric
     bool cert_dot = false;  // fp16 rows + fp32 dot products are exact (L2)
     DBuf nrm64;             // exact fp64 squared norm of every subset row (cosine)
-    bool slots_lazy = false;  // this round's slots may hold approximations (LazyExact)
+    int slots_mode = SLOTS_PLAIN;  // format of the slots the next apply reads
     bool cert_u8 = false;   // entries are integers in [0, 255]: u8 rows, s32 MMA
     int dph = 0;            // fp16 row length (multiple of 16)
     int rowb = 0;           // staged bytes per row for the tensor-core join
@@ -324,11 +324,13 @@ int run_updates(knnm_ctx *c) {
         c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), \
         cnt, lazy_of(c))
     if (E == 1) {
-        if (c->slots_lazy) KNNM_AP_LAUNCH(1, true);
-        else KNNM_AP_LAUNCH(1, false);
+        if (c->slots_mode == SLOTS_LAZY) KNNM_AP_LAUNCH(1, SLOTS_LAZY);
+        else if (c->slots_mode == SLOTS_PACKED) KNNM_AP_LAUNCH(1, SLOTS_PACKED);
+        else KNNM_AP_LAUNCH(1, SLOTS_PLAIN);
     } else {
-        if (c->slots_lazy) KNNM_AP_LAUNCH(2, true);
-        else KNNM_AP_LAUNCH(2, false);
+        if (c->slots_mode == SLOTS_LAZY) KNNM_AP_LAUNCH(2, SLOTS_LAZY);
+        else if (c->slots_mode == SLOTS_PACKED) KNNM_AP_LAUNCH(2, SLOTS_PACKED);
+        else KNNM_AP_LAUNCH(2, SLOTS_PLAIN);
     }
 #undef KNNM_AP_LAUNCH
     CKL();
@@ -648,7 +650,7 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     PhaseTimer pt(c, PH_OTHER);
     c->n = n;
     c->k = k;
-    c->slots_lazy = false;
+    c->slots_mode = SLOTS_PLAIN;
     TRY(ensure(c->ugid, sizeof(int64_t) * n));
     TRY(h2d(c, c->ugid.p, union_gids, sizeof(int64_t) * n));
     bool identity = (n == c->n_all && union_gids[0] == 0 && union_gids[n - 1] == n - 1);
@@ -847,6 +849,7 @@ static int insert_impl(knnm_ctx *c, const int32_t *rows, int64_t mrows, int32_t 
         }
         {
             PhaseTimer pt(c, PH_UPDATE);
+            c->slots_mode = SLOTS_PLAIN;  // k_directed_emit writes Bd/Bs
             TRY(run_updates(c));
         }
         acc_total += (int64_t)c->hcnt[C_ACCEPTED];
@@ -1047,7 +1050,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
     if (mode < 0 || mode > 2) return fail(KNNM_ERR_ARG, "mode %d", mode);
     if (rev_cap < 0 || rev_cap > c->k) return fail(KNNM_ERR_ARG, "rev_cap %d", rev_cap);
     CK(cudaSetDevice(c->device));
-    c->slots_lazy = false;  // set by a lazy join below
+    c->slots_mode = SLOTS_PLAIN;  // set by the join route below
     int64_t n = c->n;
     int k = c->k;
     int W = k + rev_cap;
@@ -1207,6 +1210,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                 PhaseTimer ptk(c, PH_JOINK);  // the local-join kernel alone (roofline)
                 if (use_mma) {
                     int per_sm = 1;
+                    c->slots_mode = SLOTS_PACKED;
                     // 32-entry position blocks per hood
                     const int nb = W <= 32 ? 1 : W <= 64 ? 2 : 4;
                     const void *fn;
@@ -1238,7 +1242,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                     // evaluation is deferred to the apply (LazyExact), which
                     // needs it for few slots only
                     const bool lazy = !c->cert && c->d > LAZY_MIN_D;
-                    c->slots_lazy = c->slots_lazy || lazy;
+                    c->slots_mode = c->cert ? SLOTS_PACKED : lazy ? SLOTS_LAZY : SLOTS_PLAIN;
                     const void *fn;
                     if (c->cert) fn = c->metric == 1 ? (const void *)k_join_tiled<1, true, false>
                                                      : (const void *)k_join_tiled<0, true, false>;
@@ -1273,6 +1277,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
 #undef KNNM_TJ_LAUNCH
 #undef KNNM_TJ_ARGS
                 } else {
+                    c->slots_mode = SLOTS_PLAIN;
 #define KNNM_JE_ARGS                                                                          \
     act, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,       \
         c->subp, c->dp, c->d, c->worst0.as<double>(), boff, stt, Bd, Bs
@@ -1409,11 +1414,13 @@ int knnm_round_apply(knnm_ctx *c, int32_t nsrc, const uint32_t *recv_cnt, const 
         lo, no, c->k, nsrc, off, recv_cnt, recv_Bd, recv_Bs, c->ids.as<int32_t>(),             \
         c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), cnt, lazy_of(c))
     if (E == 1) {
-        if (c->slots_lazy) KNNM_APM_LAUNCH(1, true);
-        else KNNM_APM_LAUNCH(1, false);
+        if (c->slots_mode == SLOTS_LAZY) KNNM_APM_LAUNCH(1, SLOTS_LAZY);
+        else if (c->slots_mode == SLOTS_PACKED) KNNM_APM_LAUNCH(1, SLOTS_PACKED);
+        else KNNM_APM_LAUNCH(1, SLOTS_PLAIN);
     } else {
-        if (c->slots_lazy) KNNM_APM_LAUNCH(2, true);
-        else KNNM_APM_LAUNCH(2, false);
+        if (c->slots_mode == SLOTS_LAZY) KNNM_APM_LAUNCH(2, SLOTS_LAZY);
+        else if (c->slots_mode == SLOTS_PACKED) KNNM_APM_LAUNCH(2, SLOTS_PACKED);
+        else KNNM_APM_LAUNCH(2, SLOTS_PLAIN);
     }
 #undef KNNM_APM_LAUNCH
     CKL();

@@ -731,6 +731,18 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
     if (lane == 0 && members) atomicAdd(&counters[C_MEMBERS], members);
 }
 
+// Update-slot formats.  PLAIN: Bd f64 distance + Bs int32 source.  LAZY:
+// PLAIN, where the sign bit marks an fp32 approximation (LazyExact).
+// PACKED (certified routes, whose distances are integers < 2^24 and hence
+// exact in fp32): one u64 per slot in the Bd buffer, fp32 distance bits in
+// the high word, source row in the low word -- one store per update.  The
+// all-ones prefill reads as NaN in every format ("cannot pass").
+constexpr int SLOTS_PLAIN = 0, SLOTS_LAZY = 1, SLOTS_PACKED = 2;
+
+__device__ __forceinline__ unsigned long long pack_slot(double d, int src) {
+    return ((unsigned long long)__float_as_uint((float)d) << 32) | (uint32_t)src;
+}
+
 // ---------------------------------------------------------------------------
 // Local join, exact route (_kernels.py:402-437 pair enumeration +
 // _kernels.py:113-119 distances + the candidate side of
@@ -1134,9 +1146,13 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
                 if (!pair_ok(live, ii, jj, r1, c1, tri)) continue;
                 const float f = acc[s >> 1][s & 1];
                 if (CERT) {
-                    // every fp32 value is exact
+                    // every fp32 value is exact: packed slots
                     const double dd = (double)f;
-                    if (dd < s_w[ii] || dd < s_w[jj]) emit(ii, jj, dd, dd);
+                    unsigned long long *Bp = reinterpret_cast<unsigned long long *>(Bd);
+                    if (dd < s_w[ii])
+                        Bp[s_st[ii] + pair_rank(s_P, mode, s_sc[ii], s_pos[ii], s_pos[jj])] = pack_slot(dd, s_id[jj]);
+                    if (dd < s_w[jj])
+                        Bp[s_st[jj] + pair_rank(s_P, mode, s_sc[jj], s_pos[jj], s_pos[ii])] = pack_slot(dd, s_id[ii]);
                 } else {
                     // LAZY: store the approximation (sign bit set); the apply
                     // evaluates it exactly only if it can still pass
@@ -1509,16 +1525,9 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                         const double dd =
                             U8 ? (double)((__float_as_int(R.nrm) + __float_as_int(C.nrm)) - 2 * iacc[s])
                                : (double)((R.nrm + C.nrm) - 2.0f * acc[s]);
-                        if (dd < R.w) {  // id[ii] <- id[jj]
-                            const uint64_t sl = mj_slot(Q, R, C);
-                            Bd[sl] = dd;
-                            Bs[sl] = C.id;
-                        }
-                        if (dd < C.w) {  // id[jj] <- id[ii]
-                            const uint64_t sl = mj_slot(Q, C, R);
-                            Bd[sl] = dd;
-                            Bs[sl] = R.id;
-                        }
+                        unsigned long long *Bp = reinterpret_cast<unsigned long long *>(Bd);
+                        if (dd < R.w) Bp[mj_slot(Q, R, C)] = pack_slot(dd, C.id);  // id[ii] <- id[jj]
+                        if (dd < C.w) Bp[mj_slot(Q, C, R)] = pack_slot(dd, R.id);  // id[jj] <- id[ii]
                     }
                 }
             }
@@ -1793,11 +1802,12 @@ constexpr int APPLY_WARPS = 4;
 // step (coalesced), candidates that cannot pass the current worst are
 // skipped by ballot, the rest go through warp_insert in slot order -- which
 // is the reference's sequential order, so no sorting is needed.
-template <int E, bool LAZY>
+template <int E, int MODE>
 __global__ void __launch_bounds__(APPLY_WARPS * 32)
 k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double *__restrict__ Bd,
                const int32_t *__restrict__ Bs, int32_t *ids, double *dists, uint8_t *flags,
                int32_t *sizes, unsigned long long *counters, LazyExact z) {
+    constexpr bool LAZY = MODE == SLOTS_LAZY;
     __shared__ double s_lz[LAZY ? APPLY_WARPS : 1][LAZY ? LZ_G * LZ_S : 1];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * APPLY_WARPS;
@@ -1826,6 +1836,14 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
                 dl = lazy_resolve<E>(s, k, j < ns, dl, Bs, lo + j, z, src, need);
                 if (__any_sync(FULL_MASK, need)) lazy_warp_eval(z, r, need, src, dl, s_lz[wib], lane, nexact);
                 if (!__any_sync(FULL_MASK, dl < inf)) continue;
+            } else if (MODE == SLOTS_PACKED) {
+                const unsigned long long v = __double_as_longlong(dl);
+                const float f = __uint_as_float((uint32_t)(v >> 32));
+                dl = f != f ? inf : (double)f;
+                if (j < ns && f == f) written++;
+                const bool pre = j < ns && (dl < s.worst || (s.sz < k && dl < inf));
+                if (!__any_sync(FULL_MASK, pre)) continue;
+                src = (int)(uint32_t)v;
             } else {
                 if (dl != dl) dl = inf;
                 else if (j < ns) written++;
@@ -1863,12 +1881,13 @@ __global__ void k_worst0_all(const int32_t *__restrict__ sizes, const double *__
 // source rank; blocks are processed in source order, which is hood order,
 // which is the reference's order.  off[s * (no+1) + i] = element offset of
 // row lo+i's segment in the receive buffers.
-template <int E, bool LAZY>
+template <int E, int MODE>
 __global__ void __launch_bounds__(APPLY_WARPS * 32)
 k_apply_stream_multi(int64_t lo, int64_t no, int k, int nsrc, const uint64_t *__restrict__ off,
                      const uint32_t *__restrict__ cnt, const double *__restrict__ Bd,
                      const int32_t *__restrict__ Bs, int32_t *ids, double *dists, uint8_t *flags,
                      int32_t *sizes, unsigned long long *counters, LazyExact z) {
+    constexpr bool LAZY = MODE == SLOTS_LAZY;
     __shared__ double s_lz[LAZY ? APPLY_WARPS : 1][LAZY ? LZ_G * LZ_S : 1];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * APPLY_WARPS;
@@ -1894,6 +1913,13 @@ k_apply_stream_multi(int64_t lo, int64_t no, int k, int nsrc, const uint64_t *__
                     dl = lazy_resolve<E>(st, k, j < ns, dl, Bs, base + j, z, src, need);
                     if (__any_sync(FULL_MASK, need)) lazy_warp_eval(z, r, need, src, dl, s_lz[wib], lane, nexact);
                     if (!__any_sync(FULL_MASK, dl < inf)) continue;
+                } else if (MODE == SLOTS_PACKED) {
+                    const unsigned long long v = __double_as_longlong(dl);
+                    const float f = __uint_as_float((uint32_t)(v >> 32));
+                    dl = f != f ? inf : (double)f;
+                    const bool pre = j < ns && (dl < st.worst || (st.sz < k && dl < inf));
+                    if (!__any_sync(FULL_MASK, pre)) continue;
+                    src = (int)(uint32_t)v;
                 } else {
                     if (dl != dl) dl = inf;
                     const bool pre = j < ns && (dl < st.worst || (st.sz < k && dl < inf));
