@@ -193,7 +193,9 @@ int knnm_round(knnm_ctx *ctx, int32_t mode, int32_t rev_cap,
  * the reference's order): recv_cnt (nsrc, hi-lo) u32 device array,
  * recv_base host array of nsrc element offsets of each block in recv_Bd /
  * recv_Bs (device).  knnm_local_views / knnm_state_views expose device
- * pointers for the collectives. */
+ * pointers for the collectives; knnm_local_views returns Bs = NULL when the
+ * round's slots are packed (one u64 per slot in Bd: fp32 distance bits in
+ * the high word, source row in the low word; recv_Bs is then ignored). */
 int knnm_set_shard(knnm_ctx *ctx, int64_t lo, int64_t hi);
 int knnm_round_local(knnm_ctx *ctx, int32_t mode, int32_t rev_cap,
                      uint64_t round_seed, int64_t *pairs_local);

@@ -1382,7 +1382,8 @@ int knnm_local_views(knnm_ctx *c, void **cnt, void **boff, void **Bd, void **Bs)
     if (cnt) *cnt = c->bound.p;
     if (boff) *boff = c->boff.p;
     if (Bd) *Bd = c->Bd.p;
-    if (Bs) *Bs = c->Bs.p;
+    // packed slots carry the source row in Bd: nothing to exchange in Bs
+    if (Bs) *Bs = c->slots_mode == SLOTS_PACKED ? nullptr : c->Bs.p;
     return KNNM_OK;
 }
 

@@ -89,9 +89,10 @@ class ShardEngine:
                                         ctypes.byref(bd), ctypes.byref(bs)), "knnm_local_views")
         boff_t = _view(boff.value, (n + 1,), "<i8", self.device)
         total = int(boff_t[n].item())
+        # Bs is None when the slots are packed (source row inside Bd)
         return (_view(cnt.value, (n,), "<i4", self.device), boff_t,
                 _view(bd.value, (max(total, 0),), "<f8", self.device),
-                _view(bs.value, (max(total, 0),), "<i4", self.device))
+                None if bs.value is None else _view(bs.value, (max(total, 0),), "<i4", self.device))
 
     def round_apply(self, recv_cnt, recv_base, recv_bd, recv_bs) -> int:
         acc = ctypes.c_int64()
@@ -221,11 +222,14 @@ def sharded_rounds(shards, comm, n, k, mode, params, rng, counter, report, rev_c
             parts = []
             for (lo, hi) in bounds:
                 a, b = int(boff_h[lo]), int(boff_h[hi])
-                parts.append((cnt[lo:hi], bd[a:b], bs[a:b]))
+                parts.append((cnt[lo:hi], bd[a:b], None if bs is None else bs[a:b]))
             sends[r] = parts
         recv_cnt = comm.alltoallv({r: [p[0] for p in sends[r]] for r in comm.local_ranks})
         recv_bd = comm.alltoallv({r: [p[1] for p in sends[r]] for r in comm.local_ranks})
-        recv_bs = comm.alltoallv({r: [p[2] for p in sends[r]] for r in comm.local_ranks})
+        # packed slots (certified routes) carry the source row inside Bd
+        packed = all(sends[r][0][2] is None for r in comm.local_ranks)
+        recv_bs = None if packed else \
+            comm.alltoallv({r: [p[2] for p in sends[r]] for r in comm.local_ranks})
         acc_l = {}
         for q in comm.local_ranks:
             sizes = [int(t.numel()) for t in recv_bd[q]]
@@ -233,7 +237,8 @@ def sharded_rounds(shards, comm, n, k, mode, params, rng, counter, report, rev_c
             rc = torch.cat([t.reshape(-1) for t in recv_cnt[q]]).contiguous()
             rb = torch.cat([t.reshape(-1) for t in recv_bd[q]]).contiguous() if sum(sizes) else \
                 torch.empty(1, dtype=torch.float64, device=shards[q].device)
-            rs = torch.cat([t.reshape(-1) for t in recv_bs[q]]).contiguous() if sum(sizes) else \
+            rs = torch.cat([t.reshape(-1) for t in recv_bs[q]]).contiguous() \
+                if (recv_bs is not None and sum(sizes)) else \
                 torch.empty(1, dtype=torch.int32, device=shards[q].device)
             acc_l[q] = shards[q].round_apply(rc, base, rb, rs)
         fulls = {r: list(shards[r].state_views(n, k)) for r in comm.local_ranks}
