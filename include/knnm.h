@@ -163,6 +163,14 @@ int knnm_draws_regen(knnm_ctx *ctx, const uint64_t *pcg, int32_t has_uint32,
                      uint32_t uinteger, uint64_t m, const int64_t *rows,
                      int64_t nrows, int64_t *consumed, int64_t *bad, int64_t *nbad);
 
+/* Host-side (no context, no GPU): union of two strictly ascending id arrays
+ * and each input's row in it (merge.py:217-221 np.union1d + searchsorted,
+ * one linear pass).  uni needs na + nb entries; *nu = union size; *shared =
+ * whether the inputs share an id (merge.py:181 disjointness check). */
+int knnm_merge_members(const int64_t *a, int64_t na, const int64_t *b, int64_t nb,
+                       int64_t *uni, int32_t *rows_a, int32_t *rows_b, int64_t *nu,
+                       int32_t *shared);
+
 /* Host-side (no context, no GPU): nrows successive
  * sample_distinct(rng, n, k, exclude=exclude[r]) draws (core.py:222-230,
  * numpy Generator.choice(pool, k, replace=False)) from the PCG64 state

@@ -1491,6 +1491,45 @@ int knnm_bf_topk(knnm_ctx *c, const float *queries, const int64_t *rows, int64_t
     return KNNM_OK;
 }
 
+int knnm_merge_members(const int64_t *a, int64_t na, const int64_t *b, int64_t nb, int64_t *uni,
+                       int32_t *rows_a, int32_t *rows_b, int64_t *nu, int32_t *shared) {
+    if ((na > 0 && (!a || !rows_a)) || (nb > 0 && (!b || !rows_b)) || !uni || !nu)
+        return fail(KNNM_ERR_ARG, "bad argument");
+    if (na + nb >= (1ll << 31)) return fail(KNNM_ERR_LIMIT, "union too large");
+    for (int64_t i = 1; i < na; i++)
+        if (a[i] <= a[i - 1]) return fail(KNNM_ERR_ARG, "ids must be strictly ascending");
+    for (int64_t i = 1; i < nb; i++)
+        if (b[i] <= b[i - 1]) return fail(KNNM_ERR_ARG, "ids must be strictly ascending");
+    // two-pointer merge of ascending runs (np.union1d + np.searchsorted),
+    // branch-free: both rows are written every step and only the side(s)
+    // holding the smaller id advance, so each row's last write is its own
+    // (a shared id yields one union entry that both rows point at)
+    int64_t i = 0, j = 0, o = 0;
+    int32_t sh = 0;
+    while (i < na && j < nb) {
+        const int64_t x = a[i], y = b[j];
+        const int ta = x <= y, tb = y <= x;
+        uni[o] = ta ? x : y;
+        rows_a[i] = (int32_t)o;
+        rows_b[j] = (int32_t)o;
+        sh |= ta & tb;
+        i += ta;
+        j += tb;
+        o++;
+    }
+    for (; i < na; i++) {
+        uni[o] = a[i];
+        rows_a[i] = (int32_t)o++;
+    }
+    for (; j < nb; j++) {
+        uni[o] = b[j];
+        rows_b[j] = (int32_t)o++;
+    }
+    *nu = o;
+    if (shared) *shared = sh;
+    return KNNM_OK;
+}
+
 int knnm_sample_distinct_rows(uint64_t *pcg, int32_t *has_uint32, uint32_t *uinteger, int64_t n,
                               int32_t k, const int32_t *exclude, int64_t nrows, int64_t *out) {
     if (!pcg || !has_uint32 || !uinteger || !out || (nrows > 0 && !exclude) || k < 0)

@@ -96,6 +96,25 @@ def _merge_members(a: np.ndarray, b: np.ndarray, with_overlap: bool = False):
         out = (u, _lookup_local(u, a), _lookup_local(u, b))
         return out + (bool(np.intersect1d(a, b).size),) if with_overlap else out
     na, nb = a.size, b.size
+    if a.dtype == np.int64 and b.dtype == np.int64:
+        # native linear merge (libknnm.so, host-only)
+        import ctypes
+
+        from . import _lib
+
+        a = np.ascontiguousarray(a)
+        b = np.ascontiguousarray(b)
+        uni = np.empty(na + nb, dtype=np.int64)
+        ra = np.empty(na, dtype=np.int32)
+        rb = np.empty(nb, dtype=np.int32)
+        nu, sh = ctypes.c_int64(), ctypes.c_int32()
+        _lib.check(_lib.load().knnm_merge_members(_lib.ptr(a), na, _lib.ptr(b), nb, _lib.ptr(uni),
+                                                  _lib.ptr(ra), _lib.ptr(rb), ctypes.byref(nu),
+                                                  ctypes.byref(sh)), "knnm_merge_members")
+        if with_overlap:
+            return uni[: nu.value], ra, rb, bool(sh.value)
+        if not sh.value:
+            return uni[: nu.value], ra, rb
     top = max(int(a[-1]) if na else -1, int(b[-1]) if nb else -1) + 1
     if na and nb and int(min(a[0], b[0])) >= 0 and top <= 4 * (na + nb):
         # dense id range: O(range) marker pass instead of a sort

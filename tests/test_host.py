@@ -129,3 +129,30 @@ def test_native_sample_distinct_rows_matches_numpy(n, k):
     got = sample_distinct_rows(b, n, k, rows)
     assert np.array_equal(got, want)
     assert a.bit_generator.state == b.bit_generator.state
+
+
+@pytest.mark.parametrize("a,b", [([1, 3, 5], [2, 3, 9]), ([], [4, 5]), ([7], []), ([1, 2], [3, 4]),
+                                 ([3, 4], [1, 2]), ([], [])])
+def test_native_merge_members(a, b):
+    """Union + rows (np.union1d + searchsorted, merge.py:217-221) and the
+    shared-id flag from the native linear merge."""
+    from paper_1908_00814_b200.merge import _merge_members
+
+    a = np.array(a, dtype=np.int64)
+    b = np.array(b, dtype=np.int64)
+    u, ra, rb, shared = _merge_members(a, b, with_overlap=True)
+    want = np.union1d(a, b)
+    assert np.array_equal(u, want)
+    assert np.array_equal(ra, np.searchsorted(want, a))
+    assert np.array_equal(rb, np.searchsorted(want, b))
+    assert shared == bool(np.intersect1d(a, b).size)
+
+
+def test_native_merge_members_large():
+    from paper_1908_00814_b200.merge import _merge_members
+
+    perm = np.random.default_rng(3).permutation(200_000)
+    a, b = np.sort(perm[:90_000]).astype(np.int64), np.sort(perm[90_000:]).astype(np.int64)
+    u, ra, rb = _merge_members(a, b)
+    assert np.array_equal(u, np.union1d(a, b))
+    assert np.array_equal(u[ra], a) and np.array_equal(u[rb], b)
