@@ -644,6 +644,7 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     if (n < 1) return fail(KNNM_ERR_ARG, "empty union");
     if (k < 1 || k > 64) return fail(KNNM_ERR_LIMIT, "k=%d outside [1, 64]", k);
     if ((uint64_t)n * (uint64_t)k >= (1ull << 31)) return fail(KNNM_ERR_LIMIT, "n*k too large");
+    if (n >= (1ll << 30)) return fail(KNNM_ERR_LIMIT, "n must be below 2^30");  // WarpRow id packing
     if (union_gids[0] < 0 || union_gids[n - 1] >= c->n_all)
         return fail(KNNM_ERR_ARG, "union ids outside the dataset");
     CK(cudaSetDevice(c->device));

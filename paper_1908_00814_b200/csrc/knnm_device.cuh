@@ -211,9 +211,8 @@ __device__ __forceinline__ void warp_sort_reg(T (&v)[NE], unsigned lane) {
 // ---------------------------------------------------------------------------
 template <int E>
 struct WarpRow {
-    int id[E];
+    int idf[E];  // (id << 1) | new-flag: one register moves both (ids < 2^30)
     double d[E];
-    int fl[E];
     int sz;
     double worst;  // dists[k-1] when sz == k
 };
@@ -226,13 +225,11 @@ __device__ __forceinline__ void row_load(WarpRow<E> &s, const int32_t *ids, cons
     for (int e = 0; e < E; e++) {
         int t = e * 32 + lane;
         if (t < k) {
-            s.id[e] = ids[r * k + t];
+            s.idf[e] = (int)((uint32_t)ids[r * k + t] << 1) | (flags[r * k + t] & 1);
             s.d[e] = dists[r * k + t];
-            s.fl[e] = flags[r * k + t];
         } else {
-            s.id[e] = -1;
+            s.idf[e] = -2;  // id -1, flag 0
             s.d[e] = __longlong_as_double(0x7ff0000000000000LL);
-            s.fl[e] = 0;
         }
     }
     s.sz = sizes[r];
@@ -250,33 +247,33 @@ __device__ __forceinline__ void row_store(const WarpRow<E> &s, int32_t *ids, dou
     for (int e = 0; e < E; e++) {
         int t = e * 32 + lane;
         if (t < k) {
-            ids[r * k + t] = s.id[e];
+            ids[r * k + t] = s.idf[e] >> 1;  // arithmetic: -2 -> -1
             dists[r * k + t] = s.d[e];
-            flags[r * k + t] = (uint8_t)s.fl[e];
+            flags[r * k + t] = (uint8_t)(s.idf[e] & 1);
         }
     }
     if (lane == 0) sizes[r] = s.sz;
 }
 
-// Returns 1 (warp-uniform) when the candidate is accepted.
-template <int E>
+// Returns 1 (warp-uniform) when the candidate is accepted.  CHECK = false
+// when the caller already knows the row is not full or nd < worst.
+template <int E, bool CHECK = true>
 __device__ __forceinline__ int warp_insert(WarpRow<E> &s, int k, int src, double nd, unsigned lane) {
-    if (s.sz == k && nd >= s.worst) return 0;
+    if (CHECK && s.sz == k && nd >= s.worst) return 0;
+    // duplicate test and insertion point in one pass over the entries
     bool dup = false;
-#pragma unroll
-    for (int e = 0; e < E; e++) {
-        int t = e * 32 + lane;
-        dup |= (t < s.sz && s.id[e] == src);
-    }
-    if (__any_sync(FULL_MASK, dup)) return 0;
     int pos = s.sz;
 #pragma unroll
     for (int e = E - 1; e >= 0; e--) {
-        int t = e * 32 + lane;
-        bool before = t < s.sz && (nd < s.d[e] || (nd == s.d[e] && src < s.id[e]));
-        unsigned b = __ballot_sync(FULL_MASK, before);
+        const int t = e * 32 + lane;
+        const int id = s.idf[e] >> 1;
+        const bool in = t < s.sz;
+        dup |= in && id == src;
+        const bool before = in && (nd < s.d[e] || (nd == s.d[e] && src < id));
+        const unsigned b = __ballot_sync(FULL_MASK, before);
         if (b) pos = e * 32 + __ffs(b) - 1;
     }
+    if (__any_sync(FULL_MASK, dup)) return 0;
     int last;
     if (s.sz == k) {
         last = k - 1;
@@ -286,18 +283,16 @@ __device__ __forceinline__ int warp_insert(WarpRow<E> &s, int k, int src, double
     }
 #pragma unroll
     for (int e = E - 1; e >= 0; e--) {
-        int up_id = __shfl_up_sync(FULL_MASK, s.id[e], 1);
+        int up_i = __shfl_up_sync(FULL_MASK, s.idf[e], 1);
         double up_d = __shfl_up_sync(FULL_MASK, s.d[e], 1);
-        int up_f = __shfl_up_sync(FULL_MASK, s.fl[e], 1);
         if (e > 0) {
-            int pid = __shfl_sync(FULL_MASK, s.id[e > 0 ? e - 1 : 0], 31);
-            double pd = __shfl_sync(FULL_MASK, s.d[e > 0 ? e - 1 : 0], 31);
-            int pf = __shfl_sync(FULL_MASK, s.fl[e > 0 ? e - 1 : 0], 31);
-            if (lane == 0) { up_id = pid; up_d = pd; up_f = pf; }
+            const int pi = __shfl_sync(FULL_MASK, s.idf[e > 0 ? e - 1 : 0], 31);
+            const double pd = __shfl_sync(FULL_MASK, s.d[e > 0 ? e - 1 : 0], 31);
+            if (lane == 0) { up_i = pi; up_d = pd; }
         }
-        int t = e * 32 + lane;
-        if (t > pos && t <= last) { s.id[e] = up_id; s.d[e] = up_d; s.fl[e] = up_f; }
-        if (t == pos) { s.id[e] = src; s.d[e] = nd; s.fl[e] = 1; }
+        const int t = e * 32 + lane;
+        if (t > pos && t <= last) { s.idf[e] = up_i; s.d[e] = up_d; }
+        if (t == pos) { s.idf[e] = (int)((uint32_t)src << 1) | 1; s.d[e] = nd; }
     }
     if (s.sz == k) {
 #pragma unroll
@@ -352,7 +347,7 @@ __device__ __forceinline__ double lazy_resolve(const WarpRow<E> &s, int k, bool 
 #pragma unroll
         for (int e = 0; e < E; e++)
             for (int t = 0; t < 32; t++) {
-                const int id = __shfl_sync(FULL_MASK, s.id[e], t);
+                const int id = __shfl_sync(FULL_MASK, s.idf[e], t) >> 1;
                 if (e * 32 + t < s.sz && id == src) need = false;
             }
     }
@@ -475,7 +470,7 @@ __device__ __forceinline__ int warp_apply_chunk(WarpRow<E> &s, int k, int src_l,
         i = __ffs(m) - 1;
         int src = __shfl_sync(FULL_MASK, src_l, i);
         double nd = __shfl_sync(FULL_MASK, d_l, i);
-        acc += warp_insert<E>(s, k, src, nd, lane);
+        acc += warp_insert<E, false>(s, k, src, nd, lane);  // live: not full or nd < worst
     }
     return acc;
 }
