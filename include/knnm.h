@@ -257,6 +257,12 @@ int knnm_capture_fetch(knnm_ctx *ctx, int32_t *pa, int32_t *pb, double *pd,
  * bit-identical results; the switch exists for tests and measurement. */
 int knnm_set_join_variant(knnm_ctx *ctx, int32_t variant);
 
+/* Sample rate rho < 1 (classic NN-Descent; no reference counterpart -- the
+ * reference is rho = 1): at most new_cap of a row's new entries take part in
+ * each round (the rest stay new), chosen by splitmix64 partial Fisher-Yates;
+ * pass rev_cap = new_cap to knnm_round as well.  0 = all (reference). */
+int knnm_set_sample(knnm_ctx *ctx, int32_t new_cap);
+
 /* Hood processing order (performance only; results are independent of it):
  * iters > 0 rounds of min-label propagation over the lists build a
  * locality order once per merge; 0 processes hoods in id order. */

@@ -178,14 +178,18 @@ int64_t orc_apply_grouped(int32_t *ids, double *dists, uint8_t *flags,
 void orc_reverse_csr(const int32_t *ids, const uint8_t *flags,
                      const int32_t *sizes, int64_t n, int64_t cap,
                      int64_t *indptr, int32_t *rids, uint8_t *rnew) {
+    /* flag 2 = a new entry left out of this round by rho-sampling
+     * (orc_sample_new); never present at rho = 1 (the reference) */
     memset(indptr, 0, sizeof(int64_t) * (size_t)(n + 1));
     for (int64_t i = 0; i < n; i++)
-        for (int64_t t = 0; t < sizes[i]; t++) indptr[ids[i * cap + t] + 1]++;
+        for (int64_t t = 0; t < sizes[i]; t++)
+            if (flags[i * cap + t] != 2) indptr[ids[i * cap + t] + 1]++;
     for (int64_t i = 0; i < n; i++) indptr[i + 1] += indptr[i];
     int64_t *fill = (int64_t *)malloc(sizeof(int64_t) * (size_t)(n + 1));
     memcpy(fill, indptr, sizeof(int64_t) * (size_t)n);
     for (int64_t i = 0; i < n; i++)
         for (int64_t t = 0; t < sizes[i]; t++) {
+            if (flags[i * cap + t] == 2) continue;
             int64_t j = ids[i * cap + t];
             int64_t p = fill[j]++;
             rids[p] = (int32_t)i;
@@ -201,6 +205,41 @@ static inline uint64_t orc_mix(uint64_t *state) {
     z = (z ^ (z >> 30)) * U64_MIX1;
     z = (z ^ (z >> 27)) * U64_MIX2;
     return z ^ (z >> 31);
+}
+
+/* Sample rate rho < 1 (classic NN-Descent; no reference counterpart, the
+ * reference is rho = 1): of row u's new entries (list order p_0 < p_1 <
+ * ...), at most new_cap take part in this round, chosen by the reverse
+ * sampler's partial Fisher-Yates (splitmix64, state seed ^ SALT ^
+ * (u+1)*gamma, one warm-up step); the others get flag 2: skipped by
+ * reverse_csr and assemble, and still new after the round. */
+#define ORC_FWD_SALT 0x6a09e667f3bcc909ULL
+void orc_sample_new(const int32_t *sizes, int64_t n, int64_t cap, uint8_t *flags,
+                    int64_t new_cap, uint64_t seed) {
+#pragma omp parallel for schedule(static)
+    for (int64_t u = 0; u < n; u++) {
+        int64_t pos[256];
+        int64_t c = 0;
+        for (int64_t t = 0; t < sizes[u]; t++)
+            if (flags[u * cap + t]) pos[c++] = t;
+        if (c <= new_cap) continue;
+        uint8_t keep[256];
+        memset(keep, 0, sizeof(keep));
+        int64_t idx[256];
+        for (int64_t t = 0; t < c; t++) idx[t] = t;
+        uint64_t state = (seed ^ ORC_FWD_SALT) ^ ((uint64_t)(u + 1) * U64_GAMMA);
+        (void)orc_mix(&state);
+        for (int64_t t = 0; t < new_cap; t++) {
+            uint64_t z = orc_mix(&state);
+            int64_t r = t + (int64_t)(z % (uint64_t)(c - t));
+            int64_t tmp = idx[t];
+            idx[t] = idx[r];
+            idx[r] = tmp;
+            keep[idx[t]] = 1;
+        }
+        for (int64_t t = 0; t < c; t++)
+            if (!keep[t]) flags[u * cap + pos[t]] = 2;
+    }
 }
 
 /* _kernels.py:316-383 assemble_neighborhoods.  nbh (n,width) int32 padded
@@ -224,6 +263,7 @@ void orc_assemble(const int32_t *ids, const uint8_t *flags,
             for (int64_t t = 0; t < width; t++) { out_id[t] = -1; out_new[t] = 0; }
             int64_t m = 0;
             for (int64_t t = 0; t < sizes[u]; t++) {
+                if (flags[u * cap + t] == 2) continue; /* sits out (rho) */
                 buf_id[m] = ids[u * cap + t];
                 buf_new[m] = flags[u * cap + t];
                 m++;

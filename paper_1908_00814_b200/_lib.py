@@ -96,6 +96,7 @@ SIGNATURES = {
     "knnm_capture_count": (ctypes.c_int, [P, PI64]),
     "knnm_capture_fetch": (ctypes.c_int, [P, P, P, P, I64]),
     "knnm_set_join_variant": (ctypes.c_int, [P, I32]),
+    "knnm_set_sample": (ctypes.c_int, [P, I32]),
     "knnm_set_locality": (ctypes.c_int, [P, I32]),
     "knnm_set_u8": (ctypes.c_int, [P, I32]),
     "knnm_get_info": (ctypes.c_int, [P, ctypes.POINTER(I32), ctypes.POINTER(I32)]),

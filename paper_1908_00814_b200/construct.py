@@ -10,6 +10,7 @@ exactly where the reference keeps them.
 from __future__ import annotations
 
 import logging
+import math
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -36,6 +37,10 @@ class DescentParams:
     k: int
     max_iters: int = 50
     min_update_fraction: float = 0.001
+    # sample rate (classic NN-Descent; not in the reference, whose semantics
+    # are rho = 1): per round at most ceil(rho*k) new forward entries per row
+    # take part and reverse lists are capped at ceil(rho*k)
+    rho: float = 1.0
 
     def __post_init__(self) -> None:
         if self.k < 2:
@@ -44,6 +49,13 @@ class DescentParams:
             raise ValueError("min_update_fraction must be in [0, 1)")
         if self.max_iters < 1:
             raise ValueError("max_iters must be >= 1")
+        if not 0.0 < self.rho <= 1.0:
+            raise ValueError("rho must be in (0, 1]")
+
+
+def sample_cap(rho: float, k: int) -> int:
+    """New-entry and reverse cap per round: ceil(rho * k); k at rho = 1."""
+    return k if rho >= 1.0 else max(1, int(math.ceil(rho * k)))
 
 
 @dataclass
@@ -111,7 +123,9 @@ def _descent_rounds(engine, n: int, mode: int, k: int, params, rng, counter, on_
                     report: BuildReport | None, rev_cap: int | None = None) -> None:
     """construct.py:111-179 on the device engine (state already loaded)."""
     threshold = params.min_update_fraction * n * k
-    rev_cap = k if rev_cap is None else int(rev_cap)
+    cap = sample_cap(getattr(params, "rho", 1.0), k)
+    rev_cap = cap if rev_cap is None else int(rev_cap)
+    engine.set_sample(cap if cap < k else 0)
     for it in range(1, params.max_iters + 1):
         round_seed = int(rng.integers(0, 2**63 - 1))
         pairs, accepted = engine.round(mode, rev_cap, round_seed)

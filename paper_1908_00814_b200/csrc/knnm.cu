@@ -102,7 +102,9 @@ struct knnm_ctx {
     bool cert = false;  // fp32 arithmetic is exact for this dataset + metric
     bool cert_dot = false;  // fp16 rows + fp32 dot products are exact (L2)
     DBuf nrm64;             // exact fp64 squared norm of every subset row (cosine)
+    DBuf mpack;             // fused membership segments: base << 32 | count
     int slots_mode = SLOTS_PLAIN;  // format of the slots the next apply reads
+    int new_cap = 0;               // rho-sampling: new entries per row per round (0 = all)
     bool cert_u8 = false;   // entries are integers in [0, 255]: u8 rows, s32 MMA
     int dph = 0;            // fp16 row length (multiple of 16)
     int rowb = 0;           // staged bytes per row for the tensor-core join
@@ -284,7 +286,7 @@ int ensure_memb(knnm_ctx *c, uint64_t recs, uint64_t starts) {
 int rank_memberships(knnm_ctx *c, bool fused = false) {
     k_seg_rank<<<grid_for(c, c->n * 32, SEG_WARPS * 32, 16), SEG_WARPS * 32, 0, c->st>>>(
         c->n, c->moff.as<uint32_t>(), c->memb.as<MembRec>(), c->start.as<uint32_t>(),
-        fused ? c->roff.as<uint32_t>() : nullptr, c->k + 1, c->mcount.as<uint32_t>());
+        fused ? c->mpack.as<unsigned long long>() : nullptr);
     CKL();
     return KNNM_OK;
 }
@@ -548,7 +550,7 @@ int knnm_destroy(knnm_ctx *c) {
                    &c->counters, &c->draws, &c->draw_rows,
                    &c->draw_bad, &c->pool, &c->scan_pos, &c->vec16, &c->norms, &c->sub16, &c->subnorms, &c->out_ids, &c->out_d,
                    &c->out_s, &c->phi_leaf_lo, &c->phi_leaf_len, &c->phi_left, &c->phi_right,
-                   &c->phi_level, &c->phi_leaves, &c->phi_inner};
+                   &c->phi_level, &c->phi_leaves, &c->phi_inner, &c->nrm64, &c->mpack};
     for (DBuf *b : all) release(*b);
     for (auto &b : c->scan_tmp) release(b);
     for (auto &b : c->scan_off) release(b);
@@ -1064,8 +1066,15 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
     {
         PhaseTimer pt(c, PH_REVERSE);
         CK(cudaMemsetAsync(c->indeg.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+        if (c->new_cap > 0 && c->new_cap < k) {  // rho < 1: sample the new entries
+            k_sample_new<<<grid_for(c, n, 128), 128, 0, c->st>>>(c->sizes.as<int32_t>(), n, k,
+                                                                 c->flags.as<uint8_t>(), c->new_cap,
+                                                                 round_seed);
+            CKL();
+        }
         k_rev_count<<<grid_for(c, n * k, 256), 256, 0, c->st>>>(
-            c->ids.as<int32_t>(), c->sizes.as<int32_t>(), n, k, c->indeg.as<uint32_t>(), lo, hi);
+            c->ids.as<int32_t>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), n, k,
+            c->indeg.as<uint32_t>(), lo, hi);
         CKL();
         TRY(scan<uint32_t, uint32_t>(c, c->indeg.as<uint32_t>(), c->roff.as<uint32_t>(), n));
         k_rev_fill<<<grid_for(c, n * k, 256), 256, 0, c->st>>>(
@@ -1109,7 +1118,13 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         // membership records written by k_assemble itself (unsharded rounds):
         // row x's segment holds indeg(x) + k + 1 records (see k_assemble)
         fused_memb = !local_only && lo == 0 && hi == n;
-        if (fused_memb) TRY(ensure_memb(c, (uint64_t)n * (uint64_t)(2 * k + 1), (uint64_t)n * W));
+        if (fused_memb) {
+            TRY(ensure_memb(c, (uint64_t)n * (uint64_t)(2 * k + 1), (uint64_t)n * W));
+            TRY(ensure(c->mpack, sizeof(unsigned long long) * (size_t)n));
+            k_mpack_init<<<grid_for(c, n, 256), 256, 0, c->st>>>(c->roff.as<uint32_t>(), n, k,
+                                                                 c->mpack.as<unsigned long long>());
+            CKL();
+        }
         k_assemble<<<grid_for(c, (hi - lo) * 32, ASM_WARPS * 32, 16), ASM_WARPS * 32, 0, c->st>>>(
             c->ids.as<int32_t>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
             c->dists.as<double>(), hi, k, rev_cap, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(),
@@ -1117,7 +1132,8 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
             c->nlen.as<int32_t>(), c->hpairs.as<uint32_t>(), c->worst0.as<double>(),
             c->active.as<int32_t>(), cnt, lo, c->bound.as<uint32_t>(), c->mcount.as<uint32_t>(),
             (!local_only && c->have_order) ? c->order.as<int32_t>() : nullptr,
-            fused_memb ? c->memb.as<MembRec>() : nullptr);
+            fused_memb ? c->memb.as<MembRec>() : nullptr,
+            fused_memb ? c->mpack.as<unsigned long long>() : nullptr);
         CKL();
         TRY(scan<uint32_t, uint64_t>(c, c->hpairs.as<uint32_t>(), c->poff.as<uint64_t>(), n));
     }
@@ -1720,6 +1736,13 @@ int knnm_set_locality(knnm_ctx *c, int32_t iters) {
 int knnm_set_u8(knnm_ctx *c, int32_t on) {
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
     c->u8_enabled = on != 0;
+    return KNNM_OK;
+}
+
+int knnm_set_sample(knnm_ctx *c, int32_t new_cap) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (new_cap < 0) return fail(KNNM_ERR_ARG, "new_cap must be >= 0");
+    c->new_cap = new_cap;
     return KNNM_OK;
 }
 

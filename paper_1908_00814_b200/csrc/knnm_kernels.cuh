@@ -159,6 +159,15 @@ __global__ void k_gather_rows(const float *__restrict__ src, int dp, const int64
     }
 }
 
+// Fused membership segments: mpack[x] = (roff[x] + x * (k + 1)) << 32 (the
+// base of row x's fixed-capacity record segment, count 0).
+__global__ void k_mpack_init(const uint32_t *__restrict__ roff, int64_t n, int k,
+                             unsigned long long *__restrict__ mpack) {
+    for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n;
+         x += (int64_t)gridDim.x * blockDim.x)
+        mpack[x] = (unsigned long long)(roff[x] + (uint32_t)x * (uint32_t)(k + 1)) << 32;
+}
+
 // Exact fp64 squared norm of every row (sequential, as _kernels.py:65-70).
 __global__ void k_row_sqnorm64(const float *__restrict__ sub, int dp, int d, int64_t n,
                                double *__restrict__ out) {
@@ -416,14 +425,51 @@ __global__ void k_directed_emit(const int32_t *__restrict__ rows, const int32_t 
 // (source << 1 | new-flag).  Segment order is restored where it matters
 // (Fisher-Yates subsampling) by sorting on the source id in the assemble step.
 // ---------------------------------------------------------------------------
-__global__ void k_rev_count(const int32_t *__restrict__ ids, const int32_t *__restrict__ sizes,
-                            int64_t n, int k, uint32_t *indeg, int64_t tlo, int64_t thi) {
+// Sample rate rho < 1 (classic NN-Descent; the reference is rho = 1): of
+// row u's new entries (list order), at most new_cap take part in this
+// round, chosen by the reverse sampler's partial Fisher-Yates (splitmix64,
+// state seed ^ SALT ^ (u+1)*gamma, one warm-up step; oracle orc_sample_new).
+// The others get flag 2: skipped by the reverse lists and the hood, and
+// still new after the round (k_assemble restores them).  Thread per row.
+constexpr uint64_t FWD_SALT = 0x6a09e667f3bcc909ULL;
+__global__ void k_sample_new(const int32_t *__restrict__ sizes, int64_t n, int k, uint8_t *flags,
+                             int new_cap, uint64_t seed) {
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+         u += (int64_t)gridDim.x * blockDim.x) {
+        const int sz = sizes[u];
+        uint8_t pos[64];
+        int c = 0;
+        for (int t = 0; t < sz; t++)
+            if (flags[u * k + t]) pos[c++] = (uint8_t)t;
+        if (c <= new_cap) continue;
+        uint8_t idx[64];
+        uint64_t keep = 0;
+        for (int t = 0; t < c; t++) idx[t] = (uint8_t)t;
+        const uint64_t st0 = (seed ^ FWD_SALT) ^ ((uint64_t)(u + 1) * U64_GAMMA);
+        for (int t = 0; t < new_cap; t++) {
+            const uint64_t z = mix64(st0 + (uint64_t)(t + 2) * U64_GAMMA);
+            const int r = t + (int)(z % (uint64_t)(c - t));
+            const uint8_t tmp = idx[t];
+            idx[t] = idx[r];
+            idx[r] = tmp;
+            keep |= 1ull << idx[t];
+        }
+        for (int t = 0; t < c; t++)
+            if (!((keep >> t) & 1)) flags[u * k + pos[t]] = 2;
+    }
+}
+
+// (flag 2 = a new entry sitting out this round under rho-sampling, see
+// k_sample_new: it takes no part in the reverse lists)
+__global__ void k_rev_count(const int32_t *__restrict__ ids, const uint8_t *__restrict__ flags,
+                            const int32_t *__restrict__ sizes, int64_t n, int k, uint32_t *indeg,
+                            int64_t tlo, int64_t thi) {
     int64_t total = n * k;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t r = i / k;
         int t = (int)(i % k);
-        if (t < sizes[r]) {
+        if (t < sizes[r] && flags[i] != 2) {
             const int32_t j = ids[i];
             if (j >= tlo && j < thi) atomicAdd(&indeg[j], 1u);
         }
@@ -439,7 +485,7 @@ __global__ void k_rev_fill(const int32_t *__restrict__ ids, const uint8_t *__res
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t r = i / k;
         int t = (int)(i % k);
-        if (t < sizes[r] && ids[i] >= tlo && ids[i] < thi) {
+        if (t < sizes[r] && ids[i] >= tlo && ids[i] < thi && flags[i] != 2) {
             int32_t j = ids[i];
             uint32_t p = roff[j] + atomicSub(&indeg[j], 1u) - 1u;
             rev[p] = ((uint32_t)r << 1) | (uint32_t)flags[i];
@@ -608,14 +654,14 @@ __device__ __forceinline__ uint32_t members_closed_form(int mode, int an, int ao
     return m + ((a >= 1 || b >= 2) ? bn : 0) + ((an >= 1 || bn >= 1) ? bo : 0);
 }
 
-__global__ void __launch_bounds__(ASM_WARPS * 32)
+__global__ void __launch_bounds__(ASM_WARPS * 32, 5)
 k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__restrict__ sizes,
            const double *__restrict__ dists, int64_t n, int k, int rev_cap,
            const uint32_t *__restrict__ roff, const uint32_t *__restrict__ rev, uint64_t seed,
            const int8_t *__restrict__ labels, int mode, int W, uint32_t *nbh, int32_t *nlen,
            uint32_t *hpairs, double *worst0, int32_t *active, unsigned long long *counters,
            int64_t lo, uint32_t *bound, uint32_t *mcount, const int32_t *__restrict__ order,
-           MembRec *memb) {
+           MembRec *memb, unsigned long long *mpack) {
     __shared__ uint32_t s_seg[ASM_WARPS][WARP_REV_MAX];
     __shared__ uint32_t s_idx[ASM_WARPS][WARP_REV_MAX];
     __shared__ uint32_t s_R[ASM_WARPS][MAX_W];
@@ -627,13 +673,25 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
     for (int64_t uu = lo + (int64_t)blockIdx.x * ASM_WARPS + wib; uu < n; uu += nw) {
         const int64_t u = order ? (int64_t)order[uu] : uu;
         int sz = sizes[u];
-        for (int t = lane; t < sz; t += 32)
-            buf[t] = ((uint32_t)ids[u * k + t] << 1) | (uint32_t)flags[u * k + t];
+        // forward entries (rho-skipped ones, flag 2, sit out) and the flag
+        // clear of construct.py:142 (skipped ones stay new)
+        int m = 0;
+        for (int t0 = 0; t0 < k; t0 += 32) {
+            const int t = t0 + (int)lane;
+            uint32_t f = 0, id = 0;
+            if (t < sz) {
+                id = (uint32_t)ids[u * k + t];
+                f = flags[u * k + t];
+            }
+            const bool keep = t < sz && f != 2;
+            const unsigned bal = __ballot_sync(FULL_MASK, keep);
+            if (keep) buf[m + __popc(bal & lanemask_lt())] = (id << 1) | f;
+            m += __popc(bal);
+            if (t < k) flags[u * k + t] = f == 2 ? 1 : 0;
+        }
         __syncwarp();
-        for (int t = lane; t < k; t += 32) flags[u * k + t] = 0;
         if (lane == 0) worst0[u] = sz == k ? dists[u * k + k - 1] : __longlong_as_double(0x7ff0000000000000LL);
         uint32_t lo = roff[u], deg = roff[u + 1] - lo;
-        int m = sz;
         if (deg <= (uint32_t)rev_cap) {
             for (uint32_t j = lane; j < deg; j += 32) buf[m + j] = rev[lo + j];
             m += deg;
@@ -716,14 +774,19 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
                 if (part > 0) {
                     const uint32_t x = e >> 2;
                     atomicAdd(&bound[x], (uint32_t)part);
-                    const uint32_t at = atomicAdd(&mcount[x], 1u);
-                    // fused membership record (unsharded, unchunked rounds):
-                    // row x lies in at most indeg(x) + k hoods (x in fwd(u)
-                    // <=> u in rev(x); x in rev(u) <=> u in fwd(x)), so its
-                    // records fit the segment at roff[x] + x * (k + 1)
-                    if (memb)
-                        memb[roff[x] + x * (uint32_t)(k + 1) + at] =
+                    if (memb) {
+                        // fused membership record (unsharded, unchunked
+                        // rounds): row x lies in at most indeg(x) + k hoods
+                        // (x in fwd(u) <=> u in rev(x); x in rev(u) <=> u in
+                        // fwd(x)), so its records fit a segment of that
+                        // capacity; mpack[x] = segment base << 32 | count, so
+                        // one atomic yields the record's address
+                        const unsigned long long at = atomicAdd(&mpack[x], 1ull);
+                        memb[(uint32_t)(at >> 32) + (uint32_t)at] =
                             MembRec{(uint64_t)u, (uint32_t)part, (uint32_t)(u * W + j)};
+                    } else {
+                        atomicAdd(&mcount[x], 1u);
+                    }
                 }
             }
         }
@@ -1691,8 +1754,7 @@ __global__ void k_directed_memb(const int32_t *__restrict__ rows, int64_t m, uin
 constexpr int SEG_WARPS = 8;
 __global__ void __launch_bounds__(SEG_WARPS * 32)
 k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restrict__ memb,
-           uint32_t *__restrict__ start, const uint32_t *__restrict__ roff, int kp1,
-           const uint32_t *__restrict__ mcount) {
+           uint32_t *__restrict__ start, const unsigned long long *__restrict__ mpack) {
     __shared__ uint64_t s_key[SEG_WARPS][SEG_SMEM];
     __shared__ uint32_t s_wt[SEG_WARPS][SEG_SMEM];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
@@ -1702,11 +1764,12 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
     // while the current one is ranked (the kernel is load-latency bound)
     // (pipeline: offsets two rows ahead, records one row ahead)
     // segment of row x: [moff[x], moff[x+1]) (compacted), or the fused
-    // fixed-capacity segment [roff[x] + x * kp1, + mcount[x]) (k_assemble)
+    // fixed-capacity segment of k_assemble (mpack[x] = base << 32 | count)
     auto seg = [&](int64_t x, uint32_t &a, uint32_t &b) {
-        if (roff) {
-            a = roff[x] + (uint32_t)x * (uint32_t)kp1;
-            b = a + mcount[x];
+        if (mpack) {
+            const unsigned long long v = mpack[x];
+            a = (uint32_t)(v >> 32);
+            b = a + (uint32_t)v;
         } else {
             a = moff[x];
             b = moff[x + 1];

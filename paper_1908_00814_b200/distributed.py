@@ -207,11 +207,15 @@ def sharded_rounds(shards, comm, n, k, mode, params, rng, counter, report, rev_c
     local rank r (state already initialised and replicated)."""
     import torch
 
-    rev_cap = k if rev_cap is None else int(rev_cap)
+    from .construct import sample_cap
+
+    cap = sample_cap(getattr(params, "rho", 1.0), k)
+    rev_cap = cap if rev_cap is None else int(rev_cap)
     bounds = shard_bounds(n, comm.world)
     threshold = params.min_update_fraction * n * k
     for r in comm.local_ranks:
         shards[r].set_shard(*bounds[r])
+        shards[r].e.set_sample(cap if cap < k else 0)
     for it in range(1, params.max_iters + 1):
         round_seed = int(rng.integers(0, 2**63 - 1))
         pairs_l = {r: shards[r].round_local(mode, rev_cap, round_seed) for r in comm.local_ranks}

@@ -158,6 +158,10 @@ class Engine:
                                           ctypes.byref(acc)), "knnm_draws_insert")
         return int(acc.value)
 
+    def set_sample(self, new_cap: int) -> None:
+        """rho-sampling: new entries per row per round (0 = all, the reference)."""
+        check(self._lib.knnm_set_sample(self._h, int(new_cap)), "knnm_set_sample")
+
     def round(self, mode: int, rev_cap: int, seed: int):
         pairs = ctypes.c_int64()
         acc = ctypes.c_int64()

@@ -44,12 +44,15 @@ class MergeParams:
     max_iters: int = 50
     min_update_fraction: float = 0.001
     seed: int = 0
+    rho: float = 1.0  # sample rate (DescentParams.rho; 1.0 = the reference)
 
     def __post_init__(self) -> None:
         if self.k < 2:
             raise ValueError("k must be >= 2")
         if not 0.0 <= self.r <= 1.0:
             raise ValueError("r must be in [0, 1]")
+        if not 0.0 < self.rho <= 1.0:
+            raise ValueError("rho must be in (0, 1]")
 
     @property
     def k1(self) -> int:
@@ -57,7 +60,7 @@ class MergeParams:
 
     def descent_params(self) -> DescentParams:
         return DescentParams(k=self.k, max_iters=self.max_iters,
-                             min_update_fraction=self.min_update_fraction)
+                             min_update_fraction=self.min_update_fraction, rho=self.rho)
 
 
 def _lookup_local(union_gids: np.ndarray, gids: np.ndarray) -> np.ndarray:

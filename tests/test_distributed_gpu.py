@@ -60,3 +60,25 @@ def test_sharded_j_merge_bit_identical(oracle, world):
     assert np.array_equal(got.dists, want.dists)
     assert [(r.pairs, r.updates, r.phi) for r in rep_g.rounds] == \
         [(r.pairs, r.updates, r.phi) for r in rep_w.rounds]
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_rho_sampling_bit_identical(oracle, world):
+    """rho = 0.5 sampling is deterministic per (round seed, row): every rank
+    samples all rows identically, so sharded == single-GPU."""
+    import paper_1908_00814_b200 as km
+    from paper_1908_00814_b200 import distributed as D
+
+    n = 3000
+    ds = km.generate_int_gmm(n, 128, n_centres=30, seed=5)
+    s1, s2 = split_ids(n, seed=3)
+    g = km.nn_descent(ds, km.Metric.L2, km.DescentParams(k=16), 1, member_ids=s1)
+    h = km.nn_descent(ds, km.Metric.L2, km.DescentParams(k=16), 2, member_ids=s2)
+    mp = km.MergeParams(k=16, seed=9, rho=0.5)
+    want, rep_w = km.s_merge(ds, g, h, mp, return_report=True)
+    got, rep_g = D.s_merge_sharded(ds, g, h, mp, D.LoopbackComm(world), _engines(world),
+                                   return_report=True)
+    assert np.array_equal(got.ids, want.ids)
+    assert np.array_equal(got.dists, want.dists)
+    assert [(r.pairs, r.updates, r.phi) for r in rep_g.rounds] == \
+        [(r.pairs, r.updates, r.phi) for r in rep_w.rounds]

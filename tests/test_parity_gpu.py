@@ -177,3 +177,48 @@ def test_tensor_core_routes_u8_and_fp16(oracle, u8):
     ou, orep, _ = oracle.s_merge(ds.vectors, g, h, 20, seed=4)
     _same_graph(u, ou)
     _same_report(rep, orep)
+
+
+RHO_CASES = [
+    # n, d, k, metric, data kind  (certified u8 route, non-certified fp32, cosine)
+    (4000, 128, 20, 1, "intgmm"),
+    (3000, 16, 12, 1, "uniform"),
+    (3000, 100, 20, 2, "sphere"),
+]
+
+
+@pytest.mark.parametrize("rho", [0.5, 0.3])
+@pytest.mark.parametrize("n,d,k,metric,kind", RHO_CASES)
+def test_rho_sampling_matches_oracle(oracle, rho, n, d, k, metric, kind):
+    """rho < 1 (classic NN-Descent sampling; no reference counterpart): the
+    device path equals the oracle's restatement bit for bit (nn_descent,
+    s_merge and j_merge), and rho = 1 stays the reference."""
+    km = _km()
+    ds = _data(km, n, d, kind, seed=n + d + 1)
+    s1, s2 = split_ids(n, seed=6)
+    g, rep = km.nn_descent(ds, metric, km.DescentParams(k=k, rho=rho), 1, member_ids=s1,
+                           return_report=True)
+    og, orep, _ = oracle.nn_descent(ds.vectors, metric, k, 1, member_ids=s1, rho=rho)
+    _same_graph(g, og)
+    _same_report(rep, orep)
+    h, _, _ = oracle.nn_descent(ds.vectors, metric, k, 2, member_ids=s2, rho=rho)
+    c = km.DistanceCounter()
+    u, rep = km.s_merge(ds, _to_graph(km, og), _to_graph(km, h), km.MergeParams(k=k, seed=3, rho=rho),
+                        counter=c, return_report=True)
+    ou, orep, ocount = oracle.s_merge(ds.vectors, og, h, k, seed=3, rho=rho)
+    _same_graph(u, ou)
+    _same_report(rep, orep)
+    assert c.count == ocount
+    u, rep = km.j_merge(ds, _to_graph(km, og), s2, km.MergeParams(k=k, seed=5, rho=rho),
+                        return_report=True)
+    ou, orep, _ = oracle.j_merge(ds.vectors, og, s2, k, seed=5, rho=rho)
+    _same_graph(u, ou)
+    _same_report(rep, orep)
+
+
+def test_rho_validation():
+    km = _km()
+    with pytest.raises(ValueError):
+        km.MergeParams(k=10, rho=0.0)
+    with pytest.raises(ValueError):
+        km.DescentParams(k=10, rho=1.5)
