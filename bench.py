@@ -251,12 +251,12 @@ def run_b200(args):
         comm = D.TorchComm()
         engines = {rank: eng}
 
-        def merge(gg, hh, c, out_device, data=None):
-            return D.s_merge_sharded(data if data is not None else ds, gg, hh, params, comm,
+        def merge(gg, hh, c, out_device, data=None, p=None):
+            return D.s_merge_sharded(data if data is not None else ds, gg, hh, p or params, comm,
                                      engines, counter=c, out_device=out_device)
     else:
-        def merge(gg, hh, c, out_device, data=None):
-            return km.s_merge(data if data is not None else ds, gg, hh, params, counter=c,
+        def merge(gg, hh, c, out_device, data=None, p=None):
+            return km.s_merge(data if data is not None else ds, gg, hh, p or params, counter=c,
                               device=local, out_device=out_device)
 
     def step_device():
@@ -296,6 +296,37 @@ def run_b200(args):
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_max = float(t.item())
     value = evals / (ms_max / 1e3)  # one merge split over the ranks: whole-job rate
+
+    # BASELINE's config-2 sample rate rho = 0.5 (classic NN-Descent sampling;
+    # the reference has no rho, so the headline above is rho = 1 = the
+    # reference's algorithm bit for bit).  Same inputs, device-resident.
+    rho_line = None
+    if args.rho_half:
+        p_half = km.MergeParams(k=k, r=CFG["r"], seed=CFG["merge_seed"], rho=0.5)
+        step_device_half = lambda: merge(g_dev, h_dev, km.DistanceCounter(), True, p=p_half)  # noqa: E731
+        _w = step_device_half()
+        del _w
+        barrier()
+        eng.reset_stats()
+        h_evals, u_half = 0, None
+        eng.mark(4)
+        for _ in range(args.steps):
+            c = km.DistanceCounter()
+            u_half = merge(g_dev, h_dev, c, True, p=p_half)
+            h_evals += c.count
+        eng.mark(5)
+        h_ms = eng.elapsed_ms(4, 5)
+        if world > 1:
+            t = torch.tensor([h_ms], device="cuda")
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            h_ms = float(t.item())
+        h_st = eng.stats()
+        rho_line = {"rho": 0.5, "ms_per_step": h_ms / args.steps,
+                    "merge_seconds": h_ms / args.steps / 1e3,
+                    "evals_per_step": h_evals // args.steps,
+                    "evals_per_s": h_evals / (h_ms / 1e3),
+                    "rounds_per_step": h_st["rounds"] / args.steps,
+                    "u_half": u_half}
 
     # e2e through the public API with host buffers
     _w = step_e2e()  # warm
@@ -347,6 +378,12 @@ def run_b200(args):
         pass
     u_host = None if args.no_recall else to_host(u_dev)
     rec = recall_sample(ds, u_host, local) if not args.no_recall else None
+    if rho_line is not None:
+        u_half = rho_line.pop("u_half")
+        rho_line["recall_at_10"] = (recall_sample(ds, to_host(u_half), local)
+                                    if not args.no_recall else None)
+        rho_line["recall_vs_rho1"] = (rho_line["recall_at_10"] - rec
+                                      if rec is not None and rho_line["recall_at_10"] is not None else None)
     eng.set_dataset(ds.vectors, 1)
     cpu = None if args.no_cpu else cpu_baseline()
     steps = args.steps
@@ -378,6 +415,7 @@ def run_b200(args):
         "clocks": clk.summary(),
         "setup_seconds": setup_s,
         "cpu_baseline": cpu,
+        "rho_0_5": rho_line,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
@@ -394,7 +432,10 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0, help="fraction of the config size")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-recall", action="store_true")
+    ap.add_argument("--no-rho-half", action="store_true",
+                    help="skip the rho = 0.5 leg (BASELINE's config-2 sample rate)")
     args = ap.parse_args()
+    args.rho_half = not args.no_rho_half
     if args.impl == "reference":
         run_reference(args)
     else:
