@@ -103,6 +103,8 @@ struct knnm_ctx {
     bool cert_dot = false;  // fp16 rows + fp32 dot products are exact (L2)
     DBuf nrm64;             // exact fp64 squared norm of every subset row (cosine)
     DBuf mpack;             // fused membership segments: base << 32 | count
+    DBuf f32chk;            // loaded list distances not exact in fp32 (count)
+    bool lists_f32 = true;  // every list distance is an exact fp32 value
     int slots_mode = SLOTS_PLAIN;  // format of the slots the next apply reads
     int new_cap = 0;               // rho-sampling: new entries per row per round (0 = all)
     bool cert_u8 = false;   // entries are integers in [0, 255]: u8 rows, s32 MMA
@@ -320,19 +322,22 @@ int run_updates(knnm_ctx *c) {
     CK(cudaMemsetAsync(cnt + C_WRITTEN, 0, sizeof(unsigned long long), c->st));
     const int E = (c->k + 31) / 32;
     const int blocks = grid_for(c, n * 32, APPLY_WARPS * 32, 16);
-#define KNNM_AP_LAUNCH(EE, LZ)                                                                   \
-    k_apply_stream<EE, LZ><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(                             \
+#define KNNM_AP_LAUNCH(EE, LZ, F)                                                                \
+    k_apply_stream<EE, LZ, F><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(                             \
         n, c->k, c->boff.as<uint64_t>(), c->Bd.as<double>(), c->Bs.as<int32_t>(),               \
         c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), \
         cnt, lazy_of(c))
+    const bool f32 = c->lists_f32;
     if (E == 1) {
-        if (c->slots_mode == SLOTS_LAZY) KNNM_AP_LAUNCH(1, SLOTS_LAZY);
-        else if (c->slots_mode == SLOTS_PACKED) KNNM_AP_LAUNCH(1, SLOTS_PACKED);
-        else KNNM_AP_LAUNCH(1, SLOTS_PLAIN);
+        if (c->slots_mode == SLOTS_LAZY) KNNM_AP_LAUNCH(1, SLOTS_LAZY, false);
+        else if (c->slots_mode == SLOTS_PACKED && f32) KNNM_AP_LAUNCH(1, SLOTS_PACKED, true);
+        else if (c->slots_mode == SLOTS_PACKED) KNNM_AP_LAUNCH(1, SLOTS_PACKED, false);
+        else KNNM_AP_LAUNCH(1, SLOTS_PLAIN, false);
     } else {
-        if (c->slots_mode == SLOTS_LAZY) KNNM_AP_LAUNCH(2, SLOTS_LAZY);
-        else if (c->slots_mode == SLOTS_PACKED) KNNM_AP_LAUNCH(2, SLOTS_PACKED);
-        else KNNM_AP_LAUNCH(2, SLOTS_PLAIN);
+        if (c->slots_mode == SLOTS_LAZY) KNNM_AP_LAUNCH(2, SLOTS_LAZY, false);
+        else if (c->slots_mode == SLOTS_PACKED && f32) KNNM_AP_LAUNCH(2, SLOTS_PACKED, true);
+        else if (c->slots_mode == SLOTS_PACKED) KNNM_AP_LAUNCH(2, SLOTS_PACKED, false);
+        else KNNM_AP_LAUNCH(2, SLOTS_PLAIN, false);
     }
 #undef KNNM_AP_LAUNCH
     CKL();
@@ -550,7 +555,7 @@ int knnm_destroy(knnm_ctx *c) {
                    &c->counters, &c->draws, &c->draw_rows,
                    &c->draw_bad, &c->pool, &c->scan_pos, &c->vec16, &c->norms, &c->sub16, &c->subnorms, &c->out_ids, &c->out_d,
                    &c->out_s, &c->phi_leaf_lo, &c->phi_leaf_len, &c->phi_left, &c->phi_right,
-                   &c->phi_level, &c->phi_leaves, &c->phi_inner, &c->nrm64, &c->mpack};
+                   &c->phi_level, &c->phi_leaves, &c->phi_inner, &c->nrm64, &c->mpack, &c->f32chk};
     for (DBuf *b : all) release(*b);
     for (auto &b : c->scan_tmp) release(b);
     for (auto &b : c->scan_off) release(b);
@@ -654,6 +659,11 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     c->n = n;
     c->k = k;
     c->slots_mode = SLOTS_PLAIN;
+    // fp32 list rows only on certified data (distances are integers < 2^24)
+    // and only while every loaded distance is an exact fp32 value
+    c->lists_f32 = c->cert || c->cert_dot;
+    TRY(ensure(c->f32chk, sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(c->f32chk.p, 0, sizeof(unsigned long long), c->st));
     TRY(ensure(c->ugid, sizeof(int64_t) * n));
     TRY(h2d(c, c->ugid.p, union_gids, sizeof(int64_t) * n));
     bool identity = (n == c->n_all && union_gids[0] == 0 && union_gids[n - 1] == n - 1);
@@ -776,10 +786,15 @@ static int load_impl(knnm_ctx *c, const int32_t *rows, int64_t m, const int32_t 
             c->stage[0].as<int32_t>(), m, gi, gd, gs, gk, k1, c->k, c->ugid.as<int64_t>(), c->n,
             c->ids.as<int32_t>(), c->dists.as<double>(), c->sizes.as<int32_t>(),
             tk > 0 ? c->tail_ids.as<int32_t>() : nullptr, tk > 0 ? c->tail_d.as<double>() : nullptr,
-            tk > 0 ? c->tail_s.as<int32_t>() : nullptr, tk);
+            tk > 0 ? c->tail_s.as<int32_t>() : nullptr, tk, c->f32chk.as<unsigned long long>());
         CKL();
     }
     CK(cudaStreamSynchronize(c->st));  // staging buffers are reused by the next call
+    {
+        unsigned long long bad = 0;
+        CK(cudaMemcpy(&bad, c->f32chk.p, sizeof(bad), cudaMemcpyDeviceToHost));
+        if (bad) c->lists_f32 = false;
+    }
     return KNNM_OK;
 }
 

@@ -209,16 +209,23 @@ __device__ __forceinline__ void warp_sort_reg(T (&v)[NE], unsigned lane) {
 // One row of the k-NN state held by a warp: entry t = e*32 + lane.
 // warp_insert() is _insert (_kernels.py:159-192) executed cooperatively.
 // ---------------------------------------------------------------------------
-template <int E>
+// T = double, or float when every distance of the row is exactly an fp32
+// value (certified data: integers below 2^24) -- half the shuffle traffic.
+template <int E, typename T = double>
 struct WarpRow {
     int idf[E];  // (id << 1) | new-flag: one register moves both (ids < 2^30)
-    double d[E];
+    T d[E];
     int sz;
-    double worst;  // dists[k-1] when sz == k
+    T worst;  // dists[k-1] when sz == k
 };
 
-template <int E>
-__device__ __forceinline__ void row_load(WarpRow<E> &s, const int32_t *ids, const double *dists,
+template <typename T>
+__device__ __forceinline__ T dist_inf() {
+    return (T)__longlong_as_double(0x7ff0000000000000LL);
+}
+
+template <int E, typename T>
+__device__ __forceinline__ void row_load(WarpRow<E, T> &s, const int32_t *ids, const double *dists,
                                          const uint8_t *flags, const int32_t *sizes, int64_t r,
                                          int k, unsigned lane) {
 #pragma unroll
@@ -226,21 +233,21 @@ __device__ __forceinline__ void row_load(WarpRow<E> &s, const int32_t *ids, cons
         int t = e * 32 + lane;
         if (t < k) {
             s.idf[e] = (int)((uint32_t)ids[r * k + t] << 1) | (flags[r * k + t] & 1);
-            s.d[e] = dists[r * k + t];
+            s.d[e] = (T)dists[r * k + t];
         } else {
             s.idf[e] = -2;  // id -1, flag 0
-            s.d[e] = __longlong_as_double(0x7ff0000000000000LL);
+            s.d[e] = dist_inf<T>();
         }
     }
     s.sz = sizes[r];
-    s.worst = 0.0;
+    s.worst = (T)0;
 #pragma unroll
     for (int e = 0; e < E; e++)
         if (e == ((k - 1) >> 5)) s.worst = __shfl_sync(FULL_MASK, s.d[e], (k - 1) & 31);
 }
 
-template <int E>
-__device__ __forceinline__ void row_store(const WarpRow<E> &s, int32_t *ids, double *dists,
+template <int E, typename T>
+__device__ __forceinline__ void row_store(const WarpRow<E, T> &s, int32_t *ids, double *dists,
                                           uint8_t *flags, int32_t *sizes, int64_t r, int k,
                                           unsigned lane) {
 #pragma unroll
@@ -248,7 +255,7 @@ __device__ __forceinline__ void row_store(const WarpRow<E> &s, int32_t *ids, dou
         int t = e * 32 + lane;
         if (t < k) {
             ids[r * k + t] = s.idf[e] >> 1;  // arithmetic: -2 -> -1
-            dists[r * k + t] = s.d[e];
+            dists[r * k + t] = (double)s.d[e];
             flags[r * k + t] = (uint8_t)(s.idf[e] & 1);
         }
     }
@@ -257,8 +264,8 @@ __device__ __forceinline__ void row_store(const WarpRow<E> &s, int32_t *ids, dou
 
 // Returns 1 (warp-uniform) when the candidate is accepted.  CHECK = false
 // when the caller already knows the row is not full or nd < worst.
-template <int E, bool CHECK = true>
-__device__ __forceinline__ int warp_insert(WarpRow<E> &s, int k, int src, double nd, unsigned lane) {
+template <int E, bool CHECK = true, typename T = double>
+__device__ __forceinline__ int warp_insert(WarpRow<E, T> &s, int k, int src, T nd, unsigned lane) {
     if (CHECK && s.sz == k && nd >= s.worst) return 0;
     // duplicate test and insertion point in one pass over the entries
     bool dup = false;
@@ -284,10 +291,10 @@ __device__ __forceinline__ int warp_insert(WarpRow<E> &s, int k, int src, double
 #pragma unroll
     for (int e = E - 1; e >= 0; e--) {
         int up_i = __shfl_up_sync(FULL_MASK, s.idf[e], 1);
-        double up_d = __shfl_up_sync(FULL_MASK, s.d[e], 1);
+        T up_d = __shfl_up_sync(FULL_MASK, s.d[e], 1);
         if (e > 0) {
             const int pi = __shfl_sync(FULL_MASK, s.idf[e > 0 ? e - 1 : 0], 31);
-            const double pd = __shfl_sync(FULL_MASK, s.d[e > 0 ? e - 1 : 0], 31);
+            const T pd = __shfl_sync(FULL_MASK, s.d[e > 0 ? e - 1 : 0], 31);
             if (lane == 0) { up_i = pi; up_d = pd; }
         }
         const int t = e * 32 + lane;
@@ -456,21 +463,21 @@ __device__ __forceinline__ void lazy_warp_eval(const LazyExact z, int64_t r, boo
 // Apply up to 32 in-order candidates held one per lane (lanes [0, cnt)).
 // Candidates that cannot pass the "full and nd >= worst" test are skipped
 // without changing the outcome (worst is non-increasing once a row is full).
-template <int E>
-__device__ __forceinline__ int warp_apply_chunk(WarpRow<E> &s, int k, int src_l, double d_l,
+template <int E, typename T = double>
+__device__ __forceinline__ int warp_apply_chunk(WarpRow<E, T> &s, int k, int src_l, T d_l,
                                                 int cnt, unsigned lane) {
     int acc = 0;
     int i = -1;
     while (true) {
         // d_l = +inf marks an empty slot (real distances are finite)
-        bool live = (int)lane > i && (int)lane < cnt && d_l < __longlong_as_double(0x7ff0000000000000LL) &&
+        bool live = (int)lane > i && (int)lane < cnt && d_l < dist_inf<T>() &&
                     (s.sz < k || d_l < s.worst);
         unsigned m = __ballot_sync(FULL_MASK, live);
         if (!m) break;
         i = __ffs(m) - 1;
         int src = __shfl_sync(FULL_MASK, src_l, i);
-        double nd = __shfl_sync(FULL_MASK, d_l, i);
-        acc += warp_insert<E, false>(s, k, src, nd, lane);  // live: not full or nd < worst
+        T nd = __shfl_sync(FULL_MASK, d_l, i);
+        acc += warp_insert<E, false, T>(s, k, src, nd, lane);  // live: not full or nd < worst
     }
     return acc;
 }

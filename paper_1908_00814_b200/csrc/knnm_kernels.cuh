@@ -5,6 +5,8 @@
 #pragma once
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "knnm_device.cuh"
 
 namespace knnm {
@@ -214,7 +216,7 @@ __global__ void k_load_graph(const int32_t *__restrict__ rows, int64_t m, const 
                              const double *__restrict__ gd, const int32_t *__restrict__ gs, int gk,
                              int k1, int k, const int64_t *__restrict__ ug, int64_t n, int32_t *ids,
                              double *dists, int32_t *sizes, int32_t *tail_ids, double *tail_d,
-                             int32_t *tail_s, int tk) {
+                             int32_t *tail_s, int tk, unsigned long long *not_f32) {
     int64_t total = m * (int64_t)gk;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -227,6 +229,8 @@ __global__ void k_load_graph(const int32_t *__restrict__ rows, int64_t m, const 
             int32_t g = gi[i];
             ids[r * k + t] = g >= 0 ? lookup_local(ug, n, g) : -1;
             dists[r * k + t] = gd[i];
+            // lists the fp32 apply may hold: every loaded distance exact in fp32
+            if (g >= 0 && (double)(float)gd[i] != gd[i]) atomicAdd(not_f32, 1ull);
         } else if (t >= k1 && t < sz && tk > 0) {
             tail_ids[r * tk + (t - k1)] = gi[i];
             tail_d[r * tk + (t - k1)] = gd[i];
@@ -1865,7 +1869,7 @@ constexpr int APPLY_WARPS = 4;
 // step (coalesced), candidates that cannot pass the current worst are
 // skipped by ballot, the rest go through warp_insert in slot order -- which
 // is the reference's sequential order, so no sorting is needed.
-template <int E, int MODE>
+template <int E, int MODE, bool F32 = false>
 __global__ void __launch_bounds__(APPLY_WARPS * 32)
 k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double *__restrict__ Bd,
                const int32_t *__restrict__ Bs, int32_t *ids, double *dists, uint8_t *flags,
@@ -1883,8 +1887,11 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
         const double inf = __longlong_as_double(0x7ff0000000000000LL);
         // the next 32 slot distances are loaded while this chunk is applied
         double dnext = (int64_t)lane < ns ? Bd[lo + lane] : inf;
-        WarpRow<E> s;
-        row_load<E>(s, ids, dists, flags, sizes, r, k, lane);
+        // F32: every list distance is an exact fp32 value (packed rounds on
+        // certified data whose loaded lists passed the exactness check)
+        using T = typename std::conditional<F32, float, double>::type;
+        WarpRow<E, T> s;
+        row_load<E, T>(s, ids, dists, flags, sizes, r, k, lane);
         int a = 0;
         for (int64_t c0 = 0; c0 < ns; c0 += 32) {
             const int64_t j = c0 + lane;
@@ -1893,31 +1900,34 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
             // an unwritten slot (NaN) belongs to a row that was full at round
             // start and a distance >= its worst: it can never pass
             int src;
-            if (LAZY) {
-                if (j < ns && dl == dl) written++;
-                bool need;
-                dl = lazy_resolve<E>(s, k, j < ns, dl, Bs, lo + j, z, src, need);
-                if (__any_sync(FULL_MASK, need)) lazy_warp_eval(z, r, need, src, dl, s_lz[wib], lane, nexact);
-                if (!__any_sync(FULL_MASK, dl < inf)) continue;
-            } else if (MODE == SLOTS_PACKED) {
+            const int cnt = ns - c0 < 32 ? (int)(ns - c0) : 32;
+            if constexpr (MODE == SLOTS_PACKED) {
                 const unsigned long long v = __double_as_longlong(dl);
                 const float f = __uint_as_float((uint32_t)(v >> 32));
-                dl = f != f ? inf : (double)f;
+                const T dt = f != f ? dist_inf<T>() : (T)f;
                 if (j < ns && f == f) written++;
-                const bool pre = j < ns && (dl < s.worst || (s.sz < k && dl < inf));
+                const bool pre = j < ns && (dt < s.worst || (s.sz < k && dt < dist_inf<T>()));
                 if (!__any_sync(FULL_MASK, pre)) continue;
                 src = (int)(uint32_t)v;
+                a += warp_apply_chunk<E, T>(s, k, src, dt, cnt, lane);
             } else {
-                if (dl != dl) dl = inf;
-                else if (j < ns) written++;
-                const bool pre = j < ns && (dl < s.worst || (s.sz < k && dl < inf));
-                if (!__any_sync(FULL_MASK, pre)) continue;
-                src = pre ? Bs[lo + j] : 0;
+                if constexpr (LAZY) {
+                    if (j < ns && dl == dl) written++;
+                    bool need;
+                    dl = lazy_resolve<E>(s, k, j < ns, dl, Bs, lo + j, z, src, need);
+                    if (__any_sync(FULL_MASK, need)) lazy_warp_eval(z, r, need, src, dl, s_lz[wib], lane, nexact);
+                    if (!__any_sync(FULL_MASK, dl < inf)) continue;
+                } else {
+                    if (dl != dl) dl = inf;
+                    else if (j < ns) written++;
+                    const bool pre = j < ns && (dl < s.worst || (s.sz < k && dl < inf));
+                    if (!__any_sync(FULL_MASK, pre)) continue;
+                    src = pre ? Bs[lo + j] : 0;
+                }
+                a += warp_apply_chunk<E, T>(s, k, src, dl, cnt, lane);
             }
-            const int cnt = ns - c0 < 32 ? (int)(ns - c0) : 32;
-            a += warp_apply_chunk<E>(s, k, src, dl, cnt, lane);
         }
-        if (a) row_store<E>(s, ids, dists, flags, sizes, r, k, lane);
+        if (a) row_store<E, T>(s, ids, dists, flags, sizes, r, k, lane);
         acc += a;
     }
     if (lane == 0 && acc) atomicAdd(&counters[C_ACCEPTED], acc);
