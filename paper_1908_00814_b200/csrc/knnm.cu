@@ -73,12 +73,6 @@ void release(DBuf &b) {
     b.bytes = 0;
 }
 
-int bits_for(uint64_t maxval) {  // bits to represent values in [0, maxval]
-    int b = 1;
-    while (b < 64 && (maxval >> b) != 0) b++;
-    return b;
-}
-
 enum Phase { PH_JOIN = 0, PH_REVERSE, PH_ASSEMBLE, PH_UPDATE, PH_OTHER, PH_JOINK, PH_NUM };
 
 struct PhiTree {
@@ -1187,7 +1181,6 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
 
     int64_t acc_total = 0;
     if (P > 0) {
-        const uint64_t key_max = ((uint64_t)n * W) * W;
         size_t smem = sizeof(float) * (size_t)W * c->dp;
         size_t smem_tiled = sizeof(float) * (size_t)W * (c->dp + 4);
         if (smem > 200 * 1024) return fail(KNNM_ERR_LIMIT, "neighbourhood of %d x %d floats exceeds shared memory", W, c->dp);

@@ -973,7 +973,6 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
     __shared__ double s_nrm64[QUEUE && TAG == 2 ? MAX_W : 1];
     __shared__ int s_qlen;
     __shared__ unsigned long long s_nexact;
-    const float *sv = reinterpret_cast<const float *>(sv4);
     const int tid = threadIdx.x;
     const unsigned lane = lane_id();
     const int warp = tid >> 5;
@@ -1327,11 +1326,11 @@ struct __align__(16) MjRec {
     int id;       // member row
     float nrm;    // row norm (int bits on the u8 route)
     int pk;       // nbh position | new << 8 | class << 9 | partner_self << 11
-    int pad;
+    uint32_t q4;  // byte c: partners of a class-c member at positions < this one
 };
 
 __host__ __device__ constexpr size_t mj_meta_bytes(int Wp) {
-    return (16 + (size_t)Wp * sizeof(MjRec) + sizeof(PosPrefix) + 127) & ~(size_t)127;
+    return (16 + (size_t)Wp * sizeof(MjRec) + 127) & ~(size_t)127;
 }
 
 __device__ __forceinline__ void mma16832_u8(int (&c)[4], uint32_t a0, uint32_t a1, uint32_t a2,
@@ -1343,37 +1342,6 @@ __device__ __forceinline__ void mma16832_u8(int (&c)[4], uint32_t a0, uint32_t a
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-// Warp-cooperative Q fill (build_pos_prefix) over NB position blocks.
-template <int NB>
-__device__ __forceinline__ void build_pos_prefix_nb(uint8_t *Q, const int (&clsv)[NB], int mode,
-                                                    unsigned lane) {
-    int base0 = 0, base1 = 0, base2 = 0, base3 = 0;
-    const int mk0 = partner_mask(mode, 0), mk1 = partner_mask(mode, 1);
-    const int mk2 = partner_mask(mode, 2), mk3 = partner_mask(mode, 3);
-    const unsigned lt = lanemask_lt();
-#pragma unroll
-    for (int b = 0; b < NB; b++) {
-        const unsigned m0 = __ballot_sync(FULL_MASK, clsv[b] == 0);
-        const unsigned m1 = __ballot_sync(FULL_MASK, clsv[b] == 1);
-        const unsigned m2 = __ballot_sync(FULL_MASK, clsv[b] == 2);
-        const unsigned m3 = __ballot_sync(FULL_MASK, clsv[b] == 3);
-        const int be0 = base0 + __popc(m0 & lt), be1 = base1 + __popc(m1 & lt);
-        const int be2 = base2 + __popc(m2 & lt), be3 = base3 + __popc(m3 & lt);
-        base0 += __popc(m0);
-        base1 += __popc(m1);
-        base2 += __popc(m2);
-        base3 += __popc(m3);
-        auto q = [&](int mk) {
-            return (mk & 1 ? be0 : 0) + (mk & 2 ? be1 : 0) + (mk & 4 ? be2 : 0) + (mk & 8 ? be3 : 0);
-        };
-        const int x = b * 32 + (int)lane;
-        Q[0 * (MAX_W + 1) + x] = (uint8_t)q(mk0);
-        Q[1 * (MAX_W + 1) + x] = (uint8_t)q(mk1);
-        Q[2 * (MAX_W + 1) + x] = (uint8_t)q(mk2);
-        Q[3 * (MAX_W + 1) + x] = (uint8_t)q(mk3);
-    }
-}
-
 __device__ __forceinline__ MjRec lds_rec(const MjRec *p) {
     const float4 a = reinterpret_cast<const float4 *>(p)[0];
     const float4 b = reinterpret_cast<const float4 *>(p)[1];
@@ -1383,15 +1351,17 @@ __device__ __forceinline__ MjRec lds_rec(const MjRec *p) {
     r.id = __float_as_int(b.x);
     r.nrm = b.y;
     r.pk = __float_as_int(b.z);
-    r.pad = 0;
+    r.q4 = (uint32_t)__float_as_int(b.w);
     return r;
 }
 
 // Slot of the update "member a receives partner b" (reference order, see
-// pair_rank): membership start + rank of b's position among a's partners.
-__device__ __forceinline__ uint64_t mj_slot(const uint8_t *__restrict__ Q, const MjRec &a, const MjRec &b) {
+// pair_rank): membership start + rank of b's position among a's partners,
+// i.e. byte class(a) of b's q4 (the position prefix count), minus a itself
+// when a is its own class's partner and precedes b.
+__device__ __forceinline__ uint64_t mj_slot(const MjRec &a, const MjRec &b) {
     const int pa = a.pk & 0xFF, pb = b.pk & 0xFF, ca = (a.pk >> 9) & 3;
-    return a.st + (uint32_t)Q[ca * (MAX_W + 1) + pb] - (uint32_t)(((a.pk >> 11) & 1) && pa < pb);
+    return a.st + ((b.q4 >> (8 * ca)) & 0xFFu) - (uint32_t)(((a.pk >> 11) & 1) && pa < pb);
 }
 
 // U8 = true: rows are u8 (integer data in [0, 255]); the Gram block uses
@@ -1420,7 +1390,6 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
     char *base = mj_smem + (size_t)warp * per_warp;
     uint64_t *bar = reinterpret_cast<uint64_t *>(base);
     MjRec *rec = reinterpret_cast<MjRec *>(base + 16);
-    uint8_t *Q = reinterpret_cast<uint8_t *>(rec + Wp);
     char *rows = base + mj_meta_bytes(Wp);
     if (lane == 0) mbar_init(bar, 1);
     // zero the row buffer once: slots beyond w feed the MMA tile tails
@@ -1500,6 +1469,9 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
         __syncwarp();
         {
             int f0 = 0, f1 = c0n, f2 = c0n + c1n, f3 = c0n + c1n + c2n;  // class bases
+            int g0 = 0, g1 = 0, g2 = 0, g3 = 0;  // class members at earlier positions
+            const int mk0 = partner_mask(mode, 0), mk1 = partner_mask(mode, 1);
+            const int mk2 = partner_mask(mode, 2), mk3 = partner_mask(mode, 3);
 #pragma unroll
             for (int b = 0; b < NB; b++) {
                 const unsigned k0 = __ballot_sync(FULL_MASK, clsv[b] == 0);
@@ -1507,14 +1479,21 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                 const unsigned k2 = __ballot_sync(FULL_MASK, clsv[b] == 2);
                 const unsigned k3 = __ballot_sync(FULL_MASK, clsv[b] == 3);
                 const int c = clsv[b];
-                const int sl = c == 0 ? f0 + __popc(k0 & lt)
-                             : c == 1 ? f1 + __popc(k1 & lt)
-                             : c == 2 ? f2 + __popc(k2 & lt)
-                             : c == 3 ? f3 + __popc(k3 & lt) : -1;
-                f0 += __popc(k0);
-                f1 += __popc(k1);
-                f2 += __popc(k2);
-                f3 += __popc(k3);
+                const int be0 = g0 + __popc(k0 & lt), be1 = g1 + __popc(k1 & lt);
+                const int be2 = g2 + __popc(k2 & lt), be3 = g3 + __popc(k3 & lt);
+                const int sl = c == 0 ? f0 + be0 : c == 1 ? f1 + be1 : c == 2 ? f2 + be2
+                             : c == 3 ? f3 + be3 : -1;
+                g0 += __popc(k0);
+                g1 += __popc(k1);
+                g2 += __popc(k2);
+                g3 += __popc(k3);
+                // position prefix counts of this position for each member class
+                // (the PosPrefix table row, kept in the member's record)
+                auto q = [&](int mk) {
+                    return (uint32_t)((mk & 1 ? be0 : 0) + (mk & 2 ? be1 : 0) + (mk & 4 ? be2 : 0) +
+                                      (mk & 8 ? be3 : 0));
+                };
+                const uint32_t q4 = q(mk0) | (q(mk1) << 8) | (q(mk2) << 16) | (q(mk3) << 24);
                 if (sl >= 0) {
                     // each lane stages its own members' rows (parallel TMA issue)
                     const int id = (int)(ev0[b] >> 2);
@@ -1525,11 +1504,11 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                     float4 *dst = reinterpret_cast<float4 *>(rec + sl);
                     dst[0] = make_float4(__int_as_float(__double2loint(mw0[b])), __int_as_float(__double2hiint(mw0[b])),
                                          __int_as_float((int)(uint32_t)st), __int_as_float((int)(uint32_t)(st >> 32)));
-                    dst[1] = make_float4(__int_as_float(id), mn0[b], __int_as_float(pk), 0.f);
+                    dst[1] = make_float4(__int_as_float(id), mn0[b], __int_as_float(pk),
+                                         __int_as_float((int)q4));
                 }
             }
         }
-        build_pos_prefix_nb<NB>(Q, clsv, mode, lane);
         // ---- prefetch: hood i+1 metadata, hood i+2 entries, hood i+3 id --------
         double mw1[NB];
         float mn1[NB];
@@ -1593,8 +1572,8 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                             U8 ? (double)((__float_as_int(R.nrm) + __float_as_int(C.nrm)) - 2 * iacc[s])
                                : (double)((R.nrm + C.nrm) - 2.0f * acc[s]);
                         unsigned long long *Bp = reinterpret_cast<unsigned long long *>(Bd);
-                        if (dd < R.w) Bp[mj_slot(Q, R, C)] = pack_slot(dd, C.id);  // id[ii] <- id[jj]
-                        if (dd < C.w) Bp[mj_slot(Q, C, R)] = pack_slot(dd, R.id);  // id[jj] <- id[ii]
+                        if (dd < R.w) Bp[mj_slot(R, C)] = pack_slot(dd, C.id);  // id[ii] <- id[jj]
+                        if (dd < C.w) Bp[mj_slot(C, R)] = pack_slot(dd, R.id);  // id[jj] <- id[ii]
                     }
                 }
             }
