@@ -98,6 +98,7 @@ struct knnm_ctx {
     DBuf nrm64;             // exact fp64 squared norm of every subset row (cosine)
     DBuf mpack;             // fused membership segments: base << 32 | count
     DBuf f32chk;            // loaded list distances not exact in fp32 (count)
+    DBuf live;              // per row: its hood can hold a new entry this round
     bool lists_f32 = true;  // every list distance is an exact fp32 value
     int slots_mode = SLOTS_PLAIN;  // format of the slots the next apply reads
     int new_cap = 0;               // rho-sampling: new entries per row per round (0 = all)
@@ -549,7 +550,7 @@ int knnm_destroy(knnm_ctx *c) {
                    &c->counters, &c->draws, &c->draw_rows,
                    &c->draw_bad, &c->pool, &c->scan_pos, &c->vec16, &c->norms, &c->sub16, &c->subnorms, &c->out_ids, &c->out_d,
                    &c->out_s, &c->phi_leaf_lo, &c->phi_leaf_len, &c->phi_left, &c->phi_right,
-                   &c->phi_level, &c->phi_leaves, &c->phi_inner, &c->nrm64, &c->mpack, &c->f32chk};
+                   &c->phi_level, &c->phi_leaves, &c->phi_inner, &c->nrm64, &c->mpack, &c->f32chk, &c->live};
     for (DBuf *b : all) release(*b);
     for (auto &b : c->scan_tmp) release(b);
     for (auto &b : c->scan_off) release(b);
@@ -1081,9 +1082,11 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                                                                  round_seed);
             CKL();
         }
+        TRY(ensure(c->live, (size_t)n));
+        CK(cudaMemsetAsync(c->live.p, 0, (size_t)n, c->st));
         k_rev_count<<<grid_for(c, n * k, 256), 256, 0, c->st>>>(
             c->ids.as<int32_t>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), n, k,
-            c->indeg.as<uint32_t>(), lo, hi);
+            c->indeg.as<uint32_t>(), lo, hi, c->live.as<uint8_t>());
         CKL();
         TRY(scan<uint32_t, uint32_t>(c, c->indeg.as<uint32_t>(), c->roff.as<uint32_t>(), n));
         k_rev_fill<<<grid_for(c, n * k, 256), 256, 0, c->st>>>(
@@ -1142,7 +1145,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
             c->active.as<int32_t>(), cnt, lo, c->bound.as<uint32_t>(), c->mcount.as<uint32_t>(),
             (!local_only && c->have_order) ? c->order.as<int32_t>() : nullptr,
             fused_memb ? c->memb.as<MembRec>() : nullptr,
-            fused_memb ? c->mpack.as<unsigned long long>() : nullptr);
+            fused_memb ? c->mpack.as<unsigned long long>() : nullptr, c->live.as<uint8_t>());
         CKL();
         TRY(scan<uint32_t, uint64_t>(c, c->hpairs.as<uint32_t>(), c->poff.as<uint64_t>(), n));
     }

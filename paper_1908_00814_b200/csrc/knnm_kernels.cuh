@@ -465,17 +465,28 @@ __global__ void k_sample_new(const int32_t *__restrict__ sizes, int64_t n, int k
 
 // (flag 2 = a new entry sitting out this round under rho-sampling, see
 // k_sample_new: it takes no part in the reverse lists)
+// Also marks live[x] = 1 for every row whose hood can hold a new entry this
+// round: rows with a flagged forward entry and targets of new forward
+// entries (their reverse edge is new).  Other hoods have no admissible pair
+// (_kernels.py:391-399 needs new_p or new_q): k_assemble skips them.
 __global__ void k_rev_count(const int32_t *__restrict__ ids, const uint8_t *__restrict__ flags,
                             const int32_t *__restrict__ sizes, int64_t n, int k, uint32_t *indeg,
-                            int64_t tlo, int64_t thi) {
+                            int64_t tlo, int64_t thi, uint8_t *live) {
     int64_t total = n * k;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t r = i / k;
         int t = (int)(i % k);
-        if (t < sizes[r] && flags[i] != 2) {
-            const int32_t j = ids[i];
-            if (j >= tlo && j < thi) atomicAdd(&indeg[j], 1u);
+        if (t < sizes[r]) {
+            const uint8_t f = flags[i];
+            if (f != 0) live[r] = 1;  // new or sitting out (its flag is restored)
+            if (f != 2) {
+                const int32_t j = ids[i];
+                if (j >= tlo && j < thi) {
+                    atomicAdd(&indeg[j], 1u);
+                    if (f == 1) live[j] = 1;
+                }
+            }
         }
     }
 }
@@ -665,7 +676,7 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
            const int8_t *__restrict__ labels, int mode, int W, uint32_t *nbh, int32_t *nlen,
            uint32_t *hpairs, double *worst0, int32_t *active, unsigned long long *counters,
            int64_t lo, uint32_t *bound, uint32_t *mcount, const int32_t *__restrict__ order,
-           MembRec *memb, unsigned long long *mpack) {
+           MembRec *memb, unsigned long long *mpack, const uint8_t *__restrict__ live) {
     __shared__ uint32_t s_seg[ASM_WARPS][WARP_REV_MAX];
     __shared__ uint32_t s_idx[ASM_WARPS][WARP_REV_MAX];
     __shared__ uint32_t s_R[ASM_WARPS][MAX_W];
@@ -677,6 +688,15 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
     for (int64_t uu = lo + (int64_t)blockIdx.x * ASM_WARPS + wib; uu < n; uu += nw) {
         const int64_t u = order ? (int64_t)order[uu] : uu;
         int sz = sizes[u];
+        if (!live[u]) {
+            // no new entry can reach this hood: no pairs, flags already clear
+            if (lane == 0) {
+                worst0[u] = sz == k ? dists[u * k + k - 1] : __longlong_as_double(0x7ff0000000000000LL);
+                nlen[u] = 0;
+                hpairs[u] = 0;
+            }
+            continue;
+        }
         // forward entries (rho-skipped ones, flag 2, sit out) and the flag
         // clear of construct.py:142 (skipped ones stay new)
         int m = 0;
