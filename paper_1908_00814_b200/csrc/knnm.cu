@@ -99,6 +99,7 @@ struct knnm_ctx {
     DBuf mpack;             // fused membership segments: base << 32 | count
     DBuf f32chk;            // loaded list distances not exact in fp32 (count)
     DBuf live;              // per row: its hood can hold a new entry this round
+    DBuf segheavy;          // rows with > SEG_SMEM memberships (k_seg_rank_heavy)
     bool lists_f32 = true;  // every list distance is an exact fp32 value
     int slots_mode = SLOTS_PLAIN;  // format of the slots the next apply reads
     int new_cap = 0;               // rho-sampling: new entries per row per round (0 = all)
@@ -281,9 +282,18 @@ int ensure_memb(knnm_ctx *c, uint64_t recs, uint64_t starts) {
 // Membership ranking: moff = scan(mcount); bucket memberships by row (fill
 // kernel launched by the caller between the two halves); then k_seg_rank.
 int rank_memberships(knnm_ctx *c, bool fused = false) {
+    TRY(ensure(c->segheavy, sizeof(int32_t) * (size_t)c->n));
+    unsigned long long *cnt = c->counters.as<unsigned long long>();
+    CK(cudaMemsetAsync(cnt + C_SEGHEAVY, 0, sizeof(unsigned long long), c->st));
+    const unsigned long long *mp = fused ? c->mpack.as<unsigned long long>() : nullptr;
     k_seg_rank<<<grid_for(c, c->n * 32, SEG_WARPS * 32, 16), SEG_WARPS * 32, 0, c->st>>>(
-        c->n, c->moff.as<uint32_t>(), c->memb.as<MembRec>(), c->start.as<uint32_t>(),
-        fused ? c->mpack.as<unsigned long long>() : nullptr);
+        c->n, c->moff.as<uint32_t>(), c->memb.as<MembRec>(), c->start.as<uint32_t>(), mp,
+        c->segheavy.as<int32_t>(), cnt);
+    CKL();
+    // hub rows: block per row, count read on the device
+    k_seg_rank_heavy<<<c->sms * 2, SEGH_THREADS, 0, c->st>>>(
+        c->moff.as<uint32_t>(), c->memb.as<MembRec>(), c->start.as<uint32_t>(), mp,
+        c->segheavy.as<int32_t>(), cnt);
     CKL();
     return KNNM_OK;
 }
@@ -550,7 +560,7 @@ int knnm_destroy(knnm_ctx *c) {
                    &c->counters, &c->draws, &c->draw_rows,
                    &c->draw_bad, &c->pool, &c->scan_pos, &c->vec16, &c->norms, &c->sub16, &c->subnorms, &c->out_ids, &c->out_d,
                    &c->out_s, &c->phi_leaf_lo, &c->phi_leaf_len, &c->phi_left, &c->phi_right,
-                   &c->phi_level, &c->phi_leaves, &c->phi_inner, &c->nrm64, &c->mpack, &c->f32chk, &c->live};
+                   &c->phi_level, &c->phi_leaves, &c->phi_inner, &c->nrm64, &c->mpack, &c->f32chk, &c->live, &c->segheavy};
     for (DBuf *b : all) release(*b);
     for (auto &b : c->scan_tmp) release(b);
     for (auto &b : c->scan_off) release(b);

@@ -25,6 +25,7 @@ enum Counter {
     C_EXACT = 9,      // pairs re-evaluated in fp64 after the fp32 screen
     C_MAXC = 10,      // max candidates on a giant row
     C_WRITTEN = 11,   // update slots written by the join (prefilter survivors)
+    C_SEGHEAVY = 12,  // rows with > SEG_SMEM memberships (block-ranked)
     C_NUM = 16
 };
 

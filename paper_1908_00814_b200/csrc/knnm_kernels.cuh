@@ -1751,21 +1751,20 @@ __global__ void k_directed_memb(const int32_t *__restrict__ rows, int64_t m, uin
 }
 
 // Per row: exclusive weighted rank of each membership by key (ascending
-// hood / ordinal) -> start[out] = first slot of that membership in the
-// row's bucket.  Warp per row, O(m^2 / 32); segments up to SEG_SMEM are
-// staged in shared memory, longer ones (hub rows) read through L1.
+// hood / ordinal; keys are unique per row) -> start[out] = first slot of that
+// membership in the row's bucket.  Warp per row: m <= 32 from registers (a
+// shuffle loop), m <= SEG_SMEM by a shared-memory bitonic sort of
+// (key << 32 | index) and a weighted exclusive scan; longer rows (hubs) go
+// to a list ranked by k_seg_rank_heavy with a whole block per row.
 constexpr int SEG_WARPS = 8;
 __global__ void __launch_bounds__(SEG_WARPS * 32)
 k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restrict__ memb,
-           uint32_t *__restrict__ start, const unsigned long long *__restrict__ mpack) {
+           uint32_t *__restrict__ start, const unsigned long long *__restrict__ mpack,
+           int32_t *heavy, unsigned long long *counters) {
     __shared__ uint64_t s_key[SEG_WARPS][SEG_SMEM];
     __shared__ uint32_t s_wt[SEG_WARPS][SEG_SMEM];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * SEG_WARPS;
-    // rows with m <= 32 memberships (almost all): one membership per lane in
-    // registers, ranked by a shuffle loop; the next row's segment is loaded
-    // while the current one is ranked (the kernel is load-latency bound)
-    // (pipeline: offsets two rows ahead, records one row ahead)
     // segment of row x: [moff[x], moff[x+1]) (compacted), or the fused
     // fixed-capacity segment of k_assemble (mpack[x] = base << 32 | count)
     auto seg = [&](int64_t x, uint32_t &a, uint32_t &b) {
@@ -1778,6 +1777,9 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
             b = moff[x + 1];
         }
     };
+    // rows with m <= 32 memberships (almost all): one membership per lane in
+    // registers; the next row's segment is loaded while the current one is
+    // ranked (pipeline: offsets two rows ahead, records one row ahead)
     int64_t r = (int64_t)blockIdx.x * SEG_WARPS + wib;
     uint32_t lo1 = 0, hi1 = 0, lo2 = 0, hi2 = 0;
     MembRec rec1 = MembRec{0, 0, 0};
@@ -1797,6 +1799,7 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
         if (m == 0) continue;
         if (m <= 32) {
             uint32_t acc = 0;
+#pragma unroll 4
             for (int f = 0; f < m; f++) {
                 const uint64_t kf = __shfl_sync(FULL_MASK, rec.key, f);
                 const uint32_t wf = __shfl_sync(FULL_MASK, rec.weight, f);
@@ -1805,30 +1808,85 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
             if ((int)lane < m) start[rec.out] = acc;
             continue;
         }
-        if (m <= SEG_SMEM) {
-            for (int e = lane; e < m; e += 32) {
-                s_key[wib][e] = memb[lo + e].key;
-                s_wt[wib][e] = memb[lo + e].weight;
-            }
-            __syncwarp();
-            for (int e = lane; e < m; e += 32) {
-                const uint64_t ke = s_key[wib][e];
-                uint32_t acc = 0;
-                for (int f = 0; f < m; f++) acc += s_key[wib][f] < ke ? s_wt[wib][f] : 0u;
-                start[memb[lo + e].out] = acc;
-            }
-            __syncwarp();
-        } else {
-            for (int e = lane; e < m; e += 32) {
-                const uint64_t ke = memb[lo + e].key;
-                uint32_t acc = 0;
-                for (int f = 0; f < m; f++) {
-                    const MembRec rf = memb[lo + f];
-                    acc += rf.key < ke ? rf.weight : 0u;
-                }
-                start[memb[lo + e].out] = acc;
+        if (m > SEG_SMEM) {  // hub row: ranked by a whole block later
+            if (lane == 0) heavy[atomicAdd(&counters[C_SEGHEAVY], 1ull)] = (int32_t)r;
+            continue;
+        }
+        // sort (key << 32 | index) ascending, then scan weights in that order
+        uint32_t P2 = 64;
+        while (P2 < (uint32_t)m) P2 <<= 1;
+        uint64_t *sk = s_key[wib];
+        uint32_t *sw = s_wt[wib];
+        for (uint32_t e = lane; e < P2; e += 32) {
+            if (e < (uint32_t)m) {
+                const MembRec re = memb[lo + e];
+                sk[e] = (re.key << 32) | e;
+                sw[e] = re.weight;
+            } else {
+                sk[e] = ~0ull;
             }
         }
+        __syncwarp();
+        bitonic_warp<uint64_t>(sk, P2, lane);
+        uint32_t carry = 0;
+        for (int c0 = 0; c0 < m; c0 += 32) {
+            const int i = c0 + (int)lane;
+            const uint32_t e = i < m ? (uint32_t)(sk[i] & 0xffffffffu) : 0u;
+            const uint32_t v = i < m ? sw[e] : 0u;
+            uint32_t inc = v;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+                if ((int)lane >= o) inc += t;
+            }
+            if (i < m) start[memb[lo + e].out] = carry + inc - v;
+            carry += __shfl_sync(FULL_MASK, inc, 31);
+        }
+        __syncwarp();
+    }
+}
+
+// Hub rows (> SEG_SMEM memberships): one block per row, keys staged in
+// shared memory, rank = weighted count of smaller keys.  The row list and its
+// length (counters[C_SEGHEAVY]) come from k_seg_rank: no host round trip.
+constexpr int SEGH_THREADS = 256;
+constexpr int SEGH_SMEM = 4096;  // keys staged in shared memory per block
+__global__ void __launch_bounds__(SEGH_THREADS)
+k_seg_rank_heavy(const uint32_t *__restrict__ moff, const MembRec *__restrict__ memb,
+                 uint32_t *__restrict__ start, const unsigned long long *__restrict__ mpack,
+                 const int32_t *__restrict__ heavy, const unsigned long long *__restrict__ counters) {
+    __shared__ uint64_t s_k[SEGH_SMEM];
+    __shared__ uint32_t s_w[SEGH_SMEM];
+    const int64_t nh = (int64_t)counters[C_SEGHEAVY];
+    for (int64_t h = blockIdx.x; h < nh; h += gridDim.x) {
+        const int64_t x = heavy[h];
+        uint32_t lo, hi;
+        if (mpack) {
+            const unsigned long long v = mpack[x];
+            lo = (uint32_t)(v >> 32);
+            hi = lo + (uint32_t)v;
+        } else {
+            lo = moff[x];
+            hi = moff[x + 1];
+        }
+        const int m = (int)(hi - lo);
+        const int ms = m < SEGH_SMEM ? m : SEGH_SMEM;
+        for (int e = threadIdx.x; e < ms; e += blockDim.x) {
+            s_k[e] = memb[lo + e].key;
+            s_w[e] = memb[lo + e].weight;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < m; e += blockDim.x) {
+            const MembRec re = memb[lo + e];
+            uint32_t acc = 0;
+            for (int f = 0; f < ms; f++) acc += s_k[f] < re.key ? s_w[f] : 0u;
+            for (int f = ms; f < m; f++) {
+                const MembRec rf = memb[lo + f];
+                acc += rf.key < re.key ? rf.weight : 0u;
+            }
+            start[re.out] = acc;
+        }
+        __syncthreads();
     }
 }
 
