@@ -1205,7 +1205,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                              (c->join_variant == 2 || c->join_variant < 0);
         const bool tiled = !use_mma && (c->join_variant == 1 || (c->join_variant < 0 && smem_tiled <= 200 * 1024));
         // long rows (large d): more warps share one staged hood
-        const int tj_threads = smem_tiled > 48 * 1024 ? TJ_WARPS_BIG * 32 : TJ_THREADS;
+        const int tj_threads = smem_tiled > 16 * 1024 ? TJ_WARPS_BIG * 32 : TJ_THREADS;
         // lower bounds of the exact value from the fp32 one (LazyExact)
         const double lo_rel = 1.0 - (double)(c->d + 8) * ldexp(1.0, -23);
         const double lo_abs = (double)(4 * c->d + 64) * ldexp(1.0, -24);
