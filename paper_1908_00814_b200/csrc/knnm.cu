@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/knnm.h"
@@ -100,6 +101,9 @@ struct knnm_ctx {
     DBuf f32chk;            // loaded list distances not exact in fp32 (count)
     DBuf live;              // per row: its hood can hold a new entry this round
     DBuf segheavy;          // rows with > SEG_SMEM memberships (k_seg_rank_heavy)
+    void *stg_buf[2] = {nullptr, nullptr};  // pinned staging for pageable copies
+    cudaEvent_t stg_ev[2] = {nullptr, nullptr};
+    bool stg_busy[2] = {false, false};
     bool lists_f32 = true;  // every list distance is an exact fp32 value
     int slots_mode = SLOTS_PLAIN;  // format of the slots the next apply reads
     int new_cap = 0;               // rho-sampling: new entries per row per round (0 = all)
@@ -205,18 +209,99 @@ int grid_for(knnm_ctx *c, int64_t work, int threads, int per_sm = 8) {
     return (int)g;
 }
 
+// Large transfers to / from pageable host memory (plain numpy arrays) go
+// through a pinned double buffer: the driver's own staging of pageable
+// copies runs far below PCIe rates, so chunks are DMA'd to/from pinned
+// memory while the previous chunk is copied on the host by several threads.
+constexpr size_t STG_CHUNK = 16u << 20;
+constexpr size_t STG_MIN = 8u << 20;
+
+bool host_pageable(const void *p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+void par_memcpy(void *dst, const void *src, size_t bytes) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>(std::min(8u, hw), std::max<size_t>(1, bytes >> 21));
+    if (nt <= 1) {
+        memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t part = ((bytes + nt - 1) / nt + 4095) & ~(size_t)4095;
+    std::vector<std::thread> th;
+    for (size_t t = 1; t < nt; t++) {
+        const size_t off = t * part;
+        if (off >= bytes) break;
+        th.emplace_back([=] { memcpy((char *)dst + off, (const char *)src + off, std::min(part, bytes - off)); });
+    }
+    memcpy(dst, src, std::min(part, bytes));
+    for (auto &x : th) x.join();
+}
+
+int ensure_staging(knnm_ctx *c) {
+    for (int i = 0; i < 2; i++) {
+        if (!c->stg_buf[i]) {
+            CK(cudaHostAlloc(&c->stg_buf[i], STG_CHUNK, cudaHostAllocDefault));
+            CK(cudaEventCreateWithFlags(&c->stg_ev[i], cudaEventDisableTiming));
+            c->stg_busy[i] = false;
+        }
+    }
+    return KNNM_OK;
+}
+
 int h2d(knnm_ctx *c, void *dst, const void *src, size_t bytes) {
     if (bytes == 0) return KNNM_OK;
-    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->st));
     c->stats.h2d_bytes += (int64_t)bytes;
-    return KNNM_OK;
+    if (bytes < STG_MIN || !host_pageable(src)) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, c->st));
+        return KNNM_OK;
+    }
+    TRY(ensure_staging(c));
+    for (size_t off = 0, i = 0; off < bytes; off += STG_CHUNK, i++) {
+        const int sl = (int)(i & 1);
+        const size_t len = std::min(STG_CHUNK, bytes - off);
+        if (c->stg_busy[sl]) CK(cudaEventSynchronize(c->stg_ev[sl]));  // its last DMA is done
+        par_memcpy(c->stg_buf[sl], (const char *)src + off, len);
+        CK(cudaMemcpyAsync((char *)dst + off, c->stg_buf[sl], len, cudaMemcpyHostToDevice, c->st));
+        CK(cudaEventRecord(c->stg_ev[sl], c->st));
+        c->stg_busy[sl] = true;
+    }
+    return KNNM_OK;  // the source may be released: it has been copied out
 }
 
 int d2h(knnm_ctx *c, void *dst, const void *src, size_t bytes) {
     if (bytes == 0) return KNNM_OK;
-    CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->st));
     c->stats.d2h_bytes += (int64_t)bytes;
-    return KNNM_OK;
+    if (bytes < STG_MIN || !host_pageable(dst)) {
+        CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, c->st));
+        return KNNM_OK;
+    }
+    TRY(ensure_staging(c));
+    size_t prev_off = 0, prev_len = 0;
+    int prev_sl = -1;
+    for (size_t off = 0, i = 0; off < bytes; off += STG_CHUNK, i++) {
+        const int sl = (int)(i & 1);
+        const size_t len = std::min(STG_CHUNK, bytes - off);
+        // (slot sl's previous chunk was copied out one iteration ago)
+        CK(cudaMemcpyAsync(c->stg_buf[sl], (const char *)src + off, len, cudaMemcpyDeviceToHost, c->st));
+        CK(cudaEventRecord(c->stg_ev[sl], c->st));
+        c->stg_busy[sl] = true;
+        if (prev_sl >= 0) {
+            CK(cudaEventSynchronize(c->stg_ev[prev_sl]));
+            par_memcpy((char *)dst + prev_off, c->stg_buf[prev_sl], prev_len);
+        }
+        prev_off = off;
+        prev_len = len;
+        prev_sl = sl;
+    }
+    CK(cudaEventSynchronize(c->stg_ev[prev_sl]));
+    par_memcpy((char *)dst + prev_off, c->stg_buf[prev_sl], prev_len);
+    return KNNM_OK;  // complete on return (as a pageable cudaMemcpy)
 }
 
 int sync_counters(knnm_ctx *c) {
@@ -562,6 +647,10 @@ int knnm_destroy(knnm_ctx *c) {
                    &c->out_s, &c->phi_leaf_lo, &c->phi_leaf_len, &c->phi_left, &c->phi_right,
                    &c->phi_level, &c->phi_leaves, &c->phi_inner, &c->nrm64, &c->mpack, &c->f32chk, &c->live, &c->segheavy};
     for (DBuf *b : all) release(*b);
+    for (int i = 0; i < 2; i++) {
+        if (c->stg_buf[i]) cudaFreeHost(c->stg_buf[i]);
+        if (c->stg_ev[i]) cudaEventDestroy(c->stg_ev[i]);
+    }
     for (auto &b : c->scan_tmp) release(b);
     for (auto &b : c->scan_off) release(b);
     for (auto &b : c->stage) release(b);

@@ -42,6 +42,33 @@ def main():
 
     once()
     torch.cuda.synchronize()
+    if "--timeline" in sys.argv:
+        # CUPTI kernel/memcpy activity: busy vs idle and the largest gaps
+        from torch.profiler import ProfilerActivity, profile
+
+        with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+            dt, cnt, _ = once()
+            torch.cuda.synchronize()
+        ev = [e for e in prof.events() if e.device_type.name == "CUDA"]
+        iv = sorted((e.time_range.start, e.time_range.end, e.name) for e in ev)
+        busy, gaps, cur, prev = 0.0, [], iv[0][0], None
+        for s0, e0, nm in iv:
+            if s0 > cur:
+                gaps.append((s0 - cur, prev, nm))
+            if e0 > cur:
+                busy += e0 - max(s0, cur)
+                cur = e0
+            prev = nm
+        print(f"{name}: wall {dt * 1e3:.1f} ms, gpu span {(cur - iv[0][0]) / 1e3:.1f} ms, "
+              f"busy {busy / 1e3:.1f} ms, gaps {len(gaps)}")
+        cat = {}
+        for s0, e0, nm in iv:
+            key = nm.split("(")[0] if nm.startswith(("Memcpy", "Memset")) else "kernels"
+            cat[key] = cat.get(key, 0.0) + (e0 - s0)
+        print("  by activity:", {k: round(v / 1e3, 1) for k, v in sorted(cat.items(), key=lambda x: -x[1])})
+        for d0, a, b in sorted(gaps, reverse=True)[:12]:
+            print(f"  gap {d0 / 1e3:8.3f} ms after {str(a)[:38]:38s} before {str(b)[:38]}")
+        return
     torch.cuda.profiler.start()
     dt, cnt, _ = once()
     torch.cuda.synchronize()
