@@ -619,6 +619,8 @@ int knnm_create(int device, knnm_ctx **out) {
                             (int)(2 * sizeof(uint32_t) * BLOCK_SORT_MAX)));
     for (auto f : {k_join_exact<0>, k_join_exact<1>, k_join_exact<2>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (auto f : {k_join_chunked<0>, k_join_chunked<1>, k_join_chunked<2>})
+        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (auto f : {k_join_mma<false, 1>, k_join_mma<false, 2>, k_join_mma<false, 4>,
                    k_join_mma<true, 1>, k_join_mma<true, 2>, k_join_mma<true, 4>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1393,9 +1395,23 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                         if (c->metric == 1) KNNM_TJ_LAUNCH(1, true, false);
                         else KNNM_TJ_LAUNCH(0, true, false);
                     } else if (lazy) {
-                        if (c->metric == 1) KNNM_TJ_LAUNCH(1, false, true);
-                        else if (c->metric == 2) KNNM_TJ_LAUNCH(2, false, true);
-                        else KNNM_TJ_LAUNCH(0, false, true);
+                        // rows stream through two CJ_DC-dimension buffers
+                        const size_t smem_cj = 2 * (size_t)W * (CJ_DC / 4 + 1) * sizeof(float4);
+                        const void *fc = c->metric == 1 ? (const void *)k_join_chunked<1>
+                                         : c->metric == 2 ? (const void *)k_join_chunked<2>
+                                                          : (const void *)k_join_chunked<0>;
+                        int per_cj = 1;
+                        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_cj, fc, CJ_WARPS * 32, smem_cj));
+                        const unsigned gcj = (unsigned)std::max<int64_t>(
+                            1, std::min<int64_t>(nact, (int64_t)c->sms * std::max(per_cj, 1)));
+#define KNNM_CJ_LAUNCH(T)                                                                          \
+    k_join_chunked<T><<<gcj, CJ_WARPS * 32, smem_cj, c->st>>>(                                     \
+        act, na, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, mode, c->subp, c->dp,           \
+        c->worst0.as<double>(), boff, stt, Bd, Bs, lo_rel, lo_abs)
+                        if (c->metric == 1) KNNM_CJ_LAUNCH(1);
+                        else if (c->metric == 2) KNNM_CJ_LAUNCH(2);
+                        else KNNM_CJ_LAUNCH(0);
+#undef KNNM_CJ_LAUNCH
                     } else {
                         if (c->metric == 1) KNNM_TJ_LAUNCH(1, false, false);
                         else if (c->metric == 2) KNNM_TJ_LAUNCH(2, false, false);

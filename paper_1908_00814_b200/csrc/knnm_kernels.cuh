@@ -1308,6 +1308,293 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
 }
 
 // ---------------------------------------------------------------------------
+// Local join, chunked lazy route (non-certified rows with d > LAZY_MIN_D):
+// the tiled route's arithmetic and emission (approximate slots, LazyExact),
+// but the hood's rows stream through two CJ_DC-dimension shared buffers by
+// TMA (chunk c + 2 loads while c + 1 is computed), so a CTA stages ~1 KB per
+// member instead of a whole 3.8 KB row: several CTAs fit an SM and the row
+// fetches overlap the fp32 work.  Each warp keeps its tiles' running sums in
+// registers across chunks (the same sequential fmaf chains as the tiled
+// route); hoods with more than CJ_TPW patches per warp take extra passes.
+// ---------------------------------------------------------------------------
+constexpr int CJ_DC = 128;  // dimensions per chunk
+constexpr int CJ_TPW = 2;   // patches per warp per pass
+constexpr int CJ_WARPS = 8;
+
+template <int TAG>
+__global__ void __launch_bounds__(CJ_WARPS * 32, 3)
+k_join_chunked(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
+               const int32_t *__restrict__ nlen, int W, int mode, const float *__restrict__ sub,
+               int dp, const double *__restrict__ worst0, const uint64_t *__restrict__ boff,
+               const uint32_t *__restrict__ start, double *__restrict__ Bd, int32_t *__restrict__ Bs,
+               double lo_rel, double lo_abs) {
+    extern __shared__ __align__(128) float4 cv4[];
+    __shared__ int s_id[MAX_W];
+    __shared__ int s_pos[MAX_W];
+    __shared__ int s_new[MAX_W];
+    __shared__ double s_w[MAX_W];
+    __shared__ float s_nrm[MAX_W];
+    __shared__ uint64_t s_st[MAX_W];
+    __shared__ int s_sc[MAX_W];
+    __shared__ PosPrefix s_P;
+    __shared__ int s_cls[4];
+    __shared__ __align__(8) uint64_t s_bar[2];
+    const int tid = threadIdx.x;
+    const unsigned lane = lane_id();
+    const int warp = tid >> 5;
+    constexpr int nwarps = CJ_WARPS;
+    constexpr int QC = CJ_DC / 4 + 1;  // padded chunk row stride in float4
+    const int nch = (dp + CJ_DC - 1) / CJ_DC;
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+    }
+    __syncthreads();
+    uint32_t phase0 = 0, phase1 = 0;
+
+    for (int hi = blockIdx.x; hi < nactive; hi += gridDim.x) {
+        const int64_t u = active[hi];
+        const int w = nlen[u];
+        // ---- classify members (as k_join_tiled) ------------------------------
+        if (tid < 32) {
+            uint32_t ev[4];
+            int clsv[4];
+            int cnts[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                const int j = b * 32 + (int)lane;
+                ev[b] = j < w ? nbh[u * W + j] : 0u;
+            }
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                const int j = b * 32 + (int)lane;
+                int cls = 4;
+                if (j < w) {
+                    const int lab = mode == 0 ? 0 : (int)((ev[b] >> 1) & 1);
+                    cls = lab * 2 + ((ev[b] & 1) ? 0 : 1);
+                }
+                clsv[b] = cls;
+#pragma unroll
+                for (int c = 0; c < 4; c++) cnts[c] += __popc(__ballot_sync(FULL_MASK, cls == c));
+            }
+            int f0 = 0, f1 = cnts[0], f2 = cnts[0] + cnts[1], f3 = cnts[0] + cnts[1] + cnts[2];
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                const int j = b * 32 + (int)lane;
+                const unsigned k0 = __ballot_sync(FULL_MASK, clsv[b] == 0);
+                const unsigned k1 = __ballot_sync(FULL_MASK, clsv[b] == 1);
+                const unsigned k2 = __ballot_sync(FULL_MASK, clsv[b] == 2);
+                const unsigned k3 = __ballot_sync(FULL_MASK, clsv[b] == 3);
+                const unsigned lt = lanemask_lt();
+                const int c = clsv[b];
+                const int slot = c == 0 ? f0 + __popc(k0 & lt) : c == 1 ? f1 + __popc(k1 & lt)
+                               : c == 2 ? f2 + __popc(k2 & lt) : c == 3 ? f3 + __popc(k3 & lt) : -1;
+                f0 += __popc(k0);
+                f1 += __popc(k1);
+                f2 += __popc(k2);
+                f3 += __popc(k3);
+                if (slot >= 0) {
+                    const int id = (int)(ev[b] >> 2);
+                    s_id[slot] = id;
+                    s_pos[slot] = j;
+                    s_new[slot] = (int)(ev[b] & 1);
+                    s_sc[slot] = c;
+                    s_w[slot] = worst0[id];
+                    s_st[slot] = boff[id] + start[u * W + j];
+                    s_nrm[slot] = 0.f;
+                }
+            }
+            build_pos_prefix(s_P, clsv, mode, lane);
+            if (lane < 4) s_cls[lane] = cnts[lane];
+        }
+        __syncthreads();
+        const int H = (w + 1) >> 1;  // even/odd slot split (see k_join_tiled)
+        auto rowc = [&](int buf, int sl) { return cv4 + ((size_t)buf * W + (size_t)((sl & 1) * H + (sl >> 1))) * QC; };
+        // TMA: chunk c of every member row into buffer c & 1
+        auto issue = [&](int c) {
+            if (tid == 0) {
+                const int b = c & 1;
+                const int cw = min(CJ_DC, dp - c * CJ_DC);
+                const uint32_t bytes = (uint32_t)cw * 4u;
+                fence_proxy_async();
+                mbar_expect_tx(&s_bar[b], bytes * (uint32_t)w);
+                for (int sl = 0; sl < w; sl++)
+                    bulk_g2s(rowc(b, sl), sub + (int64_t)s_id[sl] * dp + (int64_t)c * CJ_DC, bytes, &s_bar[b]);
+            }
+        };
+        // ---- blocks / patches (as k_join_tiled) ------------------------------
+        const int nAn = s_cls[0], nAo = s_cls[1], nBn = s_cls[2];
+        const int nA = nAn + nAo;
+        const int b0r0 = 0, b0r1 = mode == 0 ? w : nA, b0c0 = mode == 0 ? 0 : nA, b0c1 = w;
+        const int b0rn = nAn, b0cn = mode == 0 ? nAn : nBn, b0tri = mode == 0;
+        const int b1r0 = nA, b1r1 = w, b1c0 = nA, b1c1 = w, b1rn = nBn, b1cn = nBn;
+        const int nblk = mode == 2 ? 2 : 1;
+        const int nrt0 = (b0r1 - b0r0 + 1) >> 1, nct0 = (b0c1 - b0c0 + 1) >> 1;
+        const int nrt1 = (b1r1 - b1r0 + 1) >> 1, nct1 = (b1c1 - b1c0 + 1) >> 1;
+        // 2x2 tiles enumerated row-major over the block(s); thread tid takes
+        // tiles tid, tid + blockDim, ... (consecutive lanes share the a-row and
+        // read consecutive b-rows: conflict-free, see the even/odd split)
+        const int nt0 = nrt0 * nct0, nt1 = nblk == 2 ? nrt1 * nct1 : 0;
+        const int npatch = nt0 + nt1;  // (tiles)
+        auto geom = [&](int tix, int &i0, int &j0, int &r1, int &c1, bool &tri) {
+            const bool second = tix >= nt0;
+            const int lt = second ? tix - nt0 : tix;
+            const int ncols = second ? nct1 : nct0;
+            const int rt = lt / ncols, ct = lt - rt * ncols;
+            const int r0 = second ? b1r0 : b0r0, c0 = second ? b1c0 : b0c0;
+            r1 = second ? b1r1 : b0r1;
+            c1 = second ? b1c1 : b0c1;
+            const int rn = second ? b1rn : b0rn, cn = second ? b1cn : b0cn;
+            tri = second ? true : (bool)b0tri;
+            i0 = r0 + 2 * rt;
+            j0 = c0 + 2 * ct;
+            bool live = i0 < r1 && j0 < c1;
+            if (live && tri && rt > ct) live = false;
+            if (live && 2 * rt >= rn && 2 * ct >= cn) live = false;
+            return live;
+        };
+        constexpr int PASS = CJ_TPW * nwarps * 32;
+        for (int pg = 0; pg < (npatch > 0 ? npatch : 1); pg += PASS) {
+            const bool norms = TAG == 2 && pg == 0;  // fp32 norms accumulate in the first pass
+            float acc[CJ_TPW][2][2];
+#pragma unroll
+            for (int t = 0; t < CJ_TPW; t++) acc[t][0][0] = acc[t][0][1] = acc[t][1][0] = acc[t][1][1] = 0.f;
+            issue(0);
+            if (nch > 1) issue(1);
+            for (int c = 0; c < nch; c++) {
+                const int b = c & 1;
+                mbar_wait(&s_bar[b], b ? phase1 : phase0);
+                if (b) phase1 ^= 1u;
+                else phase0 ^= 1u;
+                const int q4c = min(CJ_DC, dp - c * CJ_DC) >> 2;
+#pragma unroll
+                for (int t = 0; t < CJ_TPW; t++) {
+                    const int pid = pg + t * nwarps * 32 + tid;
+                    if (pid >= npatch) continue;
+                    int i0, j0, r1, c1;
+                    bool tri;
+                    if (!geom(pid, i0, j0, r1, c1, tri)) continue;
+                    const float4 *a0p = rowc(b, i0);
+                    const float4 *a1p = rowc(b, i0 + 1 < r1 ? i0 + 1 : i0);
+                    const float4 *b0p = rowc(b, j0);
+                    const float4 *b1p = rowc(b, j0 + 1 < c1 ? j0 + 1 : j0);
+                    float x00 = acc[t][0][0], x01 = acc[t][0][1], x10 = acc[t][1][0], x11 = acc[t][1][1];
+#pragma unroll 4
+                    for (int q = 0; q < q4c; q++) {
+                        const float4 a0 = a0p[q], a1 = a1p[q], b0 = b0p[q], b1 = b1p[q];
+                        if (TAG == 1) {
+#define KNNM_CJ_L2(ACC, X, Y)                      \
+    {                                              \
+        float t_;                                  \
+        t_ = X.x - Y.x; ACC = fmaf(t_, t_, ACC);   \
+        t_ = X.y - Y.y; ACC = fmaf(t_, t_, ACC);   \
+        t_ = X.z - Y.z; ACC = fmaf(t_, t_, ACC);   \
+        t_ = X.w - Y.w; ACC = fmaf(t_, t_, ACC);   \
+    }
+                            KNNM_CJ_L2(x00, a0, b0);
+                            KNNM_CJ_L2(x01, a0, b1);
+                            KNNM_CJ_L2(x10, a1, b0);
+                            KNNM_CJ_L2(x11, a1, b1);
+#undef KNNM_CJ_L2
+                        } else if (TAG == 0) {
+#define KNNM_CJ_L1(ACC, X, Y)                                                      \
+    {                                                                              \
+        ACC += fabsf(X.x - Y.x); ACC += fabsf(X.y - Y.y);                          \
+        ACC += fabsf(X.z - Y.z); ACC += fabsf(X.w - Y.w);                          \
+    }
+                            KNNM_CJ_L1(x00, a0, b0);
+                            KNNM_CJ_L1(x01, a0, b1);
+                            KNNM_CJ_L1(x10, a1, b0);
+                            KNNM_CJ_L1(x11, a1, b1);
+#undef KNNM_CJ_L1
+                        } else {
+#define KNNM_CJ_DOT(ACC, X, Y)                                                     \
+    {                                                                              \
+        ACC = fmaf(X.x, Y.x, ACC); ACC = fmaf(X.y, Y.y, ACC);                      \
+        ACC = fmaf(X.z, Y.z, ACC); ACC = fmaf(X.w, Y.w, ACC);                      \
+    }
+                            KNNM_CJ_DOT(x00, a0, b0);
+                            KNNM_CJ_DOT(x01, a0, b1);
+                            KNNM_CJ_DOT(x10, a1, b0);
+                            KNNM_CJ_DOT(x11, a1, b1);
+#undef KNNM_CJ_DOT
+                        }
+                    }
+                    acc[t][0][0] = x00;
+                    acc[t][0][1] = x01;
+                    acc[t][1][0] = x10;
+                    acc[t][1][1] = x11;
+                }
+                if (norms) {
+                    for (int sl = warp; sl < w; sl += nwarps) {
+                        float a = 0.f;
+                        const float4 *rp = rowc(b, sl);
+                        for (int q = lane; q < q4c; q += 32) {
+                            const float4 v = rp[q];
+                            a = fmaf(v.x, v.x, a);
+                            a = fmaf(v.y, v.y, a);
+                            a = fmaf(v.z, v.z, a);
+                            a = fmaf(v.w, v.w, a);
+                        }
+#pragma unroll
+                        for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(FULL_MASK, a, o);
+                        if (lane == 0) s_nrm[sl] += a;
+                    }
+                }
+                __syncthreads();  // buffer b is free again
+                if (c + 2 < nch) issue(c + 2);
+            }
+            // ---- emission: approximate slots (LazyExact), as k_join_tiled ----
+#pragma unroll
+            for (int t = 0; t < CJ_TPW; t++) {
+                const int pid = pg + t * nwarps * 32 + tid;
+                if (pid >= npatch) continue;
+                int i0, j0, r1, c1;
+                bool tri;
+                const bool live = geom(pid, i0, j0, r1, c1, tri);
+#pragma unroll
+                for (int s4 = 0; s4 < 4; s4++) {
+                    const int ii = i0 + (s4 >> 1), jj = j0 + (s4 & 1);
+                    bool ok = live && ii < r1 && jj < c1;
+                    if (ok && tri) ok = ii < jj;
+                    if (ok) ok = s_new[ii] || s_new[jj];
+                    if (!ok) continue;
+                    const float f = acc[t][s4 >> 1][s4 & 1];
+                    float v;
+                    double lb;
+                    if (TAG == 2) {
+                        const float na = s_nrm[ii], nb = s_nrm[jj];
+                        if (na >= 1e-30f && nb >= 1e-30f && na <= 1e30f && nb <= 1e30f) {
+                            v = fmaxf(1.0f - f / (sqrtf(na) * sqrtf(nb)), 0.0f);
+                            lb = (double)v - lo_abs;
+                        } else {
+                            v = 0.0f;
+                            lb = -lo_abs;
+                        }
+                    } else {
+                        v = (f >= 1e-30f && f <= 1e30f) ? f : 0.0f;
+                        lb = (double)v * lo_rel;
+                    }
+                    const double dd = -(double)v;
+                    const int pi = s_pos[ii], pj = s_pos[jj];
+                    if (lb < s_w[ii]) {
+                        const uint64_t sij = s_st[ii] + pair_rank(s_P, mode, s_sc[ii], pi, pj);
+                        Bd[sij] = dd;
+                        Bs[sij] = s_id[jj];
+                    }
+                    if (lb < s_w[jj]) {
+                        const uint64_t sji = s_st[jj] + pair_rank(s_P, mode, s_sc[jj], pj, pi);
+                        Bd[sji] = dd;
+                        Bs[sji] = s_id[ii];
+                    }
+                }
+            }
+        }
+        __syncthreads();  // metadata reused by the next hood
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Local join, tensor-core route for datasets with a dot-form exactness
 // certificate (integer entries, |v| <= 2048, 2*d*max|v|^2 < 2^24): rows are
 // staged as fp16 (exact), the member Gram block is computed with
