@@ -406,6 +406,18 @@ __device__ __noinline__ double lazy_warp_eval_t(const LazyExact z, int64_t r, bo
         }
         const unsigned grp = M & ~mm;
         M = mm;
+        // pull the group's rows toward L2 first: the block loads below then
+        // wait on L2 instead of HBM latency
+        {
+            const int lines = (z.d * 4 + 127) >> 7;
+            for (int j = 0; j <= LZ_G; j++) {
+                if (j < P || j == LZ_G) {
+                    const float *rp = j == LZ_G ? ra : z.sub + (int64_t)cid[j < LZ_G ? j : 0] * z.dp;
+                    for (int l = (int)lane; l < lines; l += 32)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + l * 32));
+                }
+            }
+        }
         double acc = 0.0;
         // one block ahead in registers
         float xn = lane < (unsigned)z.d ? __ldg(ra + lane) : 0.f;
