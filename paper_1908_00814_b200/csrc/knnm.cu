@@ -1192,10 +1192,12 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         TRY(scan<uint32_t, uint32_t>(c, c->indeg.as<uint32_t>(), c->roff.as<uint32_t>(), n));
         k_rev_fill<<<grid_for(c, n * k, 256), 256, 0, c->st>>>(
             c->ids.as<int32_t>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), n, k,
-            c->roff.as<uint32_t>(), c->indeg.as<uint32_t>(), c->rev.as<uint32_t>(), lo, hi);
+            c->roff.as<uint32_t>(), c->indeg.as<uint32_t>(), c->rev.as<uint32_t>(), lo, hi,
+            c->live.as<uint8_t>());
         CKL();
         k_find_heavy<<<grid_for(c, hi - lo, 256), 256, 0, c->st>>>(
-            c->roff.as<uint32_t>(), lo, hi, std::max(rev_cap, WARP_REV_MAX), c->heavy.as<int32_t>(), cnt);
+            c->roff.as<uint32_t>(), lo, hi, std::max(rev_cap, WARP_REV_MAX), c->heavy.as<int32_t>(), cnt,
+            c->live.as<uint8_t>());
         CKL();
         k_rev_heavy<<<c->sms * 2, 256, 2 * sizeof(uint32_t) * BLOCK_SORT_MAX, c->st>>>(
             c->heavy.as<int32_t>(), cnt, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(), rev_cap,

@@ -491,16 +491,18 @@ __global__ void k_rev_count(const int32_t *__restrict__ ids, const uint8_t *__re
     }
 }
 
+// Only targets whose hood will be assembled (live, see k_rev_count) get
+// their reverse segment filled; the offsets still count every edge.
 __global__ void k_rev_fill(const int32_t *__restrict__ ids, const uint8_t *__restrict__ flags,
                            const int32_t *__restrict__ sizes, int64_t n, int k,
                            const uint32_t *__restrict__ roff, uint32_t *indeg, uint32_t *rev,
-                           int64_t tlo, int64_t thi) {
+                           int64_t tlo, int64_t thi, const uint8_t *__restrict__ live) {
     int64_t total = n * k;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         int64_t r = i / k;
         int t = (int)(i % k);
-        if (t < sizes[r] && ids[i] >= tlo && ids[i] < thi && flags[i] != 2) {
+        if (t < sizes[r] && ids[i] >= tlo && ids[i] < thi && flags[i] != 2 && live[ids[i]]) {
             int32_t j = ids[i];
             uint32_t p = roff[j] + atomicSub(&indeg[j], 1u) - 1u;
             rev[p] = ((uint32_t)r << 1) | (uint32_t)flags[i];
@@ -509,11 +511,12 @@ __global__ void k_rev_fill(const int32_t *__restrict__ ids, const uint8_t *__res
 }
 
 __global__ void k_find_heavy(const uint32_t *__restrict__ roff, int64_t lo, int64_t n, int limit,
-                             int32_t *heavy, unsigned long long *counters) {
+                             int32_t *heavy, unsigned long long *counters,
+                             const uint8_t *__restrict__ live) {
     for (int64_t u = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
          u += (int64_t)gridDim.x * blockDim.x) {
         uint32_t deg = roff[u + 1] - roff[u];
-        if (deg > (uint32_t)limit) {
+        if (deg > (uint32_t)limit && live[u]) {
             unsigned long long p = atomicAdd(&counters[C_HEAVY_REV], 1ull);
             heavy[p] = (int32_t)u;
             atomicMax(&counters[C_MAXDEG], (unsigned long long)deg);
