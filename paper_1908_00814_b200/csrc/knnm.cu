@@ -18,6 +18,11 @@
 
 using namespace knnm;
 
+struct knnm_ctx;
+extern "C" {
+static int phi_kernels(knnm_ctx *c, const double **res);  // defined with knnm_phi
+}
+
 namespace {
 
 thread_local std::string g_err;
@@ -101,6 +106,10 @@ struct knnm_ctx {
     DBuf f32chk;            // loaded list distances not exact in fp32 (count)
     DBuf live;              // per row: its hood can hold a new entry this round
     DBuf segheavy;          // rows with > SEG_SMEM memberships (k_seg_rank_heavy)
+    uint64_t state_gen = 1;      // bumped by every call that may change the lists
+    uint64_t phi_gen = 0;        // state_gen phi_val was computed at
+    double phi_val = 0.0;
+    bool phi_in_updates = false; // the round's apply also computes phi (one sync)
     void *stg_buf[2] = {nullptr, nullptr};  // pinned staging for pageable copies
     cudaEvent_t stg_ev[2] = {nullptr, nullptr};
     bool stg_busy[2] = {false, false};
@@ -431,7 +440,14 @@ int run_updates(knnm_ctx *c) {
     }
 #undef KNNM_AP_LAUNCH
     CKL();
+    // a round's final apply also reduces phi, fetched in the same wait
+    const double *phi_res = nullptr;
+    if (c->phi_in_updates && c->n * c->k > 0) TRY(phi_kernels(c, &phi_res));
     TRY(sync_counters(c));
+    if (phi_res) {
+        CK(cudaMemcpy(&c->phi_val, phi_res, sizeof(double), cudaMemcpyDeviceToHost));
+        c->phi_gen = c->state_gen;
+    }
     c->stats.candidates += (int64_t)c->hcnt[C_CAND];
     c->stats.written_slots += (int64_t)c->hcnt[C_WRITTEN];
     return KNNM_OK;
@@ -742,6 +758,7 @@ int knnm_set_dataset(knnm_ctx *c, const float *vectors, int64_t n_all, int32_t d
 }
 
 int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *labels, int32_t k) {
+    if (c) c->state_gen++;  // the lists may change: cached phi is stale
     if (!c || !union_gids || !labels) return fail(KNNM_ERR_ARG, "null argument");
     if (!c->have_data) return fail(KNNM_ERR_STATE, "knnm_set_dataset first");
     if (n < 1) return fail(KNNM_ERR_ARG, "empty union");
@@ -836,6 +853,7 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
 static int load_impl(knnm_ctx *c, const int32_t *rows, int64_t m, const int32_t *g_ids,
                      const double *g_dists, const int32_t *g_sizes, int32_t gk, int32_t k1,
                      bool on_device) {
+    if (c) c->state_gen++;  // the lists may change: cached phi is stale
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     if (m == 0) return KNNM_OK;
@@ -906,6 +924,7 @@ int knnm_load_graph_dev(knnm_ctx *c, const int32_t *rows, int64_t m, const int32
 
 static int insert_impl(knnm_ctx *c, const int32_t *rows, int64_t mrows, int32_t count,
                        const int32_t *nids, int64_t m, int64_t *accepted, bool nids_on_device) {
+    if (c) c->state_gen++;  // the lists may change: cached phi is stale
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     if (accepted) *accepted = 0;
@@ -1140,6 +1159,7 @@ int knnm_draws_replace(knnm_ctx *c, const int64_t *rows, int64_t nrows, const in
 
 int knnm_draws_insert(knnm_ctx *c, const int32_t *rows, const int32_t *pool, int64_t npool,
                       int64_t *accepted) {
+    if (c) c->state_gen++;  // the lists may change: cached phi is stale
     if (!c || !rows || !pool) return fail(KNNM_ERR_ARG, "bad argument");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     CK(cudaSetDevice(c->device));
@@ -1159,6 +1179,7 @@ int knnm_draws_insert(knnm_ctx *c, const int32_t *rows, const int32_t *pool, int
 
 static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed,
                       int64_t *pairs, int64_t *accepted, bool local_only) {
+    if (c) c->state_gen++;  // the lists may change: cached phi is stale
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     if (mode < 0 || mode > 2) return fail(KNNM_ERR_ARG, "mode %d", mode);
@@ -1197,17 +1218,18 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         CKL();
         k_find_heavy<<<grid_for(c, hi - lo, 256), 256, 0, c->st>>>(
             c->roff.as<uint32_t>(), lo, hi, std::max(rev_cap, WARP_REV_MAX), c->heavy.as<int32_t>(), cnt,
-            c->live.as<uint8_t>());
+            c->live.as<uint8_t>(), c->giant.as<int32_t>(), BLOCK_SORT_MAX);
         CKL();
         k_rev_heavy<<<c->sms * 2, 256, 2 * sizeof(uint32_t) * BLOCK_SORT_MAX, c->st>>>(
             c->heavy.as<int32_t>(), cnt, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(), rev_cap,
             round_seed, nullptr, BLOCK_SORT_MAX);
         CKL();
-        TRY(sync_counters(c));
-        unsigned long long maxdeg = c->hcnt[C_MAXDEG];
-        if (c->hcnt[C_HEAVY_REV] && next_pow2((uint32_t)maxdeg) > (uint32_t)BLOCK_SORT_MAX) {
-            TRY(ensure(c->gscratch32, 2 * sizeof(uint32_t) * next_pow2((uint32_t)maxdeg)));
-            k_rev_heavy<<<1, 1024, 0, c->st>>>(c->heavy.as<int32_t>(), cnt, c->roff.as<uint32_t>(),
+        // rows too long for a block's shared memory (in-degree above
+        // BLOCK_SORT_MAX): one block in global scratch sized for any degree
+        // (<= n); it finds them from the device-side list, so no host sync
+        if (next_pow2((uint32_t)n) > (uint32_t)BLOCK_SORT_MAX) {
+            TRY(ensure(c->gscratch32, 2 * sizeof(uint32_t) * next_pow2((uint32_t)n)));
+            k_rev_heavy<<<1, 1024, 0, c->st>>>(c->giant.as<int32_t>(), cnt, c->roff.as<uint32_t>(),
                                                c->rev.as<uint32_t>(), rev_cap, round_seed,
                                                c->gscratch32.as<uint32_t>(), BLOCK_SORT_MAX);
             CKL();
@@ -1454,7 +1476,10 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         if (local_only && 2 * P > budget)
             return fail(KNNM_ERR_LIMIT, "sharded round needs %llu slots > budget", (unsigned long long)(2 * P));
         if (2 * P <= budget) {
-            TRY(run_chunk(c->active.as<int32_t>(), (int64_t)nactive, 2 * P, true));
+            c->phi_in_updates = !local_only;
+            const int rc = run_chunk(c->active.as<int32_t>(), (int64_t)nactive, 2 * P, true);
+            c->phi_in_updates = false;
+            TRY(rc);
         } else {
             // Chunk hoods by index so each chunk's buckets fit; chunks run in
             // ascending hood order, which preserves the reference's per-row
@@ -1534,6 +1559,7 @@ int knnm_local_views(knnm_ctx *c, void **cnt, void **boff, void **Bd, void **Bs)
 
 int knnm_round_apply(knnm_ctx *c, int32_t nsrc, const uint32_t *recv_cnt, const uint64_t *recv_base,
                      const double *recv_Bd, const int32_t *recv_Bs, int64_t *accepted) {
+    if (c) c->state_gen++;  // the lists may change: cached phi is stale
     if (!c || nsrc < 1 || !recv_cnt || !recv_base) return fail(KNNM_ERR_ARG, "bad argument");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     CK(cudaSetDevice(c->device));
@@ -1578,6 +1604,7 @@ int knnm_round_apply(knnm_ctx *c, int32_t nsrc, const uint32_t *recv_cnt, const 
 }
 
 int knnm_state_views(knnm_ctx *c, void **ids, void **dists, void **flags, void **sizes) {
+    if (c) c->state_gen++;  // the lists may change: cached phi is stale
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     if (ids) *ids = c->ids.p;
@@ -1703,16 +1730,10 @@ int knnm_sample_distinct_rows(uint64_t *pcg, int32_t *has_uint32, uint32_t *uint
     return KNNM_OK;
 }
 
-int knnm_phi(knnm_ctx *c, double *out) {
-    if (!c || !out) return fail(KNNM_ERR_ARG, "null argument");
-    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
-    CK(cudaSetDevice(c->device));
+// Launch the phi reduction (numpy's pairwise tree over the present
+// distances); *res = device address of the result.
+static int phi_kernels(knnm_ctx *c, const double **res) {
     int64_t N = c->n * c->k;
-    if (N == 0) {
-        *out = 0.0;
-        return KNNM_OK;
-    }
-    PhaseTimer pt(c, PH_OTHER);
     if (c->phi.N != N) {
         build_phi_tree(c->phi, N);
         size_t nl = c->phi.leaf_lo.size(), ni = c->phi.left.size();
@@ -1756,16 +1777,38 @@ int knnm_phi(knnm_ctx *c, double *out) {
                                               c->phi_leaves.as<double>(), c->phi_inner.as<double>());
             CKL();
         }
-        TRY(d2h(c, out, c->phi_inner.as<double>() + (ni - 1), sizeof(double)));
+        *res = c->phi_inner.as<double>() + (ni - 1);
     } else {
-        TRY(d2h(c, out, c->phi_leaves.p, sizeof(double)));
+        *res = c->phi_leaves.as<double>();
     }
+    return KNNM_OK;
+}
+
+int knnm_phi(knnm_ctx *c, double *out) {
+    if (!c || !out) return fail(KNNM_ERR_ARG, "null argument");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    CK(cudaSetDevice(c->device));
+    if (c->n * c->k == 0) {
+        *out = 0.0;
+        return KNNM_OK;
+    }
+    if (c->phi_gen == c->state_gen) {  // computed by the last round, lists unchanged since
+        *out = c->phi_val;
+        return KNNM_OK;
+    }
+    PhaseTimer pt(c, PH_OTHER);
+    const double *r = nullptr;
+    TRY(phi_kernels(c, &r));
+    CK(cudaMemcpyAsync(&c->phi_val, r, sizeof(double), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
+    c->phi_gen = c->state_gen;
+    *out = c->phi_val;
     return KNNM_OK;
 }
 
 static int export_impl(knnm_ctx *c, int32_t merge_rear, int32_t *out_ids, double *out_dists,
                        int32_t *out_sizes, bool on_device) {
+    if (c) c->state_gen++;  // the lists may change: cached phi is stale
     if (!c || !out_ids || !out_dists || !out_sizes) return fail(KNNM_ERR_ARG, "null argument");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     CK(cudaSetDevice(c->device));

@@ -26,7 +26,8 @@ enum Counter {
     C_MAXC = 10,      // max candidates on a giant row
     C_WRITTEN = 11,   // update slots written by the join (prefilter survivors)
     C_SEGHEAVY = 12,  // rows with > SEG_SMEM memberships (block-ranked)
-    C_NUM = 16
+    C_GIANT = 13,     // heavy rows whose reverse segment exceeds a block's smem
+    C_NUM = 20
 };
 
 // splitmix64 output for a state that was already advanced (_kernels.py:306-313).

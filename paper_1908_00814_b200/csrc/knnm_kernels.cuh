@@ -512,13 +512,15 @@ __global__ void k_rev_fill(const int32_t *__restrict__ ids, const uint8_t *__res
 
 __global__ void k_find_heavy(const uint32_t *__restrict__ roff, int64_t lo, int64_t n, int limit,
                              int32_t *heavy, unsigned long long *counters,
-                             const uint8_t *__restrict__ live) {
+                             const uint8_t *__restrict__ live, int32_t *giant, int smem_max) {
     for (int64_t u = lo + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
          u += (int64_t)gridDim.x * blockDim.x) {
         uint32_t deg = roff[u + 1] - roff[u];
         if (deg > (uint32_t)limit && live[u]) {
             unsigned long long p = atomicAdd(&counters[C_HEAVY_REV], 1ull);
             heavy[p] = (int32_t)u;
+            // too long for a block's shared memory: the global-scratch pass
+            if (next_pow2(deg) > (uint32_t)smem_max) giant[atomicAdd(&counters[C_GIANT], 1ull)] = (int32_t)u;
             atomicMax(&counters[C_MAXDEG], (unsigned long long)deg);
         }
     }
@@ -554,12 +556,14 @@ __device__ void block_fy_select(uint32_t *seg, uint32_t *idx, uint32_t *R, uint3
 
 // Heavy reverse segments: one block per vertex, shared-memory sort.  The
 // selected entries overwrite the first rev_cap slots of the segment.
+// gscratch == nullptr: the rows of `heavy` that fit shared memory; else the
+// `giant` list (counters[C_GIANT]) in global scratch.
 __global__ void k_rev_heavy(const int32_t *__restrict__ heavy, const unsigned long long *counters,
                             const uint32_t *__restrict__ roff, uint32_t *rev, int rev_cap,
                             uint64_t seed, uint32_t *gscratch, int smem_max) {
     extern __shared__ uint32_t hs[];
     __shared__ uint32_t R[MAX_W];
-    unsigned long long cnt = counters[C_HEAVY_REV];
+    unsigned long long cnt = counters[gscratch ? C_GIANT : C_HEAVY_REV];
     for (unsigned long long h = blockIdx.x; h < cnt; h += gridDim.x) {
         int64_t u = heavy[h];
         uint32_t lo = roff[u];
