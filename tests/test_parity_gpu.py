@@ -222,3 +222,20 @@ def test_rho_validation():
         km.MergeParams(k=10, rho=0.0)
     with pytest.raises(ValueError):
         km.DescentParams(k=10, rho=1.5)
+
+
+def test_staged_host_transfers_large(oracle):
+    """Host arrays above the 8 MB staging threshold in both directions (the
+    dataset upload and the exported dists go through the pinned double
+    buffer, several chunks each) -- results stay bit-identical."""
+    km = _km()
+    n, d, k = 60000, 40, 20  # vectors 9.6 MB, exported dists 9.6 MB
+    ds = km.generate_uniform(n, d, seed=11)
+    assert ds.vectors.nbytes > 8 << 20 and n * k * 8 > 8 << 20
+    s1, s2 = split_ids(n, seed=12)
+    g, _, _ = oracle.nn_descent(ds.vectors, 1, k, 1, member_ids=s1, max_iters=3)
+    h, _, _ = oracle.nn_descent(ds.vectors, 1, k, 2, member_ids=s2, max_iters=3)
+    mp = km.MergeParams(k=k, seed=3, max_iters=3)
+    u = km.s_merge(ds, _to_graph(km, g), _to_graph(km, h), mp)
+    ou, _, _ = oracle.s_merge(ds.vectors, g, h, k, seed=3, max_iters=3)
+    _same_graph(u, ou)
