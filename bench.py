@@ -193,9 +193,11 @@ def run_reference(args):
               "oracle C/OpenMP restatement of the reference kernels")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": "config2_smerge_2x500k_d128_k20",
-                                            "sample_points": n, "parallelism": "host threads"},
+                                            "n": CFG["n"], "d": CFG["d"], "k": CFG["k"], "r": CFG["r"],
+                                            "metric": "l2", "rho": 1.0, "sample_points": n,
+                                            "parallelism": "host threads"},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                              "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
