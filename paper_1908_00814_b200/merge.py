@@ -94,13 +94,10 @@ def _merge_members(a: np.ndarray, b: np.ndarray, with_overlap: bool = False):
     """(union, rows of a, rows of b) for disjoint ascending id arrays in one
     linear pass: np.union1d + np.searchsorted of merge.py:217-221.  With
     with_overlap, also whether a and b share an id (merge.py:181)."""
-    if not (_ascending(a) and _ascending(b)):
-        u = np.union1d(a, b)
-        out = (u, _lookup_local(u, a), _lookup_local(u, b))
-        return out + (bool(np.intersect1d(a, b).size),) if with_overlap else out
     na, nb = a.size, b.size
     if a.dtype == np.int64 and b.dtype == np.int64:
-        # native linear merge (libknnm.so, host-only)
+        # native linear merge (libknnm.so, host-only); it rejects inputs that
+        # are not strictly ascending, which take the numpy path below
         import ctypes
 
         from . import _lib
@@ -111,13 +108,18 @@ def _merge_members(a: np.ndarray, b: np.ndarray, with_overlap: bool = False):
         ra = np.empty(na, dtype=np.int32)
         rb = np.empty(nb, dtype=np.int32)
         nu, sh = ctypes.c_int64(), ctypes.c_int32()
-        _lib.check(_lib.load().knnm_merge_members(_lib.ptr(a), na, _lib.ptr(b), nb, _lib.ptr(uni),
-                                                  _lib.ptr(ra), _lib.ptr(rb), ctypes.byref(nu),
-                                                  ctypes.byref(sh)), "knnm_merge_members")
-        if with_overlap:
-            return uni[: nu.value], ra, rb, bool(sh.value)
-        if not sh.value:
-            return uni[: nu.value], ra, rb
+        rc = _lib.load().knnm_merge_members(_lib.ptr(a), na, _lib.ptr(b), nb, _lib.ptr(uni),
+                                            _lib.ptr(ra), _lib.ptr(rb), ctypes.byref(nu),
+                                            ctypes.byref(sh))
+        if rc == 0:
+            if with_overlap:
+                return uni[: nu.value], ra, rb, bool(sh.value)
+            if not sh.value:
+                return uni[: nu.value], ra, rb
+    if not (_ascending(a) and _ascending(b)):
+        u = np.union1d(a, b)
+        out = (u, _lookup_local(u, a), _lookup_local(u, b))
+        return out + (bool(np.intersect1d(a, b).size),) if with_overlap else out
     top = max(int(a[-1]) if na else -1, int(b[-1]) if nb else -1) + 1
     if na and nb and int(min(a[0], b[0])) >= 0 and top <= 4 * (na + nb):
         # dense id range: O(range) marker pass instead of a sort
@@ -190,7 +192,7 @@ def _append_random(engine, rows, pool, count, rng, counter, on_pair, gids) -> No
     bad = engine.draws_gen(rng, m, rows.size, t)
     while bad.size:
         bad = engine.draws_regen(rng, m, bad)
-    engine.draws_insert(rows.astype(np.int32), pool.astype(np.int32))
+    engine.draws_insert(np.asarray(rows, dtype=np.int32), np.asarray(pool, dtype=np.int32))
     counter.add(rows.size * t)
     _emit_captured(engine, on_pair, gids)
 
@@ -240,9 +242,9 @@ def s_merge(dataset, g: KnnGraph, h: KnnGraph, params: MergeParams,
         eng.load_graph(rows_g, g, k1)
         eng.load_graph(rows_h, h, k1)
         fill = k - k1
-        _append_random(eng, rows_g, rows_h.astype(np.int64), min(fill, rows_h.size), rng,
+        _append_random(eng, rows_g, rows_h, min(fill, rows_h.size), rng,
                        counter, on_pair, union_gids)
-        _append_random(eng, rows_h, rows_g.astype(np.int64), min(fill, rows_g.size), rng,
+        _append_random(eng, rows_h, rows_g, min(fill, rows_g.size), rng,
                        counter, on_pair, union_gids)
         report = BuildReport(phi_initial=eng.phi())
         _descent_rounds(eng, n, MODE_CROSS, k, params.descent_params(), rng, counter, on_pair,
@@ -292,7 +294,7 @@ def j_merge(dataset, g: KnnGraph, raw_ids, params: MergeParams,
     _capture(eng, on_pair)
     try:
         eng.load_graph(rows_g, g, k1)
-        _append_random(eng, rows_g, rows_raw.astype(np.int64), min(k - k1, rows_raw.size), rng,
+        _append_random(eng, rows_g, rows_raw, min(k - k1, rows_raw.size), rng,
                        counter, on_pair, union_gids)
         # raw lists start from k random draws over the whole union (merge.py:318-325)
         init = sample_distinct_rows(rng, n, k, rows_raw)  # natively, same stream
