@@ -239,3 +239,27 @@ def test_staged_host_transfers_large(oracle):
     u = km.s_merge(ds, _to_graph(km, g), _to_graph(km, h), mp)
     ou, _, _ = oracle.s_merge(ds.vectors, g, h, k, seed=3, max_iters=3)
     _same_graph(u, ou)
+
+
+@pytest.mark.parametrize("n,d,k,metric,kind", [
+    (3000, 16, 64, 1, "intgmm"),   # W = 2k = 128 = MAX_W: u8 tensor-core route, 4 position blocks
+    (2500, 12, 64, 1, "uniform"),  # same width on the non-certified tiled route
+    (1200, 1, 8, 1, "uniform"),    # d = 1 (padded rows)
+])
+def test_limits_match_oracle(oracle, n, d, k, metric, kind):
+    km = _km()
+    ds = _data(km, n, d, kind, seed=n + d + 7)
+    s1, s2 = split_ids(n, seed=13)
+    g, _, _ = oracle.nn_descent(ds.vectors, metric, k, 1, member_ids=s1)
+    h, _, _ = oracle.nn_descent(ds.vectors, metric, k, 2, member_ids=s2)
+    c = km.DistanceCounter()
+    u, rep = km.s_merge(ds, _to_graph(km, g), _to_graph(km, h), km.MergeParams(k=k, seed=3),
+                        counter=c, return_report=True)
+    ou, orep, ocount = oracle.s_merge(ds.vectors, g, h, k, seed=3)
+    _same_graph(u, ou)
+    _same_report(rep, orep)
+    assert c.count == ocount
+    gg, rep = km.nn_descent(ds, metric, km.DescentParams(k=k), 4, member_ids=s1, return_report=True)
+    og, orep, _ = oracle.nn_descent(ds.vectors, metric, k, 4, member_ids=s1)
+    _same_graph(gg, og)
+    _same_report(rep, orep)
