@@ -977,7 +977,8 @@ static int insert_impl(knnm_ctx *c, const int32_t *rows, int64_t mrows, int32_t 
                 rows_d, c->stage[1].as<int32_t>() + c0, cm, c->subp, c->dp, c->d, c->metric,
                 (int)(c->cert && c->metric != KNNM_COSINE), c->sizes.as<int32_t>(), c->dists.as<double>(), c->k, c->boff.as<uint64_t>(),
                 c->start.as<uint32_t>(), c->Bd.as<double>(), c->Bs.as<int32_t>(),
-                capd ? capd + c0 : nullptr);
+                capd ? capd + c0 : nullptr, c->cert_u8 ? c->sub16p : nullptr, c->rowb,
+                c->cert_u8 ? c->subnormp : nullptr);
             CKL();
         }
         {

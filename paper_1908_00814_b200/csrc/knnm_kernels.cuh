@@ -403,16 +403,35 @@ __device__ __forceinline__ double cert_dist(const float *__restrict__ a, const f
     return (double)((s0 + s1) + (s2 + s3));
 }
 
+// u8 rows (entries in [0, 255], the u8 certificate): exact integer
+// |a|^2 + |b|^2 - 2 a.b from 128-bit loads and dp4a (rowb bytes per row).
+__device__ __forceinline__ double u8_dist(const uint8_t *__restrict__ a, const uint8_t *__restrict__ b, int rowb,
+                                          float na, float nb) {
+    const uint4 *a4 = reinterpret_cast<const uint4 *>(a);
+    const uint4 *b4 = reinterpret_cast<const uint4 *>(b);
+    unsigned dot = 0;
+    for (int c = 0; c < (rowb >> 4); c++) {
+        const uint4 x = __ldg(a4 + c), y = __ldg(b4 + c);
+        dot = __dp4a(x.x, y.x, dot);
+        dot = __dp4a(x.y, y.y, dot);
+        dot = __dp4a(x.z, y.z, dot);
+        dot = __dp4a(x.w, y.w, dot);
+    }
+    return (double)((long long)__float_as_int(na) + (long long)__float_as_int(nb) - 2ll * (long long)dot);
+}
+
 __global__ void k_directed_emit(const int32_t *__restrict__ rows, const int32_t *__restrict__ nids,
                                 int64_t m, const float *__restrict__ sub, int dp, int d, int tag, int cert,
                                 const int32_t *__restrict__ sizes, const double *__restrict__ dists,
                                 int k, const uint64_t *__restrict__ boff,
                                 const uint32_t *__restrict__ start, double *__restrict__ Bd,
-                                int32_t *__restrict__ Bs, double *cap_d) {
+                                int32_t *__restrict__ Bs, double *cap_d, const uint8_t *__restrict__ sub8,
+                                int rowb, const float *__restrict__ norms8) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int32_t r = rows[i], s = nids[i];
-        const double dd = cert ? cert_dist(sub + (int64_t)r * dp, sub + (int64_t)s * dp, dp, tag)
+        const double dd = sub8 ? u8_dist(sub8 + (int64_t)r * rowb, sub8 + (int64_t)s * rowb, rowb, norms8[r], norms8[s])
+                        : cert ? cert_dist(sub + (int64_t)r * dp, sub + (int64_t)s * dp, dp, tag)
                                : exact_dist_tag(tag, sub + (int64_t)r * dp, sub + (int64_t)s * dp, d);
         if (cap_d) cap_d[i] = dd;
         const uint64_t slot = boff[r] + start[i];
