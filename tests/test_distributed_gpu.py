@@ -82,3 +82,39 @@ def test_sharded_rho_sampling_bit_identical(oracle, world):
     assert np.array_equal(got.dists, want.dists)
     assert [(r.pairs, r.updates, r.phi) for r in rep_g.rounds] == \
         [(r.pairs, r.updates, r.phi) for r in rep_w.rounds]
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_sharded_random_cases(seed):
+    """Random shapes / metrics / r / rho / world sizes: sharded == single GPU."""
+    import paper_1908_00814_b200 as km
+    from paper_1908_00814_b200 import distributed as D
+
+    rng = np.random.default_rng(500 + seed)
+    world = int(rng.integers(2, 5))
+    n = int(rng.integers(400, 3000))
+    kind = ["uniform", "intgmm", "sphere"][rng.integers(0, 3)]
+    d = int(rng.choice([4, 16, 64, 100]))
+    metric = km.Metric.COSINE if kind == "sphere" else km.Metric(int(rng.integers(0, 2)))
+    k = int(rng.integers(4, 24))
+    ds = (km.generate_uniform(n, d, seed=seed) if kind == "uniform"
+          else km.generate_int_gmm(n, d, n_centres=12, seed=seed) if kind == "intgmm"
+          else km.generate_sphere_gmm(n, d, n_centres=12, seed=seed))
+    s1, s2 = split_ids(n, seed=seed + 1)
+    mp = km.MergeParams(k=k, r=float(rng.choice([0.0, 0.5, 1.0])), seed=seed,
+                        rho=float(rng.choice([1.0, 0.5])))
+    g = km.nn_descent(ds, metric, km.DescentParams(k=k), 1, member_ids=s1)
+    if rng.integers(0, 2):
+        h = km.nn_descent(ds, metric, km.DescentParams(k=k), 2, member_ids=s2)
+        want, rw = km.s_merge(ds, g, h, mp, return_report=True)
+        got, rg = D.s_merge_sharded(ds, g, h, mp, D.LoopbackComm(world), _engines(world),
+                                    return_report=True)
+    else:
+        want, rw = km.j_merge(ds, g, s2, mp, return_report=True)
+        got, rg = D.j_merge_sharded(ds, g, s2, mp, D.LoopbackComm(world), _engines(world),
+                                    return_report=True)
+    assert np.array_equal(got.ids, want.ids)
+    assert np.array_equal(got.dists, want.dists)
+    assert np.array_equal(got.sizes, want.sizes)
+    assert [(r.pairs, r.updates, r.phi) for r in rg.rounds] == \
+        [(r.pairs, r.updates, r.phi) for r in rw.rounds]
