@@ -222,6 +222,8 @@ def run_b200(args):
     t_setup = time.perf_counter()
     ds, s1, s2 = make_inputs(km, n)
     eng = get_engine(local)
+    if args.join_variant is not None:  # route experiments (default: auto)
+        eng.set_join_variant(args.join_variant)
     # subgraphs (untimed), kept resident in HBM as device tensors for `value`
     g_dev = km.nn_descent(ds, km.Metric.L2, km.DescentParams(k=k), CFG["g_seed"], member_ids=s1,
                           device=local, out_device=True)
@@ -439,6 +441,8 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0, help="fraction of the config size")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
     ap.add_argument("--no-recall", action="store_true")
+    ap.add_argument("--join-variant", type=int, default=None,
+                    help="force a join route (0 exact, 1 tiled, 2 tensor core)")
     ap.add_argument("--no-rho-half", action="store_true",
                     help="skip the rho = 0.5 leg (BASELINE's config-2 sample rate)")
     args = ap.parse_args()
