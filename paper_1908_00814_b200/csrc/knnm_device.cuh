@@ -481,17 +481,17 @@ template <int E, typename T = double>
 __device__ __forceinline__ int warp_apply_chunk(WarpRow<E, T> &s, int k, int src_l, T d_l,
                                                 int cnt, unsigned lane) {
     int acc = 0;
-    int i = -1;
-    while (true) {
-        // d_l = +inf marks an empty slot (real distances are finite)
-        bool live = (int)lane > i && (int)lane < cnt && d_l < dist_inf<T>() &&
-                    (s.sz < k || d_l < s.worst);
-        unsigned m = __ballot_sync(FULL_MASK, live);
-        if (!m) break;
-        i = __ffs(m) - 1;
-        int src = __shfl_sync(FULL_MASK, src_l, i);
-        T nd = __shfl_sync(FULL_MASK, d_l, i);
-        acc += warp_insert<E, false, T>(s, k, src, nd, lane);  // live: not full or nd < worst
+    // d_l = +inf marks an empty slot (real distances are finite); a candidate
+    // live at chunk start is re-tested against the current worst when its
+    // turn comes (the worst only decreases once the row is full)
+    unsigned m = __ballot_sync(FULL_MASK, (int)lane < cnt && d_l < dist_inf<T>() &&
+                                              (s.sz < k || d_l < s.worst));
+    while (m) {
+        const int i = __ffs(m) - 1;
+        m &= m - 1;
+        const int src = __shfl_sync(FULL_MASK, src_l, i);
+        const T nd = __shfl_sync(FULL_MASK, d_l, i);
+        if (s.sz < k || nd < s.worst) acc += warp_insert<E, false, T>(s, k, src, nd, lane);
     }
     return acc;
 }
