@@ -208,6 +208,14 @@ int knnm_set_shard(knnm_ctx *ctx, int64_t lo, int64_t hi);
 int knnm_round_local(knnm_ctx *ctx, int32_t mode, int32_t rev_cap,
                      uint64_t round_seed, int64_t *pairs_local);
 int knnm_local_views(knnm_ctx *ctx, void **cnt, void **boff, void **Bd, void **Bs);
+/* Same views over the WRITTEN slots only: slots the join left unwritten can
+ * never be accepted, so the exchange drops them.  Per target row the written
+ * slots keep their reference order; cnt = written slots per row, boff their
+ * offsets in the compacted Bd / Bs (Bs = NULL when packed).  *total = number
+ * of written slots.  Call after knnm_round_local; the views stay valid until
+ * the next round. */
+int knnm_local_compact(knnm_ctx *ctx, void **cnt, void **boff, void **Bd, void **Bs,
+                       int64_t *total);
 int knnm_round_apply(knnm_ctx *ctx, int32_t nsrc, const uint32_t *recv_cnt,
                      const uint64_t *recv_base, const double *recv_Bd,
                      const int32_t *recv_Bs, int64_t *accepted);

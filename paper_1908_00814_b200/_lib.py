@@ -85,6 +85,8 @@ SIGNATURES = {
     "knnm_set_shard": (ctypes.c_int, [P, I64, I64]),
     "knnm_round_local": (ctypes.c_int, [P, I32, I32, U64, PI64]),
     "knnm_local_views": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]),
+    "knnm_local_compact": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
+                                          ctypes.POINTER(ctypes.c_int64)]),
     "knnm_round_apply": (ctypes.c_int, [P, I32, P, P, P, P, PI64]),
     "knnm_state_views": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]),
     "knnm_bf_topk": (ctypes.c_int, [P, P, P, I64, I32, I32, P, P]),

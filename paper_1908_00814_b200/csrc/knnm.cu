@@ -137,6 +137,7 @@ struct knnm_ctx {
     int64_t shard_lo = 0, shard_hi = -1;  // owned rows (sharded rounds); -1 = n
     // round scratch
     DBuf indeg, roff, rev, heavy, giant, gscratch32, nbh, nlen, hpairs, poff, worst0, active;
+    DBuf wcnt, woff, cBd, cBs;  // written-slot compaction (sharded exchange)
     DBuf bound, boff, mcount, moff, mcur, memb, start, Bd, Bs;
     DBuf order, lab0, lab1;       // locality order of hoods (per merge)
     bool have_order = false;
@@ -659,7 +660,7 @@ int knnm_destroy(knnm_ctx *c) {
     DBuf *all[] = {&c->vec, &c->sub, &c->ugid, &c->labels, &c->ids, &c->dists, &c->flags,
                    &c->sizes, &c->tail_ids, &c->tail_d, &c->tail_s, &c->indeg, &c->roff,
                    &c->rev, &c->heavy, &c->giant, &c->gscratch32, &c->nbh, &c->nlen, &c->hpairs,
-                   &c->poff, &c->worst0, &c->active, &c->order, &c->lab0, &c->lab1, &c->bound, &c->boff, &c->mcount, &c->moff, &c->mcur, &c->memb, &c->start, &c->Bd, &c->Bs,
+                   &c->poff, &c->worst0, &c->active, &c->wcnt, &c->woff, &c->cBd, &c->cBs, &c->order, &c->lab0, &c->lab1, &c->bound, &c->boff, &c->mcount, &c->moff, &c->mcur, &c->memb, &c->start, &c->Bd, &c->Bs,
                    &c->counters, &c->draws, &c->draw_rows,
                    &c->draw_bad, &c->pool, &c->scan_pos, &c->vec16, &c->norms, &c->sub16, &c->subnorms, &c->out_ids, &c->out_d,
                    &c->out_s, &c->phi_leaf_lo, &c->phi_leaf_len, &c->phi_left, &c->phi_right,
@@ -1555,6 +1556,40 @@ int knnm_local_views(knnm_ctx *c, void **cnt, void **boff, void **Bd, void **Bs)
     if (Bd) *Bd = c->Bd.p;
     // packed slots carry the source row in Bd: nothing to exchange in Bs
     if (Bs) *Bs = c->slots_mode == SLOTS_PACKED ? nullptr : c->Bs.p;
+    return KNNM_OK;
+}
+
+int knnm_local_compact(knnm_ctx *c, void **cnt, void **boff, void **Bd, void **Bs, int64_t *total) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    CK(cudaSetDevice(c->device));
+    TRY(ensure_slots_noinit(c, 1));
+    const int64_t n = c->n;
+    const bool packed = c->slots_mode == SLOTS_PACKED;
+    TRY(ensure(c->wcnt, sizeof(uint32_t) * (size_t)(n + 1)));
+    TRY(ensure(c->woff, sizeof(uint64_t) * (size_t)(n + 1)));
+    const int blocks = grid_for(c, n * 32, 256, 16);
+    k_slot_wcount<<<blocks, 256, 0, c->st>>>(n, c->boff.as<uint64_t>(), c->Bd.as<double>(),
+                                             c->wcnt.as<uint32_t>());
+    CKL();
+    TRY(scan<uint32_t, uint64_t>(c, c->wcnt.as<uint32_t>(), c->woff.as<uint64_t>(), n));
+    uint64_t tot = 0;
+    CK(cudaMemcpyAsync(&c->hcnt[C_NUM - 1], c->woff.as<uint64_t>() + n, sizeof(uint64_t),
+                       cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    tot = c->hcnt[C_NUM - 1];
+    TRY(ensure(c->cBd, sizeof(double) * (size_t)(tot + 1)));
+    if (!packed) TRY(ensure(c->cBs, sizeof(int32_t) * (size_t)(tot + 1)));
+    k_slot_compact<<<blocks, 256, 0, c->st>>>(n, c->boff.as<uint64_t>(), c->woff.as<uint64_t>(),
+                                              c->Bd.as<double>(), packed ? nullptr : c->Bs.as<int32_t>(),
+                                              c->cBd.as<double>(), packed ? nullptr : c->cBs.as<int32_t>());
+    CKL();
+    CK(cudaStreamSynchronize(c->st));
+    if (cnt) *cnt = c->wcnt.p;
+    if (boff) *boff = c->woff.p;
+    if (Bd) *Bd = c->cBd.p;
+    if (Bs) *Bs = packed ? nullptr : c->cBs.p;
+    if (total) *total = (int64_t)tot;
     return KNNM_OK;
 }
 

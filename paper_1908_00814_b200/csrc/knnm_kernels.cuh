@@ -2311,6 +2311,47 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
     if (lane == 0 && nexact) atomicAdd(&counters[C_EXACT], nexact);
 }
 
+// Written-slot compaction for the sharded exchange: an unwritten slot (NaN
+// in its f64 view: the prefill, or all-ones when packed) can never be
+// accepted.  One warp per row; written slots keep their order.
+__global__ void k_slot_wcount(int64_t n, const uint64_t *__restrict__ boff, const double *__restrict__ Bd,
+                              uint32_t *__restrict__ wcnt) {
+    const unsigned lane = lane_id();
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
+        const uint64_t lo = boff[r], hi = boff[r + 1];
+        uint32_t c = 0;
+        for (uint64_t j = lo + lane; j - lane < hi; j += 32) {
+            const double v = j < hi ? Bd[j] : __longlong_as_double(-1LL);
+            c += __popc(__ballot_sync(FULL_MASK, v == v));
+        }
+        if (lane == 0) wcnt[r] = c;
+    }
+}
+
+__global__ void k_slot_compact(int64_t n, const uint64_t *__restrict__ boff, const uint64_t *__restrict__ woff,
+                               const double *__restrict__ Bd, const int32_t *__restrict__ Bs,
+                               double *__restrict__ oBd, int32_t *__restrict__ oBs) {
+    const unsigned lane = lane_id();
+    const unsigned lt = lanemask_lt();
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += nw) {
+        const uint64_t lo = boff[r], hi = boff[r + 1];
+        uint64_t o = woff[r];
+        for (uint64_t j = lo + lane; j - lane < hi; j += 32) {
+            const double v = j < hi ? Bd[j] : __longlong_as_double(-1LL);
+            const bool w = v == v;
+            const unsigned m = __ballot_sync(FULL_MASK, w);
+            if (w) {
+                const uint64_t at = o + __popc(m & lt);
+                oBd[at] = v;
+                if (oBs) oBs[at] = Bs[j];
+            }
+            o += __popc(m);
+        }
+    }
+}
+
 // Round-start worst of every row (sharded rounds: the join needs the
 // snapshot of rows owned by other ranks; lists are replicated).
 __global__ void k_worst0_all(const int32_t *__restrict__ sizes, const double *__restrict__ dists,

@@ -94,6 +94,18 @@ class ShardEngine:
                 _view(bd.value, (max(total, 0),), "<f8", self.device),
                 None if bs.value is None else _view(bs.value, (max(total, 0),), "<i4", self.device))
 
+    def local_compact(self, n):
+        """local_views over the written slots only (knnm_local_compact)."""
+        cnt, boff, bd, bs = (ctypes.c_void_p() for _ in range(4))
+        tot = ctypes.c_int64()
+        check(self.lib.knnm_local_compact(self.e._h, ctypes.byref(cnt), ctypes.byref(boff),
+                                          ctypes.byref(bd), ctypes.byref(bs), ctypes.byref(tot)),
+              "knnm_local_compact")
+        total = int(tot.value)
+        return (_view(cnt.value, (n,), "<i4", self.device), _view(boff.value, (n + 1,), "<i8", self.device),
+                _view(bd.value, (total,), "<f8", self.device),
+                None if bs.value is None else _view(bs.value, (total,), "<i4", self.device))
+
     def round_apply(self, recv_cnt, recv_base, recv_bd, recv_bs) -> int:
         acc = ctypes.c_int64()
         base = np.ascontiguousarray(recv_base, dtype=np.uint64)
@@ -202,9 +214,12 @@ class TorchComm:
 # sharded round loop (construct.py:111-179)
 # ---------------------------------------------------------------------------
 
-def sharded_rounds(shards, comm, n, k, mode, params, rng, counter, report, rev_cap=None):
+def sharded_rounds(shards, comm, n, k, mode, params, rng, counter, report, rev_cap=None,
+                   compact=True, traffic=None):
     """_descent_rounds over P ranks.  ``shards[r]`` = ShardEngine of each
-    local rank r (state already initialised and replicated)."""
+    local rank r (state already initialised and replicated).  ``compact``:
+    exchange only the written slots (unwritten ones can never be accepted);
+    ``traffic`` (dict) accumulates the slot bytes each rank sends to others."""
     import torch
 
     from .construct import sample_cap
@@ -221,12 +236,14 @@ def sharded_rounds(shards, comm, n, k, mode, params, rng, counter, report, rev_c
         pairs_l = {r: shards[r].round_local(mode, rev_cap, round_seed) for r in comm.local_ranks}
         sends = {}
         for r in comm.local_ranks:
-            cnt, boff, bd, bs = shards[r].local_views(n)
+            cnt, boff, bd, bs = shards[r].local_compact(n) if compact else shards[r].local_views(n)
             boff_h = boff.cpu().numpy()
             parts = []
-            for (lo, hi) in bounds:
+            for q, (lo, hi) in enumerate(bounds):
                 a, b = int(boff_h[lo]), int(boff_h[hi])
                 parts.append((cnt[lo:hi], bd[a:b], None if bs is None else bs[a:b]))
+                if traffic is not None and q != r:
+                    traffic[r] = traffic.get(r, 0) + (b - a) * (8 if bs is None else 12)
             sends[r] = parts
         recv_cnt = comm.alltoallv({r: [p[0] for p in sends[r]] for r in comm.local_ranks})
         recv_bd = comm.alltoallv({r: [p[1] for p in sends[r]] for r in comm.local_ranks})
@@ -293,7 +310,7 @@ def _append_random_all(engines, rows, pool, count, rng, counter):
 
 
 def s_merge_sharded(dataset, g, h, params: MergeParams, comm, engines, counter=None,
-                    return_report=False, out_device=False):
+                    return_report=False, out_device=False, compact=True, traffic=None):
     """s_merge (merge.py:195-260) over comm.world ranks; ``engines`` maps each
     local rank to an Engine.  Bit-identical to s_merge."""
     _check_merge_inputs(dataset, g, h.member_ids, params, h)
@@ -316,14 +333,15 @@ def s_merge_sharded(dataset, g, h, params: MergeParams, comm, engines, counter=N
     _append_random_all(local, rows_h, rows_g.astype(np.int64), min(fill, rows_g.size), rng, counter)
     report = BuildReport(phi_initial=local[0].phi())
     shards = {r: ShardEngine(engines[r]) for r in comm.local_ranks}
-    sharded_rounds(shards, comm, n, k, MODE_CROSS, params.descent_params(), rng, counter, report)
+    sharded_rounds(shards, comm, n, k, MODE_CROSS, params.descent_params(), rng, counter, report,
+                   compact=compact, traffic=traffic)
     ids, dists, sizes = local[0].export(merge_rear=k - k1 > 0, on_device=out_device)
     u = KnnGraph.from_arrays(union, k, metric, ids, dists, sizes)
     return (u, report) if return_report else u
 
 
 def j_merge_sharded(dataset, g, raw_ids, params: MergeParams, comm, engines, counter=None,
-                    return_report=False, out_device=False):
+                    return_report=False, out_device=False, compact=True, traffic=None):
     """j_merge (merge.py:263-338) over comm.world ranks (non-empty raw set)."""
     raw = np.unique(np.asarray(raw_ids, dtype=np.int64))
     _check_merge_inputs(dataset, g, raw, params, None)
@@ -355,7 +373,7 @@ def j_merge_sharded(dataset, g, raw_ids, params: MergeParams, comm, engines, cou
     report = BuildReport(phi_initial=local[0].phi())
     shards = {r: ShardEngine(engines[r]) for r in comm.local_ranks}
     sharded_rounds(shards, comm, n, k, MODE_CROSS_OR_S2, params.descent_params(), rng, counter,
-                   report)
+                   report, compact=compact, traffic=traffic)
     ids, dists, sizes = local[0].export(merge_rear=k - k1 > 0, on_device=out_device)
     u = KnnGraph.from_arrays(union, k, metric, ids, dists, sizes)
     return (u, report) if return_report else u

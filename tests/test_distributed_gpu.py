@@ -118,3 +118,36 @@ def test_sharded_random_cases(seed):
     assert np.array_equal(got.sizes, want.sizes)
     assert [(r.pairs, r.updates, r.phi) for r in rg.rounds] == \
         [(r.pairs, r.updates, r.phi) for r in rw.rounds]
+
+
+@pytest.mark.parametrize("kind,metric", [("intgmm", "l2"), ("uniform", "l2"), ("sphere", "cos")])
+def test_compacted_exchange_bit_identical(oracle, kind, metric):
+    """Exchanging only the written slots (knnm_local_compact) gives the same
+    merge as exchanging whole slot blocks, with less traffic."""
+    import paper_1908_00814_b200 as km
+    from paper_1908_00814_b200 import distributed as D
+
+    n = 3000
+    ds = {"intgmm": lambda: km.generate_int_gmm(n, 128, n_centres=30, seed=6),
+          "uniform": lambda: km.generate_uniform(n, 24, seed=6),
+          "sphere": lambda: km.generate_sphere_gmm(n, 100, n_centres=20, seed=6)}[kind]()
+    m = km.Metric.L2 if metric == "l2" else km.Metric.COSINE
+    s1, s2 = split_ids(n, seed=4)
+    g = km.nn_descent(ds, m, km.DescentParams(k=12), 1, member_ids=s1)
+    h = km.nn_descent(ds, m, km.DescentParams(k=12), 2, member_ids=s2)
+    mp = km.MergeParams(k=12, seed=3)
+    want = km.s_merge(ds, g, h, mp)
+    out = {}
+    for compact in (False, True):
+        tr = {}
+        got = D.s_merge_sharded(ds, g, h, mp, D.LoopbackComm(3), _engines(3), compact=compact,
+                                traffic=tr)
+        assert np.array_equal(got.ids, want.ids)
+        assert np.array_equal(got.dists, want.dists)
+        assert np.array_equal(got.sizes, want.sizes)
+        out[compact] = sum(tr.values())
+    assert 0 < out[True] < out[False]
+    # j_merge over the compacted exchange
+    wj = km.j_merge(ds, g, s2, mp)
+    gj = D.j_merge_sharded(ds, g, s2, mp, D.LoopbackComm(2), _engines(2))
+    assert np.array_equal(gj.ids, wj.ids) and np.array_equal(gj.dists, wj.dists)
