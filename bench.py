@@ -75,12 +75,28 @@ class ClockSampler:
         self._p = None
 
     def __enter__(self):
+        import threading
+
+        self._lines = []
+        self._first = threading.Event()
         try:
             self._p = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            time.sleep(0.3)  # first sample lands before the region starts
+
+            def reader():
+                for line in self._p.stdout:
+                    self._lines.append(line)
+                    self._first.set()
+                self._first.set()
+
+            self._t = threading.Thread(target=reader, daemon=True)
+            self._t.start()
+            # nvidia-smi's start-up (NVML init) must not overlap the timed
+            # region: wait for its first sample (it once stalled a step by
+            # ~250 ms when the region began during the start-up)
+            self._first.wait(timeout=15)
         except Exception:
             self._p = None
         return self
@@ -91,11 +107,11 @@ class ClockSampler:
         time.sleep(0.25)  # one more sample from inside / at the end of the region
         self._p.terminate()
         try:
-            out, _ = self._p.communicate(timeout=10)
+            self._p.wait(timeout=10)
         except Exception:
             self._p.kill()
-            out, _ = self._p.communicate()
-        for line in (out or "").splitlines():
+        self._t.join(timeout=5)
+        for line in self._lines:
             parts = [x.strip() for x in line.split(",")]
             if len(parts) == 6:
                 self.samples.append(parts)

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libknnm.so")
+# KNNM_LIB: alternative build of the same library (A/B measurements)
+LIB_PATH = os.environ.get("KNNM_LIB") or os.path.join(_HERE, "libknnm.so")
 
 KNNM_OK = 0
 _ERRORS = {
