@@ -165,11 +165,14 @@ int knnm_draws_regen(knnm_ctx *ctx, const uint64_t *pcg, int32_t has_uint32,
 
 /* Host-side (no context, no GPU): union of two strictly ascending id arrays
  * and each input's row in it (merge.py:217-221 np.union1d + searchsorted,
- * one linear pass).  uni needs na + nb entries; *nu = union size; *shared =
- * whether the inputs share an id (merge.py:181 disjointness check). */
+ * one linear pass; split by merge path over host threads for large inputs).
+ * uni needs na + nb entries; *nu = union size; *shared = whether the inputs
+ * share an id (merge.py:181 disjointness check); labels (nullable, na + nb
+ * entries) = 1 where the union entry comes from b, else 0 (the merge labels
+ * of merge.py:222-223 / 304-305). */
 int knnm_merge_members(const int64_t *a, int64_t na, const int64_t *b, int64_t nb,
                        int64_t *uni, int32_t *rows_a, int32_t *rows_b, int64_t *nu,
-                       int32_t *shared);
+                       int32_t *shared, int8_t *labels);
 
 /* Host-side (no context, no GPU): nrows successive
  * sample_distinct(rng, n, k, exclude=exclude[r]) draws (core.py:222-230,

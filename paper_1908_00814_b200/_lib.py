@@ -79,7 +79,7 @@ SIGNATURES = {
     "knnm_draws_gen": (ctypes.c_int, [P, P, I32, ctypes.c_uint32, U64, I64, I32, PI64, P, PI64]),
     "knnm_draws_regen": (ctypes.c_int, [P, P, I32, ctypes.c_uint32, U64, P, I64, PI64, P, PI64]),
     "knnm_merge_members": (ctypes.c_int, [P, I64, P, I64, P, P, P, ctypes.POINTER(I64),
-                                          ctypes.POINTER(I32)]),
+                                          ctypes.POINTER(I32), P]),
     "knnm_sample_distinct_rows": (ctypes.c_int, [P, ctypes.POINTER(I32), ctypes.POINTER(ctypes.c_uint32),
                                                  I64, I32, P, I64, P]),
     "knnm_round": (ctypes.c_int, [P, I32, I32, U64, PI64, PI64]),

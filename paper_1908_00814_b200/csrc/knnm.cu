@@ -1699,25 +1699,31 @@ int knnm_bf_topk(knnm_ctx *c, const float *queries, const int64_t *rows, int64_t
     return KNNM_OK;
 }
 
-int knnm_merge_members(const int64_t *a, int64_t na, const int64_t *b, int64_t nb, int64_t *uni,
-                       int32_t *rows_a, int32_t *rows_b, int64_t *nu, int32_t *shared) {
-    if ((na > 0 && (!a || !rows_a)) || (nb > 0 && (!b || !rows_b)) || !uni || !nu)
-        return fail(KNNM_ERR_ARG, "bad argument");
-    if (na + nb >= (1ll << 31)) return fail(KNNM_ERR_LIMIT, "union too large");
-    for (int64_t i = 1; i < na; i++)
-        if (a[i] <= a[i - 1]) return fail(KNNM_ERR_ARG, "ids must be strictly ascending");
-    for (int64_t i = 1; i < nb; i++)
-        if (b[i] <= b[i - 1]) return fail(KNNM_ERR_ARG, "ids must be strictly ascending");
-    // two-pointer merge of ascending runs (np.union1d + np.searchsorted),
-    // branch-free: both rows are written every step and only the side(s)
-    // holding the smaller id advance, so each row's last write is its own
-    // (a shared id yields one union entry that both rows point at)
-    int64_t i = 0, j = 0, o = 0;
+// Merge path: number of a-elements among the first p outputs of the merge
+// of two strictly ascending, disjoint arrays.
+static int64_t merge_split(const int64_t *a, int64_t na, const int64_t *b, int64_t nb, int64_t p) {
+    int64_t lo = std::max<int64_t>(0, p - nb), hi = std::min<int64_t>(p, na);
+    while (lo < hi) {
+        const int64_t i = (lo + hi) >> 1, j = p - i;
+        if (i < na && j > 0 && b[j - 1] > a[i]) lo = i + 1;  // b[j-1] must come after a[i]
+        else hi = i;
+    }
+    return lo;
+}
+
+// Branch-free two-pointer merge of a[i..ia1) and b[j..jb1) into uni[o..):
+// both rows are written every step and only the side(s) holding the smaller
+// id advance, so each row's last write is its own (a shared id yields one
+// union entry that both rows point at).  Returns whether an id was shared.
+static int32_t merge_run(const int64_t *a, int64_t i, int64_t ia1, const int64_t *b, int64_t j,
+                         int64_t jb1, int64_t o, int64_t *uni, int32_t *rows_a, int32_t *rows_b,
+                         int8_t *labels, int64_t *o_end) {
     int32_t sh = 0;
-    while (i < na && j < nb) {
+    while (i < ia1 && j < jb1) {
         const int64_t x = a[i], y = b[j];
         const int ta = x <= y, tb = y <= x;
         uni[o] = ta ? x : y;
+        if (labels) labels[o] = (int8_t)(ta ? 0 : 1);
         rows_a[i] = (int32_t)o;
         rows_b[j] = (int32_t)o;
         sh |= ta & tb;
@@ -1725,16 +1731,59 @@ int knnm_merge_members(const int64_t *a, int64_t na, const int64_t *b, int64_t n
         j += tb;
         o++;
     }
-    for (; i < na; i++) {
+    for (; i < ia1; i++) {
         uni[o] = a[i];
+        if (labels) labels[o] = 0;
         rows_a[i] = (int32_t)o++;
     }
-    for (; j < nb; j++) {
+    for (; j < jb1; j++) {
         uni[o] = b[j];
+        if (labels) labels[o] = 1;
         rows_b[j] = (int32_t)o++;
     }
+    if (o_end) *o_end = o;
+    return sh;
+}
+
+int knnm_merge_members(const int64_t *a, int64_t na, const int64_t *b, int64_t nb, int64_t *uni,
+                       int32_t *rows_a, int32_t *rows_b, int64_t *nu, int32_t *shared, int8_t *labels) {
+    if ((na > 0 && (!a || !rows_a)) || (nb > 0 && (!b || !rows_b)) || !uni || !nu)
+        return fail(KNNM_ERR_ARG, "bad argument");
+    if (na + nb >= (1ll << 31)) return fail(KNNM_ERR_LIMIT, "union too large");
+    const int64_t total = na + nb;
+    const int T = total < (1 << 16) ? 1
+                : (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    // ascending checks and the merge, split over T host threads (merge path)
+    std::vector<int32_t> bad(T, 0), sh(T, 0);
+    auto work = [&](int t) {
+        const int64_t p0 = total * t / T, p1 = total * (t + 1) / T;
+        const int64_t ca0 = na * t / T, ca1 = na * (t + 1) / T, cb0 = nb * t / T, cb1 = nb * (t + 1) / T;
+        for (int64_t i = std::max<int64_t>(ca0, 1); i < ca1; i++) bad[t] |= a[i] <= a[i - 1];
+        for (int64_t i = std::max<int64_t>(cb0, 1); i < cb1; i++) bad[t] |= b[i] <= b[i - 1];
+        if (T == 1) return;
+        const int64_t i0 = merge_split(a, na, b, nb, p0), i1 = merge_split(a, na, b, nb, p1);
+        sh[t] = merge_run(a, i0, i1, b, p0 - i0, p1 - i1, p0, uni, rows_a, rows_b, labels, nullptr);
+    };
+    if (T == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> th;
+        for (int t = 1; t < T; t++) th.emplace_back(work, t);
+        work(0);
+        for (auto &x : th) x.join();
+    }
+    for (int t = 0; t < T; t++)
+        if (bad[t]) return fail(KNNM_ERR_ARG, "ids must be strictly ascending");
+    int32_t s = 0;
+    for (int t = 0; t < T; t++) s |= sh[t];
+    int64_t o = total;
+    if (T == 1 || s) {
+        // serial merge (also the exact tie semantics when ids are shared:
+        // the parallel split assumes disjoint inputs)
+        s = merge_run(a, 0, na, b, 0, nb, 0, uni, rows_a, rows_b, labels, &o);
+    }
     *nu = o;
-    if (shared) *shared = sh;
+    if (shared) *shared = s;
     return KNNM_OK;
 }
 

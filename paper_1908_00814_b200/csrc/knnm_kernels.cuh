@@ -695,7 +695,7 @@ __device__ __forceinline__ uint32_t members_closed_form(int mode, int an, int ao
     return m + ((a >= 1 || b >= 2) ? bn : 0) + ((an >= 1 || bn >= 1) ? bo : 0);
 }
 
-__global__ void __launch_bounds__(ASM_WARPS * 32, 5)
+__global__ void __launch_bounds__(ASM_WARPS * 32, 6)
 k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__restrict__ sizes,
            const double *__restrict__ dists, int64_t n, int k, int rev_cap,
            const uint32_t *__restrict__ roff, const uint32_t *__restrict__ rev, uint64_t seed,

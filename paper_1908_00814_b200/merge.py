@@ -90,14 +90,17 @@ def _union(a: np.ndarray, b: np.ndarray) -> np.ndarray:
     return np.union1d(a, b)
 
 
-def _merge_members(a: np.ndarray, b: np.ndarray, with_overlap: bool = False):
+def _merge_members(a: np.ndarray, b: np.ndarray, with_overlap: bool = False,
+                   labels_out: list | None = None):
     """(union, rows of a, rows of b) for disjoint ascending id arrays in one
     linear pass: np.union1d + np.searchsorted of merge.py:217-221.  With
-    with_overlap, also whether a and b share an id (merge.py:181)."""
+    with_overlap, also whether a and b share an id (merge.py:181).  When the
+    native path runs and ``labels_out`` is a list, the int8 merge labels
+    (1 = from b, merge.py:222-223) are appended to it."""
     na, nb = a.size, b.size
     if a.dtype == np.int64 and b.dtype == np.int64:
-        # native linear merge (libknnm.so, host-only); it rejects inputs that
-        # are not strictly ascending, which take the numpy path below
+        # native merge (libknnm.so, host threads, no GPU); it rejects inputs
+        # that are not strictly ascending, which take the numpy path below
         import ctypes
 
         from . import _lib
@@ -107,11 +110,14 @@ def _merge_members(a: np.ndarray, b: np.ndarray, with_overlap: bool = False):
         uni = np.empty(na + nb, dtype=np.int64)
         ra = np.empty(na, dtype=np.int32)
         rb = np.empty(nb, dtype=np.int32)
+        lab = np.empty(na + nb, dtype=np.int8) if labels_out is not None else None
         nu, sh = ctypes.c_int64(), ctypes.c_int32()
         rc = _lib.load().knnm_merge_members(_lib.ptr(a), na, _lib.ptr(b), nb, _lib.ptr(uni),
                                             _lib.ptr(ra), _lib.ptr(rb), ctypes.byref(nu),
-                                            ctypes.byref(sh))
+                                            ctypes.byref(sh), None if lab is None else _lib.ptr(lab))
         if rc == 0:
+            if lab is not None and not sh.value:
+                labels_out.append(lab)
             if with_overlap:
                 return uni[: nu.value], ra, rb, bool(sh.value)
             if not sh.value:
@@ -198,8 +204,10 @@ def _append_random(engine, rows, pool, count, rng, counter, on_pair, gids) -> No
 
 
 def _check_merge_inputs(dataset, g: KnnGraph, other_ids: np.ndarray, params: MergeParams,
-                        other_graph: KnnGraph | None, overlap: bool | None = None) -> None:
-    """merge.py:179-192, same checks and messages."""
+                        other_graph: KnnGraph | None, overlap: bool | None = None,
+                        ascending: bool = False) -> None:
+    """merge.py:179-192, same checks and messages (``ascending``: other_ids is
+    known to be strictly ascending, so its extremes are its ends)."""
     if overlap is None:
         overlap = _overlaps(np.asarray(g.member_ids), np.asarray(other_ids))
     if overlap:
@@ -212,8 +220,10 @@ def _check_merge_inputs(dataset, g: KnnGraph, other_ids: np.ndarray, params: Mer
         if other_graph.k != params.k:
             raise ValueError("graphs must share capacity k")
     Metric(g.metric).check_kind(dataset.kind)
-    if other_ids.size and (other_ids.min() < 0 or other_ids.max() >= dataset.n):
-        raise ValueError("ids outside the dataset")
+    if other_ids.size:
+        lo, hi = (other_ids[0], other_ids[-1]) if ascending else (other_ids.min(), other_ids.max())
+        if lo < 0 or hi >= dataset.n:
+            raise ValueError("ids outside the dataset")
 
 
 def s_merge(dataset, g: KnnGraph, h: KnnGraph, params: MergeParams,
@@ -221,9 +231,11 @@ def s_merge(dataset, g: KnnGraph, h: KnnGraph, params: MergeParams,
             device: int | None = None, out_device: bool = False):
     """Symmetric merge of two built k-NN graphs over disjoint subsets
     (merge.py:195-260; Alg. 1 of the paper)."""
+    lab_out: list = []
     union_gids, rows_g, rows_h, overlap = _merge_members(
-        np.asarray(g.member_ids), np.asarray(h.member_ids), with_overlap=True)
-    _check_merge_inputs(dataset, g, h.member_ids, params, h, overlap=overlap)
+        np.asarray(g.member_ids), np.asarray(h.member_ids), with_overlap=True, labels_out=lab_out)
+    _check_merge_inputs(dataset, g, h.member_ids, params, h, overlap=overlap,
+                        ascending=bool(lab_out))
     if counter is None:
         counter = DistanceCounter()
     rng = np.random.default_rng(params.seed)
@@ -231,8 +243,11 @@ def s_merge(dataset, g: KnnGraph, h: KnnGraph, params: MergeParams,
     k = params.k
     k1 = params.k1
     n = union_gids.shape[0]
-    labels = np.zeros(n, dtype=np.int8)
-    labels[rows_h] = 1
+    if lab_out:
+        labels = lab_out[0]
+    else:
+        labels = np.zeros(n, dtype=np.int8)
+        labels[rows_h] = 1
 
     eng = get_engine(device)
     eng.set_dataset(dataset.vectors, int(metric))
@@ -282,12 +297,16 @@ def j_merge(dataset, g: KnnGraph, raw_ids, params: MergeParams,
             return out, BuildReport(phi_initial=graph_phi(out))
         return out
     rng = np.random.default_rng(params.seed)
-    union_gids, rows_g, rows_raw = _merge_members(np.asarray(g.member_ids), raw)
+    lab_out: list = []
+    union_gids, rows_g, rows_raw = _merge_members(np.asarray(g.member_ids), raw, labels_out=lab_out)
     n = union_gids.shape[0]
     if k >= n:
         raise ValueError(f"k={k} must be below the union size {n}")
-    labels = np.zeros(n, dtype=np.int8)
-    labels[rows_raw] = 1
+    if lab_out:
+        labels = lab_out[0]
+    else:
+        labels = np.zeros(n, dtype=np.int8)
+        labels[rows_raw] = 1
 
     eng.set_dataset(dataset.vectors, int(metric))
     eng.begin(union_gids, labels, k)

@@ -156,3 +156,30 @@ def test_native_merge_members_large():
     u, ra, rb = _merge_members(a, b)
     assert np.array_equal(u, np.union1d(a, b))
     assert np.array_equal(u[ra], a) and np.array_equal(u[rb], b)
+
+
+@pytest.mark.parametrize("n,split,shared", [(200_000, 90_000, False), (300_001, 1, False),
+                                            (150_000, 149_999, False), (200_000, 100_000, True)])
+def test_native_merge_members_parallel_labels(n, split, shared):
+    """The merge-path split over host threads (inputs >= 64K ids) gives the
+    serial result, plus the merge labels (1 = from b); a shared id falls
+    back to the serial tie semantics."""
+    from paper_1908_00814_b200.merge import _merge_members
+
+    perm = np.random.default_rng(n + split).permutation(n)
+    a, b = np.sort(perm[:split]).astype(np.int64), np.sort(perm[split:]).astype(np.int64)
+    if shared:
+        b = np.sort(np.concatenate((b, a[[5, len(a) // 2]])))
+    labs = []
+    u, ra, rb, sh = _merge_members(a, b, with_overlap=True, labels_out=labs)
+    want = np.union1d(a, b)
+    assert sh == shared
+    assert np.array_equal(u, want)
+    assert np.array_equal(ra, np.searchsorted(want, a))
+    assert np.array_equal(rb, np.searchsorted(want, b))
+    if not shared:
+        lab = np.zeros(want.size, dtype=np.int8)
+        lab[rb] = 1
+        assert len(labs) == 1 and np.array_equal(labs[0], lab)
+    else:
+        assert labs == []
