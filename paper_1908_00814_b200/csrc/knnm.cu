@@ -126,6 +126,7 @@ struct knnm_ctx {
     bool u8_enabled = true;
     // current merge
     DBuf sub, ugid, labels;
+    bool ug_identity = false;  // union = 0 .. n_all-1: ugid not uploaded
     const float *subp = nullptr;
     int64_t n = 0;
     int k = 0;
@@ -263,6 +264,9 @@ int ensure_staging(knnm_ctx *c) {
     }
     return KNNM_OK;
 }
+
+// device union-id table, or nullptr for an identity union
+const int64_t *ugid_of(const knnm_ctx *c) { return c->ug_identity ? nullptr : c->ugid.as<int64_t>(); }
 
 int h2d(knnm_ctx *c, void *dst, const void *src, size_t bytes) {
     if (bytes == 0) return KNNM_OK;
@@ -778,9 +782,14 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     c->lists_f32 = c->cert || c->cert_dot;
     TRY(ensure(c->f32chk, sizeof(unsigned long long)));
     CK(cudaMemsetAsync(c->f32chk.p, 0, sizeof(unsigned long long), c->st));
-    TRY(ensure(c->ugid, sizeof(int64_t) * n));
-    TRY(h2d(c, c->ugid.p, union_gids, sizeof(int64_t) * n));
+    // an identity union (0 .. n_all-1, ascending) needs no id table on the
+    // device: local row = global id
     bool identity = (n == c->n_all && union_gids[0] == 0 && union_gids[n - 1] == n - 1);
+    c->ug_identity = identity;
+    if (!identity) {
+        TRY(ensure(c->ugid, sizeof(int64_t) * n));
+        TRY(h2d(c, c->ugid.p, union_gids, sizeof(int64_t) * n));
+    }
     c->sub16p = c->vec16.as<uint8_t>();
     c->subnormp = c->norms.as<float>();
     if (c->cert_dot && !identity) {
@@ -898,7 +907,7 @@ static int load_impl(knnm_ctx *c, const int32_t *rows, int64_t m, const int32_t 
     }
     if (gk > 0) {
         k_load_graph<<<grid_for(c, m * gk, 256), 256, 0, c->st>>>(
-            c->stage[0].as<int32_t>(), m, gi, gd, gs, gk, k1, c->k, c->ugid.as<int64_t>(), c->n,
+            c->stage[0].as<int32_t>(), m, gi, gd, gs, gk, k1, c->k, ugid_of(c), c->n,
             c->ids.as<int32_t>(), c->dists.as<double>(), c->sizes.as<int32_t>(),
             tk > 0 ? c->tail_ids.as<int32_t>() : nullptr, tk > 0 ? c->tail_d.as<double>() : nullptr,
             tk > 0 ? c->tail_s.as<int32_t>() : nullptr, tk, c->f32chk.as<unsigned long long>());
@@ -1900,7 +1909,7 @@ static int export_impl(knnm_ctx *c, int32_t merge_rear, int32_t *out_ids, double
     PhaseTimer pt(c, PH_OTHER);
     int64_t n = c->n, nk = c->n * c->k;
     TRY(ensure(c->out_ids, sizeof(int32_t) * nk));
-    k_export<<<grid_for(c, nk, 256), 256, 0, c->st>>>(c->ids.as<int32_t>(), c->ugid.as<int64_t>(),
+    k_export<<<grid_for(c, nk, 256), 256, 0, c->st>>>(c->ids.as<int32_t>(), ugid_of(c),
                                                        nk, c->out_ids.as<int32_t>());
     CKL();
     const void *src_i = c->out_ids.p, *src_d = c->dists.p, *src_s = c->sizes.p;

@@ -202,7 +202,9 @@ __global__ void k_init_lists(int64_t n, int k, int32_t *ids, double *dists, uint
 }
 
 __device__ __forceinline__ int32_t lookup_local(const int64_t *__restrict__ ug, int64_t n, int64_t g) {
-    // np.searchsorted(union, g) (side='left')
+    // np.searchsorted(union, g) (side='left'); ug == nullptr: the union is
+    // 0 .. n-1 (identity)
+    if (!ug) return (int32_t)(g < 0 ? 0 : g < n ? g : n);
     int64_t lo = 0, hi = n;
     while (lo < hi) {
         int64_t mid = (lo + hi) >> 1;
@@ -2585,7 +2587,7 @@ __global__ void k_export(const int32_t *__restrict__ ids, const int64_t *__restr
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
          i += (int64_t)gridDim.x * blockDim.x) {
         int32_t v = ids[i];
-        out_ids[i] = v >= 0 ? (int32_t)ug[v] : -1;
+        out_ids[i] = v >= 0 ? (ug ? (int32_t)ug[v] : v) : -1;
     }
 }
 
