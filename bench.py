@@ -60,24 +60,64 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region:
-    one `nvidia-smi -lms 200` loop started before the region and stopped
-    after it (the profiling recipe's clocks line) -- no process is spawned
-    while the region runs."""
+    """SM clocks + throttle reasons sampled during the timed region (the
+    profiling recipe's clocks line: clocks.sm, clocks.max.sm, hw_slowdown,
+    hw_thermal_slowdown, sw_thermal_slowdown, sw_power_cap).  Sampled through
+    NVML from a host thread every 100 ms: an `nvidia-smi -lms` loop stalled
+    the step it landed in (by 2-12 ms, once by 200 ms), which the timed
+    region would include.  Falls back to nvidia-smi when NVML is missing."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    PERIOD_S = 0.1
 
     def __init__(self, device: int):
         self.device = device
         self.samples = []
         self._p = None
+        self._nvml = None
+
+    def _nvml_handle(self):
+        import pynvml as N
+
+        N.nvmlInit()
+        try:
+            import torch
+
+            pr = torch.cuda.get_device_properties(self.device)
+            bus = "%08X:%02X:%02X.0" % (int(pr.pci_domain_id), int(pr.pci_bus_id), int(pr.pci_device_id))
+            return N, N.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return N, N.nvmlDeviceGetHandleByIndex(self.device)
+
+    def _nvml_sample(self):
+        N, h = self._nvml
+        r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+        bits = (N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap)
+        return [str(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)),
+                str(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))] + \
+            ["Active" if r & b else "Not Active" for b in bits]
 
     def __enter__(self):
         import threading
 
         self._lines = []
+        self._stop = threading.Event()
+        try:
+            self._nvml = self._nvml_handle()
+            self.samples.append(self._nvml_sample())  # before the region
+
+            def poll():
+                while not self._stop.wait(self.PERIOD_S):
+                    self.samples.append(self._nvml_sample())
+
+            self._t = threading.Thread(target=poll, daemon=True)
+            self._t.start()
+            return self
+        except Exception:
+            self._nvml = None
         self._first = threading.Event()
         try:
             self._p = subprocess.Popen(
@@ -93,15 +133,22 @@ class ClockSampler:
 
             self._t = threading.Thread(target=reader, daemon=True)
             self._t.start()
-            # nvidia-smi's start-up (NVML init) must not overlap the timed
-            # region: wait for its first sample (it once stalled a step by
-            # ~250 ms when the region began during the start-up)
+            # nvidia-smi's start-up must not overlap the timed region
             self._first.wait(timeout=15)
         except Exception:
             self._p = None
         return self
 
     def __exit__(self, *a):
+        if self._nvml is not None:
+            self._stop.set()
+            self._t.join(timeout=5)
+            try:
+                self.samples.append(self._nvml_sample())  # at the end of the region
+                self._nvml[0].nvmlShutdown()
+            except Exception:
+                pass
+            return
         if self._p is None:
             return
         time.sleep(0.25)  # one more sample from inside / at the end of the region
@@ -297,8 +344,13 @@ def run_b200(args):
         eng.pinned_outputs = False
         return c.count, u
 
+    # warm-up holds each result until the next step returns, as the timed
+    # loop does: the allocator then already caches two sets of output
+    # buffers (otherwise the second timed step pays a cudaMalloc)
+    u_keep = None
     for _ in range(args.warmup):
-        step_device()
+        u_keep = step_device()
+    del u_keep
     barrier()
     eng.reset_stats()
     eng.set_profiling(True)
@@ -306,8 +358,11 @@ def run_b200(args):
     with ClockSampler(local) as clk:
         torch.cuda.profiler.start()  # ncu --profile-from-start off sees the timed region only
         eng.mark(0)
+        step_wall = []
         for _ in range(args.steps):
+            t_s = time.perf_counter()
             cnt, u_dev = step_device()
+            step_wall.append(round((time.perf_counter() - t_s) * 1e3, 2))
             evals += cnt
         eng.mark(1)
         dev_ms = eng.elapsed_ms(0, 1)
@@ -437,6 +492,7 @@ def run_b200(args):
                 "h2d_bytes_per_step": est["h2d_bytes"] // steps,
                 "d2h_bytes_per_step": est["d2h_bytes"] // steps},
         "gpu_launches": st["launches"],
+        "step_wall_ms": step_wall,
         "clocks": clk.summary(),
         "setup_seconds": setup_s,
         "cpu_baseline": cpu,
