@@ -490,23 +490,38 @@ __global__ void k_sample_new(const int32_t *__restrict__ sizes, int64_t n, int k
 // round: rows with a flagged forward entry and targets of new forward
 // entries (their reverse edge is new).  Other hoods have no admissible pair
 // (_kernels.py:391-399 needs new_p or new_q): k_assemble skips them.
+// Both reverse kernels walk the n*k list entries with 32-bit indices
+// (n*k < 2^31, checked in knnm_begin) and take REV_U entries per thread per
+// step, their loads issued together: the per-entry chain (entry -> target's
+// offset / counter -> store) is latency-bound, so independent entries in
+// flight are what hides it.
+constexpr int REV_U = 4;
+
 __global__ void k_rev_count(const int32_t *__restrict__ ids, const uint8_t *__restrict__ flags,
                             const int32_t *__restrict__ sizes, int64_t n, int k, uint32_t *indeg,
                             int64_t tlo, int64_t thi, uint8_t *live) {
-    int64_t total = n * k;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t r = i / k;
-        int t = (int)(i % k);
-        if (t < sizes[r]) {
-            const uint8_t f = flags[i];
-            if (f != 0) live[r] = 1;  // new or sitting out (its flag is restored)
-            if (f != 2) {
-                const int32_t j = ids[i];
-                if (j >= tlo && j < thi) {
-                    atomicAdd(&indeg[j], 1u);
-                    if (f == 1) live[j] = 1;
-                }
+    const uint32_t total = (uint32_t)(n * k), uk = (uint32_t)k;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += REV_U * stride) {
+        int32_t j[REV_U];
+        uint32_t f[REV_U], r[REV_U];
+        bool in[REV_U];
+#pragma unroll
+        for (int q = 0; q < REV_U; q++) {
+            const uint32_t i = i0 + q * stride;
+            in[q] = i < total;
+            r[q] = in[q] ? i / uk : 0u;
+            j[q] = in[q] ? ids[i] : -1;
+            f[q] = in[q] ? flags[i] : 0u;
+            in[q] = in[q] && (int)(i - r[q] * uk) < sizes[r[q]];
+        }
+#pragma unroll
+        for (int q = 0; q < REV_U; q++) {
+            if (!in[q]) continue;
+            if (f[q] != 0) live[r[q]] = 1;  // new or sitting out (its flag is restored)
+            if (f[q] != 2 && j[q] >= tlo && j[q] < thi) {
+                atomicAdd(&indeg[j[q]], 1u);
+                if (f[q] == 1) live[j[q]] = 1;
             }
         }
     }
@@ -518,16 +533,29 @@ __global__ void k_rev_fill(const int32_t *__restrict__ ids, const uint8_t *__res
                            const int32_t *__restrict__ sizes, int64_t n, int k,
                            const uint32_t *__restrict__ roff, uint32_t *indeg, uint32_t *rev,
                            int64_t tlo, int64_t thi, const uint8_t *__restrict__ live) {
-    int64_t total = n * k;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int64_t r = i / k;
-        int t = (int)(i % k);
-        if (t < sizes[r] && ids[i] >= tlo && ids[i] < thi && flags[i] != 2 && live[ids[i]]) {
-            int32_t j = ids[i];
-            uint32_t p = roff[j] + atomicSub(&indeg[j], 1u) - 1u;
-            rev[p] = ((uint32_t)r << 1) | (uint32_t)flags[i];
+    const uint32_t total = (uint32_t)(n * k), uk = (uint32_t)k;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t i0 = blockIdx.x * blockDim.x + threadIdx.x; i0 < total; i0 += REV_U * stride) {
+        int32_t j[REV_U];
+        uint32_t f[REV_U], r[REV_U], p[REV_U];
+        bool ok[REV_U];
+#pragma unroll
+        for (int q = 0; q < REV_U; q++) {
+            const uint32_t i = i0 + q * stride;
+            ok[q] = i < total;
+            r[q] = ok[q] ? i / uk : 0u;
+            j[q] = ok[q] ? ids[i] : -1;
+            f[q] = ok[q] ? flags[i] : 2u;
+            ok[q] = ok[q] && (int)(i - r[q] * uk) < sizes[r[q]] && j[q] >= tlo && j[q] < thi && f[q] != 2;
         }
+#pragma unroll
+        for (int q = 0; q < REV_U; q++) ok[q] = ok[q] && live[j[q]];
+#pragma unroll
+        for (int q = 0; q < REV_U; q++)
+            if (ok[q]) p[q] = roff[j[q]] + atomicSub(&indeg[j[q]], 1u) - 1u;
+#pragma unroll
+        for (int q = 0; q < REV_U; q++)
+            if (ok[q]) rev[p[q]] = (r[q] << 1) | f[q];
     }
 }
 

@@ -45,6 +45,13 @@ def main():
     span = cur_end - iv[0][0]
     print(f"wall {wall * 1e3:.1f} ms, gpu span {span / 1e3:.1f} ms, busy {busy / 1e3:.1f} ms, "
           f"idle {(span - busy) / 1e3:.1f} ms in {len(gaps)} gaps, activities {len(iv)}")
+    by = {}
+    for s_, e_, name in iv:
+        key = "memset" if name.startswith("Memset") else "memcpy " + name.split("(")[1].split(")")[0] \
+            if name.startswith("Memcpy") else name.split("(")[0].split("<")[0].replace("void ", "")
+        by[key] = by.get(key, 0.0) + (e_ - s_)
+    for key, v in sorted(by.items(), key=lambda kv: -kv[1])[:14]:
+        print(f"  {key[:48]:48s} {v / 1e3:8.3f} ms")
     for d, a, b in sorted(gaps, reverse=True)[:15]:
         print(f"  gap {d / 1e3:7.3f} ms  after {str(a)[:40]:40s} before {str(b)[:40]}")
 
