@@ -645,6 +645,8 @@ int knnm_create(int device, knnm_ctx **out) {
     for (auto f : {k_join_mma<false, 1>, k_join_mma<false, 2>, k_join_mma<false, 4>,
                    k_join_mma<true, 1>, k_join_mma<true, 2>, k_join_mma<true, 4>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    CK(cudaFuncSetAttribute(k_merge_rear, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)mr_smem_bytes(64, 64)));
     for (auto f : {k_bf_topk<0>, k_bf_topk<1>, k_bf_topk<2>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(BF_THREADS * BF_MAXK * (sizeof(double) + sizeof(int32_t)))));
@@ -1917,7 +1919,8 @@ static int export_impl(knnm_ctx *c, int32_t merge_rear, int32_t *out_ids, double
         TRY(ensure(c->out_d, sizeof(double) * nk));
         TRY(ensure(c->out_s, sizeof(int32_t) * n));
         TRY(ensure(c->stage[0], sizeof(int32_t) * nk));
-        k_merge_rear<<<(unsigned)((n + 127) / 128), 128, 0, c->st>>>(
+        const size_t mr_smem = mr_smem_bytes(c->k, c->tk);
+        k_merge_rear<<<(unsigned)((n + MR_ROWS - 1) / MR_ROWS), MR_ROWS, mr_smem, c->st>>>(
             c->out_ids.as<int32_t>(), c->dists.as<double>(), c->sizes.as<int32_t>(),
             c->tail_ids.as<int32_t>(), c->tail_d.as<double>(), c->tail_s.as<int32_t>(), n, c->k,
             c->tk, c->stage[0].as<int32_t>(), c->out_d.as<double>(), c->out_s.as<int32_t>());

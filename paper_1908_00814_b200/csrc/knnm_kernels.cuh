@@ -2619,45 +2619,83 @@ __global__ void k_export(const int32_t *__restrict__ ids, const int64_t *__restr
     }
 }
 
-__global__ void k_merge_rear(const int32_t *__restrict__ ui, const double *__restrict__ ud,
-                             const int32_t *__restrict__ us, const int32_t *__restrict__ ri,
-                             const double *__restrict__ rd, const int32_t *__restrict__ rs, int64_t n,
-                             int k, int rk, int32_t *oi, double *od, int32_t *os) {
-    int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (u >= n) return;
-    const int32_t *a_i = ui + u * k;
-    const double *a_d = ud + u * k;
-    const int32_t *b_i = ri + u * rk;
-    const double *b_d = rd + u * rk;
-    int32_t *o_i = oi + u * k;
-    double *o_d = od + u * k;
-    int a = 0, b = 0, w = 0, na = us[u], nb = rs[u];
-    while (w < k && (a < na || b < nb)) {
-        int32_t cid;
-        double cd;
-        if (a < na && (b >= nb || a_d[a] < b_d[b] || (a_d[a] == b_d[b] && a_i[a] <= b_i[b]))) {
-            cid = a_i[a];
-            cd = a_d[a];
-            a++;
-        } else {
-            cid = b_i[b];
-            cd = b_d[b];
-            b++;
-        }
-        bool dup = false;
-        for (int t = 0; t < w; t++)
-            if (o_i[t] == cid) { dup = true; break; }
-        if (!dup) {
-            o_i[w] = cid;
-            o_d[w] = cd;
-            w++;
-        }
+// One thread per row, MR_ROWS rows per block: the block's U rows, rear rows
+// and outputs are staged in shared memory with coalesced copies (a thread
+// walking its own rows in global memory touched a new sector per element).
+constexpr int MR_ROWS = 64;
+
+__host__ __device__ constexpr size_t mr_smem_bytes(int k, int rk) {
+    return (size_t)MR_ROWS * (size_t)(2 * k + rk) * (sizeof(double) + sizeof(int32_t));
+}
+
+__global__ void __launch_bounds__(MR_ROWS)
+k_merge_rear(const int32_t *__restrict__ ui, const double *__restrict__ ud,
+             const int32_t *__restrict__ us, const int32_t *__restrict__ ri,
+             const double *__restrict__ rd, const int32_t *__restrict__ rs, int64_t n,
+             int k, int rk, int32_t *oi, double *od, int32_t *os) {
+    extern __shared__ __align__(16) char mr_smem[];
+    const int64_t r0 = (int64_t)blockIdx.x * MR_ROWS;
+    const int nr = (int)((n - r0) < MR_ROWS ? (n - r0) : MR_ROWS);
+    double *sad = reinterpret_cast<double *>(mr_smem);      // [MR_ROWS][k]
+    double *sbd = sad + MR_ROWS * k;                         // [MR_ROWS][rk]
+    double *sod = sbd + MR_ROWS * rk;                        // [MR_ROWS][k]
+    int32_t *sai = reinterpret_cast<int32_t *>(sod + MR_ROWS * k);
+    int32_t *sbi = sai + MR_ROWS * k;
+    int32_t *soi = sbi + MR_ROWS * rk;
+    // coalesced staging of the block's rows (contiguous in global memory)
+    for (int e = threadIdx.x; e < nr * k; e += MR_ROWS) {
+        sad[e] = ud[r0 * k + e];
+        sai[e] = ui[r0 * k + e];
     }
-    for (int t = w; t < k; t++) {
-        o_i[t] = -1;
-        o_d[t] = __longlong_as_double(0x7ff0000000000000LL);
+    for (int e = threadIdx.x; e < nr * rk; e += MR_ROWS) {
+        sbd[e] = rd[r0 * rk + e];
+        sbi[e] = ri[r0 * rk + e];
     }
-    os[u] = w;
+    __syncthreads();
+    const int lr = threadIdx.x;
+    if (lr < nr) {
+        const int64_t u = r0 + lr;
+        const int32_t *a_i = sai + lr * k;
+        const double *a_d = sad + lr * k;
+        const int32_t *b_i = sbi + lr * rk;
+        const double *b_d = sbd + lr * rk;
+        int32_t *o_i = soi + lr * k;
+        double *o_d = sod + lr * k;
+        // graph.py:259-280 / _kernels.py:529-563: (dist, id) merge, U first
+        // on ties, ids already output skipped, at most k kept
+        int a = 0, b = 0, w = 0, na = us[u], nb = rs[u];
+        while (w < k && (a < na || b < nb)) {
+            int32_t cid;
+            double cd;
+            if (a < na && (b >= nb || a_d[a] < b_d[b] || (a_d[a] == b_d[b] && a_i[a] <= b_i[b]))) {
+                cid = a_i[a];
+                cd = a_d[a];
+                a++;
+            } else {
+                cid = b_i[b];
+                cd = b_d[b];
+                b++;
+            }
+            bool dup = false;
+            for (int t = 0; t < w; t++)
+                if (o_i[t] == cid) { dup = true; break; }
+            if (!dup) {
+                o_i[w] = cid;
+                o_d[w] = cd;
+                w++;
+            }
+        }
+        for (int t = w; t < k; t++) {
+            o_i[t] = -1;
+            o_d[t] = __longlong_as_double(0x7ff0000000000000LL);
+        }
+        os[u] = w;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * k; e += MR_ROWS) {
+        od[r0 * k + e] = sod[e];
+        oi[r0 * k + e] = soi[e];
+    }
 }
 
 }  // namespace knnm
