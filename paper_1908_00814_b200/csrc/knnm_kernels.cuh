@@ -2151,6 +2151,24 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
             if ((int)lane < m) start[rec.out] = acc;
             continue;
         }
+        if (m <= 64) {
+            // two memberships per lane, the same weighted count of smaller
+            // keys (keys are unique within a row: hood ids / ordinals)
+            const MembRec rb = (int)lane + 32 < m ? memb[lo + 32 + lane] : MembRec{~0ull, 0, 0};
+            uint32_t acc0 = 0, acc1 = 0;
+#pragma unroll 4
+            for (int f = 0; f < m; f++) {
+                const uint64_t kk = f < 32 ? rec.key : rb.key;
+                const uint32_t ww = f < 32 ? rec.weight : rb.weight;
+                const uint64_t kf = __shfl_sync(FULL_MASK, kk, f & 31);
+                const uint32_t wf = __shfl_sync(FULL_MASK, ww, f & 31);
+                acc0 += kf < rec.key ? wf : 0u;
+                acc1 += kf < rb.key ? wf : 0u;
+            }
+            start[rec.out] = acc0;
+            if ((int)lane + 32 < m) start[rb.out] = acc1;
+            continue;
+        }
         if (m > SEG_SMEM) {  // hub row: ranked by a whole block later
             if (lane == 0) heavy[atomicAdd(&counters[C_SEGHEAVY], 1ull)] = (int32_t)r;
             continue;
