@@ -2099,6 +2099,45 @@ __global__ void k_directed_memb(const int32_t *__restrict__ rows, int64_t m, uin
 // shuffle loop), m <= SEG_SMEM by a shared-memory bitonic sort of
 // (key << 32 | index) and a weighted exclusive scan; longer rows (hubs) go
 // to a list ranked by k_seg_rank_heavy with a whole block per row.
+// Rank a row's m <= 32 * NE memberships: keys sorted in registers, weights
+// and output positions staged in shared memory, weighted exclusive scan.
+template <int NE>
+__device__ __forceinline__ void seg_rank_sorted(uint32_t lo, int m, const MembRec *__restrict__ memb,
+                                                uint32_t *__restrict__ start, uint32_t *sw, uint32_t *so,
+                                                unsigned lane) {
+    uint64_t v[NE];
+#pragma unroll
+    for (int e = 0; e < NE; e++) {
+        const int i = e * 32 + (int)lane;
+        if (i < m) {
+            const MembRec re = memb[lo + i];
+            v[e] = (re.key << 32) | (uint32_t)i;
+            sw[i] = re.weight;
+            so[i] = re.out;
+        } else {
+            v[e] = ~0ull;
+        }
+    }
+    __syncwarp();
+    warp_sort_reg<NE, uint64_t>(v, lane);
+    uint32_t carry = 0;
+#pragma unroll
+    for (int e = 0; e < NE; e++) {
+        const int i = e * 32 + (int)lane;
+        const uint32_t idx = (uint32_t)v[e];
+        const uint32_t w = i < m ? sw[idx] : 0u;
+        uint32_t inc = w;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
+            if ((int)lane >= o) inc += t;
+        }
+        if (i < m) start[so[idx]] = carry + inc - w;
+        carry += __shfl_sync(FULL_MASK, inc, 31);
+    }
+    __syncwarp();
+}
+
 constexpr int SEG_WARPS = 8;
 __global__ void __launch_bounds__(SEG_WARPS * 32)
 k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restrict__ memb,
@@ -2173,36 +2212,10 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
             if (lane == 0) heavy[atomicAdd(&counters[C_SEGHEAVY], 1ull)] = (int32_t)r;
             continue;
         }
-        // sort (key << 32 | index) ascending, then scan weights in that order
-        uint32_t P2 = 64;
-        while (P2 < (uint32_t)m) P2 <<= 1;
-        uint64_t *sk = s_key[wib];
-        uint32_t *sw = s_wt[wib];
-        for (uint32_t e = lane; e < P2; e += 32) {
-            if (e < (uint32_t)m) {
-                const MembRec re = memb[lo + e];
-                sk[e] = (re.key << 32) | e;
-                sw[e] = re.weight;
-            } else {
-                sk[e] = ~0ull;
-            }
-        }
-        __syncwarp();
-        bitonic_warp<uint64_t>(sk, P2, lane);
-        uint32_t carry = 0;
-        for (int c0 = 0; c0 < m; c0 += 32) {
-            const int i = c0 + (int)lane;
-            const uint32_t e = i < m ? (uint32_t)(sk[i] & 0xffffffffu) : 0u;
-            const uint32_t v = i < m ? sw[e] : 0u;
-            uint32_t inc = v;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t t = __shfl_up_sync(FULL_MASK, inc, o);
-                if ((int)lane >= o) inc += t;
-            }
-            if (i < m) start[memb[lo + e].out] = carry + inc - v;
-            carry += __shfl_sync(FULL_MASK, inc, 31);
-        }
+        // 64 < m <= SEG_SMEM: register bitonic sort of (key << 32 | index),
+        // then the weights scanned in that order
+        if (m <= 128) seg_rank_sorted<4>(lo, m, memb, start, s_wt[wib], reinterpret_cast<uint32_t *>(s_key[wib]), lane);
+        else seg_rank_sorted<8>(lo, m, memb, start, s_wt[wib], reinterpret_cast<uint32_t *>(s_key[wib]), lane);
         __syncwarp();
     }
 }
