@@ -385,14 +385,17 @@ int rank_memberships(knnm_ctx *c, bool fused = false) {
     unsigned long long *cnt = c->counters.as<unsigned long long>();
     CK(cudaMemsetAsync(cnt + C_SEGHEAVY, 0, sizeof(unsigned long long), c->st));
     const unsigned long long *mp = fused ? c->mpack.as<unsigned long long>() : nullptr;
+    // fused rounds: the row totals (bucket sizes) come from here, not from
+    // per-membership atomics in k_assemble
+    uint32_t *tot = fused ? c->bound.as<uint32_t>() : nullptr;
     k_seg_rank<<<grid_for(c, c->n * 32, SEG_WARPS * 32, 16), SEG_WARPS * 32, 0, c->st>>>(
         c->n, c->moff.as<uint32_t>(), c->memb.as<MembRec>(), c->start.as<uint32_t>(), mp,
-        c->segheavy.as<int32_t>(), cnt);
+        c->segheavy.as<int32_t>(), cnt, tot);
     CKL();
     // hub rows: block per row, count read on the device
     k_seg_rank_heavy<<<c->sms * 2, SEGH_THREADS, 0, c->st>>>(
         c->moff.as<uint32_t>(), c->memb.as<MembRec>(), c->start.as<uint32_t>(), mp,
-        c->segheavy.as<int32_t>(), cnt);
+        c->segheavy.as<int32_t>(), cnt, tot);
     CKL();
     return KNNM_OK;
 }
@@ -1357,7 +1360,8 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                         c->mcount.as<uint32_t>(), nullptr, nullptr, nullptr);
                     CKL();
                 }
-                TRY(scan<uint32_t, uint64_t>(c, c->bound.as<uint32_t>(), c->boff.as<uint64_t>(), n));
+                // fused: bucket sizes are written by rank_memberships below
+                if (!fused) TRY(scan<uint32_t, uint64_t>(c, c->bound.as<uint32_t>(), c->boff.as<uint64_t>(), n));
                 TRY(ensure_slots(c, pairs2));
                 if (!fused) {
                     TRY(scan<uint32_t, uint32_t>(c, c->mcount.as<uint32_t>(), c->moff.as<uint32_t>(), n));
@@ -1369,6 +1373,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                     CKL();
                 }
                 TRY(rank_memberships(c, fused));
+                if (fused) TRY(scan<uint32_t, uint64_t>(c, c->bound.as<uint32_t>(), c->boff.as<uint64_t>(), n));
                 const uint64_t *boff = c->boff.as<uint64_t>();
                 const uint32_t *stt = c->start.as<uint32_t>();
                 double *Bd = c->Bd.as<double>();

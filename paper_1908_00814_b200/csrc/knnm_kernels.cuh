@@ -853,7 +853,8 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
                     if (mk & (1 << c)) part += cnt4[c];
                 if (part > 0) {
                     const uint32_t x = e >> 2;
-                    atomicAdd(&bound[x], (uint32_t)part);
+                    // fused: the row totals come from k_seg_rank instead
+                    if (!memb) atomicAdd(&bound[x], (uint32_t)part);
                     if (memb) {
                         // fused membership record (unsharded, unchunked
                         // rounds): row x lies in at most indeg(x) + k hoods
@@ -2102,7 +2103,7 @@ __global__ void k_directed_memb(const int32_t *__restrict__ rows, int64_t m, uin
 // Rank a row's m <= 32 * NE memberships: keys sorted in registers, weights
 // and output positions staged in shared memory, weighted exclusive scan.
 template <int NE>
-__device__ __forceinline__ void seg_rank_sorted(uint32_t lo, int m, const MembRec *__restrict__ memb,
+__device__ __forceinline__ uint32_t seg_rank_sorted(uint32_t lo, int m, const MembRec *__restrict__ memb,
                                                 uint32_t *__restrict__ start, uint32_t *sw, uint32_t *so,
                                                 unsigned lane) {
     uint64_t v[NE];
@@ -2136,13 +2137,14 @@ __device__ __forceinline__ void seg_rank_sorted(uint32_t lo, int m, const MembRe
         carry += __shfl_sync(FULL_MASK, inc, 31);
     }
     __syncwarp();
+    return carry;  // the row's total weight
 }
 
 constexpr int SEG_WARPS = 8;
 __global__ void __launch_bounds__(SEG_WARPS * 32)
 k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restrict__ memb,
            uint32_t *__restrict__ start, const unsigned long long *__restrict__ mpack,
-           int32_t *heavy, unsigned long long *counters) {
+           int32_t *heavy, unsigned long long *counters, uint32_t *__restrict__ total) {
     __shared__ uint64_t s_key[SEG_WARPS][SEG_SMEM];
     __shared__ uint32_t s_wt[SEG_WARPS][SEG_SMEM];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
@@ -2188,6 +2190,10 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
                 acc += kf < rec.key ? wf : 0u;
             }
             if ((int)lane < m) start[rec.out] = acc;
+            if (total) {
+                const uint32_t t = __reduce_add_sync(FULL_MASK, (int)lane < m ? rec.weight : 0u);
+                if (lane == 0) total[r] = t;
+            }
             continue;
         }
         if (m <= 64) {
@@ -2206,6 +2212,10 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
             }
             start[rec.out] = acc0;
             if ((int)lane + 32 < m) start[rb.out] = acc1;
+            if (total) {
+                const uint32_t t = __reduce_add_sync(FULL_MASK, rec.weight + rb.weight);
+                if (lane == 0) total[r] = t;
+            }
             continue;
         }
         if (m > SEG_SMEM) {  // hub row: ranked by a whole block later
@@ -2214,8 +2224,10 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
         }
         // 64 < m <= SEG_SMEM: register bitonic sort of (key << 32 | index),
         // then the weights scanned in that order
-        if (m <= 128) seg_rank_sorted<4>(lo, m, memb, start, s_wt[wib], reinterpret_cast<uint32_t *>(s_key[wib]), lane);
-        else seg_rank_sorted<8>(lo, m, memb, start, s_wt[wib], reinterpret_cast<uint32_t *>(s_key[wib]), lane);
+        const uint32_t t = m <= 128
+            ? seg_rank_sorted<4>(lo, m, memb, start, s_wt[wib], reinterpret_cast<uint32_t *>(s_key[wib]), lane)
+            : seg_rank_sorted<8>(lo, m, memb, start, s_wt[wib], reinterpret_cast<uint32_t *>(s_key[wib]), lane);
+        if (total && lane == 0) total[r] = t;
         __syncwarp();
     }
 }
@@ -2228,7 +2240,8 @@ constexpr int SEGH_SMEM = 4096;  // keys staged in shared memory per block
 __global__ void __launch_bounds__(SEGH_THREADS)
 k_seg_rank_heavy(const uint32_t *__restrict__ moff, const MembRec *__restrict__ memb,
                  uint32_t *__restrict__ start, const unsigned long long *__restrict__ mpack,
-                 const int32_t *__restrict__ heavy, const unsigned long long *__restrict__ counters) {
+                 const int32_t *__restrict__ heavy, const unsigned long long *__restrict__ counters,
+                 uint32_t *__restrict__ total) {
     __shared__ uint64_t s_k[SEGH_SMEM];
     __shared__ uint32_t s_w[SEGH_SMEM];
     const int64_t nh = (int64_t)counters[C_SEGHEAVY];
@@ -2245,10 +2258,18 @@ k_seg_rank_heavy(const uint32_t *__restrict__ moff, const MembRec *__restrict__ 
         }
         const int m = (int)(hi - lo);
         const int ms = m < SEGH_SMEM ? m : SEGH_SMEM;
-        for (int e = threadIdx.x; e < ms; e += blockDim.x) {
-            s_k[e] = memb[lo + e].key;
-            s_w[e] = memb[lo + e].weight;
+        uint32_t part = 0;
+        for (int e = threadIdx.x; e < m; e += blockDim.x) {
+            const MembRec re = memb[lo + e];
+            if (e < ms) {
+                s_k[e] = re.key;
+                s_w[e] = re.weight;
+            }
+            part += re.weight;
         }
+        // row total (total[] is zero for rows ranked here: fused rounds
+        // leave the bucket sizes to the ranking)
+        if (total && part) atomicAdd(&total[x], part);
         __syncthreads();
         for (int e = threadIdx.x; e < m; e += blockDim.x) {
             const MembRec re = memb[lo + e];
