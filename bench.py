@@ -450,6 +450,12 @@ def run_b200(args):
     slot_b = 8.0 if (inf["cert"] or inf["cert_dot"]) else 12.0
     join_bytes = (row_b + 4.0) * st["members"] + slot_b * st["written_slots"]
     achieved = join_bytes / jk_s / 1e9 if jk_s > 0 else 0.0
+    # SURVEY.md 8(d)'s per-unit figure for the same launches: fp32 member rows
+    # (|M_u| * d * 4, the dataset's own format) + 8 B per surviving update.
+    # Reported beside the headline, which counts the bytes this kernel
+    # actually has to gather (u8 rows on config 2).
+    survey_bytes = 4.0 * CFG["d"] * st["members"] + 8.0 * st["written_slots"]
+    achieved_survey = survey_bytes / jk_s / 1e9 if jk_s > 0 else 0.0
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "r1_join_traffic.json")) as f:
@@ -484,7 +490,10 @@ def run_b200(args):
                      "bytes_model": f"(row_bytes + 4) * sum|M_u| + {int(slot_b)} * written_slots",
                      "bytes_per_step": join_bytes / steps,
                      "kernel_ms_per_step": st["join_kernel_ms"] / steps,
-                     "kernel_share_of_step": st["join_kernel_ms"] / max(ms_max, 1e-9)},
+                     "kernel_share_of_step": st["join_kernel_ms"] / max(ms_max, 1e-9),
+                     "survey_formula": {"achieved": achieved_survey, "frac": achieved_survey / hbm_peak,
+                                        "bytes_model": "d * 4 * sum|M_u| + 8 * written_slots "
+                                                       "(SURVEY 8d: fp32 rows as stored in the dataset)"}},
         "stats_per_step": {key: st[key] / steps for key in ("candidates", "written_slots", "exact_evals", "members", "accepted", "join_redos", "rounds")},
         "phases_ms_per_step": {key: st[key] / steps for key in
                                ("join_ms", "join_kernel_ms", "reverse_ms", "assemble_ms", "update_ms", "other_ms")},
