@@ -238,6 +238,15 @@ int knnm_bf_topk(knnm_ctx *ctx, const float *queries, const int64_t *rows, int64
  * summation order, so the value is bit-identical to the reference. */
 int knnm_phi(knnm_ctx *ctx, double *out);
 
+/* The same phi, computed asynchronously on a side stream from the lists as
+ * they are when called (e.g. right after knnm_round): the next round's
+ * reverse, assembly and join overlap it, and every call that writes the
+ * lists waits for it on the device.  knnm_phi_fetch waits for the pending
+ * value and returns the one stored in `slot` (0 <= slot < KNNM_PHI_SLOTS). */
+#define KNNM_PHI_SLOTS 64
+int knnm_phi_async(knnm_ctx *ctx, int32_t slot);
+int knnm_phi_fetch(knnm_ctx *ctx, int32_t slot, double *out);
+
 /* Export the lists in global id space (construct.py:212-223), merging the
  * loaded rear lists back in when merge_rear != 0 (graph.py:259-280,
  * _kernels.py:529-563).  Outputs: ids int32 (n,k), dists float64 (n,k),

@@ -92,6 +92,8 @@ SIGNATURES = {
     "knnm_state_views": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]),
     "knnm_bf_topk": (ctypes.c_int, [P, P, P, I64, I32, I32, P, P]),
     "knnm_phi": (ctypes.c_int, [P, PDBL]),
+    "knnm_phi_async": (ctypes.c_int, [P, I32]),
+    "knnm_phi_fetch": (ctypes.c_int, [P, I32, PDBL]),
     "knnm_export": (ctypes.c_int, [P, I32, P, P, P]),
     "knnm_export_dev": (ctypes.c_int, [P, I32, P, P, P]),
     "knnm_get_state": (ctypes.c_int, [P, P, P, P, P]),

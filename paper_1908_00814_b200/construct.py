@@ -126,23 +126,39 @@ def _descent_rounds(engine, n: int, mode: int, k: int, params, rng, counter, on_
     cap = sample_cap(getattr(params, "rho", 1.0), k)
     rev_cap = cap if rev_cap is None else int(rev_cap)
     engine.set_sample(cap if cap < k else 0)
+    # phi of round `it` is reduced on a side stream while round it+1's
+    # reverse / assembly / join run, and read once that round has synced
+    # (the value is the same; only its report entry is completed later)
+    pending = None  # (RoundStats fields of the previous round, slot)
+
+    def flush():
+        nonlocal pending
+        if pending is None:
+            return
+        (it_, pairs_, acc_, count_), slot = pending
+        cur_phi = engine.phi_fetch(slot)
+        logger.info("iter=%d pairs=%d updates=%d phi=%.6f dists=%d", it_, pairs_, acc_, cur_phi, count_)
+        if report is not None:
+            report.rounds.append(RoundStats(it_, pairs_, acc_, cur_phi, count_))
+        pending = None
+
     for it in range(1, params.max_iters + 1):
         round_seed = int(rng.integers(0, 2**63 - 1))
         pairs, accepted = engine.round(mode, rev_cap, round_seed)
+        flush()
         if pairs > 0:
             counter.add(pairs)
         _emit_captured(engine, on_pair, gids)
         if ROUND_HOOK is not None:
             ROUND_HOOK(engine)
-        cur_phi = engine.phi()
-        logger.info("iter=%d pairs=%d updates=%d phi=%.6f dists=%d",
-                    it, pairs, accepted, cur_phi, counter.count)
-        if report is not None:
-            report.rounds.append(RoundStats(it, pairs, accepted, cur_phi, counter.count))
+        engine.phi_async(it)
+        pending = ((it, pairs, accepted, counter.count), it)
         if accepted <= threshold:
+            flush()
             if report is not None:
                 report.converged = True
             return
+    flush()
     if report is not None:
         report.converged = False
 

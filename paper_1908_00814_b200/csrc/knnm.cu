@@ -20,7 +20,7 @@ using namespace knnm;
 
 struct knnm_ctx;
 extern "C" {
-static int phi_kernels(knnm_ctx *c, const double **res);  // defined with knnm_phi
+static int phi_kernels(knnm_ctx *c, const double **res, cudaStream_t stream);  // defined with knnm_phi
 }
 
 namespace {
@@ -94,6 +94,12 @@ struct knnm_ctx {
     int device = 0;
     int sms = 148;
     cudaStream_t st = nullptr;
+    // asynchronous phi (knnm_phi_async): computed on st2 while the next
+    // round's reverse / assembly / join run on st; list writers wait on ev_phi
+    cudaStream_t st2 = nullptr;
+    cudaEvent_t ev_lists = nullptr, ev_phi = nullptr;
+    bool phi_pending = false;
+    double *hphi = nullptr;  // pinned, KNNM_PHI_SLOTS results
     // dataset
     DBuf vec;
     int64_t n_all = 0;
@@ -265,6 +271,14 @@ int ensure_staging(knnm_ctx *c) {
     return KNNM_OK;
 }
 
+// A pending asynchronous phi reads the lists: writers wait for it on st.
+void phi_wait(knnm_ctx *c) {
+    if (c && c->phi_pending) {
+        cudaStreamWaitEvent(c->st, c->ev_phi, 0);
+        c->phi_pending = false;
+    }
+}
+
 // device union-id table, or nullptr for an identity union
 const int64_t *ugid_of(const knnm_ctx *c) { return c->ug_identity ? nullptr : c->ugid.as<int64_t>(); }
 
@@ -423,6 +437,7 @@ LazyExact lazy_of(knnm_ctx *c) {
 }
 
 int run_updates(knnm_ctx *c) {
+    phi_wait(c);  // the apply writes the lists a pending phi still reads
     int64_t n = c->n;
     unsigned long long *cnt = c->counters.as<unsigned long long>();
     CK(cudaMemsetAsync(cnt + C_CAND, 0, sizeof(unsigned long long) * 2, c->st));
@@ -450,7 +465,7 @@ int run_updates(knnm_ctx *c) {
     CKL();
     // a round's final apply also reduces phi, fetched in the same wait
     const double *phi_res = nullptr;
-    if (c->phi_in_updates && c->n * c->k > 0) TRY(phi_kernels(c, &phi_res));
+    if (c->phi_in_updates && c->n * c->k > 0) TRY(phi_kernels(c, &phi_res, c->st));
     TRY(sync_counters(c));
     if (phi_res) {
         CK(cudaMemcpy(&c->phi_val, phi_res, sizeof(double), cudaMemcpyDeviceToHost));
@@ -690,6 +705,13 @@ int knnm_destroy(knnm_ctx *c) {
     for (auto e : c->marks)
         if (e) cudaEventDestroy(e);
     if (c->hcnt) cudaFreeHost(c->hcnt);
+    if (c->hphi) cudaFreeHost(c->hphi);
+    if (c->st2) {
+        cudaStreamSynchronize(c->st2);
+        cudaStreamDestroy(c->st2);
+    }
+    if (c->ev_lists) cudaEventDestroy(c->ev_lists);
+    if (c->ev_phi) cudaEventDestroy(c->ev_phi);
     cudaStreamDestroy(c->st);
     delete c;
     return KNNM_OK;
@@ -769,6 +791,7 @@ int knnm_set_dataset(knnm_ctx *c, const float *vectors, int64_t n_all, int32_t d
 
 int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *labels, int32_t k) {
     if (c) c->state_gen++;  // the lists may change: cached phi is stale
+    phi_wait(c);
     if (!c || !union_gids || !labels) return fail(KNNM_ERR_ARG, "null argument");
     if (!c->have_data) return fail(KNNM_ERR_STATE, "knnm_set_dataset first");
     if (n < 1) return fail(KNNM_ERR_ARG, "empty union");
@@ -869,6 +892,7 @@ static int load_impl(knnm_ctx *c, const int32_t *rows, int64_t m, const int32_t 
                      const double *g_dists, const int32_t *g_sizes, int32_t gk, int32_t k1,
                      bool on_device) {
     if (c) c->state_gen++;  // the lists may change: cached phi is stale
+    phi_wait(c);
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     if (m == 0) return KNNM_OK;
@@ -940,6 +964,7 @@ int knnm_load_graph_dev(knnm_ctx *c, const int32_t *rows, int64_t m, const int32
 static int insert_impl(knnm_ctx *c, const int32_t *rows, int64_t mrows, int32_t count,
                        const int32_t *nids, int64_t m, int64_t *accepted, bool nids_on_device) {
     if (c) c->state_gen++;  // the lists may change: cached phi is stale
+    phi_wait(c);
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     if (accepted) *accepted = 0;
@@ -1176,6 +1201,7 @@ int knnm_draws_replace(knnm_ctx *c, const int64_t *rows, int64_t nrows, const in
 int knnm_draws_insert(knnm_ctx *c, const int32_t *rows, const int32_t *pool, int64_t npool,
                       int64_t *accepted) {
     if (c) c->state_gen++;  // the lists may change: cached phi is stale
+    phi_wait(c);
     if (!c || !rows || !pool) return fail(KNNM_ERR_ARG, "bad argument");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     CK(cudaSetDevice(c->device));
@@ -1196,6 +1222,8 @@ int knnm_draws_insert(knnm_ctx *c, const int32_t *rows, const int32_t *pool, int
 static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed,
                       int64_t *pairs, int64_t *accepted, bool local_only) {
     if (c) c->state_gen++;  // the lists may change: cached phi is stale
+    // (no phi_wait here: a pending phi overlaps the reverse, assembly and
+    // join; run_updates waits before the apply writes the lists)
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     if (mode < 0 || mode > 2) return fail(KNNM_ERR_ARG, "mode %d", mode);
@@ -1494,7 +1522,9 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         if (local_only && 2 * P > budget)
             return fail(KNNM_ERR_LIMIT, "sharded round needs %llu slots > budget", (unsigned long long)(2 * P));
         if (2 * P <= budget) {
-            c->phi_in_updates = !local_only;
+            // phi inside the round's final wait, unless the caller reduces it
+            // asynchronously (knnm_phi_async) while the next round runs
+            c->phi_in_updates = !local_only && !c->st2;
             const int rc = run_chunk(c->active.as<int32_t>(), (int64_t)nactive, 2 * P, true);
             c->phi_in_updates = false;
             TRY(rc);
@@ -1612,6 +1642,7 @@ int knnm_local_compact(knnm_ctx *c, void **cnt, void **boff, void **Bd, void **B
 int knnm_round_apply(knnm_ctx *c, int32_t nsrc, const uint32_t *recv_cnt, const uint64_t *recv_base,
                      const double *recv_Bd, const int32_t *recv_Bs, int64_t *accepted) {
     if (c) c->state_gen++;  // the lists may change: cached phi is stale
+    phi_wait(c);
     if (!c || nsrc < 1 || !recv_cnt || !recv_base) return fail(KNNM_ERR_ARG, "bad argument");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     CK(cudaSetDevice(c->device));
@@ -1657,6 +1688,7 @@ int knnm_round_apply(knnm_ctx *c, int32_t nsrc, const uint32_t *recv_cnt, const 
 
 int knnm_state_views(knnm_ctx *c, void **ids, void **dists, void **flags, void **sizes) {
     if (c) c->state_gen++;  // the lists may change: cached phi is stale
+    phi_wait(c);
     if (!c) return fail(KNNM_ERR_ARG, "null ctx");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     if (ids) *ids = c->ids.p;
@@ -1833,7 +1865,7 @@ int knnm_sample_distinct_rows(uint64_t *pcg, int32_t *has_uint32, uint32_t *uint
 
 // Launch the phi reduction (numpy's pairwise tree over the present
 // distances); *res = device address of the result.
-static int phi_kernels(knnm_ctx *c, const double **res) {
+static int phi_kernels(knnm_ctx *c, const double **res, cudaStream_t stream) {
     int64_t N = c->n * c->k;
     if (c->phi.N != N) {
         build_phi_tree(c->phi, N);
@@ -1856,7 +1888,7 @@ static int phi_kernels(knnm_ctx *c, const double **res) {
     }
     int64_t nl = (int64_t)c->phi.leaf_lo.size();
     int64_t ni = (int64_t)c->phi.left.size();
-    k_phi_leaves<<<(unsigned)((nl + 127) / 128), 128, 0, c->st>>>(
+    k_phi_leaves<<<(unsigned)((nl + 127) / 128), 128, 0, stream>>>(
         c->dists.as<double>(), c->sizes.as<int32_t>(), c->k, c->phi_leaf_lo.as<int64_t>(),
         c->phi_leaf_len.as<int32_t>(), nl, c->phi_leaves.as<double>());
     CKL();
@@ -1867,13 +1899,13 @@ static int phi_kernels(knnm_ctx *c, const double **res) {
         for (; h < nlev; h++) {
             const int lo = c->phi.level_start[h], hi = c->phi.level_start[h + 1];
             if (hi - lo < 4096) break;
-            k_phi_level<<<(unsigned)((hi - lo + 255) / 256), 256, 0, c->st>>>(
+            k_phi_level<<<(unsigned)((hi - lo + 255) / 256), 256, 0, stream>>>(
                 c->phi_left.as<int32_t>(), c->phi_right.as<int32_t>(), lo, hi,
                 c->phi_leaves.as<double>(), c->phi_inner.as<double>());
             CKL();
         }
         if (h < nlev) {
-            k_phi_tree<<<1, 1024, 0, c->st>>>(c->phi_left.as<int32_t>(), c->phi_right.as<int32_t>(),
+            k_phi_tree<<<1, 1024, 0, stream>>>(c->phi_left.as<int32_t>(), c->phi_right.as<int32_t>(),
                                               c->phi_level.as<int32_t>() + h, nlev - h,
                                               c->phi_leaves.as<double>(), c->phi_inner.as<double>());
             CKL();
@@ -1882,6 +1914,41 @@ static int phi_kernels(knnm_ctx *c, const double **res) {
     } else {
         *res = c->phi_leaves.as<double>();
     }
+    return KNNM_OK;
+}
+
+int knnm_phi_async(knnm_ctx *c, int32_t slot) {
+    if (!c || slot < 0 || slot >= KNNM_PHI_SLOTS) return fail(KNNM_ERR_ARG, "bad argument");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    CK(cudaSetDevice(c->device));
+    if (!c->st2) {
+        CK(cudaStreamCreateWithFlags(&c->st2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->ev_lists, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&c->ev_phi, cudaEventDisableTiming));
+        CK(cudaHostAlloc((void **)&c->hphi, sizeof(double) * KNNM_PHI_SLOTS, cudaHostAllocDefault));
+    }
+    if (c->n * c->k == 0) {
+        CK(cudaStreamSynchronize(c->st2));
+        c->hphi[slot] = 0.0;
+        return KNNM_OK;
+    }
+    // the lists as of now on st, reduced on st2
+    CK(cudaEventRecord(c->ev_lists, c->st));
+    CK(cudaStreamWaitEvent(c->st2, c->ev_lists, 0));
+    const double *r = nullptr;
+    TRY(phi_kernels(c, &r, c->st2));
+    CK(cudaMemcpyAsync(c->hphi + slot, r, sizeof(double), cudaMemcpyDeviceToHost, c->st2));
+    CK(cudaEventRecord(c->ev_phi, c->st2));
+    c->phi_pending = true;
+    return KNNM_OK;
+}
+
+int knnm_phi_fetch(knnm_ctx *c, int32_t slot, double *out) {
+    if (!c || !out || slot < 0 || slot >= KNNM_PHI_SLOTS) return fail(KNNM_ERR_ARG, "bad argument");
+    if (!c->st2) return fail(KNNM_ERR_STATE, "knnm_phi_async first");
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->st2));
+    *out = c->hphi[slot];
     return KNNM_OK;
 }
 
@@ -1899,7 +1966,7 @@ int knnm_phi(knnm_ctx *c, double *out) {
     }
     PhaseTimer pt(c, PH_OTHER);
     const double *r = nullptr;
-    TRY(phi_kernels(c, &r));
+    TRY(phi_kernels(c, &r, c->st));
     CK(cudaMemcpyAsync(&c->phi_val, r, sizeof(double), cudaMemcpyDeviceToHost, c->st));
     CK(cudaStreamSynchronize(c->st));
     c->phi_gen = c->state_gen;
@@ -1910,6 +1977,7 @@ int knnm_phi(knnm_ctx *c, double *out) {
 static int export_impl(knnm_ctx *c, int32_t merge_rear, int32_t *out_ids, double *out_dists,
                        int32_t *out_sizes, bool on_device) {
     if (c) c->state_gen++;  // the lists may change: cached phi is stale
+    phi_wait(c);
     if (!c || !out_ids || !out_dists || !out_sizes) return fail(KNNM_ERR_ARG, "null argument");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
     CK(cudaSetDevice(c->device));

@@ -192,6 +192,18 @@ class Engine:
         check(self._lib.knnm_phi(self._h, ctypes.byref(out)), "knnm_phi")
         return float(out.value)
 
+    PHI_SLOTS = 64  # KNNM_PHI_SLOTS
+
+    def phi_async(self, slot: int) -> None:
+        """Start phi of the current lists on a side stream (knnm_phi_async)."""
+        check(self._lib.knnm_phi_async(self._h, int(slot) % self.PHI_SLOTS), "knnm_phi_async")
+
+    def phi_fetch(self, slot: int) -> float:
+        out = ctypes.c_double()
+        check(self._lib.knnm_phi_fetch(self._h, int(slot) % self.PHI_SLOTS, ctypes.byref(out)),
+              "knnm_phi_fetch")
+        return float(out.value)
+
     def export(self, merge_rear: bool, on_device: bool = False):
         if on_device:
             import torch
