@@ -1264,9 +1264,15 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
             c->roff.as<uint32_t>(), lo, hi, std::max(rev_cap, WARP_REV_MAX), c->heavy.as<int32_t>(), cnt,
             c->live.as<uint8_t>(), c->giant.as<int32_t>(), BLOCK_SORT_MAX);
         CKL();
+        // heavy segments: most fit a 2 x 16 KB sort (several blocks per SM),
+        // the rest a 2 x 64 KB one
+        k_rev_heavy<<<c->sms * 8, 256, 2 * sizeof(uint32_t) * HEAVY_SORT_SMALL, c->st>>>(
+            c->heavy.as<int32_t>(), cnt, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(), rev_cap,
+            round_seed, nullptr, HEAVY_SORT_SMALL, 0);
+        CKL();
         k_rev_heavy<<<c->sms * 2, 256, 2 * sizeof(uint32_t) * BLOCK_SORT_MAX, c->st>>>(
             c->heavy.as<int32_t>(), cnt, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(), rev_cap,
-            round_seed, nullptr, BLOCK_SORT_MAX);
+            round_seed, nullptr, BLOCK_SORT_MAX, HEAVY_SORT_SMALL);
         CKL();
         // rows too long for a block's shared memory (in-degree above
         // BLOCK_SORT_MAX): one block in global scratch sized for any degree
@@ -1275,7 +1281,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
             TRY(ensure(c->gscratch32, 2 * sizeof(uint32_t) * next_pow2((uint32_t)n)));
             k_rev_heavy<<<1, 1024, 0, c->st>>>(c->giant.as<int32_t>(), cnt, c->roff.as<uint32_t>(),
                                                c->rev.as<uint32_t>(), rev_cap, round_seed,
-                                               c->gscratch32.as<uint32_t>(), BLOCK_SORT_MAX);
+                                               c->gscratch32.as<uint32_t>(), BLOCK_SORT_MAX, 0);
             CKL();
         }
     }

@@ -13,6 +13,7 @@ namespace knnm {
 
 constexpr int WARP_REV_MAX = 256;      // reverse segments a warp sorts itself
 constexpr int BLOCK_SORT_MAX = 16384;  // elements a block sorts in shared memory
+constexpr int HEAVY_SORT_SMALL = 4096; // ... in the first (small shared memory) heavy pass
 constexpr int MAX_W = 128;             // k + rev_cap upper bound
 constexpr int SEG_SMEM = 256;          // membership segments ranked in shared memory
 
@@ -607,9 +608,12 @@ __device__ void block_fy_select(uint32_t *seg, uint32_t *idx, uint32_t *R, uint3
 // selected entries overwrite the first rev_cap slots of the segment.
 // gscratch == nullptr: the rows of `heavy` that fit shared memory; else the
 // `giant` list (counters[C_GIANT]) in global scratch.
+// Segments with smem_min < next_pow2(deg) <= smem_max are sorted in shared
+// memory (launched once with a small smem_max, so that many blocks share an
+// SM, and once for the rest); gscratch != nullptr: the giant pass.
 __global__ void k_rev_heavy(const int32_t *__restrict__ heavy, const unsigned long long *counters,
                             const uint32_t *__restrict__ roff, uint32_t *rev, int rev_cap,
-                            uint64_t seed, uint32_t *gscratch, int smem_max) {
+                            uint64_t seed, uint32_t *gscratch, int smem_max, int smem_min) {
     extern __shared__ uint32_t hs[];
     __shared__ uint32_t R[MAX_W];
     unsigned long long cnt = counters[gscratch ? C_GIANT : C_HEAVY_REV];
@@ -619,8 +623,9 @@ __global__ void k_rev_heavy(const int32_t *__restrict__ heavy, const unsigned lo
         uint32_t deg = roff[u + 1] - lo;
         uint32_t P2 = next_pow2(deg);
         bool in_smem = P2 <= (uint32_t)smem_max;
-        if (!in_smem && gscratch == nullptr) continue;  // giant: second pass
+        if (!in_smem && gscratch == nullptr) continue;  // a later pass
         if (in_smem && gscratch != nullptr) continue;
+        if (gscratch == nullptr && P2 <= (uint32_t)smem_min) continue;  // an earlier pass
         uint32_t *seg = in_smem ? hs : gscratch;
         uint32_t *idx = seg + P2;
         for (uint32_t j = threadIdx.x; j < P2; j += blockDim.x) seg[j] = j < deg ? rev[lo + j] : 0xffffffffu;
