@@ -990,8 +990,42 @@ static int insert_impl(knnm_ctx *c, const int32_t *rows, int64_t mrows, int32_t 
     }
     unsigned long long *cnt = c->counters.as<unsigned long long>();
     int64_t acc_total = 0;
+    bool direct = false;
+    if (count > 0) {
+        // row-grouped inserts with distinct rows take the direct per-row path
+        TRY(ensure(c->segheavy, sizeof(uint32_t) * (size_t)((c->n + 31) / 32 + 1)));
+        CK(cudaMemsetAsync(c->segheavy.p, 0, sizeof(uint32_t) * (size_t)((c->n + 31) / 32 + 1), c->st));
+        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
+        k_rows_distinct<<<grid_for(c, mrows, 256), 256, 0, c->st>>>(
+            c->stage[3].as<int32_t>(), mrows, c->segheavy.as<uint32_t>(), cnt);
+        CKL();
+        unsigned long long dups = 0;
+        CK(cudaMemcpyAsync(&c->hcnt[C_DUPROWS], cnt + C_DUPROWS, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        dups = c->hcnt[C_DUPROWS];
+        direct = dups == 0;
+    }
+    if (direct) {
+        PhaseTimer pt(c, PH_UPDATE);
+        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
+        const int E = (c->k + 31) / 32;
+        const int blocks = grid_for(c, mrows * 32, 256, 8);
+#define KNNM_IRD_LAUNCH(EE)                                                                          \
+    k_insert_rows_direct<EE><<<blocks, 256, 0, c->st>>>(                                            \
+        c->stage[3].as<int32_t>(), mrows, count, c->stage[1].as<int32_t>(), c->subp, c->dp, c->d,    \
+        c->metric, (int)(c->cert && c->metric != KNNM_COSINE), c->cert_u8 ? c->sub16p : nullptr,     \
+        c->rowb, c->cert_u8 ? c->subnormp : nullptr, c->ids.as<int32_t>(), c->dists.as<double>(),   \
+        c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), c->k, capd, cnt)
+        if (E == 1) KNNM_IRD_LAUNCH(1);
+        else KNNM_IRD_LAUNCH(2);
+#undef KNNM_IRD_LAUNCH
+        CKL();
+        TRY(sync_counters(c));
+        acc_total = (int64_t)c->hcnt[C_ACCEPTED];
+    }
     const int64_t chunk = (int64_t)std::max<uint64_t>(bucket_budget(c), 1u << 20);
-    for (int64_t c0 = 0; c0 < m; c0 += chunk) {
+    for (int64_t c0 = 0; c0 < m && !direct; c0 += chunk) {
         const int64_t cm = std::min<int64_t>(chunk, m - c0);
         const int32_t *rows_d = c->stage[0].as<int32_t>() + c0;
         CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));

@@ -27,6 +27,7 @@ enum Counter {
     C_WRITTEN = 11,   // update slots written by the join (prefilter survivors)
     C_SEGHEAVY = 12,  // rows with > SEG_SMEM memberships (block-ranked)
     C_GIANT = 13,     // heavy rows whose reverse segment exceeds a block's smem
+    C_DUPROWS = 14,   // rows given twice to a row-grouped insert (direct path check)
     C_NUM = 20
 };
 

@@ -446,6 +446,62 @@ __global__ void k_directed_emit(const int32_t *__restrict__ rows, const int32_t 
     }
 }
 
+// Row-grouped directed inserts (insert_rows / draws_insert: every row given
+// once, with `count` candidates in order): apply_updates_directed
+// (_kernels.py:208-214) is _insert per candidate in input order, rows
+// independent, so one warp per row applies them straight from registers --
+// no bucket layout, ranking or slot round trip.  Distances as k_directed_emit.
+template <int E>
+__global__ void __launch_bounds__(256)
+k_insert_rows_direct(const int32_t *__restrict__ rows, int64_t mrows, int count,
+                     const int32_t *__restrict__ nids, const float *__restrict__ sub, int dp, int d,
+                     int tag, int cert, const uint8_t *__restrict__ sub8, int rowb,
+                     const float *__restrict__ norms8, int32_t *ids, double *dists, uint8_t *flags,
+                     int32_t *sizes, int k, double *cap_d, unsigned long long *counters) {
+    const unsigned lane = lane_id();
+    const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+    unsigned long long acc = 0;
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < mrows; i += nw) {
+        const int32_t r = rows[i];
+        WarpRow<E, double> s;
+        row_load<E, double>(s, ids, dists, flags, sizes, r, k, lane);
+        int a = 0;
+        for (int t0 = 0; t0 < count; t0 += 32) {
+            const int t = t0 + (int)lane;
+            int32_t src = 0;
+            double dd = 0.0;
+            if (t < count) {
+                src = nids[i * count + t];
+                dd = sub8 ? u8_dist(sub8 + (int64_t)r * rowb, sub8 + (int64_t)src * rowb, rowb, norms8[r], norms8[src])
+                   : cert ? cert_dist(sub + (int64_t)r * dp, sub + (int64_t)src * dp, dp, tag)
+                          : exact_dist_tag(tag, sub + (int64_t)r * dp, sub + (int64_t)src * dp, d);
+                if (cap_d) cap_d[i * count + t] = dd;
+            }
+            const int cnt = count - t0 < 32 ? count - t0 : 32;
+            for (int j = 0; j < cnt; j++) {
+                const int sj = __shfl_sync(FULL_MASK, src, j);
+                const double dj = __shfl_sync(FULL_MASK, dd, j);
+                a += warp_insert<E, true, double>(s, k, sj, dj, lane);
+            }
+        }
+        if (a) row_store<E, double>(s, ids, dists, flags, sizes, r, k, lane);
+        acc += (unsigned long long)a;
+    }
+    if (lane == 0 && acc) atomicAdd(&counters[C_ACCEPTED], acc);
+}
+
+// Duplicate-row test for the direct path: counters[C_DUPROWS] > 0 when a
+// row occurs twice in rows[0, m).
+__global__ void k_rows_distinct(const int32_t *__restrict__ rows, int64_t m, uint32_t *bits,
+                                unsigned long long *counters) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t r = (uint32_t)rows[i];
+        const uint32_t b = 1u << (r & 31);
+        if (atomicOr(&bits[r >> 5], b) & b) atomicAdd(&counters[C_DUPROWS], 1ull);
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Reverse CSR (_kernels.py:262-281): in-degree histogram, then scatter of
 // (source << 1 | new-flag).  Segment order is restored where it matters
