@@ -2023,29 +2023,35 @@ static int export_impl(knnm_ctx *c, int32_t merge_rear, int32_t *out_ids, double
     CK(cudaSetDevice(c->device));
     PhaseTimer pt(c, PH_OTHER);
     int64_t n = c->n, nk = c->n * c->k;
+    const bool rear = merge_rear && c->have_tail && c->tk > 0;
+    // device outputs are written in place by the last kernel (no copies)
     TRY(ensure(c->out_ids, sizeof(int32_t) * nk));
-    k_export<<<grid_for(c, nk, 256), 256, 0, c->st>>>(c->ids.as<int32_t>(), ugid_of(c),
-                                                       nk, c->out_ids.as<int32_t>());
+    int32_t *exp_ids = (on_device && !rear) ? out_ids : c->out_ids.as<int32_t>();
+    k_export<<<grid_for(c, nk, 256), 256, 0, c->st>>>(c->ids.as<int32_t>(), ugid_of(c), nk, exp_ids);
     CKL();
-    const void *src_i = c->out_ids.p, *src_d = c->dists.p, *src_s = c->sizes.p;
-    if (merge_rear && c->have_tail && c->tk > 0) {
+    const void *src_i = exp_ids, *src_d = c->dists.p, *src_s = c->sizes.p;
+    if (rear) {
         TRY(ensure(c->out_d, sizeof(double) * nk));
         TRY(ensure(c->out_s, sizeof(int32_t) * n));
         TRY(ensure(c->stage[0], sizeof(int32_t) * nk));
+        int32_t *oi = on_device ? out_ids : c->stage[0].as<int32_t>();
+        double *od = on_device ? out_dists : c->out_d.as<double>();
+        int32_t *os = on_device ? out_sizes : c->out_s.as<int32_t>();
         const size_t mr_smem = mr_smem_bytes(c->k, c->tk);
         k_merge_rear<<<(unsigned)((n + MR_ROWS - 1) / MR_ROWS), MR_ROWS, mr_smem, c->st>>>(
             c->out_ids.as<int32_t>(), c->dists.as<double>(), c->sizes.as<int32_t>(),
             c->tail_ids.as<int32_t>(), c->tail_d.as<double>(), c->tail_s.as<int32_t>(), n, c->k,
-            c->tk, c->stage[0].as<int32_t>(), c->out_d.as<double>(), c->out_s.as<int32_t>());
+            c->tk, oi, od, os);
         CKL();
-        src_i = c->stage[0].p;
-        src_d = c->out_d.p;
-        src_s = c->out_s.p;
+        src_i = oi;
+        src_d = od;
+        src_s = os;
     }
     if (on_device) {
-        CK(cudaMemcpyAsync(out_ids, src_i, sizeof(int32_t) * nk, cudaMemcpyDeviceToDevice, c->st));
-        CK(cudaMemcpyAsync(out_dists, src_d, sizeof(double) * nk, cudaMemcpyDeviceToDevice, c->st));
-        CK(cudaMemcpyAsync(out_sizes, src_s, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, c->st));
+        if (!rear) {
+            CK(cudaMemcpyAsync(out_dists, src_d, sizeof(double) * nk, cudaMemcpyDeviceToDevice, c->st));
+            CK(cudaMemcpyAsync(out_sizes, src_s, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, c->st));
+        }
     } else {
         TRY(d2h(c, out_ids, src_i, sizeof(int32_t) * nk));
         TRY(d2h(c, out_dists, src_d, sizeof(double) * nk));
