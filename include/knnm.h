@@ -79,6 +79,8 @@ typedef struct knnm_stats {
     double join_kernel_ms; /* local-join kernel alone (roofline denominator) */
     int64_t written_slots; /* update slots the join wrote (prefilter survivors) */
     int64_t join_row_bytes; /* bytes per gathered member row in the join   */
+    int64_t heavy_rev_rows; /* reverse segments longer than a warp sorts (block path) */
+    int64_t seg_hub_rows;   /* rows with more memberships than a warp ranks (block path) */
 } knnm_stats;
 
 const char *knnm_last_error(void);

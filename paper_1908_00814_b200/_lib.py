@@ -56,6 +56,8 @@ class KnnmStats(ctypes.Structure):
         ("join_kernel_ms", ctypes.c_double),
         ("written_slots", I64),
         ("join_row_bytes", I64),
+        ("heavy_rev_rows", I64),
+        ("seg_hub_rows", I64),
     ]
 
     def as_dict(self) -> dict:

@@ -473,6 +473,7 @@ int run_updates(knnm_ctx *c) {
     }
     c->stats.candidates += (int64_t)c->hcnt[C_CAND];
     c->stats.written_slots += (int64_t)c->hcnt[C_WRITTEN];
+    c->stats.seg_hub_rows += (int64_t)c->hcnt[C_SEGHEAVY];
     return KNNM_OK;
 }
 
@@ -1365,6 +1366,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
     P = c->hcnt[C_NUM - 1];
     unsigned long long nactive = c->hcnt[C_ACTIVE];
     c->stats.members += (int64_t)c->hcnt[C_MEMBERS];
+    c->stats.heavy_rev_rows += (int64_t)c->hcnt[C_HEAVY_REV];
     c->stats.pairs += (int64_t)P;
     c->stats.rounds += 1;
 
