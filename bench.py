@@ -384,7 +384,10 @@ def run_b200(args):
     if args.rho_half:
         p_half = km.MergeParams(k=k, r=CFG["r"], seed=CFG["merge_seed"], rho=0.5)
         step_device_half = lambda: merge(g_dev, h_dev, km.DistanceCounter(), True, p=p_half)  # noqa: E731
-        _w = step_device_half()
+        # warm-up as for the headline: results held like the timed loop's
+        _w = None
+        for _ in range(max(2, args.warmup)):
+            _w = step_device_half()
         del _w
         barrier()
         eng.reset_stats()
