@@ -1997,8 +1997,8 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                             U8 ? (double)((__float_as_int(R.nrm) + __float_as_int(C.nrm)) - 2 * iacc[s])
                                : (double)((R.nrm + C.nrm) - 2.0f * acc[s]);
                         unsigned long long *Bp = reinterpret_cast<unsigned long long *>(Bd);
-                        if (dd < R.w) Bp[mj_slot(R, C)] = pack_slot(dd, C.id);  // id[ii] <- id[jj]
-                        if (dd < C.w) Bp[mj_slot(C, R)] = pack_slot(dd, R.id);  // id[jj] <- id[ii]
+                        if (dd < R.w) __stcs(Bp + mj_slot(R, C), pack_slot(dd, C.id));  // id[ii] <- id[jj]
+                        if (dd < C.w) __stcs(Bp + mj_slot(C, R), pack_slot(dd, R.id));  // id[jj] <- id[ii]
                     }
                 }
             }
@@ -2399,7 +2399,8 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
         slots += (unsigned long long)ns;
         const double inf = __longlong_as_double(0x7ff0000000000000LL);
         // the next 32 slot distances are loaded while this chunk is applied
-        double dnext = (int64_t)lane < ns ? Bd[lo + lane] : inf;
+        // slots are read once: streaming loads keep L2 for the lists
+        double dnext = (int64_t)lane < ns ? __ldcs(Bd + lo + lane) : inf;
         // F32: every list distance is an exact fp32 value (packed rounds on
         // certified data whose loaded lists passed the exactness check)
         using T = typename std::conditional<F32, float, double>::type;
@@ -2409,7 +2410,7 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
         for (int64_t c0 = 0; c0 < ns; c0 += 32) {
             const int64_t j = c0 + lane;
             double dl = dnext;
-            dnext = j + 32 < ns ? Bd[lo + j + 32] : inf;
+            dnext = j + 32 < ns ? __ldcs(Bd + lo + j + 32) : inf;
             // an unwritten slot (NaN) belongs to a row that was full at round
             // start and a distance >= its worst: it can never pass
             int src;
