@@ -29,6 +29,12 @@ struct MembRec {  // one (hood, member) membership, bucketed by member row
     uint32_t out;    // where its exclusive rank goes: u * W + p (or ordinal)
 };
 
+// Streaming (read-once) load of a membership record.
+__device__ __forceinline__ MembRec ldcs_memb(const MembRec *p) {
+    const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(p));
+    return MembRec{((uint64_t)v.y << 32) | v.x, v.z, v.w};
+}
+
 // Admissible partner classes of a member, by pair mode and member class
 // (class = (label != 0) * 2 + !new; _kernels.py:391-399).  bit c set ->
 // members of class c are partners; SELF: the member's own class is in the
@@ -2230,7 +2236,7 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
     MembRec rec1 = MembRec{0, 0, 0};
     if (r < n) {
         seg(r, lo1, hi1);
-        if (lane < hi1 - lo1) rec1 = memb[lo1 + lane];
+        if (lane < hi1 - lo1) rec1 = ldcs_memb(memb + lo1 + lane);
     }
     if (r + nw < n) seg(r + nw, lo2, hi2);
     for (; r < n; r += nw) {
@@ -2239,7 +2245,7 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
         const MembRec rec = rec1;
         lo1 = lo2;
         hi1 = hi2;
-        rec1 = (r + nw < n && lane < hi1 - lo1) ? memb[lo1 + lane] : MembRec{0, 0, 0};
+        rec1 = (r + nw < n && lane < hi1 - lo1) ? ldcs_memb(memb + lo1 + lane) : MembRec{0, 0, 0};
         if (r + 2 * nw < n) seg(r + 2 * nw, lo2, hi2);
         if (m == 0) continue;
         if (m <= 32) {
@@ -2260,7 +2266,7 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
         if (m <= 64) {
             // two memberships per lane, the same weighted count of smaller
             // keys (keys are unique within a row: hood ids / ordinals)
-            const MembRec rb = (int)lane + 32 < m ? memb[lo + 32 + lane] : MembRec{~0ull, 0, 0};
+            const MembRec rb = (int)lane + 32 < m ? ldcs_memb(memb + lo + 32 + lane) : MembRec{~0ull, 0, 0};
             uint32_t acc0 = 0, acc1 = 0;
 #pragma unroll 4
             for (int f = 0; f < m; f++) {
