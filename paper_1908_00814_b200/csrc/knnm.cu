@@ -131,7 +131,7 @@ struct knnm_ctx {
     int join_variant = -1;  // -1 auto, 0 exact (fp64 every pair), 1 tiled, 2 tensor core
     bool u8_enabled = true;
     // current merge
-    DBuf sub, ugid, labels;
+    DBuf sub, ugid, labels, labbits;
     bool ug_identity = false;  // union = 0 .. n_all-1: ugid not uploaded
     const float *subp = nullptr;
     int64_t n = 0;
@@ -682,7 +682,7 @@ int knnm_destroy(knnm_ctx *c) {
     if (!c) return KNNM_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->st);
-    DBuf *all[] = {&c->vec, &c->sub, &c->ugid, &c->labels, &c->ids, &c->dists, &c->flags,
+    DBuf *all[] = {&c->vec, &c->sub, &c->ugid, &c->labels, &c->labbits, &c->ids, &c->dists, &c->flags,
                    &c->sizes, &c->tail_ids, &c->tail_d, &c->tail_s, &c->indeg, &c->roff,
                    &c->rev, &c->heavy, &c->giant, &c->gscratch32, &c->nbh, &c->nlen, &c->hpairs,
                    &c->poff, &c->worst0, &c->active, &c->wcnt, &c->woff, &c->cBd, &c->cBs, &c->order, &c->lab0, &c->lab1, &c->bound, &c->boff, &c->mcount, &c->moff, &c->mcur, &c->memb, &c->start, &c->Bd, &c->Bs,
@@ -852,6 +852,10 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     }
     TRY(ensure(c->labels, n));
     TRY(h2d(c, c->labels.p, labels, n));
+    TRY(ensure(c->labbits, sizeof(uint32_t) * (size_t)((n + 31) / 32 + 1)));
+    k_label_bits<<<grid_for(c, (n + 31) / 32, 256), 256, 0, c->st>>>(c->labels.as<int8_t>(), n,
+                                                                     c->labbits.as<uint32_t>());
+    CKL();
     size_t nk = (size_t)n * k;
     TRY(ensure(c->ids, sizeof(int32_t) * nk));
     TRY(ensure(c->dists, sizeof(double) * nk));
@@ -1350,7 +1354,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         k_assemble<<<grid_for(c, (hi - lo) * 32, ASM_WARPS * 32, 16), ASM_WARPS * 32, 0, c->st>>>(
             c->ids.as<int32_t>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
             c->dists.as<double>(), hi, k, rev_cap, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(),
-            round_seed, c->labels.as<int8_t>(), mode, W, c->nbh.as<uint32_t>(),
+            round_seed, c->labbits.as<uint32_t>(), mode, W, c->nbh.as<uint32_t>(),
             c->nlen.as<int32_t>(), c->hpairs.as<uint32_t>(), c->worst0.as<double>(),
             c->active.as<int32_t>(), cnt, lo, c->bound.as<uint32_t>(), c->mcount.as<uint32_t>(),
             (!local_only && c->have_order) ? c->order.as<int32_t>() : nullptr,

@@ -723,6 +723,20 @@ __global__ void k_label_prop(const int32_t *__restrict__ ids, const uint8_t *__r
     }
 }
 
+// labels (int8, one per row) -> bitmap, one bit per row.
+__global__ void k_label_bits(const int8_t *__restrict__ labels, int64_t n, uint32_t *__restrict__ bits) {
+    const int64_t nw = (n + 31) >> 5;
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; w < nw;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t b = 0;
+        for (int i = 0; i < 32; i++) {
+            const int64_t r = w * 32 + i;
+            if (r < n && labels[r] != 0) b |= 1u << i;
+        }
+        bits[w] = b;
+    }
+}
+
 __global__ void k_iota(int32_t *a, int64_t n) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
@@ -796,7 +810,7 @@ __global__ void __launch_bounds__(ASM_WARPS * 32, 6)
 k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__restrict__ sizes,
            const double *__restrict__ dists, int64_t n, int k, int rev_cap,
            const uint32_t *__restrict__ roff, const uint32_t *__restrict__ rev, uint64_t seed,
-           const int8_t *__restrict__ labels, int mode, int W, uint32_t *nbh, int32_t *nlen,
+           const uint32_t *__restrict__ labbits, int mode, int W, uint32_t *nbh, int32_t *nlen,
            uint32_t *hpairs, double *worst0, int32_t *active, unsigned long long *counters,
            int64_t lo, uint32_t *bound, uint32_t *mcount, const int32_t *__restrict__ order,
            MembRec *memb, unsigned long long *mpack, const uint8_t *__restrict__ live) {
@@ -883,7 +897,9 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
             unsigned em = __ballot_sync(FULL_MASK, end);
             int lab = 0;
             if (end) {
-                lab = labels[v >> 1] != 0;
+                // label bitmap (1 bit per row: 8x denser than the int8 labels,
+                // so the random gathers mostly hit L1)
+                lab = (labbits[(v >> 1) >> 5] >> ((v >> 1) & 31)) & 1u;
                 // hood entry: id << 2 | label << 1 | new (the label rides along
                 // so the join needs no dependent labels[] load)
                 nbh[u * W + w + __popc(em & lanemask_lt())] = ((v >> 1) << 2) | ((uint32_t)lab << 1) | (v & 1);
