@@ -475,12 +475,52 @@ __device__ __forceinline__ void lazy_warp_eval(const LazyExact z, int64_t r, boo
     else dl = lazy_warp_eval_t<2>(z, r, need, src, dl, sm, lane);
 }
 
+// _insert for rows held one entry per lane (k <= 32), cheapest tests first:
+// a duplicate id costs one vote; "full and nd >= worst" is read off a
+// ballot (worst = entry k-1, rows sorted by (d, id)) instead of a tracked
+// worst.  Returns 1 (warp-uniform) when accepted.  s.worst is left stale:
+// the caller refreshes it (warp_apply_chunk).
+template <typename T>
+__device__ __forceinline__ int warp_insert1(WarpRow<1, T> &s, int k, int src, T nd, unsigned lane) {
+    const int idf = s.idf[0];
+    const T d = s.d[0];
+    const bool in = (int)lane < s.sz;
+    const int id = idf >> 1;
+    if (__any_sync(FULL_MASK, in && id == src)) return 0;  // already listed
+    const bool full = s.sz == k;
+    const unsigned bs = __ballot_sync(FULL_MASK, in && nd < d);
+    if (full && !((bs >> (k - 1)) & 1u)) return 0;  // nd >= worst (distance only)
+    const unsigned b = bs | __ballot_sync(FULL_MASK, in && nd == d && src < id);
+    const int pos = b ? __ffs(b) - 1 : s.sz;
+    const int last = full ? k - 1 : s.sz;
+    const int up_i = __shfl_up_sync(FULL_MASK, idf, 1);
+    const T up_d = __shfl_up_sync(FULL_MASK, d, 1);
+    const bool here = (int)lane == pos, shift = (int)lane > pos && (int)lane <= last;
+    s.idf[0] = here ? (int)(((uint32_t)src << 1) | 1u) : shift ? up_i : idf;
+    s.d[0] = here ? nd : shift ? up_d : d;
+    if (!full) s.sz += 1;
+    return 1;
+}
+
 // Apply up to 32 in-order candidates held one per lane (lanes [0, cnt)).
 // Candidates that cannot pass the "full and nd >= worst" test are skipped
 // without changing the outcome (worst is non-increasing once a row is full).
 template <int E, typename T = double>
 __device__ __forceinline__ int warp_apply_chunk(WarpRow<E, T> &s, int k, int src_l, T d_l,
                                                 int cnt, unsigned lane) {
+    if constexpr (E == 1) {
+        int acc = 0;
+        unsigned m = __ballot_sync(FULL_MASK, (int)lane < cnt && d_l < dist_inf<T>() &&
+                                                  (s.sz < k || d_l < s.worst));
+        while (m) {
+            const int i = __ffs(m) - 1;
+            m &= m - 1;
+            acc += warp_insert1<T>(s, k, __shfl_sync(FULL_MASK, src_l, i),
+                                   __shfl_sync(FULL_MASK, d_l, i), lane);
+        }
+        if (acc && s.sz == k) s.worst = __shfl_sync(FULL_MASK, s.d[0], (k - 1) & 31);
+        return acc;
+    }
     int acc = 0;
     // d_l = +inf marks an empty slot (real distances are finite); a candidate
     // live at chunk start is re-tested against the current worst when its
