@@ -1768,7 +1768,9 @@ __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1
 
 // One member of a staged hood (32 bytes: two 128-bit shared loads).
 struct __align__(16) MjRec {
-    double w;     // round-start worst of the member's row
+    float w;      // round-start worst of the member's row, rounded up to fp32
+                  // (for an fp32 distance d: d < w <=> d < worst)
+    float pad_;
     uint64_t st;  // first bucket slot of the membership
     int id;       // member row
     float nrm;    // row norm (int bits on the u8 route)
@@ -1793,7 +1795,7 @@ __device__ __forceinline__ MjRec lds_rec(const MjRec *p) {
     const float4 a = reinterpret_cast<const float4 *>(p)[0];
     const float4 b = reinterpret_cast<const float4 *>(p)[1];
     MjRec r;
-    r.w = __hiloint2double(__float_as_int(a.y), __float_as_int(a.x));
+    r.w = a.x;
     r.st = ((uint64_t)(uint32_t)__float_as_int(a.w) << 32) | (uint32_t)__float_as_int(a.z);
     r.id = __float_as_int(b.x);
     r.nrm = b.y;
@@ -1949,7 +1951,7 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                     const int pk = j | (int)((ev0[b] & 1) << 8) | (c << 9) | ((int)partner_self(mode, c) << 11);
                     const uint64_t st = mb0[b] + ms0[b];
                     float4 *dst = reinterpret_cast<float4 *>(rec + sl);
-                    dst[0] = make_float4(__int_as_float(__double2loint(mw0[b])), __int_as_float(__double2hiint(mw0[b])),
+                    dst[0] = make_float4(__double2float_ru(mw0[b]), 0.f,
                                          __int_as_float((int)(uint32_t)st), __int_as_float((int)(uint32_t)(st >> 32)));
                     dst[1] = make_float4(__int_as_float(id), mn0[b], __int_as_float(pk),
                                          __int_as_float((int)q4));
@@ -2015,12 +2017,15 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                         if (ok && tri) ok = ii < jj;
                         if (ok) ok = ((R.pk | C.pk) >> 8) & 1;  // at least one new
                         if (!ok) continue;
-                        const double dd =
-                            U8 ? (double)((__float_as_int(R.nrm) + __float_as_int(C.nrm)) - 2 * iacc[s])
-                               : (double)((R.nrm + C.nrm) - 2.0f * acc[s]);
+                        // fp32 distance: an exact integer (u8) / exact under the
+                        // dot-form certificate (fp16)
+                        const float dd =
+                            U8 ? (float)((__float_as_int(R.nrm) + __float_as_int(C.nrm)) - 2 * iacc[s])
+                               : (R.nrm + C.nrm) - 2.0f * acc[s];
                         unsigned long long *Bp = reinterpret_cast<unsigned long long *>(Bd);
-                        if (dd < R.w) __stcs(Bp + mj_slot(R, C), pack_slot(dd, C.id));  // id[ii] <- id[jj]
-                        if (dd < C.w) __stcs(Bp + mj_slot(C, R), pack_slot(dd, R.id));  // id[jj] <- id[ii]
+                        const unsigned long long pv = (unsigned long long)__float_as_uint(dd) << 32;
+                        if (dd < R.w) __stcs(Bp + mj_slot(R, C), pv | (uint32_t)C.id);  // id[ii] <- id[jj]
+                        if (dd < C.w) __stcs(Bp + mj_slot(C, R), pv | (uint32_t)R.id);  // id[jj] <- id[ii]
                     }
                 }
             }
