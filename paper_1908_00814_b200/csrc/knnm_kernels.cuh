@@ -1808,6 +1808,13 @@ __device__ __forceinline__ MjRec lds_rec(const MjRec *p) {
 // pair_rank): membership start + rank of b's position among a's partners,
 // i.e. byte class(a) of b's q4 (the position prefix count), minus a itself
 // when a is its own class's partner and precedes b.
+// Address form of mj_slot: the record's st holds the byte address of its
+// first slot, so a slot is one 32-bit offset from it.
+__device__ __forceinline__ unsigned long long *mj_slot_ptr(const MjRec &a, const MjRec &b) {
+    const int pa = a.pk & 0xFF, pb = b.pk & 0xFF, ca = (a.pk >> 9) & 3;
+    const uint32_t off = ((b.q4 >> (8 * ca)) & 0xFFu) - (uint32_t)(((a.pk >> 11) & 1) && pa < pb);
+    return reinterpret_cast<unsigned long long *>(a.st) + off;
+}
 __device__ __forceinline__ uint64_t mj_slot(const MjRec &a, const MjRec &b) {
     const int pa = a.pk & 0xFF, pb = b.pk & 0xFF, ca = (a.pk >> 9) & 3;
     return a.st + ((b.q4 >> (8 * ca)) & 0xFFu) - (uint32_t)(((a.pk >> 11) & 1) && pa < pb);
@@ -1949,7 +1956,8 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                     const int j = b * 32 + (int)lane;
                     bulk_g2s(rows + (size_t)sl * rs, sub16 + (int64_t)id * rowb, row_bytes, bar);
                     const int pk = j | (int)((ev0[b] & 1) << 8) | (c << 9) | ((int)partner_self(mode, c) << 11);
-                    const uint64_t st = mb0[b] + ms0[b];
+                    // st: byte address of the membership's first slot
+                    const uint64_t st = reinterpret_cast<uint64_t>(Bd) + 8ull * (mb0[b] + ms0[b]);
                     float4 *dst = reinterpret_cast<float4 *>(rec + sl);
                     dst[0] = make_float4(__double2float_ru(mw0[b]), 0.f,
                                          __int_as_float((int)(uint32_t)st), __int_as_float((int)(uint32_t)(st >> 32)));
@@ -2022,10 +2030,9 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                         const float dd =
                             U8 ? (float)((__float_as_int(R.nrm) + __float_as_int(C.nrm)) - 2 * iacc[s])
                                : (R.nrm + C.nrm) - 2.0f * acc[s];
-                        unsigned long long *Bp = reinterpret_cast<unsigned long long *>(Bd);
                         const unsigned long long pv = (unsigned long long)__float_as_uint(dd) << 32;
-                        if (dd < R.w) __stcs(Bp + mj_slot(R, C), pv | (uint32_t)C.id);  // id[ii] <- id[jj]
-                        if (dd < C.w) __stcs(Bp + mj_slot(C, R), pv | (uint32_t)R.id);  // id[jj] <- id[ii]
+                        if (dd < R.w) __stcs(mj_slot_ptr(R, C), pv | (uint32_t)C.id);  // id[ii] <- id[jj]
+                        if (dd < C.w) __stcs(mj_slot_ptr(C, R), pv | (uint32_t)R.id);  // id[jj] <- id[ii]
                     }
                 }
             }
