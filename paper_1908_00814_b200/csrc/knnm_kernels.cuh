@@ -825,10 +825,13 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
     for (int64_t uu = lo + (int64_t)blockIdx.x * ASM_WARPS + wib; uu < n; uu += nw) {
         const int64_t u = order ? (int64_t)order[uu] : uu;
         int sz = sizes[u];
+        // issued early: they overlap the forward-list pass below
+        const double dlast = dists[u * k + k - 1];
+        const uint32_t ro0 = roff[u], ro1 = roff[u + 1];
         if (!live[u]) {
             // no new entry can reach this hood: no pairs, flags already clear
             if (lane == 0) {
-                worst0[u] = sz == k ? dists[u * k + k - 1] : __longlong_as_double(0x7ff0000000000000LL);
+                worst0[u] = sz == k ? dlast : __longlong_as_double(0x7ff0000000000000LL);
                 nlen[u] = 0;
                 hpairs[u] = 0;
             }
@@ -851,8 +854,8 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
             if (t < k) flags[u * k + t] = f == 2 ? 1 : 0;
         }
         __syncwarp();
-        if (lane == 0) worst0[u] = sz == k ? dists[u * k + k - 1] : __longlong_as_double(0x7ff0000000000000LL);
-        uint32_t lo = roff[u], deg = roff[u + 1] - lo;
+        if (lane == 0) worst0[u] = sz == k ? dlast : __longlong_as_double(0x7ff0000000000000LL);
+        uint32_t lo = ro0, deg = ro1 - lo;
         if (deg <= (uint32_t)rev_cap) {
             for (uint32_t j = lane; j < deg; j += 32) buf[m + j] = rev[lo + j];
             m += deg;
@@ -902,7 +905,10 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
                 lab = (labbits[(v >> 1) >> 5] >> ((v >> 1) & 31)) & 1u;
                 // hood entry: id << 2 | label << 1 | new (the label rides along
                 // so the join needs no dependent labels[] load)
-                nbh[u * W + w + __popc(em & lanemask_lt())] = ((v >> 1) << 2) | ((uint32_t)lab << 1) | (v & 1);
+                const uint32_t ent = ((v >> 1) << 2) | ((uint32_t)lab << 1) | (v & 1);
+                const int at = w + __popc(em & lanemask_lt());
+                nbh[u * W + at] = ent;
+                R[at] = ent;  // staged for the membership pass below (R is free now)
             }
             bool nw_ = end && (v & 1);
             an += __popc(__ballot_sync(FULL_MASK, end && lab == 0 && nw_));
@@ -927,7 +933,7 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
             // first pass of k_hood_memb, fused): admissible partners per member
             const int cnt4[4] = {an, ao, bn, bo};
             for (int j = lane; j < w; j += 32) {
-                const uint32_t e = nbh[u * W + j];
+                const uint32_t e = R[j];
                 const int cls = (mode == 0 ? 0 : (int)((e >> 1) & 1)) * 2 + ((e & 1) ? 0 : 1);
                 const int mk = partner_mask(mode, cls);
                 int part = -(int)partner_self(mode, cls);
