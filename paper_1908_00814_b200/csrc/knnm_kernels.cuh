@@ -2283,12 +2283,14 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
         if (r + 2 * nw < n) seg(r + 2 * nw, lo2, hi2);
         if (m == 0) continue;
         if (m <= 32) {
+            // keys (hood ids < 2^30, or chunk ordinals) fit 32 bits
             uint32_t acc = 0;
+            const uint32_t key = (uint32_t)rec.key;
 #pragma unroll 4
             for (int f = 0; f < m; f++) {
-                const uint64_t kf = __shfl_sync(FULL_MASK, rec.key, f);
+                const uint32_t kf = __shfl_sync(FULL_MASK, key, f);
                 const uint32_t wf = __shfl_sync(FULL_MASK, rec.weight, f);
-                acc += kf < rec.key ? wf : 0u;
+                acc += kf < key ? wf : 0u;
             }
             if ((int)lane < m) start[rec.out] = acc;
             if (total) {
@@ -2302,14 +2304,15 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
             // keys (keys are unique within a row: hood ids / ordinals)
             const MembRec rb = (int)lane + 32 < m ? ldcs_memb(memb + lo + 32 + lane) : MembRec{~0ull, 0, 0};
             uint32_t acc0 = 0, acc1 = 0;
+            const uint32_t key0 = (uint32_t)rec.key, key1 = (uint32_t)rb.key;
 #pragma unroll 4
             for (int f = 0; f < m; f++) {
-                const uint64_t kk = f < 32 ? rec.key : rb.key;
+                const uint32_t kk = f < 32 ? key0 : key1;
                 const uint32_t ww = f < 32 ? rec.weight : rb.weight;
-                const uint64_t kf = __shfl_sync(FULL_MASK, kk, f & 31);
+                const uint32_t kf = __shfl_sync(FULL_MASK, kk, f & 31);
                 const uint32_t wf = __shfl_sync(FULL_MASK, ww, f & 31);
-                acc0 += kf < rec.key ? wf : 0u;
-                acc1 += kf < rb.key ? wf : 0u;
+                acc0 += kf < key0 ? wf : 0u;
+                acc1 += kf < key1 ? wf : 0u;
             }
             start[rec.out] = acc0;
             if ((int)lane + 32 < m) start[rb.out] = acc1;
