@@ -487,7 +487,9 @@ __device__ __forceinline__ int warp_insert1(WarpRow<1, T> &s, int k, int src, T 
     const bool in = (int)lane < s.sz;
     const int id = idf >> 1;
     if (__any_sync(FULL_MASK, in && id == src)) return 0;  // already listed
-    const bool full = s.sz == k;
+    // (sz is the same in every lane; a vote makes that visible to the compiler,
+    // so the tests below are uniform branches)
+    const bool full = __all_sync(FULL_MASK, s.sz == k);
     const unsigned bs = __ballot_sync(FULL_MASK, in && nd < d);
     if (full && !((bs >> (k - 1)) & 1u)) return 0;  // nd >= worst (distance only)
     const unsigned b = bs | __ballot_sync(FULL_MASK, in && nd == d && src < id);
