@@ -661,9 +661,12 @@ int knnm_create(int device, knnm_ctx **out) {
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (auto f : {k_join_chunked<0>, k_join_chunked<1>, k_join_chunked<2>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    for (auto f : {k_join_mma<false, 1>, k_join_mma<false, 2>, k_join_mma<false, 4>,
-                   k_join_mma<true, 1>, k_join_mma<true, 2>, k_join_mma<true, 4>})
+#define KNNM_MJ_ALL(M)                                                                       \
+    k_join_mma<false, 1, M>, k_join_mma<false, 2, M>, k_join_mma<false, 4, M>,              \
+        k_join_mma<true, 1, M>, k_join_mma<true, 2, M>, k_join_mma<true, 4, M>
+    for (auto f : {KNNM_MJ_ALL(0), KNNM_MJ_ALL(1), KNNM_MJ_ALL(2)})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+#undef KNNM_MJ_ALL
     CK(cudaFuncSetAttribute(k_merge_rear, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)mr_smem_bytes(64, 64)));
     for (auto f : {k_bf_topk<0>, k_bf_topk<1>, k_bf_topk<2>})
@@ -1459,28 +1462,27 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                     // 32-entry position blocks per hood
                     const int nb = W <= 32 ? 1 : W <= 64 ? 2 : 4;
                     const void *fn;
-                    if (c->cert_u8) fn = nb == 1 ? (const void *)k_join_mma<true, 1>
-                                       : nb == 2 ? (const void *)k_join_mma<true, 2> : (const void *)k_join_mma<true, 4>;
-                    else fn = nb == 1 ? (const void *)k_join_mma<false, 1>
-                              : nb == 2 ? (const void *)k_join_mma<false, 2> : (const void *)k_join_mma<false, 4>;
+#define KNNM_MJ_FN(U, N) (mode == 0 ? (const void *)k_join_mma<U, N, 0>                     \
+                          : mode == 1 ? (const void *)k_join_mma<U, N, 1> : (const void *)k_join_mma<U, N, 2>)
+                    if (c->cert_u8) fn = nb == 1 ? KNNM_MJ_FN(true, 1) : nb == 2 ? KNNM_MJ_FN(true, 2) : KNNM_MJ_FN(true, 4);
+                    else fn = nb == 1 ? KNNM_MJ_FN(false, 1) : nb == 2 ? KNNM_MJ_FN(false, 2) : KNNM_MJ_FN(false, 4);
+#undef KNNM_MJ_FN
                     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, MJ_WARPS * 32, smem_mma));
                     unsigned grid = (unsigned)std::min<int64_t>((nact + MJ_WARPS - 1) / MJ_WARPS,
                                                                 (int64_t)c->sms * std::max(per_sm, 1));
                     if (grid == 0) grid = 1;
-#define KNNM_MJ_LAUNCH(U, N)                                                                      \
-    k_join_mma<U, N><<<grid, MJ_WARPS * 32, smem_mma, c->st>>>(                                  \
-        act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), \
-        mode, c->sub16p, c->rowb, c->subnormp, c->worst0.as<double>(), boff, stt, Bd, Bs)
-                    if (c->cert_u8) {
-                        if (nb == 1) KNNM_MJ_LAUNCH(true, 1);
-                        else if (nb == 2) KNNM_MJ_LAUNCH(true, 2);
-                        else KNNM_MJ_LAUNCH(true, 4);
-                    } else {
-                        if (nb == 1) KNNM_MJ_LAUNCH(false, 1);
-                        else if (nb == 2) KNNM_MJ_LAUNCH(false, 2);
-                        else KNNM_MJ_LAUNCH(false, 4);
-                    }
-#undef KNNM_MJ_LAUNCH
+                    int nact32 = (int)nact, Wi = W, modei = mode, rowbi = c->rowb;
+                    const uint32_t *nbhp = c->nbh.as<uint32_t>();
+                    const int32_t *nlp = c->nlen.as<int32_t>();
+                    const int8_t *labp = c->labels.as<int8_t>();
+                    const uint8_t *s16 = c->sub16p;
+                    const float *nrmp = c->subnormp;
+                    const double *w0p = c->worst0.as<double>();
+                    void *args[] = {(void *)&act, (void *)&nact32, (void *)&nbhp, (void *)&nlp, (void *)&Wi,
+                                    (void *)&labp, (void *)&modei, (void *)&s16, (void *)&rowbi,
+                                    (void *)&nrmp, (void *)&w0p, (void *)&boff, (void *)&stt,
+                                    (void *)&Bd, (void *)&Bs};
+                    CK(cudaLaunchKernel(fn, dim3(grid), dim3(MJ_WARPS * 32), args, smem_mma, c->st));
                 } else if (tiled) {
                     // non-certified rows: exact values in the join from the
                     // staged rows for short rows; for long rows the exact

@@ -1816,9 +1816,12 @@ __device__ __forceinline__ MjRec lds_rec(const MjRec *p) {
 // when a is its own class's partner and precedes b.
 // Address form of mj_slot: the record's st holds the byte address of its
 // first slot, so a slot is one 32-bit offset from it.
+// (mode 1: no class is its own partner, so there is no self correction)
+template <int MODE>
 __device__ __forceinline__ unsigned long long *mj_slot_ptr(const MjRec &a, const MjRec &b) {
-    const int pa = a.pk & 0xFF, pb = b.pk & 0xFF, ca = (a.pk >> 9) & 3;
-    const uint32_t off = ((b.q4 >> (8 * ca)) & 0xFFu) - (uint32_t)(((a.pk >> 11) & 1) && pa < pb);
+    const int ca = (a.pk >> 9) & 3;
+    uint32_t off = (b.q4 >> (8 * ca)) & 0xFFu;
+    if (MODE != 1) off -= (uint32_t)(((a.pk >> 11) & 1) && (a.pk & 0xFF) < (b.pk & 0xFF));
     return reinterpret_cast<unsigned long long *>(a.st) + off;
 }
 __device__ __forceinline__ uint64_t mj_slot(const MjRec &a, const MjRec &b) {
@@ -1836,13 +1839,17 @@ __device__ __forceinline__ uint64_t mj_slot(const MjRec &a, const MjRec &b) {
 // in flight (TMA) and its Gram block computes, hood i+1's per-member metadata
 // gathers (worst, norm, bucket offset) and hood i+2's neighbour entries are
 // already loading into registers.
-template <bool U8, int NB>
+template <bool U8, int NB, int MODE>
 __global__ void __launch_bounds__(MJ_WARPS * 32, 4)
 k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
-           const int32_t *__restrict__ nlen, int W, const int8_t *__restrict__ labels, int mode,
+           const int32_t *__restrict__ nlen, int W, const int8_t *__restrict__ labels, int mode_rt,
            const uint8_t *__restrict__ sub16, int rowb, const float *__restrict__ norms,
            const double *__restrict__ worst0, const uint64_t *__restrict__ boff,
            const uint32_t *__restrict__ start, double *__restrict__ Bd, int32_t *__restrict__ Bs) {
+    // the pair mode is a template parameter (mode_rt == MODE): partner masks,
+    // block shapes and the slot correction fold into constants
+    constexpr int mode = MODE;
+    (void)mode_rt;
     extern __shared__ __align__(128) char mj_smem[];
     const unsigned lane = lane_id();
     const int warp = threadIdx.x >> 5;
@@ -2037,8 +2044,8 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                             U8 ? (float)((__float_as_int(R.nrm) + __float_as_int(C.nrm)) - 2 * iacc[s])
                                : (R.nrm + C.nrm) - 2.0f * acc[s];
                         const unsigned long long pv = (unsigned long long)__float_as_uint(dd) << 32;
-                        if (dd < R.w) __stcs(mj_slot_ptr(R, C), pv | (uint32_t)C.id);  // id[ii] <- id[jj]
-                        if (dd < C.w) __stcs(mj_slot_ptr(C, R), pv | (uint32_t)R.id);  // id[jj] <- id[ii]
+                        if (dd < R.w) __stcs(mj_slot_ptr<MODE>(R, C), pv | (uint32_t)C.id);  // id[ii] <- id[jj]
+                        if (dd < C.w) __stcs(mj_slot_ptr<MODE>(C, R), pv | (uint32_t)R.id);  // id[jj] <- id[ii]
                     }
                 }
             }
