@@ -1354,15 +1354,20 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                                                                  c->mpack.as<unsigned long long>());
             CKL();
         }
-        k_assemble<<<grid_for(c, (hi - lo) * 32, ASM_WARPS * 32, 16), ASM_WARPS * 32, 0, c->st>>>(
-            c->ids.as<int32_t>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
-            c->dists.as<double>(), hi, k, rev_cap, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(),
-            round_seed, c->labbits.as<uint32_t>(), mode, W, c->nbh.as<uint32_t>(),
-            c->nlen.as<int32_t>(), c->hpairs.as<uint32_t>(), c->worst0.as<double>(),
-            c->active.as<int32_t>(), cnt, lo, c->bound.as<uint32_t>(), c->mcount.as<uint32_t>(),
-            (!local_only && c->have_order) ? c->order.as<int32_t>() : nullptr,
-            fused_memb ? c->memb.as<MembRec>() : nullptr,
-            fused_memb ? c->mpack.as<unsigned long long>() : nullptr, c->live.as<uint8_t>());
+#define KNNM_ASM_LAUNCH(M)                                                                          \
+        k_assemble<M><<<grid_for(c, (hi - lo) * 32, ASM_WARPS * 32, 16), ASM_WARPS * 32, 0, c->st>>>(  \
+            c->ids.as<int32_t>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),                   \
+            c->dists.as<double>(), hi, k, rev_cap, c->roff.as<uint32_t>(), c->rev.as<uint32_t>(),   \
+            round_seed, c->labbits.as<uint32_t>(), mode, W, c->nbh.as<uint32_t>(),                  \
+            c->nlen.as<int32_t>(), c->hpairs.as<uint32_t>(), c->worst0.as<double>(),                \
+            c->active.as<int32_t>(), cnt, lo, c->bound.as<uint32_t>(), c->mcount.as<uint32_t>(),    \
+            (!local_only && c->have_order) ? c->order.as<int32_t>() : nullptr,                      \
+            fused_memb ? c->memb.as<MembRec>() : nullptr,                                           \
+            fused_memb ? c->mpack.as<unsigned long long>() : nullptr, c->live.as<uint8_t>())
+        if (mode == 0) KNNM_ASM_LAUNCH(0);
+        else if (mode == 1) KNNM_ASM_LAUNCH(1);
+        else KNNM_ASM_LAUNCH(2);
+#undef KNNM_ASM_LAUNCH
         CKL();
         TRY(scan<uint32_t, uint64_t>(c, c->hpairs.as<uint32_t>(), c->poff.as<uint64_t>(), n));
     }

@@ -806,14 +806,17 @@ __device__ __forceinline__ uint32_t members_closed_form(int mode, int an, int ao
     return m + ((a >= 1 || b >= 2) ? bn : 0) + ((an >= 1 || bn >= 1) ? bo : 0);
 }
 
+template <int MODE>
 __global__ void __launch_bounds__(ASM_WARPS * 32, 6)
 k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__restrict__ sizes,
            const double *__restrict__ dists, int64_t n, int k, int rev_cap,
            const uint32_t *__restrict__ roff, const uint32_t *__restrict__ rev, uint64_t seed,
-           const uint32_t *__restrict__ labbits, int mode, int W, uint32_t *nbh, int32_t *nlen,
+           const uint32_t *__restrict__ labbits, int mode_rt, int W, uint32_t *nbh, int32_t *nlen,
            uint32_t *hpairs, double *worst0, int32_t *active, unsigned long long *counters,
            int64_t lo, uint32_t *bound, uint32_t *mcount, const int32_t *__restrict__ order,
            MembRec *memb, unsigned long long *mpack, const uint8_t *__restrict__ live) {
+    constexpr int mode = MODE;  // (mode_rt == MODE)
+    (void)mode_rt;
     __shared__ uint32_t s_seg[ASM_WARPS][WARP_REV_MAX];
     __shared__ uint32_t s_idx[ASM_WARPS][WARP_REV_MAX];
     __shared__ uint32_t s_R[ASM_WARPS][MAX_W];
