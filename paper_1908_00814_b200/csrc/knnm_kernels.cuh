@@ -487,7 +487,8 @@ k_insert_rows_direct(const int32_t *__restrict__ rows, int64_t mrows, int count,
             for (int j = 0; j < cnt; j++) {
                 const int sj = __shfl_sync(FULL_MASK, src, j);
                 const double dj = __shfl_sync(FULL_MASK, dd, j);
-                a += warp_insert<E, true, double>(s, k, sj, dj, lane);
+                if constexpr (E == 1) a += warp_insert1<double>(s, k, sj, dj, lane);
+                else a += warp_insert<E, true, double>(s, k, sj, dj, lane);
             }
         }
         if (a) row_store<E, double>(s, ids, dists, flags, sizes, r, k, lane);
