@@ -1837,7 +1837,10 @@ __device__ __forceinline__ uint64_t mj_slot(const MjRec &a, const MjRec &b) {
 // mma.m16n8k32 u8 x u8 -> s32, exact integer arithmetic; norms are integers.
 // U8 = false: fp16 rows, m16n8k16 fp16 -> fp32 (exact under the dot-form
 // certificate).  `rowb` = staged bytes per row (multiple of 32).  NB = 32-entry
-// blocks of a hood (W <= 32 * NB).
+// blocks of a hood (W <= 32 * NB).  MODE = the pair mode (0 all, 1 cross,
+// 2 cross-or-S2), a template parameter so partner masks and block shapes
+// are constants.  Distances are compared and packed in fp32 against each
+// member's round-start worst rounded up to fp32 (exact for fp32 values).
 //
 // One warp per hood, software-pipelined three deep: while hood i's rows are
 // in flight (TMA) and its Gram block computes, hood i+1's per-member metadata
