@@ -1828,10 +1828,6 @@ __device__ __forceinline__ unsigned long long *mj_slot_ptr(const MjRec &a, const
     if (MODE != 1) off -= (uint32_t)(((a.pk >> 11) & 1) && (a.pk & 0xFF) < (b.pk & 0xFF));
     return reinterpret_cast<unsigned long long *>(a.st) + off;
 }
-__device__ __forceinline__ uint64_t mj_slot(const MjRec &a, const MjRec &b) {
-    const int pa = a.pk & 0xFF, pb = b.pk & 0xFF, ca = (a.pk >> 9) & 3;
-    return a.st + ((b.q4 >> (8 * ca)) & 0xFFu) - (uint32_t)(((a.pk >> 11) & 1) && pa < pb);
-}
 
 // U8 = true: rows are u8 (integer data in [0, 255]); the Gram block uses
 // mma.m16n8k32 u8 x u8 -> s32, exact integer arithmetic; norms are integers.
