@@ -1817,10 +1817,9 @@ __device__ __forceinline__ MjRec lds_rec(const MjRec *p) {
 // Slot of the update "member a receives partner b" (reference order, see
 // pair_rank): membership start + rank of b's position among a's partners,
 // i.e. byte class(a) of b's q4 (the position prefix count), minus a itself
-// when a is its own class's partner and precedes b.
-// Address form of mj_slot: the record's st holds the byte address of its
-// first slot, so a slot is one 32-bit offset from it.
-// (mode 1: no class is its own partner, so there is no self correction)
+// when a is its own class's partner and precedes b.  The record's st holds
+// the byte address of its first slot, so a slot is one 32-bit offset from
+// it.  (Mode 1: no class is its own partner, so there is no self correction.)
 template <int MODE>
 __device__ __forceinline__ unsigned long long *mj_slot_ptr(const MjRec &a, const MjRec &b) {
     const int ca = (a.pk >> 9) & 3;
