@@ -143,7 +143,7 @@ struct knnm_ctx {
     bool have_tail = false;
     int64_t shard_lo = 0, shard_hi = -1;  // owned rows (sharded rounds); -1 = n
     // round scratch
-    DBuf indeg, roff, rev, heavy, giant, gscratch32, nbh, nlen, hpairs, poff, worst0, active;
+    DBuf indeg, roff, rev, heavy, giant, gscratch32, nbh, nlen, hpairs, poff, worst0, active, rowmeta;
     DBuf wcnt, woff, cBd, cBs;  // written-slot compaction (sharded exchange)
     DBuf bound, boff, mcount, moff, mcur, memb, start, Bd, Bs;
     DBuf order, lab0, lab1;       // locality order of hoods (per merge)
@@ -688,7 +688,7 @@ int knnm_destroy(knnm_ctx *c) {
     DBuf *all[] = {&c->vec, &c->sub, &c->ugid, &c->labels, &c->labbits, &c->ids, &c->dists, &c->flags,
                    &c->sizes, &c->tail_ids, &c->tail_d, &c->tail_s, &c->indeg, &c->roff,
                    &c->rev, &c->heavy, &c->giant, &c->gscratch32, &c->nbh, &c->nlen, &c->hpairs,
-                   &c->poff, &c->worst0, &c->active, &c->wcnt, &c->woff, &c->cBd, &c->cBs, &c->order, &c->lab0, &c->lab1, &c->bound, &c->boff, &c->mcount, &c->moff, &c->mcur, &c->memb, &c->start, &c->Bd, &c->Bs,
+                   &c->poff, &c->worst0, &c->active, &c->rowmeta, &c->wcnt, &c->woff, &c->cBd, &c->cBs, &c->order, &c->lab0, &c->lab1, &c->bound, &c->boff, &c->mcount, &c->moff, &c->mcur, &c->memb, &c->start, &c->Bd, &c->Bs,
                    &c->counters, &c->draws, &c->draw_rows,
                    &c->draw_bad, &c->pool, &c->scan_pos, &c->vec16, &c->norms, &c->sub16, &c->subnorms, &c->out_ids, &c->out_d,
                    &c->out_s, &c->phi_leaf_lo, &c->phi_leaf_len, &c->phi_left, &c->phi_right,
@@ -1481,12 +1481,15 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
                     const int32_t *nlp = c->nlen.as<int32_t>();
                     const int8_t *labp = c->labels.as<int8_t>();
                     const uint8_t *s16 = c->sub16p;
-                    const float *nrmp = c->subnormp;
-                    const double *w0p = c->worst0.as<double>();
+                    // per-row worst / norm / bucket base in one 16-byte record
+                    TRY(ensure(c->rowmeta, sizeof(RowMeta) * (size_t)n));
+                    k_rowmeta<<<grid_for(c, n, 256), 256, 0, c->st>>>(n, c->worst0.as<double>(), c->subnormp,
+                                                                     boff, c->rowmeta.as<RowMeta>());
+                    CKL();
+                    const RowMeta *rmp = c->rowmeta.as<RowMeta>();
                     void *args[] = {(void *)&act, (void *)&nact32, (void *)&nbhp, (void *)&nlp, (void *)&Wi,
                                     (void *)&labp, (void *)&modei, (void *)&s16, (void *)&rowbi,
-                                    (void *)&nrmp, (void *)&w0p, (void *)&boff, (void *)&stt,
-                                    (void *)&Bd, (void *)&Bs};
+                                    (void *)&rmp, (void *)&stt, (void *)&Bd, (void *)&Bs};
                     CK(cudaLaunchKernel(fn, dim3(grid), dim3(MJ_WARPS * 32), args, smem_mma, c->st));
                 } else if (tiled) {
                     // non-certified rows: exact values in the join from the

@@ -1776,6 +1776,23 @@ __device__ __forceinline__ void mma16816(float (&c)[4], uint32_t a0, uint32_t a1
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
+// Per-row join metadata, gathered with one 16-byte load per member: the
+// round-start worst rounded up to fp32 (for an fp32 distance d:
+// d < wru <=> d < worst), the row norm (int bits on the u8 route) and the
+// row's first bucket slot.
+struct __align__(16) RowMeta {
+    float wru;
+    float nrm;
+    uint64_t boff;
+};
+
+__global__ void k_rowmeta(int64_t n, const double *__restrict__ worst0, const float *__restrict__ norms,
+                          const uint64_t *__restrict__ boff, RowMeta *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = RowMeta{__double2float_ru(worst0[i]), norms[i], boff[i]};
+}
+
 // One member of a staged hood (32 bytes: two 128-bit shared loads).
 struct __align__(16) MjRec {
     float w;      // round-start worst of the member's row, rounded up to fp32
@@ -1845,8 +1862,7 @@ template <bool U8, int NB, int MODE>
 __global__ void __launch_bounds__(MJ_WARPS * 32, 4)
 k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
            const int32_t *__restrict__ nlen, int W, const int8_t *__restrict__ labels, int mode_rt,
-           const uint8_t *__restrict__ sub16, int rowb, const float *__restrict__ norms,
-           const double *__restrict__ worst0, const uint64_t *__restrict__ boff,
+           const uint8_t *__restrict__ sub16, int rowb, const RowMeta *__restrict__ rmeta,
            const uint32_t *__restrict__ start, double *__restrict__ Bd, int32_t *__restrict__ Bs) {
     // the pair mode is a template parameter (mode_rt == MODE): partner masks,
     // block shapes and the slot correction fold into constants
@@ -1884,19 +1900,20 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
     // per-member metadata of hood u (independent gathers, issued together)
     // (results are consumed one hood later: no arithmetic on them here, or
     // the warp would wait for the loads right away)
-    auto gather = [&](int64_t u, int w, const uint32_t (&ev)[NB], double (&mw)[NB], float (&mn)[NB],
+    auto gather = [&](int64_t u, int w, const uint32_t (&ev)[NB], float (&mw)[NB], float (&mn)[NB],
                       uint64_t (&mb)[NB], uint32_t (&ms)[NB]) {
 #pragma unroll
         for (int b = 0; b < NB; b++) {
             const int j = b * 32 + (int)lane;
             if (j < w) {
                 const int id = (int)(ev[b] >> 2);
-                mw[b] = __ldg(worst0 + id);
-                mn[b] = __ldg(norms + id);
-                mb[b] = __ldg(boff + id);
+                const uint4 rm = __ldg(reinterpret_cast<const uint4 *>(rmeta + id));
+                mw[b] = __uint_as_float(rm.x);
+                mn[b] = __uint_as_float(rm.y);
+                mb[b] = ((uint64_t)rm.w << 32) | rm.z;
                 ms[b] = __ldg(start + u * W + j);
             } else {
-                mw[b] = 0.0;
+                mw[b] = 0.f;
                 mn[b] = 0.f;
                 mb[b] = 0;
                 ms[b] = 0;
@@ -1914,7 +1931,7 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
     uint32_t ev1[NB];
     load_ev(hi + stride < nactive, u1, ev1);
     int64_t u2 = hi + 2 * stride < nactive ? __ldg(active + hi + 2 * stride) : 0;
-    double mw0[NB];
+    float mw0[NB];
     float mn0[NB];
     uint64_t mb0[NB];
     uint32_t ms0[NB];
@@ -1974,7 +1991,7 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                     // st: byte address of the membership's first slot
                     const uint64_t st = reinterpret_cast<uint64_t>(Bd) + 8ull * (mb0[b] + ms0[b]);
                     float4 *dst = reinterpret_cast<float4 *>(rec + sl);
-                    dst[0] = make_float4(__double2float_ru(mw0[b]), 0.f,
+                    dst[0] = make_float4(mw0[b], 0.f,
                                          __int_as_float((int)(uint32_t)st), __int_as_float((int)(uint32_t)(st >> 32)));
                     dst[1] = make_float4(__int_as_float(id), mn0[b], __int_as_float(pk),
                                          __int_as_float((int)q4));
@@ -1982,7 +1999,7 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
             }
         }
         // ---- prefetch: hood i+1 metadata, hood i+2 entries, hood i+3 id --------
-        double mw1[NB];
+        float mw1[NB];
         float mn1[NB];
         uint64_t mb1[NB];
         uint32_t ms1[NB];
