@@ -1410,7 +1410,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
         size_t smem = sizeof(float) * (size_t)W * c->dp;
         size_t smem_tiled = sizeof(float) * (size_t)W * (c->dp + 4);
         if (smem > 200 * 1024) return fail(KNNM_ERR_LIMIT, "neighbourhood of %d x %d floats exceeds shared memory", W, c->dp);
-        const int Wp = W + 16;
+        const int Wp = mj_rows(W, mode);
         const size_t mj_per_warp = mj_meta_bytes(Wp) + (size_t)Wp * (c->rowb + 16);
         const size_t smem_mma = MJ_WARPS * mj_per_warp;
         c->stats.join_row_bytes = c->cert_dot ? c->rowb : 4 * c->dp;

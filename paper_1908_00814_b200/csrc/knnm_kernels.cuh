@@ -1805,6 +1805,13 @@ struct __align__(16) MjRec {
     uint32_t q4;  // byte c: partners of a class-c member at positions < this one
 };
 
+// Staged rows per warp: a hood (<= W) plus the tile tails past it.  Row
+// tiles start at 0 except mode 2's second block (start nA: tails up to 15
+// rows); column tiles of 8 start anywhere (tails up to 7 rows).
+__host__ __device__ constexpr int mj_rows(int W, int mode) {
+    return mode == 2 ? W + 16 : (((W + 15) & ~15) > W + 8 ? ((W + 15) & ~15) : W + 8);
+}
+
 __host__ __device__ constexpr size_t mj_meta_bytes(int Wp) {
     return (16 + (size_t)Wp * sizeof(MjRec) + 127) & ~(size_t)127;
 }
@@ -1871,7 +1878,7 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
     extern __shared__ __align__(128) char mj_smem[];
     const unsigned lane = lane_id();
     const int warp = threadIdx.x >> 5;
-    const int Wp = W + 16;
+    const int Wp = mj_rows(W, MODE);
     const int rs = rowb + 16;  // padded row stride: conflict-free ldmatrix
     const size_t per_warp = mj_meta_bytes(Wp) + (size_t)Wp * rs;
     char *base = mj_smem + (size_t)warp * per_warp;
