@@ -2279,7 +2279,7 @@ __global__ void __launch_bounds__(SEG_WARPS * 32)
 k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restrict__ memb,
            uint32_t *__restrict__ start, const unsigned long long *__restrict__ mpack,
            int32_t *heavy, unsigned long long *counters, uint32_t *__restrict__ total) {
-    __shared__ uint64_t s_key[SEG_WARPS][SEG_SMEM];
+    __shared__ uint32_t s_out[SEG_WARPS][SEG_SMEM];  // output positions of the sorted path
     __shared__ uint32_t s_wt[SEG_WARPS][SEG_SMEM];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * SEG_WARPS;
@@ -2362,8 +2362,8 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
         // 64 < m <= SEG_SMEM: register bitonic sort of (key << 32 | index),
         // then the weights scanned in that order
         const uint32_t t = m <= 128
-            ? seg_rank_sorted<4>(lo, m, memb, start, s_wt[wib], reinterpret_cast<uint32_t *>(s_key[wib]), lane)
-            : seg_rank_sorted<8>(lo, m, memb, start, s_wt[wib], reinterpret_cast<uint32_t *>(s_key[wib]), lane);
+            ? seg_rank_sorted<4>(lo, m, memb, start, s_wt[wib], s_out[wib], lane)
+            : seg_rank_sorted<8>(lo, m, memb, start, s_wt[wib], s_out[wib], lane);
         if (total && lane == 0) total[r] = t;
         __syncwarp();
     }
