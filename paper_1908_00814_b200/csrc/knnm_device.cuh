@@ -534,7 +534,13 @@ __device__ __forceinline__ int warp_apply_chunk(WarpRow<E, T> &s, int k, int src
         m &= m - 1;
         const int src = __shfl_sync(FULL_MASK, src_l, i);
         const T nd = __shfl_sync(FULL_MASK, d_l, i);
-        if (s.sz < k || nd < s.worst) acc += warp_insert<E, false, T>(s, k, src, nd, lane);
+        if (!(s.sz < k || nd < s.worst)) continue;
+        // a listed id (the common rejection in later rounds) costs one vote
+        bool dup = false;
+#pragma unroll
+        for (int e = 0; e < E; e++) dup |= e * 32 + (int)lane < s.sz && (s.idf[e] >> 1) == src;
+        if (__any_sync(FULL_MASK, dup)) continue;
+        acc += warp_insert<E, false, T>(s, k, src, nd, lane);
     }
     return acc;
 }
