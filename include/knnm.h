@@ -95,6 +95,10 @@ int knnm_destroy(knnm_ctx *ctx);
  * copy is kept across merges (tree merges and H-Merge reuse it). */
 int knnm_set_dataset(knnm_ctx *ctx, const float *vectors, int64_t n_all,
                      int32_t d, int32_t metric);
+/* Host-only content fingerprint of a buffer (threads, no GPU): the Python
+ * engine keys its device-resident dataset on it, so an in-place edit of
+ * Dataset.vectors is never served from a stale device copy. */
+int knnm_fingerprint(const void *p, int64_t bytes, uint64_t *out);
 
 /* Begin a merge or build over `n` local rows.  Replaces
  * `Dataset.take(union_gids)` (core.py:148-166; merge.py:217-219, 297-301),
@@ -148,6 +152,11 @@ int knnm_draws_replace(knnm_ctx *ctx, const int64_t *rows, int64_t nrows,
                        const int64_t *vals, int64_t *bad, int64_t *nbad);
 int knnm_draws_insert(knnm_ctx *ctx, const int32_t *rows, const int32_t *pool,
                       int64_t npool, int64_t *accepted);
+/* knnm_draws_insert restricted to draw rows [r0, r1) (a sharded merge's
+ * owned rows); the draw matrix is still generated for every row, so the
+ * PCG64 stream advances exactly as the reference's. */
+int knnm_draws_insert_range(knnm_ctx *ctx, const int32_t *rows, const int32_t *pool,
+                            int64_t npool, int64_t r0, int64_t r1, int64_t *accepted);
 
 /* Device-side draws for knnm_draws_*: a bit-exact restatement of numpy's
  * PCG64 + Generator.integers(0, m, size=(nrows, t)) (pcg64.h,
@@ -210,8 +219,18 @@ int knnm_round(knnm_ctx *ctx, int32_t mode, int32_t rev_cap,
  * round's slots are packed (one u64 per slot in Bd: fp32 distance bits in
  * the high word, source row in the low word; recv_Bs is then ignored). */
 int knnm_set_shard(knnm_ctx *ctx, int64_t lo, int64_t hi);
+/* knnm_round_local runs the reverse step and the hoods; the local join then
+ * runs per hood chunk: knnm_local_chunks gives this rank's chunk count (1
+ * when the round's 2P slots fit the candidate budget, 0 without pairs), and
+ * knnm_local_join(c) fills the slots of chunk c (an empty slot view for
+ * c >= count, so every rank can run the busiest rank's number of chunks).
+ * Chunks are consecutive ascending hood ranges, so applying the received
+ * blocks in (source rank, chunk) order is still the reference's per-row
+ * order (construct.py:147-164 chunks the same way). */
 int knnm_round_local(knnm_ctx *ctx, int32_t mode, int32_t rev_cap,
                      uint64_t round_seed, int64_t *pairs_local);
+int knnm_local_chunks(knnm_ctx *ctx, int32_t *nchunks);
+int knnm_local_join(knnm_ctx *ctx, int32_t chunk);
 int knnm_local_views(knnm_ctx *ctx, void **cnt, void **boff, void **Bd, void **Bs);
 /* Same views over the WRITTEN slots only: slots the join left unwritten can
  * never be accepted, so the exchange drops them.  Per target row the written
@@ -225,6 +244,28 @@ int knnm_round_apply(knnm_ctx *ctx, int32_t nsrc, const uint32_t *recv_cnt,
                      const uint64_t *recv_base, const double *recv_Bd,
                      const int32_t *recv_Bs, int64_t *accepted);
 int knnm_state_views(knnm_ctx *ctx, void **ids, void **dists, void **flags, void **sizes);
+/* Replication of owned rows without re-sending unchanged ones: after
+ * knnm_round_apply, knnm_pack_rows packs the owned rows the round changed
+ * (flags cleared by the assembly or an accepted insert; all owned rows when
+ * all != 0, e.g. after a sharded initialisation) into row records
+ * (f64 dists[k] | i32 ids[k] | i32 row | i32 size | u8 flags[k], padded to
+ * *rec_bytes, a multiple of 8) in a context-owned device buffer, valid until
+ * the next call; knnm_unpack_rows writes received records into the lists. */
+int knnm_pack_rows(knnm_ctx *ctx, int32_t all, void **buf, int64_t *count, int32_t *rec_bytes);
+int knnm_unpack_rows(knnm_ctx *ctx, const void *buf, int64_t count);
+
+/* Candidate-slot budget in bytes (default 40 GiB; 0 restores it).  Rounds
+ * whose 2P slots exceed it run in ascending hood chunks; a small budget
+ * forces the chunked path (tests). */
+int knnm_set_cand_budget(knnm_ctx *ctx, int64_t bytes);
+
+/* Stream ordering with caller-owned CUDA streams (e.g. torch's current
+ * stream), without a host sync: knnm_wait_stream makes the context's stream
+ * wait for the work queued so far on `stream` (call before passing tensors
+ * another stream produced); knnm_signal_stream makes `stream` wait for the
+ * context's queued work (call before another stream reads context memory). */
+int knnm_wait_stream(knnm_ctx *ctx, void *stream);
+int knnm_signal_stream(knnm_ctx *ctx, void *stream);
 
 /* Exact brute-force top-k (construct.py:273-348; _kernels.py:445-506):
  * for each query -- queries[nq, d] (host) or dataset rows rows[nq] -- the k

@@ -70,6 +70,7 @@ SIGNATURES = {
     "knnm_create": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(P)]),
     "knnm_destroy": (ctypes.c_int, [P]),
     "knnm_set_dataset": (ctypes.c_int, [P, P, I64, I32, I32]),
+    "knnm_fingerprint": (ctypes.c_int, [P, I64, ctypes.POINTER(U64)]),
     "knnm_begin": (ctypes.c_int, [P, P, I64, P, I32]),
     "knnm_load_graph": (ctypes.c_int, [P, P, I64, P, P, P, I32, I32]),
     "knnm_load_graph_dev": (ctypes.c_int, [P, P, I64, P, P, P, I32, I32]),
@@ -78,6 +79,7 @@ SIGNATURES = {
     "knnm_draws_load": (ctypes.c_int, [P, P, I64, I32, P, PI64]),
     "knnm_draws_replace": (ctypes.c_int, [P, P, I64, P, P, PI64]),
     "knnm_draws_insert": (ctypes.c_int, [P, P, P, I64, PI64]),
+    "knnm_draws_insert_range": (ctypes.c_int, [P, P, P, I64, I64, I64, PI64]),
     "knnm_draws_gen": (ctypes.c_int, [P, P, I32, ctypes.c_uint32, U64, I64, I32, PI64, P, PI64]),
     "knnm_draws_regen": (ctypes.c_int, [P, P, I32, ctypes.c_uint32, U64, P, I64, PI64, P, PI64]),
     "knnm_merge_members": (ctypes.c_int, [P, I64, P, I64, P, P, P, ctypes.POINTER(I64),
@@ -87,10 +89,18 @@ SIGNATURES = {
     "knnm_round": (ctypes.c_int, [P, I32, I32, U64, PI64, PI64]),
     "knnm_set_shard": (ctypes.c_int, [P, I64, I64]),
     "knnm_round_local": (ctypes.c_int, [P, I32, I32, U64, PI64]),
+    "knnm_local_chunks": (ctypes.c_int, [P, ctypes.POINTER(I32)]),
+    "knnm_local_join": (ctypes.c_int, [P, I32]),
+    "knnm_set_cand_budget": (ctypes.c_int, [P, I64]),
+    "knnm_wait_stream": (ctypes.c_int, [P, P]),
+    "knnm_signal_stream": (ctypes.c_int, [P, P]),
     "knnm_local_views": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]),
     "knnm_local_compact": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P),
                                           ctypes.POINTER(ctypes.c_int64)]),
     "knnm_round_apply": (ctypes.c_int, [P, I32, P, P, P, P, PI64]),
+    "knnm_pack_rows": (ctypes.c_int, [P, I32, ctypes.POINTER(P), ctypes.POINTER(ctypes.c_int64),
+                                      ctypes.POINTER(I32)]),
+    "knnm_unpack_rows": (ctypes.c_int, [P, P, I64]),
     "knnm_state_views": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]),
     "knnm_bf_topk": (ctypes.c_int, [P, P, P, I64, I32, I32, P, P]),
     "knnm_phi": (ctypes.c_int, [P, PDBL]),

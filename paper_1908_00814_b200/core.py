@@ -158,7 +158,7 @@ def generate_uniform(n: int, d: int, seed: int) -> Dataset:
     if n < 1 or d < 1:
         raise ValueError("n and d must be >= 1")
     rng = np.random.default_rng(seed)
-    return Dataset.from_dense(rng.random((n, d), dtype=np.float32), validate=False)
+    return _owned(rng.random((n, d), dtype=np.float32))
 
 
 def sample_distinct(rng, n: int, k: int, exclude: int = -1) -> np.ndarray:
@@ -206,6 +206,13 @@ def sample_distinct_rows(rng, n: int, k: int, exclude: np.ndarray) -> np.ndarray
 # ---------------------------------------------------------------------------
 
 
+def _owned(x: np.ndarray) -> Dataset:
+    """A Dataset over an array only it holds, made read-only: the engine
+    then trusts its device copy by identity (no fingerprint per merge)."""
+    x.flags.writeable = False
+    return Dataset.from_dense(x, validate=False)
+
+
 def _chunked_gmm(rng, n, d, centres, sigma, chunk=1 << 16):
     out = np.empty((n, d), dtype=np.float32)
     labels = rng.integers(0, centres.shape[0], size=n)
@@ -225,7 +232,7 @@ def generate_int_gmm(n: int, d: int = 128, n_centres: int = 1000, sigma: float =
     x = _chunked_gmm(rng, n, d, centres, sigma)
     np.clip(x, 0.0, 255.0, out=x)
     np.rint(x, out=x)
-    return Dataset.from_dense(x, validate=False)
+    return _owned(x)
 
 
 def generate_unit_gmm(n: int, d: int = 960, n_centres: int = 500, sigma: float = 0.05,
@@ -235,7 +242,7 @@ def generate_unit_gmm(n: int, d: int = 960, n_centres: int = 500, sigma: float =
     centres = rng.uniform(0.0, 1.0, size=(n_centres, d)).astype(np.float32)
     x = _chunked_gmm(rng, n, d, centres, sigma)
     np.clip(x, 0.0, 1.0, out=x)
-    return Dataset.from_dense(x, validate=False)
+    return _owned(x)
 
 
 def generate_sphere_gmm(n: int, d: int = 100, n_centres: int = 2000, sigma: float = 0.3,
@@ -246,4 +253,4 @@ def generate_sphere_gmm(n: int, d: int = 100, n_centres: int = 2000, sigma: floa
     centres = rng.standard_normal((n_centres, d)).astype(np.float32)
     x = _chunked_gmm(rng, n, d, centres, sigma)
     x /= np.linalg.norm(x, axis=1, keepdims=True).astype(np.float32)
-    return Dataset.from_dense(x, validate=False)
+    return _owned(x)

@@ -145,6 +145,7 @@ struct knnm_ctx {
     // round scratch
     DBuf indeg, roff, rev, heavy, giant, gscratch32, nbh, nlen, hpairs, poff, worst0, active, rowmeta;
     DBuf wcnt, woff, cBd, cBs;  // written-slot compaction (sharded exchange)
+    DBuf dirty, rsel, rsoff, rpack;  // owned rows changed by a sharded round, their records
     DBuf bound, boff, mcount, moff, mcur, memb, start, Bd, Bs;
     DBuf order, lab0, lab1;       // locality order of hoods (per merge)
     bool have_order = false;
@@ -156,7 +157,13 @@ struct knnm_ctx {
     DBuf scan_tmp[4], scan_off[4];
     DBuf counters;
     unsigned long long cap = 0;  // candidate record capacity
-    size_t cand_budget_bytes = (size_t)40 << 30;
+    size_t cand_budget_bytes = (size_t)40 << 30;  // knnm_set_cand_budget
+    // sharded round in progress: its hood chunks (knnm_local_join)
+    int lc_mode = 0, lc_W = 0;
+    bool lc_single = true;  // one chunk = the round's active hoods
+    int64_t lc_nact = 0;
+    std::vector<std::vector<int32_t>> lc_lists;
+    std::vector<uint64_t> lc_pairs2;
     // staging
     DBuf stage[4];
     unsigned long long *hcnt = nullptr;  // pinned mirror of counters
@@ -176,6 +183,7 @@ struct knnm_ctx {
     double phase_ms[PH_NUM] = {0, 0, 0, 0, 0, 0};
     knnm_stats stats{};
     cudaEvent_t marks[8] = {};
+    cudaEvent_t ev_wait = nullptr, ev_sig = nullptr;  // knnm_wait_stream / knnm_signal_stream
 };
 
 namespace {
@@ -706,6 +714,8 @@ int knnm_destroy(knnm_ctx *c) {
         cudaEventDestroy(p.second.second);
     }
     for (auto e : c->ev_pool) cudaEventDestroy(e);
+    if (c->ev_wait) cudaEventDestroy(c->ev_wait);
+    if (c->ev_sig) cudaEventDestroy(c->ev_sig);
     for (auto e : c->marks)
         if (e) cudaEventDestroy(e);
     if (c->hcnt) cudaFreeHost(c->hcnt);
@@ -1240,14 +1250,15 @@ int knnm_draws_replace(knnm_ctx *c, const int64_t *rows, int64_t nrows, const in
     return dup_check(c, c->draw_rows.as<int64_t>(), nrows, bad, nbad);
 }
 
-int knnm_draws_insert(knnm_ctx *c, const int32_t *rows, const int32_t *pool, int64_t npool,
-                      int64_t *accepted) {
+int knnm_draws_insert_range(knnm_ctx *c, const int32_t *rows, const int32_t *pool, int64_t npool,
+                            int64_t r0, int64_t r1, int64_t *accepted) {
     if (c) c->state_gen++;  // the lists may change: cached phi is stale
     phi_wait(c);
     if (!c || !rows || !pool) return fail(KNNM_ERR_ARG, "bad argument");
     if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    if (r0 < 0 || r1 < r0 || r1 > c->draw_n) return fail(KNNM_ERR_ARG, "bad draw rows [%lld, %lld)", (long long)r0, (long long)r1);
     CK(cudaSetDevice(c->device));
-    int64_t m = c->draw_n * c->draw_t;
+    const int64_t m = (r1 - r0) * c->draw_t;
     if (m == 0) {
         if (accepted) *accepted = 0;
         return KNNM_OK;
@@ -1255,10 +1266,251 @@ int knnm_draws_insert(knnm_ctx *c, const int32_t *rows, const int32_t *pool, int
     TRY(ensure(c->pool, sizeof(int32_t) * npool));
     TRY(h2d(c, c->pool.p, pool, sizeof(int32_t) * npool));
     TRY(ensure(c->stage[1], sizeof(int32_t) * m));
-    k_pool_map<<<grid_for(c, m, 256), 256, 0, c->st>>>(c->draws.as<int64_t>(), m, c->pool.as<int32_t>(),
-                                                         c->stage[1].as<int32_t>());
+    k_pool_map<<<grid_for(c, m, 256), 256, 0, c->st>>>(c->draws.as<int64_t>() + r0 * c->draw_t, m,
+                                                         c->pool.as<int32_t>(), c->stage[1].as<int32_t>());
     CKL();
-    return insert_impl(c, rows, c->draw_n, c->draw_t, nullptr, m, accepted, true);
+    return insert_impl(c, rows + r0, r1 - r0, c->draw_t, nullptr, m, accepted, true);
+}
+
+int knnm_draws_insert(knnm_ctx *c, const int32_t *rows, const int32_t *pool, int64_t npool,
+                      int64_t *accepted) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    return knnm_draws_insert_range(c, rows, pool, npool, 0, c->draw_n, accepted);
+}
+
+// Route of the local join for this round (dataset, k, rev_cap, mode).
+struct JoinRoute {
+    bool use_mma, tiled, lazy;
+    size_t smem, smem_tiled, smem_mma;
+};
+
+static int join_route(knnm_ctx *c, int W, int mode, JoinRoute *r) {
+    const size_t smem = sizeof(float) * (size_t)W * c->dp;
+    const size_t smem_tiled = sizeof(float) * (size_t)W * (c->dp + 4);
+    const int Wp = mj_rows(W, mode);
+    const size_t mj_per_warp = mj_meta_bytes(Wp) + (size_t)Wp * (c->rowb + 16);
+    const size_t smem_mma = MJ_WARPS * mj_per_warp;
+    const bool use_mma = c->cert_dot && smem_mma <= 200 * 1024 &&
+                         (c->join_variant == 2 || c->join_variant < 0);
+    // the d-chunked lazy route streams rows through fixed-size buffers, so it
+    // takes every non-certified long-row dataset and anything whose whole
+    // hood does not fit shared memory (e.g. d = 960 with k >= 27)
+    const bool tiled_fits = smem_tiled <= 200 * 1024;
+    const bool tiled = !use_mma && c->join_variant != 0 &&
+                       (c->join_variant == 1 || tiled_fits || c->d > LAZY_MIN_D);
+    const bool lazy = tiled && ((!c->cert && c->d > LAZY_MIN_D) || !tiled_fits);
+    if (!use_mma && !tiled && smem > 200 * 1024)
+        return fail(KNNM_ERR_LIMIT, "neighbourhood of %d x %d floats exceeds shared memory", W, c->dp);
+    if (tiled && !lazy && !tiled_fits)
+        return fail(KNNM_ERR_LIMIT, "neighbourhood of %d x %d floats exceeds shared memory", W, c->dp);
+    c->slots_mode = use_mma ? SLOTS_PACKED
+                    : tiled ? (lazy ? SLOTS_LAZY : c->cert ? SLOTS_PACKED : SLOTS_PLAIN)
+                            : SLOTS_PLAIN;
+    r->use_mma = use_mma;
+    r->tiled = tiled;
+    r->lazy = lazy;
+    r->smem = smem;
+    r->smem_tiled = smem_tiled;
+    r->smem_mma = smem_mma;
+    return KNNM_OK;
+}
+
+// One hood chunk of a round: membership layout -> bucket offsets -> local
+// join -> (unless local_only) apply.  ``counted``: k_assemble already
+// counted (and, with fused_memb, wrote) the memberships of exactly these
+// hoods.  Chunks must run in ascending hood order (the reference's per-row
+// order is (u, p, q)).
+static int join_chunk(knnm_ctx *c, int32_t mode, int W, const int32_t *act, int64_t nact,
+                      uint64_t pairs2, bool counted, bool fused_memb, bool local_only,
+                      int64_t *acc_out) {
+    const int64_t n = c->n;
+    unsigned long long *cnt = c->counters.as<unsigned long long>();
+    JoinRoute rt;
+    TRY(join_route(c, W, mode, &rt));
+    const bool use_mma = rt.use_mma, tiled = rt.tiled, lazy = rt.lazy;
+    const size_t smem = rt.smem, smem_tiled = rt.smem_tiled, smem_mma = rt.smem_mma;
+    c->stats.join_row_bytes = use_mma ? c->rowb : 4 * c->dp;
+    // long rows (large d): more warps share one staged hood
+    const int tj_threads = smem_tiled > 16 * 1024 ? TJ_WARPS_BIG * 32 : TJ_THREADS;
+    // lower bounds of the exact value from the fp32 one (LazyExact)
+    const double lo_rel = 1.0 - (double)(c->d + 8) * ldexp(1.0, -23);
+    const double lo_abs = (double)(4 * c->d + 64) * ldexp(1.0, -24);
+    CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
+    {
+        PhaseTimer pt(c, PH_JOIN);
+        // reference-order slot layout (see MembRec in knnm_kernels.cuh);
+        // k_assemble already counted every active hood's memberships
+        // (and, when fused, wrote their records)
+        const bool fused = counted && fused_memb;
+        if (!fused) CK(cudaMemsetAsync(c->mcur.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+        const int hgrid = grid_for(c, nact * 32, 256, 16);
+        if (!counted) {
+            CK(cudaMemsetAsync(c->bound.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+            CK(cudaMemsetAsync(c->mcount.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+            k_hood_memb<false><<<hgrid, 256, 0, c->st>>>(
+                act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
+                c->labels.as<int8_t>(), mode, c->bound.as<uint32_t>(),
+                c->mcount.as<uint32_t>(), nullptr, nullptr, nullptr);
+            CKL();
+        }
+        // fused: bucket sizes are written by rank_memberships below
+        if (!fused) TRY(scan<uint32_t, uint64_t>(c, c->bound.as<uint32_t>(), c->boff.as<uint64_t>(), n));
+        TRY(ensure_slots(c, pairs2));
+        if (!fused) {
+            TRY(scan<uint32_t, uint32_t>(c, c->mcount.as<uint32_t>(), c->moff.as<uint32_t>(), n));
+            TRY(ensure_memb(c, (uint64_t)n * W, (uint64_t)n * W));
+            k_hood_memb<true><<<hgrid, 256, 0, c->st>>>(
+                act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
+                c->labels.as<int8_t>(), mode, nullptr, nullptr, c->moff.as<uint32_t>(),
+                c->mcur.as<uint32_t>(), c->memb.as<MembRec>());
+            CKL();
+        }
+        TRY(rank_memberships(c, fused));
+        if (fused) TRY(scan<uint32_t, uint64_t>(c, c->bound.as<uint32_t>(), c->boff.as<uint64_t>(), n));
+        const uint64_t *boff = c->boff.as<uint64_t>();
+        const uint32_t *stt = c->start.as<uint32_t>();
+        double *Bd = c->Bd.as<double>();
+        int32_t *Bs = c->Bs.as<int32_t>();
+        PhaseTimer ptk(c, PH_JOINK);  // the local-join kernel alone (roofline)
+        if (use_mma) {
+            int per_sm = 1;
+            // 32-entry position blocks per hood
+            const int nb = W <= 32 ? 1 : W <= 64 ? 2 : 4;
+            const void *fn;
+#define KNNM_MJ_FN(U, N) (mode == 0 ? (const void *)k_join_mma<U, N, 0>                     \
+                  : mode == 1 ? (const void *)k_join_mma<U, N, 1> : (const void *)k_join_mma<U, N, 2>)
+            if (c->cert_u8) fn = nb == 1 ? KNNM_MJ_FN(true, 1) : nb == 2 ? KNNM_MJ_FN(true, 2) : KNNM_MJ_FN(true, 4);
+            else fn = nb == 1 ? KNNM_MJ_FN(false, 1) : nb == 2 ? KNNM_MJ_FN(false, 2) : KNNM_MJ_FN(false, 4);
+#undef KNNM_MJ_FN
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, MJ_WARPS * 32, smem_mma));
+            unsigned grid = (unsigned)std::min<int64_t>((nact + MJ_WARPS - 1) / MJ_WARPS,
+                                                        (int64_t)c->sms * std::max(per_sm, 1));
+            if (grid == 0) grid = 1;
+            int nact32 = (int)nact, Wi = W, modei = mode, rowbi = c->rowb;
+            const uint32_t *nbhp = c->nbh.as<uint32_t>();
+            const int32_t *nlp = c->nlen.as<int32_t>();
+            const int8_t *labp = c->labels.as<int8_t>();
+            const uint8_t *s16 = c->sub16p;
+            // per-row worst / norm / bucket base in one 16-byte record
+            TRY(ensure(c->rowmeta, sizeof(RowMeta) * (size_t)n));
+            k_rowmeta<<<grid_for(c, n, 256), 256, 0, c->st>>>(n, c->worst0.as<double>(), c->subnormp,
+                                                             boff, c->rowmeta.as<RowMeta>());
+            CKL();
+            const RowMeta *rmp = c->rowmeta.as<RowMeta>();
+            void *args[] = {(void *)&act, (void *)&nact32, (void *)&nbhp, (void *)&nlp, (void *)&Wi,
+                            (void *)&labp, (void *)&modei, (void *)&s16, (void *)&rowbi,
+                            (void *)&rmp, (void *)&stt, (void *)&Bd, (void *)&Bs};
+            CK(cudaLaunchKernel(fn, dim3(grid), dim3(MJ_WARPS * 32), args, smem_mma, c->st));
+        } else if (tiled) {
+            // non-certified rows: exact values in the join from the
+            // staged rows for short rows; for long rows the exact
+            // evaluation is deferred to the apply (LazyExact), which
+            // needs it for few slots only
+            const void *fn;
+            if (lazy) fn = nullptr;  // k_join_chunked below
+            else if (c->cert) fn = c->metric == 1 ? (const void *)k_join_tiled<1, true, false>
+                                             : (const void *)k_join_tiled<0, true, false>;
+            else fn = c->metric == 1 ? (const void *)k_join_tiled<1, false, false>
+                      : c->metric == 2 ? (const void *)k_join_tiled<2, false, false>
+                                       : (const void *)k_join_tiled<0, false, false>;
+            int per_sm = 1;
+            if (fn) CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, tj_threads, smem_tiled));
+            unsigned grid = (unsigned)std::min<int64_t>(nact, (int64_t)c->sms * std::max(per_sm, 1));
+            if (grid == 0) grid = 1;
+            int na = (int)nact;
+            const double *nrm = c->metric == KNNM_COSINE ? c->nrm64.as<double>() : nullptr;
+#define KNNM_TJ_ARGS                                                                          \
+act, na, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,  \
+c->subp, c->dp, c->d, c->worst0.as<double>(), boff, stt, Bd, Bs, lo_rel, lo_abs, nrm, cnt
+#define KNNM_TJ_LAUNCH(T, C, L) k_join_tiled<T, C, L><<<grid, tj_threads, smem_tiled, c->st>>>(KNNM_TJ_ARGS)
+            if (c->cert && !lazy) {
+                if (c->metric == 1) KNNM_TJ_LAUNCH(1, true, false);
+                else KNNM_TJ_LAUNCH(0, true, false);
+            } else if (lazy) {
+                // rows stream through two CJ_DC-dimension buffers
+                const size_t smem_cj = 2 * (size_t)W * (CJ_DC / 4 + 1) * sizeof(float4);
+                const void *fc = c->metric == 1 ? (const void *)k_join_chunked<1>
+                                 : c->metric == 2 ? (const void *)k_join_chunked<2>
+                                                  : (const void *)k_join_chunked<0>;
+                int per_cj = 1;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_cj, fc, CJ_WARPS * 32, smem_cj));
+                const unsigned gcj = (unsigned)std::max<int64_t>(
+                    1, std::min<int64_t>(nact, (int64_t)c->sms * std::max(per_cj, 1)));
+#define KNNM_CJ_LAUNCH(T)                                                                          \
+k_join_chunked<T><<<gcj, CJ_WARPS * 32, smem_cj, c->st>>>(                                     \
+act, na, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, mode, c->subp, c->dp,           \
+c->worst0.as<double>(), boff, stt, Bd, Bs, lo_rel, lo_abs)
+                if (c->metric == 1) KNNM_CJ_LAUNCH(1);
+                else if (c->metric == 2) KNNM_CJ_LAUNCH(2);
+                else KNNM_CJ_LAUNCH(0);
+#undef KNNM_CJ_LAUNCH
+            } else {
+                if (c->metric == 1) KNNM_TJ_LAUNCH(1, false, false);
+                else if (c->metric == 2) KNNM_TJ_LAUNCH(2, false, false);
+                else KNNM_TJ_LAUNCH(0, false, false);
+            }
+#undef KNNM_TJ_LAUNCH
+#undef KNNM_TJ_ARGS
+        } else {
+#define KNNM_JE_ARGS                                                                          \
+act, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,       \
+c->subp, c->dp, c->d, c->worst0.as<double>(), boff, stt, Bd, Bs
+            if (c->metric == 1)
+                k_join_exact<1><<<(unsigned)nact, JOIN_THREADS, smem, c->st>>>(KNNM_JE_ARGS);
+            else if (c->metric == 2)
+                k_join_exact<2><<<(unsigned)nact, JOIN_THREADS, smem, c->st>>>(KNNM_JE_ARGS);
+            else
+                k_join_exact<0><<<(unsigned)nact, JOIN_THREADS, smem, c->st>>>(KNNM_JE_ARGS);
+#undef KNNM_JE_ARGS
+        }
+        CKL();
+        c->stats.join_launches += 1;
+    }
+    if (local_only) {  // slots stay for the exchange (knnm_local_views)
+        TRY(sync_counters(c));
+        c->stats.exact_evals += (int64_t)c->hcnt[C_EXACT];
+        return KNNM_OK;
+    }
+    {
+        PhaseTimer pt(c, PH_UPDATE);
+        TRY(run_updates(c));
+    }
+    c->stats.exact_evals += (int64_t)c->hcnt[C_EXACT];
+    *acc_out += (int64_t)c->hcnt[C_ACCEPTED];
+    return KNNM_OK;
+}
+
+// Hood chunks for a round whose 2P slots exceed the candidate budget:
+// consecutive hood ranges (ascending, which keeps the reference's per-row
+// order: keys are (u, p, q)), each holding at most ``budget`` slots (a single
+// hood larger than that gets a chunk of its own).
+static int plan_chunks(knnm_ctx *c, uint64_t budget, std::vector<std::vector<int32_t>> &lists,
+                       std::vector<uint64_t> &pairs2) {
+    const int64_t n = c->n;
+    std::vector<uint64_t> hpoff(n + 1);
+    std::vector<uint32_t> hh(n);
+    CK(cudaMemcpyAsync(hpoff.data(), c->poff.p, sizeof(uint64_t) * (n + 1), cudaMemcpyDeviceToHost,
+                       c->st));
+    CK(cudaMemcpyAsync(hh.data(), c->hpairs.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost, c->st));
+    CK(cudaStreamSynchronize(c->st));
+    c->stats.join_redos += 1;
+    lists.clear();
+    pairs2.clear();
+    int64_t lo = 0;
+    while (lo < n) {
+        int64_t hi = lo;
+        std::vector<int32_t> lst;
+        while (hi < n && (2 * (hpoff[hi + 1] - hpoff[lo]) <= budget || hi == lo)) {
+            if (hh[hi]) lst.push_back((int32_t)hi);
+            hi++;
+        }
+        if (!lst.empty()) {
+            lists.push_back(std::move(lst));
+            pairs2.push_back(2 * (hpoff[hi] - hpoff[lo]));
+        }
+        lo = hi;
+    }
+    return KNNM_OK;
 }
 
 static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_seed,
@@ -1406,213 +1658,52 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
     }
 
     int64_t acc_total = 0;
+    {  // the slot format is fixed even when this rank has no pairs
+        JoinRoute rt;
+        TRY(join_route(c, W, mode, &rt));
+    }
+    const uint64_t budget = bucket_budget(c);
+    if (local_only) {
+        // sharded round: the join runs chunk by chunk in knnm_local_join,
+        // with the exchange of each chunk's slots in between
+        c->lc_mode = mode;
+        c->lc_W = W;
+        c->lc_single = true;
+        c->lc_nact = (int64_t)nactive;
+        c->lc_lists.clear();
+        c->lc_pairs2.clear();
+        if (P > 0) {
+            if (2 * P <= budget) {
+                c->lc_pairs2.push_back(2 * P);
+            } else {
+                c->lc_single = false;
+                TRY(plan_chunks(c, budget, c->lc_lists, c->lc_pairs2));
+            }
+        }
+        TRY(resolve_timers(c));
+        if (pairs) *pairs = (int64_t)P;
+        if (accepted) *accepted = 0;
+        return KNNM_OK;
+    }
     if (P > 0) {
-        size_t smem = sizeof(float) * (size_t)W * c->dp;
-        size_t smem_tiled = sizeof(float) * (size_t)W * (c->dp + 4);
-        if (smem > 200 * 1024) return fail(KNNM_ERR_LIMIT, "neighbourhood of %d x %d floats exceeds shared memory", W, c->dp);
-        const int Wp = mj_rows(W, mode);
-        const size_t mj_per_warp = mj_meta_bytes(Wp) + (size_t)Wp * (c->rowb + 16);
-        const size_t smem_mma = MJ_WARPS * mj_per_warp;
-        c->stats.join_row_bytes = c->cert_dot ? c->rowb : 4 * c->dp;
-        const bool use_mma = c->cert_dot && smem_mma <= 200 * 1024 &&
-                             (c->join_variant == 2 || c->join_variant < 0);
-        const bool tiled = !use_mma && (c->join_variant == 1 || (c->join_variant < 0 && smem_tiled <= 200 * 1024));
-        // long rows (large d): more warps share one staged hood
-        const int tj_threads = smem_tiled > 16 * 1024 ? TJ_WARPS_BIG * 32 : TJ_THREADS;
-        // lower bounds of the exact value from the fp32 one (LazyExact)
-        const double lo_rel = 1.0 - (double)(c->d + 8) * ldexp(1.0, -23);
-        const double lo_abs = (double)(4 * c->d + 64) * ldexp(1.0, -24);
-        // One pass per hood chunk: bounds -> bucket offsets -> join -> apply.
-        auto run_chunk = [&](const int32_t *act, int64_t nact, uint64_t pairs2, bool counted) -> int {
-            CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
-            {
-                PhaseTimer pt(c, PH_JOIN);
-                // reference-order slot layout (see MembRec in knnm_kernels.cuh);
-                // k_assemble already counted every active hood's memberships
-                // (and, when fused, wrote their records)
-                const bool fused = counted && fused_memb;
-                if (!fused) CK(cudaMemsetAsync(c->mcur.p, 0, sizeof(uint32_t) * (n + 1), c->st));
-                const int hgrid = grid_for(c, nact * 32, 256, 16);
-                if (!counted) {
-                    CK(cudaMemsetAsync(c->bound.p, 0, sizeof(uint32_t) * (n + 1), c->st));
-                    CK(cudaMemsetAsync(c->mcount.p, 0, sizeof(uint32_t) * (n + 1), c->st));
-                    k_hood_memb<false><<<hgrid, 256, 0, c->st>>>(
-                        act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
-                        c->labels.as<int8_t>(), mode, c->bound.as<uint32_t>(),
-                        c->mcount.as<uint32_t>(), nullptr, nullptr, nullptr);
-                    CKL();
-                }
-                // fused: bucket sizes are written by rank_memberships below
-                if (!fused) TRY(scan<uint32_t, uint64_t>(c, c->bound.as<uint32_t>(), c->boff.as<uint64_t>(), n));
-                TRY(ensure_slots(c, pairs2));
-                if (!fused) {
-                    TRY(scan<uint32_t, uint32_t>(c, c->mcount.as<uint32_t>(), c->moff.as<uint32_t>(), n));
-                    TRY(ensure_memb(c, (uint64_t)n * W, (uint64_t)n * W));
-                    k_hood_memb<true><<<hgrid, 256, 0, c->st>>>(
-                        act, (int)nact, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
-                        c->labels.as<int8_t>(), mode, nullptr, nullptr, c->moff.as<uint32_t>(),
-                        c->mcur.as<uint32_t>(), c->memb.as<MembRec>());
-                    CKL();
-                }
-                TRY(rank_memberships(c, fused));
-                if (fused) TRY(scan<uint32_t, uint64_t>(c, c->bound.as<uint32_t>(), c->boff.as<uint64_t>(), n));
-                const uint64_t *boff = c->boff.as<uint64_t>();
-                const uint32_t *stt = c->start.as<uint32_t>();
-                double *Bd = c->Bd.as<double>();
-                int32_t *Bs = c->Bs.as<int32_t>();
-                PhaseTimer ptk(c, PH_JOINK);  // the local-join kernel alone (roofline)
-                if (use_mma) {
-                    int per_sm = 1;
-                    c->slots_mode = SLOTS_PACKED;
-                    // 32-entry position blocks per hood
-                    const int nb = W <= 32 ? 1 : W <= 64 ? 2 : 4;
-                    const void *fn;
-#define KNNM_MJ_FN(U, N) (mode == 0 ? (const void *)k_join_mma<U, N, 0>                     \
-                          : mode == 1 ? (const void *)k_join_mma<U, N, 1> : (const void *)k_join_mma<U, N, 2>)
-                    if (c->cert_u8) fn = nb == 1 ? KNNM_MJ_FN(true, 1) : nb == 2 ? KNNM_MJ_FN(true, 2) : KNNM_MJ_FN(true, 4);
-                    else fn = nb == 1 ? KNNM_MJ_FN(false, 1) : nb == 2 ? KNNM_MJ_FN(false, 2) : KNNM_MJ_FN(false, 4);
-#undef KNNM_MJ_FN
-                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, MJ_WARPS * 32, smem_mma));
-                    unsigned grid = (unsigned)std::min<int64_t>((nact + MJ_WARPS - 1) / MJ_WARPS,
-                                                                (int64_t)c->sms * std::max(per_sm, 1));
-                    if (grid == 0) grid = 1;
-                    int nact32 = (int)nact, Wi = W, modei = mode, rowbi = c->rowb;
-                    const uint32_t *nbhp = c->nbh.as<uint32_t>();
-                    const int32_t *nlp = c->nlen.as<int32_t>();
-                    const int8_t *labp = c->labels.as<int8_t>();
-                    const uint8_t *s16 = c->sub16p;
-                    // per-row worst / norm / bucket base in one 16-byte record
-                    TRY(ensure(c->rowmeta, sizeof(RowMeta) * (size_t)n));
-                    k_rowmeta<<<grid_for(c, n, 256), 256, 0, c->st>>>(n, c->worst0.as<double>(), c->subnormp,
-                                                                     boff, c->rowmeta.as<RowMeta>());
-                    CKL();
-                    const RowMeta *rmp = c->rowmeta.as<RowMeta>();
-                    void *args[] = {(void *)&act, (void *)&nact32, (void *)&nbhp, (void *)&nlp, (void *)&Wi,
-                                    (void *)&labp, (void *)&modei, (void *)&s16, (void *)&rowbi,
-                                    (void *)&rmp, (void *)&stt, (void *)&Bd, (void *)&Bs};
-                    CK(cudaLaunchKernel(fn, dim3(grid), dim3(MJ_WARPS * 32), args, smem_mma, c->st));
-                } else if (tiled) {
-                    // non-certified rows: exact values in the join from the
-                    // staged rows for short rows; for long rows the exact
-                    // evaluation is deferred to the apply (LazyExact), which
-                    // needs it for few slots only
-                    const bool lazy = !c->cert && c->d > LAZY_MIN_D;
-                    c->slots_mode = c->cert ? SLOTS_PACKED : lazy ? SLOTS_LAZY : SLOTS_PLAIN;
-                    const void *fn;
-                    if (c->cert) fn = c->metric == 1 ? (const void *)k_join_tiled<1, true, false>
-                                                     : (const void *)k_join_tiled<0, true, false>;
-                    else if (lazy) fn = c->metric == 1 ? (const void *)k_join_tiled<1, false, true>
-                                        : c->metric == 2 ? (const void *)k_join_tiled<2, false, true>
-                                                         : (const void *)k_join_tiled<0, false, true>;
-                    else fn = c->metric == 1 ? (const void *)k_join_tiled<1, false, false>
-                              : c->metric == 2 ? (const void *)k_join_tiled<2, false, false>
-                                               : (const void *)k_join_tiled<0, false, false>;
-                    int per_sm = 1;
-                    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, tj_threads, smem_tiled));
-                    unsigned grid = (unsigned)std::min<int64_t>(nact, (int64_t)c->sms * std::max(per_sm, 1));
-                    if (grid == 0) grid = 1;
-                    int na = (int)nact;
-                    const double *nrm = c->metric == KNNM_COSINE ? c->nrm64.as<double>() : nullptr;
-#define KNNM_TJ_ARGS                                                                          \
-    act, na, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,  \
-        c->subp, c->dp, c->d, c->worst0.as<double>(), boff, stt, Bd, Bs, lo_rel, lo_abs, nrm, cnt
-#define KNNM_TJ_LAUNCH(T, C, L) k_join_tiled<T, C, L><<<grid, tj_threads, smem_tiled, c->st>>>(KNNM_TJ_ARGS)
-                    if (c->cert) {
-                        if (c->metric == 1) KNNM_TJ_LAUNCH(1, true, false);
-                        else KNNM_TJ_LAUNCH(0, true, false);
-                    } else if (lazy) {
-                        // rows stream through two CJ_DC-dimension buffers
-                        const size_t smem_cj = 2 * (size_t)W * (CJ_DC / 4 + 1) * sizeof(float4);
-                        const void *fc = c->metric == 1 ? (const void *)k_join_chunked<1>
-                                         : c->metric == 2 ? (const void *)k_join_chunked<2>
-                                                          : (const void *)k_join_chunked<0>;
-                        int per_cj = 1;
-                        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_cj, fc, CJ_WARPS * 32, smem_cj));
-                        const unsigned gcj = (unsigned)std::max<int64_t>(
-                            1, std::min<int64_t>(nact, (int64_t)c->sms * std::max(per_cj, 1)));
-#define KNNM_CJ_LAUNCH(T)                                                                          \
-    k_join_chunked<T><<<gcj, CJ_WARPS * 32, smem_cj, c->st>>>(                                     \
-        act, na, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, mode, c->subp, c->dp,           \
-        c->worst0.as<double>(), boff, stt, Bd, Bs, lo_rel, lo_abs)
-                        if (c->metric == 1) KNNM_CJ_LAUNCH(1);
-                        else if (c->metric == 2) KNNM_CJ_LAUNCH(2);
-                        else KNNM_CJ_LAUNCH(0);
-#undef KNNM_CJ_LAUNCH
-                    } else {
-                        if (c->metric == 1) KNNM_TJ_LAUNCH(1, false, false);
-                        else if (c->metric == 2) KNNM_TJ_LAUNCH(2, false, false);
-                        else KNNM_TJ_LAUNCH(0, false, false);
-                    }
-#undef KNNM_TJ_LAUNCH
-#undef KNNM_TJ_ARGS
-                } else {
-                    c->slots_mode = SLOTS_PLAIN;
-#define KNNM_JE_ARGS                                                                          \
-    act, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, c->labels.as<int8_t>(), mode,       \
-        c->subp, c->dp, c->d, c->worst0.as<double>(), boff, stt, Bd, Bs
-                    if (c->metric == 1)
-                        k_join_exact<1><<<(unsigned)nact, JOIN_THREADS, smem, c->st>>>(KNNM_JE_ARGS);
-                    else if (c->metric == 2)
-                        k_join_exact<2><<<(unsigned)nact, JOIN_THREADS, smem, c->st>>>(KNNM_JE_ARGS);
-                    else
-                        k_join_exact<0><<<(unsigned)nact, JOIN_THREADS, smem, c->st>>>(KNNM_JE_ARGS);
-#undef KNNM_JE_ARGS
-                }
-                CKL();
-                c->stats.join_launches += 1;
-            }
-            if (local_only) {  // slots stay for the exchange (knnm_local_views)
-                TRY(sync_counters(c));
-                c->stats.exact_evals += (int64_t)c->hcnt[C_EXACT];
-                return KNNM_OK;
-            }
-            {
-                PhaseTimer pt(c, PH_UPDATE);
-                TRY(run_updates(c));
-            }
-            c->stats.exact_evals += (int64_t)c->hcnt[C_EXACT];
-            acc_total += (int64_t)c->hcnt[C_ACCEPTED];
-            return KNNM_OK;
-        };
-        const uint64_t budget = bucket_budget(c);
-        if (local_only && 2 * P > budget)
-            return fail(KNNM_ERR_LIMIT, "sharded round needs %llu slots > budget", (unsigned long long)(2 * P));
         if (2 * P <= budget) {
             // phi inside the round's final wait, unless the caller reduces it
             // asynchronously (knnm_phi_async) while the next round runs
-            c->phi_in_updates = !local_only && !c->st2;
-            const int rc = run_chunk(c->active.as<int32_t>(), (int64_t)nactive, 2 * P, true);
+            c->phi_in_updates = !c->st2;
+            const int rc = join_chunk(c, mode, W, c->active.as<int32_t>(), (int64_t)nactive, 2 * P,
+                                      true, fused_memb, false, &acc_total);
             c->phi_in_updates = false;
             TRY(rc);
         } else {
-            // Chunk hoods by index so each chunk's buckets fit; chunks run in
-            // ascending hood order, which preserves the reference's per-row
-            // order (keys are (u, p, q)).
-            std::vector<uint64_t> hpoff(n + 1);
-            std::vector<uint32_t> hh(n);
-            CK(cudaMemcpyAsync(hpoff.data(), c->poff.p, sizeof(uint64_t) * (n + 1),
-                               cudaMemcpyDeviceToHost, c->st));
-            CK(cudaMemcpyAsync(hh.data(), c->hpairs.p, sizeof(uint32_t) * n, cudaMemcpyDeviceToHost,
-                               c->st));
-            CK(cudaStreamSynchronize(c->st));
-            c->stats.join_redos += 1;
-            int64_t lo = 0;
-            std::vector<int32_t> lst;
-            while (lo < n) {
-                int64_t hi = lo;
-                lst.clear();
-                while (hi < n && (2 * (hpoff[hi + 1] - hpoff[lo]) <= budget || hi == lo)) {
-                    if (hh[hi]) lst.push_back((int32_t)hi);
-                    hi++;
-                }
-                if (!lst.empty()) {
-                    CK(cudaMemcpyAsync(c->active.p, lst.data(), sizeof(int32_t) * lst.size(),
-                                       cudaMemcpyHostToDevice, c->st));
-                    TRY(run_chunk(c->active.as<int32_t>(), (int64_t)lst.size(),
-                                  2 * (hpoff[hi] - hpoff[lo]), false));
-                    CK(cudaStreamSynchronize(c->st));  // lst is reused
-                }
-                lo = hi;
+            std::vector<std::vector<int32_t>> lists;
+            std::vector<uint64_t> p2;
+            TRY(plan_chunks(c, budget, lists, p2));
+            for (size_t i = 0; i < lists.size(); i++) {
+                CK(cudaMemcpyAsync(c->active.p, lists[i].data(), sizeof(int32_t) * lists[i].size(),
+                                   cudaMemcpyHostToDevice, c->st));
+                TRY(join_chunk(c, mode, W, c->active.as<int32_t>(), (int64_t)lists[i].size(), p2[i],
+                               false, fused_memb, false, &acc_total));
+                CK(cudaStreamSynchronize(c->st));
             }
         }
     }
@@ -1646,7 +1737,65 @@ int knnm_round_local(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round_
     CK(cudaSetDevice(c->device));
     CK(cudaMemsetAsync(c->bound.p, 0, sizeof(uint32_t) * (c->n + 1), c->st));
     CK(cudaMemsetAsync(c->boff.p, 0, sizeof(uint64_t) * (c->n + 1), c->st));
+    TRY(ensure(c->dirty, (size_t)c->n + 1));
+    CK(cudaMemsetAsync(c->dirty.p, 0, (size_t)c->n + 1, c->st));
     return round_impl(c, mode, rev_cap, round_seed, pairs_local, nullptr, true);
+}
+
+int knnm_local_chunks(knnm_ctx *c, int32_t *nchunks) {
+    if (!c || !nchunks) return fail(KNNM_ERR_ARG, "null argument");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    *nchunks = (int32_t)c->lc_pairs2.size();
+    return KNNM_OK;
+}
+
+int knnm_local_join(knnm_ctx *c, int32_t chunk) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    if (chunk < 0) return fail(KNNM_ERR_ARG, "chunk %d", chunk);
+    CK(cudaSetDevice(c->device));
+    const int64_t n = c->n;
+    if ((size_t)chunk >= c->lc_pairs2.size()) {
+        // this rank has fewer chunks than the busiest one: empty slot views
+        CK(cudaMemsetAsync(c->bound.p, 0, sizeof(uint32_t) * (n + 1), c->st));
+        CK(cudaMemsetAsync(c->boff.p, 0, sizeof(uint64_t) * (n + 1), c->st));
+        return KNNM_OK;
+    }
+    int64_t acc = 0;
+    if (c->lc_single)
+        return join_chunk(c, c->lc_mode, c->lc_W, c->active.as<int32_t>(), c->lc_nact,
+                          c->lc_pairs2[0], true, false, true, &acc);
+    const std::vector<int32_t> &lst = c->lc_lists[chunk];
+    CK(cudaMemcpyAsync(c->active.p, lst.data(), sizeof(int32_t) * lst.size(), cudaMemcpyHostToDevice,
+                       c->st));
+    return join_chunk(c, c->lc_mode, c->lc_W, c->active.as<int32_t>(), (int64_t)lst.size(),
+                      c->lc_pairs2[chunk], false, false, true, &acc);
+}
+
+int knnm_wait_stream(knnm_ctx *c, void *stream) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    CK(cudaSetDevice(c->device));
+    if (!c->ev_wait) CK(cudaEventCreateWithFlags(&c->ev_wait, cudaEventDisableTiming));
+    CK(cudaEventRecord(c->ev_wait, (cudaStream_t)stream));
+    CK(cudaStreamWaitEvent(c->st, c->ev_wait, 0));
+    return KNNM_OK;
+}
+
+int knnm_signal_stream(knnm_ctx *c, void *stream) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    CK(cudaSetDevice(c->device));
+    if (!c->ev_sig) CK(cudaEventCreateWithFlags(&c->ev_sig, cudaEventDisableTiming));
+    CK(cudaEventRecord(c->ev_sig, c->st));
+    CK(cudaStreamWaitEvent((cudaStream_t)stream, c->ev_sig, 0));
+    return KNNM_OK;
+}
+
+int knnm_set_cand_budget(knnm_ctx *c, int64_t bytes) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (bytes < 0) return fail(KNNM_ERR_ARG, "budget %lld", (long long)bytes);
+    // 0 restores the default; a tiny budget forces one hood per chunk
+    c->cand_budget_bytes = bytes == 0 ? ((size_t)40 << 30) : (size_t)bytes;
+    return KNNM_OK;
 }
 
 int knnm_local_views(knnm_ctx *c, void **cnt, void **boff, void **Bd, void **Bs) {
@@ -1723,7 +1872,8 @@ int knnm_round_apply(knnm_ctx *c, int32_t nsrc, const uint32_t *recv_cnt, const 
 #define KNNM_APM_LAUNCH(EE, LZ)                                                                 \
     k_apply_stream_multi<EE, LZ><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(                      \
         lo, no, c->k, nsrc, off, recv_cnt, recv_Bd, recv_Bs, c->ids.as<int32_t>(),             \
-        c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), cnt, lazy_of(c))
+        c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), cnt, lazy_of(c), \
+        c->dirty.as<uint8_t>())
     if (E == 1) {
         if (c->slots_mode == SLOTS_LAZY) KNNM_APM_LAUNCH(1, SLOTS_LAZY);
         else if (c->slots_mode == SLOTS_PACKED) KNNM_APM_LAUNCH(1, SLOTS_PACKED);
@@ -1739,6 +1889,55 @@ int knnm_round_apply(knnm_ctx *c, int32_t nsrc, const uint32_t *recv_cnt, const 
     c->stats.accepted += (int64_t)c->hcnt[C_ACCEPTED];
     c->stats.exact_evals += (int64_t)c->hcnt[C_EXACT];
     if (accepted) *accepted = (int64_t)c->hcnt[C_ACCEPTED];
+    return KNNM_OK;
+}
+
+int knnm_pack_rows(knnm_ctx *c, int32_t all, void **buf, int64_t *count, int32_t *rec_bytes) {
+    if (!c || !buf || !count) return fail(KNNM_ERR_ARG, "null argument");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    CK(cudaSetDevice(c->device));
+    const int64_t lo = c->shard_lo, hi = c->shard_hi < 0 ? c->n : c->shard_hi, no = hi - lo;
+    const int rb = row_rec_bytes(c->k);
+    if (rec_bytes) *rec_bytes = rb;
+    TRY(ensure(c->dirty, (size_t)c->n + 1));
+    TRY(ensure(c->live, (size_t)c->n + 1));
+    TRY(ensure(c->rsel, sizeof(uint32_t) * (size_t)(no + 1)));
+    TRY(ensure(c->rsoff, sizeof(uint64_t) * (size_t)(no + 1)));
+    uint64_t cntr = 0;
+    if (no > 0) {
+        k_row_select<<<grid_for(c, no, 256), 256, 0, c->st>>>(lo, no, all, c->live.as<uint8_t>(),
+                                                              c->dirty.as<uint8_t>(), c->rsel.as<uint32_t>());
+        CKL();
+        TRY(scan<uint32_t, uint64_t>(c, c->rsel.as<uint32_t>(), c->rsoff.as<uint64_t>(), no));
+        CK(cudaMemcpyAsync(&c->hcnt[C_NUM - 1], c->rsoff.as<uint64_t>() + no, sizeof(uint64_t),
+                           cudaMemcpyDeviceToHost, c->st));
+        CK(cudaStreamSynchronize(c->st));
+        cntr = c->hcnt[C_NUM - 1];
+    }
+    TRY(ensure(c->rpack, (size_t)rb * (size_t)(cntr + 1)));
+    if (cntr > 0) {
+        k_pack_rows<<<grid_for(c, no * 32, 256, 16), 256, 0, c->st>>>(
+            lo, no, c->k, c->rsel.as<uint32_t>(), c->rsoff.as<uint64_t>(), c->ids.as<int32_t>(),
+            c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(),
+            c->rpack.as<uint8_t>());
+        CKL();
+    }
+    *buf = c->rpack.p;
+    *count = (int64_t)cntr;
+    return KNNM_OK;
+}
+
+int knnm_unpack_rows(knnm_ctx *c, const void *buf, int64_t count) {
+    if (c) c->state_gen++;  // the lists change: cached phi is stale
+    phi_wait(c);
+    if (!c || (count > 0 && !buf) || count < 0) return fail(KNNM_ERR_ARG, "bad argument");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    if (count == 0) return KNNM_OK;
+    CK(cudaSetDevice(c->device));
+    k_unpack_rows<<<grid_for(c, count * 32, 256, 16), 256, 0, c->st>>>(
+        count, c->k, (const uint8_t *)buf, c->ids.as<int32_t>(), c->dists.as<double>(),
+        c->flags.as<uint8_t>(), c->sizes.as<int32_t>());
+    CKL();
     return KNNM_OK;
 }
 
@@ -1888,6 +2087,44 @@ int knnm_merge_members(const int64_t *a, int64_t na, const int64_t *b, int64_t n
     }
     *nu = o;
     if (shared) *shared = s;
+    return KNNM_OK;
+}
+
+// Content fingerprint of a host buffer (the dataset cache key): the 64-bit
+// words w_i folded as sum(w_i * (2i + 1)) mod 2^64 per thread slice, the
+// slices combined with a mix.  Any single-word change alters the sum (odd
+// multipliers are invertible mod 2^64).  Host threads, memory-bound.
+int knnm_fingerprint(const void *p, int64_t bytes, uint64_t *out) {
+    if ((!p && bytes > 0) || bytes < 0 || !out) return fail(KNNM_ERR_ARG, "bad argument");
+    const uint64_t *w = (const uint64_t *)p;
+    const int64_t nw = bytes / 8;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int64_t nt = std::min<int64_t>(std::min(16u, hw), std::max<int64_t>(1, nw >> 18));
+    std::vector<uint64_t> part((size_t)nt, 0);
+    auto body = [&](int64_t t) {
+        const int64_t a = nw * t / nt, b = nw * (t + 1) / nt;
+        uint64_t h0 = 0, h1 = 0;
+        int64_t i = a;
+        for (; i + 1 < b; i += 2) {
+            h0 += w[i] * (2 * (uint64_t)i + 1);
+            h1 += w[i + 1] * (2 * (uint64_t)i + 3);
+        }
+        if (i < b) h0 += w[i] * (2 * (uint64_t)i + 1);
+        part[(size_t)t] = h0 + h1;
+    };
+    std::vector<std::thread> th;
+    for (int64_t t = 1; t < nt; t++) th.emplace_back(body, t);
+    body(0);
+    for (auto &x : th) x.join();
+    uint64_t h = 0x9e3779b97f4a7c15ull ^ (uint64_t)bytes;
+    for (uint64_t v : part) h += v;
+    uint64_t tail = 0;
+    memcpy(&tail, (const char *)p + nw * 8, (size_t)(bytes - nw * 8));
+    h += tail * 0xff51afd7ed558ccdull;
+    h ^= h >> 33;
+    h *= 0xc4ceb9fe1a85ec53ull;
+    h ^= h >> 33;
+    *out = h;
     return KNNM_OK;
 }
 

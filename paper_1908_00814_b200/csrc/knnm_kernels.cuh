@@ -2590,7 +2590,8 @@ __global__ void __launch_bounds__(APPLY_WARPS * 32)
 k_apply_stream_multi(int64_t lo, int64_t no, int k, int nsrc, const uint64_t *__restrict__ off,
                      const uint32_t *__restrict__ cnt, const double *__restrict__ Bd,
                      const int32_t *__restrict__ Bs, int32_t *ids, double *dists, uint8_t *flags,
-                     int32_t *sizes, unsigned long long *counters, LazyExact z) {
+                     int32_t *sizes, unsigned long long *counters, LazyExact z,
+                     uint8_t *dirty) {
     constexpr bool LAZY = MODE == SLOTS_LAZY;
     __shared__ double s_lz[LAZY ? APPLY_WARPS : 1][LAZY ? LZ_G * LZ_S : 1];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
@@ -2634,13 +2635,75 @@ k_apply_stream_multi(int64_t lo, int64_t no, int k, int nsrc, const uint64_t *__
                 a += warp_apply_chunk<E>(st, k, src, dl, c, lane);
             }
         }
-        if (a) row_store<E>(st, ids, dists, flags, sizes, r, k, lane);
+        if (a) {
+            row_store<E>(st, ids, dists, flags, sizes, r, k, lane);
+            if (lane == 0) dirty[r] = 1;
+        }
         acc += a;
     }
     if (lane == 0 && acc) atomicAdd(&counters[C_ACCEPTED], acc);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nexact += __shfl_xor_sync(FULL_MASK, nexact, o);
     if (lane == 0 && nexact) atomicAdd(&counters[C_EXACT], nexact);
+}
+
+// ---- replication of owned rows (sharded rounds) --------------------------
+// A row record: f64 dists[k] | i32 ids[k] | i32 row | i32 size | u8 flags[k],
+// padded to 8 bytes (row_rec_bytes).  Rows changed by a sharded round are
+// the owned rows whose flags the assembly cleared (live: any flag set at
+// round start) or that accepted an insert (dirty).
+__host__ __device__ inline int row_rec_bytes(int k) { return (12 * k + 8 + k + 7) & ~7; }
+
+__global__ void k_row_select(int64_t lo, int64_t no, int all, const uint8_t *__restrict__ live,
+                             const uint8_t *__restrict__ dirty, uint32_t *sel) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < no;
+         i += (int64_t)gridDim.x * blockDim.x)
+        sel[i] = (all || live[lo + i] || dirty[lo + i]) ? 1u : 0u;
+}
+
+// one warp per selected row: coalesced row reads, record writes
+__global__ void k_pack_rows(int64_t lo, int64_t no, int k, const uint32_t *__restrict__ sel,
+                            const uint64_t *__restrict__ soff, const int32_t *__restrict__ ids,
+                            const double *__restrict__ dists, const uint8_t *__restrict__ flags,
+                            const int32_t *__restrict__ sizes, uint8_t *out) {
+    const unsigned lane = lane_id();
+    const int rb = row_rec_bytes(k);
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < no; i += nw) {
+        if (!sel[i]) continue;
+        const int64_t r = lo + i;
+        uint8_t *rec = out + (size_t)soff[i] * rb;
+        double *d = (double *)rec;
+        int32_t *id = (int32_t *)(rec + 8 * (size_t)k);
+        for (int t = lane; t < k; t += 32) {
+            d[t] = dists[r * k + t];
+            id[t] = ids[r * k + t];
+            rec[12 * k + 8 + t] = flags[r * k + t];
+        }
+        if (lane == 0) {
+            id[k] = (int32_t)r;
+            id[k + 1] = sizes[r];
+        }
+    }
+}
+
+__global__ void k_unpack_rows(int64_t count, int k, const uint8_t *__restrict__ in, int32_t *ids,
+                              double *dists, uint8_t *flags, int32_t *sizes) {
+    const unsigned lane = lane_id();
+    const int rb = row_rec_bytes(k);
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < count; i += nw) {
+        const uint8_t *rec = in + (size_t)i * rb;
+        const double *d = (const double *)rec;
+        const int32_t *id = (const int32_t *)(rec + 8 * (size_t)k);
+        const int64_t r = id[k];
+        for (int t = lane; t < k; t += 32) {
+            dists[r * k + t] = d[t];
+            ids[r * k + t] = id[t];
+            flags[r * k + t] = rec[12 * k + 8 + t];
+        }
+        if (lane == 0) sizes[r] = id[k + 1];
+    }
 }
 
 __global__ void k_add_base(uint64_t *off, int64_t m, uint64_t base) {

@@ -28,6 +28,8 @@ class Engine:
         self._lib = lib
         self._vectors = None  # host array currently resident on the device
         self._metric = None
+        self._key = None      # (shape, metric) of the resident copy
+        self._fp = None       # its content fingerprint
         self.pinned_outputs = False  # export into page-locked host buffers
         self.n = 0
         self.k = 0
@@ -45,16 +47,35 @@ class Engine:
 
     # -- dataset -----------------------------------------------------------
     def set_dataset(self, vectors: np.ndarray, metric: int) -> None:
-        """Upload Dataset.vectors once; re-used while the same array is passed."""
-        if self._vectors is vectors and self._metric == int(metric):
-            return
+        """Keep Dataset.vectors resident in HBM across merges.
+
+        The device copy is re-used when the same read-only array is passed
+        again (its whole base chain read-only, so it cannot change), or when
+        the content fingerprint (knnm_fingerprint, host threads) equals the
+        uploaded one -- an in-place edit of a writeable array is re-uploaded,
+        never served stale.  ``invalidate()`` drops the copy explicitly."""
         v = np.ascontiguousarray(vectors, dtype=np.float32)
         if v.ndim != 2:
             raise ValueError("dense data must be a 2-D array")
+        key = (v.shape, int(metric))
+        if self._vectors is vectors and self._key == key and _frozen(vectors):
+            return
+        fp = fingerprint(v)
+        if self._vectors is not None and self._key == key and self._fp == fp:
+            self._vectors = vectors
+            return
         check(self._lib.knnm_set_dataset(self._h, ptr(v), v.shape[0], v.shape[1], int(metric)),
               "knnm_set_dataset")
         self._vectors = vectors
         self._metric = int(metric)
+        self._key = key
+        self._fp = fp
+
+    def invalidate(self) -> None:
+        """Forget the resident dataset: the next set_dataset uploads."""
+        self._vectors = None
+        self._key = None
+        self._fp = None
 
     # -- merge state -------------------------------------------------------
     def begin(self, union_gids: np.ndarray, labels: np.ndarray, k: int) -> None:
@@ -73,6 +94,7 @@ class Engine:
                 if not (_is_cuda_tensor(t) and t.is_contiguous() and str(t.dtype).endswith(dt)):
                     raise ValueError("device graph arrays must be contiguous CUDA tensors "
                                      "(ids int32, dists float64, sizes int32)")
+            self.wait_torch()  # the tensors may still be in flight on torch's stream
             check(self._lib.knnm_load_graph_dev(
                 self._h, ptr(rows), rows.shape[0], ctypes.c_void_p(gi.data_ptr()),
                 ctypes.c_void_p(gd.data_ptr()), ctypes.c_void_p(gs.data_ptr()), int(graph.k),
@@ -150,6 +172,16 @@ class Engine:
         _pcg_consume(rng, st, int(used.value))
         return bad[: nb.value].copy()
 
+    def draws_insert_range(self, rows: np.ndarray, pool: np.ndarray, r0: int, r1: int) -> int:
+        """draws_insert for draw rows [r0, r1) only (sharded initialisation)."""
+        rows = np.ascontiguousarray(rows, dtype=np.int32)
+        pool = np.ascontiguousarray(pool, dtype=np.int32)
+        acc = ctypes.c_int64()
+        check(self._lib.knnm_draws_insert_range(self._h, ptr(rows), ptr(pool), pool.shape[0],
+                                                int(r0), int(r1), ctypes.byref(acc)),
+              "knnm_draws_insert_range")
+        return int(acc.value)
+
     def draws_insert(self, rows: np.ndarray, pool: np.ndarray) -> int:
         rows = np.ascontiguousarray(rows, dtype=np.int32)
         pool = np.ascontiguousarray(pool, dtype=np.int32)
@@ -212,10 +244,12 @@ class Engine:
             ids = torch.empty((self.n, self.k), dtype=torch.int32, device=dev)
             dists = torch.empty((self.n, self.k), dtype=torch.float64, device=dev)
             sizes = torch.empty(self.n, dtype=torch.int32, device=dev)
+            self.wait_torch()  # fresh allocations: no pending torch reads of them
             check(self._lib.knnm_export_dev(self._h, int(bool(merge_rear)),
                                             ctypes.c_void_p(ids.data_ptr()),
                                             ctypes.c_void_p(dists.data_ptr()),
                                             ctypes.c_void_p(sizes.data_ptr())), "knnm_export_dev")
+            self.signal_torch()  # torch work on the outputs runs after the export
             return ids, dists, sizes
         ids = _host_empty((self.n, self.k), np.int32, self.pinned_outputs)
         dists = _host_empty((self.n, self.k), np.float64, self.pinned_outputs)
@@ -248,6 +282,27 @@ class Engine:
               "knnm_capture_fetch")
         return pa, pb, pd
 
+    def set_cand_budget(self, nbytes: int) -> None:
+        """Candidate-slot budget (bytes; 0 = default 40 GiB).  Rounds whose
+        slots exceed it run in hood chunks (a small value forces that path)."""
+        check(self._lib.knnm_set_cand_budget(self._h, int(nbytes)), "knnm_set_cand_budget")
+
+    def wait_torch(self) -> None:
+        """Order the engine's stream after work queued on torch's current
+        stream of this device (tensors torch produced that the engine reads)."""
+        import torch
+
+        s = torch.cuda.current_stream(self.device)
+        check(self._lib.knnm_wait_stream(self._h, ctypes.c_void_p(s.cuda_stream)), "knnm_wait_stream")
+
+    def signal_torch(self) -> None:
+        """Order torch's current stream after the engine's queued work."""
+        import torch
+
+        s = torch.cuda.current_stream(self.device)
+        check(self._lib.knnm_signal_stream(self._h, ctypes.c_void_p(s.cuda_stream)),
+              "knnm_signal_stream")
+
     def set_join_variant(self, variant: int) -> None:
         """-1 auto, 0 exact fp64 route, 1 tiled fp32-screen route, 2 tensor-core route."""
         check(self._lib.knnm_set_join_variant(self._h, int(variant)), "knnm_set_join_variant")
@@ -266,7 +321,7 @@ class Engine:
     def set_u8(self, on: bool) -> None:
         """Enable/disable the u8 integer tensor-core route (next set_dataset)."""
         check(self._lib.knnm_set_u8(self._h, int(bool(on))), "knnm_set_u8")
-        self._vectors = None
+        self.invalidate()
 
     # -- instrumentation ---------------------------------------------------
     def set_profiling(self, on: bool) -> None:
@@ -364,6 +419,26 @@ def pinned_copy(a: np.ndarray) -> np.ndarray:
     out = t.numpy()
     out[...] = a
     return out
+
+
+def fingerprint(a: np.ndarray) -> int:
+    """Content fingerprint of a C-contiguous host array (knnm_fingerprint)."""
+    a = np.ascontiguousarray(a)
+    out = ctypes.c_uint64()
+    check(_lib.load().knnm_fingerprint(ptr(a), a.nbytes, ctypes.byref(out)), "knnm_fingerprint")
+    return int(out.value)
+
+
+def _frozen(a) -> bool:
+    """True when no writeable array can alias ``a``: it and every base it
+    views are read-only numpy arrays (numpy refuses to make a view of a
+    read-only base writeable)."""
+    x = a
+    while isinstance(x, np.ndarray):
+        if x.flags.writeable:
+            return False
+        x = x.base
+    return x is None
 
 
 def _is_cuda_tensor(x) -> bool:

@@ -337,7 +337,14 @@ def merge_rear(u: KnnGraph, tail: KnnGraph, device: int | None = None) -> KnnGra
     if not np.all(np.isin(tail.member_ids, u.member_ids)):
         raise ValueError("tail vertices must be members of the merged graph")
     if tail.k > u.k:
-        raise ValueError("rear lists wider than the merged capacity are not supported")
+        # rows are sorted by (dist, id): a wider rear list only ever
+        # contributes its first u.k entries to a k-entry merged row
+        # (merge_rear_rows stops at k, _kernels.py:529-563)
+        narrow = KnnGraph(tail.member_ids, u.k, tail.metric)
+        narrow.ids = np.ascontiguousarray(np.asarray(tail.ids)[:, : u.k])
+        narrow.dists = np.ascontiguousarray(np.asarray(tail.dists)[:, : u.k])
+        narrow.sizes = np.minimum(np.asarray(tail.sizes), u.k).astype(np.int32)
+        tail = narrow
     eng = get_engine(device)
     # the engine needs a dataset that covers the member ids; rear merging
     # never reads vectors, so a one-column placeholder is enough

@@ -1,7 +1,8 @@
 """World-size-2 gloo tests (CPU) of the torch.distributed communicator that
 carries the sharded rounds between GPUs (paper_1908_00814_b200/distributed.py):
-uneven all-to-all of slot blocks, in-place all-gather of owned row blocks,
-all-reduce of counters, and the shard bounds."""
+the packed uneven exchange of slot blocks (with the chunk-count header), the
+counter and row-record all-gathers, the in-place all-gather of owned row
+blocks, all-reduce, the shard bounds and the tree's groups."""
 
 import os
 import socket
@@ -27,15 +28,32 @@ def _worker(rank, world, port, q):
         from paper_1908_00814_b200.distributed import TorchComm, shard_bounds
 
         comm = TorchComm()
-        # uneven all-to-all: rank s sends (s+1)*(q+1) elements valued 100*s+q to q
-        sends = [torch.full(((rank + 1) * (d + 1),), 100 * rank + d, dtype=torch.float64)
-                 for d in range(world)]
-        sends[1 % world] = torch.empty(0, dtype=torch.float64) if rank == 0 else sends[1 % world]
-        recv = comm.alltoallv({rank: sends})[rank]
-        ok_a2a = True
+        # uneven exchange of (count, slot, source) parts: rank s sends
+        # (s+1)*(q+1) slots valued 100*s+q to q; rank 0 sends nothing to 1
+        sends = []
+        for dd in range(world):
+            m = 0 if (rank == 0 and dd == 1 % world) else (rank + 1) * (dd + 1)
+            sends.append([torch.full((3,), m, dtype=torch.int32),
+                          torch.full((m,), 100 * rank + dd, dtype=torch.float64),
+                          torch.arange(m, dtype=torch.int32)])
+        recv, mx = comm.exchange({rank: sends}, {rank: 7 + rank})
+        recv = recv[rank]
+        ok_a2a = mx == 7 + world - 1
         for s in range(world):
             exp = 0 if (s == 0 and rank == 1 % world) else (s + 1) * (rank + 1)
-            ok_a2a &= recv[s].numel() == exp and bool(torch.all(recv[s] == 100 * s + rank))
+            cnt, bd, bs = recv[s]
+            ok_a2a &= bool(torch.all(cnt == exp)) and bd.numel() == exp and bs.numel() == exp
+            ok_a2a &= bool(torch.all(bd == 100 * s + rank)) and bool(torch.equal(bs, torch.arange(exp, dtype=torch.int32)))
+        # packed slots: a None part is skipped on both sides
+        recv2, _ = comm.exchange({rank: [[t[0], t[1], None] for t in sends]}, {rank: 0})
+        ok_a2a &= all(p[2] is None for p in recv2[rank])
+        # counters and row records
+        st = comm.allgather_counts({rank: [rank + 1, 10 * rank]})
+        ok_ag = st.tolist() == [[r + 1, 10 * r] for r in range(world)]
+        buf = torch.full(((rank + 1) * 16,), rank, dtype=torch.uint8)
+        rows = comm.allgather_bytes({rank: buf}, st[:, 0], 16)[rank]
+        ok_ag &= all(rows[s].numel() == (s + 1) * 16 and bool(torch.all(rows[s] == s))
+                     for s in range(world))
         # all-gather of owned row blocks into replicated (n, k) arrays
         n, k = 11, 3
         bounds = shard_bounds(n, world)
@@ -43,7 +61,7 @@ def _worker(rank, world, port, q):
         lo, hi = bounds[rank]
         full[lo:hi] = torch.arange(lo * k, hi * k, dtype=torch.int32).reshape(-1, k)
         comm.allgather_blocks({rank: [full]}, bounds)
-        ok_ag = bool(torch.equal(full, torch.arange(n * k, dtype=torch.int32).reshape(n, k)))
+        ok_ag &= bool(torch.equal(full, torch.arange(n * k, dtype=torch.int32).reshape(n, k)))
         ok_ar = comm.allreduce_sum({rank: rank + 5}) == sum(r + 5 for r in range(world))
         q.put((rank, ok_a2a, ok_ag, ok_ar))
     finally:
@@ -76,3 +94,14 @@ def test_shard_bounds_cover_rows():
             assert b[0][0] == 0 and b[-1][1] == n
             assert all(b[i][1] == b[i + 1][0] for i in range(world - 1))
             assert all(hi >= lo for lo, hi in b)
+
+
+def test_tree_groups():
+    from paper_1908_00814_b200.distributed import tree_groups
+
+    g = tree_groups(8)
+    assert [lv for lv, _ in g] == [1, 1, 1, 1, 2, 2, 3]
+    assert g[-1][1] == list(range(8)) and g[0][1] == [0, 1] and g[5][1] == [4, 5, 6, 7]
+    assert tree_groups(1) == []
+    with pytest.raises(ValueError):
+        tree_groups(6)

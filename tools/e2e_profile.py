@@ -20,13 +20,13 @@ for gr in (g, h):
 eng = get_engine()
 p = km.MergeParams(k=20, seed=3)
 for _ in range(2):
-    eng._vectors = None
+    eng.invalidate()
     eng.pinned_outputs = True
     t = time.perf_counter()
     km.s_merge(dsp, g, h, p)
     print("e2e wall", time.perf_counter() - t, flush=True)
 t = time.perf_counter(); eng.set_dataset(dsp.vectors, 1); print("set_dataset", time.perf_counter() - t)
-eng._vectors = None
+eng.invalidate()
 pr = cProfile.Profile()
 pr.enable()
 km.s_merge(dsp, g, h, p)
