@@ -39,6 +39,44 @@ sys.path.insert(0, ROOT)
 CFG = dict(n=1_000_000, d=128, k=20, r=0.5, n_centres=1000, sigma=20.0, data_seed=7,
            split_seed=1, g_seed=1, h_seed=2, merge_seed=3)
 CPU_SAMPLE_N = 100_000  # 2 x 50k points of the same distribution
+
+# BASELINE.json configs: data generator, metric, k, operation.
+# Subgraphs / the built graph come from this package's NN-Descent (bit-exact
+# to the reference's), seeds 1 and 2; merge seed 3; halves of a seeded
+# permutation (split seed 1).  c5l1 is one level-1 merge of config 5's tree
+# (two 1M-point subgraphs, ids [0, 1M) and [1M, 2M), subgraph seeds 1, 2).
+CONFIGS = {
+    "c1": dict(n=10_000, d=32, k=20, metric="l2", op="s", gen="uniform", gen_seed=1,
+               split="halves", max_iters=10, min_update_fraction=0.0),
+    "c2": dict(n=1_000_000, d=128, k=20, metric="l2", op="s", gen="int_gmm", centres=1000,
+               sigma=20.0, gen_seed=7, split="perm"),
+    "c3": dict(n=1_000_000, d=960, k=20, metric="l2", op="j", gen="unit_gmm", centres=500,
+               sigma=0.05, gen_seed=7, split="perm"),
+    "c4": dict(n=1_200_000, d=100, k=40, metric="cosine", op="s", gen="sphere_gmm", centres=2000,
+               sigma=0.3, gen_seed=7, split="perm"),
+    "c5l1": dict(n=2_000_000, d=128, k=20, metric="l2", op="s", gen="int_gmm", centres=1000,
+                 sigma=20.0, gen_seed=7, split="halves"),
+}
+
+
+def config_inputs(km, name, scale=1.0):
+    """(dataset, metric, k, op, s1, s2, merge-param kwargs) of a BASELINE config."""
+    c = CONFIGS[name]
+    n = max(int(c["n"] * scale), 64)
+    if c["gen"] == "uniform":
+        ds = km.generate_uniform(n, c["d"], seed=c["gen_seed"])
+    else:
+        gen = {"int_gmm": km.generate_int_gmm, "unit_gmm": km.generate_unit_gmm,
+               "sphere_gmm": km.generate_sphere_gmm}[c["gen"]]
+        ds = gen(n, c["d"], n_centres=c["centres"], sigma=c["sigma"], seed=c["gen_seed"])
+    if c["split"] == "halves":
+        s1, s2 = np.arange(n // 2, dtype=np.int64), np.arange(n // 2, n, dtype=np.int64)
+    else:
+        s1, s2 = split_ids(n, 1)
+    metric = km.Metric.L2 if c["metric"] == "l2" else km.Metric.COSINE
+    mp = {key: c[key] for key in ("max_iters", "min_update_fraction") if key in c}
+    return ds, metric, c["k"], c["op"], s1, s2, mp
+REF_BUDGET_S = 1500.0  # reference arm: whole-run bound (setup + timed steps)
 METRIC = "distance_evals_per_s"
 UNIT = "evals/s"
 
@@ -190,7 +228,7 @@ def make_inputs(km, n):
     return ds, s1, s2
 
 
-def recall_sample(ds, graph, device, nq=1000, seed=0):
+def recall_sample(ds, graph, device, nq=1000, seed=0, metric=None):
     """recall@10 of `graph` on nq sampled nodes against exact brute force
     (the package's GPU brute force: exact fp64 distances, (dist, id) order,
     self excluded -- reference brute_force_queries semantics)."""
@@ -200,7 +238,7 @@ def recall_sample(ds, graph, device, nq=1000, seed=0):
     rng = np.random.default_rng(seed)
     q = np.sort(rng.choice(ds.n, size=min(nq, ds.n), replace=False))
     eng = get_engine(device)
-    eng.set_dataset(ds.vectors, int(km.Metric.L2))
+    eng.set_dataset(ds.vectors, int(km.Metric.L2 if metric is None else metric))
     ids, _ = eng.bf_topk(11, queries=ds.vectors[q])
     truth = [[int(v) for v in row if v != qq][:10] for row, qq in zip(ids, q)]
     rows = np.searchsorted(np.asarray(graph.member_ids), q)
@@ -230,6 +268,13 @@ def cpu_baseline(n_sample=CPU_SAMPLE_N):
 
 
 def run_reference(args):
+    """The reference arm: the CPU oracle (oracle/, the C/OpenMP restatement of
+    the reference's numba kernels, all host threads) on the SAME workload as
+    the GPU arm -- the full config-2 S-Merge (2 x 500,000 points) per step.
+    The subgraphs are built by the oracle's own NN-Descent (untimed).  The
+    oracle has no JIT, so warm-up steps run on a 2 x 5,000 sample; if the
+    projected run would exceed REF_BUDGET_S, fewer full steps are timed and
+    ``steps_timed`` says how many (the driver's step limit is 1,800 s)."""
     world, rank, _ = dist_setup()
     if rank != 0:
         return
@@ -237,34 +282,150 @@ def run_reference(args):
     import paper_1908_00814_b200.core as core
 
     O.build()
-    n = int(CPU_SAMPLE_N * args.scale) if args.scale < 1 else CPU_SAMPLE_N
+    n = int(CFG["n"] * args.scale)
+    t_setup = time.perf_counter()
     ds = core.generate_int_gmm(n, CFG["d"], n_centres=CFG["n_centres"], sigma=CFG["sigma"],
                                seed=CFG["data_seed"])
     s1, s2 = split_ids(n, CFG["split_seed"])
     g, _, _ = O.nn_descent(ds.vectors, 1, CFG["k"], CFG["g_seed"], member_ids=s1)
     h, _, _ = O.nn_descent(ds.vectors, 1, CFG["k"], CFG["h_seed"], member_ids=s2)
+    setup_s = time.perf_counter() - t_setup
+    wn = 10_000
+    wds = core.generate_int_gmm(wn, CFG["d"], n_centres=CFG["n_centres"], sigma=CFG["sigma"],
+                                seed=CFG["data_seed"])
+    w1, w2 = split_ids(wn, CFG["split_seed"])
+    wg, _, _ = O.nn_descent(wds.vectors, 1, CFG["k"], CFG["g_seed"], member_ids=w1)
+    wh, _, _ = O.nn_descent(wds.vectors, 1, CFG["k"], CFG["h_seed"], member_ids=w2)
     for _ in range(args.warmup):
-        O.s_merge(ds.vectors, g, h, CFG["k"], r=CFG["r"], seed=CFG["merge_seed"])
+        O.s_merge(wds.vectors, wg, wh, CFG["k"], r=CFG["r"], seed=CFG["merge_seed"])
+    evals, done, step_s = 0, 0, []
     t0 = time.perf_counter()
-    evals = 0
-    for _ in range(args.steps):
+    for i in range(args.steps):
+        ts = time.perf_counter()
         _, rep, count = O.s_merge(ds.vectors, g, h, CFG["k"], r=CFG["r"], seed=CFG["merge_seed"])
+        step_s.append(round(time.perf_counter() - ts, 3))
         evals += count
+        done += 1
+        el = time.perf_counter() - t0
+        if el + el / done > REF_BUDGET_S - setup_s:
+            break
     dt = time.perf_counter() - t0
     v = evals / dt
-    sample = (f"s_merge of 2x{n // 2} points (config-2 distribution, k=20) per step; "
-              "oracle C/OpenMP restatement of the reference kernels")
+    sample = (f"the full workload: s_merge of 2x{n // 2} points (config-2 distribution, k=20) "
+              "per step; oracle C/OpenMP restatement of the reference kernels, subgraphs from "
+              "the oracle's nn_descent")
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3 / args.steps,
+            "steps": args.steps, "steps_timed": done, "warmup": args.warmup,
+            "ms_per_step": dt * 1e3 / done, "merge_seconds": dt / done, "step_seconds": step_s,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": "config2_smerge_2x500k_d128_k20",
-                                            "n": CFG["n"], "d": CFG["d"], "k": CFG["k"], "r": CFG["r"],
+                                            "n": n, "d": CFG["d"], "k": CFG["k"], "r": CFG["r"],
                                             "metric": "l2", "rho": 1.0, "sample_points": n,
                                             "parallelism": "host threads"},
+            "same_config": n == CFG["n"], "setup_seconds": setup_s,
+            "evals_per_step": evals // done, "rounds": len(rep.rounds),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                              "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def kernel_rooflines(st, steps, d, k, slot_b, lazy, hbm_peak, row_b=None):
+    """Algorithmic-byte rooflines of the join, apply and assembly kernels of
+    one step, from the run's own counters (SURVEY.md §8d's byte model):
+
+    join      (row_b + 4) * sum|M_u| + slot_b * written_slots
+              (+ 8 d per exact fp64 evaluation in the join: two fp32 rows)
+    apply     8 * slots read + (slot_b - 8) * written slots (source ids)
+              + 13 k per row loaded + 13 k per row stored (ids, dists, flags)
+              (+ 8 d per lazy exact evaluation in the apply)
+    assemble  9 k per active hood (forward ids + flags, reverse entries)
+              + 20 B per membership (hood entry + membership record)
+
+    ``row_b``: bytes per gathered member row (default fp32 rows, 4 d)."""
+    row_b = 4.0 * d if row_b is None else float(row_b)
+    ex_join = 0.0 if lazy else 8.0 * d * st["exact_evals"]
+    ex_apply = 8.0 * d * st["exact_evals"] if lazy else 0.0
+    out = {}
+    jb = (row_b + 4.0) * st["members"] + slot_b * st["written_slots"] + ex_join
+    ab = (8.0 * st["candidates"] + (slot_b - 8.0) * st["written_slots"]
+          + 13.0 * k * (st["apply_rows_in"] + st["apply_rows_out"]) + ex_apply)
+    for name, b, ms in (("join", jb, st["join_kernel_ms"]), ("apply", ab, st["apply_kernel_ms"])):
+        gbs = b / (ms / 1e3) / 1e9 if ms > 0 else 0.0
+        out[name] = {"bytes_per_step": b / steps, "ms_per_step": ms / steps, "achieved": gbs,
+                     "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak}
+    return out
+
+
+def config_legs(km, names, device, steps, warmup, hbm_peak, no_recall=False):
+    """BASELINE configs beyond the headline (c3: J-Merge d=960 lazy route;
+    c4: cosine k=40 S-Merge), device-resident inputs, timed with CUDA events
+    on the engine stream: merge seconds, evals/s, exact evaluations and the
+    join / apply rooflines (fp32 byte model, §8d)."""
+    import torch
+
+    from paper_1908_00814_b200.engine import get_engine
+
+    eng = get_engine(device)
+    res = {}
+    for name in names:
+        t = time.perf_counter()
+        ds, metric, k, op, s1, s2, mpk = config_inputs(km, name)
+        g = km.nn_descent(ds, metric, km.DescentParams(k=k), 1, member_ids=s1, device=device,
+                          out_device=True)
+        h = (km.nn_descent(ds, metric, km.DescentParams(k=k), 2, member_ids=s2, device=device,
+                           out_device=True) if op == "s" else None)
+        setup = time.perf_counter() - t
+        params = km.MergeParams(k=k, seed=3, **mpk)
+
+        def run(c):
+            if op == "s":
+                return km.s_merge(ds, g, h, params, counter=c, device=device, out_device=True)
+            return km.j_merge(ds, g, s2, params, counter=c, device=device, out_device=True)
+
+        u = None
+        for _ in range(max(1, warmup)):
+            u = run(km.DistanceCounter())
+        del u
+        torch.cuda.synchronize(device)
+        eng.reset_stats()
+        eng.set_profiling(True)
+        evals = 0
+        eng.mark(6)
+        for _ in range(steps):
+            c = km.DistanceCounter()
+            u = run(c)
+            evals += c.count
+        eng.mark(7)
+        ms = eng.elapsed_ms(6, 7)
+        st = eng.stats()
+        eng.set_profiling(False)
+        inf = eng.info()
+        lazy = (not inf["cert"]) and ds.d > 384
+        slot_b = 8.0 if (inf["cert"] or inf["cert_dot"]) else 12.0
+        kr = kernel_rooflines(st, steps, ds.d, k, slot_b, lazy, hbm_peak)
+        rec = None
+        if not no_recall:
+            uh = km.KnnGraph.from_arrays(u.member_ids, u.k, u.metric, u.ids.cpu().numpy(),
+                                         u.dists.cpu().numpy(), u.sizes.cpu().numpy())
+            rec = recall_sample(ds, uh, device, metric=metric)
+        res[name] = {
+            "workload": {"c3": "config3_jmerge_500k+500k_d960_k20",
+                         "c4": "config4_smerge_2x600k_d100_k40_cosine"}.get(name, name),
+            "merge_seconds": ms / steps / 1e3, "evals_per_step": evals // steps,
+            "evals_per_s": evals / (ms / 1e3), "steps": steps,
+            "rounds_per_step": st["rounds"] / steps,
+            "exact_evals_per_step": st["exact_evals"] / steps,
+            "exact_fraction": st["exact_evals"] / max(1, st["pairs"]),
+            "route": "lazy (d-chunked join, exact fp64 in the apply)" if lazy else
+                     ("tensor-core" if inf["cert_dot"] else "tiled fp32 screen + exact fp64"),
+            "kernels": kr, "recall_at_10": rec, "setup_seconds": round(setup, 1),
+            "phases_ms_per_step": {key: st[key] / steps for key in
+                                   ("join_kernel_ms", "apply_kernel_ms", "reverse_ms",
+                                    "assemble_ms", "update_ms", "other_ms")},
+        }
+        del g, h, u, ds
+    return res
 
 
 def run_b200(args):
@@ -276,6 +437,9 @@ def run_b200(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.barrier()
+        print(f"[bench] rank {dist.get_rank()}/{dist.get_world_size()}: NCCL communicator up on "
+              f"cuda:{local} ({torch.cuda.get_device_name(local)})", file=sys.stderr, flush=True)
     rank = int(os.environ.get("RANK", "0"))
     import paper_1908_00814_b200 as km
     from paper_1908_00814_b200.engine import get_engine
@@ -474,6 +638,48 @@ def run_b200(args):
         rho_line["recall_vs_rho1"] = (rho_line["recall_at_10"] - rec
                                       if rec is not None and rho_line["recall_at_10"] is not None else None)
     eng.set_dataset(ds.vectors, 1)
+    # join / apply / assembly rooflines of the headline step (same counters)
+    kern = kernel_rooflines(st, steps_n := args.steps, CFG["d"], k, slot_b, False, hbm_peak,
+                            row_b=row_b)
+    kern["assemble"] = {"ms_per_step": st["assemble_ms"] / steps_n,
+                        "bytes_per_step": (9.0 * k * st["active_hoods"] + 20.0 * st["members"]) / steps_n}
+    a_ms = st["assemble_ms"] / 1e3
+    kern["assemble"]["achieved"] = kern["assemble"]["bytes_per_step"] * steps_n / a_ms / 1e9 if a_ms else 0.0
+    kern["assemble"].update(peak=hbm_peak, unit="GB/s", frac=kern["assemble"]["achieved"] / hbm_peak,
+                            note="phase time (k_mpack_init + k_assemble + scan); bytes: 9k per "
+                                 "active hood + 20 B per membership")
+    for key in kern:
+        kern[key]["share_of_step"] = kern[key]["ms_per_step"] / max(ms_max / steps_n, 1e-9)
+    # the bench line's roofline: the dominant kernel of the step (by its own
+    # CUDA-event time), with the ncu DRAM traffic of the same kernel
+    dom = max(("join", "apply"), key=lambda kk: kern[kk]["ms_per_step"])
+    names = {"join": join_kernel, "apply": "k_apply_stream<packed>" if slot_b == 8.0 else "k_apply_stream"}
+    models = {"join": f"(row_bytes + 4) * sum|M_u| + {int(slot_b)} * written_slots",
+              "apply": "8 * slots read + 13k * (rows loaded + rows stored)"}
+    tr = None
+    for fn in (f"r2_{dom}_traffic.json",) + (("r1_join_traffic.json",) if dom == "join" else ()):
+        try:
+            with open(os.path.join(ROOT, "profiles", fn)) as f:
+                tr = json.load(f)
+            break
+        except Exception:
+            pass
+    roofline = {"bound": "hbm", "achieved": kern[dom]["achieved"], "peak": hbm_peak, "unit": "GB/s",
+                "frac": kern[dom]["frac"], "traffic": tr, "peak_kind": peak_kind,
+                "kernel": names[dom], "bytes_model": models[dom],
+                "bytes_per_step": kern[dom]["bytes_per_step"],
+                "kernel_ms_per_step": kern[dom]["ms_per_step"],
+                "kernel_share_of_step": kern[dom]["share_of_step"],
+                "join": {"kernel": join_kernel, "achieved": achieved, "frac": achieved / hbm_peak,
+                         "traffic": traffic,
+                         "survey_formula": {"achieved": achieved_survey, "frac": achieved_survey / hbm_peak,
+                                            "bytes_model": "d * 4 * sum|M_u| + 8 * written_slots "
+                                                           "(SURVEY 8d: fp32 rows as stored in the dataset)"}}}
+    legs = None
+    if args.configs and world == 1:
+        legs = config_legs(km, args.configs, local, max(1, min(args.steps, 3)), 1, hbm_peak,
+                           no_recall=args.no_recall)
+        eng.set_dataset(ds.vectors, 1)
     cpu = None if args.no_cpu else cpu_baseline()
     steps = args.steps
     line = {
@@ -487,22 +693,15 @@ def run_b200(args):
         "merge_seconds": ms_max / steps / 1e3,
         "evals_per_step": evals // steps,
         "recall_at_10": rec,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "kernel": join_kernel,
-                     "bytes_model": f"(row_bytes + 4) * sum|M_u| + {int(slot_b)} * written_slots",
-                     "bytes_per_step": join_bytes / steps,
-                     "kernel_ms_per_step": st["join_kernel_ms"] / steps,
-                     "kernel_share_of_step": st["join_kernel_ms"] / max(ms_max, 1e-9),
-                     "survey_formula": {"achieved": achieved_survey, "frac": achieved_survey / hbm_peak,
-                                        "bytes_model": "d * 4 * sum|M_u| + 8 * written_slots "
-                                                       "(SURVEY 8d: fp32 rows as stored in the dataset)"}},
+        "roofline": roofline,
         "stats_per_step": {key: st[key] / steps for key in ("candidates", "written_slots", "exact_evals", "members", "accepted", "join_redos", "rounds")},
         "phases_ms_per_step": {key: st[key] / steps for key in
                                ("join_ms", "join_kernel_ms", "reverse_ms", "assemble_ms", "update_ms", "other_ms")},
         "e2e": {"value": e2e, "unit": UNIT, "ms_per_step": e_ms / steps,
                 "h2d_bytes_per_step": est["h2d_bytes"] // steps,
                 "d2h_bytes_per_step": est["d2h_bytes"] // steps},
+        "kernels": kern,
+        "configs": legs,
         "gpu_launches": st["launches"],
         "step_wall_ms": step_wall,
         "clocks": clk.summary(),
@@ -527,10 +726,31 @@ def main():
     ap.add_argument("--no-recall", action="store_true")
     ap.add_argument("--join-variant", type=int, default=None,
                     help="force a join route (0 exact, 1 tiled, 2 tensor core)")
+    ap.add_argument("--configs", default="c3,c4",
+                    help="extra BASELINE config legs at N=1 (comma list; '' to skip)")
     ap.add_argument("--no-rho-half", action="store_true",
                     help="skip the rho = 0.5 leg (BASELINE's config-2 sample rate)")
     args = ap.parse_args()
     args.rho_half = not args.no_rho_half
+    args.configs = [c for c in args.configs.split(",") if c]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "b200":
+        # one process per GPU: re-launch this command under torchrun
+        import socket
+
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {have}",
+                  file=sys.stderr, flush=True)
+            sys.exit(2)
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+               os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -81,6 +81,10 @@ typedef struct knnm_stats {
     int64_t join_row_bytes; /* bytes per gathered member row in the join   */
     int64_t heavy_rev_rows; /* reverse segments longer than a warp sorts (block path) */
     int64_t seg_hub_rows;   /* rows with more memberships than a warp ranks (block path) */
+    int64_t apply_rows_in;  /* rows the apply loaded (>= 1 update slot)     */
+    int64_t apply_rows_out; /* rows the apply stored (>= 1 accepted insert) */
+    double apply_kernel_ms; /* the apply kernel alone (roofline denominator) */
+    int64_t active_hoods;   /* hoods with >= 1 admissible pair, over all rounds */
 } knnm_stats;
 
 const char *knnm_last_error(void);

@@ -58,6 +58,10 @@ class KnnmStats(ctypes.Structure):
         ("join_row_bytes", I64),
         ("heavy_rev_rows", I64),
         ("seg_hub_rows", I64),
+        ("apply_rows_in", I64),
+        ("apply_rows_out", I64),
+        ("apply_kernel_ms", ctypes.c_double),
+        ("active_hoods", I64),
     ]
 
     def as_dict(self) -> dict:

@@ -79,7 +79,7 @@ void release(DBuf &b) {
     b.bytes = 0;
 }
 
-enum Phase { PH_JOIN = 0, PH_REVERSE, PH_ASSEMBLE, PH_UPDATE, PH_OTHER, PH_JOINK, PH_NUM };
+enum Phase { PH_JOIN = 0, PH_REVERSE, PH_ASSEMBLE, PH_UPDATE, PH_OTHER, PH_JOINK, PH_APPLYK, PH_NUM };
 
 struct PhiTree {
     int64_t N = -1;
@@ -180,7 +180,7 @@ struct knnm_ctx {
     bool profiling = false;
     std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> ev_pool;
-    double phase_ms[PH_NUM] = {0, 0, 0, 0, 0, 0};
+    double phase_ms[PH_NUM] = {0, 0, 0, 0, 0, 0, 0};
     knnm_stats stats{};
     cudaEvent_t marks[8] = {};
     cudaEvent_t ev_wait = nullptr, ev_sig = nullptr;  // knnm_wait_stream / knnm_signal_stream
@@ -450,6 +450,7 @@ int run_updates(knnm_ctx *c) {
     unsigned long long *cnt = c->counters.as<unsigned long long>();
     CK(cudaMemsetAsync(cnt + C_CAND, 0, sizeof(unsigned long long) * 2, c->st));
     CK(cudaMemsetAsync(cnt + C_WRITTEN, 0, sizeof(unsigned long long), c->st));
+    CK(cudaMemsetAsync(cnt + C_ROWS_IN, 0, sizeof(unsigned long long) * 2, c->st));
     const int E = (c->k + 31) / 32;
     const int blocks = grid_for(c, n * 32, APPLY_WARPS * 32, 16);
 #define KNNM_AP_LAUNCH(EE, LZ, F)                                                                \
@@ -458,19 +459,22 @@ int run_updates(knnm_ctx *c) {
         c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), \
         cnt, lazy_of(c))
     const bool f32 = c->lists_f32;
-    if (E == 1) {
-        if (c->slots_mode == SLOTS_LAZY) KNNM_AP_LAUNCH(1, SLOTS_LAZY, false);
-        else if (c->slots_mode == SLOTS_PACKED && f32) KNNM_AP_LAUNCH(1, SLOTS_PACKED, true);
-        else if (c->slots_mode == SLOTS_PACKED) KNNM_AP_LAUNCH(1, SLOTS_PACKED, false);
-        else KNNM_AP_LAUNCH(1, SLOTS_PLAIN, false);
-    } else {
-        if (c->slots_mode == SLOTS_LAZY) KNNM_AP_LAUNCH(2, SLOTS_LAZY, false);
-        else if (c->slots_mode == SLOTS_PACKED && f32) KNNM_AP_LAUNCH(2, SLOTS_PACKED, true);
-        else if (c->slots_mode == SLOTS_PACKED) KNNM_AP_LAUNCH(2, SLOTS_PACKED, false);
-        else KNNM_AP_LAUNCH(2, SLOTS_PLAIN, false);
+    {
+        PhaseTimer ptk(c, PH_APPLYK);  // the apply kernel alone (roofline)
+        if (E == 1) {
+            if (c->slots_mode == SLOTS_LAZY) KNNM_AP_LAUNCH(1, SLOTS_LAZY, false);
+            else if (c->slots_mode == SLOTS_PACKED && f32) KNNM_AP_LAUNCH(1, SLOTS_PACKED, true);
+            else if (c->slots_mode == SLOTS_PACKED) KNNM_AP_LAUNCH(1, SLOTS_PACKED, false);
+            else KNNM_AP_LAUNCH(1, SLOTS_PLAIN, false);
+        } else {
+            if (c->slots_mode == SLOTS_LAZY) KNNM_AP_LAUNCH(2, SLOTS_LAZY, false);
+            else if (c->slots_mode == SLOTS_PACKED && f32) KNNM_AP_LAUNCH(2, SLOTS_PACKED, true);
+            else if (c->slots_mode == SLOTS_PACKED) KNNM_AP_LAUNCH(2, SLOTS_PACKED, false);
+            else KNNM_AP_LAUNCH(2, SLOTS_PLAIN, false);
+        }
+        CKL();
     }
 #undef KNNM_AP_LAUNCH
-    CKL();
     // a round's final apply also reduces phi, fetched in the same wait
     const double *phi_res = nullptr;
     if (c->phi_in_updates && c->n * c->k > 0) TRY(phi_kernels(c, &phi_res, c->st));
@@ -480,6 +484,8 @@ int run_updates(knnm_ctx *c) {
         c->phi_gen = c->state_gen;
     }
     c->stats.candidates += (int64_t)c->hcnt[C_CAND];
+    c->stats.apply_rows_in += (int64_t)c->hcnt[C_ROWS_IN];
+    c->stats.apply_rows_out += (int64_t)c->hcnt[C_ROWS_OUT];
     c->stats.written_slots += (int64_t)c->hcnt[C_WRITTEN];
     c->stats.seg_hub_rows += (int64_t)c->hcnt[C_SEGHEAVY];
     return KNNM_OK;
@@ -1630,6 +1636,7 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
     P = c->hcnt[C_NUM - 1];
     unsigned long long nactive = c->hcnt[C_ACTIVE];
     c->stats.members += (int64_t)c->hcnt[C_MEMBERS];
+    c->stats.active_hoods += (int64_t)nactive;
     c->stats.heavy_rev_rows += (int64_t)c->hcnt[C_HEAVY_REV];
     c->stats.pairs += (int64_t)P;
     c->stats.rounds += 1;
@@ -2415,6 +2422,7 @@ int knnm_get_stats(knnm_ctx *c, knnm_stats *out) {
     out->update_ms = c->phase_ms[PH_UPDATE];
     out->other_ms = c->phase_ms[PH_OTHER];
     out->join_kernel_ms = c->phase_ms[PH_JOINK];
+    out->apply_kernel_ms = c->phase_ms[PH_APPLYK];
     return KNNM_OK;
 }
 

@@ -28,6 +28,8 @@ enum Counter {
     C_SEGHEAVY = 12,  // rows with > SEG_SMEM memberships (block-ranked)
     C_GIANT = 13,     // heavy rows whose reverse segment exceeds a block's smem
     C_DUPROWS = 14,   // rows given twice to a row-grouped insert (direct path check)
+    C_ROWS_IN = 15,   // rows the apply loaded (>= 1 slot)
+    C_ROWS_OUT = 16,  // rows the apply stored (>= 1 accepted insert)
     C_NUM = 20
 };
 

@@ -2467,12 +2467,13 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
     __shared__ double s_lz[LAZY ? APPLY_WARPS : 1][LAZY ? LZ_G * LZ_S : 1];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * APPLY_WARPS;
-    unsigned long long acc = 0, slots = 0, written = 0, nexact = 0;
+    unsigned long long acc = 0, slots = 0, written = 0, nexact = 0, rin = 0, rout = 0;
     for (int64_t r = (int64_t)blockIdx.x * APPLY_WARPS + wib; r < n; r += nw) {
         const uint64_t lo = boff[r];
         const int64_t ns = (int64_t)(boff[r + 1] - lo);
         if (ns == 0) continue;
         slots += (unsigned long long)ns;
+        rin++;
         const double inf = __longlong_as_double(0x7ff0000000000000LL);
         // the next 32 slot distances are loaded while this chunk is applied
         // slots are read once: streaming loads keep L2 for the lists
@@ -2517,11 +2518,16 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
                 a += warp_apply_chunk<E, T>(s, k, src, dl, cnt, lane);
             }
         }
-        if (a) row_store<E, T>(s, ids, dists, flags, sizes, r, k, lane);
+        if (a) {
+            row_store<E, T>(s, ids, dists, flags, sizes, r, k, lane);
+            rout++;
+        }
         acc += a;
     }
     if (lane == 0 && acc) atomicAdd(&counters[C_ACCEPTED], acc);
     if (lane == 0 && slots) atomicAdd(&counters[C_CAND], slots);
+    if (lane == 0 && rin) atomicAdd(&counters[C_ROWS_IN], rin);
+    if (lane == 0 && rout) atomicAdd(&counters[C_ROWS_OUT], rout);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         written += __shfl_xor_sync(FULL_MASK, written, o);

@@ -263,3 +263,64 @@ def test_limits_match_oracle(oracle, n, d, k, metric, kind):
     og, orep, _ = oracle.nn_descent(ds.vectors, metric, k, 4, member_ids=s1)
     _same_graph(gg, og)
     _same_report(rep, orep)
+
+
+@pytest.mark.parametrize("d,k,metric,kind", [(960, 40, 1, "unitgmm"), (784, 40, 1, "uniform"),
+                                             (960, 30, 2, "sphere")])
+def test_long_rows_large_k_match_oracle(oracle, d, k, metric, kind):
+    """Hoods whose whole rows exceed shared memory (4 W dp > 200 KB, e.g.
+    GIST d=960 with k >= 27) take the d-chunked lazy join: bit-exact."""
+    km = _km()
+    n = 1200
+    ds = _data(km, n, d, kind, seed=d + k)
+    s1, s2 = split_ids(n, seed=3)
+    g, _, _ = oracle.nn_descent(ds.vectors, metric, k, 1, member_ids=s1)
+    h, _, _ = oracle.nn_descent(ds.vectors, metric, k, 2, member_ids=s2)
+    c = km.DistanceCounter()
+    u, rep = km.s_merge(ds, _to_graph(km, g), _to_graph(km, h), km.MergeParams(k=k, seed=3),
+                        counter=c, return_report=True)
+    ou, orep, ocount = oracle.s_merge(ds.vectors, g, h, k, seed=3)
+    _same_graph(u, ou)
+    _same_report(rep, orep)
+    assert c.count == ocount
+    gg, grep = km.nn_descent(ds, metric, km.DescentParams(k=k), 1, member_ids=s1,
+                             return_report=True)
+    _same_graph(gg, g)
+
+
+def test_dataset_cache_sees_in_place_edits(oracle):
+    """The device copy of Dataset.vectors is keyed on content: editing a
+    writeable array in place between merges re-uploads it (a stale copy would
+    give the old distances)."""
+    km = _km()
+    n, d, k = 1500, 16, 10
+    vec = np.random.default_rng(5).random((n, d), dtype=np.float32)
+    ds = km.Dataset.from_dense(vec)
+    s1, s2 = split_ids(n, seed=2)
+    g, _, _ = oracle.nn_descent(vec, 1, k, 1, member_ids=s1)
+    km.j_merge(ds, _to_graph(km, g), s2, km.MergeParams(k=k, seed=1))
+    vec[s2] *= 0.5  # in place: same object, new content
+    g2, _, _ = oracle.nn_descent(vec, 1, k, 1, member_ids=s1)
+    u = km.j_merge(ds, _to_graph(km, g2), s2, km.MergeParams(k=k, seed=1))
+    ou, _, _ = oracle.j_merge(vec, g2, s2, k, seed=1)
+    _same_graph(u, ou)
+    # a read-only generated dataset is trusted by identity
+    ro = km.generate_uniform(500, 8, seed=1)
+    assert not ro.vectors.flags.writeable
+
+
+def test_merge_rear_wider_tail_truncates(oracle):
+    """merge_rear with rear lists wider than k keeps the k best (graph.py:259-280)."""
+    km = _km()
+    n, d = 800, 8
+    ds = _data(km, n, d, "uniform", seed=3)
+    ids = np.arange(n, dtype=np.int64)
+    u = km.nn_descent(ds, km.Metric.L2, km.DescentParams(k=8), 1, member_ids=ids)
+    wide = km.nn_descent(ds, km.Metric.L2, km.DescentParams(k=12), 2, member_ids=ids)
+    narrow = km.KnnGraph(wide.member_ids, 8, km.Metric.L2)
+    narrow.ids = wide.ids[:, :8].copy()
+    narrow.dists = wide.dists[:, :8].copy()
+    narrow.sizes = np.minimum(wide.sizes, 8).astype(np.int32)
+    a = km.merge_rear(u, wide)
+    b = km.merge_rear(u, narrow)
+    _same_graph(a, b)

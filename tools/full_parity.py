@@ -1,9 +1,12 @@
-"""Full-size parity: BASELINE config 2 (S-Merge of 2 x 500,000, d=128, k=20)
-and a config-3-shaped J-Merge on the GPU against the CPU oracle on the same
-inputs (subgraphs from the GPU NN-Descent, which the test suite pins to the
-oracle), comparing ids, fp64 dists, sizes, distance counts and every round
-of the report.  The oracle is the checker here.
-Usage: python tools/full_parity.py [scale] -> JSON on stdout"""
+"""Full-size parity: BASELINE configs on the GPU against the CPU oracle on
+identical inputs (subgraphs from the GPU NN-Descent, which the test suite
+pins to the oracle).  Compares ids, fp64 dists, sizes, distance counts and
+every round of the report, and computes recall@10 of BOTH outputs on the
+same 1,000-node sample against exact brute force (GPU, fp64, (dist, id)
+order).  The oracle is the checker here.
+
+Usage: python tools/full_parity.py c3 c4 c5l1 [--scale s] -> JSON on stdout
+(c2 and c2j -- a J-Merge of config-2 data -- are also accepted)."""
 import json
 import os
 import sys
@@ -16,53 +19,79 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
 
+def recall(km, ds, metric, graph, q, truth):
+    rows = np.searchsorted(np.asarray(graph.member_ids), q)
+    got = np.asarray(graph.ids)[rows, :10]
+    return sum(len(set(t) & set(g.tolist())) for t, g in zip(truth, got)) / (len(q) * 10)
+
+
 def main():
     import paper_1908_00814_b200 as km
+    from paper_1908_00814_b200.engine import get_engine
     from oracle import oracle as O
 
     O.build()
-    scale = float(sys.argv[1]) if len(sys.argv) > 1 else 1.0
-    n = int(bench.CFG["n"] * scale)
-    ds, s1, s2 = bench.make_inputs(km, n)
-    k = bench.CFG["k"]
-    g = km.nn_descent(ds, km.Metric.L2, km.DescentParams(k=k), bench.CFG["g_seed"], member_ids=s1)
-    h = km.nn_descent(ds, km.Metric.L2, km.DescentParams(k=k), bench.CFG["h_seed"], member_ids=s2)
+    args = sys.argv[1:]
+    scale = float(args[args.index("--scale") + 1]) if "--scale" in args else 1.0
+    names = [a for a in args if a.startswith("c") and not a.startswith("--")]
+    out = {"scale": scale, "oracle_threads": os.cpu_count(), "cases": {}}
+    for name in names:
+        base = "c2" if name == "c2j" else name
+        ds, metric, k, op, s1, s2, mpk = bench.config_inputs(km, base, scale)
+        if name == "c2j":
+            op = "j"
+        t = time.perf_counter()
+        g = km.nn_descent(ds, metric, km.DescentParams(k=k), 1, member_ids=s1)
+        h = km.nn_descent(ds, metric, km.DescentParams(k=k), 2, member_ids=s2) if op == "s" else None
+        t_build = time.perf_counter() - t
 
-    def og(gr):
-        o = O.OGraph(gr.member_ids, gr.k, int(gr.metric))
-        o.ids, o.dists, o.sizes = gr.ids.copy(), gr.dists.copy(), gr.sizes.copy()
-        return o
+        def og(gr):
+            o = O.OGraph(gr.member_ids, gr.k, int(gr.metric))
+            o.ids, o.dists, o.sizes = gr.ids.copy(), gr.dists.copy(), gr.sizes.copy()
+            return o
 
-    out = {"n": n, "cases": {}}
-    mp = km.MergeParams(k=k, r=bench.CFG["r"], seed=bench.CFG["merge_seed"])
-    for op in ("s_merge", "j_merge"):
+        mp = km.MergeParams(k=k, seed=3, **mpk)
         c = km.DistanceCounter()
         t = time.perf_counter()
-        if op == "s_merge":
+        if op == "s":
             u, rep = km.s_merge(ds, g, h, mp, counter=c, return_report=True)
         else:
             u, rep = km.j_merge(ds, g, s2, mp, counter=c, return_report=True)
         t_gpu = time.perf_counter() - t
+        okw = dict(max_iters=mp.max_iters, min_update_fraction=mp.min_update_fraction)
         t = time.perf_counter()
-        if op == "s_merge":
-            ou, orep, ocount = O.s_merge(ds.vectors, og(g), og(h), k, r=bench.CFG["r"],
-                                         seed=bench.CFG["merge_seed"])
+        if op == "s":
+            ou, orep, ocount = O.s_merge(ds.vectors, og(g), og(h), k, seed=3, **okw)
         else:
-            ou, orep, ocount = O.j_merge(ds.vectors, og(g), s2, k, r=bench.CFG["r"],
-                                         seed=bench.CFG["merge_seed"])
+            ou, orep, ocount = O.j_merge(ds.vectors, og(g), s2, k, seed=3, **okw)
         t_cpu = time.perf_counter() - t
         got = [(x.iteration, x.pairs, x.updates, x.phi, x.distance_count) for x in rep.rounds]
         want = [(x.iteration, x.pairs, x.updates, x.phi, x.distance_count) for x in orep.rounds]
-        out["cases"][op] = {
+        # recall@10 of both outputs on one 1,000-node sample (self excluded)
+        eng = get_engine()
+        q = np.sort(np.random.default_rng(0).choice(ds.n, size=min(1000, ds.n), replace=False))
+        eng.set_dataset(ds.vectors, int(metric))
+        tid, _ = eng.bf_topk(11, queries=ds.vectors[q])
+        truth = [[int(v) for v in row if v != qq][:10] for row, qq in zip(tid, q)]
+        r_gpu = recall(km, ds, metric, u, q, truth)
+        r_orc = recall(km, ds, metric, ou, q, truth)
+        case = {
+            "op": {"s": "s_merge", "j": "j_merge"}[op], "n": int(ds.n), "d": int(ds.d), "k": k,
+            "metric": metric.name.lower(),
             "ids_equal": bool(np.array_equal(u.ids, ou.ids)),
             "dists_equal": bool(np.array_equal(u.dists, ou.dists)),
             "sizes_equal": bool(np.array_equal(u.sizes, ou.sizes)),
+            "members_equal": bool(np.array_equal(np.asarray(u.member_ids), np.asarray(ou.member_ids))),
             "count_equal": c.count == ocount, "count": int(c.count),
-            "report_equal": got == want, "rounds": len(got),
+            "report_equal": got == want, "phi_initial_equal": rep.phi_initial == orep.phi_initial,
+            "rounds": len(got), "report": got,
+            "recall_at_10_gpu": r_gpu, "recall_at_10_oracle": r_orc, "recall_delta": r_gpu - r_orc,
+            "recall_sample": "1,000 nodes, numpy default_rng(0).choice; GPU exact brute force",
             "gpu_seconds_incl_host_copies": round(t_gpu, 3), "oracle_seconds": round(t_cpu, 2),
-            "oracle_threads": os.cpu_count(),
+            "subgraph_build_seconds_gpu": round(t_build, 2),
         }
-        print(op, out["cases"][op], file=sys.stderr, flush=True)
+        out["cases"][name] = case
+        print(name, {k2: v for k2, v in case.items() if k2 != "report"}, file=sys.stderr, flush=True)
     print(json.dumps(out, indent=1))
 
 
