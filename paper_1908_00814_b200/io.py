@@ -112,3 +112,81 @@ def save_member_ids(path, member_ids) -> None:
 
 def load_member_ids(path) -> np.ndarray:
     return read_ivecs(path).reshape(-1).astype(np.int64)
+
+
+# -- hierarchy directories (reference io.py:201-271) --------------------------
+# One directory per hierarchy: per layer ``layer_<t>.knng`` (graph),
+# ``layer_<t>.ids.ivecs`` (ascending member ids) and, when a diversified
+# adjacency exists, ``layer_<t>.kadj`` (not produced on this path), plus a
+# ``manifest.json`` naming them -- the same names and JSON layout as the
+# reference, so either package reads the other's directories.
+
+
+def _layer_files(t: int) -> dict:
+    return {"graph": f"layer_{t}.knng", "ids": f"layer_{t}.ids.ivecs", "adjacency": f"layer_{t}.kadj"}
+
+
+def save_hierarchy_layer(directory, hierarchy, index: int) -> None:
+    """Write layer ``index``'s member ids and (if held) its graph; the
+    layer's ``path`` then points at the graph file."""
+    import os
+
+    os.makedirs(directory, exist_ok=True)
+    layer = hierarchy.layers[index]
+    files = _layer_files(index)
+    save_member_ids(os.path.join(directory, files["ids"]), layer.member_ids)
+    if layer.graph is not None:
+        layer.path = os.path.join(directory, files["graph"])
+        save_graph(layer.path, layer.graph)
+    if layer.adjacency is not None:
+        raise ValueError("diversified adjacency layers are not supported on the merge path")
+
+
+def save_hierarchy_manifest(directory, hierarchy) -> None:
+    import json
+    import os
+
+    os.makedirs(directory, exist_ok=True)
+    entries = []
+    for t, layer in enumerate(hierarchy.layers):
+        files = _layer_files(t)
+        entries.append({"size": int(layer.size), "ids": files["ids"], "graph": files["graph"],
+                        "adjacency": files["adjacency"] if layer.adjacency is not None else None})
+    manifest = {"k": int(hierarchy.k), "metric": Metric(hierarchy.metric).name,
+                "layer_sizes": [int(s) for s in hierarchy.layer_sizes], "layers": entries}
+    with open(os.path.join(directory, "manifest.json"), "w") as fh:
+        json.dump(manifest, fh, indent=2)
+
+
+def save_hierarchy(directory, hierarchy) -> None:
+    """Write every layer, reading dropped ones back from their files first."""
+    for t, layer in enumerate(hierarchy.layers):
+        dropped = layer.graph is None and layer.path is not None
+        if dropped:
+            layer.graph = hierarchy.layer_graph(t)
+        save_hierarchy_layer(directory, hierarchy, t)
+        if dropped:
+            layer.graph = None
+    save_hierarchy_manifest(directory, hierarchy)
+
+
+def load_hierarchy(directory, lazy: bool = True):
+    """A ``Hierarchy`` from a manifest directory; with ``lazy`` the graphs
+    stay on disk until ``Hierarchy.layer_graph`` asks for them."""
+    import json
+    import os
+
+    from .hierarchy import Hierarchy, HierarchyLayer
+
+    with open(os.path.join(directory, "manifest.json")) as fh:
+        manifest = json.load(fh)
+    out = Hierarchy(layers=[], k=int(manifest["k"]), metric=Metric.from_name(manifest["metric"]))
+    for entry in manifest["layers"]:
+        layer = HierarchyLayer(member_ids=load_member_ids(os.path.join(directory, entry["ids"])))
+        gpath = os.path.join(directory, entry["graph"])
+        if os.path.exists(gpath):
+            layer.path = gpath
+            if not lazy:
+                layer.graph = load_graph(gpath, member_ids=layer.member_ids)
+        out.layers.append(layer)
+    return out

@@ -169,6 +169,16 @@ def extra():
                          layer_sizes=hier.layer_sizes,
                          layers=[h_graph(l.graph.ids, l.graph.dists, l.graph.sizes) for l in hier.layers],
                          reports=[[name, report_dict(r)] for name, r in reps])
+    # the same build with layer snapshots on disk: every file's hash
+    # (reference merge.py:457-467 _maybe_snapshot, io.py:201-248)
+    import hashlib
+    import tempfile
+
+    with tempfile.TemporaryDirectory() as tmp:
+        km.h_merge(ds, km.Metric.L2, km.MergeParams(k=10, seed=4), snapshot_dir=tmp)
+        out["hmerge"]["snapshot_sha256"] = {
+            f: hashlib.sha256(open(os.path.join(tmp, f), "rb").read()).hexdigest()
+            for f in sorted(os.listdir(tmp))}
     ds2 = km.Dataset.from_dense(C.make_data(dict(data="uniform", n=300, d=5, data_seed=2)), validate=False)
     g = km.nn_descent(ds2, km.Metric.L2, km.DescentParams(k=6), 3, member_ids=np.arange(0, 300, 2))
     with tempfile.TemporaryDirectory() as tmp:
