@@ -85,6 +85,7 @@ typedef struct knnm_stats {
     int64_t apply_rows_out; /* rows the apply stored (>= 1 accepted insert) */
     double apply_kernel_ms; /* the apply kernel alone (roofline denominator) */
     int64_t active_hoods;   /* hoods with >= 1 admissible pair, over all rounds */
+    int64_t bf_tc_launches; /* brute-force calls served by the tcgen05 route */
 } knnm_stats;
 
 const char *knnm_last_error(void);
@@ -277,9 +278,21 @@ int knnm_signal_stream(knnm_ctx *ctx, void *stream);
  * rows of the current union (knnm_begin; ids are local rows); vector queries
  * search the whole dataset.  exclude_self drops the query row itself
  * (brute_force_graph).
- * Missing entries are -1 / +inf.  k <= 64. */
+ * Missing entries are -1 / +inf.  k <= 64.
+ * Certified u8 L2 datasets (integers in [0, 255]) with k <= 32 run on the
+ * tensor cores (tcgen05 kind::i8 Gram tiles, exact s32 -> exact distances);
+ * everything else on the exact fp64 SIMT kernel. */
 int knnm_bf_topk(knnm_ctx *ctx, const float *queries, const int64_t *rows, int64_t nq,
                  int32_t k, int32_t exclude_self, int32_t *out_ids, double *out_dists);
+/* pair_dists_dense (_kernels.py:113-119): exact reference distances of the
+ * union-row pairs (pa[i], pb[i]) -> out[i] (host arrays; knnm_begin first).
+ * Serves the on_pair route of brute_force_graph (construct.py:296-312). */
+int knnm_pair_dists(knnm_ctx *ctx, const int32_t *pa, const int32_t *pb, int64_t m, double *out);
+/* Brute-force route: -1 auto (default), 0 exact SIMT, 1 tensor cores
+ * (fails with KNNM_ERR_LIMIT when the data is not certified u8 L2). */
+int knnm_set_bf_variant(knnm_ctx *ctx, int32_t variant);
+/* Route the last knnm_bf_topk took: 0 SIMT, 1 tensor cores. */
+int knnm_bf_route(knnm_ctx *ctx, int32_t *route);
 
 /* phi over the current lists (construct.py:79-83), with numpy's pairwise
  * summation order, so the value is bit-identical to the reference. */

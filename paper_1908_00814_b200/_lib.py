@@ -62,6 +62,7 @@ class KnnmStats(ctypes.Structure):
         ("apply_rows_out", I64),
         ("apply_kernel_ms", ctypes.c_double),
         ("active_hoods", I64),
+        ("bf_tc_launches", I64),
     ]
 
     def as_dict(self) -> dict:
@@ -107,6 +108,9 @@ SIGNATURES = {
     "knnm_unpack_rows": (ctypes.c_int, [P, P, I64]),
     "knnm_state_views": (ctypes.c_int, [P, ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(P)]),
     "knnm_bf_topk": (ctypes.c_int, [P, P, P, I64, I32, I32, P, P]),
+    "knnm_set_bf_variant": (ctypes.c_int, [P, I32]),
+    "knnm_pair_dists": (ctypes.c_int, [P, P, P, I64, P]),
+    "knnm_bf_route": (ctypes.c_int, [P, P]),
     "knnm_phi": (ctypes.c_int, [P, PDBL]),
     "knnm_phi_async": (ctypes.c_int, [P, I32]),
     "knnm_phi_fetch": (ctypes.c_int, [P, I32, PDBL]),

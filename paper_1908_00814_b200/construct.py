@@ -245,9 +245,10 @@ def brute_force_graph(dataset: Dataset, metric: Metric, k: int, member_ids=None,
 
     The reference inserts candidates in ascending id order, which makes its
     lists exactly the top-k by (fp64 distance, id); the device computes the
-    same exact distances and selects by (distance, id)."""
-    if on_pair is not None:
-        raise NotImplementedError("the on_pair route of brute_force_graph is not supported on the GPU")
+    same exact distances and selects by (distance, id).  With ``on_pair``
+    every pair (i, j), i < j, is also handed to the hook as
+    ``(gid_i, gid_j, d)`` in the reference's order (j ascending, then i;
+    construct.py:296-312), the distances evaluated exactly on the device."""
     metric = Metric(metric)
     metric.check_kind(dataset.kind)
     gids = _resolve_members(dataset, member_ids)
@@ -260,10 +261,31 @@ def brute_force_graph(dataset: Dataset, metric: Metric, k: int, member_ids=None,
     eng.set_dataset(dataset.vectors, int(metric))
     eng.begin(gids, np.zeros(n, dtype=np.int8), k)
     loc, dists = eng.bf_topk(k, rows=np.arange(n, dtype=np.int64), exclude_self=True)
+    if on_pair is not None:
+        _stream_all_pairs(eng, gids, on_pair)
     counter.add(n * (n - 1) // 2)
     ids = np.where(loc >= 0, gids.astype(np.int32)[np.maximum(loc, 0)], -1).astype(np.int32)
     sizes = np.full(n, min(k, n - 1), dtype=np.int32)
     return _graph_from(gids, k, metric, ids, dists, sizes)
+
+
+def _stream_all_pairs(eng, gids: np.ndarray, on_pair, chunk_pairs: int = 1 << 22) -> None:
+    """(gid_i, gid_j, d) for every i < j, j-major, in blocks of rows j."""
+    n = gids.shape[0]
+    j0 = 1
+    while j0 < n:
+        j1 = j0 + 1
+        while j1 < n and (j1 * (j1 - 1) - j0 * (j0 - 1)) // 2 + j1 <= chunk_pairs:
+            j1 += 1
+        js = np.arange(j0, j1, dtype=np.int64)
+        pb = np.repeat(js, js).astype(np.int32)
+        starts = np.repeat(np.cumsum(js) - js, js)
+        pa = (np.arange(pb.shape[0], dtype=np.int64) - starts).astype(np.int32)
+        d = eng.pair_dists(pa, pb)
+        ga, gb = gids[pa], gids[pb]
+        for t in range(pa.shape[0]):
+            on_pair(int(ga[t]), int(gb[t]), float(d[t]))
+        j0 = j1
 
 
 def brute_force_queries(dataset: Dataset, metric: Metric, queries: Dataset, k: int,

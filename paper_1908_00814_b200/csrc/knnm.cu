@@ -2,6 +2,7 @@
 // for the B200 S-Merge / J-Merge round engine.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <cmath>
 
 #include <algorithm>
@@ -15,6 +16,7 @@
 
 #include "../../include/knnm.h"
 #include "knnm_kernels.cuh"
+#include "knnm_bf.cuh"
 
 using namespace knnm;
 
@@ -129,6 +131,11 @@ struct knnm_ctx {
     const uint8_t *sub16p = nullptr;
     const float *subnormp = nullptr;
     int join_variant = -1;  // -1 auto, 0 exact (fp64 every pair), 1 tiled, 2 tensor core
+    int bf_variant = -1;    // brute force: -1 auto, 0 SIMT exact, 1 tcgen05 (certified u8 only)
+    int bf_last_route = 0;  // route the last knnm_bf_topk took (0 SIMT, 1 tcgen05)
+    DBuf bfq, bfqn, bfpart;  // brute force: gathered query rows / norms, partial lists
+    bool bf_u8 = false;      // integers in [0, 255]: exact u8 Gram tiles for brute force
+    DBuf bfx, bfxn;          // u8 copy of the candidate rows when the join has none
     bool u8_enabled = true;
     // current merge
     DBuf sub, ugid, labels, labbits;
@@ -787,6 +794,8 @@ int knnm_set_dataset(knnm_ctx *c, const float *vectors, int64_t n_all, int32_t d
                       2.0 * (double)d * maxabs * maxabs < 16777216.0;
         CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
         c->cert_u8 = c->cert_dot && mn >= 0.0 && mx <= 255.0 && c->u8_enabled;
+        // brute force needs only exact s32 dot products and u32 distances
+        c->bf_u8 = ints && mn >= 0.0 && mx <= 255.0 && (double)d * 65025.0 < 2147483648.0;
         if (c->cert_u8) {
             c->dph = (d + 31) & ~31;  // u8 elements per row
             c->rowb = c->dph;
@@ -1960,6 +1969,58 @@ int knnm_state_views(knnm_ctx *c, void **ids, void **dists, void **flags, void *
     return KNNM_OK;
 }
 
+// TMA descriptor of a row-major u8 matrix (rows x rb bytes), boxes of
+// TB_KB bytes x box_rows rows, 128-byte swizzle (the UMMA operand layout).
+static int tb_tensor_map(CUtensorMap *map, const void *ptr, int64_t rows, int rb, int box_rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q;
+        void *fn = nullptr;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) return fail(KNNM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t gdim[2] = {(cuuint64_t)rb, (cuuint64_t)rows};
+    const cuuint64_t gstride[1] = {(cuuint64_t)rb};
+    const cuuint32_t box[2] = {(cuuint32_t)TB_KB, (cuuint32_t)box_rows};
+    const cuuint32_t estride[2] = {1, 1};
+    const CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(ptr), gdim, gstride, box,
+                              estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(KNNM_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return KNNM_OK;
+}
+
+// Brute force on the tensor cores (knnm_bf.cuh): certified u8 data, L2.
+// X = the candidate rows (union rows, or the whole dataset for vector
+// queries), Q = the query rows as a dense u8 matrix with their norms.
+static int bf_tc(knnm_ctx *c, const uint8_t *X, const int32_t *xnorm, int64_t nx, int rb, const uint8_t *Q,
+                 const int32_t *qnorm, const int64_t *qself, int64_t nq, int k, int32_t *oi, double *od) {
+    const int nkb = (rb + TB_KB - 1) / TB_KB;
+    const size_t smem = tb_smem_bytes(nkb, k);
+    CUtensorMap mq, mx;
+    TRY(tb_tensor_map(&mq, Q, nq, rb, TB_M));
+    TRY(tb_tensor_map(&mx, X, nx, rb, TB_N));
+    static size_t smem_set = 0;
+    if (smem > smem_set) {
+        CK(cudaFuncSetAttribute(k_bf_tc_u8, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_set = smem;
+    }
+    const int64_t nqb = (nq + TB_M - 1) / TB_M, ntiles = (nx + TB_N - 1) / TB_N;
+    // data slices so that small query sets still fill the SMs
+    int S = (int)std::min<int64_t>({(int64_t)16, std::max<int64_t>(1, (c->sms + nqb - 1) / nqb), ntiles});
+    const int64_t tps = (ntiles + S - 1) / S;
+    S = (int)((ntiles + tps - 1) / tps);
+    TRY(ensure(c->bfpart, sizeof(uint64_t) * (size_t)S * nq * k));
+    k_bf_tc_u8<<<dim3((unsigned)nqb, (unsigned)S), TB_THREADS, smem, c->st>>>(
+        mq, mx, nq, nx, nkb, qnorm, xnorm, qself, k, tps, c->bfpart.as<uint64_t>());
+    CKL();
+    k_bf_tc_finish<<<grid_for(c, nq, 128), 128, 0, c->st>>>(c->bfpart.as<uint64_t>(), nq, k, S, oi, od);
+    CKL();
+    c->stats.bf_tc_launches += 1;
+    return KNNM_OK;
+}
+
 int knnm_bf_topk(knnm_ctx *c, const float *queries, const int64_t *rows, int64_t nq, int32_t k,
                  int32_t exclude_self, int32_t *out_ids, double *out_dists) {
     if (!c || (!queries && !rows) || !out_ids || !out_dists) return fail(KNNM_ERR_ARG, "null argument");
@@ -1995,17 +2056,97 @@ int knnm_bf_topk(knnm_ctx *c, const float *queries, const int64_t *rows, int64_t
     TRY(ensure(c->stage[2], (sizeof(int32_t) + sizeof(double)) * (size_t)nq * k + 8));
     int32_t *oi = c->stage[2].as<int32_t>();
     double *od = reinterpret_cast<double *>(c->stage[2].as<char>() + ((sizeof(int32_t) * (size_t)nq * k + 7) & ~(size_t)7));
-    const size_t smem = (size_t)BF_THREADS * k * (sizeof(double) + sizeof(int32_t));
-    const unsigned grid = (unsigned)std::min<int64_t>(nq, (int64_t)c->sms * 8);
+    // tensor-core route: exact integer Gram tiles (u8 rows, L2)
+    const int rb = (c->d + 31) & ~31;
+    bool tc = c->bf_u8 && c->metric == KNNM_L2 && k <= TB_MAX_K && c->bf_variant != 0 &&
+              tb_smem_bytes((rb + TB_KB - 1) / TB_KB, k) <= 227 * 1024 && n >= 1;
+    if (tc && !rows) {
+        // vector queries must themselves be integers in [0, 255]
+        unsigned long long *cnt = c->counters.as<unsigned long long>();
+        unsigned long long init[3] = {0ull, 0ull, 0xffffffffull};
+        CK(cudaMemcpyAsync(cnt + C_NUM - 3, init, sizeof(init), cudaMemcpyHostToDevice, c->st));
+        k_data_stats<<<grid_for(c, nq * c->dp, 256), 256, 0, c->st>>>(qd, nq * c->dp, cnt + C_NUM - 3);
+        CKL();
+        TRY(sync_counters(c));
+        const uint32_t mxk = (uint32_t)c->hcnt[C_NUM - 2], mnk = (uint32_t)c->hcnt[C_NUM - 1];
+        // ordered keys of 0.0f and 255.0f (see k_data_stats)
+        tc = c->hcnt[C_NUM - 3] == 0 && mnk >= 0x80000000u && mxk <= (0x437f0000u | 0x80000000u);
+        CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
+    }
+    if (c->bf_variant == 1 && !tc) return fail(KNNM_ERR_LIMIT, "tensor-core brute force needs u8 L2 data, k <= %d", TB_MAX_K);
+    c->bf_last_route = tc ? 1 : 0;
+    if (tc) {
+        const uint8_t *X;
+        const int32_t *xn;
+        if (c->cert_u8) {  // the join's u8 copy (same row length)
+            X = rows ? c->sub16p : c->vec16.as<uint8_t>();
+            xn = reinterpret_cast<const int32_t *>(rows ? c->subnormp : c->norms.as<float>());
+        } else {
+            TRY(ensure(c->bfx, (size_t)n * rb));
+            TRY(ensure(c->bfxn, sizeof(int32_t) * (size_t)n));
+            k_to_u8<<<grid_for(c, n * 32, 256, 16), 256, 0, c->st>>>(data, c->dp, n, rb, c->bfx.as<uint8_t>(),
+                                                                    reinterpret_cast<float *>(c->bfxn.p));
+            CKL();
+            X = c->bfx.as<uint8_t>();
+            xn = c->bfxn.as<int32_t>();
+        }
+        TRY(ensure(c->bfq, (size_t)nq * rb));
+        TRY(ensure(c->bfqn, sizeof(int32_t) * (size_t)nq));
+        if (rows) {
+            k_bf_gather_u8<<<grid_for(c, nq * (rb / 16), 256), 256, 0, c->st>>>(
+                X, rb, xn, rd, nq, c->bfq.as<uint8_t>(), c->bfqn.as<int32_t>());
+        } else {
+            k_to_u8<<<grid_for(c, nq * 32, 256, 16), 256, 0, c->st>>>(qd, c->dp, nq, rb, c->bfq.as<uint8_t>(),
+                                                                     reinterpret_cast<float *>(c->bfqn.p));
+        }
+        CKL();
+        TRY(bf_tc(c, X, xn, n, rb, c->bfq.as<uint8_t>(), c->bfqn.as<int32_t>(), (rows && exclude_self) ? rd : nullptr,
+                  nq, k, oi, od));
+    } else {
+        const size_t smem = (size_t)BF_THREADS * k * (sizeof(double) + sizeof(int32_t));
+        const unsigned grid = (unsigned)std::min<int64_t>(nq, (int64_t)c->sms * 8);
 #define KNNM_BF_ARGS data, n, c->dp, c->d, qd, c->dp, rd, nq, k, exclude_self, oi, od
-    if (c->metric == 1) k_bf_topk<1><<<grid, BF_THREADS, smem, c->st>>>(KNNM_BF_ARGS);
-    else if (c->metric == 2) k_bf_topk<2><<<grid, BF_THREADS, smem, c->st>>>(KNNM_BF_ARGS);
-    else k_bf_topk<0><<<grid, BF_THREADS, smem, c->st>>>(KNNM_BF_ARGS);
+        if (c->metric == 1) k_bf_topk<1><<<grid, BF_THREADS, smem, c->st>>>(KNNM_BF_ARGS);
+        else if (c->metric == 2) k_bf_topk<2><<<grid, BF_THREADS, smem, c->st>>>(KNNM_BF_ARGS);
+        else k_bf_topk<0><<<grid, BF_THREADS, smem, c->st>>>(KNNM_BF_ARGS);
 #undef KNNM_BF_ARGS
-    CKL();
+        CKL();
+    }
     TRY(d2h(c, out_ids, oi, sizeof(int32_t) * (size_t)nq * k));
     TRY(d2h(c, out_dists, od, sizeof(double) * (size_t)nq * k));
     CK(cudaStreamSynchronize(c->st));
+    return KNNM_OK;
+}
+
+int knnm_pair_dists(knnm_ctx *c, const int32_t *pa, const int32_t *pb, int64_t m, double *out) {
+    if (!c || ((!pa || !pb || !out) && m > 0)) return fail(KNNM_ERR_ARG, "null argument");
+    if (!c->begun) return fail(KNNM_ERR_STATE, "knnm_begin first");
+    if (m == 0) return KNNM_OK;
+    CK(cudaSetDevice(c->device));
+    PhaseTimer pt(c, PH_OTHER);
+    TRY(ensure(c->stage[0], sizeof(int32_t) * (size_t)m));
+    TRY(ensure(c->stage[1], sizeof(int32_t) * (size_t)m));
+    TRY(ensure(c->stage[2], sizeof(double) * (size_t)m));
+    TRY(h2d(c, c->stage[0].p, pa, sizeof(int32_t) * (size_t)m));
+    TRY(h2d(c, c->stage[1].p, pb, sizeof(int32_t) * (size_t)m));
+    k_pair_dists<<<grid_for(c, m, 256), 256, 0, c->st>>>(c->stage[0].as<int32_t>(), c->stage[1].as<int32_t>(), m,
+                                                         c->subp, c->dp, c->d, c->metric, c->stage[2].as<double>());
+    CKL();
+    TRY(d2h(c, out, c->stage[2].p, sizeof(double) * (size_t)m));
+    CK(cudaStreamSynchronize(c->st));
+    return KNNM_OK;
+}
+
+int knnm_set_bf_variant(knnm_ctx *c, int32_t variant) {
+    if (!c) return fail(KNNM_ERR_ARG, "null ctx");
+    if (variant < -1 || variant > 1) return fail(KNNM_ERR_ARG, "bf variant %d", variant);
+    c->bf_variant = variant;
+    return KNNM_OK;
+}
+
+int knnm_bf_route(knnm_ctx *c, int32_t *route) {
+    if (!c || !route) return fail(KNNM_ERR_ARG, "null argument");
+    *route = c->bf_last_route;
     return KNNM_OK;
 }
 

@@ -2423,6 +2423,14 @@ k_seg_rank_heavy(const uint32_t *__restrict__ moff, const MembRec *__restrict__ 
 }
 
 
+// pair_dists_dense (_kernels.py:113-119): exact reference distance of each
+// (pa[i], pb[i]) pair of union rows, one thread per pair.
+__global__ void k_pair_dists(const int32_t *__restrict__ pa, const int32_t *__restrict__ pb, int64_t m,
+                             const float *__restrict__ sub, int dp, int d, int tag, double *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = exact_dist_tag(tag, sub + (int64_t)pa[i] * dp, sub + (int64_t)pb[i] * dp, d);
+}
+
 // on_pair capture: every admissible pair of every hood in (u, p, q) order.
 __global__ void k_capture_pairs(const uint32_t *__restrict__ nbh, const int32_t *__restrict__ nlen,
                                 int64_t lo, int64_t hi, int W, const int8_t *__restrict__ labels,

@@ -303,6 +303,24 @@ class Engine:
         check(self._lib.knnm_signal_stream(self._h, ctypes.c_void_p(s.cuda_stream)),
               "knnm_signal_stream")
 
+    def pair_dists(self, pa: np.ndarray, pb: np.ndarray) -> np.ndarray:
+        """Exact reference distances of union-row pairs (pair_dists_dense)."""
+        a = np.ascontiguousarray(pa, dtype=np.int32)
+        b = np.ascontiguousarray(pb, dtype=np.int32)
+        out = np.empty(a.shape[0], dtype=np.float64)
+        check(self._lib.knnm_pair_dists(self._h, ptr(a), ptr(b), a.shape[0], ptr(out)), "knnm_pair_dists")
+        return out
+
+    def set_bf_variant(self, variant: int) -> None:
+        """Brute-force route: -1 auto, 0 exact SIMT, 1 tensor cores (tcgen05)."""
+        check(self._lib.knnm_set_bf_variant(self._h, int(variant)), "knnm_set_bf_variant")
+
+    def bf_route(self) -> int:
+        """Route of the last bf_topk call: 0 SIMT, 1 tensor cores."""
+        r = ctypes.c_int32(0)
+        check(self._lib.knnm_bf_route(self._h, ctypes.byref(r)), "knnm_bf_route")
+        return int(r.value)
+
     def set_join_variant(self, variant: int) -> None:
         """-1 auto, 0 exact fp64 route, 1 tiled fp32-screen route, 2 tensor-core route."""
         check(self._lib.knnm_set_join_variant(self._h, int(variant)), "knnm_set_join_variant")
