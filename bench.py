@@ -330,30 +330,42 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def kernel_rooflines(st, steps, d, k, slot_b, lazy, hbm_peak, row_b=None):
+def kernel_rooflines(st, steps, d, k, slot_b, lazy, hbm_peak, row_b=None, cosine=False):
     """Algorithmic-byte rooflines of the join, apply and assembly kernels of
     one step, from the run's own counters (SURVEY.md §8d's byte model):
 
     join      (row_b + 4) * sum|M_u| + slot_b * written_slots
-              (+ 8 d per exact fp64 evaluation in the join: two fp32 rows)
+              (exact fp64 evaluations in the join read the rows already
+              staged in shared memory: no HBM bytes of their own; they are
+              reported against the fp64 pipe instead, ``fp64`` below)
     apply     8 * slots read + (slot_b - 8) * written slots (source ids)
               + 13 k per row loaded + 13 k per row stored (ids, dists, flags)
-              (+ 8 d per lazy exact evaluation in the apply)
+              (+ 4 d per lazy exact evaluation in the apply: the candidate row)
     assemble  9 k per active hood (forward ids + flags, reverse entries)
               + 20 B per membership (hood entry + membership record)
 
     ``row_b``: bytes per gathered member row (default fp32 rows, 4 d)."""
     row_b = 4.0 * d if row_b is None else float(row_b)
-    ex_join = 0.0 if lazy else 8.0 * d * st["exact_evals"]
-    ex_apply = 8.0 * d * st["exact_evals"] if lazy else 0.0
+    ex_apply = 4.0 * d * st["exact_evals"] if lazy else 0.0
     out = {}
-    jb = (row_b + 4.0) * st["members"] + slot_b * st["written_slots"] + ex_join
+    jb = (row_b + 4.0) * st["members"] + slot_b * st["written_slots"]
     ab = (8.0 * st["candidates"] + (slot_b - 8.0) * st["written_slots"]
           + 13.0 * k * (st["apply_rows_in"] + st["apply_rows_out"]) + ex_apply)
     for name, b, ms in (("join", jb, st["join_kernel_ms"]), ("apply", ab, st["apply_kernel_ms"])):
         gbs = b / (ms / 1e3) / 1e9 if ms > 0 else 0.0
         out[name] = {"bytes_per_step": b / steps, "ms_per_step": ms / steps, "achieved": gbs,
                      "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak}
+    if st["exact_evals"] > 0:
+        # exact reference sums: d dependent fp64 steps per evaluation, 3 fp64
+        # instructions per dimension (sub, mul, add; 2 for the cosine dot),
+        # against 64 fp64 lanes x 148 SMs x 1.965 GHz (nominal, non-FMA)
+        ops = float(st["exact_evals"]) * d * (2.0 if cosine else 3.0)
+        ms = st["apply_kernel_ms"] if lazy else st["join_kernel_ms"]
+        peak = 64 * 148 * 1.965e9
+        out["apply" if lazy else "join"]["fp64"] = {
+            "exact_evals_per_step": st["exact_evals"] / steps, "ops_per_step": ops / steps,
+            "achieved_tops": ops / (ms / 1e3) / 1e12, "peak_tops": peak / 1e12,
+            "frac": ops / (ms / 1e3) / peak, "peak_kind": "nominal"}
     return out
 
 
@@ -403,7 +415,7 @@ def config_legs(km, names, device, steps, warmup, hbm_peak, no_recall=False):
         inf = eng.info()
         lazy = (not inf["cert"]) and ds.d > 384
         slot_b = 8.0 if (inf["cert"] or inf["cert_dot"]) else 12.0
-        kr = kernel_rooflines(st, steps, ds.d, k, slot_b, lazy, hbm_peak)
+        kr = kernel_rooflines(st, steps, ds.d, k, slot_b, lazy, hbm_peak, cosine=int(metric) == 2)
         rec = None
         if not no_recall:
             uh = km.KnnGraph.from_arrays(u.member_ids, u.k, u.metric, u.ids.cpu().numpy(),

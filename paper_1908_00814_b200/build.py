@@ -31,7 +31,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
         t = os.path.getmtime(OUT)
         if all(os.path.getmtime(d) <= t for d in DEPS):
             return OUT
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", OUT, SRC]
+    # KNNM_NVCC_EXTRA: extra flags for debug builds (e.g. "-DKNNM_DEBUG":
+    # device-side bounds asserts on the lazy / batch paths)
+    extra = os.environ.get("KNNM_NVCC_EXTRA", "").split()
+    cmd = [nvcc(), *NVCC_FLAGS, *extra, "-o", OUT, SRC]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     subprocess.run(cmd, check=True)

@@ -441,6 +441,7 @@ constexpr int LAZY_MIN_D = 384;
 
 LazyExact lazy_of(knnm_ctx *c) {
     LazyExact z;
+    z.nrows = c->n;
     z.sub = c->subp;
     z.nrm64 = c->metric == KNNM_COSINE ? c->nrm64.as<double>() : nullptr;
     z.dp = c->dp;

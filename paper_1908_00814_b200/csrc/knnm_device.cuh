@@ -5,6 +5,15 @@
 
 #define FULL_MASK 0xffffffffu
 
+// Device-side bounds checks of the debug build (-DKNNM_DEBUG; compute-sanitizer
+// is not available on the GPU pool): a failed check traps with its line.
+#ifdef KNNM_DEBUG
+#include <cassert>
+#define KNNM_CHECK(cond) assert(cond)
+#else
+#define KNNM_CHECK(cond) ((void)0)
+#endif
+
 namespace knnm {
 
 constexpr uint64_t U64_GAMMA = 0x9E3779B97F4A7C15ULL;  // _kernels.py:33
@@ -98,6 +107,18 @@ __device__ __forceinline__ double exact_cos_norms(const float *__restrict__ a, c
     if (dot > 0.0 && __dmul_rn(dot, dot) >= __dmul_rn(na, nb)) return 0.0;
     double r = __dsub_rn(1.0, __ddiv_rn(dot, __dmul_rn(__dsqrt_rn(na), __dsqrt_rn(nb))));
     return r < 0.0 ? 0.0 : r;
+}
+
+// One step of the exact reference sums (_kernels.py:43-80): acc + term(x, y)
+// with the reference's fp64 roundings (cosine: the dot; norms precomputed).
+template <int TAG>
+__device__ __forceinline__ double exact_term(double acc, float x, float y) {
+    if (TAG == 1) {
+        const double df = __dsub_rn((double)x, (double)y);
+        return __dadd_rn(acc, __dmul_rn(df, df));
+    }
+    if (TAG == 0) return __dadd_rn(acc, fabs(__dsub_rn((double)x, (double)y)));
+    return __dadd_rn(acc, __dmul_rn((double)x, (double)y));  // dot (norms precomputed)
 }
 
 __device__ __forceinline__ double exact_sqnorm(const float *__restrict__ a, int d) {
@@ -324,6 +345,7 @@ __device__ __forceinline__ int warp_insert(WarpRow<E, T> &s, int k, int src, T n
 //   cosine  : exact >= f - lo_abs    (|f - exact| <= (4 d + 64) 2^-24)
 // ---------------------------------------------------------------------------
 struct LazyExact {
+    int64_t nrows;        // rows of sub (bounds checks of the debug build)
     const float *sub;     // subset rows, dp floats each (zero padded)
     const double *nrm64;  // exact fp64 squared norms per row (cosine only)
     int dp, d, tag;
@@ -475,6 +497,163 @@ __device__ __forceinline__ void lazy_warp_eval(const LazyExact z, int64_t r, boo
     if (z.tag == 1) dl = lazy_warp_eval_t<1>(z, r, need, src, dl, sm, lane);
     else if (z.tag == 0) dl = lazy_warp_eval_t<0>(z, r, need, src, dl, sm, lane);
     else dl = lazy_warp_eval_t<2>(z, r, need, src, dl, sm, lane);
+}
+
+// ---------------------------------------------------------------------------
+// Batched speculative lazy evaluation.  The sequential fold of one exact
+// value is a chain of d dependent fp64 adds, so a warp is only busy when many
+// pairs fold at once: when a chunk of a row needs exact values, the warp also
+// takes, from the next LZB_AHEAD chunks of the same slot segment, every
+// approximate slot that could pass the row's current state (lower bound below
+// the current worst, id not listed) -- up to 32 pairs -- and folds all of them
+// together, one pair per lane.  The values are kept in a per-lane cache keyed
+// by slot index and handed out when their chunks come up.  The decisions are
+// unchanged (they are still taken on exact values at each slot's turn); a
+// speculative value that is never asked for is wasted work only.
+// ---------------------------------------------------------------------------
+constexpr int LZB_AHEAD = 8;   // chunks of look-ahead per batch
+constexpr int LZB_STRIDE = 33; // padded staging stride (conflict-free column reads)
+
+struct LazyBatchSmem {
+    float y[2][32 * LZB_STRIDE];  // y[buf][j * 33 + t]: dimension t0 + t of pair j's candidate row
+    float x[2][32];               // the row's own dimensions t0 .. t0 + 31
+    int sid[32];                  // candidate row of pair j
+    uint32_t spos[32];            // slot index (within the row's segment) of pair j
+};
+
+__device__ __forceinline__ void cp_async4(float *dst, const float *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+
+// Exact values of batch pairs 0 .. P-1 (row r against b.sid[j]); lane j
+// folds pair j.  The 32-dimension blocks of the rows are staged by cp.async
+// into two buffers: block t + 1 is in flight while block t is folded.
+template <int TAG>
+__device__ __noinline__ double lazy_batch_t(const LazyExact z, int64_t r, int P, LazyBatchSmem &b, unsigned lane) {
+    const float *ra = z.sub + r * z.dp;
+    const int my = (int)lane < P ? b.sid[lane] : 0;
+    KNNM_CHECK(P >= 1 && P <= 32 && r >= 0 && r < z.nrows && my >= 0 && my < z.nrows);
+    const int nblk = (z.d + 31) >> 5;
+    auto issue = [&](int blk) {
+        const int t = blk * 32 + (int)lane, buf = blk & 1;
+        if (t < z.d) {
+            cp_async4(&b.x[buf][lane], ra + t);
+            for (int j = 0; j < P; j++) cp_async4(&b.y[buf][j * LZB_STRIDE + lane], z.sub + (int64_t)b.sid[j] * z.dp + t);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    double acc = 0.0;
+    const int off = (int)lane * LZB_STRIDE;
+    issue(0);
+    for (int blk = 0; blk < nblk; blk++) {
+        if (blk + 1 < nblk) issue(blk + 1);
+        else asm volatile("cp.async.commit_group;" ::: "memory");
+        asm volatile("cp.async.wait_group 1;" ::: "memory");
+        __syncwarp();
+        if ((int)lane < P) {
+            const float *xs = b.x[blk & 1], *col = b.y[blk & 1] + off;
+            const int nb = z.d - blk * 32 < 32 ? z.d - blk * 32 : 32;
+            for (int i = 0; i < nb; i++) acc = exact_term<TAG>(acc, xs[i], col[i]);
+        }
+        __syncwarp();
+    }
+    if (TAG == 2 && (int)lane < P) acc = cos_finish(acc, z.nrm64[r], z.nrm64[my]);
+    return acc;
+}
+
+template <int E>
+__device__ __forceinline__ bool row_lists(const WarpRow<E> &s, int src) {
+    bool hit = false;
+#pragma unroll
+    for (int e = 0; e < E; e++)
+        for (int t = 0; t < 32; t++) {
+            const int id = __shfl_sync(FULL_MASK, s.idf[e], t) >> 1;
+            hit |= e * 32 + t < s.sz && id == src;
+        }
+    return hit;
+}
+
+// Resolve the need lanes of chunk c0 of a slot segment (slots seg[0, ns) of
+// row r): from the cache, else by a new batch starting at this chunk.
+// cpos/cval: the lane's cache entry (slot index, exact value).
+template <int E>
+__device__ __forceinline__ void lazy_chunk_eval(const WarpRow<E> &s, int k, const LazyExact z, int64_t r,
+                                                const double *__restrict__ Bd, const int32_t *__restrict__ Bs,
+                                                uint64_t seg, int64_t ns, int64_t c0, bool need, int src,
+                                                double &dl, uint32_t &cpos, double &cval, LazyBatchSmem &b,
+                                                unsigned lane, unsigned long long &nexact) {
+    const uint32_t mypos = (uint32_t)(c0 + lane);
+    // cache hits
+    unsigned m = __ballot_sync(FULL_MASK, need);
+    unsigned miss = 0;
+    while (m) {
+        const int i = __ffs(m) - 1;
+        m &= m - 1;
+        const uint32_t p = (uint32_t)(c0 + i);
+        const unsigned h = __ballot_sync(FULL_MASK, cpos == p);
+        if (h) {
+            const double v = __shfl_sync(FULL_MASK, cval, __ffs(h) - 1);
+            if ((int)lane == i) dl = v;
+        } else {
+            miss |= 1u << i;
+        }
+    }
+    if (!miss) return;
+    // a new batch: this chunk's misses, then look-ahead candidates in order
+    int P = 0;
+    {
+        const bool mine = (miss >> lane) & 1u;
+        const unsigned mm = __ballot_sync(FULL_MASK, mine);
+        if (mine) {
+            const int at = __popc(mm & lanemask_lt());
+            KNNM_CHECK(src >= 0 && src < z.nrows);
+            b.sid[at] = src;
+            b.spos[at] = mypos;
+        }
+        P = __popc(mm);
+    }
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+#pragma unroll 1
+    for (int a = 1; a <= LZB_AHEAD; a++) {
+        const int64_t cc = c0 + 32 * a;
+        if (P >= 32 || cc >= ns) break;
+        const int64_t j = cc + lane;
+        const bool in = j < ns;
+        const double v = in ? Bd[seg + j] : inf;
+        const bool apx = in && slot_is_approx(v);
+        const double lb = apx ? slot_lower(v, z) : inf;
+        bool cand = apx && (lb < s.worst || (s.sz < k && lb < inf));
+        const int sv = cand ? Bs[seg + j] : 0;
+        if (__any_sync(FULL_MASK, cand)) {
+            const bool listed = row_lists<E>(s, sv);
+            cand = cand && !listed;
+        }
+        const unsigned cm = __ballot_sync(FULL_MASK, cand);
+        const int at = P + __popc(cm & lanemask_lt());
+        if (cand && at < 32) {
+            KNNM_CHECK(sv >= 0 && sv < z.nrows);
+            b.sid[at] = sv;
+            b.spos[at] = (uint32_t)j;
+        }
+        __syncwarp();
+        P += __popc(cm);
+    }
+    if (P > 32) P = 32;
+    __syncwarp();
+    double v;
+    if (z.tag == 1) v = lazy_batch_t<1>(z, r, P, b, lane);
+    else if (z.tag == 0) v = lazy_batch_t<0>(z, r, P, b, lane);
+    else v = lazy_batch_t<2>(z, r, P, b, lane);
+    if (lane == 0) nexact += (unsigned long long)P;
+    cpos = (int)lane < P ? b.spos[lane] : 0xffffffffu;
+    cval = v;
+    __syncwarp();
+    // the misses of this chunk are batch entries 0 .. popc(miss) - 1
+    const int rank = __popc(miss & lanemask_lt());
+    const double mv = __shfl_sync(FULL_MASK, v, rank & 31);
+    if ((miss >> lane) & 1u) dl = mv;
 }
 
 // _insert for rows held one entry per lane (k <= 32), cheapest tests first:

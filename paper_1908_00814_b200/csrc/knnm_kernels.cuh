@@ -2472,7 +2472,7 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
                const int32_t *__restrict__ Bs, int32_t *ids, double *dists, uint8_t *flags,
                int32_t *sizes, unsigned long long *counters, LazyExact z) {
     constexpr bool LAZY = MODE == SLOTS_LAZY;
-    __shared__ double s_lz[LAZY ? APPLY_WARPS : 1][LAZY ? LZ_G * LZ_S : 1];
+    __shared__ LazyBatchSmem s_lz[LAZY ? APPLY_WARPS : 1];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * APPLY_WARPS;
     unsigned long long acc = 0, slots = 0, written = 0, nexact = 0, rin = 0, rout = 0;
@@ -2492,6 +2492,8 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
         WarpRow<E, T> s;
         row_load<E, T>(s, ids, dists, flags, sizes, r, k, lane);
         int a = 0;
+        uint32_t cpos = 0xffffffffu;  // lazy batch cache (slot index, exact value)
+        double cval = 0.0;
         for (int64_t c0 = 0; c0 < ns; c0 += 32) {
             const int64_t j = c0 + lane;
             double dl = dnext;
@@ -2514,7 +2516,9 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
                     if (j < ns && dl == dl) written++;
                     bool need;
                     dl = lazy_resolve<E>(s, k, j < ns, dl, Bs, lo + j, z, src, need);
-                    if (__any_sync(FULL_MASK, need)) lazy_warp_eval(z, r, need, src, dl, s_lz[wib], lane, nexact);
+                    if (__any_sync(FULL_MASK, need))
+                        lazy_chunk_eval<E>(s, k, z, r, Bd, Bs, lo, ns, c0, need, src, dl, cpos, cval, s_lz[wib],
+                                           lane, nexact);
                     if (!__any_sync(FULL_MASK, dl < inf)) continue;
                 } else {
                     if (dl != dl) dl = inf;
@@ -2607,7 +2611,7 @@ k_apply_stream_multi(int64_t lo, int64_t no, int k, int nsrc, const uint64_t *__
                      int32_t *sizes, unsigned long long *counters, LazyExact z,
                      uint8_t *dirty) {
     constexpr bool LAZY = MODE == SLOTS_LAZY;
-    __shared__ double s_lz[LAZY ? APPLY_WARPS : 1][LAZY ? LZ_G * LZ_S : 1];
+    __shared__ LazyBatchSmem s_lz[LAZY ? APPLY_WARPS : 1];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
     const int64_t nw = (int64_t)gridDim.x * APPLY_WARPS;
     const double inf = __longlong_as_double(0x7ff0000000000000LL);
@@ -2623,6 +2627,8 @@ k_apply_stream_multi(int64_t lo, int64_t no, int k, int nsrc, const uint64_t *__
         for (int s = 0; s < nsrc; s++) {
             const uint64_t base = off[(int64_t)s * (no + 1) + i];
             const int64_t ns = cnt[(int64_t)s * no + i];
+            uint32_t cpos = 0xffffffffu;  // lazy batch cache of this segment
+            double cval = 0.0;
             for (int64_t c0 = 0; c0 < ns; c0 += 32) {
                 const int64_t j = c0 + lane;
                 double dl = j < ns ? Bd[base + j] : inf;
@@ -2630,7 +2636,9 @@ k_apply_stream_multi(int64_t lo, int64_t no, int k, int nsrc, const uint64_t *__
                 if (LAZY) {
                     bool need;
                     dl = lazy_resolve<E>(st, k, j < ns, dl, Bs, base + j, z, src, need);
-                    if (__any_sync(FULL_MASK, need)) lazy_warp_eval(z, r, need, src, dl, s_lz[wib], lane, nexact);
+                    if (__any_sync(FULL_MASK, need))
+                        lazy_chunk_eval<E>(st, k, z, r, Bd, Bs, base, ns, c0, need, src, dl, cpos, cval,
+                                           s_lz[wib], lane, nexact);
                     if (!__any_sync(FULL_MASK, dl < inf)) continue;
                 } else if (MODE == SLOTS_PACKED) {
                     const unsigned long long v = __double_as_longlong(dl);
