@@ -363,7 +363,8 @@ def kernel_rooflines(st, steps, d, k, slot_b, lazy, hbm_peak, row_b=None, cosine
         ms = st["apply_kernel_ms"] if lazy else st["join_kernel_ms"]
         peak = 64 * 148 * 1.965e9
         out["apply" if lazy else "join"]["fp64"] = {
-            "exact_evals_per_step": st["exact_evals"] / steps, "ops_per_step": ops / steps,
+            "exact_evals_per_step": st["exact_evals"] / steps,
+            "lazy_batches_per_step": st["lazy_batches"] / steps, "ops_per_step": ops / steps,
             "achieved_tops": ops / (ms / 1e3) / 1e12, "peak_tops": peak / 1e12,
             "frac": ops / (ms / 1e3) / peak, "peak_kind": "nominal"}
     return out

@@ -86,6 +86,7 @@ typedef struct knnm_stats {
     double apply_kernel_ms; /* the apply kernel alone (roofline denominator) */
     int64_t active_hoods;   /* hoods with >= 1 admissible pair, over all rounds */
     int64_t bf_tc_launches; /* brute-force calls served by the tcgen05 route */
+    int64_t lazy_batches;   /* lazy exact-evaluation batches in the apply (pairs: exact_evals) */
 } knnm_stats;
 
 const char *knnm_last_error(void);

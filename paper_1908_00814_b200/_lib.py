@@ -63,6 +63,7 @@ class KnnmStats(ctypes.Structure):
         ("apply_kernel_ms", ctypes.c_double),
         ("active_hoods", I64),
         ("bf_tc_launches", I64),
+        ("lazy_batches", I64),
     ]
 
     def as_dict(self) -> dict:

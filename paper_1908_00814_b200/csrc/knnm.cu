@@ -132,6 +132,7 @@ struct knnm_ctx {
     const float *subnormp = nullptr;
     int join_variant = -1;  // -1 auto, 0 exact (fp64 every pair), 1 tiled, 2 tensor core
     int bf_variant = -1;    // brute force: -1 auto, 0 SIMT exact, 1 tcgen05 (certified u8 only)
+    int lazy_ahead = LZB_AHEAD;  // look-ahead chunks of a lazy evaluation batch (KNNM_LAZY_AHEAD)
     int bf_last_route = 0;  // route the last knnm_bf_topk took (0 SIMT, 1 tcgen05)
     DBuf bfq, bfqn, bfpart;  // brute force: gathered query rows / norms, partial lists
     bool bf_u8 = false;      // integers in [0, 255]: exact u8 Gram tiles for brute force
@@ -442,6 +443,7 @@ constexpr int LAZY_MIN_D = 384;
 LazyExact lazy_of(knnm_ctx *c) {
     LazyExact z;
     z.nrows = c->n;
+    z.ahead = c->lazy_ahead;
     z.sub = c->subp;
     z.nrm64 = c->metric == KNNM_COSINE ? c->nrm64.as<double>() : nullptr;
     z.dp = c->dp;
@@ -458,7 +460,7 @@ int run_updates(knnm_ctx *c) {
     unsigned long long *cnt = c->counters.as<unsigned long long>();
     CK(cudaMemsetAsync(cnt + C_CAND, 0, sizeof(unsigned long long) * 2, c->st));
     CK(cudaMemsetAsync(cnt + C_WRITTEN, 0, sizeof(unsigned long long), c->st));
-    CK(cudaMemsetAsync(cnt + C_ROWS_IN, 0, sizeof(unsigned long long) * 2, c->st));
+    CK(cudaMemsetAsync(cnt + C_ROWS_IN, 0, sizeof(unsigned long long) * 3, c->st));
     const int E = (c->k + 31) / 32;
     const int blocks = grid_for(c, n * 32, APPLY_WARPS * 32, 16);
 #define KNNM_AP_LAUNCH(EE, LZ, F)                                                                \
@@ -494,6 +496,7 @@ int run_updates(knnm_ctx *c) {
     c->stats.candidates += (int64_t)c->hcnt[C_CAND];
     c->stats.apply_rows_in += (int64_t)c->hcnt[C_ROWS_IN];
     c->stats.apply_rows_out += (int64_t)c->hcnt[C_ROWS_OUT];
+    c->stats.lazy_batches += (int64_t)c->hcnt[C_LZ_BATCHES];
     c->stats.written_slots += (int64_t)c->hcnt[C_WRITTEN];
     c->stats.seg_hub_rows += (int64_t)c->hcnt[C_SEGHEAVY];
     return KNNM_OK;
@@ -673,6 +676,7 @@ int knnm_create(int device, knnm_ctx **out) {
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
     c->sms = prop.multiProcessorCount;
+    if (const char *e = getenv("KNNM_LAZY_AHEAD")) c->lazy_ahead = std::max(0, std::min(64, atoi(e)));
     CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     CK(cudaHostAlloc((void **)&c->hcnt, sizeof(unsigned long long) * C_NUM, cudaHostAllocDefault));
     TRY(ensure(c->counters, sizeof(unsigned long long) * C_NUM));

@@ -39,6 +39,7 @@ enum Counter {
     C_DUPROWS = 14,   // rows given twice to a row-grouped insert (direct path check)
     C_ROWS_IN = 15,   // rows the apply loaded (>= 1 slot)
     C_ROWS_OUT = 16,  // rows the apply stored (>= 1 accepted insert)
+    C_LZ_BATCHES = 17,// lazy exact-evaluation batches (folds of up to 32 pairs)
     C_NUM = 20
 };
 
@@ -111,6 +112,17 @@ __device__ __forceinline__ double exact_cos_norms(const float *__restrict__ a, c
 
 // One step of the exact reference sums (_kernels.py:43-80): acc + term(x, y)
 // with the reference's fp64 roundings (cosine: the dot; norms precomputed).
+// The same step with x already in fp64 (exactly (double) of an fp32 value).
+template <int TAG>
+__device__ __forceinline__ double exact_term_d(double acc, double x, float y) {
+    if (TAG == 1) {
+        const double df = __dsub_rn(x, (double)y);
+        return __dadd_rn(acc, __dmul_rn(df, df));
+    }
+    if (TAG == 0) return __dadd_rn(acc, fabs(__dsub_rn(x, (double)y)));
+    return __dadd_rn(acc, __dmul_rn(x, (double)y));
+}
+
 template <int TAG>
 __device__ __forceinline__ double exact_term(double acc, float x, float y) {
     if (TAG == 1) {
@@ -346,6 +358,7 @@ __device__ __forceinline__ int warp_insert(WarpRow<E, T> &s, int k, int src, T n
 // ---------------------------------------------------------------------------
 struct LazyExact {
     int64_t nrows;        // rows of sub (bounds checks of the debug build)
+    int ahead;            // look-ahead chunks of a speculative batch (lazy_chunk_eval)
     const float *sub;     // subset rows, dp floats each (zero padded)
     const double *nrm64;  // exact fp64 squared norms per row (cosine only)
     int dp, d, tag;
@@ -511,51 +524,73 @@ __device__ __forceinline__ void lazy_warp_eval(const LazyExact z, int64_t r, boo
 // unchanged (they are still taken on exact values at each slot's turn); a
 // speculative value that is never asked for is wasted work only.
 // ---------------------------------------------------------------------------
-constexpr int LZB_AHEAD = 8;   // chunks of look-ahead per batch
-constexpr int LZB_STRIDE = 33; // padded staging stride (conflict-free column reads)
+constexpr int LZB_AHEAD = 16;  // chunks of look-ahead per batch (default of LazyExact::ahead)
 
-struct LazyBatchSmem {
-    float y[2][32 * LZB_STRIDE];  // y[buf][j * 33 + t]: dimension t0 + t of pair j's candidate row
-    float x[2][32];               // the row's own dimensions t0 .. t0 + 31
-    int sid[32];                  // candidate row of pair j
-    uint32_t spos[32];            // slot index (within the row's segment) of pair j
+struct __align__(16) LazyBatchSmem {
+    // y[buf][j * 32 + 4 * (g ^ (j & 7)) + e]: dimension t0 + 4 g + e of pair
+    // j's candidate row (16-byte groups XOR-swizzled by row: a warp's float4
+    // reads of one group from 32 rows are conflict-free per quarter-warp)
+    float y[2][32 * 32];
+    float x[2][32];     // the row's own dimensions t0 .. t0 + 31
+    double xd[32];      // the same in fp64 (one conversion per dimension, not per pair)
+    int sid[32];        // candidate row of pair j
+    uint32_t spos[32];  // slot index (within the row's segment) of pair j
 };
 
-__device__ __forceinline__ void cp_async4(float *dst, const float *src) {
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+__device__ __forceinline__ void cp_async16(float *dst, const float *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
                  "l"(src)
                  : "memory");
 }
 
 // Exact values of batch pairs 0 .. P-1 (row r against b.sid[j]); lane j
-// folds pair j.  The 32-dimension blocks of the rows are staged by cp.async
-// into two buffers: block t + 1 is in flight while block t is folded.
+// folds pair j.  The 32-dimension blocks of the rows are staged by 16-byte
+// cp.async copies (a warp instruction moves one block of four rows) into two
+// buffers: block t + 1 is in flight while block t is folded.
 template <int TAG>
 __device__ __noinline__ double lazy_batch_t(const LazyExact z, int64_t r, int P, LazyBatchSmem &b, unsigned lane) {
     const float *ra = z.sub + r * z.dp;
     const int my = (int)lane < P ? b.sid[lane] : 0;
     KNNM_CHECK(P >= 1 && P <= 32 && r >= 0 && r < z.nrows && my >= 0 && my < z.nrows);
     const int nblk = (z.d + 31) >> 5;
+    const int g = (int)(lane & 7);
     auto issue = [&](int blk) {
-        const int t = blk * 32 + (int)lane, buf = blk & 1;
-        if (t < z.d) {
-            cp_async4(&b.x[buf][lane], ra + t);
-            for (int j = 0; j < P; j++) cp_async4(&b.y[buf][j * LZB_STRIDE + lane], z.sub + (int64_t)b.sid[j] * z.dp + t);
+        const int t0 = blk * 32, buf = blk & 1;
+        // chunk c = i * 32 + lane: row c >> 3, group c & 7 (= lane & 7)
+        if (t0 + 4 * g < z.dp) {
+            if (lane < 8) cp_async16(&b.x[buf][4 * g], ra + t0 + 4 * g);
+            for (int j = (int)(lane >> 3); j < P; j += 4)
+                cp_async16(&b.y[buf][j * 32 + 4 * (g ^ (j & 7))], z.sub + (int64_t)b.sid[j] * z.dp + t0 + 4 * g);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     double acc = 0.0;
-    const int off = (int)lane * LZB_STRIDE;
     issue(0);
     for (int blk = 0; blk < nblk; blk++) {
         if (blk + 1 < nblk) issue(blk + 1);
         else asm volatile("cp.async.commit_group;" ::: "memory");
         asm volatile("cp.async.wait_group 1;" ::: "memory");
         __syncwarp();
+        b.xd[lane] = (double)b.x[blk & 1][lane];  // the conversion unit is the scarce pipe
+        __syncwarp();
         if ((int)lane < P) {
-            const float *xs = b.x[blk & 1], *col = b.y[blk & 1] + off;
+            const double2 *xs = reinterpret_cast<const double2 *>(b.xd);
+            const float *yr = b.y[blk & 1] + lane * 32;
+            const int sw = (int)(lane & 7);
             const int nb = z.d - blk * 32 < 32 ? z.d - blk * 32 : 32;
-            for (int i = 0; i < nb; i++) acc = exact_term<TAG>(acc, xs[i], col[i]);
+            if (nb == 32) {
+#pragma unroll 2
+                for (int q = 0; q < 8; q++) {
+                    const double2 x01 = xs[2 * q], x23 = xs[2 * q + 1];
+                    const float4 yv = *reinterpret_cast<const float4 *>(yr + 4 * (q ^ sw));
+                    acc = exact_term_d<TAG>(acc, x01.x, yv.x);
+                    acc = exact_term_d<TAG>(acc, x01.y, yv.y);
+                    acc = exact_term_d<TAG>(acc, x23.x, yv.z);
+                    acc = exact_term_d<TAG>(acc, x23.y, yv.w);
+                }
+            } else {
+                for (int i = 0; i < nb; i++) acc = exact_term_d<TAG>(acc, b.xd[i], yr[4 * ((i >> 2) ^ sw) + (i & 3)]);
+            }
         }
         __syncwarp();
     }
@@ -616,7 +651,7 @@ __device__ __forceinline__ void lazy_chunk_eval(const WarpRow<E> &s, int k, cons
     }
     const double inf = __longlong_as_double(0x7ff0000000000000LL);
 #pragma unroll 1
-    for (int a = 1; a <= LZB_AHEAD; a++) {
+    for (int a = 1; a <= z.ahead; a++) {
         const int64_t cc = c0 + 32 * a;
         if (P >= 32 || cc >= ns) break;
         const int64_t j = cc + lane;
@@ -646,7 +681,7 @@ __device__ __forceinline__ void lazy_chunk_eval(const WarpRow<E> &s, int k, cons
     if (z.tag == 1) v = lazy_batch_t<1>(z, r, P, b, lane);
     else if (z.tag == 0) v = lazy_batch_t<0>(z, r, P, b, lane);
     else v = lazy_batch_t<2>(z, r, P, b, lane);
-    if (lane == 0) nexact += (unsigned long long)P;
+    if (lane == 0) nexact += (unsigned long long)P | (1ull << 40);  // pairs | batches << 40
     cpos = (int)lane < P ? b.spos[lane] : 0xffffffffu;
     cval = v;
     __syncwarp();

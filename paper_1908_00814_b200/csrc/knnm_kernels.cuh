@@ -2467,7 +2467,7 @@ constexpr int APPLY_WARPS = 4;
 // skipped by ballot, the rest go through warp_insert in slot order -- which
 // is the reference's sequential order, so no sorting is needed.
 template <int E, int MODE, bool F32 = false>
-__global__ void __launch_bounds__(APPLY_WARPS * 32)
+__global__ void __launch_bounds__(APPLY_WARPS * 32, 6)
 k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double *__restrict__ Bd,
                const int32_t *__restrict__ Bs, int32_t *ids, double *dists, uint8_t *flags,
                int32_t *sizes, unsigned long long *counters, LazyExact z) {
@@ -2546,7 +2546,8 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
         nexact += __shfl_xor_sync(FULL_MASK, nexact, o);
     }
     if (lane == 0 && written) atomicAdd(&counters[C_WRITTEN], written);
-    if (lane == 0 && nexact) atomicAdd(&counters[C_EXACT], nexact);
+    if (lane == 0 && (nexact & ((1ull << 40) - 1))) atomicAdd(&counters[C_EXACT], nexact & ((1ull << 40) - 1));
+    if (lane == 0 && (nexact >> 40)) atomicAdd(&counters[C_LZ_BATCHES], nexact >> 40);
 }
 
 // Written-slot compaction for the sharded exchange: an unwritten slot (NaN
@@ -2604,7 +2605,7 @@ __global__ void k_worst0_all(const int32_t *__restrict__ sizes, const double *__
 // which is the reference's order.  off[s * (no+1) + i] = element offset of
 // row lo+i's segment in the receive buffers.
 template <int E, int MODE>
-__global__ void __launch_bounds__(APPLY_WARPS * 32)
+__global__ void __launch_bounds__(APPLY_WARPS * 32, 6)
 k_apply_stream_multi(int64_t lo, int64_t no, int k, int nsrc, const uint64_t *__restrict__ off,
                      const uint32_t *__restrict__ cnt, const double *__restrict__ Bd,
                      const int32_t *__restrict__ Bs, int32_t *ids, double *dists, uint8_t *flags,
@@ -2666,7 +2667,8 @@ k_apply_stream_multi(int64_t lo, int64_t no, int k, int nsrc, const uint64_t *__
     if (lane == 0 && acc) atomicAdd(&counters[C_ACCEPTED], acc);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) nexact += __shfl_xor_sync(FULL_MASK, nexact, o);
-    if (lane == 0 && nexact) atomicAdd(&counters[C_EXACT], nexact);
+    if (lane == 0 && (nexact & ((1ull << 40) - 1))) atomicAdd(&counters[C_EXACT], nexact & ((1ull << 40) - 1));
+    if (lane == 0 && (nexact >> 40)) atomicAdd(&counters[C_LZ_BATCHES], nexact >> 40);
 }
 
 // ---- replication of owned rows (sharded rounds) --------------------------
