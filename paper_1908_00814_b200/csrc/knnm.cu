@@ -133,6 +133,9 @@ struct knnm_ctx {
     int join_variant = -1;  // -1 auto, 0 exact (fp64 every pair), 1 tiled, 2 tensor core
     int bf_variant = -1;    // brute force: -1 auto, 0 SIMT exact, 1 tcgen05 (certified u8 only)
     int lazy_ahead = LZB_AHEAD;  // look-ahead chunks of a lazy evaluation batch (KNNM_LAZY_AHEAD)
+    // rows longer than this defer exact values to the apply (KNNM_LAZY_MIN_D;
+    // measured: config 4, d = 100, is faster exact-in-join, config 3, d = 960, lazy)
+    int lazy_min_d = 384;
     int bf_last_route = 0;  // route the last knnm_bf_topk took (0 SIMT, 1 tcgen05)
     DBuf bfq, bfqn, bfpart;  // brute force: gathered query rows / norms, partial lists
     bool bf_u8 = false;      // integers in [0, 255]: exact u8 Gram tiles for brute force
@@ -436,9 +439,6 @@ int rank_memberships(knnm_ctx *c, bool fused = false) {
 // bit set) are written only by the non-certified tiled join.
 bool metric_is_cos(const knnm_ctx *c) { return c->metric == KNNM_COSINE; }
 
-// Row length above which non-certified joins defer exact evaluation to the
-// apply (measured crossover: d = 100 favours the join, d = 960 the apply).
-constexpr int LAZY_MIN_D = 384;
 
 LazyExact lazy_of(knnm_ctx *c) {
     LazyExact z;
@@ -677,6 +677,7 @@ int knnm_create(int device, knnm_ctx **out) {
     CK(cudaGetDeviceProperties(&prop, device));
     c->sms = prop.multiProcessorCount;
     if (const char *e = getenv("KNNM_LAZY_AHEAD")) c->lazy_ahead = std::max(0, std::min(64, atoi(e)));
+    if (const char *e = getenv("KNNM_LAZY_MIN_D")) c->lazy_min_d = std::max(0, atoi(e));
     CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     CK(cudaHostAlloc((void **)&c->hcnt, sizeof(unsigned long long) * C_NUM, cudaHostAllocDefault));
     TRY(ensure(c->counters, sizeof(unsigned long long) * C_NUM));
@@ -1317,8 +1318,8 @@ static int join_route(knnm_ctx *c, int W, int mode, JoinRoute *r) {
     // hood does not fit shared memory (e.g. d = 960 with k >= 27)
     const bool tiled_fits = smem_tiled <= 200 * 1024;
     const bool tiled = !use_mma && c->join_variant != 0 &&
-                       (c->join_variant == 1 || tiled_fits || c->d > LAZY_MIN_D);
-    const bool lazy = tiled && ((!c->cert && c->d > LAZY_MIN_D) || !tiled_fits);
+                       (c->join_variant == 1 || tiled_fits || c->d > c->lazy_min_d);
+    const bool lazy = tiled && ((!c->cert && c->d > c->lazy_min_d) || !tiled_fits);
     if (!use_mma && !tiled && smem > 200 * 1024)
         return fail(KNNM_ERR_LIMIT, "neighbourhood of %d x %d floats exceeds shared memory", W, c->dp);
     if (tiled && !lazy && !tiled_fits)

@@ -375,7 +375,7 @@ __device__ __forceinline__ double slot_lower(double v, const LazyExact z) {
 // Resolve the lane's slot for row r: returns the distance to apply (+inf when
 // the slot cannot pass the row's current state).  need = approximate slot
 // whose lower bound beats the current worst: its exact value must be
-// computed (lazy_warp_eval) before the chunk is applied.
+// computed (lazy_chunk_eval) before the chunk is applied.
 template <int E>
 __device__ __forceinline__ double lazy_resolve(const WarpRow<E> &s, int k, bool in, double dl,
                                                const int32_t *__restrict__ Bs, uint64_t pos,
@@ -400,116 +400,6 @@ __device__ __forceinline__ double lazy_resolve(const WarpRow<E> &s, int k, bool 
     }
     if (!pre || apx) return inf;  // approximate: replaced by the exact value if needed
     return dl;
-}
-
-// Exact reference metric for every lane with need set, computed by the whole
-// warp: groups of up to LZ_G pairs; for each block of 32 dimensions lane t
-// forms the terms of dimension t0 + t for all pairs of the group (coalesced
-// loads, one row conversion shared by the group), the terms go through
-// shared memory, and lane j folds pair j's terms sequentially in index order
-// -- the reference's exact sequence of fp64 roundings (_kernels.py:43-80).
-constexpr int LZ_G = 8;
-constexpr int LZ_S = 33;  // padded term stride (conflict-free column reads)
-
-template <int TAG>
-__device__ __forceinline__ double lz_term(double x, double y) {
-    if (TAG == 1) {
-        const double t = __dsub_rn(x, y);
-        return __dmul_rn(t, t);
-    }
-    if (TAG == 0) return fabs(__dsub_rn(x, y));
-    return __dmul_rn(x, y);
-}
-
-template <int TAG>
-__device__ __noinline__ double lazy_warp_eval_t(const LazyExact z, int64_t r, bool need, int src, double dl,
-                                                double *__restrict__ sm, unsigned lane) {
-    unsigned M = __ballot_sync(FULL_MASK, need);
-    const float *ra = z.sub + r * z.dp;
-    while (M) {
-        // the group: the first (up to) LZ_G lanes of M
-        int cid[LZ_G];
-        unsigned mm = M;
-        int P = 0;
-#pragma unroll
-        for (int j = 0; j < LZ_G; j++) {
-            cid[j] = 0;
-            if (mm) {
-                const int pl = __ffs(mm) - 1;
-                mm &= mm - 1;
-                cid[j] = __shfl_sync(FULL_MASK, src, pl);
-                P = j + 1;
-            } else {
-                (void)__shfl_sync(FULL_MASK, src, 0);
-            }
-        }
-        const unsigned grp = M & ~mm;
-        M = mm;
-        // pull the group's rows toward L2 first: the block loads below then
-        // wait on L2 instead of HBM latency
-        {
-            const int lines = (z.d * 4 + 127) >> 7;
-            for (int j = 0; j <= LZ_G; j++) {
-                if (j < P || j == LZ_G) {
-                    const float *rp = j == LZ_G ? ra : z.sub + (int64_t)cid[j < LZ_G ? j : 0] * z.dp;
-                    for (int l = (int)lane; l < lines; l += 32)
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + l * 32));
-                }
-            }
-        }
-        double acc = 0.0;
-        // one block ahead in registers
-        float xn = lane < (unsigned)z.d ? __ldg(ra + lane) : 0.f;
-        float yn[LZ_G];
-#pragma unroll
-        for (int j = 0; j < LZ_G; j++)
-            yn[j] = (j < P && lane < (unsigned)z.d) ? __ldg(z.sub + (int64_t)cid[j] * z.dp + lane) : 0.f;
-        for (int t0 = 0; t0 < z.d; t0 += 32) {
-            const float xc = xn;
-            float yc[LZ_G];
-#pragma unroll
-            for (int j = 0; j < LZ_G; j++) yc[j] = yn[j];
-            const int tn = t0 + 32 + (int)lane;
-            if (t0 + 32 < z.d) {
-                xn = tn < z.d ? __ldg(ra + tn) : 0.f;
-#pragma unroll
-                for (int j = 0; j < LZ_G; j++)
-                    yn[j] = (j < P && tn < z.d) ? __ldg(z.sub + (int64_t)cid[j] * z.dp + tn) : 0.f;
-            }
-            const double x = (double)xc;
-#pragma unroll
-            for (int j = 0; j < LZ_G; j++)
-                if (j < P) sm[j * LZ_S + lane] = lz_term<TAG>(x, (double)yc[j]);
-            __syncwarp();
-            if ((int)lane < P) {
-                const int nb = z.d - t0 < 32 ? z.d - t0 : 32;
-                const double *col = sm + lane * LZ_S;
-                for (int i = 0; i < nb; i++) acc = __dadd_rn(acc, col[i]);
-            }
-            __syncwarp();
-        }
-        if (TAG == 2 && (int)lane < P) {
-            int my = 0;
-#pragma unroll
-            for (int j = 0; j < LZ_G; j++)
-                if (j == (int)lane) my = cid[j];
-            acc = cos_finish(acc, z.nrm64[r], z.nrm64[my]);
-        }
-        // hand pair j's value to its lane
-        const int rank = __popc(grp & lanemask_lt());
-        const double v = __shfl_sync(FULL_MASK, acc, rank < LZ_G ? rank : 0);
-        if ((grp >> lane) & 1u) dl = v;
-    }
-    return dl;
-}
-
-__device__ __forceinline__ void lazy_warp_eval(const LazyExact z, int64_t r, bool need, int src, double &dl,
-                                               double *sm, unsigned lane, unsigned long long &nexact) {
-    const unsigned m = __ballot_sync(FULL_MASK, need);
-    if (lane == 0) nexact += (unsigned long long)__popc(m);
-    if (z.tag == 1) dl = lazy_warp_eval_t<1>(z, r, need, src, dl, sm, lane);
-    else if (z.tag == 0) dl = lazy_warp_eval_t<0>(z, r, need, src, dl, sm, lane);
-    else dl = lazy_warp_eval_t<2>(z, r, need, src, dl, sm, lane);
 }
 
 // ---------------------------------------------------------------------------
