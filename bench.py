@@ -434,7 +434,7 @@ def config_legs(km, names, device, steps, warmup, hbm_peak, no_recall=False):
                      ("tensor-core" if inf["cert_dot"] else "tiled fp32 screen + exact fp64"),
             "kernels": kr, "recall_at_10": rec, "setup_seconds": round(setup, 1),
             "phases_ms_per_step": {key: st[key] / steps for key in
-                                   ("join_kernel_ms", "apply_kernel_ms", "reverse_ms",
+                                   ("join_ms", "join_kernel_ms", "apply_kernel_ms", "reverse_ms",
                                     "assemble_ms", "update_ms", "other_ms")},
         }
         del g, h, u, ds

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <functional>
+#include <memory>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -658,6 +659,220 @@ void host_choice(HostPcg &p, int64_t pop, int64_t size, int64_t *out, std::vecto
         std::swap(out[i], out[j]);
     }
 }
+// ---- the per-row choice loop, parallel ------------------------------------
+// numpy's per-row Generator.choice(pool, k, replace=False) calls share one
+// PCG64 stream, so row r's draws start where row r-1's ended.  Every draw is
+// one 32-bit word of the stream except for Lemire rejections (probability
+// < pool / 2^32 per draw).  So: (1) the 64-bit outputs are generated in
+// parallel by LCG jump-ahead into a word buffer; (2) one sequential pass
+// finds each row's first word by replaying only the draw *counts* (a
+// multiply-compare per draw, no sets, no shuffles); (3) the rows are then
+// computed in parallel from their own offsets by host_choice over a buffer
+// reader -- the same arithmetic, so the same values, and the generator ends
+// in the same state.
+struct WordPcg {  // host_choice's interface over a pre-generated word buffer
+    const uint32_t *w;
+    size_t i, n;
+    bool ok = true;
+    uint32_t next32() {
+        if (i >= n) { ok = false; return 0; }
+        return w[i++];
+    }
+    uint64_t bounded(uint64_t rng) {
+        if (rng == 0) return 0;
+        if (rng == 0xFFFFFFFFull) return next32();
+        const uint64_t excl = rng + 1;
+        uint64_t m = (uint64_t)next32() * excl;
+        uint32_t left = (uint32_t)m;
+        if (left < excl) {
+            const uint32_t thr = (uint32_t)((0xFFFFFFFFull - rng) % excl);
+            while (left < thr && ok) {
+                m = (uint64_t)next32() * excl;
+                left = (uint32_t)m;
+            }
+        }
+        return m >> 32;
+    }
+};
+
+template <typename G>
+void choice_draws(G &p, int64_t pop, int64_t size, int64_t *out, std::vector<uint64_t> &hs,
+                  std::vector<int64_t> &tmp) {
+    if (pop > 10000 && size > pop / 50) {  // tail shuffle
+        tmp.resize(pop);
+        for (int64_t i = 0; i < pop; i++) tmp[i] = i;
+        for (int64_t i = pop - 1; i >= std::max<int64_t>(pop - size, 1); i--) {
+            const int64_t j = (int64_t)p.bounded((uint64_t)i);
+            std::swap(tmp[i], tmp[j]);
+        }
+        for (int64_t t = 0; t < size; t++) out[t] = tmp[pop - size + t];
+        return;
+    }
+    uint64_t mask = (uint64_t)(1.2 * (double)size);
+    for (int sh = 1; sh < 64; sh <<= 1) mask |= mask >> sh;
+    hs.assign(mask + 1, ~0ull);
+    for (int64_t j = pop - size; j < pop; j++) {
+        const uint64_t val = p.bounded((uint64_t)j);
+        uint64_t loc = val & mask;
+        while (hs[loc] != ~0ull && hs[loc] != val) loc = (loc + 1) & mask;
+        if (hs[loc] == ~0ull) {
+            hs[loc] = val;
+            out[j - pop + size] = (int64_t)val;
+        } else {
+            loc = (uint64_t)j & mask;
+            while (hs[loc] != ~0ull) loc = (loc + 1) & mask;
+            hs[loc] = (uint64_t)j;
+            out[j - pop + size] = j;
+        }
+    }
+    for (int64_t i = size - 1; i >= 1; i--) {
+        const int64_t j = (int64_t)p.bounded((uint64_t)i);
+        std::swap(out[i], out[j]);
+    }
+}
+
+// Words a row's draws consume from the reader (its values are not needed).
+void choice_skip(WordPcg &p, int64_t pop, int64_t size) {
+    if (pop > 10000 && size > pop / 50) {
+        for (int64_t i = pop - 1; i >= std::max<int64_t>(pop - size, 1); i--) p.bounded((uint64_t)i);
+        return;
+    }
+    for (int64_t j = pop - size; j < pop; j++) p.bounded((uint64_t)j);
+    for (int64_t i = size - 1; i >= 1; i--) p.bounded((uint64_t)i);
+}
+
+// LCG jump-ahead of the PCG64 state by `delta` steps.
+unsigned __int128 pcg_advance(unsigned __int128 s, unsigned __int128 inc, uint64_t delta) {
+    unsigned __int128 cm = HostPcg::mult(), cp = inc, am = 1, ap = 0;
+    while (delta) {
+        if (delta & 1) {
+            am *= cm;
+            ap = ap * cm + cp;
+        }
+        cp = (cm + 1) * cp;
+        cm *= cm;
+        delta >>= 1;
+    }
+    return am * s + ap;
+}
+
+// 64-bit outputs [first, first + count) after state s0 (output i comes from
+// the state advanced i + 1 times), as 32-bit words lo, hi.
+void pcg_words(unsigned __int128 s0, unsigned __int128 inc, uint64_t first, uint64_t count, uint32_t *out) {
+    unsigned __int128 s = pcg_advance(s0, inc, first);
+    for (uint64_t i = 0; i < count; i++) {
+        s = s * HostPcg::mult() + inc;
+        const uint64_t x = (uint64_t)(s >> 64) ^ (uint64_t)s;
+        const unsigned r = (unsigned)(s >> 122);
+        const uint64_t v = (x >> r) | (x << ((64u - r) & 63u));
+        out[2 * i] = (uint32_t)v;
+        out[2 * i + 1] = (uint32_t)(v >> 32);
+    }
+}
+
+// Parallel form of the per-row loop; returns false when the word estimate
+// was short (the caller then runs the sequential loop).
+bool sample_rows_parallel(HostPcg &p, int64_t n, int32_t k, const int32_t *exclude, int64_t nrows,
+                          int64_t *out) {
+    auto pool_of = [&](int64_t r) {
+        const int64_t ex = exclude[r];
+        return (ex >= 0 && ex < n) ? n - 1 : n;
+    };
+    // nominal words per row (+ slack for rejections)
+    uint64_t nominal = 0;
+    for (int64_t r = 0; r < nrows; r++) {
+        const int64_t pop = pool_of(r);
+        nominal += (pop > 10000 && k > pop / 50) ? (uint64_t)std::min<int64_t>(k, pop - 1) : (uint64_t)(2 * k - 1);
+    }
+    const uint64_t need = nominal + nominal / 256 + 4096;
+    const uint64_t outs = need / 2 + 1;
+    // (uninitialised: every word is written by the generator threads)
+    std::unique_ptr<uint32_t[]> bufp(new uint32_t[1 + 2 * outs]);
+    uint32_t *buf = bufp.get();
+    const size_t nbuf = 1 + 2 * outs;
+    const size_t base = p.has ? 0 : 1;  // word 0 = the buffered half when present
+    buf[0] = p.u;
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const uint64_t nt = std::min<uint64_t>(std::min(16u, hw), std::max<uint64_t>(1, outs >> 16));
+    {
+        std::vector<std::thread> th;
+        const uint64_t part = (outs + nt - 1) / nt;
+        for (uint64_t t = 0; t < nt; t++) {
+            const uint64_t a = t * part, b = std::min(outs, a + part);
+            if (a >= b) break;
+            th.emplace_back(pcg_words, p.s, p.inc, a, b - a, buf + 1 + 2 * a);
+        }
+        for (auto &x : th) x.join();
+    }
+    // sequential pass: each row's first word.  A Floyd row without a
+    // rejection candidate (low word of w * excl below excl, checked for all
+    // its draws at once: a vectorisable loop) consumes exactly 2k - 1 words;
+    // any other row is replayed draw by draw.
+    std::vector<uint64_t> start(nrows + 1);
+    WordPcg rd{buf + base, 0, nbuf - base};
+    for (int64_t r = 0; r < nrows; r++) {
+        start[r] = rd.i;
+        const int64_t pop = pool_of(r);
+        const bool floyd = !(pop > 10000 && k > pop / 50);
+        if (floyd && k >= 1 && rd.i + 2 * (size_t)k - 1 <= rd.n) {
+            const uint32_t *w = rd.w + rd.i;
+            uint32_t flag = 0;
+            for (int d2 = 0; d2 < k; d2++) {
+                const uint32_t excl = (uint32_t)(pop - k + d2 + 1);
+                flag |= (uint32_t)(w[d2] * excl) < excl;
+            }
+            for (int d2 = 0; d2 < k - 1; d2++) {
+                const uint32_t excl = (uint32_t)(k - d2);
+                flag |= (uint32_t)(w[k + d2] * excl) < excl;
+            }
+            if (!flag) {
+                rd.i += 2 * (size_t)k - 1;
+                continue;
+            }
+        }
+        choice_skip(rd, pop, k);
+        if (!rd.ok) return false;
+    }
+    start[nrows] = rd.i;
+    // the rows, in parallel
+    {
+        const uint64_t nr = (uint64_t)nrows;
+        const uint64_t ntr = std::min<uint64_t>(std::min(16u, hw), std::max<uint64_t>(1, nr >> 12));
+        std::vector<std::thread> th;
+        const uint64_t part = (nr + ntr - 1) / ntr;
+        for (uint64_t t = 0; t < ntr; t++) {
+            const uint64_t a = t * part, b = std::min(nr, a + part);
+            if (a >= b) break;
+            th.emplace_back([&, a, b] {
+                std::vector<uint64_t> hs;
+                std::vector<int64_t> tmp;
+                for (uint64_t r = a; r < b; r++) {
+                    WordPcg w{buf + base, (size_t)start[r], (size_t)start[r + 1]};
+                    int64_t *o = out + r * k;
+                    choice_draws(w, pool_of((int64_t)r), k, o, hs, tmp);
+                    const int64_t ex = exclude[r];
+                    if (ex >= 0 && ex < n)
+                        for (int t2 = 0; t2 < k; t2++) o[t2] += o[t2] >= ex ? 1 : 0;
+                }
+            });
+        }
+        for (auto &x : th) x.join();
+    }
+    // generator state after the consumed words
+    const uint64_t used = start[nrows];  // words read from buf[base ...]
+    const uint64_t from_pairs = p.has ? (used > 0 ? used - 1 : 0) : used;
+    if (p.has && used == 0) return true;  // nothing consumed
+    const uint64_t nout = (from_pairs + 1) / 2;
+    p.s = pcg_advance(p.s, p.inc, nout);
+    if (from_pairs & 1) {
+        p.has = 1;
+        p.u = buf[1 + 2 * (nout - 1) + 1];
+    } else {
+        p.has = 0;
+    }
+    return true;
+}
+
 }  // namespace
 
 extern "C" {
@@ -2291,6 +2506,21 @@ int knnm_sample_distinct_rows(uint64_t *pcg, int32_t *has_uint32, uint32_t *uint
     p.inc = ((unsigned __int128)pcg[2] << 64) | pcg[3];
     p.has = *has_uint32;
     p.u = *uinteger;
+    for (int64_t r = 0; r < nrows; r++) {
+        const int64_t ex = exclude[r];
+        const int64_t pool = (ex >= 0 && ex < n) ? n - 1 : n;  // core.py:222-230
+        if (k > pool) return fail(KNNM_ERR_ARG, "not enough values to sample from");
+        if (pool > 0xFFFFFFFFll) return fail(KNNM_ERR_LIMIT, "population too large");
+    }
+    HostPcg p0 = p;
+    if (nrows >= 4096 && sample_rows_parallel(p, n, k, exclude, nrows, out)) {
+        pcg[0] = (uint64_t)(p.s >> 64);
+        pcg[1] = (uint64_t)p.s;
+        *has_uint32 = p.has;
+        *uinteger = p.u;
+        return KNNM_OK;
+    }
+    p = p0;
     std::vector<uint64_t> hs;
     std::vector<int64_t> tmp;
     for (int64_t r = 0; r < nrows; r++) {
