@@ -1264,15 +1264,24 @@ static int insert_impl(knnm_ctx *c, const int32_t *rows, int64_t mrows, int32_t 
         PhaseTimer pt(c, PH_UPDATE);
         CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long) * C_NUM, c->st));
         const int E = (c->k + 31) / 32;
-        const int blocks = grid_for(c, mrows * 32, 256, 8);
-#define KNNM_IRD_LAUNCH(EE)                                                                          \
-    k_insert_rows_direct<EE><<<blocks, 256, 0, c->st>>>(                                            \
+        const int certi = (int)(c->cert && c->metric != KNNM_COSINE);
+        // non-certified rows (exact fp64 values): batched folds from d = 64
+        const bool batch = !c->cert_u8 && !certi && c->d >= 64;
+        const int thr = batch ? 128 : 256;
+        const int blocks = grid_for(c, mrows * 32, thr, 8);
+#define KNNM_IRD_LAUNCH(EE, BB)                                                                      \
+    k_insert_rows_direct<EE, BB><<<blocks, thr, 0, c->st>>>(                                        \
         c->stage[3].as<int32_t>(), mrows, count, c->stage[1].as<int32_t>(), c->subp, c->dp, c->d,    \
-        c->metric, (int)(c->cert && c->metric != KNNM_COSINE), c->cert_u8 ? c->sub16p : nullptr,     \
+        c->metric, certi, c->cert_u8 ? c->sub16p : nullptr,                                          \
         c->rowb, c->cert_u8 ? c->subnormp : nullptr, c->ids.as<int32_t>(), c->dists.as<double>(),   \
-        c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), c->k, capd, cnt)
-        if (E == 1) KNNM_IRD_LAUNCH(1);
-        else KNNM_IRD_LAUNCH(2);
+        c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), c->k, capd, cnt, lazy_of(c))
+        if (E == 1) {
+            if (batch) KNNM_IRD_LAUNCH(1, true);
+            else KNNM_IRD_LAUNCH(1, false);
+        } else {
+            if (batch) KNNM_IRD_LAUNCH(2, true);
+            else KNNM_IRD_LAUNCH(2, false);
+        }
 #undef KNNM_IRD_LAUNCH
         CKL();
         TRY(sync_counters(c));

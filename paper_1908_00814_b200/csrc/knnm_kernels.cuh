@@ -457,13 +457,17 @@ __global__ void k_directed_emit(const int32_t *__restrict__ rows, const int32_t 
 // (_kernels.py:208-214) is _insert per candidate in input order, rows
 // independent, so one warp per row applies them straight from registers --
 // no bucket layout, ranking or slot round trip.  Distances as k_directed_emit.
-template <int E>
-__global__ void __launch_bounds__(256)
+// BATCH (non-certified rows): a chunk's up to 32 exact values are folded
+// together by lazy_batch_t (cp.async-staged dimension blocks, one pair per
+// lane) instead of one strided sequential scan per lane.
+template <int E, bool BATCH>
+__global__ void __launch_bounds__(BATCH ? 128 : 256)
 k_insert_rows_direct(const int32_t *__restrict__ rows, int64_t mrows, int count,
                      const int32_t *__restrict__ nids, const float *__restrict__ sub, int dp, int d,
                      int tag, int cert, const uint8_t *__restrict__ sub8, int rowb,
                      const float *__restrict__ norms8, int32_t *ids, double *dists, uint8_t *flags,
-                     int32_t *sizes, int k, double *cap_d, unsigned long long *counters) {
+                     int32_t *sizes, int k, double *cap_d, unsigned long long *counters, LazyExact z) {
+    __shared__ LazyBatchSmem s_b[BATCH ? 4 : 1];
     const unsigned lane = lane_id();
     const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
     unsigned long long acc = 0;
@@ -476,14 +480,26 @@ k_insert_rows_direct(const int32_t *__restrict__ rows, int64_t mrows, int count,
             const int t = t0 + (int)lane;
             int32_t src = 0;
             double dd = 0.0;
-            if (t < count) {
+            const int cnt = count - t0 < 32 ? count - t0 : 32;
+            if constexpr (BATCH) {
+                LazyBatchSmem &b = s_b[threadIdx.x >> 5];
+                if (t < count) {
+                    src = nids[i * count + t];
+                    b.sid[lane] = src;
+                }
+                __syncwarp();
+                if (z.tag == 1) dd = lazy_batch_t<1>(z, r, cnt, b, lane);
+                else if (z.tag == 0) dd = lazy_batch_t<0>(z, r, cnt, b, lane);
+                else dd = lazy_batch_t<2>(z, r, cnt, b, lane);
+                if (t < count && cap_d) cap_d[i * count + t] = dd;
+                __syncwarp();
+            } else if (t < count) {
                 src = nids[i * count + t];
                 dd = sub8 ? u8_dist(sub8 + (int64_t)r * rowb, sub8 + (int64_t)src * rowb, rowb, norms8[r], norms8[src])
                    : cert ? cert_dist(sub + (int64_t)r * dp, sub + (int64_t)src * dp, dp, tag)
                           : exact_dist_tag(tag, sub + (int64_t)r * dp, sub + (int64_t)src * dp, d);
                 if (cap_d) cap_d[i * count + t] = dd;
             }
-            const int cnt = count - t0 < 32 ? count - t0 : 32;
             for (int j = 0; j < cnt; j++) {
                 const int sj = __shfl_sync(FULL_MASK, src, j);
                 const double dj = __shfl_sync(FULL_MASK, dd, j);
