@@ -1231,11 +1231,12 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
         // 2x2 tile sit in different halves, so consecutive tiles of a warp
         // read consecutive rows (16 B apart modulo 128 B: conflict-free).
         const int H = (w + 1) >> 1;
-        if (tid == 0) {
+        if (warp == 0) {  // the copies are issued by all lanes of warp 0
             fence_proxy_async();
             const uint32_t row_bytes = (uint32_t)dp * 4u;
-            mbar_expect_tx(&s_bar, row_bytes * (uint32_t)w);
-            for (int sl = 0; sl < w; sl++)
+            if (lane == 0) mbar_expect_tx(&s_bar, row_bytes * (uint32_t)w);
+            __syncwarp();
+            for (int sl = (int)lane; sl < w; sl += 32)
                 bulk_g2s(sv4 + (size_t)((sl & 1) * H + (sl >> 1)) * qs, sub + (int64_t)s_id[sl] * dp,
                          row_bytes, &s_bar);
         }
@@ -1578,13 +1579,14 @@ k_join_chunked(const int32_t *__restrict__ active, int nactive, const uint32_t *
         auto rowc = [&](int buf, int sl) { return cv4 + ((size_t)buf * W + (size_t)((sl & 1) * H + (sl >> 1))) * QC; };
         // TMA: chunk c of every member row into buffer c & 1
         auto issue = [&](int c) {
-            if (tid == 0) {
+            if (warp == 0) {  // the copies are issued by all lanes of warp 0
                 const int b = c & 1;
                 const int cw = min(CJ_DC, dp - c * CJ_DC);
                 const uint32_t bytes = (uint32_t)cw * 4u;
                 fence_proxy_async();
-                mbar_expect_tx(&s_bar[b], bytes * (uint32_t)w);
-                for (int sl = 0; sl < w; sl++)
+                if (lane == 0) mbar_expect_tx(&s_bar[b], bytes * (uint32_t)w);
+                __syncwarp();
+                for (int sl = (int)lane; sl < w; sl += 32)
                     bulk_g2s(rowc(b, sl), sub + (int64_t)s_id[sl] * dp + (int64_t)c * CJ_DC, bytes, &s_bar[b]);
             }
         };
