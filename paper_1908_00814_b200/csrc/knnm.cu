@@ -1673,7 +1673,7 @@ c->subp, c->dp, c->d, c->worst0.as<double>(), boff, stt, Bd, Bs, lo_rel, lo_abs,
                 else KNNM_TJ_LAUNCH(0, true, false);
             } else if (lazy) {
                 // rows stream through two CJ_DC-dimension buffers
-                const size_t smem_cj = 2 * (size_t)W * (CJ_DC / 4 + 1) * sizeof(float4);
+                const size_t smem_cj = CJ_NBUF * (size_t)W * (CJ_DC / 4 + 1) * sizeof(float4);
                 const void *fc = c->metric == 1 ? (const void *)k_join_chunked<1>
                                  : c->metric == 2 ? (const void *)k_join_chunked<2>
                                                   : (const void *)k_join_chunked<0>;

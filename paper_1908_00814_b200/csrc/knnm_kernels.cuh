@@ -1487,9 +1487,10 @@ k_join_tiled(const int32_t *__restrict__ active, int nactive, const uint32_t *__
 constexpr int CJ_DC = 128;  // dimensions per chunk
 constexpr int CJ_TPW = 2;   // patches per warp per pass
 constexpr int CJ_WARPS = 8;
+constexpr int CJ_NBUF = 2;  // chunk buffers (3 measured slower: 480 vs 467 ms at config 3, fewer CTAs per SM)
 
 template <int TAG>
-__global__ void __launch_bounds__(CJ_WARPS * 32, 3)
+__global__ void __launch_bounds__(CJ_WARPS * 32, 4)
 k_join_chunked(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
                const int32_t *__restrict__ nlen, int W, int mode, const float *__restrict__ sub,
                int dp, const double *__restrict__ worst0, const uint64_t *__restrict__ boff,
@@ -1505,19 +1506,17 @@ k_join_chunked(const int32_t *__restrict__ active, int nactive, const uint32_t *
     __shared__ int s_sc[MAX_W];
     __shared__ PosPrefix s_P;
     __shared__ int s_cls[4];
-    __shared__ __align__(8) uint64_t s_bar[2];
+    __shared__ __align__(8) uint64_t s_bar[CJ_NBUF];
     const int tid = threadIdx.x;
     const unsigned lane = lane_id();
     const int warp = tid >> 5;
     constexpr int nwarps = CJ_WARPS;
     constexpr int QC = CJ_DC / 4 + 1;  // padded chunk row stride in float4
     const int nch = (dp + CJ_DC - 1) / CJ_DC;
-    if (tid == 0) {
-        mbar_init(&s_bar[0], 1);
-        mbar_init(&s_bar[1], 1);
-    }
+    if (tid == 0)
+        for (int b = 0; b < CJ_NBUF; b++) mbar_init(&s_bar[b], 1);
     __syncthreads();
-    uint32_t phase0 = 0, phase1 = 0;
+    uint32_t phases = 0;  // bit b: parity of buffer b's next completion
 
     for (int hi = blockIdx.x; hi < nactive; hi += gridDim.x) {
         const int64_t u = active[hi];
@@ -1577,10 +1576,10 @@ k_join_chunked(const int32_t *__restrict__ active, int nactive, const uint32_t *
         __syncthreads();
         const int H = (w + 1) >> 1;  // even/odd slot split (see k_join_tiled)
         auto rowc = [&](int buf, int sl) { return cv4 + ((size_t)buf * W + (size_t)((sl & 1) * H + (sl >> 1))) * QC; };
-        // TMA: chunk c of every member row into buffer c & 1
+        // TMA: chunk c of every member row into buffer c % CJ_NBUF
         auto issue = [&](int c) {
             if (warp == 0) {  // the copies are issued by all lanes of warp 0
-                const int b = c & 1;
+                const int b = c % CJ_NBUF;
                 const int cw = min(CJ_DC, dp - c * CJ_DC);
                 const uint32_t bytes = (uint32_t)cw * 4u;
                 fence_proxy_async();
@@ -1627,13 +1626,14 @@ k_join_chunked(const int32_t *__restrict__ active, int nactive, const uint32_t *
             float acc[CJ_TPW][2][2];
 #pragma unroll
             for (int t = 0; t < CJ_TPW; t++) acc[t][0][0] = acc[t][0][1] = acc[t][1][0] = acc[t][1][1] = 0.f;
-            issue(0);
-            if (nch > 1) issue(1);
+            for (int c = 0; c < CJ_NBUF - 1 && c < nch; c++) issue(c);
             for (int c = 0; c < nch; c++) {
-                const int b = c & 1;
-                mbar_wait(&s_bar[b], b ? phase1 : phase0);
-                if (b) phase1 ^= 1u;
-                else phase0 ^= 1u;
+                const int b = c % CJ_NBUF;
+                // chunk c + NBUF - 1 goes into the buffer chunk c - 1 left
+                // free (the barrier at the end of the previous step)
+                if (c + CJ_NBUF - 1 < nch) issue(c + CJ_NBUF - 1);
+                mbar_wait(&s_bar[b], (phases >> b) & 1u);
+                phases ^= 1u << b;
                 const int q4c = min(CJ_DC, dp - c * CJ_DC) >> 2;
 #pragma unroll
                 for (int t = 0; t < CJ_TPW; t++) {
@@ -1710,7 +1710,7 @@ k_join_chunked(const int32_t *__restrict__ active, int nactive, const uint32_t *
                     }
                 }
                 __syncthreads();  // buffer b is free again
-                if (c + 2 < nch) issue(c + 2);
+
             }
             // ---- emission: approximate slots (LazyExact), as k_join_tiled ----
 #pragma unroll
