@@ -859,17 +859,15 @@ bool sample_rows_parallel(HostPcg &p, int64_t n, int32_t k, const int32_t *exclu
         for (auto &x : th) x.join();
     }
     // generator state after the consumed words
+    // (numpy: fetching a 64-bit output stores its high half and sets the
+    // flag; consuming the stored half only clears the flag)
     const uint64_t used = start[nrows];  // words read from buf[base ...]
-    const uint64_t from_pairs = p.has ? (used > 0 ? used - 1 : 0) : used;
-    if (p.has && used == 0) return true;  // nothing consumed
+    if (used == 0) return true;          // nothing consumed
+    const uint64_t from_pairs = p.has ? used - 1 : used;
     const uint64_t nout = (from_pairs + 1) / 2;
     p.s = pcg_advance(p.s, p.inc, nout);
-    if (from_pairs & 1) {
-        p.has = 1;
-        p.u = buf[1 + 2 * (nout - 1) + 1];
-    } else {
-        p.has = 0;
-    }
+    if (nout > 0) p.u = buf[2 + 2 * (nout - 1)];
+    p.has = (from_pairs & 1) ? 1 : 0;
     return true;
 }
 

@@ -183,3 +183,26 @@ def test_native_merge_members_parallel_labels(n, split, shared):
         assert len(labs) == 1 and np.array_equal(labs[0], lab)
     else:
         assert labs == []
+
+
+@pytest.mark.parametrize("n,k,nrows,pre", [(1_000_000, 20, 6000, 1), (1_000_000, 20, 6000, 2),
+                                           (8000, 40, 5000, 0), (3_000_000_000, 20, 4500, 3),
+                                           (70_000, 1, 4200, 1)])
+def test_parallel_sample_distinct_rows_matches_numpy(n, k, nrows, pre):
+    """The parallel path of the per-row choice loop (>= 4096 rows: PCG64
+    words by jump-ahead, rejection scan, rows on threads) == numpy's
+    sequential per-row Generator.choice, values and final state; covers
+    both half-buffer states, Floyd and tail-shuffle rows, rows without an
+    exclusion and populations near 2^32 (frequent Lemire rejections)."""
+    from paper_1908_00814_b200.core import sample_distinct, sample_distinct_rows
+
+    g = np.random.default_rng(n % 997)
+    rows = g.integers(-1, min(n, 2**31 - 1), size=nrows).astype(np.int32)
+    a = np.random.default_rng(nrows + k)
+    a.integers(0, 3, size=pre)
+    b = np.random.default_rng(nrows + k)
+    b.integers(0, 3, size=pre)
+    want = np.stack([sample_distinct(a, n, k, exclude=int(r)) for r in rows])
+    got = sample_distinct_rows(b, n, k, rows)
+    assert np.array_equal(got, want)
+    assert a.bit_generator.state == b.bit_generator.state
