@@ -441,6 +441,80 @@ def config_legs(km, names, device, steps, warmup, hbm_peak, no_recall=False):
     return res
 
 
+def bf_leg(km, ds, device, k=20):
+    """Exact k-NN ground truth of the whole config-2 dataset (1M x 1M x 128)
+    on the tcgen05 tensor cores (knnm_bf.cuh; exact u8 Gram tiles), host
+    numpy output; plus a 200-row spot check against the fp64 SIMT kernel."""
+    import torch
+
+    from paper_1908_00814_b200.engine import get_engine
+
+    eng = get_engine(device)
+    km.brute_force_graph(ds, km.Metric.L2, k, member_ids=np.arange(8192), device=device)  # warm-up
+    torch.cuda.synchronize(device)
+    t = time.perf_counter()
+    g = km.brute_force_graph(ds, km.Metric.L2, k, device=device)
+    torch.cuda.synchronize(device)
+    dt = time.perf_counter() - t
+    route = eng.bf_route()
+    rows = np.sort(np.random.default_rng(0).choice(ds.n, 200, replace=False))
+    eng.set_bf_variant(0)
+    try:
+        eng.begin(np.arange(ds.n, dtype=np.int64), np.zeros(ds.n, dtype=np.int8), k)
+        sid, sd = eng.bf_topk(k, rows=rows, exclude_self=True)
+    finally:
+        eng.set_bf_variant(-1)
+    same = bool(np.array_equal(g.ids[rows], sid) and np.array_equal(g.dists[rows], sd))
+    n = ds.n
+    return {"workload": f"exact {k}-NN graph of the config-2 dataset ({n} x {n} x {ds.d})",
+            "route": "tcgen05 kind::i8 (exact u8 Gram tiles)" if route == 1 else "simt fp64",
+            "seconds": dt, "pairs_per_s": n * (n - 1) / dt,
+            "gram_tops": 2.0 * n * n * ds.d / dt / 1e12,
+            "spot_check_rows": 200, "equal_to_fp64_simt": same,
+            "note": "host numpy output (240 MB device->host inside the time)"}
+
+
+def c5_leg(km, device):
+    """BASELINE config 5 on one GPU: 8 k=20 subgraphs of 1M points (config-2
+    distribution), pairwise S-Merge tree of 3 levels run one after another
+    (the 8-GPU placement is tools/c5_tree.py --dist); device-resident,
+    CUDA-event time of the three levels."""
+    import torch
+
+    from paper_1908_00814_b200.engine import get_engine
+
+    per = 1_000_000
+    ds = km.generate_int_gmm(8 * per, 128, 1000, 20.0, seed=7)
+    parts = [np.arange(i * per, (i + 1) * per, dtype=np.int64) for i in range(8)]
+    graphs = [km.nn_descent(ds, km.Metric.L2, km.DescentParams(k=20), i + 1, member_ids=p,
+                            device=device, out_device=True) for i, p in enumerate(parts)]
+    params = km.MergeParams(k=20, seed=3)
+    eng = get_engine(device)
+
+    def tree():
+        torch.cuda.synchronize(device)
+        level, evals, lv = graphs, 0, []
+        eng.mark(4)
+        while len(level) > 1:
+            nxt = []
+            for a, b in zip(level[0::2], level[1::2]):
+                c = km.DistanceCounter()
+                nxt.append(km.s_merge(ds, a, b, params, counter=c, device=device, out_device=True))
+                evals += c.count
+            eng.mark(5)
+            lv.append(eng.elapsed_ms(4, 5) / 1e3 - sum(lv))
+            level = nxt
+        return evals, lv
+
+    tree()  # warm-up: buffers sized for the 8M-point level
+    evals, lv = tree()
+    total = sum(lv)
+    del graphs
+    return {"workload": "config5_tree_8x1M_d128_k20 (levels sequential on one GPU)",
+            "seconds": total, "level_seconds": [round(x, 4) for x in lv], "evals": evals,
+            "evals_per_s": evals / total}
+
+
 def run_b200(args):
     import torch
 
@@ -693,6 +767,14 @@ def run_b200(args):
         legs = config_legs(km, args.configs, local, max(1, min(args.steps, 3)), 1, hbm_peak,
                            no_recall=args.no_recall)
         eng.set_dataset(ds.vectors, 1)
+    gt = None
+    if not args.no_bf and world == 1:
+        gt = bf_leg(km, ds, local)
+        eng.set_dataset(ds.vectors, 1)
+    c5 = None
+    if not args.no_c5 and world == 1 and args.scale == 1.0:
+        c5 = c5_leg(km, local)
+        eng.set_dataset(ds.vectors, 1)
     cpu = None if args.no_cpu else cpu_baseline()
     steps = args.steps
     line = {
@@ -715,6 +797,8 @@ def run_b200(args):
                 "d2h_bytes_per_step": est["d2h_bytes"] // steps},
         "kernels": kern,
         "configs": legs,
+        "ground_truth": gt,
+        "config5": c5,
         "gpu_launches": st["launches"],
         "step_wall_ms": step_wall,
         "clocks": clk.summary(),
@@ -741,6 +825,8 @@ def main():
                     help="force a join route (0 exact, 1 tiled, 2 tensor core)")
     ap.add_argument("--configs", default="c3,c4",
                     help="extra BASELINE config legs at N=1 (comma list; '' to skip)")
+    ap.add_argument("--no-bf", action="store_true", help="skip the tensor-core ground-truth leg")
+    ap.add_argument("--no-c5", action="store_true", help="skip the config-5 tree leg (one GPU)")
     ap.add_argument("--no-rho-half", action="store_true",
                     help="skip the rho = 0.5 leg (BASELINE's config-2 sample rate)")
     args = ap.parse_args()
