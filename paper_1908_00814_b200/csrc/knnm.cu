@@ -124,6 +124,15 @@ struct knnm_ctx {
     bool stg_busy[2] = {false, false};
     bool lists_f32 = true;  // every list distance is an exact fp32 value
     int slots_mode = SLOTS_PLAIN;  // format of the slots the next apply reads
+    // generation-tagged packed slots (tensor-core join, unsharded rounds):
+    // bits 24-31 of a slot's low word carry the round's tag (1..254), so a
+    // slot left from an earlier round reads as unwritten and the per-round
+    // "cannot pass" prefill is not needed.  slot_gen = tag of the current
+    // round's slots (0: NaN-prefilled format); gen_valid = the buffer holds
+    // only tagged slots (else it is zeroed before the next tagged round).
+    uint32_t slot_gen = 0, last_gen = 0;
+    bool gen_valid = false;
+    bool gen_slots = true;  // KNNM_GEN_SLOTS=0 turns the tagged format off
     int new_cap = 0;               // rho-sampling: new entries per row per round (0 = all)
     bool cert_u8 = false;   // entries are integers in [0, 255]: u8 rows, s32 MMA
     int dph = 0;            // fp16 row length (multiple of 16)
@@ -389,6 +398,7 @@ uint64_t bucket_budget(knnm_ctx *c) { return c->cand_budget_bytes / (sizeof(doub
 int ensure_slots_noinit(knnm_ctx *c, uint64_t slots) {
     TRY(ensure(c->Bd, sizeof(double) * slots));
     TRY(ensure(c->Bs, sizeof(int32_t) * slots));
+    c->gen_valid = false;
     return KNNM_OK;
 }
 
@@ -397,6 +407,24 @@ int ensure_slots(knnm_ctx *c, uint64_t slots) {
     TRY(ensure(c->Bs, sizeof(int32_t) * slots));
     // NaN fill: a slot the join does not write cannot pass (see k_apply_stream)
     CK(cudaMemsetAsync(c->Bd.p, 0xff, sizeof(double) * slots, c->st));
+    c->gen_valid = false;
+    c->slot_gen = 0;
+    return KNNM_OK;
+}
+
+// Packed slots with a generation tag instead of the prefill: a new tag per
+// round (1..254); the whole buffer is zeroed only when it was (re)allocated,
+// used in another format, or the tags wrap.
+int ensure_slots_tagged(knnm_ctx *c, uint64_t slots) {
+    const size_t before = c->Bd.bytes;
+    TRY(ensure(c->Bd, sizeof(double) * slots));
+    TRY(ensure(c->Bs, sizeof(int32_t) * slots));
+    if (c->Bd.bytes != before || !c->gen_valid || c->last_gen >= 254) {
+        CK(cudaMemsetAsync(c->Bd.p, 0, c->Bd.bytes, c->st));
+        c->last_gen = 0;
+        c->gen_valid = true;
+    }
+    c->slot_gen = ++c->last_gen;
     return KNNM_OK;
 }
 
@@ -468,7 +496,7 @@ int run_updates(knnm_ctx *c) {
     k_apply_stream<EE, LZ, F><<<blocks, APPLY_WARPS * 32, 0, c->st>>>(                             \
         n, c->k, c->boff.as<uint64_t>(), c->Bd.as<double>(), c->Bs.as<int32_t>(),               \
         c->ids.as<int32_t>(), c->dists.as<double>(), c->flags.as<uint8_t>(), c->sizes.as<int32_t>(), \
-        cnt, lazy_of(c))
+        cnt, lazy_of(c), c->slots_mode == SLOTS_PACKED ? c->slot_gen : 0u)
     const bool f32 = c->lists_f32;
     {
         PhaseTimer ptk(c, PH_APPLYK);  // the apply kernel alone (roofline)
@@ -891,6 +919,7 @@ int knnm_create(int device, knnm_ctx **out) {
     c->sms = prop.multiProcessorCount;
     if (const char *e = getenv("KNNM_LAZY_AHEAD")) c->lazy_ahead = std::max(0, std::min(64, atoi(e)));
     if (const char *e = getenv("KNNM_LAZY_MIN_D")) c->lazy_min_d = std::max(0, atoi(e));
+    if (const char *e = getenv("KNNM_GEN_SLOTS")) c->gen_slots = atoi(e) != 0;
     CK(cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking));
     CK(cudaHostAlloc((void **)&c->hcnt, sizeof(unsigned long long) * C_NUM, cudaHostAllocDefault));
     TRY(ensure(c->counters, sizeof(unsigned long long) * C_NUM));
@@ -1598,7 +1627,10 @@ static int join_chunk(knnm_ctx *c, int32_t mode, int W, const int32_t *act, int6
         }
         // fused: bucket sizes are written by rank_memberships below
         if (!fused) TRY(scan<uint32_t, uint64_t>(c, c->bound.as<uint32_t>(), c->boff.as<uint64_t>(), n));
-        TRY(ensure_slots(c, pairs2));
+        // tensor-core join, unsharded: generation-tagged slots, no prefill
+        const bool tagged = use_mma && !local_only && c->gen_slots && n < (int64_t)(1 << 24);
+        if (tagged) TRY(ensure_slots_tagged(c, pairs2));
+        else TRY(ensure_slots(c, pairs2));
         if (!fused) {
             TRY(scan<uint32_t, uint32_t>(c, c->mcount.as<uint32_t>(), c->moff.as<uint32_t>(), n));
             TRY(ensure_memb(c, (uint64_t)n * W, (uint64_t)n * W));
@@ -1640,9 +1672,10 @@ static int join_chunk(knnm_ctx *c, int32_t mode, int W, const int32_t *act, int6
                                                              boff, c->rowmeta.as<RowMeta>());
             CKL();
             const RowMeta *rmp = c->rowmeta.as<RowMeta>();
+            uint32_t gtag = c->slot_gen << 24;  // 0: NaN-prefilled slots
             void *args[] = {(void *)&act, (void *)&nact32, (void *)&nbhp, (void *)&nlp, (void *)&Wi,
                             (void *)&labp, (void *)&modei, (void *)&s16, (void *)&rowbi,
-                            (void *)&rmp, (void *)&stt, (void *)&Bd, (void *)&Bs};
+                            (void *)&rmp, (void *)&stt, (void *)&Bd, (void *)&Bs, (void *)&gtag};
             CK(cudaLaunchKernel(fn, dim3(grid), dim3(MJ_WARPS * 32), args, smem_mma, c->st));
         } else if (tiled) {
             // non-certified rows: exact values in the join from the

@@ -1888,7 +1888,9 @@ __global__ void __launch_bounds__(MJ_WARPS * 32, 4)
 k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
            const int32_t *__restrict__ nlen, int W, const int8_t *__restrict__ labels, int mode_rt,
            const uint8_t *__restrict__ sub16, int rowb, const RowMeta *__restrict__ rmeta,
-           const uint32_t *__restrict__ start, double *__restrict__ Bd, int32_t *__restrict__ Bs) {
+           const uint32_t *__restrict__ start, double *__restrict__ Bd, int32_t *__restrict__ Bs,
+           uint32_t gtag) {
+    // gtag: the round's slot generation << 24 (0: NaN-prefilled slots)
     // the pair mode is a template parameter (mode_rt == MODE): partner masks,
     // block shapes and the slot correction fold into constants
     constexpr int mode = MODE;
@@ -2088,8 +2090,8 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                             U8 ? (float)((__float_as_int(R.nrm) + __float_as_int(C.nrm)) - 2 * iacc[s])
                                : (R.nrm + C.nrm) - 2.0f * acc[s];
                         const unsigned long long pv = (unsigned long long)__float_as_uint(dd) << 32;
-                        if (dd < R.w) __stcs(mj_slot_ptr<MODE>(R, C), pv | (uint32_t)C.id);  // id[ii] <- id[jj]
-                        if (dd < C.w) __stcs(mj_slot_ptr<MODE>(C, R), pv | (uint32_t)R.id);  // id[jj] <- id[ii]
+                        if (dd < R.w) __stcs(mj_slot_ptr<MODE>(R, C), pv | gtag | (uint32_t)C.id);  // id[ii] <- id[jj]
+                        if (dd < C.w) __stcs(mj_slot_ptr<MODE>(C, R), pv | gtag | (uint32_t)R.id);  // id[jj] <- id[ii]
                     }
                 }
             }
@@ -2488,7 +2490,9 @@ template <int E, int MODE, bool F32 = false>
 __global__ void __launch_bounds__(APPLY_WARPS * 32, 6)
 k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double *__restrict__ Bd,
                const int32_t *__restrict__ Bs, int32_t *ids, double *dists, uint8_t *flags,
-               int32_t *sizes, unsigned long long *counters, LazyExact z) {
+               int32_t *sizes, unsigned long long *counters, LazyExact z, uint32_t gen) {
+    // gen (packed slots only): the round's slot generation; a slot whose tag
+    // differs was not written this round (0: NaN-prefilled format)
     constexpr bool LAZY = MODE == SLOTS_LAZY;
     __shared__ LazyBatchSmem s_lz[LAZY ? APPLY_WARPS : 1];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
@@ -2523,11 +2527,12 @@ k_apply_stream(int64_t n, int k, const uint64_t *__restrict__ boff, const double
             if constexpr (MODE == SLOTS_PACKED) {
                 const unsigned long long v = __double_as_longlong(dl);
                 const float f = __uint_as_float((uint32_t)(v >> 32));
-                const T dt = f != f ? dist_inf<T>() : (T)f;
-                if (j < ns && f == f) written++;
+                const bool wr = gen ? (((uint32_t)v >> 24) == gen) : (f == f);
+                const T dt = wr ? (T)f : dist_inf<T>();
+                if (j < ns && wr) written++;
                 const bool pre = j < ns && (dt < s.worst || (s.sz < k && dt < dist_inf<T>()));
                 if (!__any_sync(FULL_MASK, pre)) continue;
-                src = (int)(uint32_t)v;
+                src = gen ? (int)((uint32_t)v & 0xFFFFFFu) : (int)(uint32_t)v;
                 a += warp_apply_chunk<E, T>(s, k, src, dt, cnt, lane);
             } else {
                 if constexpr (LAZY) {
