@@ -515,18 +515,90 @@ def c5_leg(km, device):
             "evals_per_s": evals / total}
 
 
+def tree_leg_dist(km, world, rank, local):
+    """BASELINE config 5 across the job's ranks (world = 8: 8 x 1M points,
+    one subgraph per GPU; smaller powers of two: the same tree over world x
+    1M): distributed.tree_merge, each level's merges sharded over their
+    group's GPUs through new_group sub-communicators (NCCL), groups of a
+    level concurrent, no re-sharding between levels.  Per-level CUDA-event
+    times, max over ranks; a warm-up tree first."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1908_00814_b200 import distributed as D
+    from paper_1908_00814_b200.engine import get_engine
+
+    per = int(os.environ.get("BENCH_TREE_PER", "1000000"))  # (smaller only in tests)
+    ds8 = km.generate_int_gmm(world * per, 128, 1000, 20.0, seed=7)
+    sets = [np.arange(r * per, (r + 1) * per, dtype=np.int64) for r in range(world)]
+    eng = get_engine(local)
+    mine = km.nn_descent(ds8, km.Metric.L2, km.DescentParams(k=20), rank + 1, member_ids=sets[rank],
+                         device=local, out_device=True)
+    groups = {tuple(m): dist.new_group(m) for _, m in D.tree_groups(world)}
+
+    def group_comm(level, ranks):
+        return D.TorchComm(groups[tuple(ranks)]) if rank in ranks else None
+
+    params = km.MergeParams(k=20, seed=3)
+    marks = []
+
+    def hook(level, members, cnt):
+        torch.cuda.synchronize()
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        marks.append((level, len(members), ev, cnt.count))
+
+    def run():
+        marks.clear()
+        torch.cuda.synchronize()
+        dist.barrier()
+        st = torch.cuda.Event(enable_timing=True)
+        st.record()
+        D.tree_merge(ds8, {rank: mine}, sets, params, world, group_comm, {rank: eng}, level_hook=hook)
+        torch.cuda.synchronize()
+        times, evals, prev = [], [], st
+        for _, gsize, ev, cnt in marks:
+            times.append(prev.elapsed_time(ev) / 1e3)
+            evals.append(cnt / gsize)  # summed over ranks: once per group
+            prev = ev
+        return times, evals
+
+    run()
+    times, evals = run()
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(times, dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e = torch.tensor(evals, dtype=torch.float64, device=dev)
+    dist.all_reduce(e, op=dist.ReduceOp.SUM)
+    lv = t.tolist()
+    total_evals = int(round(sum(e.tolist())))
+    return {"workload": f"tree merge of {world} x {per}-point k=20 subgraphs (d=128), one per GPU"
+                        + (" = BASELINE config 5" if world == 8 and per == 1_000_000 else ""),
+            "seconds": sum(lv), "level_seconds": [round(x, 4) for x in lv], "evals": total_evals,
+            "evals_per_s": total_evals / sum(lv), "ranks": world,
+            "timing": "per level: CUDA events on each rank, max over ranks (warm-up tree first)"}
+
+
 def run_b200(args):
     import torch
 
     world, rank, local = dist_setup()
+    # BENCH_BACKEND=gloo (tests of the multi-rank code on one GPU only): all
+    # ranks share cuda:0 and the collectives are staged through the host
+    test_gloo = os.environ.get("BENCH_BACKEND") == "gloo"
+    if test_gloo:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if test_gloo:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist.barrier()
-        print(f"[bench] rank {dist.get_rank()}/{dist.get_world_size()}: NCCL communicator up on "
-              f"cuda:{local} ({torch.cuda.get_device_name(local)})", file=sys.stderr, flush=True)
+        print(f"[bench] rank {dist.get_rank()}/{dist.get_world_size()}: {dist.get_backend()} communicator "
+              f"up on cuda:{local} ({torch.cuda.get_device_name(local)})", file=sys.stderr, flush=True)
     rank = int(os.environ.get("RANK", "0"))
     import paper_1908_00814_b200 as km
     from paper_1908_00814_b200.engine import get_engine
@@ -623,7 +695,7 @@ def run_b200(args):
     eng.set_profiling(False)
     ms_max = dev_ms
     if world > 1:
-        t = torch.tensor([dev_ms], device="cuda")
+        t = torch.tensor([dev_ms], device="cpu" if test_gloo else "cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         ms_max = float(t.item())
     value = evals / (ms_max / 1e3)  # one merge split over the ranks: whole-job rate
@@ -677,10 +749,20 @@ def run_b200(args):
     e_ms = eng.elapsed_ms(2, 3)
     est = eng.stats()
     if world > 1:
-        t = torch.tensor([e_ms], device="cuda")
+        t = torch.tensor([e_ms], device="cpu" if test_gloo else "cuda")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e_ms = float(t.item())
     e2e = e_evals / (e_ms / 1e3)
+
+    # config 5 across the job's GPUs (all ranks take part)
+    tree = None
+    if (world > 1 and not args.no_c5 and (world & (world - 1)) == 0
+            and (args.scale == 1.0 or "BENCH_TREE_PER" in os.environ)):
+        try:
+            tree = tree_leg_dist(km, world, rank, local)
+        except Exception as exc:  # report it; the merge line above stands
+            tree = {"error": f"{type(exc).__name__}: {exc}"[:400]}
+        eng.set_dataset(ds.vectors, 1)
 
     if rank != 0:
         if world > 1:
@@ -798,7 +880,7 @@ def run_b200(args):
         "kernels": kern,
         "configs": legs,
         "ground_truth": gt,
-        "config5": c5,
+        "config5": c5 if world == 1 else tree,
         "gpu_launches": st["launches"],
         "step_wall_ms": step_wall,
         "clocks": clk.summary(),
