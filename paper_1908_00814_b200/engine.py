@@ -60,12 +60,26 @@ class Engine:
         key = (v.shape, int(metric))
         if self._vectors is vectors and self._key == key and _frozen(vectors):
             return
-        fp = fingerprint(v)
-        if self._vectors is not None and self._key == key and self._fp == fp:
-            self._vectors = vectors
-            return
-        check(self._lib.knnm_set_dataset(self._h, ptr(v), v.shape[0], v.shape[1], int(metric)),
-              "knnm_set_dataset")
+        if self._vectors is not None and self._key == key:
+            fp = fingerprint(v)
+            if self._fp == fp:
+                self._vectors = vectors
+                return
+            check(self._lib.knnm_set_dataset(self._h, ptr(v), v.shape[0], v.shape[1], int(metric)),
+                  "knnm_set_dataset")
+        else:
+            # nothing comparable is resident: the upload happens anyway, so the
+            # fingerprint (kept for the next call) runs beside it (both native
+            # calls release the GIL)
+            box = {}
+            th = threading.Thread(target=lambda: box.setdefault("fp", fingerprint(v)))
+            th.start()
+            try:
+                check(self._lib.knnm_set_dataset(self._h, ptr(v), v.shape[0], v.shape[1], int(metric)),
+                      "knnm_set_dataset")
+            finally:
+                th.join()
+            fp = box["fp"]
         self._vectors = vectors
         self._metric = int(metric)
         self._key = key
