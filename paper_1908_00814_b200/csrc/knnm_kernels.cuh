@@ -2856,27 +2856,38 @@ __global__ void k_phi_leaves(const double *__restrict__ dists, const int32_t *__
     if (li >= nleaves) return;
     int64_t lo = leaf_lo[li];
     int n = leaf_len[li];
-    auto val = [&](int64_t e) -> double {
-        int64_t u = e / k;
-        int t = (int)(e - u * k);
-        return t < sizes[u] ? dists[e] : 0.0;
+    // elements are visited in index order: (row, slot) advance incrementally
+    // (no division per element)
+    int64_t u = lo / k;
+    int t = (int)(lo - u * k);
+    int sz = sizes[u];
+    int64_t e = lo;
+    auto next = [&]() -> double {
+        const double v = t < sz ? dists[e] : 0.0;
+        e++;
+        if (++t == k) {
+            t = 0;
+            u++;
+            sz = e < lo + n ? sizes[u] : 0;
+        }
+        return v;
     };
     double res;
     if (n < 8) {
         res = 0.0;
-        for (int i = 0; i < n; i++) res = __dadd_rn(res, val(lo + i));
+        for (int i = 0; i < n; i++) res = __dadd_rn(res, next());
     } else {
         double r[8];
 #pragma unroll
-        for (int j = 0; j < 8; j++) r[j] = val(lo + j);
+        for (int j = 0; j < 8; j++) r[j] = next();
         int i;
         for (i = 8; i < n - (n % 8); i += 8) {
 #pragma unroll
-            for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], val(lo + i + j));
+            for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], next());
         }
         res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-        for (; i < n; i++) res = __dadd_rn(res, val(lo + i));
+        for (; i < n; i++) res = __dadd_rn(res, next());
     }
     out[li] = res;
 }
