@@ -1,4 +1,6 @@
-"""Quality and cost metrics (reference evaluate.py:28-55)."""
+"""Quality and cost metrics of a build (reference evaluate.py:28-55):
+recall against exact ground truth and the scanning rate (distance
+evaluations relative to one all-pairs pass)."""
 
 from __future__ import annotations
 
@@ -7,25 +9,24 @@ import numpy as np
 from .core import DistanceCounter
 
 
-def _as_count(counter) -> int:
-    if isinstance(counter, DistanceCounter):
-        return counter.count
-    return int(counter)
+def _evals(counter) -> int:
+    return counter.count if isinstance(counter, DistanceCounter) else int(counter)
 
 
 def recall_at_k(results, truth, k: int) -> float:
-    """Mean per-list overlap of evaluated vs truth top-k ids (evaluate.py:28-48)."""
+    """Fraction of the true top-k ids found in each result's first k, over
+    aligned sequences of id lists (evaluate.py:28-48; same errors)."""
     if len(results) != len(truth):
         raise ValueError(f"misaligned lists: {len(results)} results vs {len(truth)} truth")
     if len(truth) == 0:
         raise ValueError("empty evaluation")
-    hits = 0
+    found = 0
     for got, want in zip(results, truth):
-        want = [int(v) for v in want]
         if len(want) < k:
             raise ValueError("truth list shorter than k")
-        hits += len(set(want[:k]).intersection(int(v) for v in got[:k]))
-    return hits / (len(truth) * k)
+        top = {int(v) for v in list(want)[:k]}
+        found += sum(1 for v in {int(x) for x in list(got)[:k]} if v in top)
+    return found / (k * len(truth))
 
 
 def recall_at_k_arrays(got_ids: np.ndarray, truth_ids: np.ndarray, k: int) -> float:
@@ -40,7 +41,7 @@ def recall_at_k_arrays(got_ids: np.ndarray, truth_ids: np.ndarray, k: int) -> fl
 
 
 def scanning_rate(counter, n: int) -> float:
-    """Distance evaluations relative to one full pairwise pass (evaluate.py:51-55)."""
+    """Evaluations / (n (n - 1) / 2) (evaluate.py:51-55)."""
     if n < 2:
         raise ValueError("scanning rate needs n >= 2")
-    return _as_count(counter) / (n * (n - 1) / 2.0)
+    return _evals(counter) * 2.0 / (n * (n - 1))
