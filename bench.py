@@ -794,7 +794,7 @@ def run_b200(args):
     achieved_survey = survey_bytes / jk_s / 1e9 if jk_s > 0 else 0.0
     traffic = None
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_join_traffic.json")) as f:
+        with open(os.path.join(ROOT, "profiles", "r2_join_traffic.json")) as f:
             traffic = json.load(f)
     except Exception:
         pass
@@ -826,7 +826,7 @@ def run_b200(args):
     models = {"join": f"(row_bytes + 4) * sum|M_u| + {int(slot_b)} * written_slots",
               "apply": "8 * slots read + 13k * (rows loaded + rows stored)"}
     tr = None
-    for fn in (f"r2_{dom}_traffic.json",) + (("r1_join_traffic.json",) if dom == "join" else ()):
+    for fn in (f"r2_{dom}_traffic.json",):
         try:
             with open(os.path.join(ROOT, "profiles", fn)) as f:
                 tr = json.load(f)
