@@ -442,7 +442,9 @@ int ensure_memb(knnm_ctx *c, uint64_t recs, uint64_t starts) {
 
 // Membership ranking: moff = scan(mcount); bucket memberships by row (fill
 // kernel launched by the caller between the two halves); then k_seg_rank.
-int rank_memberships(knnm_ctx *c, bool fused = false) {
+// wout: records of hood memberships rank into start[u * W + p] (wout = W);
+// directed-insert records into start[ordinal] (wout = 1)
+int rank_memberships(knnm_ctx *c, uint32_t wout, bool fused = false) {
     TRY(ensure(c->segheavy, sizeof(int32_t) * (size_t)c->n));
     unsigned long long *cnt = c->counters.as<unsigned long long>();
     CK(cudaMemsetAsync(cnt + C_SEGHEAVY, 0, sizeof(unsigned long long), c->st));
@@ -452,12 +454,12 @@ int rank_memberships(knnm_ctx *c, bool fused = false) {
     uint32_t *tot = fused ? c->bound.as<uint32_t>() : nullptr;
     k_seg_rank<<<grid_for(c, c->n * 32, SEG_WARPS * 32, 16), SEG_WARPS * 32, 0, c->st>>>(
         c->n, c->moff.as<uint32_t>(), c->memb.as<MembRec>(), c->start.as<uint32_t>(), mp,
-        c->segheavy.as<int32_t>(), cnt, tot);
+        c->segheavy.as<int32_t>(), cnt, tot, wout);
     CKL();
     // hub rows: block per row, count read on the device
     k_seg_rank_heavy<<<c->sms * 2, SEGH_THREADS, 0, c->st>>>(
         c->moff.as<uint32_t>(), c->memb.as<MembRec>(), c->start.as<uint32_t>(), mp,
-        c->segheavy.as<int32_t>(), cnt, tot);
+        c->segheavy.as<int32_t>(), cnt, tot, wout);
     CKL();
     return KNNM_OK;
 }
@@ -1336,7 +1338,7 @@ static int insert_impl(knnm_ctx *c, const int32_t *rows, int64_t mrows, int32_t 
                 rows_d, cm, nullptr, c->moff.as<uint32_t>(), c->mcur.as<uint32_t>(),
                 c->memb.as<MembRec>());
             CKL();
-            TRY(rank_memberships(c));
+            TRY(rank_memberships(c, 1u));
             k_directed_emit<<<grid_for(c, cm, 256, 32), 256, 0, c->st>>>(
                 rows_d, c->stage[1].as<int32_t>() + c0, cm, c->subp, c->dp, c->d, c->metric,
                 (int)(c->cert && c->metric != KNNM_COSINE), c->sizes.as<int32_t>(), c->dists.as<double>(), c->k, c->boff.as<uint64_t>(),
@@ -1640,7 +1642,7 @@ static int join_chunk(knnm_ctx *c, int32_t mode, int W, const int32_t *act, int6
                 c->mcur.as<uint32_t>(), c->memb.as<MembRec>());
             CKL();
         }
-        TRY(rank_memberships(c, fused));
+        TRY(rank_memberships(c, (uint32_t)W, fused));
         if (fused) TRY(scan<uint32_t, uint64_t>(c, c->bound.as<uint32_t>(), c->boff.as<uint64_t>(), n));
         const uint64_t *boff = c->boff.as<uint64_t>();
         const uint32_t *stt = c->start.as<uint32_t>();

@@ -23,16 +23,19 @@ constexpr int SEG_SMEM = 256;          // membership segments ranked in shared m
 // (x, p) with x < p, then (p, x) with x > p, _kernels.py:424-436).  Slot
 // base of (hood u, member at position p) = boff[r] + start[u * W + p]; the
 // partner's rank within the hood comes from per-class position prefix counts.
-struct MembRec {  // one (hood, member) membership, bucketed by member row
-    uint64_t key;    // hood id (or directed-insert ordinal)
-    uint32_t weight; // slots the membership occupies (admissible partners)
-    uint32_t out;    // where its exclusive rank goes: u * W + p (or ordinal)
+struct __align__(8) MembRec {  // one (hood, member) membership, bucketed by member row
+    uint32_t key;     // hood id u (or directed-insert ordinal)
+    uint16_t weight;  // slots the membership occupies (admissible partners)
+    uint16_t pos;     // the member's hood position p (0 for directed inserts)
 };
+// where a record's exclusive rank goes: u * W + p (hoods), or the ordinal
+// (directed inserts: wout = 1, pos = 0)
+__device__ __forceinline__ uint32_t memb_out(const MembRec &r, uint32_t wout) { return r.key * wout + r.pos; }
 
 // Streaming (read-once) load of a membership record.
 __device__ __forceinline__ MembRec ldcs_memb(const MembRec *p) {
-    const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(p));
-    return MembRec{((uint64_t)v.y << 32) | v.x, v.z, v.w};
+    const uint2 v = __ldcs(reinterpret_cast<const uint2 *>(p));
+    return MembRec{v.x, (uint16_t)(v.y & 0xFFFFu), (uint16_t)(v.y >> 16)};
 }
 
 // Admissible partner classes of a member, by pair mode and member class
@@ -973,7 +976,7 @@ k_assemble(const int32_t *__restrict__ ids, uint8_t *flags, const int32_t *__res
                         // one atomic yields the record's address
                         const unsigned long long at = atomicAdd(&mpack[x], 1ull);
                         memb[(uint32_t)(at >> 32) + (uint32_t)at] =
-                            MembRec{(uint64_t)u, (uint32_t)part, (uint32_t)(u * W + j)};
+                            MembRec{(uint32_t)u, (uint16_t)part, (uint16_t)j};
                     } else {
                         atomicAdd(&mcount[x], 1u);
                     }
@@ -2224,7 +2227,7 @@ __global__ void k_hood_memb(const int32_t *__restrict__ active, int nactive,
                         atomicAdd(&mcount[id], 1u);
                     } else {
                         const uint32_t at = moff[id] + atomicAdd(&mcur[id], 1u);
-                        memb[at] = MembRec{(uint64_t)u, (uint32_t)part, (uint32_t)(u * W + j)};
+                        memb[at] = MembRec{(uint32_t)u, (uint16_t)part, (uint16_t)j};
                     }
                 }
             }
@@ -2243,7 +2246,7 @@ __global__ void k_directed_memb(const int32_t *__restrict__ rows, int64_t m, uin
             atomicAdd(&mcount[r], 1u);
         } else {
             const uint32_t at = moff[r] + atomicAdd(&mcur[r], 1u);
-            memb[at] = MembRec{(uint64_t)i, 1u, (uint32_t)i};
+            memb[at] = MembRec{(uint32_t)i, 1, 0};
         }
     }
 }
@@ -2259,16 +2262,16 @@ __global__ void k_directed_memb(const int32_t *__restrict__ rows, int64_t m, uin
 template <int NE>
 __device__ __forceinline__ uint32_t seg_rank_sorted(uint32_t lo, int m, const MembRec *__restrict__ memb,
                                                 uint32_t *__restrict__ start, uint32_t *sw, uint32_t *so,
-                                                unsigned lane) {
+                                                unsigned lane, uint32_t wout) {
     uint64_t v[NE];
 #pragma unroll
     for (int e = 0; e < NE; e++) {
         const int i = e * 32 + (int)lane;
         if (i < m) {
             const MembRec re = memb[lo + i];
-            v[e] = (re.key << 32) | (uint32_t)i;
+            v[e] = ((uint64_t)re.key << 32) | (uint32_t)i;
             sw[i] = re.weight;
-            so[i] = re.out;
+            so[i] = memb_out(re, wout);
         } else {
             v[e] = ~0ull;
         }
@@ -2298,7 +2301,7 @@ constexpr int SEG_WARPS = 8;
 __global__ void __launch_bounds__(SEG_WARPS * 32)
 k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restrict__ memb,
            uint32_t *__restrict__ start, const unsigned long long *__restrict__ mpack,
-           int32_t *heavy, unsigned long long *counters, uint32_t *__restrict__ total) {
+           int32_t *heavy, unsigned long long *counters, uint32_t *__restrict__ total, uint32_t wout) {
     __shared__ uint32_t s_out[SEG_WARPS][SEG_SMEM];  // output positions of the sorted path
     __shared__ uint32_t s_wt[SEG_WARPS][SEG_SMEM];
     const unsigned lane = lane_id(), wib = threadIdx.x >> 5;
@@ -2320,7 +2323,7 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
     // ranked (pipeline: offsets two rows ahead, records one row ahead)
     int64_t r = (int64_t)blockIdx.x * SEG_WARPS + wib;
     uint32_t lo1 = 0, hi1 = 0, lo2 = 0, hi2 = 0;
-    MembRec rec1 = MembRec{0, 0, 0};
+    MembRec rec1 = MembRec{0u, 0, 0};
     if (r < n) {
         seg(r, lo1, hi1);
         if (lane < hi1 - lo1) rec1 = ldcs_memb(memb + lo1 + lane);
@@ -2332,7 +2335,7 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
         const MembRec rec = rec1;
         lo1 = lo2;
         hi1 = hi2;
-        rec1 = (r + nw < n && lane < hi1 - lo1) ? ldcs_memb(memb + lo1 + lane) : MembRec{0, 0, 0};
+        rec1 = (r + nw < n && lane < hi1 - lo1) ? ldcs_memb(memb + lo1 + lane) : MembRec{0u, 0, 0};
         if (r + 2 * nw < n) seg(r + 2 * nw, lo2, hi2);
         if (m == 0) continue;
         if (m <= 32) {
@@ -2345,7 +2348,7 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
                 const uint32_t wf = __shfl_sync(FULL_MASK, rec.weight, f);
                 acc += kf < key ? wf : 0u;
             }
-            if ((int)lane < m) start[rec.out] = acc;
+            if ((int)lane < m) start[memb_out(rec, wout)] = acc;
             if (total) {
                 const uint32_t t = __reduce_add_sync(FULL_MASK, (int)lane < m ? rec.weight : 0u);
                 if (lane == 0) total[r] = t;
@@ -2355,7 +2358,7 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
         if (m <= 64) {
             // two memberships per lane, the same weighted count of smaller
             // keys (keys are unique within a row: hood ids / ordinals)
-            const MembRec rb = (int)lane + 32 < m ? ldcs_memb(memb + lo + 32 + lane) : MembRec{~0ull, 0, 0};
+            const MembRec rb = (int)lane + 32 < m ? ldcs_memb(memb + lo + 32 + lane) : MembRec{~0u, 0, 0};
             uint32_t acc0 = 0, acc1 = 0;
             const uint32_t key0 = (uint32_t)rec.key, key1 = (uint32_t)rb.key;
 #pragma unroll 4
@@ -2367,8 +2370,8 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
                 acc0 += kf < key0 ? wf : 0u;
                 acc1 += kf < key1 ? wf : 0u;
             }
-            start[rec.out] = acc0;
-            if ((int)lane + 32 < m) start[rb.out] = acc1;
+            start[memb_out(rec, wout)] = acc0;
+            if ((int)lane + 32 < m) start[memb_out(rb, wout)] = acc1;
             if (total) {
                 const uint32_t t = __reduce_add_sync(FULL_MASK, rec.weight + rb.weight);
                 if (lane == 0) total[r] = t;
@@ -2382,8 +2385,8 @@ k_seg_rank(int64_t n, const uint32_t *__restrict__ moff, const MembRec *__restri
         // 64 < m <= SEG_SMEM: register bitonic sort of (key << 32 | index),
         // then the weights scanned in that order
         const uint32_t t = m <= 128
-            ? seg_rank_sorted<4>(lo, m, memb, start, s_wt[wib], s_out[wib], lane)
-            : seg_rank_sorted<8>(lo, m, memb, start, s_wt[wib], s_out[wib], lane);
+            ? seg_rank_sorted<4>(lo, m, memb, start, s_wt[wib], s_out[wib], lane, wout)
+            : seg_rank_sorted<8>(lo, m, memb, start, s_wt[wib], s_out[wib], lane, wout);
         if (total && lane == 0) total[r] = t;
         __syncwarp();
     }
@@ -2398,7 +2401,7 @@ __global__ void __launch_bounds__(SEGH_THREADS)
 k_seg_rank_heavy(const uint32_t *__restrict__ moff, const MembRec *__restrict__ memb,
                  uint32_t *__restrict__ start, const unsigned long long *__restrict__ mpack,
                  const int32_t *__restrict__ heavy, const unsigned long long *__restrict__ counters,
-                 uint32_t *__restrict__ total) {
+                 uint32_t *__restrict__ total, uint32_t wout) {
     __shared__ uint64_t s_k[SEGH_SMEM];
     __shared__ uint32_t s_w[SEGH_SMEM];
     const int64_t nh = (int64_t)counters[C_SEGHEAVY];
@@ -2436,7 +2439,7 @@ k_seg_rank_heavy(const uint32_t *__restrict__ moff, const MembRec *__restrict__ 
                 const MembRec rf = memb[lo + f];
                 acc += rf.key < re.key ? rf.weight : 0u;
             }
-            start[re.out] = acc;
+            start[memb_out(re, wout)] = acc;
         }
         __syncthreads();
     }
