@@ -87,6 +87,7 @@ typedef struct knnm_stats {
     int64_t active_hoods;   /* hoods with >= 1 admissible pair, over all rounds */
     int64_t bf_tc_launches; /* brute-force calls served by the tcgen05 route */
     int64_t lazy_batches;   /* lazy exact-evaluation batches in the apply (pairs: exact_evals) */
+    int64_t tc_join_launches; /* local joins on the tcgen05 lazy route (k_join_tc) */
 } knnm_stats;
 
 const char *knnm_last_error(void);
@@ -334,8 +335,11 @@ int knnm_capture_fetch(knnm_ctx *ctx, int32_t *pa, int32_t *pb, double *pd,
 /* Local-join kernel choice: -1 auto, 0 = exact route (fp64 on every pair),
  * 1 = tiled route (fp32 SIMT screen, exact by certificate or by fp64
  * re-evaluation), 2 = tensor-core route (fp16 mma.sync Gram blocks; only for
- * datasets with the dot-form certificate, otherwise auto).  All routes give
- * bit-identical results; the switch exists for tests and measurement. */
+ * datasets with the dot-form certificate, otherwise auto), 3 = tcgen05 route
+ * for non-certified long rows (rigorous fixed-point lower bounds from u8 limb
+ * products, exact values in the apply; non-negative L2 data, k + rev_cap <=
+ * 80; otherwise auto).  All routes give bit-identical results; the switch
+ * exists for tests and measurement. */
 int knnm_set_join_variant(knnm_ctx *ctx, int32_t variant);
 
 /* Sample rate rho < 1 (classic NN-Descent; no reference counterpart -- the

@@ -64,6 +64,7 @@ class KnnmStats(ctypes.Structure):
         ("active_hoods", I64),
         ("bf_tc_launches", I64),
         ("lazy_batches", I64),
+        ("tc_join_launches", I64),
     ]
 
     def as_dict(self) -> dict:

@@ -18,6 +18,7 @@
 #include "../../include/knnm.h"
 #include "knnm_kernels.cuh"
 #include "knnm_bf.cuh"
+#include "knnm_tcjoin.cuh"
 
 using namespace knnm;
 
@@ -140,7 +141,9 @@ struct knnm_ctx {
     DBuf vec16, norms, sub16, subnorms;
     const uint8_t *sub16p = nullptr;
     const float *subnormp = nullptr;
-    int join_variant = -1;  // -1 auto, 0 exact (fp64 every pair), 1 tiled, 2 tensor core
+    // -1 auto, 0 exact (fp64 every pair), 1 tiled / chunked fp32, 2 tensor core
+    // (mma.sync, certified), 3 tensor core (tcgen05 lazy bounds)
+    int join_variant = -1;
     int bf_variant = -1;    // brute force: -1 auto, 0 SIMT exact, 1 tcgen05 (certified u8 only)
     int lazy_ahead = LZB_AHEAD;  // look-ahead chunks of a lazy evaluation batch (KNNM_LAZY_AHEAD)
     // rows longer than this defer exact values to the apply (KNNM_LAZY_MIN_D;
@@ -151,6 +154,14 @@ struct knnm_ctx {
     bool bf_u8 = false;      // integers in [0, 255]: exact u8 Gram tiles for brute force
     DBuf bfx, bfxn;          // u8 copy of the candidate rows when the join has none
     bool u8_enabled = true;
+    // tcgen05 lazy join (k_join_tc): non-negative finite L2 data in 24-bit
+    // fixed point, three u8 limb planes per union row (built once per merge)
+    bool tcj_data = false;
+    double tcj_scale = 0.0;  // 2^(24 - e), max entry <= 2^e
+    int tcj_dpad = 0;        // limb plane length (roundup(d, 16))
+    bool limbs_ready = false;
+    bool tcj_round = false;  // the round's lazy slots hold k_join_tc's bounds (lo_rel = 1)
+    DBuf limbs, lnx, lax;
     // current merge
     DBuf sub, ugid, labels, labbits;
     bool ug_identity = false;  // union = 0 .. n_all-1: ugid not uploaded
@@ -480,7 +491,8 @@ LazyExact lazy_of(knnm_ctx *c) {
     z.dp = c->dp;
     z.d = c->d;
     z.tag = c->metric;
-    z.lo_rel = 1.0 - (double)(c->d + 8) * ldexp(1.0, -23);
+    // k_join_tc stores rigorous lower bounds of the reference value itself
+    z.lo_rel = c->tcj_round ? 1.0 : 1.0 - (double)(c->d + 8) * ldexp(1.0, -23);
     z.lo_abs = (double)(4 * c->d + 64) * ldexp(1.0, -24);
     return z;
 }
@@ -940,6 +952,7 @@ int knnm_create(int device, knnm_ctx **out) {
 #undef KNNM_MJ_ALL
     CK(cudaFuncSetAttribute(k_merge_rear, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)mr_smem_bytes(64, 64)));
+    CK(cudaFuncSetAttribute(k_join_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TJC_SMEM_CAP));
     for (auto f : {k_bf_topk<0>, k_bf_topk<1>, k_bf_topk<2>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)(BF_THREADS * BF_MAXK * (sizeof(double) + sizeof(int32_t)))));
@@ -959,7 +972,7 @@ int knnm_destroy(knnm_ctx *c) {
     DBuf *all[] = {&c->vec, &c->sub, &c->ugid, &c->labels, &c->labbits, &c->ids, &c->dists, &c->flags,
                    &c->sizes, &c->tail_ids, &c->tail_d, &c->tail_s, &c->indeg, &c->roff,
                    &c->rev, &c->heavy, &c->giant, &c->gscratch32, &c->nbh, &c->nlen, &c->hpairs,
-                   &c->poff, &c->worst0, &c->active, &c->rowmeta, &c->wcnt, &c->woff, &c->cBd, &c->cBs, &c->order, &c->lab0, &c->lab1, &c->bound, &c->boff, &c->mcount, &c->moff, &c->mcur, &c->memb, &c->start, &c->Bd, &c->Bs,
+                   &c->poff, &c->worst0, &c->active, &c->rowmeta, &c->wcnt, &c->woff, &c->cBd, &c->cBs, &c->order, &c->lab0, &c->lab1, &c->bound, &c->boff, &c->mcount, &c->moff, &c->mcur, &c->memb, &c->start, &c->Bd, &c->Bs, &c->limbs, &c->lnx, &c->lax,
                    &c->counters, &c->draws, &c->draw_rows,
                    &c->draw_bad, &c->pool, &c->scan_pos, &c->vec16, &c->norms, &c->sub16, &c->subnorms, &c->out_ids, &c->out_d,
                    &c->out_s, &c->phi_leaf_lo, &c->phi_leaf_len, &c->phi_left, &c->phi_right,
@@ -1046,6 +1059,16 @@ int knnm_set_dataset(knnm_ctx *c, const float *vectors, int64_t n_all, int32_t d
         c->cert_u8 = c->cert_dot && mn >= 0.0 && mx <= 255.0 && c->u8_enabled;
         // brute force needs only exact s32 dot products and u32 distances
         c->bf_u8 = ints && mn >= 0.0 && mx <= 255.0 && (double)d * 65025.0 < 2147483648.0;
+        // fixed-point limbs: every G accumulator below 2^31 (3 d 255^2)
+        c->tcj_data = metric == KNNM_L2 && mn >= 0.0 && std::isfinite(mx) && mx > 0.0 &&
+                      3.0 * (double)d * 65025.0 < 2147483648.0;
+        if (c->tcj_data) {
+            int e = 0;
+            std::frexp(mx, &e);  // mx < 2^e
+            c->tcj_scale = std::ldexp(1.0, 24 - e);
+            c->tcj_dpad = (d + 15) & ~15;  // limb plane length (16-byte copies)
+        }
+        c->limbs_ready = false;
         if (c->cert_u8) {
             c->dph = (d + 31) & ~31;  // u8 elements per row
             c->rowb = c->dph;
@@ -1084,6 +1107,8 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     c->n = n;
     c->k = k;
     c->slots_mode = SLOTS_PLAIN;
+    c->limbs_ready = false;  // limb planes follow the union
+    c->tcj_round = false;
     // fp32 list rows only on certified data (distances are integers < 2^24)
     // and only while every loaded distance is an exact fp32 value
     c->lists_f32 = c->cert || c->cert_dot;
@@ -1552,9 +1577,24 @@ int knnm_draws_insert(knnm_ctx *c, const int32_t *rows, const int32_t *pool, int
     return knnm_draws_insert_range(c, rows, pool, npool, 0, c->draw_n, accepted);
 }
 
+// Fixed-point limb planes of the union rows for k_join_tc (once per merge).
+static int ensure_limbs(knnm_ctx *c) {
+    if (c->limbs_ready) return KNNM_OK;
+    const int64_t n = c->n;
+    TRY(ensure(c->limbs, (size_t)n * 3 * c->tcj_dpad));
+    TRY(ensure(c->lnx, sizeof(double) * (size_t)n));
+    TRY(ensure(c->lax, sizeof(double) * (size_t)n));
+    k_make_limbs<<<grid_for(c, n * 32, 256, 16), 256, 0, c->st>>>(c->subp, c->dp, c->d, n, c->tcj_dpad,
+                                                                  c->tcj_scale, c->limbs.as<uint8_t>(),
+                                                                  c->lnx.as<double>(), c->lax.as<double>());
+    CKL();
+    c->limbs_ready = true;
+    return KNNM_OK;
+}
+
 // Route of the local join for this round (dataset, k, rev_cap, mode).
 struct JoinRoute {
-    bool use_mma, tiled, lazy;
+    bool use_mma, tiled, lazy, tc;
     size_t smem, smem_tiled, smem_mma;
 };
 
@@ -1580,6 +1620,11 @@ static int join_route(knnm_ctx *c, int W, int mode, JoinRoute *r) {
     c->slots_mode = use_mma ? SLOTS_PACKED
                     : tiled ? (lazy ? SLOTS_LAZY : c->cert ? SLOTS_PACKED : SLOTS_PLAIN)
                             : SLOTS_PLAIN;
+    // lazy rows on the 5th-generation tensor cores (rigorous fixed-point
+    // bounds, k_join_tc) when the data is non-negative and the hood's three
+    // accumulators fit TMEM
+    r->tc = lazy && c->tcj_data && W <= TJC_MAX_W && (c->join_variant == 3 || c->join_variant < 0);
+    c->tcj_round = r->tc;
     r->use_mma = use_mma;
     r->tiled = tiled;
     r->lazy = lazy;
@@ -1704,6 +1749,16 @@ c->subp, c->dp, c->d, c->worst0.as<double>(), boff, stt, Bd, Bs, lo_rel, lo_abs,
             if (c->cert && !lazy) {
                 if (c->metric == 1) KNNM_TJ_LAUNCH(1, true, false);
                 else KNNM_TJ_LAUNCH(0, true, false);
+            } else if (rt.tc) {
+                TRY(ensure_limbs(c));
+                // one CTA per SM: a deep ring of (hood, K block) stages
+                const int stages = tjc_stages(W);
+                const unsigned gtc = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nact, (int64_t)c->sms));
+                k_join_tc<<<gtc, TJC_THREADS, tjc_smem_bytes(W, stages), c->st>>>(
+                    act, na, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W, mode, c->limbs.as<uint8_t>(),
+                    c->tcj_dpad, c->d, stages, c->lnx.as<double>(), c->lax.as<double>(), 1.0 / c->tcj_scale,
+                    c->worst0.as<double>(), boff, stt, Bd, Bs);
+                c->stats.tc_join_launches += 1;
             } else if (lazy) {
                 // rows stream through two CJ_DC-dimension buffers
                 const size_t smem_cj = CJ_NBUF * (size_t)W * (CJ_DC / 4 + 1) * sizeof(float4);
@@ -2813,7 +2868,7 @@ int knnm_set_sample(knnm_ctx *c, int32_t new_cap) {
 }
 
 int knnm_set_join_variant(knnm_ctx *c, int32_t variant) {
-    if (!c || variant < -1 || variant > 2) return fail(KNNM_ERR_ARG, "variant %d", variant);
+    if (!c || variant < -1 || variant > 3) return fail(KNNM_ERR_ARG, "variant %d", variant);
     c->join_variant = variant;
     return KNNM_OK;
 }

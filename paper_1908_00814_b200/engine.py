@@ -336,7 +336,8 @@ class Engine:
         return int(r.value)
 
     def set_join_variant(self, variant: int) -> None:
-        """-1 auto, 0 exact fp64 route, 1 tiled fp32-screen route, 2 tensor-core route."""
+        """-1 auto, 0 exact fp64 route, 1 tiled / chunked fp32-screen route, 2 tensor-core
+        route (mma.sync, certified data), 3 tcgen05 lazy route (fixed-point bounds)."""
         check(self._lib.knnm_set_join_variant(self._h, int(variant)), "knnm_set_join_variant")
 
     def set_locality(self, iters: int) -> None:

@@ -324,3 +324,37 @@ def test_merge_rear_wider_tail_truncates(oracle):
     a = km.merge_rear(u, wide)
     b = km.merge_rear(u, narrow)
     _same_graph(a, b)
+
+
+@pytest.mark.parametrize("variant", [-1, 1])
+@pytest.mark.parametrize("n,d,k,kind,scale", [(2000, 960, 20, "unitgmm", 1.0), (1500, 960, 40, "unitgmm", 1.0),
+                                              (1500, 784, 40, "uniform", 1.0), (1500, 500, 12, "uniform", 300.0),
+                                              (1200, 1000, 8, "uniform", 1e-3)])
+def test_tc_lazy_join_matches_oracle(oracle, variant, n, d, k, kind, scale):
+    """Long non-certified L2 rows: the tcgen05 route (u8 limb products of a
+    24-bit fixed-point image, rigorous lower bounds, exact values in the
+    apply) and the fp32 chunked route are both bit-identical to the oracle,
+    for data scaled so the fixed point's exponent moves."""
+    km = _km()
+    from paper_1908_00814_b200.engine import get_engine
+
+    eng = get_engine()
+    ds0 = _data(km, n, d, kind, seed=d + k + 11)
+    vec = (ds0.vectors * np.float32(scale)).astype(np.float32)
+    ds = km.Dataset.from_dense(vec)
+    s1, s2 = split_ids(n, seed=6)
+    g, _, _ = oracle.nn_descent(vec, 1, k, 1, member_ids=s1)
+    eng.set_join_variant(variant)
+    eng.reset_stats()
+    try:
+        c = km.DistanceCounter()
+        u, rep = km.j_merge(ds, _to_graph(km, g), s2, km.MergeParams(k=k, seed=5), counter=c,
+                            return_report=True)
+        launches = eng.stats()["tc_join_launches"]
+    finally:
+        eng.set_join_variant(-1)
+    ou, orep, ocount = oracle.j_merge(vec, g, s2, k, seed=5)
+    _same_graph(u, ou)
+    _same_report(rep, orep)
+    assert c.count == ocount
+    assert (launches > 0) == (variant == -1 and 2 * k <= 80)

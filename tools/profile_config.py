@@ -69,11 +69,17 @@ def main():
         for d0, a, b in sorted(gaps, reverse=True)[:12]:
             print(f"  gap {d0 / 1e3:8.3f} ms after {str(a)[:38]:38s} before {str(b)[:38]}")
         return
+    from paper_1908_00814_b200.engine import get_engine
+
+    get_engine().reset_stats()
+    get_engine().set_profiling(True)
     torch.cuda.profiler.start()
     dt, cnt, _ = once()
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
-    print(f"{name} scale {scale}: merge {dt:.3f} s evals {cnt}")
+    st = get_engine().stats()
+    print(f"{name} scale {scale}: merge {dt:.3f} s evals {cnt}; join kernel {st['join_kernel_ms']:.1f} ms "
+          f"apply kernel {st['apply_kernel_ms']:.1f} ms, tc joins {st['tc_join_launches']}, join launches {st['join_launches']}")
 
 
 if __name__ == "__main__":
