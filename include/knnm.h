@@ -88,6 +88,7 @@ typedef struct knnm_stats {
     int64_t bf_tc_launches; /* brute-force calls served by the tcgen05 route */
     int64_t lazy_batches;   /* lazy exact-evaluation batches in the apply (pairs: exact_evals) */
     int64_t tc_join_launches; /* local joins on the tcgen05 lazy route (k_join_tc) */
+    int64_t dense_join_launches; /* local joins on the fp64 register-tile route (k_join_dense) */
 } knnm_stats;
 
 const char *knnm_last_error(void);
@@ -338,8 +339,10 @@ int knnm_capture_fetch(knnm_ctx *ctx, int32_t *pa, int32_t *pb, double *pd,
  * datasets with the dot-form certificate, otherwise auto), 3 = tcgen05 route
  * for non-certified long rows (rigorous fixed-point lower bounds from u8 limb
  * products, exact values in the apply; non-negative L2 data, k + rev_cap <=
- * 80; otherwise auto).  All routes give bit-identical results; the switch
- * exists for tests and measurement. */
+ * 80; otherwise auto), 4 = exact fp64 register tiles for non-certified short
+ * rows (every admissible pair exact, no fp32 screen; otherwise auto).  All
+ * routes give bit-identical results; the switch exists for tests and
+ * measurement. */
 int knnm_set_join_variant(knnm_ctx *ctx, int32_t variant);
 
 /* Sample rate rho < 1 (classic NN-Descent; no reference counterpart -- the

@@ -65,6 +65,7 @@ class KnnmStats(ctypes.Structure):
         ("bf_tc_launches", I64),
         ("lazy_batches", I64),
         ("tc_join_launches", I64),
+        ("dense_join_launches", I64),
     ]
 
     def as_dict(self) -> dict:

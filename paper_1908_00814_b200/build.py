@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc", "knnm.cu")
 OUT = os.path.join(HERE, "libknnm.so")
 DEPS = [os.path.join(HERE, "csrc", f) for f in ("knnm.cu", "knnm_kernels.cuh", "knnm_device.cuh", "knnm_bf.cuh",
-                                                   "knnm_tcjoin.cuh")]
+                                                   "knnm_tcjoin.cuh", "knnm_dense.cuh")]
 DEPS.append(os.path.join(os.path.dirname(HERE), "include", "knnm.h"))
 
 NVCC_FLAGS = [

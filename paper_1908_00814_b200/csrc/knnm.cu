@@ -19,6 +19,7 @@
 #include "knnm_kernels.cuh"
 #include "knnm_bf.cuh"
 #include "knnm_tcjoin.cuh"
+#include "knnm_dense.cuh"
 
 using namespace knnm;
 
@@ -160,6 +161,8 @@ struct knnm_ctx {
     double tcj_scale = 0.0;  // 2^(24 - e), max entry <= 2^e
     int tcj_dpad = 0;        // limb plane length (roundup(d, 16))
     bool limbs_ready = false;
+    bool sub64_ready = false;  // fp64 union rows for k_join_dense
+    DBuf sub64, nsq, djrec;
     bool tcj_round = false;  // the round's lazy slots hold k_join_tc's bounds (lo_rel = 1)
     DBuf limbs, lnx, lax;
     // current merge
@@ -944,6 +947,8 @@ int knnm_create(int device, knnm_ctx **out) {
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     for (auto f : {k_join_chunked<0>, k_join_chunked<1>, k_join_chunked<2>})
         CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    for (auto f : {k_join_dense<0>, k_join_dense<1>, k_join_dense<2>})
+        CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)DJ_SMEM_CAP));
 #define KNNM_MJ_ALL(M)                                                                       \
     k_join_mma<false, 1, M>, k_join_mma<false, 2, M>, k_join_mma<false, 4, M>,              \
         k_join_mma<true, 1, M>, k_join_mma<true, 2, M>, k_join_mma<true, 4, M>
@@ -972,7 +977,7 @@ int knnm_destroy(knnm_ctx *c) {
     DBuf *all[] = {&c->vec, &c->sub, &c->ugid, &c->labels, &c->labbits, &c->ids, &c->dists, &c->flags,
                    &c->sizes, &c->tail_ids, &c->tail_d, &c->tail_s, &c->indeg, &c->roff,
                    &c->rev, &c->heavy, &c->giant, &c->gscratch32, &c->nbh, &c->nlen, &c->hpairs,
-                   &c->poff, &c->worst0, &c->active, &c->rowmeta, &c->wcnt, &c->woff, &c->cBd, &c->cBs, &c->order, &c->lab0, &c->lab1, &c->bound, &c->boff, &c->mcount, &c->moff, &c->mcur, &c->memb, &c->start, &c->Bd, &c->Bs, &c->limbs, &c->lnx, &c->lax,
+                   &c->poff, &c->worst0, &c->active, &c->rowmeta, &c->wcnt, &c->woff, &c->cBd, &c->cBs, &c->order, &c->lab0, &c->lab1, &c->bound, &c->boff, &c->mcount, &c->moff, &c->mcur, &c->memb, &c->start, &c->Bd, &c->Bs, &c->limbs, &c->lnx, &c->lax, &c->sub64, &c->nsq, &c->djrec,
                    &c->counters, &c->draws, &c->draw_rows,
                    &c->draw_bad, &c->pool, &c->scan_pos, &c->vec16, &c->norms, &c->sub16, &c->subnorms, &c->out_ids, &c->out_d,
                    &c->out_s, &c->phi_leaf_lo, &c->phi_leaf_len, &c->phi_left, &c->phi_right,
@@ -1069,6 +1074,7 @@ int knnm_set_dataset(knnm_ctx *c, const float *vectors, int64_t n_all, int32_t d
             c->tcj_dpad = (d + 15) & ~15;  // limb plane length (16-byte copies)
         }
         c->limbs_ready = false;
+        c->sub64_ready = false;
         if (c->cert_u8) {
             c->dph = (d + 31) & ~31;  // u8 elements per row
             c->rowb = c->dph;
@@ -1108,6 +1114,7 @@ int knnm_begin(knnm_ctx *c, const int64_t *union_gids, int64_t n, const int8_t *
     c->k = k;
     c->slots_mode = SLOTS_PLAIN;
     c->limbs_ready = false;  // limb planes follow the union
+    c->sub64_ready = false;
     c->tcj_round = false;
     // fp32 list rows only on certified data (distances are integers < 2^24)
     // and only while every loaded distance is an exact fp32 value
@@ -1592,9 +1599,27 @@ static int ensure_limbs(knnm_ctx *c) {
     return KNNM_OK;
 }
 
+// fp64 copy of the union rows (+ the roots of the cosine norms) for
+// k_join_dense (once per merge).
+static int ensure_sub64(knnm_ctx *c) {
+    if (c->sub64_ready) return KNNM_OK;
+    const int64_t n = c->n;
+    TRY(ensure(c->sub64, sizeof(double) * (size_t)n * c->dp));
+    k_to_f64<<<grid_for(c, n * c->dp, 256), 256, 0, c->st>>>(c->subp, n * c->dp, c->sub64.as<double>());
+    CKL();
+    if (metric_is_cos(c)) {
+        TRY(ensure(c->nsq, sizeof(double) * (size_t)n));
+        k_sqrt64<<<grid_for(c, n, 256), 256, 0, c->st>>>(c->nrm64.as<double>(), n, c->nsq.as<double>());
+        CKL();
+    }
+    c->sub64_ready = true;
+    return KNNM_OK;
+}
+
 // Route of the local join for this round (dataset, k, rev_cap, mode).
 struct JoinRoute {
-    bool use_mma, tiled, lazy, tc;
+    bool use_mma, tiled, lazy, tc, dense;
+    int dense_rows;  // k_join_dense circular row buffer
     size_t smem, smem_tiled, smem_mma;
 };
 
@@ -1625,6 +1650,11 @@ static int join_route(knnm_ctx *c, int W, int mode, JoinRoute *r) {
     // accumulators fit TMEM
     r->tc = lazy && c->tcj_data && W <= TJC_MAX_W && (c->join_variant == 3 || c->join_variant < 0);
     c->tcj_round = r->tc;
+    // short non-certified rows: every admissible pair exact in register-
+    // blocked fp64 tiles (k_join_dense) when the hood's fp64 rows fit
+    r->dense_rows = dj_rows(W, c->dp, metric_is_cos(c));
+    r->dense = tiled && !lazy && !c->cert && r->dense_rows > 0 &&
+               (c->join_variant == 4 || (c->join_variant < 0 && c->d >= 64));
     r->use_mma = use_mma;
     r->tiled = tiled;
     r->lazy = lazy;
@@ -1749,6 +1779,32 @@ c->subp, c->dp, c->d, c->worst0.as<double>(), boff, stt, Bd, Bs, lo_rel, lo_abs,
             if (c->cert && !lazy) {
                 if (c->metric == 1) KNNM_TJ_LAUNCH(1, true, false);
                 else KNNM_TJ_LAUNCH(0, true, false);
+            } else if (rt.dense) {
+                TRY(ensure_sub64(c));
+                const bool cos = metric_is_cos(c);
+                const int RB = dj_rec_bytes(W, cos);
+                TRY(ensure(c->djrec, (size_t)nact * RB));
+                const int rgrid = grid_for(c, nact * 32, 256, 16);
+                if (cos)
+                    k_dense_rec<true><<<rgrid, 256, 0, c->st>>>(act, na, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
+                                                               c->worst0.as<double>(), boff, stt, nrm, c->nsq.as<double>(),
+                                                               c->djrec.as<uint8_t>(), RB);
+                else
+                    k_dense_rec<false><<<rgrid, 256, 0, c->st>>>(act, na, c->nbh.as<uint32_t>(), c->nlen.as<int32_t>(), W,
+                                                                c->worst0.as<double>(), boff, stt, nullptr, nullptr,
+                                                                c->djrec.as<uint8_t>(), RB);
+                CKL();
+                const int nrows = rt.dense_rows;
+                const size_t smem_dj = dj_smem_bytes(W, c->dp, cos, nrows);
+                const unsigned gdj = (unsigned)std::max<int64_t>(1, std::min<int64_t>(nact, (int64_t)c->sms));
+#define KNNM_DJ_LAUNCH(T)                                                                        \
+k_join_dense<T><<<gdj, DJ_THREADS, smem_dj, c->st>>>(na, W, mode, c->sub64.as<double>(), c->dp, c->d, \
+c->djrec.as<uint8_t>(), RB, nrows, Bd, Bs, cnt)
+                if (c->metric == 1) KNNM_DJ_LAUNCH(1);
+                else if (c->metric == 2) KNNM_DJ_LAUNCH(2);
+                else KNNM_DJ_LAUNCH(0);
+#undef KNNM_DJ_LAUNCH
+                c->stats.dense_join_launches += 1;
             } else if (rt.tc) {
                 TRY(ensure_limbs(c));
                 // one CTA per SM: a deep ring of (hood, K block) stages
@@ -2868,7 +2924,7 @@ int knnm_set_sample(knnm_ctx *c, int32_t new_cap) {
 }
 
 int knnm_set_join_variant(knnm_ctx *c, int32_t variant) {
-    if (!c || variant < -1 || variant > 3) return fail(KNNM_ERR_ARG, "variant %d", variant);
+    if (!c || variant < -1 || variant > 4) return fail(KNNM_ERR_ARG, "variant %d", variant);
     c->join_variant = variant;
     return KNNM_OK;
 }

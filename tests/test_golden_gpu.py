@@ -25,7 +25,7 @@ def _state_hash(eng):
     return h.hexdigest()[:32]
 
 
-@pytest.mark.parametrize("variant", [-1, 0])
+@pytest.mark.parametrize("variant", [-1, 0, 1])
 @pytest.mark.parametrize("name", sorted(GOLDEN["cases"]))
 def test_cuda_matches_reference(oracle, name, variant):
     import paper_1908_00814_b200 as km

@@ -115,7 +115,7 @@ def _to_graph(km, og):
     return g
 
 
-@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("variant", [0, 1, 2, 4])
 @pytest.mark.parametrize("n,d,k,metric,kind", [CASES[1], CASES[5], CASES[6], CASES[8]])
 def test_join_variants_agree(oracle, variant, n, d, k, metric, kind):
     """Both local-join routes (fp64-every-pair / fp32-screen tiled) are
