@@ -416,7 +416,18 @@ def config_legs(km, names, device, steps, warmup, hbm_peak, no_recall=False):
         inf = eng.info()
         lazy = (not inf["cert"]) and ds.d > 384
         slot_b = 8.0 if (inf["cert"] or inf["cert_dot"]) else 12.0
-        kr = kernel_rooflines(st, steps, ds.d, k, slot_b, lazy, hbm_peak, cosine=int(metric) == 2)
+        tc = st["tc_join_launches"] > 0
+        dense = st["dense_join_launches"] > 0
+        # k_join_tc gathers three u8 limb planes per row (3 bytes per dimension,
+        # rows padded to 16), not the fp32 row: the byte model follows the kernel
+        row_b = 3.0 * ((ds.d + 15) // 16 * 16) if tc else None
+        kr = kernel_rooflines(st, steps, ds.d, k, slot_b, lazy, hbm_peak, row_b=row_b,
+                              cosine=int(metric) == 2)
+        kr["join"]["bytes_model"] = (
+            "3-byte fixed-point limb rows (k_join_tc) + hood entries + 12 B per written slot" if tc else
+            "fp32 rows (4 d, SURVEY 8d) + hood entries + slot bytes; k_join_dense actually gathers "
+            "fp64 rows (8 d) and a per-hood record" if dense else
+            "fp32 rows (4 d, SURVEY 8d) + hood entries + slot bytes")
         rec = None
         if not no_recall:
             uh = km.KnnGraph.from_arrays(u.member_ids, u.k, u.metric, u.ids.cpu().numpy(),
@@ -430,8 +441,12 @@ def config_legs(km, names, device, steps, warmup, hbm_peak, no_recall=False):
             "rounds_per_step": st["rounds"] / steps,
             "exact_evals_per_step": st["exact_evals"] / steps,
             "exact_fraction": st["exact_evals"] / max(1, st["pairs"]),
-            "route": "lazy (d-chunked join, exact fp64 in the apply)" if lazy else
-                     ("tensor-core" if inf["cert_dot"] else "tiled fp32 screen + exact fp64"),
+            "route": ("lazy: tcgen05 fixed-point lower bounds in the join (k_join_tc), exact fp64 in the apply"
+                      if lazy and tc else
+                      "lazy (d-chunked fp32 join, exact fp64 in the apply)" if lazy else
+                      "tensor-core (mma.sync, certified)" if inf["cert_dot"] else
+                      "dense exact fp64 register tiles (k_join_dense)" if dense else
+                      "tiled fp32 screen + exact fp64"),
             "kernels": kr, "recall_at_10": rec, "setup_seconds": round(setup, 1),
             "phases_ms_per_step": {key: st[key] / steps for key in
                                    ("join_ms", "join_kernel_ms", "apply_kernel_ms", "reverse_ms",

@@ -89,6 +89,17 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, int32_t (&v)[16]) {
 }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
+// One lane of the (converged) warp; the compiler then knows the region is
+// single-threaded and feeds tcgen05.mma from uniform registers directly
+// (with `lane == 0` it wraps every MMA in a vote/branch loop).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n .reg .b32 rx;\n .reg .pred px;\n elect.sync rx|px, 0xffffffff;\n selp.u32 %0, 1, 0, px;\n}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 __device__ __forceinline__ void cp16(uint32_t dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
@@ -289,7 +300,7 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
     const uint32_t tmem = s_tmem;
 
     if (warp == 0) {
-        if (lane == 0) {
+        if (elect_one()) {
             for (int t = 0; t < T; t++) {
                 const int h = t / nki, kq = t - h * nki;
                 const int st = t % stages;
@@ -300,34 +311,36 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
                 mbar_wait(&s_full[st], (uint32_t)(t / stages) & 1u);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 tc_fence_after();
-                const int npad = (meta[h % TJC_R].width + 15) & ~15;
                 const uint32_t sb = sbase + (uint32_t)st * sstride;
-                const uint32_t idesc = tjc_idesc(npad);
+                // The limb tiles of a K block lie back to back ([L0 | L1 | L2],
+                // npw rows each), so one MMA with N = 3 npw takes L0 against
+                // all three (G0, G1, G2 partial), N = 2 npw takes L1 against
+                // [L0 | L1] (G1, G2) and N = npw takes L2 against L0 (G2):
+                // three instructions per K step instead of six, same products.
+                const uint32_t i3 = tjc_idesc(3 * npw), i2 = tjc_idesc(2 * npw), i1 = tjc_idesc(npw);
                 const uint32_t acc = tmem + (uint32_t)((h % NS) * 3 * npw);
                 const uint32_t d0 = acc, d1 = acc + (uint32_t)npw, d2 = acc + 2u * (uint32_t)npw;
 #pragma unroll
                 for (int j = 0; j < TJC_KI; j++) {
                     const int kb = kq * TJC_KI + j;
                     if (kb >= nkb) break;
-                    const uint64_t b0 = tb_desc(sb + (uint32_t)j * tile),
-                                   b1 = tb_desc(sb + (uint32_t)(TJC_KI + j) * tile),
-                                   b2 = tb_desc(sb + (uint32_t)(2 * TJC_KI + j) * tile);
+                    const uint64_t b0 = tb_desc(sb + (uint32_t)(3 * j) * tile),
+                                   b1 = tb_desc(sb + (uint32_t)(3 * j + 1) * tile),
+                                   b2 = tb_desc(sb + (uint32_t)(3 * j + 2) * tile);
 #pragma unroll
                     for (int kk = 0; kk < TJC_KB / 32; kk++) {
                         const uint32_t a = (kb | kk) == 0 ? 0u : 1u;
                         const uint64_t a0 = b0 + 2 * kk, a1 = b1 + 2 * kk, a2 = b2 + 2 * kk;
-                        tc_mma_i8(d0, a0, a0, idesc, a);
-                        tc_mma_i8(d1, a0, a1, idesc, a);
-                        tc_mma_i8(d1, a1, a0, idesc, 1u);
-                        tc_mma_i8(d2, a0, a2, idesc, a);
-                        tc_mma_i8(d2, a1, a1, idesc, 1u);
-                        tc_mma_i8(d2, a2, a0, idesc, 1u);
+                        tc_mma_i8(d0, a0, a0, i3, a);   // L0 x [L0 | L1 | L2]
+                        tc_mma_i8(d1, a1, a0, i2, 1u);  // L1 x [L0 | L1]
+                        tc_mma_i8(d2, a2, a0, i1, 1u);  // L2 x L0
                     }
                 }
                 tc_commit(&s_empty[st]);
                 if (kq == nki - 1) tc_commit(&s_accf[h % NS]);
             }
         }
+        __syncwarp();
     } else if (warp <= 2) {
         for (int h = warp - 1; h < nh; h += 2) {
             const int slot = h % TJC_R;
@@ -338,7 +351,14 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
             mbar_arrive(&s_metaf[slot]);
         }
     } else if (warp < 8) {
+        // thread -> (16-byte column c of the item's KI K blocks, rows r0,
+        // r0 + rstep, ...): the column, its K block and the swizzle phase are
+        // fixed per thread; each step copies the three limbs of one row chunk
+        static_assert(TJC_LOADERS % (8 * TJC_KI) == 0, "loader threads per row chunk set");
         const int lt = tid - 96;  // 0 .. TJC_LOADERS - 1
+        const int c = lt & (8 * TJC_KI - 1), r0 = lt / (8 * TJC_KI);
+        constexpr int rstep = TJC_LOADERS / (8 * TJC_KI);
+        const int j = c >> 3, c16 = c & 7;
         for (int t = 0; t < T; t++) {
             const int h = t / nki, kq = t - h * nki;
             const int st = t % stages;
@@ -346,20 +366,17 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
             if (kq == 0) mbar_wait(&s_metaf[h % TJC_R], (uint32_t)(h / TJC_R) & 1u);
             const TjcMeta &m = meta[h % TJC_R];
             const int w = m.width;
-            const uint32_t sb = sbase + (uint32_t)st * sstride;
-            const int kc = kq * TJC_KI * TJC_KB;
-            const int per = w * 8 * TJC_KI;  // 16-byte chunks of one limb
-#pragma unroll
-            for (int l = 0; l < 3; l++) {
-                for (int q = lt; q < per; q += TJC_LOADERS) {
-                    const int c = q & (8 * TJC_KI - 1), r = q / (8 * TJC_KI);
-                    const int j = c >> 3, c16 = c & 7;
-                    if (kq * TJC_KI + j >= nkb) continue;  // block past the row: no MMA reads it
-                    const int col = kc + c * 16;
-                    const uint32_t dst = sb + (uint32_t)(l * TJC_KI + j) * tile + (uint32_t)r * 128u +
-                                         (uint32_t)((c16 ^ (r & 7)) * 16);
-                    const bool in = col < dg;
-                    cp16z(dst, limbs + (int64_t)m.id[r] * rowb + l * dg + (in ? col : 0), in);
+            if (kq * TJC_KI + j < nkb) {  // else: block past the row, no MMA reads it
+                const int col = kq * TJC_KI * TJC_KB + c * 16;
+                const bool in = col < dg;  // columns past the padded row read as zero
+                const uint8_t *src0 = limbs + (in ? col : 0);
+                const uint32_t db = sbase + (uint32_t)st * sstride + (uint32_t)(3 * j) * tile;
+                for (int r = r0; r < w; r += rstep) {
+                    const uint8_t *src = src0 + (int64_t)m.id[r] * rowb;
+                    const uint32_t dst = db + (uint32_t)r * 128u + (uint32_t)((c16 ^ (r & 7)) << 4);
+                    cp16z(dst, src, in);
+                    cp16z(dst + tile, src + dg, in);
+                    cp16z(dst + 2u * tile, src + 2 * dg, in);
                 }
             }
             cp_async_arrive(&s_full[st]);
