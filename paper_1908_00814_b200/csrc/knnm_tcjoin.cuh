@@ -64,9 +64,9 @@ __host__ inline size_t tjc_smem_bytes(int W, int stages) {
 
 struct TjcMeta {
     int id[TJC_MAX_W];
-    int pos[TJC_MAX_W];
-    int nw[TJC_MAX_W];
-    int sc[TJC_MAX_W];
+    uint8_t pos[TJC_MAX_W];
+    uint8_t nw[TJC_MAX_W];
+    uint8_t sc[TJC_MAX_W];
     double w[TJC_MAX_W];   // round-start worst
     double nx[TJC_MAX_W];  // |x|^2 (fp64, sequential: within d 2^-53 of the real value)
     double ax[TJC_MAX_W];  // sum x (upper bound)
@@ -86,6 +86,16 @@ __device__ __forceinline__ void tc_ld16(uint32_t taddr, int32_t (&v)[16]) {
         : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
           "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
         : "r"(taddr));
+}
+__device__ __forceinline__ void tc_ld4(uint32_t taddr, int32_t (&v)[4]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                 : "r"(taddr));
+}
+template <int CB>
+__device__ __forceinline__ void tc_ldn(uint32_t taddr, int32_t (&v)[CB]) {
+    if constexpr (CB == 16) tc_ld16(taddr, v);
+    else tc_ld4(taddr, v);
 }
 __device__ __forceinline__ void tc_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 
@@ -150,9 +160,9 @@ __device__ __forceinline__ void tjc_classify(TjcMeta &m, int64_t u, const uint32
         if (slot >= 0) {
             const int id = (int)(ev[b] >> 2);
             m.id[slot] = id;
-            m.pos[slot] = j;
-            m.nw[slot] = (int)(ev[b] & 1);
-            m.sc[slot] = c;
+            m.pos[slot] = (uint8_t)j;
+            m.nw[slot] = (uint8_t)(ev[b] & 1);
+            m.sc[slot] = (uint8_t)c;
             m.w[slot] = worst0[id];
             m.nx[slot] = nx[id];
             m.ax[slot] = ax[id];
@@ -163,12 +173,17 @@ __device__ __forceinline__ void tjc_classify(TjcMeta &m, int64_t u, const uint32
     if (lane == 0) m.width = w;
 }
 
-// epilogue of one hood by 8 warps: warp e reads TMEM lane quarter e % 4
-// (rows 32 (e % 4) ..), 16-column blocks alternating between e < 4 and
-// e >= 4; each thread emits the admissible pairs (i = its row, j > i)
+// epilogue of one hood by 8 warps.  A warp may read only the TMEM lane
+// quarter warp % 4 (rows 32 q4 ..), so the warps of a quarter split the
+// columns: blocks of CB columns dealt round-robin to the quarter's `nparts`
+// warps (part = this warp's index among them); each thread emits the
+// admissible pairs (i = its row, j > i).  Hoods of up to 64 members occupy
+// quarters 0 and 1 only: four warps per quarter with 4-column blocks
+// (k_join_tc's narrow layout) instead of two with 16-column blocks.
+template <int CB>
 __device__ __forceinline__ void tjc_epilogue(const TjcMeta &m, uint32_t tacc, int npw, int mode, int d, double s,
-                                             double *__restrict__ Bd, int32_t *__restrict__ Bs, int warp,
-                                             unsigned lane) {
+                                             double *__restrict__ Bd, int32_t *__restrict__ Bs, int q4, int part,
+                                             int nparts, unsigned lane) {
     const double s2 = s * s;
     const double eps = ldexp(1.0, -50);
     const double tail = (double)d * TJC_GMAX_TAIL;
@@ -176,7 +191,6 @@ __device__ __forceinline__ void tjc_epilogue(const TjcMeta &m, uint32_t tacc, in
     const double lrel = 1.0 - (double)(d + 8) * ldexp(1.0, -53);
     const int w = m.width;
     const int npad = (w + 15) & ~15;
-    const int q4 = warp & 3;
     const int i = q4 * 32 + (int)lane;
     const bool rowok = i < w;
     const int ri = rowok ? i : 0;
@@ -184,17 +198,17 @@ __device__ __forceinline__ void tjc_epilogue(const TjcMeta &m, uint32_t tacc, in
     const int newi = m.nw[ri], sci = m.sc[ri], posi = m.pos[ri], idi = m.id[ri];
     const uint64_t sti = m.st[ri];
     const int labi = sci >> 1;
-    for (int c0 = (warp >> 2) * 16; c0 < npad; c0 += 32) {
-        if (q4 * 32 >= w || c0 + 15 <= q4 * 32) continue;  // no pair (i < j < w) here (warp-uniform)
-        int32_t g0[16], g1[16], g2[16];
+    for (int c0 = part * CB; c0 < npad; c0 += nparts * CB) {
+        if (q4 * 32 >= w || c0 + CB - 1 <= q4 * 32) continue;  // no pair (i < j < w) here (warp-uniform)
+        int32_t g0[CB], g1[CB], g2[CB];
         const uint32_t ta = tacc + ((uint32_t)(q4 * 32) << 16) + (uint32_t)c0;
-        tc_ld16(ta, g0);
-        tc_ld16(ta + (uint32_t)npw, g1);
-        tc_ld16(ta + 2u * (uint32_t)npw, g2);
+        tc_ldn<CB>(ta, g0);
+        tc_ldn<CB>(ta + (uint32_t)npw, g1);
+        tc_ldn<CB>(ta + 2u * (uint32_t)npw, g2);
         tc_wait_ld();
         if (!rowok) continue;
 #pragma unroll
-        for (int tt = 0; tt < 16; tt++) {
+        for (int tt = 0; tt < CB; tt++) {
             const int j = c0 + tt;
             if (j <= i || j >= w) continue;
             // admissible (_kernels.py:391-399) and at least one new
@@ -237,19 +251,26 @@ __device__ __forceinline__ void cp16z(uint32_t dst, const void *src, bool valid)
 }
 
 // Warp roles (mbarrier handshakes, no CTA-wide barrier in the steady state):
-//   warp 0 (lane 0)   tensor core issue: item t waits full[t % S], issues the
-//                     limb MMAs, commits empty[t % S]; a hood's last item
-//                     also commits accf[hood & 1]
-//   warps 1-2         members of hood h (warp 1 + h % 2) into meta[h % R]
-//                     once hood h - R's epilogue released it -> metaf
-//   warps 3-7         row gathers: item t into stage t % S once the MMAs of
+//   MMA (one elected lane)  item t waits full[t % S], issues the limb MMAs,
+//                     commits empty[t % S]; a hood's last item also commits
+//                     accf[hood % NS]
+//   classify (2 warps)  members of hood h (warp h % 2) into meta[h % R] once
+//                     hood h - R's epilogue released it -> metaf
+//   loaders (5 warps)  row gathers: item t into stage t % S once the MMAs of
 //                     item t - S retired (cp.async, arrive-on-completion)
-//   warps 8-15        epilogue of hood h (TMEM set h % NS, lane quarter
-//                     warp % 4) -> acce[h % NS], metae[h % R]
+//   epilogue (8 warps)  hood h from TMEM set h % NS -> acce[h % NS], metae[h % R]
+// A warp reads only the TMEM lane quarter warp % 4, and a hood's rows sit in
+// lanes 0 .. w - 1.  Narrow hoods (W <= 64, the usual case) therefore put
+// all eight epilogue warps on quarters 0 and 1 -- warps {0,4,8,12} and
+// {1,5,9,13}, four column parts each -- and the other roles on the warps
+// of quarters 2 and 3 (MMA 3; classify 7, 11; loaders 2, 6, 10, 14, 15).
+// Wide hoods keep two epilogue warps per quarter (MMA 0; classify 1-2;
+// loaders 3-7; epilogue 8-15).  With the epilogue on two warps per busy
+// quarter it, not the tensor core, set the pace (19.3 -> 11.6 ms without it).
 // NS = accumulator sets that fit TMEM's 512 columns (3 for W <= 48), so the
 // tensor core runs up to NS - 1 hoods ahead of the epilogue.
-constexpr int TJC_R = 4;              // member-metadata ring (hoods)
-constexpr int TJC_LOADERS = 5 * 32;   // warps 3-7
+constexpr int TJC_R = 4;              // member-metadata ring (hoods; 6 and 7 measured: no change)
+constexpr int TJC_LOADERS = 5 * 32;   // five loader warps
 
 __global__ void __launch_bounds__(TJC_THREADS, 1)
 k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__restrict__ nbh,
@@ -275,6 +296,26 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
     const int nh = (int)blockIdx.x < nactive ? (nactive - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     const int T = nh * nki;
     const int ns0 = 512 / (3 * npw), NS = ns0 < 4 ? ns0 : 4;  // accumulator sets
+    // roles (see above): 0 MMA, 1 classify, 2 loader, 3 epilogue; idx = index within the role
+    const bool wide = W > 64;
+    int role, idx;
+    if (wide) {
+        role = warp == 0 ? 0 : warp <= 2 ? 1 : warp < 8 ? 2 : 3;
+        idx = warp == 0 ? 0 : warp <= 2 ? warp - 1 : warp < 8 ? warp - 3 : (warp - 8) >> 2;
+    } else if ((warp & 3) <= 1) {
+        role = 3;
+        idx = warp >> 2;
+    } else if (warp == 3) {
+        role = 0;
+        idx = 0;
+    } else if (warp == 7 || warp == 11) {
+        role = 1;
+        idx = warp == 7 ? 0 : 1;
+    } else {
+        role = 2;
+        idx = warp == 15 ? 4 : warp >> 2;  // 2, 6, 10, 14 -> 0..3; 15 -> 4
+    }
+    const int q4 = warp & 3, part = idx;  // epilogue: lane quarter, column part
 
     if (tid == 0) {
         for (int b = 0; b < stages; b++) {
@@ -299,7 +340,7 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
     tc_fence_after();
     const uint32_t tmem = s_tmem;
 
-    if (warp == 0) {
+    if (role == 0) {
         if (elect_one()) {
             for (int t = 0; t < T; t++) {
                 const int h = t / nki, kq = t - h * nki;
@@ -341,8 +382,8 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
             }
         }
         __syncwarp();
-    } else if (warp <= 2) {
-        for (int h = warp - 1; h < nh; h += 2) {
+    } else if (role == 1) {
+        for (int h = idx; h < nh; h += 2) {
             const int slot = h % TJC_R;
             if (h >= TJC_R) mbar_wait(&s_metae[slot], (uint32_t)((h - TJC_R) / TJC_R) & 1u);
             tjc_classify(meta[slot], active[blockIdx.x + (int64_t)h * gridDim.x], nbh, nlen, W, mode, nx, ax,
@@ -350,12 +391,12 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
             __syncwarp();
             mbar_arrive(&s_metaf[slot]);
         }
-    } else if (warp < 8) {
+    } else if (role == 2) {
         // thread -> (16-byte column c of the item's KI K blocks, rows r0,
         // r0 + rstep, ...): the column, its K block and the swizzle phase are
         // fixed per thread; each step copies the three limbs of one row chunk
         static_assert(TJC_LOADERS % (8 * TJC_KI) == 0, "loader threads per row chunk set");
-        const int lt = tid - 96;  // 0 .. TJC_LOADERS - 1
+        const int lt = idx * 32 + (int)lane;  // 0 .. TJC_LOADERS - 1
         const int c = lt & (8 * TJC_KI - 1), r0 = lt / (8 * TJC_KI);
         constexpr int rstep = TJC_LOADERS / (8 * TJC_KI);
         const int j = c >> 3, c16 = c & 7;
@@ -387,8 +428,12 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
             mbar_wait(&s_metaf[slot], (uint32_t)(h / TJC_R) & 1u);
             mbar_wait(&s_accf[h % NS], (uint32_t)(h / NS) & 1u);
             tc_fence_after();
-            tjc_epilogue(meta[slot], tmem + (uint32_t)((h % NS) * 3 * npw), npw, mode, d, s, Bd, Bs, warp - 8,
-                         lane);
+            if (wide)
+                tjc_epilogue<16>(meta[slot], tmem + (uint32_t)((h % NS) * 3 * npw), npw, mode, d, s, Bd, Bs, q4,
+                                 part, 2, lane);
+            else
+                tjc_epilogue<4>(meta[slot], tmem + (uint32_t)((h % NS) * 3 * npw), npw, mode, d, s, Bd, Bs, q4,
+                                part, 4, lane);
             tc_fence_before();
             mbar_arrive(&s_acce[h % NS]);
             mbar_arrive(&s_metae[slot]);

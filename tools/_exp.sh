@@ -5,6 +5,6 @@ python - <<PY
 import json
 d=json.loads(open('gpurun_out/c3_new.json').read().strip().splitlines()[-1])
 c=d['configs']['c3']
-print('c3 merge_s',c['merge_seconds'],c['phases_ms_per_step'],c['route'])
-print(c['kernels']['join'])
+print('c3 merge_s',c['merge_seconds'],c['phases_ms_per_step'])
 PY
+python tools/_exp.py c3 0.3 1 2>&1 | tail -1
