@@ -42,7 +42,10 @@ namespace knnm {
 
 constexpr int TJC_THREADS = 512;  // 16 warps (roles: see k_join_tc)
 constexpr int TJC_KB = 128;          // K bytes per block (one swizzle atom row)
-constexpr int TJC_KI = 2;            // K blocks per ring item
+#ifndef KNNM_TJC_KI
+#define KNNM_TJC_KI 2
+#endif
+constexpr int TJC_KI = KNNM_TJC_KI;   // K blocks per ring item
 constexpr int TJC_MAX_W = 80;        // 3 accumulators x 80 columns <= 256
 constexpr int TJC_MAX_STAGES = 16;
 constexpr size_t TJC_SMEM_CAP = 200 * 1024;
@@ -114,20 +117,37 @@ __device__ __forceinline__ void cp16(uint32_t dst, const void *src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 
-// warp 0: members of hood u in class order (as k_join_chunked) into m
-__device__ __forceinline__ void tjc_classify(TjcMeta &m, int64_t u, const uint32_t *__restrict__ nbh,
-                                             const int32_t *__restrict__ nlen, int W, int mode,
+// A hood's length and neighbour entries, loaded one hood ahead of their use
+// (the classification warps are a chain of dependent global loads: hood id
+// -> length / entries -> per-member gathers; without the look-ahead two
+// warps delivered a hood every 2.6 us, the floor of the whole kernel).
+struct TjcPre {
+    int w;
+    uint32_t ev[4];
+};
+__device__ __forceinline__ void tjc_prefetch(TjcPre &p, bool ok, int64_t u, const uint32_t *__restrict__ nbh,
+                                             const int32_t *__restrict__ nlen, int W, unsigned lane) {
+    p.w = ok ? __ldg(nlen + u) : 0;
+#pragma unroll
+    for (int b = 0; b < 4; b++) {
+        const int j = b * 32 + (int)lane;
+        p.ev[b] = (ok && j < W) ? __ldg(nbh + u * W + j) : 0u;  // masked by the length below
+    }
+}
+
+// classification warp: members of hood u in class order (as k_join_chunked) into m
+__device__ __forceinline__ void tjc_classify(TjcMeta &m, int64_t u, const TjcPre &pre, int W, int mode,
                                              const double *__restrict__ nx, const double *__restrict__ ax,
                                              const double *__restrict__ worst0, const uint64_t *__restrict__ boff,
                                              const uint32_t *__restrict__ start, unsigned lane) {
-    const int w = nlen[u];
+    const int w = pre.w;
     uint32_t ev[4];
     int clsv[4];
     int cnts[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int b = 0; b < 4; b++) {
         const int j = b * 32 + (int)lane;
-        ev[b] = j < w ? nbh[u * W + j] : 0u;
+        ev[b] = j < w ? pre.ev[b] : 0u;
     }
 #pragma unroll
     for (int b = 0; b < 4; b++) {
@@ -269,7 +289,10 @@ __device__ __forceinline__ void cp16z(uint32_t dst, const void *src, bool valid)
 // quarter it, not the tensor core, set the pace (19.3 -> 11.6 ms without it).
 // NS = accumulator sets that fit TMEM's 512 columns (3 for W <= 48), so the
 // tensor core runs up to NS - 1 hoods ahead of the epilogue.
-constexpr int TJC_R = 4;              // member-metadata ring (hoods; 6 and 7 measured: no change)
+#ifndef KNNM_TJC_R
+#define KNNM_TJC_R 4
+#endif
+constexpr int TJC_R = KNNM_TJC_R;     // member-metadata ring (hoods)
 constexpr int TJC_LOADERS = 5 * 32;   // five loader warps
 
 __global__ void __launch_bounds__(TJC_THREADS, 1)
@@ -361,20 +384,25 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
                 const uint32_t i3 = tjc_idesc(3 * npw), i2 = tjc_idesc(2 * npw), i1 = tjc_idesc(npw);
                 const uint32_t acc = tmem + (uint32_t)((h % NS) * 3 * npw);
                 const uint32_t d0 = acc, d1 = acc + (uint32_t)npw, d2 = acc + 2u * (uint32_t)npw;
+                // Same-shape MMAs back to back: the three products write
+                // overlapping accumulator columns with different N, and the
+                // tensor core drains between such instructions (interleaved
+                // per K step they ran at ~120 cycles each, three times the
+                // pipelined rate).  Integer sums: the order is free.
 #pragma unroll
-                for (int j = 0; j < TJC_KI; j++) {
-                    const int kb = kq * TJC_KI + j;
-                    if (kb >= nkb) break;
-                    const uint64_t b0 = tb_desc(sb + (uint32_t)(3 * j) * tile),
-                                   b1 = tb_desc(sb + (uint32_t)(3 * j + 1) * tile),
-                                   b2 = tb_desc(sb + (uint32_t)(3 * j + 2) * tile);
+                for (int p3 = 0; p3 < 3; p3++) {
 #pragma unroll
-                    for (int kk = 0; kk < TJC_KB / 32; kk++) {
-                        const uint32_t a = (kb | kk) == 0 ? 0u : 1u;
-                        const uint64_t a0 = b0 + 2 * kk, a1 = b1 + 2 * kk, a2 = b2 + 2 * kk;
-                        tc_mma_i8(d0, a0, a0, i3, a);   // L0 x [L0 | L1 | L2]
-                        tc_mma_i8(d1, a1, a0, i2, 1u);  // L1 x [L0 | L1]
-                        tc_mma_i8(d2, a2, a0, i1, 1u);  // L2 x L0
+                    for (int j = 0; j < TJC_KI; j++) {
+                        const int kb = kq * TJC_KI + j;
+                        if (kb >= nkb) break;
+                        const uint64_t b0 = tb_desc(sb + (uint32_t)(3 * j) * tile);
+                        const uint64_t bp = tb_desc(sb + (uint32_t)(3 * j + p3) * tile);
+#pragma unroll
+                        for (int kk = 0; kk < TJC_KB / 32; kk++) {
+                            if (p3 == 0) tc_mma_i8(d0, b0 + 2 * kk, b0 + 2 * kk, i3, (kb | kk) == 0 ? 0u : 1u);  // L0 x [L0 | L1 | L2]
+                            else if (p3 == 1) tc_mma_i8(d1, bp + 2 * kk, b0 + 2 * kk, i2, 1u);  // L1 x [L0 | L1]
+                            else tc_mma_i8(d2, bp + 2 * kk, b0 + 2 * kk, i1, 1u);               // L2 x L0
+                        }
                     }
                 }
                 tc_commit(&s_empty[st]);
@@ -383,13 +411,30 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
         }
         __syncwarp();
     } else if (role == 1) {
-        for (int h = idx; h < nh; h += 2) {
+        // two register sets (A: this warp's even turns, B: odd) so a
+        // prefetched hood is consumed without register moves
+        auto hood_of = [&](int h) { return h < nh ? (int64_t)__ldg(active + blockIdx.x + (int64_t)h * gridDim.x) : 0; };
+        auto step = [&](int h, int64_t u, const TjcPre &pre) {
             const int slot = h % TJC_R;
             if (h >= TJC_R) mbar_wait(&s_metae[slot], (uint32_t)((h - TJC_R) / TJC_R) & 1u);
-            tjc_classify(meta[slot], active[blockIdx.x + (int64_t)h * gridDim.x], nbh, nlen, W, mode, nx, ax,
-                         worst0, boff, start, lane);
+            tjc_classify(meta[slot], u, pre, W, mode, nx, ax, worst0, boff, start, lane);
             __syncwarp();
             mbar_arrive(&s_metaf[slot]);
+        };
+        int h = idx;
+        int64_t uA = hood_of(h), uB = hood_of(h + 2);
+        TjcPre pA, pB;
+        tjc_prefetch(pA, h < nh, uA, nbh, nlen, W, lane);
+        for (; h < nh; h += 4) {
+            tjc_prefetch(pB, h + 2 < nh, uB, nbh, nlen, W, lane);
+            const int64_t uA2 = hood_of(h + 4);
+            step(h, uA, pA);
+            if (h + 2 >= nh) break;
+            tjc_prefetch(pA, h + 4 < nh, uA2, nbh, nlen, W, lane);
+            const int64_t uB2 = hood_of(h + 6);
+            step(h + 2, uB, pB);
+            uA = uA2;
+            uB = uB2;
         }
     } else if (role == 2) {
         // thread -> (16-byte column c of the item's KI K blocks, rows r0,
