@@ -407,7 +407,11 @@ int scan(knnm_ctx *c, const TI *in, TO *out, int64_t n, int level = 0) {
     return KNNM_OK;
 }
 
-uint64_t bucket_budget(knnm_ctx *c) { return c->cand_budget_bytes / (sizeof(double) + sizeof(int32_t)); }
+// Slots the candidate budget holds: 8 bytes each when the source row rides in
+// the packed slot (tensor-core join: no Bs array), else 8 + 4.
+uint64_t bucket_budget(knnm_ctx *c, bool packed_only = false) {
+    return c->cand_budget_bytes / (packed_only ? sizeof(double) : sizeof(double) + sizeof(int32_t));
+}
 
 int ensure_slots_noinit(knnm_ctx *c, uint64_t slots) {
     TRY(ensure(c->Bd, sizeof(double) * slots));
@@ -416,9 +420,9 @@ int ensure_slots_noinit(knnm_ctx *c, uint64_t slots) {
     return KNNM_OK;
 }
 
-int ensure_slots(knnm_ctx *c, uint64_t slots) {
+int ensure_slots(knnm_ctx *c, uint64_t slots, bool need_bs = true) {
     TRY(ensure(c->Bd, sizeof(double) * slots));
-    TRY(ensure(c->Bs, sizeof(int32_t) * slots));
+    if (need_bs) TRY(ensure(c->Bs, sizeof(int32_t) * slots));
     // NaN fill: a slot the join does not write cannot pass (see k_apply_stream)
     CK(cudaMemsetAsync(c->Bd.p, 0xff, sizeof(double) * slots, c->st));
     c->gen_valid = false;
@@ -430,9 +434,9 @@ int ensure_slots(knnm_ctx *c, uint64_t slots) {
 // round (1..254); the whole buffer is zeroed only when it was (re)allocated,
 // used in another format, or the tags wrap.
 int ensure_slots_tagged(knnm_ctx *c, uint64_t slots) {
+    // (tensor-core join only: the source row is in the slot, no Bs array)
     const size_t before = c->Bd.bytes;
     TRY(ensure(c->Bd, sizeof(double) * slots));
-    TRY(ensure(c->Bs, sizeof(int32_t) * slots));
     if (c->Bd.bytes != before || !c->gen_valid || c->last_gen >= 254) {
         CK(cudaMemsetAsync(c->Bd.p, 0, c->Bd.bytes, c->st));
         c->last_gen = 0;
@@ -1707,7 +1711,7 @@ static int join_chunk(knnm_ctx *c, int32_t mode, int W, const int32_t *act, int6
         // tensor-core join, unsharded: generation-tagged slots, no prefill
         const bool tagged = use_mma && !local_only && c->gen_slots && n < (int64_t)(1 << 24);
         if (tagged) TRY(ensure_slots_tagged(c, pairs2));
-        else TRY(ensure_slots(c, pairs2));
+        else TRY(ensure_slots(c, pairs2, !use_mma));
         if (!fused) {
             TRY(scan<uint32_t, uint32_t>(c, c->mcount.as<uint32_t>(), c->moff.as<uint32_t>(), n));
             TRY(ensure_memb(c, (uint64_t)n * W, (uint64_t)n * W));
@@ -2048,11 +2052,9 @@ static int round_impl(knnm_ctx *c, int32_t mode, int32_t rev_cap, uint64_t round
     }
 
     int64_t acc_total = 0;
-    {  // the slot format is fixed even when this rank has no pairs
-        JoinRoute rt;
-        TRY(join_route(c, W, mode, &rt));
-    }
-    const uint64_t budget = bucket_budget(c);
+    JoinRoute rt0;  // the slot format is fixed even when this rank has no pairs
+    TRY(join_route(c, W, mode, &rt0));
+    const uint64_t budget = bucket_budget(c, rt0.use_mma);
     if (local_only) {
         // sharded round: the join runs chunk by chunk in knnm_local_join,
         // with the exchange of each chunk's slots in between

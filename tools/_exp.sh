@@ -1,3 +1,8 @@
-for v in R7 KI1 KI1R7; do
-  KNNM_LIB=$PWD/tools/_var/libknnm_$v.so timeout 300 python tools/_exp.py c3 0.3 1 2>&1 | tail -1
-done
+python -m pytest tests -m gpu -x -q 2>&1 | tail -3
+F="--no-cpu --no-recall --no-bf --no-rho-half --steps 3 --warmup 2 --configs="
+python bench.py $F > gpurun_out/c5_new.json 2> gpurun_out/c5_new.err
+python - <<PY
+import json
+d=json.loads(open('gpurun_out/c5_new.json').read().strip().splitlines()[-1])
+print('c2 ms',d['ms_per_step'],'c5',d['config5'])
+PY
