@@ -167,12 +167,12 @@ __global__ void k_sqrt64(const double *__restrict__ a, int64_t n, double *__rest
 // Producer: order a hood's members by class (class = (label != 0) * 2 +
 // !new, _kernels.py:391-399) from its record, build the pair-rank table and
 // the rectangles.
-__device__ __forceinline__ void dj_classify(DjMeta &M, const uint8_t *R, int mode, unsigned lane) {
+__device__ __forceinline__ void dj_classify(DjMeta &M, const uint8_t *R, int mode, unsigned lane, int (&cnts)[4]) {
     const int w = *reinterpret_cast<const int *>(R);
     const uint32_t *E = reinterpret_cast<const uint32_t *>(R + 16);
     uint32_t ev[4];
     int clsv[4];
-    int cnts[4] = {0, 0, 0, 0};
+    cnts[0] = cnts[1] = cnts[2] = cnts[3] = 0;
 #pragma unroll
     for (int b = 0; b < 4; b++) {
         const int j = b * 32 + (int)lane;
@@ -212,9 +212,20 @@ __device__ __forceinline__ void dj_classify(DjMeta &M, const uint8_t *R, int mod
         int nr = 0, np = 0;
         auto add = [&](int r0, int r1, int c0, int c1, int tri) {
             if (r1 > r0 && c1 > c0) {
-                const int h = r1 - r0, wd = c1 - c0;
+                int h = r1 - r0, wd = c1 - c0;
                 const int a0 = ((h + 31) & ~31) * ((wd + 7) & ~7), a1 = ((h + 15) & ~15) * ((wd + 15) & ~15);
-                const int lay = a1 < a0 ? 1 : 0;
+                // a full rectangle may also run transposed (distances and
+                // the emission are symmetric in the pair): 32 x 8 patches
+                // along its long side, e.g. 5 new x 40 members -> 2 patches
+                // instead of 3 (16 x 16) or 5 (32 x 8)
+                const int a0t = tri ? 0x7fffffff : ((wd + 31) & ~31) * ((h + 7) & ~7);
+                int lay = a1 < a0 ? 1 : 0;
+                if (a0t < (lay ? a1 : a0)) {
+                    lay = 0;
+                    int t = r0; r0 = c0; c0 = t;
+                    t = r1; r1 = c1; c1 = t;
+                    t = h; h = wd; wd = t;
+                }
                 const int npc = (wd + dj_pcols(lay) - 1) / dj_pcols(lay);
                 M.rect[nr++] = DjRect{r0, r1, c0, c1, tri, lay, npc, np};
                 np += ((h + dj_prows(lay) - 1) / dj_prows(lay)) * npc;
@@ -298,17 +309,31 @@ k_join_dense(int nactive, int W, int mode, const double *__restrict__ sub64, int
             const int w = *reinterpret_cast<const int *>(R);
             while (head + w - tail > C) release_one();
             DjMeta &M = M0[h];
-            dj_classify(M, R, mode, lane);
+            int cn[4];
+            dj_classify(M, R, mode, lane, cn);
             if (lane == 0) M.base = (int)(head % C);
             __syncwarp();
             const uint32_t *E = reinterpret_cast<const uint32_t *>(R + 16);
             fence_proxy_async();
             const uint32_t row_bytes = (uint32_t)dp * 8u;
-            if (lane == 0) mbar_expect_tx(&full[h], row_bytes * (uint32_t)w);
+            // Rows no rectangle touches are not fetched (their slots in the
+            // ring stay stale): with A = label 0, B = label 1, old A members
+            // pair only with new B members and old B members only with new
+            // A members (modes 1, 2; mode 2's B x B block needs a new B
+            // member) -- in late rounds, with a new member or two per hood,
+            // about half of a hood's rows.
+            const int nAn = cn[0], nA = cn[0] + cn[1], nBn = cn[2];
+            const bool needAo = mode == 0 || nBn > 0;
+            const bool needBo = mode == 0 || nAn > 0 || (mode == 2 && nBn > 0);
+            const int nfetch = nAn + (needAo ? nA - nAn : 0) + nBn + (needBo ? w - nA - nBn : 0);
+            if (lane == 0) mbar_expect_tx(&full[h], row_bytes * (uint32_t)nfetch);
             __syncwarp();
-            for (int sl = (int)lane; sl < w; sl += 32)
-                bulk_g2s(F0 + (size_t)((head + sl) % C) * S, sub64 + (int64_t)(E[M.pos[sl]] >> 2) * dp, row_bytes,
-                         &full[h]);
+            for (int sl = (int)lane; sl < w; sl += 32) {
+                const bool need = sl < nAn || (sl < nA ? needAo : (sl < nA + nBn || needBo));
+                if (need)
+                    bulk_g2s(F0 + (size_t)((head + sl) % C) * S, sub64 + (int64_t)(E[M.pos[sl]] >> 2) * dp,
+                             row_bytes, &full[h]);
+            }
             head += w;
         }
     } else {
