@@ -586,18 +586,22 @@ __device__ __forceinline__ void lazy_chunk_eval(const WarpRow<E> &s, int k, cons
 // ballot (worst = entry k-1, rows sorted by (d, id)) instead of a tracked
 // worst.  Returns 1 (warp-uniform) when accepted.  s.worst is left stale:
 // the caller refreshes it (warp_apply_chunk).
-template <typename T>
+// FULL: the row is known to hold k entries (the usual state: no size vote,
+// no growth).
+template <typename T, bool FULL = false>
 __device__ __forceinline__ int warp_insert1(WarpRow<1, T> &s, int k, int src, T nd, unsigned lane) {
     const int idf = s.idf[0];
     const T d = s.d[0];
-    const bool in = (int)lane < s.sz;
+    const bool in = (int)lane < (FULL ? k : s.sz);
     const int id = idf >> 1;
     if (__any_sync(FULL_MASK, in && id == src)) return 0;  // already listed
     // (sz is the same in every lane; a vote makes that visible to the compiler,
     // so the tests below are uniform branches)
-    const bool full = __all_sync(FULL_MASK, s.sz == k);
+    const bool full = FULL ? true : __all_sync(FULL_MASK, s.sz == k);
     const unsigned bs = __ballot_sync(FULL_MASK, in && nd < d);
-    if (full && !((bs >> (k - 1)) & 1u)) return 0;  // nd >= worst (distance only)
+    // nd >= worst (distance only).  FULL callers pass only candidates below the
+    // current worst (warp_apply_chunk refreshes its live mask after every insert)
+    if (!FULL && full && !((bs >> (k - 1)) & 1u)) return 0;
     const unsigned b = bs | __ballot_sync(FULL_MASK, in && nd == d && src < id);
     const int pos = b ? __ffs(b) - 1 : s.sz;
     const int last = full ? k - 1 : s.sz;
@@ -620,13 +624,30 @@ __device__ __forceinline__ int warp_apply_chunk(WarpRow<E, T> &s, int k, int src
         int acc = 0;
         unsigned m = __ballot_sync(FULL_MASK, (int)lane < cnt && d_l < dist_inf<T>() &&
                                                   (s.sz < k || d_l < s.worst));
+        // rows still filling up (first inserts of a fresh row)
+        while (m && s.sz < k) {
+            const int i = __ffs(m) - 1;
+            m &= m - 1;
+            acc += warp_insert1<T>(s, k, __shfl_sync(FULL_MASK, src_l, i), __shfl_sync(FULL_MASK, d_l, i), lane);
+            if (s.sz == k) {
+                s.worst = __shfl_sync(FULL_MASK, s.d[0], (k - 1) & 31);
+                m &= __ballot_sync(FULL_MASK, d_l < s.worst);
+            }
+        }
         while (m) {
             const int i = __ffs(m) - 1;
             m &= m - 1;
-            acc += warp_insert1<T>(s, k, __shfl_sync(FULL_MASK, src_l, i),
-                                   __shfl_sync(FULL_MASK, d_l, i), lane);
+            if (warp_insert1<T, true>(s, k, __shfl_sync(FULL_MASK, src_l, i), __shfl_sync(FULL_MASK, d_l, i),
+                                      lane)) {
+                acc++;
+                // the worst only decreases once the row is full: candidates it
+                // now excludes leave the loop with one ballot instead of a
+                // turn each (so every candidate that gets a turn is below
+                // the worst of its turn)
+                s.worst = __shfl_sync(FULL_MASK, s.d[0], (k - 1) & 31);
+                m &= __ballot_sync(FULL_MASK, d_l < s.worst);
+            }
         }
-        if (acc && s.sz == k) s.worst = __shfl_sync(FULL_MASK, s.d[0], (k - 1) & 31);
         return acc;
     }
     int acc = 0;

@@ -1,3 +1,8 @@
-for it in 1 6; do python tools/_exp.py c4 1.0 $it 2>&1 | tail -1; done
-python tools/_exp.py c1 1.0 10 2>&1 | tail -1
-python -m pytest tests -m gpu -x -q -k "parity or golden or reference_suite or random" 2>&1 | tail -3
+F="--no-cpu --no-recall --configs= --no-bf --no-c5 --no-rho-half --steps 5 --warmup 3"
+python bench.py $F > gpurun_out/c2_new.json 2> gpurun_out/c2_new.err
+python - <<PY
+import json
+d=json.loads(open('gpurun_out/c2_new.json').read().strip().splitlines()[-1])
+print('c2 ms',d['ms_per_step'],d['phases_ms_per_step'],'apply',d['kernels']['apply']['ms_per_step'])
+PY
+python -m pytest tests -m gpu -x -q -k "parity or golden or random" 2>&1 | tail -3

@@ -1,6 +1,8 @@
 set -x
-python tools/full_parity.py c3 c4 c2 > gpurun_out/full_parity_r2b.json 2> gpurun_out/full_parity_r2b.err
-tail -c 600 gpurun_out/full_parity_r2b.json
-ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_join_tc -c 1 -o gpurun_out/c3_tc -f python tools/profile_config.py c3 --scale 0.3 > gpurun_out/ncu_c3.log 2>&1
-ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:k_join_dense -c 1 -o gpurun_out/c4_dense -f python tools/profile_config.py c4 --scale 0.3 > gpurun_out/ncu_c4.log 2>&1
-tail -3 gpurun_out/ncu_c3.log gpurun_out/ncu_c4.log
+F="--steps 1 --warmup 1 --no-cpu --no-recall --configs= --no-bf --no-c5 --no-rho-half"
+ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv --log-file gpurun_out/launches_c2.csv python bench.py $F > gpurun_out/ncu_launch.log 2>&1
+tail -n 2 gpurun_out/ncu_launch.log
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --profile-from-start off -k regex:'k_join_mma|k_apply_stream|k_assemble' --csv --log-file gpurun_out/traffic_c2.csv python bench.py $F > gpurun_out/ncu_traffic.log 2>&1
+tail -n 2 gpurun_out/ncu_traffic.log
+python tools/full_parity.py c3 c4 c2 > gpurun_out/full_parity_final.json 2> gpurun_out/full_parity_final.err
+tail -c 300 gpurun_out/full_parity_final.json
