@@ -1,4 +1,6 @@
-"""Round-1 join kernel time of a config stand-in (experiment helper)."""
+"""Join / apply kernel time of the first N rounds of a BASELINE config (device-resident inputs):
+    python tools/join_round_time.py c3 0.3 1   # config, scale, rounds
+KNNM_LIB selects another build of libknnm.so (ablation variants)."""
 import os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
