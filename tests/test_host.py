@@ -206,3 +206,26 @@ def test_parallel_sample_distinct_rows_matches_numpy(n, k, nrows, pre):
     got = sample_distinct_rows(b, n, k, rows)
     assert np.array_equal(got, want)
     assert a.bit_generator.state == b.bit_generator.state
+
+
+def test_from_arrays_flags_materialise_on_access():
+    """KnnGraph.from_arrays without flags: all False, created on first access
+    (reference layout, graph.py:96); explicit flags and assignment are kept."""
+    import paper_1908_00814_b200 as km
+
+    ids = np.arange(12, dtype=np.int32).reshape(4, 3)
+    dists = np.arange(12, dtype=np.float64).reshape(4, 3)
+    sizes = np.full(4, 3, dtype=np.int32)
+    g = km.KnnGraph.from_arrays(np.arange(4), 3, km.Metric.L2, ids, dists, sizes)
+    assert g._flags is None
+    assert g.flags.shape == (4, 3) and g.flags.dtype == np.bool_ and not g.flags.any()
+    assert g.flags is g.flags  # one array, not a fresh one per access
+    g.flags[1, 2] = True
+    assert g.flags[1, 2]
+    h = g.with_capacity(5)
+    assert h.flags.shape == (4, 5) and h.flags[1, 2] and h.flags.sum() == 1
+    f = np.ones((4, 3), dtype=np.bool_)
+    g2 = km.KnnGraph.from_arrays(np.arange(4), 3, km.Metric.L2, ids, dists, sizes, flags=f)
+    assert g2.flags is f
+    g2.flags = ~f
+    assert not g2.flags.any()
