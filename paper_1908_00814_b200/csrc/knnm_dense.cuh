@@ -21,19 +21,24 @@
 //   k_dense_rec   one warp per active hood gathers what the join needs per
 //                 member (nbh entry, round-start worst, first slot, cosine
 //                 norm and root) into a fixed-size record in HBM;
-//   k_join_dense  warp 0 (producer) bulk-copies the records into a ring of
-//                 DJ_NRR shared slots, orders the members by class, and
-//                 bulk-copies the member rows -- fp64 rows of the union
-//                 (fp32 -> fp64 is exact; B200 converts at 16 lanes/clk/SM
-//                 against 64 fp64 ops, so rows are converted once per merge,
-//                 not per hood) -- into a circular shared row buffer
+//   k_join_dense  warp 0 (loader) bulk-copies the records into a ring of
+//                 DJ_NRR shared slots and, as soon as a record is there, the
+//                 member rows -- fp64 rows of the union (fp32 -> fp64 is
+//                 exact; B200 converts at 16 lanes/clk/SM against 64 fp64
+//                 ops, so rows are converted once per merge, not per hood)
+//                 -- into a circular shared row buffer in nbh position order
 //                 (mbarrier tx-count completion, up to DJ_NH hoods in
-//                 flight); warps 1..15 (consumers) take 4 x 2-tile patches
-//                 of the oldest ready hood from a per-hood counter and
-//                 arrive on the hood's "empty" barrier when it has no
-//                 patches left, so a warp moves on to the next hood while
-//                 others finish the previous one; the producer reclaims
-//                 rows and record slots in hood order.
+//                 flight; rows no rectangle touches are skipped);
+//                 warp 1 (classifier) orders each hood's members by class
+//                 and builds the pair-rank table and the rectangles;
+//                 warps 2..15 (consumers) take 4 x 2-tile patches of the
+//                 oldest ready hood from a per-hood counter and arrive on
+//                 the hood's "empty" barrier when it has no patches left, so
+//                 a warp moves on to the next hood while others finish the
+//                 previous one; the loader reclaims rows and record slots in
+//                 hood order.  (Loading and classifying in one warp delivered
+//                 a hood every 4.7 us -- 38 of the 48 ms of config 4's first
+//                 round with the arithmetic removed.)
 // Shared rows have S = dp + 2 doubles (S / 2 odd: the rows a load touches
 // start in distinct 16-byte bank groups).  Members are ordered by class
 // (label, new first), so the admissible set of a hood is a union of at most
@@ -50,8 +55,8 @@
 
 namespace knnm {
 
-constexpr int DJ_THREADS = 512;  // warp 0: producer; warps 1..15: consumers
-constexpr int DJ_CONS = DJ_THREADS / 32 - 1;
+constexpr int DJ_THREADS = 512;  // warp 0: loader; warp 1: classifier; warps 2..15: consumers
+constexpr int DJ_CONS = DJ_THREADS / 32 - 2;
 constexpr int DJ_NH = 8;         // hoods in flight (descriptor / barrier ring)
 constexpr int DJ_NRR = 12;       // record slots (requested DJ_NRR - DJ_NH hoods ahead)
 constexpr size_t DJ_SMEM_CAP = 225 * 1024;
@@ -82,12 +87,12 @@ struct __align__(16) DjMeta {
     uint8_t sc[MAX_W];
     PosPrefix P;
     DjRect rect[4];
-    int nrect, npatch, width, next, base;  // base: first row in the circular buffer
+    int nrect, npatch, width, next;
 };
 
 __host__ inline size_t dj_fixed_bytes(int W, bool cos) {
     return (size_t)DJ_NRR * dj_rec_bytes(W, cos) + DJ_NH * sizeof(DjMeta) +
-           (2 * DJ_NH + DJ_NRR) * sizeof(uint64_t);
+           (3 * DJ_NH + DJ_NRR) * sizeof(uint64_t) + 2 * DJ_NH * sizeof(int);
 }
 // rows of the circular shared row buffer (0: a whole hood does not fit twice,
 // the route does not apply)
@@ -261,7 +266,10 @@ k_join_dense(int nactive, int W, int mode, const double *__restrict__ sub64, int
     DjMeta *M0 = reinterpret_cast<DjMeta *>(R0 + (size_t)DJ_NRR * RB);
     uint64_t *full = reinterpret_cast<uint64_t *>(M0 + DJ_NH);
     uint64_t *empty = full + DJ_NH;
-    uint64_t *recb = empty + DJ_NH;
+    uint64_t *metaf = empty + DJ_NH;
+    uint64_t *recb = metaf + DJ_NH;
+    int *s_base = reinterpret_cast<int *>(recb + DJ_NRR);  // first ring row of the hood in slot h
+    int *s_wid = s_base + DJ_NH;                           // its width (loader's release bookkeeping)
     __shared__ unsigned long long s_nev;
     const int tid = threadIdx.x;
     const unsigned lane = lane_id();
@@ -273,6 +281,7 @@ k_join_dense(int nactive, int W, int mode, const double *__restrict__ sub64, int
         for (int h = 0; h < DJ_NH; h++) {
             mbar_init(&full[h], 1);
             mbar_init(&empty[h], DJ_CONS);
+            mbar_init(&metaf[h], 1);
         }
         for (int r = 0; r < DJ_NRR; r++) mbar_init(&recb[r], 1);
         s_nev = 0;
@@ -280,11 +289,14 @@ k_join_dense(int nactive, int W, int mode, const double *__restrict__ sub64, int
     __syncthreads();
     unsigned long long nev = 0;
     if (warp == 0) {
-        // ------------------------------ producer ------------------------------
+        // ------------------------------- loader -------------------------------
         // Hoods are released by the consumers in order; rel counts the
-        // releases observed so far.  Hood j needs: descriptor slot j % NH
-        // (hood j - NH released), its record (requested when hood
-        // j - NRR was released), and w free rows in the circular buffer.
+        // releases observed so far.  Hood j needs: ring slot j % NH (hood
+        // j - NH released), its record (requested when hood j - NRR was
+        // released), and w free rows in the circular buffer.  Rows go in
+        // nbh position order, so the copies depend on the record alone (the
+        // class order is the classifier warp's business: one warp doing
+        // both delivered a hood every 4.7 us, 80% of the kernel's time).
         auto rec_req = [&](int j) {  // lane 0
             uint64_t *bar = &recb[j % DJ_NRR];
             mbar_expect_tx(bar, (uint32_t)RB);
@@ -297,10 +309,11 @@ k_join_dense(int nactive, int W, int mode, const double *__restrict__ sub64, int
         int64_t head = 0, tail = 0;  // rows allocated / released (monotonic)
         auto release_one = [&]() {
             mbar_wait(&empty[rel % DJ_NH], (uint32_t)(rel / DJ_NH) & 1u);
-            tail += M0[rel % DJ_NH].width;
+            tail += s_wid[rel % DJ_NH];
             if (lane == 0 && rel + DJ_NRR < J) rec_req(rel + DJ_NRR);  // its record slot is free
             rel++;
         };
+        const uint32_t row_bytes = (uint32_t)dp * 8u;
         for (int j = 0; j < J; j++) {
             while (rel < j - DJ_NH + 1) release_one();
             const int r = j % DJ_NRR, h = j % DJ_NH;
@@ -308,39 +321,59 @@ k_join_dense(int nactive, int W, int mode, const double *__restrict__ sub64, int
             const uint8_t *R = R0 + (size_t)r * RB;
             const int w = *reinterpret_cast<const int *>(R);
             while (head + w - tail > C) release_one();
-            DjMeta &M = M0[h];
-            int cn[4];
-            dj_classify(M, R, mode, lane, cn);
-            if (lane == 0) M.base = (int)(head % C);
-            __syncwarp();
             const uint32_t *E = reinterpret_cast<const uint32_t *>(R + 16);
-            fence_proxy_async();
-            const uint32_t row_bytes = (uint32_t)dp * 8u;
-            // Rows no rectangle touches are not fetched (their slots in the
-            // ring stay stale): with A = label 0, B = label 1, old A members
-            // pair only with new B members and old B members only with new
-            // A members (modes 1, 2; mode 2's B x B block needs a new B
-            // member) -- in late rounds, with a new member or two per hood,
-            // about half of a hood's rows.
-            const int nAn = cn[0], nA = cn[0] + cn[1], nBn = cn[2];
-            const bool needAo = mode == 0 || nBn > 0;
-            const bool needBo = mode == 0 || nAn > 0 || (mode == 2 && nBn > 0);
-            const int nfetch = nAn + (needAo ? nA - nAn : 0) + nBn + (needBo ? w - nA - nBn : 0);
-            if (lane == 0) mbar_expect_tx(&full[h], row_bytes * (uint32_t)nfetch);
+            // Rows no rectangle touches are not fetched (their ring rows stay
+            // stale): with A = label 0, B = label 1, old A members pair only
+            // with new B members and old B members only with new A members
+            // (modes 1, 2; mode 2's B x B block needs a new B member).
+            uint32_t ev[4];
+            int cls[4], cn[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                const int p = b * 32 + (int)lane;
+                ev[b] = p < w ? E[p] : 0u;
+                const int lab = mode == 0 ? 0 : (int)((ev[b] >> 1) & 1);
+                cls[b] = p < w ? lab * 2 + ((ev[b] & 1) ? 0 : 1) : 4;
+#pragma unroll
+                for (int c = 0; c < 4; c++) cn[c] += __popc(__ballot_sync(FULL_MASK, cls[b] == c));
+            }
+            const bool needAo = mode == 0 || cn[2] > 0;
+            const bool needBo = mode == 0 || cn[0] > 0 || (mode == 2 && cn[2] > 0);
+            const int nfetch = cn[0] + (needAo ? cn[1] : 0) + cn[2] + (needBo ? cn[3] : 0);
+            fence_proxy_async();  // the consumers' reads of the recycled rows vs. the bulk copies
+            if (lane == 0) {
+                s_base[h] = (int)(head % C);
+                s_wid[h] = w;
+                mbar_expect_tx(&full[h], row_bytes * (uint32_t)nfetch);
+            }
             __syncwarp();
-            for (int sl = (int)lane; sl < w; sl += 32) {
-                const bool need = sl < nAn || (sl < nA ? needAo : (sl < nA + nBn || needBo));
+#pragma unroll
+            for (int b = 0; b < 4; b++) {
+                const int p = b * 32 + (int)lane;
+                const bool need = cls[b] == 0 || cls[b] == 2 || (cls[b] == 1 && needAo) || (cls[b] == 3 && needBo);
                 if (need)
-                    bulk_g2s(F0 + (size_t)((head + sl) % C) * S, sub64 + (int64_t)(E[M.pos[sl]] >> 2) * dp,
-                             row_bytes, &full[h]);
+                    bulk_g2s(F0 + (size_t)((head + p) % C) * S, sub64 + (int64_t)(ev[b] >> 2) * dp, row_bytes,
+                             &full[h]);
             }
             head += w;
+        }
+    } else if (warp == 1) {
+        // ----------------------------- classifier ----------------------------
+        for (int j = 0; j < J; j++) {
+            const int r = j % DJ_NRR, h = j % DJ_NH;
+            if (j >= DJ_NH) mbar_wait(&empty[h], (uint32_t)((j - DJ_NH) / DJ_NH) & 1u);  // slot free
+            mbar_wait(&recb[r], (uint32_t)(j / DJ_NRR) & 1u);
+            int cn[4];
+            dj_classify(M0[h], R0 + (size_t)r * RB, mode, lane, cn);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&metaf[h]);
         }
     } else {
         // ------------------------------ consumers -----------------------------
         const double2 *dv2 = reinterpret_cast<const double2 *>(F0);
         for (int j = 0; j < J; j++) {
             const int r = j % DJ_NRR, h = j % DJ_NH;
+            mbar_wait(&metaf[h], (uint32_t)(j / DJ_NH) & 1u);
             mbar_wait(&full[h], (uint32_t)(j / DJ_NH) & 1u);
             DjMeta &M = M0[h];
             const uint8_t *R = R0 + (size_t)r * RB;
@@ -349,7 +382,7 @@ k_join_dense(int nactive, int W, int mode, const double *__restrict__ sub64, int
             const uint64_t *ST = reinterpret_cast<const uint64_t *>(R + 16 + 12 * Wr);
             const double *N64 = reinterpret_cast<const double *>(R + 16 + 20 * Wr);
             const double *SQ = reinterpret_cast<const double *>(R + 16 + 28 * Wr);
-            const int base = M.base;
+            const int base = s_base[h];
             const int npatch = M.npatch, nrect = M.nrect;
             while (true) {
                 int pid = 0;
@@ -368,13 +401,13 @@ k_join_dense(int nactive, int W, int mode, const double *__restrict__ sub64, int
                 const int j0 = C0 + (Rc.lay ? (int)(lane & 7) : (int)(lane & 3));
                 const double2 *pa[4], *pb[2];
 #pragma unroll
-                for (int m = 0; m < 4; m++) {
-                    int row = base + min(i0 + m * rs, Rc.r1 - 1);
+                for (int m = 0; m < 4; m++) {  // ring rows are in nbh position order
+                    int row = base + (int)M.pos[min(i0 + m * rs, Rc.r1 - 1)];
                     pa[m] = dv2 + (size_t)(row >= C ? row - C : row) * S2;
                 }
 #pragma unroll
                 for (int n = 0; n < 2; n++) {
-                    int row = base + min(j0 + n * cs, Rc.c1 - 1);
+                    int row = base + (int)M.pos[min(j0 + n * cs, Rc.c1 - 1)];
                     pb[n] = dv2 + (size_t)(row >= C ? row - C : row) * S2;
                 }
                 double acc[4][2];
