@@ -2062,7 +2062,12 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                     float acc[4] = {0.f, 0.f, 0.f, 0.f};
                     int iacc[4] = {0, 0, 0, 0};
                     const uint32_t a_addr = rbase + (uint32_t)((m0 + (lane & 15)) * rs + (lane >> 4) * 16);
-                    const uint32_t b_addr = rbase + (uint32_t)((n0 + (lane & 7)) * rs + ((lane >> 3) & 1) * 16);
+                    // tile column j holds member n0 + (j >> 1) + 4 (j & 1): a lane's two
+                    // columns are members n0 + t4 and n0 + t4 + 4, so the four lanes of a
+                    // row store to consecutive slots (one or two 32-byte sectors per
+                    // store instruction and row instead of two or three)
+                    const uint32_t b_addr = rbase + (uint32_t)((n0 + ((lane & 7) >> 1) + 4 * (lane & 1)) * rs +
+                                                               ((lane >> 3) & 1) * 16);
                     // 32 bytes of K per step: 16 fp16 or 32 u8 elements; the
                     // ldmatrix byte layout is the same for both
 #pragma unroll 4
@@ -2075,7 +2080,7 @@ k_join_mma(const int32_t *__restrict__ active, int nactive, const uint32_t *__re
                         else
                             mma16816(acc, a0, a1, a2, a3, b0, b1);
                     }
-                    const int ja = n0 + 2 * t4, jb = ja + 1;
+                    const int ja = n0 + t4, jb = ja + 4;
                     const MjRec ca = lds_rec(rec + (ja < cc1 ? ja : cc0));
                     const MjRec cb = lds_rec(rec + (jb < cc1 ? jb : cc0));
 #pragma unroll
