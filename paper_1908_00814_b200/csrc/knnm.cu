@@ -501,6 +501,20 @@ LazyExact lazy_of(knnm_ctx *c) {
     // k_join_tc stores rigorous lower bounds of the reference value itself
     z.lo_rel = c->tcj_round ? 1.0 : 1.0 - (double)(c->d + 8) * ldexp(1.0, -23);
     z.lo_abs = (double)(4 * c->d + 64) * ldexp(1.0, -24);
+    if (c->metric == KNNM_COSINE) {
+        z.hi_rel = 1.0;
+        z.hi_abs = z.lo_abs;
+    } else if (c->tcj_round) {
+        // k_join_tc: bound - exact <= 2 (dropped limb products + truncation);
+        // entries <= 2^24 / scale, so sum x <= d 2^24 / scale
+        const double sc = 1.0 / c->tcj_scale;
+        z.hi_rel = 1.0 + (double)(c->d + 16) * ldexp(1.0, -50);
+        z.hi_abs = 2.0 * ((double)c->d * TJC_GMAX_TAIL * sc * sc + 2.0 * sc * (double)c->d * ldexp(1.0, 24) * sc +
+                          (double)c->d * sc * sc);
+    } else {
+        z.hi_rel = 1.0 / (1.0 - (double)(c->d + 8) * ldexp(1.0, -23));
+        z.hi_abs = 0.0;
+    }
     return z;
 }
 

@@ -363,6 +363,10 @@ struct LazyExact {
     const double *nrm64;  // exact fp64 squared norms per row (cosine only)
     int dp, d, tag;
     double lo_rel, lo_abs;
+    // estimate of the exact value from above, f * hi_rel + hi_abs: only
+    // steers the speculation of lazy_chunk_eval (a slot it leaves out is
+    // evaluated on demand), so it need not be rigorous
+    double hi_rel, hi_abs;
 };
 
 __device__ __forceinline__ bool slot_is_approx(double v) { return __double_as_longlong(v) < 0; }
@@ -371,6 +375,7 @@ __device__ __forceinline__ double slot_lower(double v, const LazyExact z) {
     const double f = -v;
     return z.tag == 2 ? f - z.lo_abs : f * z.lo_rel;
 }
+__device__ __forceinline__ double slot_upper(double v, const LazyExact z) { return -v * z.hi_rel + z.hi_abs; }
 
 // Resolve the lane's slot for row r: returns the distance to apply (+inf when
 // the slot cannot pass the row's current state).  need = approximate slot
@@ -414,7 +419,8 @@ __device__ __forceinline__ double lazy_resolve(const WarpRow<E> &s, int k, bool 
 // unchanged (they are still taken on exact values at each slot's turn); a
 // speculative value that is never asked for is wasted work only.
 // ---------------------------------------------------------------------------
-constexpr int LZB_AHEAD = 16;  // chunks of look-ahead per batch (default of LazyExact::ahead)
+constexpr int LZB_AHEAD = 32;  // chunks of look-ahead per batch (default of LazyExact::ahead; with the
+                               // simulated-worst filter 16 / 24 / 32 / 48 measure 276 / 272 / 273 / 270 ms at config 3)
 
 struct __align__(16) LazyBatchSmem {
     // y[buf][j * 32 + 4 * (g ^ (j & 7)) + e]: dimension t0 + 4 g + e of pair
@@ -527,6 +533,27 @@ __device__ __forceinline__ void lazy_chunk_eval(const WarpRow<E> &s, int k, cons
     }
     if (!miss) return;
     // a new batch: this chunk's misses, then look-ahead candidates in order
+    const double inf = __longlong_as_double(0x7ff0000000000000LL);
+    // Simulated worst: lane t (t < k, row full) counts the batch's candidates
+    // whose upper estimate lies below its entry d[t]; once k - t of them do,
+    // the row's worst will have dropped to d[t] or below by the time the
+    // later slots get their turn, so look-ahead slots whose lower bound is
+    // not below that are left out of the batch (most would have been
+    // evaluated for nothing: 257 M evaluations for 179 M needed at config 3).
+    const bool sim = E == 1 && s.sz == k;
+    int simcnt = 0;
+    double wsim = s.worst;
+    auto sim_add = [&](unsigned cm, double ub) {  // cm: lanes holding a candidate, ub: its estimate
+        if (!sim) return;
+        while (cm) {
+            const int i = __ffs(cm) - 1;
+            cm &= cm - 1;
+            const double u = __shfl_sync(FULL_MASK, ub, i);
+            simcnt += u < s.d[0] ? 1 : 0;
+        }
+        const unsigned ok = __ballot_sync(FULL_MASK, (int)lane < k && simcnt >= k - (int)lane);
+        if (ok) wsim = __shfl_sync(FULL_MASK, s.d[0], __ffs(ok) - 1);
+    };
     int P = 0;
     {
         const bool mine = (miss >> lane) & 1u;
@@ -538,8 +565,8 @@ __device__ __forceinline__ void lazy_chunk_eval(const WarpRow<E> &s, int k, cons
             b.spos[at] = mypos;
         }
         P = __popc(mm);
+        if (sim) sim_add(mm, mine ? slot_upper(Bd[seg + mypos], z) : inf);
     }
-    const double inf = __longlong_as_double(0x7ff0000000000000LL);
 #pragma unroll 1
     for (int a = 1; a <= z.ahead; a++) {
         const int64_t cc = c0 + 32 * a;
@@ -549,13 +576,14 @@ __device__ __forceinline__ void lazy_chunk_eval(const WarpRow<E> &s, int k, cons
         const double v = in ? Bd[seg + j] : inf;
         const bool apx = in && slot_is_approx(v);
         const double lb = apx ? slot_lower(v, z) : inf;
-        bool cand = apx && (lb < s.worst || (s.sz < k && lb < inf));
+        bool cand = apx && (lb < wsim || (s.sz < k && lb < inf));
         const int sv = cand ? Bs[seg + j] : 0;
         if (__any_sync(FULL_MASK, cand)) {
             const bool listed = row_lists<E>(s, sv);
             cand = cand && !listed;
         }
         const unsigned cm = __ballot_sync(FULL_MASK, cand);
+        if (cm) sim_add(cm, cand ? slot_upper(v, z) : inf);
         const int at = P + __popc(cm & lanemask_lt());
         if (cand && at < 32) {
             KNNM_CHECK(sv >= 0 && sv < z.nrows);
