@@ -544,15 +544,17 @@ __device__ __forceinline__ void lazy_chunk_eval(const WarpRow<E> &s, int k, cons
     int simcnt = 0;
     double wsim = s.worst;
     auto sim_add = [&](unsigned cm, double ub) {  // cm: lanes holding a candidate, ub: its estimate
-        if (!sim) return;
-        while (cm) {
-            const int i = __ffs(cm) - 1;
-            cm &= cm - 1;
-            const double u = __shfl_sync(FULL_MASK, ub, i);
-            simcnt += u < s.d[0] ? 1 : 0;
+        if constexpr (E == 1) {  // (rows of one entry per lane)
+            if (!sim) return;
+            while (cm) {
+                const int i = __ffs(cm) - 1;
+                cm &= cm - 1;
+                const double u = __shfl_sync(FULL_MASK, ub, i);
+                simcnt += u < s.d[0] ? 1 : 0;
+            }
+            const unsigned ok = __ballot_sync(FULL_MASK, (int)lane < k && simcnt >= k - (int)lane);
+            if (ok) wsim = __shfl_sync(FULL_MASK, s.d[0], __ffs(ok) - 1);
         }
-        const unsigned ok = __ballot_sync(FULL_MASK, (int)lane < k && simcnt >= k - (int)lane);
-        if (ok) wsim = __shfl_sync(FULL_MASK, s.d[0], __ffs(ok) - 1);
     };
     int P = 0;
     {
