@@ -365,14 +365,21 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
 
     if (role == 0) {
         if (elect_one()) {
+            // The issuing thread is one instruction stream: everything it can
+            // keep as a running counter (hood, K item, stage and accumulator
+            // set with their barrier parities, the instruction descriptors) it
+            // does -- a skeleton of this kernel without MMAs, copies and
+            // epilogue took 5.4 of the kernel's 13.5 ms, all of it this
+            // thread's index arithmetic (runtime divisions per item).
+            const uint32_t i3 = tjc_idesc(3 * npw), i2 = tjc_idesc(2 * npw), i1 = tjc_idesc(npw);
+            int h = 0, kq = 0, st = 0, hs = 0;      // hood, item of the hood, stage, accumulator set
+            uint32_t fph = 0, aph = 0;              // parities of full[st] and of acce[hs]'s previous use
             for (int t = 0; t < T; t++) {
-                const int h = t / nki, kq = t - h * nki;
-                const int st = t % stages;
                 if (kq == 0) {
                     mbar_wait(&s_metaf[h % TJC_R], (uint32_t)(h / TJC_R) & 1u);
-                    if (h >= NS) mbar_wait(&s_acce[h % NS], (uint32_t)((h - NS) / NS) & 1u);
+                    if (h >= NS) mbar_wait(&s_acce[hs], aph ^ 1u);
                 }
-                mbar_wait(&s_full[st], (uint32_t)(t / stages) & 1u);
+                mbar_wait(&s_full[st], fph);
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 tc_fence_after();
                 const uint32_t sb = sbase + (uint32_t)st * sstride;
@@ -381,8 +388,7 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
                 // all three (G0, G1, G2 partial), N = 2 npw takes L1 against
                 // [L0 | L1] (G1, G2) and N = npw takes L2 against L0 (G2):
                 // three instructions per K step instead of six, same products.
-                const uint32_t i3 = tjc_idesc(3 * npw), i2 = tjc_idesc(2 * npw), i1 = tjc_idesc(npw);
-                const uint32_t acc = tmem + (uint32_t)((h % NS) * 3 * npw);
+                const uint32_t acc = tmem + (uint32_t)(hs * 3 * npw);
                 const uint32_t d0 = acc, d1 = acc + (uint32_t)npw, d2 = acc + 2u * (uint32_t)npw;
                 // Same-shape MMAs back to back: the three products write
                 // overlapping accumulator columns with different N, and the
@@ -406,7 +412,19 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
                     }
                 }
                 tc_commit(&s_empty[st]);
-                if (kq == nki - 1) tc_commit(&s_accf[h % NS]);
+                if (++st == stages) {
+                    st = 0;
+                    fph ^= 1u;
+                }
+                if (++kq == nki) {  // the hood's last item: its accumulators are complete
+                    tc_commit(&s_accf[hs]);
+                    kq = 0;
+                    h++;
+                    if (++hs == NS) {
+                        hs = 0;
+                        aph ^= 1u;
+                    }
+                }
             }
         }
         __syncwarp();
@@ -445,10 +463,10 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
         const int c = lt & (8 * TJC_KI - 1), r0 = lt / (8 * TJC_KI);
         constexpr int rstep = TJC_LOADERS / (8 * TJC_KI);
         const int j = c >> 3, c16 = c & 7;
+        int h = 0, kq = 0, st = 0;  // running counters instead of divisions per item
+        uint32_t eph = 1;           // parity of empty[st]'s previous use (first pass: nothing to wait for)
         for (int t = 0; t < T; t++) {
-            const int h = t / nki, kq = t - h * nki;
-            const int st = t % stages;
-            if (t >= stages) mbar_wait(&s_empty[st], (uint32_t)(t / stages - 1) & 1u);
+            if (t >= stages) mbar_wait(&s_empty[st], eph);
             if (kq == 0) mbar_wait(&s_metaf[h % TJC_R], (uint32_t)(h / TJC_R) & 1u);
             const TjcMeta &m = meta[h % TJC_R];
             const int w = m.width;
@@ -466,6 +484,14 @@ k_join_tc(const int32_t *__restrict__ active, int nactive, const uint32_t *__res
                 }
             }
             cp_async_arrive(&s_full[st]);
+            if (++st == stages) {
+                st = 0;
+                eph ^= 1u;
+            }
+            if (++kq == nki) {
+                kq = 0;
+                h++;
+            }
         }
     } else {
         for (int h = 0; h < nh; h++) {
